@@ -1,0 +1,212 @@
+/*
+ * mmb200.h -- C ABI of libmmb200.so, the B200-native engine for MAMMOTH's
+ * modular-training hot path (arXiv 2403.07544, Algorithm 1).
+ *
+ * Plain C: pointers, sizes and opaque handles only.  Device pointers come
+ * from the caller (PyTorch owns device memory and streams); `stream` is a
+ * cudaStream_t passed as void*.  Every call returns 0 on success and a
+ * negative code on failure (-1 argument, -2 CUDA, -3 NCCL, -4 unsupported);
+ * mm_last_error() returns the message of the calling thread's last failure.
+ *
+ * Reference interfaces each entry point replaces are cited per declaration
+ * (paths relative to the reference tree, pkg/src/mmtplan/...).
+ */
+#ifndef MMB200_H
+#define MMB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MMB200_ABI_VERSION 4
+#define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
+
+int mm_abi_version(void);
+const char* mm_last_error(void);
+/* SM count and compute capability (major*10+minor) of the current device. */
+int mm_device_info(int* sm_count, int* cc);
+
+/* ---------------------------------------------------------------------------
+ * K9: allocator communication cost.  Same arguments, loop order and float64
+ * accumulation as comm_cost_kernel (_speedups.pyx:11-57, twin _cost_py.py:11-48),
+ * called by CostContext.cost (allocator.py:101-111).  Host code.
+ */
+int mm_comm_cost(const double* params, int64_t n_modules, const int64_t* mod_task_off,
+                 const int64_t* mod_task_idx, const int64_t* task_dev,
+                 const int64_t* dev_node, int64_t n_devices, double w_intra, double w_inter,
+                 double* out_per_module, double* total);
+
+/* ---------------------------------------------------------------------------
+ * Algorithm 1 over emulated devices that share one GPU: the literal
+ * sync_step(devices) of syncsim.py:121-153.  For every module: n = popcount
+ * (used_mask); n == 0 -> buffers untouched, `out` zero-filled; otherwise
+ * total = sum of member buffers in ascending member order (fp32), total /= n,
+ * installed into every member buffer (and `out` if non-NULL).
+ * only_ready != 0 sums only members whose used bit is set (exact when unused
+ * buffers are zero, which DeviceState.reset guarantees, syncsim.py:108-111).
+ */
+typedef struct {
+    float* bufs[MM_MAX_GROUP]; /* member buffers, ascending device index */
+    float* out;                /* optional synced copy, may be NULL */
+    int64_t n_elems;
+    int32_t group_size;
+    uint32_t used_mask; /* bit r: member r used the module this step */
+} mm_sync_module;
+
+int mm_sync_emulated(const mm_sync_module* mods, int n_mods, int only_ready, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * K3: fused masked rescale + loss unscale + Adam + bf16 parameter cast on a
+ * flat per-module bucket.  g = grad / n * inv_loss_scale (the "/ n_j" of
+ * Algorithm 1, syncsim.py:149); modules with n == 0 are skipped
+ * entirely (no optimizer step).  n is read from ready_dev[ready_index]
+ * when ready_dev != NULL and ready_index >= 0, else from n_ready.
+ * Adam follows torch.optim.Adam's update form (bias corrections folded into
+ * step_size = lr / (1 - beta1^t) and inv_sqrt_bc2 = 1 / sqrt(1 - beta2^t)).
+ */
+typedef struct {
+    const float* grad;
+    float* master;
+    float* exp_avg;
+    float* exp_avg_sq;
+    uint16_t* param_bf16; /* may be NULL */
+    int64_t n_elems;
+    int32_t n_ready;
+    int32_t ready_index;
+    float step_size;
+    float inv_sqrt_bc2;
+} mm_adam_module;
+
+typedef struct {
+    float beta1, beta2, eps, weight_decay, inv_loss_scale;
+    float one_minus_beta1, one_minus_beta2; /* computed in double on the host */
+} mm_adam_hyper;
+
+int mm_fused_update(const mm_adam_module* mods, int n_mods, const mm_adam_hyper* hyper,
+                    const int32_t* ready_dev, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * K1/K2: module-group communicators over NCCL (NVLink 5 / NVSwitch).
+ * Replaces the in-process loops of sync_step (syncsim.py:140-152) and the
+ * group map of run_benchmark (syncsim.py:337-340).
+ */
+int mm_nccl_unique_id(char out[128]);
+/* World communicator for `rank` of `world` on CUDA device `device`. */
+int mm_comm_init(int rank, int world, const char uid[128], int device, void** ctx);
+int mm_comm_destroy(void* ctx);
+/* Collective over the world communicator: every rank calls it with the same
+ * member list (ascending ranks) in the same order.  *grp = NULL for
+ * non-members and for singleton groups (they never communicate). */
+int mm_group_create(void* ctx, const int* ranks, int n, void** grp);
+int mm_group_destroy(void* grp);
+/* Ready-count exchange: n_dev[m] = sum over ranks of flags_dev[m] (int32).
+ * Non-hosting ranks contribute 0, so the world sum is the group sum. */
+int mm_ready_count(void* ctx, const int32_t* flags_dev, int32_t* n_dev, int n_modules,
+                   void* stream);
+
+typedef struct {
+    void* group;     /* from mm_group_create; NULL items are skipped */
+    void* buf;       /* in-place sum */
+    int64_t n_elems;
+    int32_t dtype;   /* 0 = fp32, 1 = bf16 */
+    int32_t pad;
+} mm_reduce_item;
+
+/* Sum-allreduce of every item on its group communicator, issued in array order
+ * (callers pass sorted ModuleKey order) inside one ncclGroupStart/End. */
+int mm_reduce_modules(void* ctx, const mm_reduce_item* items, int n, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * K4: bf16 GEMM on tcgen05 tensor cores (TMA-staged operands, fp32 TMEM
+ * accumulator).  D[M,N] = A[M,K] * B[N,K]^T with per-operand major-ness:
+ *   a_kmajor: A stored [M,K] row-major (lda = row stride) else [K,M];
+ *   b_kmajor: B stored [N,K] row-major else [K,N].
+ * Epilogues: see MM_EPI_*.  Replaces the toy W @ h of forward / local_backward
+ * (syncsim.py:55-87) with the transformer contractions.
+ */
+enum {
+    MM_EPI_BF16 = 0,        /* D_bf16 = acc (+bias) */
+    MM_EPI_BF16_RELU = 1,   /* D_bf16 = relu(acc + bias) */
+    MM_EPI_F32 = 2,         /* D_f32 = acc (+bias) */
+    MM_EPI_F32_ACCUM = 3,   /* D_f32 += acc */
+    MM_EPI_F32_RESID = 4,   /* D_f32 = resid_f32 + acc + bias (resid may alias D) */
+    MM_EPI_BF16_DRELU = 5   /* D_bf16 = acc * (aux_bf16 > 0) */
+};
+
+typedef struct {
+    const void* a;      /* bf16 */
+    const void* b;      /* bf16 */
+    void* d;            /* bf16 or fp32 per epilogue */
+    const float* bias;  /* [N] or NULL */
+    const float* resid; /* MM_EPI_F32_RESID */
+    const void* aux;    /* MM_EPI_BF16_DRELU mask source, bf16 [M, ldd] */
+    int64_t m, n, k;
+    int64_t lda, ldb, ldd; /* row strides in elements */
+    int32_t a_kmajor, b_kmajor;
+    int32_t epilogue;
+    int32_t pad;
+} mm_gemm_args;
+
+int mm_gemm(const mm_gemm_args* args, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * K6: LayerNorm over rows of x (fp32 residual stream) -> bf16, saving
+ * per-row mean / rstd; backward accumulates into dx (fp32) and writes its
+ * bf16 copy, and accumulates dgamma / dbeta (fp32).
+ */
+int mm_layernorm_fwd(const float* x, const float* gamma, const float* beta, uint16_t* y,
+                     float* mean, float* rstd, int64_t rows, int cols, float eps, void* stream);
+int mm_layernorm_bwd(const float* dy, const float* x, const float* gamma, const float* mean,
+                     const float* rstd, float* dx, uint16_t* dx_bf16, float* dgamma,
+                     float* dbeta, int64_t rows, int cols, void* stream);
+
+/* K8: embedding gather with scale + sinusoidal position, and its scatter-add. */
+int mm_embed_fwd(const int32_t* ids, const int32_t* pos, const uint16_t* table, float* out,
+                 int64_t rows, int cols, float scale, void* stream);
+int mm_embed_bwd(const int32_t* ids, const float* dout, float* dtable, int64_t rows, int cols,
+                 float scale, void* stream);
+
+/* K5: packed varlen multi-head attention (bf16 in/out, fp32 softmax). */
+typedef struct {
+    const uint16_t* q; const uint16_t* k; const uint16_t* v; /* [tokens, ld*] */
+    uint16_t* o;                                              /* [tq, ldo] */
+    float* lse;                                               /* [heads, tq] */
+    const uint16_t* d_o;                                      /* backward */
+    uint16_t* dq; uint16_t* dk; uint16_t* dv;                 /* backward */
+    const int32_t* cu_q; const int32_t* cu_k;                 /* [n_seq+1] */
+    int64_t ldq, ldk, ldv, ldo, ld_dq, ld_dk, ld_dv;
+    int32_t n_seq, heads, head_dim, causal;
+    int32_t max_q, max_k;
+    float scale;
+    int32_t total_q;
+} mm_attn_args;
+
+int mm_attention_fwd(const mm_attn_args* a, void* stream);
+int mm_attention_bwd(const mm_attn_args* a, void* stream);
+
+/* K7: softmax cross-entropy over bf16 logits; writes dlogits (bf16, in place
+ * allowed) scaled by grad_scale, per-row loss (fp32) and, if loss_sum is not
+ * NULL, adds every row's loss times grad_scale to *loss_sum (the token mean
+ * for grad_scale = 1/rows).  Labels < 0 are padding.
+ * Replaces loss() of the toy model (syncsim.py:67-69). */
+int mm_xent_fwd_bwd(const uint16_t* logits, const int32_t* labels, uint16_t* dlogits,
+                    float* row_loss, float* loss_sum, int64_t rows, int vocab, float grad_scale,
+                    void* stream);
+
+/* helpers */
+/* out[c] += sum over rows of x[r, c] (bf16 in, fp32 accumulate) */
+int mm_colsum_bf16(const uint16_t* x, float* out, int64_t rows, int cols, void* stream);
+int mm_cast_f32_bf16(const float* x, uint16_t* y, int64_t n, void* stream);
+int mm_flush_l2(void* scratch, size_t bytes, void* stream);
+/* y += alpha * x (fp32): DeviceState.accumulate (syncsim.py:113-118) */
+int mm_axpy_f32(float* y, const float* x, float alpha, int64_t n, void* stream);
+/* stream-ordered byte fill (DeviceState.reset of the grad buckets, syncsim.py:108-111) */
+int mm_memset(void* ptr, int value, size_t bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MMB200_H */

@@ -1,0 +1,163 @@
+"""ctypes binding of the C-ABI library ``libmmb200.so`` (declared in
+``include/mmb200.h``).
+
+There is no fallback: if the library is missing the import of any product
+module that needs it raises ``NativeLibraryError``.  Every entry point returns
+an ``int`` status (0 = OK, negative = CUDA/NCCL/argument error) and the
+message of the last failure is available from ``mm_last_error``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_int64, c_size_t, c_uint32, c_void_p
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "csrc", "libmmb200.so")
+
+#: must match MMB200_ABI_VERSION in include/mmb200.h
+ABI_VERSION = 4
+MAX_GROUP = 8
+
+
+class NativeLibraryError(RuntimeError):
+    pass
+
+
+class MMError(RuntimeError):
+    """A C-ABI call returned a non-zero status."""
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeLibraryError(
+                f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        handle = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+        _declare(handle)
+        got = handle.mm_abi_version()
+        if got != ABI_VERSION:
+            raise NativeLibraryError(f"libmmb200 ABI {got} != expected {ABI_VERSION}; rebuild")
+        _lib = handle
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    if status != 0:
+        msg = lib().mm_last_error().decode(errors="replace")
+        raise MMError(f"{what} failed ({status}): {msg}")
+
+
+# ----------------------------------------------------------------------------
+# descriptor structs (layouts mirror include/mmb200.h)
+
+
+class SyncModule(ctypes.Structure):
+    _fields_ = [
+        ("bufs", c_void_p * MAX_GROUP),
+        ("out", c_void_p),
+        ("n_elems", c_int64),
+        ("group_size", c_int32),
+        ("used_mask", c_uint32),
+    ]
+
+
+class AdamModule(ctypes.Structure):
+    _fields_ = [
+        ("grad", c_void_p),
+        ("master", c_void_p),
+        ("exp_avg", c_void_p),
+        ("exp_avg_sq", c_void_p),
+        ("param_bf16", c_void_p),
+        ("n_elems", c_int64),
+        ("n_ready", c_int32),
+        ("ready_index", c_int32),
+        ("step_size", c_float),
+        ("inv_sqrt_bc2", c_float),
+    ]
+
+
+class AdamHyper(ctypes.Structure):
+    _fields_ = [
+        ("beta1", c_float),
+        ("beta2", c_float),
+        ("eps", c_float),
+        ("weight_decay", c_float),
+        ("inv_loss_scale", c_float),
+        ("one_minus_beta1", c_float),
+        ("one_minus_beta2", c_float),
+    ]
+
+    @classmethod
+    def make(cls, beta1, beta2, eps, weight_decay=0.0, inv_loss_scale=1.0):
+        return cls(beta1=beta1, beta2=beta2, eps=eps, weight_decay=weight_decay,
+                   inv_loss_scale=inv_loss_scale, one_minus_beta1=1.0 - beta1,
+                   one_minus_beta2=1.0 - beta2)
+
+
+class ReduceItem(ctypes.Structure):
+    _fields_ = [
+        ("group", c_void_p),
+        ("buf", c_void_p),
+        ("n_elems", c_int64),
+        ("dtype", c_int32),
+        ("pad", c_int32),
+    ]
+
+
+def _declare(h: ctypes.CDLL) -> None:
+    def sig(name, res, *args):
+        fn = getattr(h, name)
+        fn.restype = res
+        fn.argtypes = list(args)
+
+    sig("mm_abi_version", c_int)
+    sig("mm_last_error", c_char_p)
+    sig("mm_device_info", c_int, POINTER(c_int), POINTER(c_int))
+    # K9 -- comm cost (replaces _speedups.pyx:11-57)
+    sig("mm_comm_cost", c_int, POINTER(c_double), c_int64, POINTER(c_int64), POINTER(c_int64),
+        POINTER(c_int64), POINTER(c_int64), c_int64, c_double, c_double, POINTER(c_double),
+        POINTER(c_double))
+    # Algorithm-1 sync, emulated devices on one GPU (sync_step syncsim.py:121-153)
+    sig("mm_sync_emulated", c_int, POINTER(SyncModule), c_int, c_int, c_void_p)
+    # K3 fused rescale + unscale + Adam + bf16 cast
+    sig("mm_fused_update", c_int, POINTER(AdamModule), c_int, POINTER(AdamHyper), c_void_p, c_void_p)
+    # NCCL plumbing (K1/K2)
+    sig("mm_nccl_unique_id", c_int, ctypes.c_char_p)
+    sig("mm_comm_init", c_int, c_int, c_int, ctypes.c_char_p, c_int, POINTER(c_void_p))
+    sig("mm_comm_destroy", c_int, c_void_p)
+    sig("mm_group_create", c_int, c_void_p, POINTER(c_int), c_int, POINTER(c_void_p))
+    sig("mm_group_destroy", c_int, c_void_p)
+    sig("mm_ready_count", c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p)
+    sig("mm_reduce_modules", c_int, c_void_p, POINTER(ReduceItem), c_int, c_void_p)
+    # layer kernels (K4-K8)
+    sig("mm_gemm", c_int, c_void_p, c_void_p)
+    sig("mm_layernorm_fwd", c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+        c_int64, c_int, c_float, c_void_p)
+    sig("mm_layernorm_bwd", c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+        c_void_p, c_void_p, c_void_p, c_int64, c_int, c_void_p)
+    sig("mm_embed_fwd", c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int, c_float,
+        c_void_p)
+    sig("mm_embed_bwd", c_int, c_void_p, c_void_p, c_void_p, c_int64, c_int, c_float, c_void_p)
+    sig("mm_attention_fwd", c_int, c_void_p, c_void_p)
+    sig("mm_attention_bwd", c_int, c_void_p, c_void_p)
+    sig("mm_xent_fwd_bwd", c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
+        c_int, c_float, c_void_p)
+    sig("mm_colsum_bf16", c_int, c_void_p, c_void_p, c_int64, c_int, c_void_p)
+    sig("mm_cast_f32_bf16", c_int, c_void_p, c_void_p, c_int64, c_void_p)
+    sig("mm_flush_l2", c_int, c_void_p, c_size_t, c_void_p)
+    sig("mm_memset", c_int, c_void_p, c_int, c_size_t, c_void_p)
+    sig("mm_axpy_f32", c_int, c_void_p, c_void_p, c_float, c_int64, c_void_p)
+
+
+def symbols() -> list[str]:
+    """Names of every entry point declared in include/mmb200.h."""
+    import re
+    hdr = os.path.join(os.path.dirname(_HERE), "include", "mmb200.h")
+    with open(hdr) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"\b(mm_[a-z0-9_]+)\s*\(", text)))

@@ -1,0 +1,74 @@
+"""Several ranks of the modular trainer emulated on ONE GPU.
+
+Each emulated rank is an ``Engine`` with its own buckets; after every rank's
+micro-batches the Algorithm-1 exchange runs as one ``mm_sync_emulated``
+launch over all ranks' grad buckets (each module's group = its hosting
+ranks, ascending; only ready members are read), then K3 runs per rank with
+the group ready counts.  This is the single-GPU stand-in for the NCCL path
+(the profiling recipe forbids running inter-dependent ranks as separate
+processes on one GPU) and gives the config-1 plumbing run on a B200.
+"""
+from __future__ import annotations
+
+from typing import Sequence
+
+from . import _native, ops
+from .domain import ModuleKey
+from .engine import DeviceBatch, Engine
+from .plan import embedding_keys, ready_counts_all
+
+
+class EmulatedCluster:
+    def __init__(self, tasks, topo, shape, world: int, device=None, seed: int = 0, **kw):
+        self.world = world
+        self.ranks = [Engine(tasks, topo, shape, rank=r, world=1, device=device, seed=seed, **kw)
+                      for r in range(world)]
+        self.plan = self.ranks[0].plan
+
+    def step(self, step_idx: int, batches: Sequence[Sequence[DeviceBatch]]) -> dict:
+        """batches[r] = rank r's micro-batches for this step."""
+        used_by_rank: dict[int, set] = {}
+        picks = {}
+        for r, eng in enumerate(self.ranks):
+            if r not in self.plan.tasks_by_rank:
+                continue
+            eng.zero_grads()
+            ops.memset(eng.loss_sum, 0)
+            used: set[ModuleKey] = set()
+            picks[r] = []
+            for db in batches[r]:
+                task = eng.mux.pick(step_idx)
+                picks[r].append(task.id)
+                eng.forward_backward(task, db, eng.loss_sum)
+                used.update(task.modules())
+                used.update(embedding_keys(task))
+            used_by_rank[r] = used
+        counts = ready_counts_all(self.plan, used_by_rank)
+        table = []
+        for k in self.plan.keys:
+            members = self.plan.groups[k]
+            if len(members) < 2:
+                continue
+            m = _native.SyncModule()
+            for j, r in enumerate(members):
+                m.bufs[j] = self.ranks[r].states[k].grad.data_ptr()
+            m.out = None
+            m.n_elems = self.ranks[members[0]].states[k].grad.numel()
+            m.group_size = len(members)
+            m.used_mask = sum(1 << j for j, r in enumerate(members) if k in used_by_rank.get(r, ()))
+            if m.used_mask:
+                table.append(m)
+        if table:
+            # the emulated kernel already divides by n and installs the mean on
+            # every member; K3 then runs with n = 1 for those modules
+            ops.sync_emulated(table, only_ready=True)
+        idx = self.plan.index()
+        for r, eng in enumerate(self.ranks):
+            if r not in used_by_rank:
+                continue
+            per_rank = []
+            for k in self.plan.keys:
+                n = counts[idx[k]]
+                per_rank.append(1 if (n >= 1 and len(self.plan.groups[k]) >= 2) else n)
+            eng.fused_update(per_rank)
+        return {"tasks": picks, "ready": dict(zip(self.plan.keys, counts))}

@@ -1,0 +1,458 @@
+// K4: bf16 GEMM on 5th-generation tensor cores (tcgen05), sm_100a.
+//
+//   D[M,N] = A[M,K] * B[N,K]^T      (fp32 accumulate in TMEM)
+//
+// One persistent CTA per SM walks a static list of work units (output tile x
+// K split).  Warp roles (192 threads):
+//   warp 0      TMA producer: A/B tiles -> 128B-swizzled smem ring (mbarrier
+//               complete_tx), one elected lane
+//   warp 1      MMA issuer: one elected lane issues tcgen05.mma (M=128, N=BN,
+//               K=16) from smem descriptors into a double-buffered TMEM
+//               accumulator, tcgen05.commit releases smem stages / signals the
+//               epilogue; this warp also owns the TMEM allocation
+//   warps 2..5  epilogue: tcgen05.ld (32 lanes x 32 columns per warp access),
+//               fused bias / ReLU / ReLU-backward mask / residual add /
+//               fp32 accumulate, 128-bit global stores
+// Operands may be K-major or MN-major (transpose bits of the instruction
+// descriptor), which is what lets forward, dgrad and wgrad all run without a
+// transpose pass:
+//   forward  Y  = X  W^T : A = X  (K-major), B = W (K-major)
+//   dgrad    dX = dY W   : A = dY (K-major), B = W (MN-major)
+//   wgrad    dW = dY^T X : A = dY (MN-major), B = X (MN-major), fp32 accumulate
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "mm_common.h"
+#include "tc_ptx.cuh"
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // one 128-byte swizzle row of bf16
+constexpr int UMMA_K = 16;
+constexpr int kThreads = 192;
+constexpr int kEpiWarp0 = 2;
+
+template <int BN>
+struct Cfg {
+    static constexpr int kStages = BN == 256 ? 4 : 6;
+    static constexpr int kABytes = BM * BK * 2;
+    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct Params {
+    int64_t m, n, k;
+    int64_t ldd;
+    void* d;
+    const float* bias;
+    const float* resid;
+    const __nv_bfloat16* aux;
+    int epilogue;
+    int tiles_m, tiles_n, splits, kb_per_split, num_kb;
+    int units;
+};
+
+__device__ __forceinline__ float bf16_to_f(uint16_t h) {
+    return __uint_as_float(static_cast<uint32_t>(h) << 16);
+}
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Epilogue for one row segment of 32 columns held in registers.
+__device__ __forceinline__ void epilogue_chunk(const Params& p, int64_t row, int64_t col0,
+                                               float (&acc)[32], bool atomic) {
+    if (row >= p.m) return;
+    const int ep = p.epilogue;
+    const int64_t ncols = (p.n - col0) < 32 ? (p.n - col0) : 32;
+    if (ncols <= 0) return;
+    if (p.bias && (ep == MM_EPI_BF16 || ep == MM_EPI_BF16_RELU || ep == MM_EPI_F32 ||
+                   ep == MM_EPI_F32_RESID)) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < ncols) acc[j] += __ldg(p.bias + col0 + j);
+    }
+    if (ep == MM_EPI_BF16_RELU) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = fmaxf(acc[j], 0.f);
+    }
+    const bool full = ncols == 32;
+    if (ep == MM_EPI_BF16_DRELU) {
+        const uint16_t* aux = reinterpret_cast<const uint16_t*>(p.aux) + row * p.ldd + col0;
+        if (full) {
+            const uint4* a4 = reinterpret_cast<const uint4*>(aux);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint4 w = __ldg(a4 + q);
+                const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int j = q * 8 + e * 2;
+                    if (bf16_to_f(ws[e] & 0xffff) <= 0.f) acc[j] = 0.f;
+                    if (bf16_to_f(ws[e] >> 16) <= 0.f) acc[j + 1] = 0.f;
+                }
+            }
+        } else {
+            for (int j = 0; j < ncols; ++j)
+                if (bf16_to_f(aux[j]) <= 0.f) acc[j] = 0.f;
+        }
+    }
+    if (ep == MM_EPI_BF16 || ep == MM_EPI_BF16_RELU || ep == MM_EPI_BF16_DRELU) {
+        uint16_t* out = reinterpret_cast<uint16_t*>(p.d) + row * p.ldd + col0;
+        if (full) {
+            uint4* o4 = reinterpret_cast<uint4*>(out);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint4 w;
+                w.x = pack2(acc[q * 8 + 0], acc[q * 8 + 1]);
+                w.y = pack2(acc[q * 8 + 2], acc[q * 8 + 3]);
+                w.z = pack2(acc[q * 8 + 4], acc[q * 8 + 5]);
+                w.w = pack2(acc[q * 8 + 6], acc[q * 8 + 7]);
+                o4[q] = w;
+            }
+        } else {
+            for (int j = 0; j < ncols; ++j) {
+                __nv_bfloat16 h = __float2bfloat16_rn(acc[j]);
+                out[j] = *reinterpret_cast<uint16_t*>(&h);
+            }
+        }
+        return;
+    }
+    float* out = reinterpret_cast<float*>(p.d) + row * p.ldd + col0;
+    if (ep == MM_EPI_F32_RESID) {
+        const float* res = p.resid + row * p.ldd + col0;
+        if (full) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                float4 r = *reinterpret_cast<const float4*>(res + q * 4);
+                acc[q * 4 + 0] += r.x; acc[q * 4 + 1] += r.y;
+                acc[q * 4 + 2] += r.z; acc[q * 4 + 3] += r.w;
+            }
+        } else {
+            for (int j = 0; j < ncols; ++j) acc[j] += res[j];
+        }
+    }
+    if (ep == MM_EPI_F32_ACCUM) {
+        if (full) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                float4* o = reinterpret_cast<float4*>(out + q * 4);
+                float4 v = make_float4(acc[q * 4], acc[q * 4 + 1], acc[q * 4 + 2], acc[q * 4 + 3]);
+                if (atomic) {
+                    atomicAdd(o, v);
+                } else {
+                    float4 c = *o;
+                    c.x += v.x; c.y += v.y; c.z += v.z; c.w += v.w;
+                    *o = c;
+                }
+            }
+        } else {
+            for (int j = 0; j < ncols; ++j) {
+                if (atomic) atomicAdd(out + j, acc[j]);
+                else out[j] += acc[j];
+            }
+        }
+        return;
+    }
+    if (full) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<float4*>(out + q * 4) =
+                make_float4(acc[q * 4], acc[q * 4 + 1], acc[q * 4 + 2], acc[q * 4 + 3]);
+    } else {
+        for (int j = 0; j < ncols; ++j) out[j] = acc[j];
+    }
+}
+
+template <int BN, int A_MN, int B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                        const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ Params p) {
+    using C = Cfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* smem_a = smem;
+    uint8_t* smem_b = smem + C::kStages * C::kABytes;
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    uint64_t* empty_bar = full_bar + C::kStages;
+    uint64_t* tfull_bar = empty_bar + C::kStages;
+    uint64_t* tempty_bar = tfull_bar + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        tc::tma_prefetch(&tmap_a);
+        tc::tma_prefetch(&tmap_b);
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            tc::mbar_init(&full_bar[s], 1);
+            tc::mbar_init(&empty_bar[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            tc::mbar_init(&tfull_bar[a], 1);
+            tc::mbar_init(&tempty_bar[a], 128);
+        }
+        tc::fence_barrier_init();
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, C::kTmemCols);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                const int tile = u / p.splits, split = u % p.splits;
+                const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+                const int kb0 = split * p.kb_per_split;
+                const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+                const int m0 = tm * BM, n0 = tn * BN;
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    tc::mbar_wait(&empty_bar[stage], phase ^ 1);
+                    tc::mbar_expect_tx(&full_bar[stage], C::kStageBytes);
+                    uint8_t* sa = smem_a + stage * C::kABytes;
+                    uint8_t* sb = smem_b + stage * C::kBBytes;
+                    const int k0 = kb * BK;
+                    if (A_MN) {
+#pragma unroll
+                        for (int c = 0; c < BM / 64; ++c)
+                            tc::tma_load_2d(sa + c * 64 * BK * 2, &tmap_a, &full_bar[stage],
+                                            m0 + c * 64, k0);
+                    } else {
+                        tc::tma_load_2d(sa, &tmap_a, &full_bar[stage], k0, m0);
+                    }
+                    if (B_MN) {
+#pragma unroll
+                        for (int c = 0; c < BN / 64; ++c)
+                            tc::tma_load_2d(sb + c * 64 * BK * 2, &tmap_b, &full_bar[stage],
+                                            n0 + c * 64, k0);
+                    } else {
+                        tc::tma_load_2d(sb, &tmap_b, &full_bar[stage], k0, n0);
+                    }
+                    if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        constexpr uint32_t idesc = tc::idesc_bf16_f32(BM, BN, A_MN, B_MN);
+        int stage = 0;
+        uint32_t phase = 0;
+        int local = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
+            const int split = u % p.splits;
+            const int kb0 = split * p.kb_per_split;
+            const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            tc::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+            tc::tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * BN;
+            for (int kb = kb0; kb < kb1; ++kb) {
+                tc::mbar_wait(&full_bar[stage], phase);
+                tc::tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t sa = tc::smem_u32(smem_a + stage * C::kABytes);
+                    const uint32_t sb = tc::smem_u32(smem_b + stage * C::kBBytes);
+#pragma unroll
+                    for (int k = 0; k < BK / UMMA_K; ++k) {
+                        // K-major: advance 32 B inside the swizzled row;
+                        // MN-major: advance 16 K-rows = 2 x 1024 B
+                        const uint64_t ad =
+                            A_MN ? tc::umma_desc_sw128(sa + k * 2048, 64 * BK * 2, 1024)
+                                 : tc::umma_desc_sw128(sa + k * 32, 16, 1024);
+                        const uint64_t bd =
+                            B_MN ? tc::umma_desc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
+                                 : tc::umma_desc_sw128(sb + k * 32, 16, 1024);
+                        tc::mma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                    }
+                    tc::mma_commit(&empty_bar[stage]);
+                }
+                __syncwarp();
+                if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+            }
+            if (lane == 0) tc::mma_commit(&tfull_bar[acc]);
+            __syncwarp();
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const int lane_grp = warp & 3;  // TMEM lanes this warp may access
+        const int row_in_tile = lane_grp * 32 + lane;
+        const bool atomic = p.splits > 1;
+        int local = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
+            const int tile = u / p.splits;
+            const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            tc::mbar_wait(&tfull_bar[acc], acc_phase);
+            tc::tc_fence_after();
+            const int64_t row = int64_t(tm) * BM + row_in_tile;
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) + acc * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t v[32];
+                tc::tmem_ld_32x32(t_row + c * 32, v);
+                tc::tmem_ld_wait();
+                float f[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+                epilogue_chunk(p, row, int64_t(tn) * BN + c * 32, f, atomic);
+            }
+            tc::tc_fence_before();
+            tc::mbar_arrive(&tempty_bar[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc(tmem_base, C::kTmemCols);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// host side
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    return fn;
+}
+
+// 2D bf16 tensor map over a row-major [outer, inner] matrix with row stride
+// `ld` elements; box = {64 (inner), box_outer}, 128-byte swizzle, OOB -> 0.
+int make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int64_t ld,
+             int box_outer) {
+    auto enc = get_encode();
+    if (!enc) {
+        mm::set_error("cuTensorMapEncodeTiled unavailable");
+        return mm::kCuda;
+    }
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_outer)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        mm::set_error("cuTensorMapEncodeTiled failed (%d): inner=%lld outer=%lld ld=%lld box=%d",
+                      (int)r, (long long)inner, (long long)outer, (long long)ld, box_outer);
+        return mm::kCuda;
+    }
+    return 0;
+}
+
+template <int BN, int A_MN, int B_MN>
+int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t s) {
+    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN>;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg<BN>::kSmem));
+        attr_set = true;
+    }
+    const int grid = std::min(p.units, mm::num_sms());
+    kern<<<grid, kThreads, Cfg<BN>::kSmem, s>>>(ma, mb, p);
+    MM_LAUNCH_CHECK("gemm_tcgen05_kernel");
+    return 0;
+}
+
+template <int BN>
+int dispatch(int a_mn, int b_mn, const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
+             cudaStream_t s) {
+    if (!a_mn && !b_mn) return launch<BN, 0, 0>(ma, mb, p, s);
+    if (!a_mn && b_mn) return launch<BN, 0, 1>(ma, mb, p, s);
+    if (a_mn && !b_mn) return launch<BN, 1, 0>(ma, mb, p, s);
+    return launch<BN, 1, 1>(ma, mb, p, s);
+}
+
+}  // namespace
+
+extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
+    MM_CHECK_ARG(a != nullptr, "args is NULL");
+    MM_CHECK_ARG(a->m > 0 && a->n > 0 && a->k > 0, "empty GEMM %lldx%lldx%lld", (long long)a->m,
+                 (long long)a->n, (long long)a->k);
+    MM_CHECK_ARG(a->epilogue >= MM_EPI_BF16 && a->epilogue <= MM_EPI_BF16_DRELU, "bad epilogue");
+    MM_CHECK_ARG(a->a && a->b && a->d, "NULL operand");
+    const bool out_bf16 = a->epilogue == MM_EPI_BF16 || a->epilogue == MM_EPI_BF16_RELU ||
+                          a->epilogue == MM_EPI_BF16_DRELU;
+    MM_CHECK_ARG((a->lda % 8) == 0 && (a->ldb % 8) == 0, "lda/ldb must be multiples of 8");
+    MM_CHECK_ARG((reinterpret_cast<uintptr_t>(a->a) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(a->b) & 15) == 0,
+                 "A/B must be 16-byte aligned");
+    MM_CHECK_ARG((reinterpret_cast<uintptr_t>(a->d) & 15) == 0 && (a->ldd % (out_bf16 ? 8 : 4)) == 0,
+                 "D must be 16-byte aligned with 16-byte row stride");
+    MM_CHECK_ARG(a->epilogue != MM_EPI_F32_RESID || a->resid, "RESID epilogue needs resid");
+    MM_CHECK_ARG(a->epilogue != MM_EPI_BF16_DRELU || a->aux, "DRELU epilogue needs aux");
+    const int a_mn = a->a_kmajor ? 0 : 1;
+    const int b_mn = a->b_kmajor ? 0 : 1;
+
+    // tile width: 256 when it still yields ~a full wave, else 128
+    const int64_t tiles_m = (a->m + BM - 1) / BM;
+    const int sms = mm::num_sms();
+    int bn = 128;
+    if (a->n >= 256 && tiles_m * ((a->n + 255) / 256) >= sms) bn = 256;
+    const int64_t tiles_n = (a->n + bn - 1) / bn;
+    const int num_kb = static_cast<int>((a->k + BK - 1) / BK);
+    const int64_t tiles = tiles_m * tiles_n;
+    // split K (fp32 accumulate only) until there are ~2 units per SM
+    int splits = 1;
+    if (a->epilogue == MM_EPI_F32_ACCUM) {
+        while (tiles * splits * 2 <= 2 * sms && splits * 2 <= num_kb / 2) splits *= 2;
+    }
+    const int kb_per = (num_kb + splits - 1) / splits;
+    splits = (num_kb + kb_per - 1) / kb_per;  // no empty splits
+    MM_CHECK_ARG(tiles * splits < (int64_t(1) << 31), "GEMM too large");
+
+    CUtensorMap ma, mb;
+    int st;
+    // A: K-major [M, K] rows of lda; MN-major [K, M] rows of lda
+    st = a_mn ? make_map(&ma, a->a, a->m, a->k, a->lda, BK)
+              : make_map(&ma, a->a, a->k, a->m, a->lda, BM);
+    if (st) return st;
+    st = b_mn ? make_map(&mb, a->b, a->n, a->k, a->ldb, BK)
+              : make_map(&mb, a->b, a->k, a->n, a->ldb, bn);
+    if (st) return st;
+
+    Params p{};
+    p.m = a->m; p.n = a->n; p.k = a->k; p.ldd = a->ldd;
+    p.d = a->d; p.bias = a->bias; p.resid = a->resid;
+    p.aux = reinterpret_cast<const __nv_bfloat16*>(a->aux);
+    p.epilogue = a->epilogue;
+    p.tiles_m = static_cast<int>(tiles_m);
+    p.tiles_n = static_cast<int>(tiles_n);
+    p.splits = splits;
+    p.kb_per_split = kb_per;
+    p.num_kb = num_kb;
+    p.units = static_cast<int>(tiles * splits);
+    cudaStream_t s = mm::as_stream(stream);
+    return bn == 256 ? dispatch<256>(a_mn, b_mn, ma, mb, p, s)
+                     : dispatch<128>(a_mn, b_mn, ma, mb, p, s);
+}

@@ -1,0 +1,428 @@
+// K6 LayerNorm, K8 embedding gather / scatter-add, K7 softmax cross-entropy,
+// and the bias-gradient column sums.  All HBM-bound: warp-per-row mappings
+// with 128-bit vector accesses and warp-shuffle reductions.
+#include <cuda_bf16.h>
+
+#include "mm_common.h"
+
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float bf2f(uint16_t h) { return __uint_as_float(uint32_t(h) << 16); }
+__device__ __forceinline__ uint16_t f2bf(float f) {
+    __nv_bfloat16 h = __float2bfloat16_rn(f);
+    return *reinterpret_cast<uint16_t*>(&h);
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+    return uint32_t(f2bf(a)) | (uint32_t(f2bf(b)) << 16);
+}
+
+// ----------------------------------------------------------------------------
+// LayerNorm: one warp per row; lane owns columns {4*lane + 128*i}.  COLS/128
+// float4 per lane held in registers (COLS in {512, 1024} for the configs).
+template <int COLS>
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x,
+                                                     const float* __restrict__ gamma,
+                                                     const float* __restrict__ beta,
+                                                     uint16_t* __restrict__ y, float* mean_out,
+                                                     float* rstd_out, int64_t rows, float eps) {
+    constexpr int V = COLS / 128;
+    const int lane = threadIdx.x & 31;
+    const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const float4* xr = reinterpret_cast<const float4*>(x + row * COLS);
+    float4 v[V];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        v[i] = xr[lane + 32 * i];
+        s += v[i].x + v[i].y + v[i].z + v[i].w;
+    }
+    const float mu = warp_sum(s) * (1.f / COLS);
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        const float a = v[i].x - mu, b = v[i].y - mu, c = v[i].z - mu, d = v[i].w - mu;
+        q += a * a + b * b + c * c + d * d;
+    }
+    const float rs = rsqrtf(warp_sum(q) * (1.f / COLS) + eps);
+    uint2* yr = reinterpret_cast<uint2*>(y + row * COLS);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        const int c = 4 * lane + 128 * i;
+        const float4 g = *reinterpret_cast<const float4*>(gamma + c);
+        const float4 b = *reinterpret_cast<const float4*>(beta + c);
+        uint2 o;
+        o.x = pack2((v[i].x - mu) * rs * g.x + b.x, (v[i].y - mu) * rs * g.y + b.y);
+        o.y = pack2((v[i].z - mu) * rs * g.z + b.z, (v[i].w - mu) * rs * g.w + b.w);
+        yr[lane + 32 * i] = o;
+    }
+    if (lane == 0) {
+        mean_out[row] = mu;
+        rstd_out[row] = rs;
+    }
+}
+
+// Backward: dxhat = dy*gamma; dx_ln = rstd*(dxhat - mean(dxhat) - xhat*mean(dxhat*xhat)).
+// dx += dx_ln (residual-stream gradient, fp32) and its bf16 copy is written;
+// dgamma += sum(dy*xhat), dbeta += sum(dy) accumulated per lane across the
+// block's rows, reduced over warps in smem, one atomicAdd per column per block.
+template <int COLS>
+__global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ dy,
+                                                     const float* __restrict__ x,
+                                                     const float* __restrict__ gamma,
+                                                     const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd, float* dx,
+                                                     uint16_t* dx_bf16, float* dgamma,
+                                                     float* dbeta, int64_t rows) {
+    constexpr int V = COLS / 128;
+    __shared__ float red_g[8][COLS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float4 ag[V], ab[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) ag[i] = ab[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t row = int64_t(blockIdx.x) * 8 + warp; row < rows; row += int64_t(gridDim.x) * 8) {
+        const float mu = mean[row], rs = rstd[row];
+        const float4* dyr = reinterpret_cast<const float4*>(dy + row * COLS);
+        const float4* xr = reinterpret_cast<const float4*>(x + row * COLS);
+        float4 g[V], xh[V];
+        float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            const int c = 4 * lane + 128 * i;
+            const float4 d = dyr[lane + 32 * i];
+            const float4 xv = xr[lane + 32 * i];
+            const float4 gm = *reinterpret_cast<const float4*>(gamma + c);
+            xh[i] = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs,
+                                (xv.w - mu) * rs);
+            g[i] = make_float4(d.x * gm.x, d.y * gm.y, d.z * gm.z, d.w * gm.w);
+            s1 += g[i].x + g[i].y + g[i].z + g[i].w;
+            s2 += g[i].x * xh[i].x + g[i].y * xh[i].y + g[i].z * xh[i].z + g[i].w * xh[i].w;
+            ag[i].x += d.x * xh[i].x; ag[i].y += d.y * xh[i].y;
+            ag[i].z += d.z * xh[i].z; ag[i].w += d.w * xh[i].w;
+            ab[i].x += d.x; ab[i].y += d.y; ab[i].z += d.z; ab[i].w += d.w;
+        }
+        const float m1 = warp_sum(s1) * (1.f / COLS), m2 = warp_sum(s2) * (1.f / COLS);
+        float4* dxr = reinterpret_cast<float4*>(dx + row * COLS);
+        uint2* dbr = reinterpret_cast<uint2*>(dx_bf16 + row * COLS);
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            float4 o = dxr[lane + 32 * i];
+            o.x += rs * (g[i].x - m1 - xh[i].x * m2);
+            o.y += rs * (g[i].y - m1 - xh[i].y * m2);
+            o.z += rs * (g[i].z - m1 - xh[i].z * m2);
+            o.w += rs * (g[i].w - m1 - xh[i].w * m2);
+            dxr[lane + 32 * i] = o;
+            if (dx_bf16) {
+                uint2 b;
+                b.x = pack2(o.x, o.y);
+                b.y = pack2(o.z, o.w);
+                dbr[lane + 32 * i] = b;
+            }
+        }
+    }
+    // two reductions through the same smem buffer
+    for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            const float4 a = pass == 0 ? ag[i] : ab[i];
+            *reinterpret_cast<float4*>(&red_g[warp][4 * lane + 128 * i]) = a;
+        }
+        __syncthreads();
+        float* dst = pass == 0 ? dgamma : dbeta;
+        for (int c = threadIdx.x; c < COLS; c += 256) {
+            float s = 0.f;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) s += red_g[w][c];
+            atomicAdd(dst + c, s);
+        }
+        __syncthreads();
+    }
+}
+
+// ----------------------------------------------------------------------------
+// Embedding: out[r,:] = table[id[r],:] * scale + PE(pos[r]) (sinusoidal,
+// sin on even / cos on odd columns, OpenNMT layout).  One warp per row.
+__global__ void __launch_bounds__(256) embed_fwd_kernel(const int32_t* __restrict__ ids,
+                                                        const int32_t* __restrict__ pos,
+                                                        const uint16_t* __restrict__ table,
+                                                        float* __restrict__ out, int64_t rows,
+                                                        int cols, float scale) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const int64_t id = ids[row];
+    const float p = static_cast<float>(pos[row]);
+    const uint2* tr = reinterpret_cast<const uint2*>(table + id * cols);
+    float4* orow = reinterpret_cast<float4*>(out + row * cols);
+    const float kLog = -9.210340371976184f / static_cast<float>(cols);  // -ln(10000)/d
+    for (int v = lane; v < cols / 4; v += 32) {
+        const uint2 w = __ldg(tr + v);
+        const int c = 4 * v;
+        const float f0 = expf(kLog * static_cast<float>(c));
+        const float f1 = expf(kLog * static_cast<float>(c + 2));
+        float s0, c0, s1, c1;
+        sincosf(p * f0, &s0, &c0);
+        sincosf(p * f1, &s1, &c1);
+        float4 o;
+        o.x = bf2f(w.x & 0xffff) * scale + s0;
+        o.y = bf2f(w.x >> 16) * scale + c0;
+        o.z = bf2f(w.y & 0xffff) * scale + s1;
+        o.w = bf2f(w.y >> 16) * scale + c1;
+        orow[v] = o;
+    }
+}
+
+__global__ void __launch_bounds__(256) embed_bwd_kernel(const int32_t* __restrict__ ids,
+                                                        const float* __restrict__ dout,
+                                                        float* dtable, int64_t rows, int cols,
+                                                        float scale) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const int64_t id = ids[row];
+    const float4* d = reinterpret_cast<const float4*>(dout + row * cols);
+    float4* t = reinterpret_cast<float4*>(dtable + id * cols);
+    for (int v = lane; v < cols / 4; v += 32) {
+        float4 g = d[v];
+        g.x *= scale; g.y *= scale; g.z *= scale; g.w *= scale;
+        atomicAdd(t + v, g);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// Cross-entropy over bf16 logits, one CTA per row.  Pass 1: per-thread online
+// (max, sum-exp) over 8-wide bf16 vectors, block-combined.  Pass 2 (row is
+// L1/L2-resident): dlogits = (softmax - onehot(label)) * grad_scale in bf16.
+// label < 0 marks padding: zero loss, zero gradient.
+constexpr int kXentThreads = 512;
+
+__global__ void __launch_bounds__(kXentThreads) xent_kernel(const uint16_t* logits,
+                                                            const int32_t* __restrict__ labels,
+                                                            uint16_t* dlogits, float* row_loss,
+                                                            float* loss_sum, int vocab,
+                                                            float grad_scale) {
+    __shared__ float sm_m[kXentThreads / 32], sm_s[kXentThreads / 32];
+    const int64_t row = blockIdx.x;
+    const int label = labels[row];
+    const uint16_t* lr = logits + row * int64_t(vocab);
+    uint16_t* dr = dlogits + row * int64_t(vocab);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (label < 0) {
+        for (int v = threadIdx.x; v < vocab / 8; v += kXentThreads)
+            reinterpret_cast<uint4*>(dr)[v] = make_uint4(0, 0, 0, 0);
+        for (int c = (vocab / 8) * 8 + threadIdx.x; c < vocab; c += kXentThreads) dr[c] = 0;
+        if (threadIdx.x == 0) row_loss[row] = 0.f;
+        return;
+    }
+    float m = -INFINITY, s = 0.f;
+    const int nv = vocab / 8;
+    for (int v = threadIdx.x; v < nv; v += kXentThreads) {
+        const uint4 w = reinterpret_cast<const uint4*>(lr)[v];
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        float f[8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            f[2 * e] = bf2f(ws[e] & 0xffff);
+            f[2 * e + 1] = bf2f(ws[e] >> 16);
+        }
+        float lm = f[0];
+#pragma unroll
+        for (int e = 1; e < 8; ++e) lm = fmaxf(lm, f[e]);
+        const float nm = fmaxf(m, lm);
+        float acc = s * __expf(m - nm);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc += __expf(f[e] - nm);
+        m = nm;
+        s = acc;
+    }
+    for (int c = nv * 8 + threadIdx.x; c < vocab; c += kXentThreads) {
+        const float f = bf2f(lr[c]);
+        const float nm = fmaxf(m, f);
+        s = s * __expf(m - nm) + __expf(f - nm);
+        m = nm;
+    }
+    // combine (m, s) across the warp, then across warps
+    float wm = warp_max(m);
+    float ws_ = warp_sum(m == -INFINITY ? 0.f : s * __expf(m - wm));
+    if (lane == 0) { sm_m[warp] = wm; sm_s[warp] = ws_; }
+    __syncthreads();
+    float gm = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kXentThreads / 32; ++w) gm = fmaxf(gm, sm_m[w]);
+    float gs = 0.f;
+#pragma unroll
+    for (int w = 0; w < kXentThreads / 32; ++w) gs += sm_s[w] * __expf(sm_m[w] - gm);
+    const float lse = gm + __logf(gs);
+    const float inv = 1.f / gs;
+    if (threadIdx.x == 0) {
+        const float l = lse - bf2f(lr[label]);
+        row_loss[row] = l;
+        if (loss_sum) atomicAdd(loss_sum, l * grad_scale);  // token mean when scale = 1/rows
+    }
+    __syncthreads();  // every read of the row's label logit precedes in-place writes
+    for (int v = threadIdx.x; v < nv; v += kXentThreads) {
+        const uint4 w = reinterpret_cast<const uint4*>(lr)[v];
+        const uint32_t wsv[4] = {w.x, w.y, w.z, w.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int c = v * 8 + 2 * e;
+            float p0 = __expf(bf2f(wsv[e] & 0xffff) - gm) * inv;
+            float p1 = __expf(bf2f(wsv[e] >> 16) - gm) * inv;
+            if (c == label) p0 -= 1.f;
+            if (c + 1 == label) p1 -= 1.f;
+            o[e] = pack2(p0 * grad_scale, p1 * grad_scale);
+        }
+        reinterpret_cast<uint4*>(dr)[v] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    for (int c = nv * 8 + threadIdx.x; c < vocab; c += kXentThreads) {
+        float pr = __expf(bf2f(lr[c]) - gm) * inv;
+        if (c == label) pr -= 1.f;
+        dr[c] = f2bf(pr * grad_scale);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// out[c] += sum_r x[r, c] (bias gradients).  A thread owns a column pair, a
+// block covers 512 columns x a 64-row slab; slab sums go out with atomics.
+constexpr int kColRows = 64;
+
+__global__ void __launch_bounds__(256) colsum_kernel(const uint16_t* __restrict__ x, float* out,
+                                                     int64_t rows, int cols) {
+    const int cp = blockIdx.x * 256 + threadIdx.x;  // column pair
+    if (2 * cp >= cols) return;
+    const int64_t r0 = int64_t(blockIdx.y) * kColRows;
+    const int64_t r1 = min(rows, r0 + kColRows);
+    float a = 0.f, b = 0.f;
+    const uint32_t* xp = reinterpret_cast<const uint32_t*>(x);
+    for (int64_t r = r0; r < r1; ++r) {
+        const uint32_t w = __ldg(xp + r * (cols / 2) + cp);
+        a += bf2f(w & 0xffff);
+        b += bf2f(w >> 16);
+    }
+    atomicAdd(out + 2 * cp, a);
+    atomicAdd(out + 2 * cp + 1, b);
+}
+
+__global__ void cast_kernel(const float* __restrict__ x, uint16_t* __restrict__ y, int64_t n4) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const float4 v = reinterpret_cast<const float4*>(x)[i];
+        uint2 o;
+        o.x = pack2(v.x, v.y);
+        o.y = pack2(v.z, v.w);
+        reinterpret_cast<uint2*>(y)[i] = o;
+    }
+}
+
+}  // namespace
+
+extern "C" int mm_layernorm_fwd(const float* x, const float* gamma, const float* beta, uint16_t* y,
+                                float* mean, float* rstd, int64_t rows, int cols, float eps,
+                                void* stream) {
+    MM_CHECK_ARG(x && gamma && beta && y && mean && rstd, "NULL argument");
+    if (rows == 0) return 0;
+    const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
+    auto s = mm::as_stream(stream);
+    if (cols == 512)
+        ln_fwd_kernel<512><<<grid, 256, 0, s>>>(x, gamma, beta, y, mean, rstd, rows, eps);
+    else if (cols == 1024)
+        ln_fwd_kernel<1024><<<grid, 256, 0, s>>>(x, gamma, beta, y, mean, rstd, rows, eps);
+    else if (cols == 128)
+        ln_fwd_kernel<128><<<grid, 256, 0, s>>>(x, gamma, beta, y, mean, rstd, rows, eps);
+    else if (cols == 256)
+        ln_fwd_kernel<256><<<grid, 256, 0, s>>>(x, gamma, beta, y, mean, rstd, rows, eps);
+    else {
+        mm::set_error("layernorm: cols=%d unsupported (128/256/512/1024)", cols);
+        return mm::kUnsupported;
+    }
+    MM_LAUNCH_CHECK("ln_fwd_kernel");
+    return 0;
+}
+
+extern "C" int mm_layernorm_bwd(const float* dy, const float* x, const float* gamma,
+                                const float* mean, const float* rstd, float* dx, uint16_t* dx_bf16,
+                                float* dgamma, float* dbeta, int64_t rows, int cols, void* stream) {
+    MM_CHECK_ARG(dy && x && gamma && mean && rstd && dx && dgamma && dbeta, "NULL argument");
+    if (rows == 0) return 0;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((rows + 7) / 8, 4 * mm::num_sms()));
+    auto s = mm::as_stream(stream);
+    if (cols == 512)
+        ln_bwd_kernel<512><<<grid, 256, 0, s>>>(dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows);
+    else if (cols == 1024)
+        ln_bwd_kernel<1024><<<grid, 256, 0, s>>>(dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows);
+    else if (cols == 128)
+        ln_bwd_kernel<128><<<grid, 256, 0, s>>>(dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows);
+    else if (cols == 256)
+        ln_bwd_kernel<256><<<grid, 256, 0, s>>>(dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows);
+    else {
+        mm::set_error("layernorm: cols=%d unsupported (128/256/512/1024)", cols);
+        return mm::kUnsupported;
+    }
+    MM_LAUNCH_CHECK("ln_bwd_kernel");
+    return 0;
+}
+
+extern "C" int mm_embed_fwd(const int32_t* ids, const int32_t* pos, const uint16_t* table,
+                            float* out, int64_t rows, int cols, float scale, void* stream) {
+    MM_CHECK_ARG(ids && pos && table && out, "NULL argument");
+    MM_CHECK_ARG(cols % 4 == 0, "cols must be a multiple of 4");
+    if (rows == 0) return 0;
+    embed_fwd_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, mm::as_stream(stream)>>>(
+        ids, pos, table, out, rows, cols, scale);
+    MM_LAUNCH_CHECK("embed_fwd_kernel");
+    return 0;
+}
+
+extern "C" int mm_embed_bwd(const int32_t* ids, const float* dout, float* dtable, int64_t rows,
+                            int cols, float scale, void* stream) {
+    MM_CHECK_ARG(ids && dout && dtable, "NULL argument");
+    MM_CHECK_ARG(cols % 4 == 0, "cols must be a multiple of 4");
+    if (rows == 0) return 0;
+    embed_bwd_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, mm::as_stream(stream)>>>(
+        ids, dout, dtable, rows, cols, scale);
+    MM_LAUNCH_CHECK("embed_bwd_kernel");
+    return 0;
+}
+
+extern "C" int mm_xent_fwd_bwd(const uint16_t* logits, const int32_t* labels, uint16_t* dlogits,
+                               float* row_loss, float* loss_sum, int64_t rows, int vocab,
+                               float grad_scale, void* stream) {
+    MM_CHECK_ARG(logits && labels && dlogits && row_loss, "NULL argument");
+    MM_CHECK_ARG(vocab % 8 == 0, "vocab must be a multiple of 8");
+    if (rows == 0) return 0;
+    xent_kernel<<<static_cast<unsigned>(rows), kXentThreads, 0, mm::as_stream(stream)>>>(
+        logits, labels, dlogits, row_loss, loss_sum, vocab, grad_scale);
+    MM_LAUNCH_CHECK("xent_kernel");
+    return 0;
+}
+
+extern "C" int mm_colsum_bf16(const uint16_t* x, float* out, int64_t rows, int cols,
+                              void* stream) {
+    MM_CHECK_ARG(x && out && cols % 2 == 0, "bad arguments");
+    if (rows == 0) return 0;
+    dim3 grid((cols / 2 + 255) / 256, static_cast<unsigned>((rows + kColRows - 1) / kColRows));
+    colsum_kernel<<<grid, 256, 0, mm::as_stream(stream)>>>(x, out, rows, cols);
+    MM_LAUNCH_CHECK("colsum_kernel");
+    return 0;
+}
+
+extern "C" int mm_cast_f32_bf16(const float* x, uint16_t* y, int64_t n, void* stream) {
+    MM_CHECK_ARG(x && y && n % 4 == 0, "n must be a multiple of 4");
+    if (n == 0) return 0;
+    const int64_t n4 = n / 4;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n4 + 255) / 256, 8 * mm::num_sms()));
+    cast_kernel<<<grid, 256, 0, mm::as_stream(stream)>>>(x, y, n4);
+    MM_LAUNCH_CHECK("cast_kernel");
+    return 0;
+}

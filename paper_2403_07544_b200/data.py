@@ -1,0 +1,114 @@
+"""Synthetic token batches with the shapes and distributions of BASELINE.json
+(the paper's Europarl corpora and SentencePiece models are not available; no
+dataset items are reproduced).
+
+A batch is a list of sentence pairs packed without padding:
+* source ids ``[Ts]`` with in-sentence positions and ``cu_src`` offsets;
+* decoder input ``[Tt]`` = BOS + target content, labels = content + EOS,
+  positions and ``cu_tgt`` offsets.
+Ids 0..3 are pad / bos / eos / unk; content ids are drawn from 4..V-1,
+uniformly (config 1) or Zipf(s) by rank (configs 3-5).  Sentence lengths are
+uniform in [lo, hi] (config 1) or round(lognormal(mu, sigma)) clipped to
+[lo, hi]; sentences are added until the target side holds exactly
+``tokens`` tokens (the last target sentence is shortened, min 1).
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Optional
+
+import numpy as np
+
+BOS, EOS = 1, 2
+FIRST_ID = 4
+
+
+@dataclasses.dataclass
+class Batch:
+    src: np.ndarray      # int32 [Ts]
+    src_pos: np.ndarray
+    cu_src: np.ndarray   # int32 [n+1]
+    tgt_in: np.ndarray   # int32 [Tt]
+    tgt_pos: np.ndarray
+    labels: np.ndarray   # int32 [Tt]
+    cu_tgt: np.ndarray
+
+    @property
+    def n_seq(self) -> int:
+        return len(self.cu_src) - 1
+
+    @property
+    def n_src(self) -> int:
+        return int(self.cu_src[-1])
+
+    @property
+    def n_tgt(self) -> int:
+        return int(self.cu_tgt[-1])
+
+    @property
+    def max_src(self) -> int:
+        return int(np.diff(self.cu_src).max())
+
+    @property
+    def max_tgt(self) -> int:
+        return int(np.diff(self.cu_tgt).max())
+
+    def host_arrays(self) -> dict[str, np.ndarray]:
+        return {"src": self.src, "src_pos": self.src_pos, "cu_src": self.cu_src,
+                "tgt_in": self.tgt_in, "tgt_pos": self.tgt_pos, "labels": self.labels,
+                "cu_tgt": self.cu_tgt}
+
+    def nbytes(self) -> int:
+        return sum(a.nbytes for a in self.host_arrays().values())
+
+
+class ZipfIds:
+    """Inverse-CDF sampler of rank-Zipf(s) ids over [FIRST_ID, vocab)."""
+
+    def __init__(self, vocab: int, s: float):
+        ranks = np.arange(1, vocab - FIRST_ID + 1, dtype=np.float64)
+        w = ranks ** (-s) if s > 0 else np.ones_like(ranks)
+        self.cdf = np.cumsum(w) / w.sum()
+
+    def draw(self, rng: np.random.Generator, n: int) -> np.ndarray:
+        idx = np.searchsorted(self.cdf, rng.random(n), side="right")
+        return (np.minimum(idx, len(self.cdf) - 1) + FIRST_ID).astype(np.int32)
+
+
+def _lengths(rng, n, spec) -> np.ndarray:
+    if spec.len_mu == 0:
+        return rng.integers(spec.len_min, spec.len_max + 1, size=n)
+    x = np.round(rng.lognormal(spec.len_mu, spec.len_sigma, size=n))
+    return np.clip(x, spec.len_min, spec.len_max).astype(np.int64)
+
+
+def make_batch(rng: np.random.Generator, spec, vocab: int, sentences: Optional[int] = None,
+               ids: Optional[ZipfIds] = None) -> Batch:
+    """One micro-batch: ``sentences`` pairs if given, else ``spec.tokens_per_gpu``
+    target tokens."""
+    ids = ids or ZipfIds(vocab, spec.zipf_s)
+    if sentences is not None:
+        ls, lt = _lengths(rng, sentences, spec), _lengths(rng, sentences, spec)
+    else:
+        ls_l, lt_l, tot = [], [], 0
+        while tot < spec.tokens_per_gpu:
+            a, b = _lengths(rng, 2, spec)
+            b = min(int(b), spec.tokens_per_gpu - tot)
+            ls_l.append(int(a))
+            lt_l.append(b)
+            tot += b
+        ls, lt = np.asarray(ls_l), np.asarray(lt_l)
+    cu_s = np.concatenate([[0], np.cumsum(ls)]).astype(np.int32)
+    cu_t = np.concatenate([[0], np.cumsum(lt)]).astype(np.int32)
+    src = ids.draw(rng, int(cu_s[-1]))
+    content = ids.draw(rng, int(cu_t[-1]))
+    labels = content.copy()
+    tgt_in = np.empty_like(content)
+    for j in range(len(lt)):
+        a, b = cu_t[j], cu_t[j + 1]
+        labels[b - 1] = EOS
+        tgt_in[a] = BOS
+        tgt_in[a + 1:b] = content[a:b - 1]
+    src_pos = np.concatenate([np.arange(n) for n in ls]).astype(np.int32)
+    tgt_pos = np.concatenate([np.arange(n) for n in lt]).astype(np.int32)
+    return Batch(src, src_pos, cu_s, tgt_in, tgt_pos, labels, cu_t)

@@ -1,0 +1,451 @@
+"""The B200 modular-training step: per-language transformer modules, one
+process per GPU, Algorithm-1 gradient exchange and the fused optimizer.
+
+Replaces the trainer loop of the reference simulator (``run_benchmark``,
+``syncsim.py:346-392``): for every rank, ``accum_count`` micro-batches are
+drawn through the multiplexer (``syncsim.py:353``), each runs the task's
+encoder stacks then decoder stacks (``TaskSpec.modules()``, core.py:147-149)
+with hand-written sm_100a kernels (K4-K8), gradients accumulate straight into
+each module's flat fp32 bucket (``DeviceState.accumulate``, syncsim.py:113-118),
+then
+
+* K1  ready counts: world int32 allreduce of the used-flags (NCCL),
+* K2  per-module sum over the module's own NCCL sub-communicator, only for
+      groups with >= 2 ranks and n >= 1, in sorted ModuleKey order,
+* K3  fused ``/ n`` rescale + Adam + bf16 weight write for every hosted
+      module with n >= 1 (n == 0: no update, no optimizer step).
+
+All compute goes through ``libmmb200.so``; torch provides allocations and
+the stream only.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _native, ops
+from .configs import ModelShape
+from .data import Batch
+from .domain import ClusterTopology, ModuleKey, Side, TaskSpec
+from .model import LN_EPS, ModuleState, module_layouts
+from .plan import Multiplexer, build_plan, embedding_keys, ready_flags
+
+
+@dataclasses.dataclass
+class AdamConfig:
+    lr: float = 2e-4
+    beta1: float = 0.9
+    beta2: float = 0.998
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+
+
+class DeviceBatch:
+    """A packed batch resident in HBM (one H2D copy from a pinned buffer)."""
+
+    FIELDS = ("src", "src_pos", "cu_src", "tgt_in", "tgt_pos", "labels", "cu_tgt")
+
+    def __init__(self, b: Batch, device, pinned: Optional[torch.Tensor] = None,
+                 non_blocking: bool = True):
+        arrs = b.host_arrays()
+        sizes = [len(arrs[f]) for f in self.FIELDS]
+        total = sum(sizes)
+        host = pinned if pinned is not None and pinned.numel() >= total else \
+            torch.empty(total, dtype=torch.int32, pin_memory=True)
+        flat = host.numpy()
+        off = 0
+        for f, n in zip(self.FIELDS, sizes):
+            flat[off:off + n] = arrs[f]
+            off += n
+        self.h2d_bytes = total * 4
+        dev = torch.empty(total, dtype=torch.int32, device=device)
+        dev.copy_(host[:total], non_blocking=non_blocking)
+        off = 0
+        for f, n in zip(self.FIELDS, sizes):
+            setattr(self, f, dev[off:off + n])
+            off += n
+        self.n_seq = b.n_seq
+        self.n_src, self.n_tgt = b.n_src, b.n_tgt
+        self.max_src, self.max_tgt = b.max_src, b.max_tgt
+        self._keep = host  # keep the pinned staging alive until the copy retires
+
+
+class CommGroups:
+    """NCCL world + one sub-communicator per distinct member set (K1/K2)."""
+
+    def __init__(self, plan, rank: int, world: int, device_index: int, store):
+        L = _native.lib()
+        if rank == 0:
+            uid = ctypes_buf(128)
+            _native.check(L.mm_nccl_unique_id(uid), "mm_nccl_unique_id")
+            store.set("mmb200_nccl_uid", bytes(uid.raw))
+        uid_bytes = store.get("mmb200_nccl_uid")
+        self.ctx = ctypes_voidp()
+        _native.check(L.mm_comm_init(rank, world, uid_bytes, device_index, ctypes_ref(self.ctx)),
+                      "mm_comm_init")
+        self.by_set: dict[tuple, object] = {}
+        for members in plan.member_sets():  # identical order on every rank
+            arr = (ctypes_int * len(members))(*members)
+            grp = ctypes_voidp()
+            _native.check(L.mm_group_create(self.ctx, arr, len(members), ctypes_ref(grp)),
+                          "mm_group_create")
+            self.by_set[members] = grp.value
+        self.rank, self.world = rank, world
+
+    def ready_count(self, flags_dev: torch.Tensor, n_dev: torch.Tensor) -> None:
+        _native.check(_native.lib().mm_ready_count(self.ctx, flags_dev.data_ptr(), n_dev.data_ptr(),
+                                                   flags_dev.numel(), ops.stream_ptr()),
+                      "mm_ready_count")
+
+    def reduce(self, items) -> None:
+        if not items:
+            return
+        arr = (_native.ReduceItem * len(items))(*items)
+        _native.check(_native.lib().mm_reduce_modules(self.ctx, arr, len(items), ops.stream_ptr()),
+                      "mm_reduce_modules")
+
+    def close(self) -> None:
+        L = _native.lib()
+        for g in self.by_set.values():
+            if g:
+                L.mm_group_destroy(g)
+        L.mm_comm_destroy(self.ctx)
+
+
+import ctypes  # noqa: E402  (helpers for CommGroups)
+
+ctypes_int = ctypes.c_int
+
+
+def ctypes_buf(n):
+    return ctypes.create_string_buffer(n)
+
+
+def ctypes_voidp():
+    return ctypes.c_void_p()
+
+
+def ctypes_ref(x):
+    return ctypes.byref(x)
+
+
+class Engine:
+    """One rank of the modular trainer."""
+
+    def __init__(self, tasks: Sequence[TaskSpec], topo: ClusterTopology, shape: ModelShape,
+                 rank: int = 0, world: int = 1, device=None, seed: int = 0,
+                 adam: AdamConfig = AdamConfig(), store=None, masters=None):
+        if shape.head_dim != 64:
+            raise ValueError("the attention kernel is specialised for head_dim 64")
+        self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
+        self.shape = shape
+        self.rank, self.world = rank, world
+        self.plan = build_plan(tasks, topo)
+        self.layouts = module_layouts(self.plan, shape)
+        self.index = self.plan.index()
+        self.hosted = sorted(self.plan.hosted.get(rank, frozenset()))
+        self.states: dict[ModuleKey, ModuleState] = {}
+        for k in self.hosted:
+            m = None if masters is None else masters.get(k)
+            st = ModuleState(self.layouts[k], shape, self.device, seed, master=m)
+            self.states[k] = st
+        self.mux = Multiplexer(self.plan, rank, seed)
+        self.adam = adam
+        self.comm = CommGroups(self.plan, rank, world, self.device.index or 0, store) \
+            if world > 1 else None
+        self.loss_sum = torch.zeros(1, device=self.device)
+        self.n_ready_dev = torch.zeros(len(self.plan.keys), dtype=torch.int32, device=self.device)
+        self.flags_dev = torch.zeros(len(self.plan.keys), dtype=torch.int32, device=self.device)
+        self.scale = math.sqrt(shape.d_model)
+        self.trace = None  # set to a dict to capture intermediates (diagnostics)
+
+    # ------------------------------------------------------------------ layers
+    def _zeros(self, *shape):
+        t = torch.empty(*shape, device=self.device)
+        ops.memset(t, 0)
+        return t
+
+    def _tr(self, name, t):
+        if self.trace is not None:
+            self.trace[name] = t.detach().float().cpu()
+
+    def _ln(self, st, name, x):
+        T, d = x.shape
+        y = torch.empty(T, d, device=self.device, dtype=torch.bfloat16)
+        mean = torch.empty(T, device=self.device)
+        rstd = torch.empty(T, device=self.device)
+        ops.layernorm_fwd(x, st.f32(name + ".g"), st.f32(name + ".b"), y, mean, rstd, LN_EPS)
+        return y, mean, rstd
+
+    def _ln_bwd(self, st, name, dy, x, mean, rstd, dx, dx_bf):
+        ops.layernorm_bwd(dy, x, st.f32(name + ".g"), mean, rstd, dx, dx_bf,
+                          st.g(name + ".g"), st.g(name + ".b"))
+
+    def _attn_args(self, q, k, v, o, lse, cu_q, cu_k, n_seq, max_q, max_k, causal, **kw):
+        return ops.attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, self.shape.heads, max_q,
+                                  max_k, causal, **kw)
+
+    def _self_block_fwd(self, st, p, x, cu, n_seq, max_len, causal, sv):
+        d = self.shape.d_model
+        T = x.shape[0]
+        h, mean, rstd = self._ln(st, p + "ln1", x)
+        qkv = torch.empty(T, 3 * d, device=self.device, dtype=torch.bfloat16)
+        ops.gemm(h, st.w(p + "qkv.w"), qkv, epilogue=ops.EPI_BF16, bias=st.f32(p + "qkv.b"))
+        a = torch.empty(T, d, device=self.device, dtype=torch.bfloat16)
+        lse = torch.empty(self.shape.heads, T, device=self.device)
+        ops.attention_fwd(self._attn_args(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], a, lse, cu,
+                                          cu, n_seq, max_len, max_len, causal))
+        out = torch.empty_like(x)
+        ops.gemm(a, st.w(p + "out.w"), out, epilogue=ops.EPI_F32_RESID, bias=st.f32(p + "out.b"),
+                 resid=x)
+        sv.append(("self", x, h, mean, rstd, qkv, a, lse))
+        return out
+
+    def _cross_block_fwd(self, st, p, x, mem, db, sv):
+        d = self.shape.d_model
+        T, S = x.shape[0], mem.shape[0]
+        h, mean, rstd = self._ln(st, p + "lnc", x)
+        q = torch.empty(T, d, device=self.device, dtype=torch.bfloat16)
+        ops.gemm(h, st.w(p + "cq.w"), q, epilogue=ops.EPI_BF16, bias=st.f32(p + "cq.b"))
+        kv = torch.empty(S, 2 * d, device=self.device, dtype=torch.bfloat16)
+        ops.gemm(mem, st.w(p + "ckv.w"), kv, epilogue=ops.EPI_BF16, bias=st.f32(p + "ckv.b"))
+        a = torch.empty(T, d, device=self.device, dtype=torch.bfloat16)
+        lse = torch.empty(self.shape.heads, T, device=self.device)
+        ops.attention_fwd(self._attn_args(q, kv[:, :d], kv[:, d:], a, lse, db.cu_tgt, db.cu_src,
+                                          db.n_seq, db.max_tgt, db.max_src, False))
+        out = torch.empty_like(x)
+        ops.gemm(a, st.w(p + "cout.w"), out, epilogue=ops.EPI_F32_RESID, bias=st.f32(p + "cout.b"),
+                 resid=x)
+        self._tr(p + "ckv", kv)
+        self._tr(p + "ca", a)
+        self._tr(p + "cx_in", x)
+        sv.append(("cross", x, h, mean, rstd, q, kv, a, lse))
+        return out
+
+    def _ffn_fwd(self, st, p, x, sv):
+        T = x.shape[0]
+        h, mean, rstd = self._ln(st, p + "ln2", x)
+        f = torch.empty(T, self.shape.ffn, device=self.device, dtype=torch.bfloat16)
+        ops.gemm(h, st.w(p + "ff1.w"), f, epilogue=ops.EPI_BF16_RELU, bias=st.f32(p + "ff1.b"))
+        out = torch.empty_like(x)
+        ops.gemm(f, st.w(p + "ff2.w"), out, epilogue=ops.EPI_F32_RESID, bias=st.f32(p + "ff2.b"),
+                 resid=x)
+        sv.append(("ffn", x, h, mean, rstd, f))
+        return out
+
+    # backward of the three block kinds; dx (fp32) / dx_bf hold dL/d(block output)
+    def _ffn_bwd(self, st, p, rec, dx, dx_bf):
+        _, x_in, h, mean, rstd, f = rec
+        T = x_in.shape[0]
+        ops.gemm(dx_bf, f, st.g(p + "ff2.w"), a_kmajor=False, b_kmajor=False,
+                 epilogue=ops.EPI_F32_ACCUM)
+        ops.colsum(dx_bf, st.g(p + "ff2.b"))
+        df = torch.empty(T, self.shape.ffn, device=self.device, dtype=torch.bfloat16)
+        ops.gemm(dx_bf, st.w(p + "ff2.w"), df, b_kmajor=False, epilogue=ops.EPI_BF16_DRELU, aux=f)
+        ops.gemm(df, h, st.g(p + "ff1.w"), a_kmajor=False, b_kmajor=False,
+                 epilogue=ops.EPI_F32_ACCUM)
+        ops.colsum(df, st.g(p + "ff1.b"))
+        dh = torch.empty(T, self.shape.d_model, device=self.device)
+        ops.gemm(df, st.w(p + "ff1.w"), dh, b_kmajor=False, epilogue=ops.EPI_F32)
+        self._ln_bwd(st, p + "ln2", dh, x_in, mean, rstd, dx, dx_bf)
+
+    def _self_bwd(self, st, p, rec, dx, dx_bf, cu, n_seq, max_len, causal):
+        _, x_in, h, mean, rstd, qkv, a, lse = rec
+        d = self.shape.d_model
+        T = x_in.shape[0]
+        ops.gemm(dx_bf, a, st.g(p + "out.w"), a_kmajor=False, b_kmajor=False,
+                 epilogue=ops.EPI_F32_ACCUM)
+        ops.colsum(dx_bf, st.g(p + "out.b"))
+        da = torch.empty(T, d, device=self.device, dtype=torch.bfloat16)
+        ops.gemm(dx_bf, st.w(p + "out.w"), da, b_kmajor=False, epilogue=ops.EPI_BF16)
+        dqkv = torch.empty(T, 3 * d, device=self.device, dtype=torch.bfloat16)
+        ops.attention_bwd(self._attn_args(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], a, lse, cu,
+                                          cu, n_seq, max_len, max_len, causal, d_o=da,
+                                          dq=dqkv[:, :d], dk=dqkv[:, d:2 * d], dv=dqkv[:, 2 * d:]))
+        ops.gemm(dqkv, h, st.g(p + "qkv.w"), a_kmajor=False, b_kmajor=False,
+                 epilogue=ops.EPI_F32_ACCUM)
+        ops.colsum(dqkv, st.g(p + "qkv.b"))
+        dh = torch.empty(T, d, device=self.device)
+        ops.gemm(dqkv, st.w(p + "qkv.w"), dh, b_kmajor=False, epilogue=ops.EPI_F32)
+        self._ln_bwd(st, p + "ln1", dh, x_in, mean, rstd, dx, dx_bf)
+
+    def _cross_bwd(self, st, p, rec, dx, dx_bf, mem, dmem, db):
+        _, x_in, h, mean, rstd, q, kv, a, lse = rec
+        d = self.shape.d_model
+        T, S = x_in.shape[0], mem.shape[0]
+        ops.gemm(dx_bf, a, st.g(p + "cout.w"), a_kmajor=False, b_kmajor=False,
+                 epilogue=ops.EPI_F32_ACCUM)
+        ops.colsum(dx_bf, st.g(p + "cout.b"))
+        da = torch.empty(T, d, device=self.device, dtype=torch.bfloat16)
+        ops.gemm(dx_bf, st.w(p + "cout.w"), da, b_kmajor=False, epilogue=ops.EPI_BF16)
+        dq = torch.empty(T, d, device=self.device, dtype=torch.bfloat16)
+        dkv = torch.empty(S, 2 * d, device=self.device, dtype=torch.bfloat16)
+        ops.attention_bwd(self._attn_args(q, kv[:, :d], kv[:, d:], a, lse, db.cu_tgt, db.cu_src,
+                                          db.n_seq, db.max_tgt, db.max_src, False, d_o=da, dq=dq,
+                                          dk=dkv[:, :d], dv=dkv[:, d:]))
+        self._tr(p + "dckv", dkv)
+        self._tr(p + "dca", da)
+        self._tr(p + "dcx_out", dx)
+        ops.gemm(dkv, mem, st.g(p + "ckv.w"), a_kmajor=False, b_kmajor=False,
+                 epilogue=ops.EPI_F32_ACCUM)
+        ops.colsum(dkv, st.g(p + "ckv.b"))
+        ops.gemm(dkv, st.w(p + "ckv.w"), dmem, b_kmajor=False, epilogue=ops.EPI_F32_ACCUM)
+        ops.gemm(dq, h, st.g(p + "cq.w"), a_kmajor=False, b_kmajor=False,
+                 epilogue=ops.EPI_F32_ACCUM)
+        ops.colsum(dq, st.g(p + "cq.b"))
+        dh = torch.empty(T, d, device=self.device)
+        ops.gemm(dq, st.w(p + "cq.w"), dh, b_kmajor=False, epilogue=ops.EPI_F32)
+        self._ln_bwd(st, p + "lnc", dh, x_in, mean, rstd, dx, dx_bf)
+
+    # ------------------------------------------------------------------ task
+    def forward_backward(self, task: TaskSpec, db: DeviceBatch, loss_sum: torch.Tensor) -> None:
+        """One micro-batch of one task; gradients accumulate into the buckets."""
+        shp, dev, d = self.shape, self.device, self.shape.d_model
+        ek, dk = embedding_keys(task)
+        emb_e, emb_d = self.states[ek], self.states[dk]
+        Ts, Tt = db.n_src, db.n_tgt
+        # ---- encoder
+        x = torch.empty(Ts, d, device=dev)
+        ops.embed_fwd(db.src, db.src_pos, emb_e.w("emb"), x, self.scale)
+        self._tr("emb_src", x)
+        enc_saved = []
+        for key in task.enc_modules:
+            st = self.states[key]
+            for i in range(st.layout.n_layers):
+                sv = []
+                x = self._self_block_fwd(st, f"l{i}.", x, db.cu_src, db.n_seq, db.max_src, False, sv)
+                self._tr(f"enc_l{i}_attn", x)
+                x = self._ffn_fwd(st, f"l{i}.", x, sv)
+                self._tr(f"enc_l{i}_ffn", x)
+                enc_saved.append((st, f"l{i}.", sv))
+        lnf_e = self.states[task.enc_modules[-1]]
+        mem, mem_mean, mem_rstd = self._ln(lnf_e, "lnf", x)
+        self._tr("x_enc", x)
+        self._tr("mem", mem)
+        x_enc = x
+        # ---- decoder
+        y = torch.empty(Tt, d, device=dev)
+        ops.embed_fwd(db.tgt_in, db.tgt_pos, emb_d.w("emb"), y, self.scale)
+        dec_saved = []
+        for key in task.dec_modules:
+            st = self.states[key]
+            for i in range(st.layout.n_layers):
+                sv = []
+                y = self._self_block_fwd(st, f"l{i}.", y, db.cu_tgt, db.n_seq, db.max_tgt, True, sv)
+                y = self._cross_block_fwd(st, f"l{i}.", y, mem, db, sv)
+                y = self._ffn_fwd(st, f"l{i}.", y, sv)
+                dec_saved.append((st, f"l{i}.", sv))
+        lnf_d = self.states[task.dec_modules[-1]]
+        hdec, hd_mean, hd_rstd = self._ln(lnf_d, "lnf", y)
+        self._tr("y_dec", y)
+        self._tr("hdec", hdec)
+        logits = torch.empty(Tt, shp.vocab, device=dev, dtype=torch.bfloat16)
+        ops.gemm(hdec, emb_d.w("gen.w"), logits, epilogue=ops.EPI_BF16, bias=emb_d.f32("gen.b"))
+        row_loss = torch.empty(Tt, device=dev)
+        self._tr("logits", logits)
+        ops.xent(logits, db.labels, logits, row_loss, 1.0 / Tt, loss_sum)  # dlogits in place
+        dlogits = logits
+        self._tr("dlogits", dlogits)
+        # ---- generator backward
+        ops.gemm(dlogits, hdec, emb_d.g("gen.w"), a_kmajor=False, b_kmajor=False,
+                 epilogue=ops.EPI_F32_ACCUM)
+        ops.colsum(dlogits, emb_d.g("gen.b"))
+        dh = torch.empty(Tt, d, device=dev)
+        ops.gemm(dlogits, emb_d.w("gen.w"), dh, b_kmajor=False, epilogue=ops.EPI_F32)
+        del logits, dlogits
+        dy = self._zeros(Tt, d)
+        dy_bf = torch.empty(Tt, d, device=dev, dtype=torch.bfloat16)
+        self._ln_bwd(lnf_d, "lnf", dh, y, hd_mean, hd_rstd, dy, dy_bf)
+        self._tr("dh", dh)
+        self._tr("dy_top", dy)
+        dmem = self._zeros(Ts, d)
+        for st, p, sv in reversed(dec_saved):
+            self._ffn_bwd(st, p, sv[2], dy, dy_bf)
+            self._cross_bwd(st, p, sv[1], dy, dy_bf, mem, dmem, db)
+            self._self_bwd(st, p, sv[0], dy, dy_bf, db.cu_tgt, db.n_seq, db.max_tgt, True)
+        self._tr("dy_bottom", dy)
+        self._tr("dmem", dmem)
+        ops.embed_bwd(db.tgt_in, dy, emb_d.g("emb"), self.scale)
+        # ---- encoder backward
+        dx = self._zeros(Ts, d)
+        dx_bf = torch.empty(Ts, d, device=dev, dtype=torch.bfloat16)
+        self._ln_bwd(lnf_e, "lnf", dmem, x_enc, mem_mean, mem_rstd, dx, dx_bf)
+        for st, p, sv in reversed(enc_saved):
+            self._ffn_bwd(st, p, sv[1], dx, dx_bf)
+            self._self_bwd(st, p, sv[0], dx, dx_bf, db.cu_src, db.n_seq, db.max_src, False)
+        self._tr("dx_bottom", dx)
+        ops.embed_bwd(db.src, dx, emb_e.g("emb"), self.scale)
+
+    # ------------------------------------------------------------------ step
+    def zero_grads(self) -> None:
+        """DeviceState.reset (syncsim.py:108-111): zero every hosted bucket."""
+        for st in self.states.values():
+            ops.memset(st.grad, 0)
+
+    def step(self, step_idx: int, batches: Sequence[DeviceBatch]) -> dict:
+        """One optimizer step: len(batches) micro-batches (accum_count), then
+        the Algorithm-1 exchange and the fused update.  Returns host-side
+        bookkeeping; the loss stays on device in ``self.loss_sum``."""
+        self.zero_grads()
+        ops.memset(self.loss_sum, 0)
+        used: set[ModuleKey] = set()
+        picked = []
+        for db in batches:
+            task = self.mux.pick(step_idx)
+            picked.append(task.id)
+            self.forward_backward(task, db, self.loss_sum)
+            used.update(task.modules())
+            used.update(embedding_keys(task))
+        flags = ready_flags(self.plan, self.rank, used)
+        if self.comm is not None:
+            self.flags_dev.copy_(torch.tensor(flags, dtype=torch.int32), non_blocking=True)
+            self.comm.ready_count(self.flags_dev, self.n_ready_dev)
+            counts = self.n_ready_dev.tolist()  # host needs n to post the right collectives
+        else:
+            counts = flags
+        self.exchange_and_update(counts)
+        return {"tasks": picked, "ready": dict(zip(self.plan.keys, counts))}
+
+    def exchange_and_update(self, counts: Sequence[int]) -> None:
+        items = []
+        if self.comm is not None:
+            for k in self.plan.keys:  # sorted ModuleKey = global issue order
+                g = tuple(self.plan.groups[k])
+                n = counts[self.index[k]]
+                if len(g) < 2 or n < 1 or k not in self.states:
+                    continue
+                grp = self.comm.by_set.get(g)
+                st = self.states[k]
+                items.append(_native.ReduceItem(group=grp, buf=st.grad.data_ptr(),
+                                                n_elems=st.grad.numel(), dtype=0))
+            self.comm.reduce(items)
+        self.fused_update(counts)
+
+    def fused_update(self, counts: Sequence[int]) -> None:
+        a = self.adam
+        mods = []
+        for k, st in self.states.items():
+            n = counts[self.index[k]]
+            if n < 1:
+                continue
+            st.step += 1
+            bc1 = 1.0 - a.beta1 ** st.step
+            bc2 = 1.0 - a.beta2 ** st.step
+            mods.append(_native.AdamModule(
+                grad=st.grad.data_ptr(), master=st.master.data_ptr(), exp_avg=st.exp_avg.data_ptr(),
+                exp_avg_sq=st.exp_avg_sq.data_ptr(), param_bf16=st.weights.data_ptr(),
+                n_elems=st.master.numel(), n_ready=n, ready_index=-1, step_size=a.lr / bc1,
+                inv_sqrt_bc2=1.0 / math.sqrt(bc2)))
+        if mods:
+            ops.fused_update(mods, _native.AdamHyper.make(beta1=a.beta1, beta2=a.beta2, eps=a.eps,
+                                                     weight_decay=a.weight_decay,
+                                                     inv_loss_scale=1.0))
+
+    def close(self) -> None:
+        if self.comm is not None:
+            self.comm.close()
+            self.comm = None

@@ -1,0 +1,191 @@
+"""Python wrappers over the C-ABI kernels of ``libmmb200.so``.
+
+PyTorch tensors are used only as device allocations: each wrapper checks
+device / dtype / contiguity, passes raw pointers and the current CUDA stream,
+and raises ``MMError`` on a non-zero status.  Nothing here computes on the
+host or falls back to a torch op.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import _native
+from ._native import check, lib
+
+EPI_BF16, EPI_BF16_RELU, EPI_F32, EPI_F32_ACCUM, EPI_F32_RESID, EPI_BF16_DRELU = range(6)
+
+
+class GemmArgs(ctypes.Structure):
+    _fields_ = [
+        ("a", ctypes.c_void_p), ("b", ctypes.c_void_p), ("d", ctypes.c_void_p),
+        ("bias", ctypes.c_void_p), ("resid", ctypes.c_void_p), ("aux", ctypes.c_void_p),
+        ("m", ctypes.c_int64), ("n", ctypes.c_int64), ("k", ctypes.c_int64),
+        ("lda", ctypes.c_int64), ("ldb", ctypes.c_int64), ("ldd", ctypes.c_int64),
+        ("a_kmajor", ctypes.c_int32), ("b_kmajor", ctypes.c_int32),
+        ("epilogue", ctypes.c_int32), ("pad", ctypes.c_int32),
+    ]
+
+
+class AttnArgs(ctypes.Structure):
+    _fields_ = [
+        ("q", ctypes.c_void_p), ("k", ctypes.c_void_p), ("v", ctypes.c_void_p),
+        ("o", ctypes.c_void_p), ("lse", ctypes.c_void_p), ("d_o", ctypes.c_void_p),
+        ("dq", ctypes.c_void_p), ("dk", ctypes.c_void_p), ("dv", ctypes.c_void_p),
+        ("cu_q", ctypes.c_void_p), ("cu_k", ctypes.c_void_p),
+        ("ldq", ctypes.c_int64), ("ldk", ctypes.c_int64), ("ldv", ctypes.c_int64),
+        ("ldo", ctypes.c_int64), ("ld_dq", ctypes.c_int64), ("ld_dk", ctypes.c_int64),
+        ("ld_dv", ctypes.c_int64),
+        ("n_seq", ctypes.c_int32), ("heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+        ("causal", ctypes.c_int32), ("max_q", ctypes.c_int32), ("max_k", ctypes.c_int32),
+        ("scale", ctypes.c_float), ("total_q", ctypes.c_int32),
+    ]
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _need(t: torch.Tensor, dtype, name: str) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+def _rowstride(t: torch.Tensor, name: str) -> int:
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError(f"{name} must be a 2-D row-major view")
+    return t.stride(0)
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bool = True,
+         b_kmajor: bool = True, epilogue: int = EPI_BF16, bias=None, resid=None, aux=None) -> None:
+    """d[M,N] (epilogue)= op(a) @ op(b)^T on tcgen05.
+
+    a: [M,K] if a_kmajor else [K,M]; b: [N,K] if b_kmajor else [K,N] (bf16).
+    """
+    _need(a, torch.bfloat16, "a")
+    _need(b, torch.bfloat16, "b")
+    m, k = (a.shape[0], a.shape[1]) if a_kmajor else (a.shape[1], a.shape[0])
+    n, kb = (b.shape[0], b.shape[1]) if b_kmajor else (b.shape[1], b.shape[0])
+    if k != kb:
+        raise ValueError(f"K mismatch {k} vs {kb}")
+    if tuple(d.shape) != (m, n):
+        raise ValueError(f"d shape {tuple(d.shape)} != {(m, n)}")
+    out_bf16 = epilogue in (EPI_BF16, EPI_BF16_RELU, EPI_BF16_DRELU)
+    _need(d, torch.bfloat16 if out_bf16 else torch.float32, "d")
+    args = GemmArgs(a=a.data_ptr(), b=b.data_ptr(), d=d.data_ptr(), bias=_ptr(bias),
+                    resid=_ptr(resid), aux=_ptr(aux), m=m, n=n, k=k,
+                    lda=_rowstride(a, "a"), ldb=_rowstride(b, "b"), ldd=_rowstride(d, "d"),
+                    a_kmajor=int(a_kmajor), b_kmajor=int(b_kmajor), epilogue=epilogue)
+    if resid is not None and _rowstride(resid, "resid") != args.ldd:
+        raise ValueError("resid must share d's row stride")
+    if aux is not None and _rowstride(aux, "aux") != args.ldd:
+        raise ValueError("aux must share d's row stride")
+    check(lib().mm_gemm(ctypes.byref(args), stream_ptr()), "mm_gemm")
+
+
+def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-6) -> None:
+    rows, cols = x.shape
+    check(lib().mm_layernorm_fwd(x.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
+                                 mean.data_ptr(), rstd.data_ptr(), rows, cols, eps,
+                                 stream_ptr()), "mm_layernorm_fwd")
+
+
+def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta) -> None:
+    rows, cols = x.shape
+    check(lib().mm_layernorm_bwd(dy.data_ptr(), x.data_ptr(), gamma.data_ptr(), mean.data_ptr(),
+                                 rstd.data_ptr(), dx.data_ptr(), _ptr(dx_bf16), dgamma.data_ptr(),
+                                 dbeta.data_ptr(), rows, cols, stream_ptr()), "mm_layernorm_bwd")
+
+
+def embed_fwd(ids, pos, table_bf16, out, scale) -> None:
+    rows, cols = out.shape
+    check(lib().mm_embed_fwd(ids.data_ptr(), pos.data_ptr(), table_bf16.data_ptr(), out.data_ptr(),
+                             rows, cols, scale, stream_ptr()), "mm_embed_fwd")
+
+
+def embed_bwd(ids, dout, dtable, scale) -> None:
+    rows, cols = dout.shape
+    check(lib().mm_embed_bwd(ids.data_ptr(), dout.data_ptr(), dtable.data_ptr(), rows, cols, scale,
+                             stream_ptr()), "mm_embed_bwd")
+
+
+def xent(logits, labels, dlogits, row_loss, grad_scale, loss_sum=None) -> None:
+    rows, vocab = logits.shape
+    check(lib().mm_xent_fwd_bwd(logits.data_ptr(), labels.data_ptr(), dlogits.data_ptr(),
+                                row_loss.data_ptr(), _ptr(loss_sum), rows, vocab, grad_scale,
+                                stream_ptr()), "mm_xent_fwd_bwd")
+
+
+def colsum(x, out) -> None:
+    rows, cols = x.shape
+    check(lib().mm_colsum_bf16(x.data_ptr(), out.data_ptr(), rows, cols, stream_ptr()),
+          "mm_colsum_bf16")
+
+
+def cast_bf16(x, y) -> None:
+    check(lib().mm_cast_f32_bf16(x.data_ptr(), y.data_ptr(), x.numel(), stream_ptr()),
+          "mm_cast_f32_bf16")
+
+
+def attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, heads, max_q, max_k, causal,
+                   d_o=None, dq=None, dk=None, dv=None) -> AttnArgs:
+    hd = 64
+    return AttnArgs(
+        q=q.data_ptr(), k=k.data_ptr(), v=v.data_ptr(), o=o.data_ptr(), lse=lse.data_ptr(),
+        d_o=_ptr(d_o), dq=_ptr(dq), dk=_ptr(dk), dv=_ptr(dv),
+        cu_q=cu_q.data_ptr(), cu_k=cu_k.data_ptr(),
+        ldq=q.stride(0), ldk=k.stride(0), ldv=v.stride(0), ldo=o.stride(0),
+        ld_dq=dq.stride(0) if dq is not None else 0, ld_dk=dk.stride(0) if dk is not None else 0,
+        ld_dv=dv.stride(0) if dv is not None else 0,
+        n_seq=n_seq, heads=heads, head_dim=hd, causal=int(causal), max_q=max_q, max_k=max_k,
+        scale=1.0 / math.sqrt(hd), total_q=q.shape[0])
+
+
+def attention_fwd(args: AttnArgs) -> None:
+    check(lib().mm_attention_fwd(ctypes.byref(args), stream_ptr()), "mm_attention_fwd")
+
+
+def attention_bwd(args: AttnArgs) -> None:
+    check(lib().mm_attention_bwd(ctypes.byref(args), stream_ptr()), "mm_attention_bwd")
+
+
+def flush_l2(scratch: torch.Tensor) -> None:
+    check(lib().mm_flush_l2(scratch.data_ptr(), scratch.numel() * scratch.element_size(),
+                            stream_ptr()), "mm_flush_l2")
+
+
+def memset(t: torch.Tensor, value: int = 0) -> None:
+    if not t.is_contiguous():
+        raise ValueError("memset needs a contiguous tensor")
+    check(lib().mm_memset(t.data_ptr(), value, t.numel() * t.element_size(), stream_ptr()),
+          "mm_memset")
+
+
+def axpy(y: torch.Tensor, x: torch.Tensor, alpha: float) -> None:
+    _need(y, torch.float32, "y")
+    _need(x, torch.float32, "x")
+    if y.numel() != x.numel() or not (y.is_contiguous() and x.is_contiguous()):
+        raise ValueError("axpy needs equal-size contiguous tensors")
+    check(lib().mm_axpy_f32(y.data_ptr(), x.data_ptr(), alpha, y.numel(), stream_ptr()),
+          "mm_axpy_f32")
+
+
+def sync_emulated(mods, only_ready: bool) -> None:
+    arr = (_native.SyncModule * len(mods))(*mods)
+    check(lib().mm_sync_emulated(arr, len(mods), int(only_ready), stream_ptr()),
+          "mm_sync_emulated")
+
+
+def fused_update(mods, hyper: "_native.AdamHyper", ready_dev=None) -> None:
+    arr = (_native.AdamModule * len(mods))(*mods)
+    check(lib().mm_fused_update(arr, len(mods), ctypes.byref(hyper), _ptr(ready_dev),
+                                stream_ptr()), "mm_fused_update")

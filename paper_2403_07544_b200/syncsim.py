@@ -1,0 +1,217 @@
+"""Drop-in for the hot-path names of ``mmtplan.syncsim`` on B200 buffers.
+
+* ``DeviceState`` / ``sync_step``: the literal Algorithm-1 exchange of
+  ``syncsim.py:90-153`` over devices whose buffers are CUDA fp32 tensors; the
+  whole exchange is ONE launch of the sm_100a kernel ``mm_sync_emulated``
+  (sum over each module's hosting devices in ascending index, ``/ n`` with n =
+  devices that used it, n == 0 untouched).  Results are bit-identical to the
+  reference's numpy on fp32 buffers.
+* ``multiplex``, ``Reservoir`` / ``reservoir_batch``,
+  ``ring_allreduce_time``, ``StepRecord`` / ``CommLedger``,
+  ``synthetic_uniform_tasks``: same semantics as syncsim.py:190-292, 409-458
+  (host-side bookkeeping; the ledger additionally carries measured times).
+
+The real training step (``run_benchmark``'s loop) is ``engine.Engine`` /
+``cluster.EmulatedCluster``.
+"""
+from __future__ import annotations
+
+import dataclasses
+import random
+from typing import Iterable, Mapping, Sequence
+
+import torch
+
+from . import _native, ops
+from .domain import ClusterTopology, ModuleKey, TaskSpec, task_id
+from .plan import SimulationError, multiplex  # noqa: F401  (re-exported API)
+from .sharing import ArchSpec, SharingPattern, build_module_sequence
+
+GRAD_BYTES_PER_PARAM = 4
+READY_ENTRY_BYTES = 4
+
+
+@dataclasses.dataclass
+class DeviceState:
+    """One device: hosted modules, a CUDA fp32 buffer per hosted module and
+    the set of modules used this step (syncsim.py:90-118)."""
+
+    index: int
+    hosted: frozenset
+    dim: int
+    buffers: dict = dataclasses.field(default_factory=dict)
+    used: set = dataclasses.field(default_factory=set)
+    device: str = "cuda"
+
+    def __post_init__(self) -> None:
+        if not self.buffers:
+            self.buffers = {k: torch.zeros(self.dim, self.dim, device=self.device)
+                            for k in sorted(self.hosted)}
+
+    def reset(self) -> None:
+        for buf in self.buffers.values():
+            ops.memset(buf, 0)
+        self.used.clear()
+
+    def accumulate(self, grads: Mapping[ModuleKey, torch.Tensor]) -> None:
+        for key, g in grads.items():
+            if key not in self.hosted:
+                raise SimulationError(f"gradient for unhosted module {key}")
+            buf = self.buffers[key]
+            if g.shape != buf.shape:
+                raise SimulationError(f"gradient shape {tuple(g.shape)} != {tuple(buf.shape)}")
+            ops.axpy(buf, g.to(buf.device, torch.float32).contiguous(), 1.0)
+            self.used.add(key)
+
+
+def sync_step(devices: Sequence[DeviceState], only_ready: bool = False) -> dict:
+    """Algorithm 1 over all devices (syncsim.py:121-153), one kernel launch.
+
+    ``only_ready=True`` skips reading the buffers of members that did not
+    use the module (exact when those buffers are zero, as after ``reset``).
+    """
+    ordered = sorted(devices, key=lambda d: d.index)
+    if len({d.index for d in ordered}) != len(ordered):
+        raise SimulationError("duplicate device index")
+    if len({d.dim for d in ordered}) > 1:
+        raise SimulationError("inconsistent module dimensions across devices")
+    keys = sorted(set().union(*(d.hosted for d in ordered))) if ordered else []
+    synced: dict = {}
+    table = []
+    for key in keys:
+        members = [d for d in ordered if key in d.hosted]
+        if len(members) > _native.MAX_GROUP:
+            raise SimulationError(f"module {key}: {len(members)} hosts > {_native.MAX_GROUP}")
+        ref = members[0].buffers[key]
+        for d in members:
+            b = d.buffers[key]
+            if b.dtype != torch.float32 or not b.is_cuda or not b.is_contiguous():
+                raise SimulationError("buffers must be contiguous CUDA fp32 tensors")
+            if b.shape != ref.shape:
+                raise SimulationError(f"module {key}: buffer shapes differ across devices")
+        out = torch.empty_like(ref)
+        synced[key] = out
+        m = _native.SyncModule()
+        for r, d in enumerate(members):
+            m.bufs[r] = d.buffers[key].data_ptr()
+        m.out = out.data_ptr()
+        m.n_elems = ref.numel()
+        m.group_size = len(members)
+        m.used_mask = sum(1 << r for r, d in enumerate(members) if key in d.used)
+        table.append(m)
+    if table:
+        ops.sync_emulated(table, only_ready)
+    return synced
+
+
+class Reservoir:
+    """Single-pass reservoir sample (syncsim.py:208-227)."""
+
+    def __init__(self, capacity: int, seed: int = 0):
+        if capacity < 1:
+            raise ValueError("capacity must be >= 1")
+        self.capacity = capacity
+        self._rng = random.Random(seed)
+        self._seen = 0
+        self.items: list = []
+
+    def add(self, item) -> None:
+        self._seen += 1
+        if len(self.items) < self.capacity:
+            self.items.append(item)
+            return
+        j = self._rng.randrange(self._seen)
+        if j < self.capacity:
+            self.items[j] = item
+
+
+def reservoir_batch(stream: Iterable, capacity: int, seed: int = 0) -> list:
+    res = Reservoir(capacity, seed)
+    for item in stream:
+        res.add(item)
+    return res.items
+
+
+def ring_allreduce_time(payload_bytes: float, group: int, alpha: float, beta: float) -> float:
+    """2(g-1) alpha + 2(g-1)/g * bytes / beta (syncsim.py:237-242)."""
+    if group < 2:
+        return 0.0
+    return 2 * (group - 1) * alpha + 2 * (group - 1) / group * payload_bytes / beta
+
+
+@dataclasses.dataclass
+class StepRecord:
+    step: int
+    ready_bytes: int
+    grad_bytes: int
+    comm_time: float
+    compute_time: float
+    tokens: int
+
+
+@dataclasses.dataclass
+class CommLedger:
+    """Per-step accounting (syncsim.py:245-292); times here are measured
+    (CUDA events), the byte columns follow the reference's definitions."""
+
+    records: list = dataclasses.field(default_factory=list)
+
+    @property
+    def total_tokens(self) -> int:
+        return sum(r.tokens for r in self.records)
+
+    @property
+    def total_time(self) -> float:
+        return sum(r.comm_time + r.compute_time for r in self.records)
+
+    @property
+    def total_grad_bytes(self) -> int:
+        return sum(r.grad_bytes for r in self.records)
+
+    @property
+    def total_ready_bytes(self) -> int:
+        return sum(r.ready_bytes for r in self.records)
+
+    @property
+    def comm_fraction(self) -> float:
+        t = self.total_time
+        return sum(r.comm_time for r in self.records) / t if t > 0 else 0.0
+
+    @property
+    def tokens_per_sec(self) -> float:
+        t = self.total_time
+        return self.total_tokens / t if t > 0 else 0.0
+
+    def to_tsv(self) -> str:
+        rows = ["step\tready_bytes\tgrad_bytes\tcomm_time\tcompute_time\ttokens"]
+        rows += [f"{r.step}\t{r.ready_bytes}\t{r.grad_bytes}\t{r.comm_time:.9e}"
+                 f"\t{r.compute_time:.9e}\t{r.tokens}" for r in self.records]
+        return "\n".join(rows) + "\n"
+
+
+SCALING_ARCHS = ("independent", "partially_shared", "fully_shared")
+
+
+def synthetic_uniform_tasks(arch_kind: str, n_gpus: int, topo: ClusterTopology) -> list[TaskSpec]:
+    """One self-pair task per GPU under the paper's three sharing schemes
+    (syncsim.py:412-458)."""
+    SP = SharingPattern
+    archs = {
+        "independent": ArchSpec(((SP.LANGUAGE, 6),), ((SP.LANGUAGE, 6),)),
+        "partially_shared": ArchSpec(((SP.LANGUAGE, 4), (SP.FULL, 4)), ((SP.LANGUAGE, 4),)),
+        "fully_shared": ArchSpec(((SP.FULL, 9),), ((SP.FULL, 4),)),
+    }
+    if arch_kind not in archs:
+        raise ValueError(f"unknown architecture kind: {arch_kind}")
+    devices = topo.devices()
+    if n_gpus > len(devices):
+        raise ValueError("more tasks than GPUs in topology")
+    out = []
+    for i in range(n_gpus):
+        lang = f"l{i:02d}"
+        enc, dec, el, dl = build_module_sequence(archs[arch_kind], lang, lang)
+        out.append(TaskSpec(id=task_id(lang, lang), src_lang=lang, tgt_lang=lang,
+                            src_path=f"synthetic/{lang}.src", tgt_path=f"synthetic/{lang}.tgt",
+                            enc_modules=enc, dec_modules=dec, enc_layers=el, dec_layers=dl,
+                            device=devices[i]))
+    return out

@@ -1,0 +1,222 @@
+"""Numerics of every CUDA kernel in libmmb200 against a plain PyTorch fp32
+reference of the same op (bf16 inputs upcast to fp32)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_err(got, ref):
+    got = got.float()
+    ref = ref.float()
+    return (got - ref).abs().max().item() / max(ref.abs().max().item(), 1e-30)
+
+
+GEMM_SHAPES = [(128, 128, 64), (256, 512, 512), (296, 200, 136), (4096, 1536, 512),
+               (1000, 2048, 512), (512, 512, 4096), (264, 32000, 512)]
+
+
+@pytest.mark.parametrize("shape", GEMM_SHAPES)
+@pytest.mark.parametrize("a_k,b_k", [(True, True), (True, False), (False, True), (False, False)])
+def test_gemm_majors_f32(cuda, shape, a_k, b_k):
+    from paper_2403_07544_b200 import ops
+    m, n, k = shape
+    g = torch.Generator(device="cuda").manual_seed(m * 7 + n * 3 + k)
+    A = torch.randn(m, k, device=cuda, generator=g).bfloat16()
+    B = torch.randn(n, k, device=cuda, generator=g).bfloat16()
+    a = A if a_k else A.t().contiguous()
+    b = B if b_k else B.t().contiguous()
+    d = torch.empty(m, n, device=cuda, dtype=torch.float32)
+    ops.gemm(a, b, d, a_kmajor=a_k, b_kmajor=b_k, epilogue=ops.EPI_F32)
+    ref = A.float() @ B.float().t()
+    assert rel_err(d, ref) < 2e-3
+
+
+@pytest.mark.parametrize("shape", [(4096, 512, 512), (333, 1536, 512), (4096, 2048, 512)])
+def test_gemm_epilogues(cuda, shape):
+    from paper_2403_07544_b200 import ops
+    m, n, k = shape
+    g = torch.Generator(device="cuda").manual_seed(1)
+    A = torch.randn(m, k, device=cuda, generator=g).bfloat16()
+    B = (torch.randn(n, k, device=cuda, generator=g) / math.sqrt(k)).bfloat16()
+    bias = torch.randn(n, device=cuda, generator=g)
+    ref = A.float() @ B.float().t() + bias
+    # bf16 + bias
+    d = torch.empty(m, n, device=cuda, dtype=torch.bfloat16)
+    ops.gemm(A, B, d, epilogue=ops.EPI_BF16, bias=bias)
+    assert rel_err(d, ref) < 1e-2
+    # bf16 relu
+    ops.gemm(A, B, d, epilogue=ops.EPI_BF16_RELU, bias=bias)
+    assert rel_err(d, ref.clamp_min(0)) < 1e-2
+    # fp32 residual add, in place
+    resid = torch.randn(m, n, device=cuda, generator=g)
+    out = resid.clone()
+    ops.gemm(A, B, out, epilogue=ops.EPI_F32_RESID, bias=bias, resid=out)
+    assert rel_err(out, resid + ref) < 2e-3
+    # relu-backward mask
+    aux = torch.randn(m, n, device=cuda, generator=g).bfloat16()
+    ops.gemm(A, B, d, epilogue=ops.EPI_BF16_DRELU, aux=aux)
+    assert rel_err(d, (ref - bias) * (aux.float() > 0)) < 1e-2
+
+
+@pytest.mark.parametrize("shape", [(512, 512, 4096), (1536, 512, 4111), (32000, 512, 2048),
+                                   (2048, 512, 300)])
+def test_gemm_wgrad_accumulate(cuda, shape):
+    """dW += dY^T X with both operands MN-major (split-K, fp32 atomics)."""
+    from paper_2403_07544_b200 import ops
+    n_out, n_in, t = shape
+    g = torch.Generator(device="cuda").manual_seed(5)
+    dy = torch.randn(t, n_out, device=cuda, generator=g).bfloat16()
+    x = torch.randn(t, n_in, device=cuda, generator=g).bfloat16()
+    dw = torch.randn(n_out, n_in, device=cuda, generator=g)
+    ref = dw + dy.float().t() @ x.float()
+    ops.gemm(dy, x, dw, a_kmajor=False, b_kmajor=False, epilogue=ops.EPI_F32_ACCUM)
+    assert rel_err(dw, ref) < 2e-3
+
+
+def test_layernorm(cuda):
+    from paper_2403_07544_b200 import ops
+    for cols in (512, 1024):
+        rows = 1031
+        g = torch.Generator(device="cuda").manual_seed(cols)
+        x = torch.randn(rows, cols, device=cuda, generator=g) * 3 + 1
+        gamma = torch.randn(cols, device=cuda, generator=g)
+        beta = torch.randn(cols, device=cuda, generator=g)
+        y = torch.empty(rows, cols, device=cuda, dtype=torch.bfloat16)
+        mean = torch.empty(rows, device=cuda)
+        rstd = torch.empty(rows, device=cuda)
+        ops.layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-6)
+        xr = x.clone().requires_grad_(True)
+        gr = gamma.clone().requires_grad_(True)
+        br = beta.clone().requires_grad_(True)
+        ref = torch.nn.functional.layer_norm(xr, (cols,), gr, br, eps=1e-6)
+        assert rel_err(y, ref) < 1e-2
+        dy = torch.randn(rows, cols, device=cuda, generator=g)
+        ref.backward(dy)
+        dx = torch.randn(rows, cols, device=cuda, generator=g)
+        dx0 = dx.clone()
+        dxb = torch.empty(rows, cols, device=cuda, dtype=torch.bfloat16)
+        dgamma = torch.zeros(cols, device=cuda)
+        dbeta = torch.zeros(cols, device=cuda)
+        ops.layernorm_bwd(dy, x, gamma, mean, rstd, dx, dxb, dgamma, dbeta)
+        assert rel_err(dx - dx0, xr.grad) < 1e-4
+        assert rel_err(dxb, dx) < 1e-2
+        assert rel_err(dgamma, gr.grad) < 1e-4
+        assert rel_err(dbeta, br.grad) < 1e-4
+
+
+def sinusoid(pos, d):
+    div = torch.exp(torch.arange(0, d, 2, dtype=torch.float32) * -(math.log(10000.0) / d))
+    pe = torch.zeros(len(pos), d)
+    pe[:, 0::2] = torch.sin(pos[:, None].float() * div)
+    pe[:, 1::2] = torch.cos(pos[:, None].float() * div)
+    return pe
+
+
+def test_embedding(cuda):
+    from paper_2403_07544_b200 import ops
+    rows, vocab, d = 2000, 1000, 512
+    g = torch.Generator().manual_seed(3)
+    ids = torch.randint(0, vocab, (rows,), generator=g, dtype=torch.int32)
+    ids[:300] = 7  # hot row
+    pos = torch.randint(0, 128, (rows,), generator=g, dtype=torch.int32)
+    table = torch.randn(vocab, d, generator=g).bfloat16()
+    out = torch.empty(rows, d, device=cuda)
+    scale = math.sqrt(d)
+    ops.embed_fwd(ids.cuda(), pos.cuda(), table.cuda(), out, scale)
+    ref = table.float()[ids.long()] * scale + sinusoid(pos, d)
+    assert rel_err(out.cpu(), ref) < 1e-5
+    dout = torch.randn(rows, d, generator=g)
+    dtable = torch.zeros(vocab, d, device=cuda)
+    ops.embed_bwd(ids.cuda(), dout.cuda(), dtable, scale)
+    ref_d = torch.zeros(vocab, d).index_add_(0, ids.long(), dout * scale)
+    assert rel_err(dtable.cpu(), ref_d) < 1e-5
+
+
+def test_cross_entropy(cuda):
+    from paper_2403_07544_b200 import ops
+    rows, vocab = 777, 32000
+    g = torch.Generator(device="cuda").manual_seed(9)
+    logits = (torch.randn(rows, vocab, device=cuda, generator=g) * 4).bfloat16()
+    labels = torch.randint(0, vocab, (rows,), device=cuda, generator=g, dtype=torch.int32)
+    labels[5] = -1
+    dl = torch.empty_like(logits)
+    loss = torch.empty(rows, device=cuda)
+    scale = 1.0 / 700
+    ops.xent(logits, labels, dl, loss, scale)
+    lf = logits.float().requires_grad_(True)
+    keep = labels >= 0
+    ref_rows = torch.nn.functional.cross_entropy(lf, labels.long().clamp_min(0), reduction="none")
+    ref_rows = ref_rows * keep
+    (ref_rows.sum() * scale).backward()
+    assert rel_err(loss, ref_rows) < 1e-5
+    assert rel_err(dl, lf.grad) < 1e-2
+    # in place
+    ops.xent(logits, labels, logits, loss, scale)
+    assert torch.equal(logits, dl)
+
+
+def ref_attention(q, k, v, cu_q, cu_k, heads, causal):
+    out = torch.zeros_like(q)
+    for s in range(len(cu_q) - 1):
+        qs, ks = slice(cu_q[s], cu_q[s + 1]), slice(cu_k[s], cu_k[s + 1])
+        for h in range(heads):
+            hs = slice(h * 64, (h + 1) * 64)
+            sc = q[qs, hs] @ k[ks, hs].t() / 8.0
+            if causal:
+                lq, lk = sc.shape
+                mask = torch.ones(lq, lk, dtype=torch.bool).triu(1)
+                sc = sc.masked_fill(mask, float("-inf"))
+            out[qs, hs] = torch.softmax(sc, -1) @ v[ks, hs]
+    return out
+
+
+@pytest.mark.parametrize("causal,maxlen", [(True, 128), (False, 128), (True, 256)])
+def test_attention(cuda, causal, maxlen):
+    from paper_2403_07544_b200 import ops
+    rng = np.random.default_rng(maxlen + causal)
+    heads, d = 8, 512
+    lq = rng.integers(1, maxlen + 1, size=13)
+    lk = lq.copy() if causal else rng.integers(1, maxlen + 1, size=13)
+    cu_q = np.concatenate([[0], np.cumsum(lq)]).astype(np.int32)
+    cu_k = np.concatenate([[0], np.cumsum(lk)]).astype(np.int32)
+    tq, tk = int(cu_q[-1]), int(cu_k[-1])
+    g = torch.Generator().manual_seed(0)
+    q = torch.randn(tq, d, generator=g).bfloat16().float()
+    k = torch.randn(tk, d, generator=g).bfloat16().float()
+    v = torch.randn(tk, d, generator=g).bfloat16().float()
+    qr, kr, vr = (t.clone().requires_grad_(True) for t in (q, k, v))
+    ref = ref_attention(qr, kr, vr, cu_q, cu_k, heads, causal)
+    do = torch.randn(tq, d, generator=g).bfloat16().float()
+    ref.backward(do)
+    qd, kd, vd = (t.bfloat16().cuda() for t in (q, k, v))
+    o = torch.empty(tq, d, device=cuda, dtype=torch.bfloat16)
+    lse = torch.empty(heads, tq, device=cuda)
+    cq, ck = torch.from_numpy(cu_q).cuda(), torch.from_numpy(cu_k).cuda()
+    dq = torch.empty_like(qd)
+    dk = torch.empty_like(kd)
+    dv = torch.empty_like(vd)
+    dod = do.bfloat16().cuda()
+    args = ops.attention_args(qd, kd, vd, o, lse, cq, ck, 13, heads, int(lq.max()), int(lk.max()),
+                              causal, d_o=dod, dq=dq, dk=dk, dv=dv)
+    ops.attention_fwd(args)
+    assert rel_err(o.cpu(), ref.detach()) < 1e-2
+    ops.attention_bwd(args)
+    assert rel_err(dq.cpu(), qr.grad) < 2e-2
+    assert rel_err(dk.cpu(), kr.grad) < 2e-2
+    assert rel_err(dv.cpu(), vr.grad) < 2e-2
+
+
+def test_colsum_and_cast(cuda):
+    from paper_2403_07544_b200 import ops
+    x = torch.randn(4097, 1536, device=cuda).bfloat16()
+    out = torch.ones(1536, device=cuda)
+    ops.colsum(x, out)
+    assert rel_err(out, 1 + x.float().sum(0)) < 1e-4
+    y = torch.randn(1000, 512, device=cuda)
+    yb = torch.empty(1000, 512, device=cuda, dtype=torch.bfloat16)
+    ops.cast_bf16(y, yb)
+    assert torch.equal(yb, y.bfloat16())
