@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 modular-training hot path (BASELINE.json metric).
+
+Default workload: config 3 (Transformer-base modular NMT, 8 languages, 56
+directions round-robin over the ranks, LANGUAGE(6)/LANGUAGE(6) modules,
+d=512, 8 heads, FFN 2048, 32000-word vocab per language, bf16 compute with
+fp32 master weights), 4096 target tokens per GPU per step, synthetic Zipf(1.1)
+ids and lognormal(3.0, 0.5) lengths clipped to [4, 128].  One step = the
+multiplexer's task for this rank, forward + backward through the sm_100a
+kernels, the Algorithm-1 exchange (ready counts, per-module-group NCCL sum,
+/ n) and the fused Adam update.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload train|reduce]
+
+For N > 1 the driver launches it under torchrun (one rank per GPU over NCCL).
+``--impl reference`` times the CPU restatement of the same step (oracle/,
+PyTorch-CPU fp32, all host threads) on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train tok/s at 1/2/4/8 B200; module-grad reduce GB/s vs NVLink peak"
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return {"hbm_gbs": p["hbm_gbs"], "bf16_tflops": p["bf16_tflops"],
+                "bf16_tflops_sustained": p.get("bf16_tflops_sustained", p["bf16_tflops"]),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.rows = []
+        if self.proc is None:
+            return False
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+        return False
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ---------------------------------------------------------------------------
+# CPU reference leg (oracle): the same step in PyTorch-CPU fp32
+
+
+def cpu_step_rate(workload, n_steps: int, threads: int, tokens: int = None):
+    """tokens/s of the oracle's fp32 CPU step on rank 0's task stream."""
+    import numpy as np
+    import torch
+    from oracle import transformer as OT
+    from paper_2403_07544_b200.data import ZipfIds, make_batch
+    from paper_2403_07544_b200.model import init_module, module_layouts
+    from paper_2403_07544_b200.plan import Multiplexer, build_plan, embedding_keys
+    torch.set_num_threads(threads)
+    plan = build_plan(workload.tasks, workload.topo)
+    layouts = module_layouts(plan, workload.shape)
+    mux = Multiplexer(plan, 0, seed=0)
+    rng = np.random.default_rng([0, 0])
+    ids = ZipfIds(workload.shape.vocab, workload.data.zipf_s)
+    spec = workload.data
+    if tokens is not None:
+        import dataclasses
+        spec = dataclasses.replace(spec, tokens_per_gpu=tokens)
+    masters, state = {}, {}
+    total_tok, total_t = 0, 0.0
+    for step in range(n_steps):
+        task = mux.pick(step)
+        batch = make_batch(rng, spec, workload.shape.vocab, ids=ids)
+        keys = list(task.modules()) + list(embedding_keys(task))
+        for k in keys:
+            if k not in masters:
+                masters[k] = init_module(layouts[k], workload.shape)
+                state[k] = [torch.from_numpy(masters[k]), torch.zeros(layouts[k].numel),
+                            torch.zeros(layouts[k].numel), 0]
+        t0 = time.perf_counter()
+        grads, used, losses = OT.local_grads([(task, batch)], {k: state[k][0].numpy() for k in keys},
+                                             layouts, workload.shape, embedding_keys)
+        for k in used:
+            st = state[k]
+            st[3] += 1
+            OT.adam_step(st[0], st[1], st[2], grads[k], st[3], 2e-4, 0.9, 0.998, 1e-8)
+        total_t += time.perf_counter() - t0
+        total_tok += batch.n_tgt
+    return total_tok / total_t, total_t / n_steps, spec.tokens_per_gpu
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2403_07544_b200 import configs
+    threads = os.cpu_count() or 1
+    wl = configs.config3(1)
+    if args.workload == "reduce":
+        rate, sample = reduce_cpu_rate(args.steps)
+        line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "GB/s",
+                "higher_is_better": True, "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "config2 module-grad reduce (CPU, oracle sync_step)"},
+                "cpu_baseline": {"value": rate, "unit": "GB/s", "cores": 1, "kind": "port",
+                                 "sample": sample},
+                "e2e": {"value": rate, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+    if args.warmup:
+        cpu_step_rate(wl, 1, threads)
+    rate, sec, tokens = cpu_step_rate(wl, max(1, args.steps), threads)
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "tok/s",
+            "higher_is_better": True, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": sec * 1e3, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (Zipf 1.1, lognormal 3.0/0.5)",
+            "config": {"workload": "config3 transformer-base modular NMT, 1 rank (CPU oracle)",
+                       "tokens_per_step": tokens},
+            "cpu_baseline": {"value": rate, "unit": "tok/s", "cores": threads, "kind": "port",
+                             "sample": f"{max(1, args.steps)} steps x {tokens} target tokens"},
+            "e2e": {"value": rate, "unit": "tok/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# module-gradient reduction (config 2) -- emulated ranks in one GPU's HBM
+
+
+def reduce_bytes(mods):
+    """Algorithmic bytes of the emulated exchange: read every ready member's
+    bucket once, write the mean into every member (fp32)."""
+    return sum(4 * m.n_params * (m.n_ready + m.group) for m in mods)
+
+
+def reduce_cpu_rate(n_steps, scale: float = 1 / 16):
+    """The oracle's numpy sync_step (1 core) on a scaled config-2 instance."""
+    import numpy as np
+    from oracle.algorithm1 import Dev, sync_step
+    from paper_2403_07544_b200.configs import reduce_microbench
+    rng, mods = reduce_microbench(lo=1e6 * scale, hi=64e6 * scale)
+    devs = []
+    for r in range(8):
+        hosted = frozenset(i for i, m in enumerate(mods) if r in m.ranks)
+        bufs = {i: (rng.standard_normal(m.n_params, dtype=np.float32) if m.ready[r - m.start]
+                    else np.zeros(m.n_params, np.float32)) for i, m in enumerate(mods) if r in m.ranks}
+        used = {i for i, m in enumerate(mods) if r in m.ranks and m.ready[r - m.start]}
+        devs.append(Dev(r, hosted, bufs, used))
+    t0 = time.perf_counter()
+    for _ in range(max(1, n_steps)):
+        sync_step(devs)
+    dt = (time.perf_counter() - t0) / max(1, n_steps)
+    return reduce_bytes(mods) / dt / 1e9, f"config-2 generator at 1/16 size ({sum(m.n_params for m in mods)/1e6:.1f}M params), numpy, 1 core"
+
+
+def run_reduce(args, pk):
+    import numpy as np
+    import torch
+    from paper_2403_07544_b200 import _native, ops
+    from paper_2403_07544_b200.configs import reduce_microbench
+    dev = torch.device("cuda:0")
+    rng, mods = reduce_microbench()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    bufs = {}
+    for r in range(8):
+        for i, m in enumerate(mods):
+            if r in m.ranks:
+                t = torch.empty(m.n_params, device=dev)
+                if m.ready[r - m.start]:
+                    t.normal_(generator=g)
+                else:
+                    ops.memset(t, 0)
+                bufs[(r, i)] = t
+    table = []
+    for i, m in enumerate(mods):
+        sm = _native.SyncModule()
+        for j in range(m.group):
+            sm.bufs[j] = bufs[(m.start + j, i)].data_ptr()
+        sm.out = None
+        sm.n_elems, sm.group_size = m.n_params, m.group
+        sm.used_mask = sum(1 << j for j, f in enumerate(m.ready) if f)
+        table.append(sm)
+    for _ in range(args.warmup):
+        ops.sync_emulated(table, True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            ops.sync_emulated(table, True)
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    nbytes = reduce_bytes(mods)
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "config2 module-grad reduce, 8 ranks emulated in one GPU",
+                       "params": sum(m.n_params for m in mods), "l2": "working set 7.7 GB > L2"},
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": gbs / pk["hbm_gbs"], "traffic": None},
+            "clocks": clk.summary(), "gpu_launches": args.steps}
+
+
+# ---------------------------------------------------------------------------
+# training step (configs 3-5)
+
+
+def run_train(args, pk):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2403_07544_b200 import configs, ops
+    from paper_2403_07544_b200.data import ZipfIds, make_batch
+    from paper_2403_07544_b200.engine import DeviceBatch, Trainer
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    store = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        store = dist.distributed_c10d._get_default_store()
+    wl = {"config3": configs.config3, "config5": configs.config5}[args.config](world)
+    trainer = Trainer(wl.tasks, wl.topo, wl.shape, rank=rank, world=world, device=dev, seed=0,
+                      store=store)
+    eng = trainer.engine
+    ids = ZipfIds(wl.shape.vocab, wl.data.zipf_s)
+    rng = np.random.default_rng([0, rank])
+    n_total = args.warmup + args.steps
+    host = [make_batch(rng, wl.data, wl.shape.vocab, ids=ids) for _ in range(n_total)]
+    dbs = [DeviceBatch(b, dev) for b in host]
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident inputs (value)
+    for s in range(args.warmup):
+        eng.step(s, [dbs[s]])
+    barrier()
+    launches0 = ops.LAUNCHES[0]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for s in range(args.warmup, n_total):
+            eng.step(s, [dbs[s]])
+        e1.record()
+        barrier()
+    launches = (ops.LAUNCHES[0] - launches0) // args.steps
+    ms = e0.elapsed_time(e1) / args.steps
+    tokens_local = sum(b.n_tgt for b in host[args.warmup:]) / args.steps
+    src_local = sum(b.n_src for b in host[args.warmup:]) / args.steps
+    t = torch.tensor([ms, tokens_local], device=dev, dtype=torch.float64)
+    if world > 1:
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms, tokens_all = float(mx[0]), float(sm[1])
+    else:
+        tokens_all = tokens_local
+    value = tokens_all / (ms * 1e-3)
+
+    # ---- GEMM roofline: one instrumented step (events around every GEMM)
+    ops.GEMM_PROFILE = []
+    eng.step(n_total, [dbs[-1]])
+    torch.cuda.synchronize()
+    prof = ops.GEMM_PROFILE
+    ops.GEMM_PROFILE = None
+    gemm_flops = sum(f for f, _, _ in prof)
+    gemm_ms = sum(a.elapsed_time(b) for _, a, b in prof)
+    gemm_tflops = gemm_flops / (gemm_ms * 1e-3) / 1e12
+
+    # ---- end to end through the public API (host batches, H2D + D2H inside)
+    rng2 = np.random.default_rng([1, rank])
+    host2 = [make_batch(rng2, wl.data, wl.shape.vocab, ids=ids) for _ in range(args.steps + 1)]
+    trainer.step_idx = n_total + 1
+    trainer.train_step([host2[0]])
+    barrier()
+    t0 = time.perf_counter()
+    h2d = 0
+    for b in host2[1:]:
+        trainer.train_step([b])
+        h2d += trainer.h2d_bytes
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    te = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = tokens_all / float(te[0])
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: Zipf(1.1) ids, lognormal lengths; random-init weights",
+        "config": {"workload": f"{args.config} modular NMT ({wl.shape.d_model}d, "
+                               f"{len(wl.tasks)} directions, {len(eng.plan.keys)} modules)",
+                   "global_batch": int(tokens_all), "tokens": "target tokens per step",
+                   "src_tokens_per_gpu": src_local, "parallelism": f"module-groups x{world}",
+                   "l2": "working set per step > 126 MB L2 (weights+activations ~1.5 GB); no flush"},
+        "roofline": {"bound": "tensor", "achieved": gemm_tflops,
+                     "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                     "frac": gemm_tflops / pk["bf16_tflops_sustained"], "traffic": None,
+                     "kernel": "gemm_tcgen05_kernel (all GEMM launches of one step)",
+                     "gemm_ms_per_step": gemm_ms, "gemm_share_of_step": gemm_ms / ms,
+                     "peak_source": pk["source"] + ", sustained"},
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_value, "unit": "tok/s", "h2d_bytes_per_step": h2d // args.steps,
+                "d2h_bytes_per_step": 4},
+        "gpu_launches": launches * args.steps,
+    }
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, sec, tok = cpu_step_rate(wl, 2, threads)
+        line["cpu_baseline"] = {"value": rate, "unit": "tok/s", "cores": threads, "kind": "port",
+                                "sample": f"2 steps x {tok} target tokens, PyTorch-CPU fp32 oracle"}
+    if rank == 0:
+        print(json.dumps(line))
+    trainer.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="train", choices=["train", "reduce"])
+    ap.add_argument("--config", default="config3", choices=["config3", "config5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    pk = peaks()
+    if args.workload == "reduce":
+        line = run_reduce(args, pk)
+        line["cpu_baseline"] = dict(zip(("value", "sample"), reduce_cpu_rate(3)), unit="GB/s",
+                                    cores=1, kind="port")
+        line["e2e"] = {"value": line["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0, "note": "device-resident microbench"}
+        print(json.dumps(line))
+        return 0
+    return run_train(args, pk)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

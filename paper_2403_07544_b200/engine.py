@@ -449,3 +449,44 @@ class Engine:
         if self.comm is not None:
             self.comm.close()
             self.comm = None
+
+
+class Trainer:
+    """Public entry point of the trainer step for one rank.
+
+    ``train_step(host_batches)`` takes this rank's micro-batches as host
+    ``data.Batch`` objects, stages them through a pinned buffer (one H2D copy
+    per micro-batch), runs forward / backward / Algorithm-1 exchange / fused
+    update and returns the step's loss (sum over micro-batches of the token
+    mean) read back to the host.
+    """
+
+    def __init__(self, tasks, topo, shape, rank: int = 0, world: int = 1, device=None,
+                 seed: int = 0, adam: AdamConfig = AdamConfig(), store=None,
+                 pinned_elems: int = 1 << 20):
+        self.engine = Engine(tasks, topo, shape, rank, world, device, seed, adam, store)
+        self.device = self.engine.device
+        self._pinned = [torch.empty(pinned_elems, dtype=torch.int32, pin_memory=True)
+                        for _ in range(4)]
+        self._loss_host = torch.empty(1, dtype=torch.float32, pin_memory=True)
+        self.step_idx = 0
+        self.h2d_bytes = 0
+        self.d2h_bytes = 4
+
+    def stage(self, batches) -> list:
+        out = []
+        for i, b in enumerate(batches):
+            out.append(DeviceBatch(b, self.device, pinned=self._pinned[i % len(self._pinned)]))
+        self.h2d_bytes = sum(d.h2d_bytes for d in out)
+        return out
+
+    def train_step(self, host_batches) -> float:
+        dbs = self.stage(host_batches)
+        self.engine.step(self.step_idx, dbs)
+        self.step_idx += 1
+        self._loss_host.copy_(self.engine.loss_sum, non_blocking=True)
+        torch.cuda.current_stream().synchronize()  # also retires the pinned staging
+        return float(self._loss_host[0])
+
+    def close(self) -> None:
+        self.engine.close()

@@ -44,6 +44,12 @@ class AttnArgs(ctypes.Structure):
     ]
 
 
+#: when a list, every GEMM launch appends (flops, start_event, end_event)
+GEMM_PROFILE = None
+#: launches issued through these wrappers (each wrapper = one kernel launch)
+LAUNCHES = [0]
+
+
 def stream_ptr() -> int:
     return torch.cuda.current_stream().cuda_stream
 
@@ -89,11 +95,20 @@ def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bool = 
         raise ValueError("resid must share d's row stride")
     if aux is not None and _rowstride(aux, "aux") != args.ldd:
         raise ValueError("aux must share d's row stride")
+    LAUNCHES[0] += 1
+    if GEMM_PROFILE is not None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        check(lib().mm_gemm(ctypes.byref(args), stream_ptr()), "mm_gemm")
+        e1.record()
+        GEMM_PROFILE.append((2.0 * m * n * k, e0, e1))
+        return
     check(lib().mm_gemm(ctypes.byref(args), stream_ptr()), "mm_gemm")
 
 
 def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-6) -> None:
     rows, cols = x.shape
+    LAUNCHES[0] += 1
     check(lib().mm_layernorm_fwd(x.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
                                  mean.data_ptr(), rstd.data_ptr(), rows, cols, eps,
                                  stream_ptr()), "mm_layernorm_fwd")
@@ -101,6 +116,7 @@ def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-6) -> None:
 
 def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta) -> None:
     rows, cols = x.shape
+    LAUNCHES[0] += 1
     check(lib().mm_layernorm_bwd(dy.data_ptr(), x.data_ptr(), gamma.data_ptr(), mean.data_ptr(),
                                  rstd.data_ptr(), dx.data_ptr(), _ptr(dx_bf16), dgamma.data_ptr(),
                                  dbeta.data_ptr(), rows, cols, stream_ptr()), "mm_layernorm_bwd")
@@ -108,18 +124,21 @@ def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta) -> None:
 
 def embed_fwd(ids, pos, table_bf16, out, scale) -> None:
     rows, cols = out.shape
+    LAUNCHES[0] += 1
     check(lib().mm_embed_fwd(ids.data_ptr(), pos.data_ptr(), table_bf16.data_ptr(), out.data_ptr(),
                              rows, cols, scale, stream_ptr()), "mm_embed_fwd")
 
 
 def embed_bwd(ids, dout, dtable, scale) -> None:
     rows, cols = dout.shape
+    LAUNCHES[0] += 1
     check(lib().mm_embed_bwd(ids.data_ptr(), dout.data_ptr(), dtable.data_ptr(), rows, cols, scale,
                              stream_ptr()), "mm_embed_bwd")
 
 
 def xent(logits, labels, dlogits, row_loss, grad_scale, loss_sum=None) -> None:
     rows, vocab = logits.shape
+    LAUNCHES[0] += 1
     check(lib().mm_xent_fwd_bwd(logits.data_ptr(), labels.data_ptr(), dlogits.data_ptr(),
                                 row_loss.data_ptr(), _ptr(loss_sum), rows, vocab, grad_scale,
                                 stream_ptr()), "mm_xent_fwd_bwd")
@@ -127,11 +146,13 @@ def xent(logits, labels, dlogits, row_loss, grad_scale, loss_sum=None) -> None:
 
 def colsum(x, out) -> None:
     rows, cols = x.shape
+    LAUNCHES[0] += 1
     check(lib().mm_colsum_bf16(x.data_ptr(), out.data_ptr(), rows, cols, stream_ptr()),
           "mm_colsum_bf16")
 
 
 def cast_bf16(x, y) -> None:
+    LAUNCHES[0] += 1
     check(lib().mm_cast_f32_bf16(x.data_ptr(), y.data_ptr(), x.numel(), stream_ptr()),
           "mm_cast_f32_bf16")
 
@@ -151,10 +172,12 @@ def attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, heads, max_q, max_k, caus
 
 
 def attention_fwd(args: AttnArgs) -> None:
+    LAUNCHES[0] += 1
     check(lib().mm_attention_fwd(ctypes.byref(args), stream_ptr()), "mm_attention_fwd")
 
 
 def attention_bwd(args: AttnArgs) -> None:
+    LAUNCHES[0] += 1
     check(lib().mm_attention_bwd(ctypes.byref(args), stream_ptr()), "mm_attention_bwd")
 
 
@@ -175,17 +198,20 @@ def axpy(y: torch.Tensor, x: torch.Tensor, alpha: float) -> None:
     _need(x, torch.float32, "x")
     if y.numel() != x.numel() or not (y.is_contiguous() and x.is_contiguous()):
         raise ValueError("axpy needs equal-size contiguous tensors")
+    LAUNCHES[0] += 1
     check(lib().mm_axpy_f32(y.data_ptr(), x.data_ptr(), alpha, y.numel(), stream_ptr()),
           "mm_axpy_f32")
 
 
 def sync_emulated(mods, only_ready: bool) -> None:
     arr = (_native.SyncModule * len(mods))(*mods)
+    LAUNCHES[0] += 1
     check(lib().mm_sync_emulated(arr, len(mods), int(only_ready), stream_ptr()),
           "mm_sync_emulated")
 
 
 def fused_update(mods, hyper: "_native.AdamHyper", ready_dev=None) -> None:
     arr = (_native.AdamModule * len(mods))(*mods)
+    LAUNCHES[0] += 1
     check(lib().mm_fused_update(arr, len(mods), ctypes.byref(hyper), _ptr(ready_dev),
                                 stream_ptr()), "mm_fused_update")
