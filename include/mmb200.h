@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 4
+#define MMB200_ABI_VERSION 5
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 
 int mm_abi_version(void);
@@ -169,7 +169,12 @@ int mm_embed_fwd(const int32_t* ids, const int32_t* pos, const uint16_t* table, 
 int mm_embed_bwd(const int32_t* ids, const float* dout, float* dtable, int64_t rows, int cols,
                  float scale, void* stream);
 
-/* K5: packed varlen multi-head attention (bf16 in/out, fp32 softmax). */
+/* K5: packed varlen multi-head attention (bf16 in/out, fp32 softmax).
+ * Work is split into CTA groups of consecutive sequences: groups[2g] = first
+ * sequence, groups[2g+1] = count; every sequence occupies ceil(len/32)*32
+ * rows of the group's shared-memory tile and the per-group footprint is at
+ * most `cap` rows on each of the query and key sides (host-built, see
+ * data.attention_groups). */
 typedef struct {
     const uint16_t* q; const uint16_t* k; const uint16_t* v; /* [tokens, ld*] */
     uint16_t* o;                                              /* [tq, ldo] */
@@ -182,6 +187,9 @@ typedef struct {
     int32_t max_q, max_k;
     float scale;
     int32_t total_q;
+    const int32_t* groups; /* [2 * n_groups] */
+    int32_t n_groups;
+    int32_t cap;
 } mm_attn_args;
 
 int mm_attention_fwd(const mm_attn_args* a, void* stream);

@@ -182,7 +182,7 @@ def local_grads(tasks_and_batches, masters: dict, layouts: dict, shape, emb_keys
         ek = emb_keys_fn(task)
         loss = task_loss(task, batch, flats, layouts, shape, ek, bf16)
         loss.backward()
-        losses.append(float(loss))
+        losses.append(float(loss.detach()))
         used.update(task.modules())
         used.update(ek)
     grads = {k: (f.grad.detach().clone() if f.grad is not None else torch.zeros_like(f))

@@ -15,7 +15,7 @@ from typing import Sequence
 from . import _native, ops
 from .domain import ModuleKey
 from .engine import DeviceBatch, Engine
-from .plan import embedding_keys, ready_counts_all
+from .plan import ready_counts_all, task_modules
 
 
 class EmulatedCluster:
@@ -32,16 +32,16 @@ class EmulatedCluster:
         for r, eng in enumerate(self.ranks):
             if r not in self.plan.tasks_by_rank:
                 continue
-            eng.zero_grads()
             ops.memset(eng.loss_sum, 0)
             used: set[ModuleKey] = set()
             picks[r] = []
             for db in batches[r]:
                 task = eng.mux.pick(step_idx)
                 picks[r].append(task.id)
+                fresh = [k for k in task_modules(task) if k not in used]
+                eng.zero_grads(fresh)
+                used.update(fresh)
                 eng.forward_backward(task, db, eng.loss_sum)
-                used.update(task.modules())
-                used.update(embedding_keys(task))
             used_by_rank[r] = used
         counts = ready_counts_all(self.plan, used_by_rank)
         table = []

@@ -1,11 +1,24 @@
-// K5: packed varlen multi-head attention for short NMT sentences (lengths
-// 4..256), head_dim 64.  One CTA per (sequence, head); the sequence's K / V
-// (and Q / dO in backward) are staged in shared memory as bf16 pairs with a
-// 33-word row pitch so lane-parallel row accesses are bank-conflict free.
-// Softmax statistics are fp32; the forward saves the natural-log LSE per
-// (head, query) for the backward's recomputation.  Attention is <1 % of the
-// step's FLOPs at these lengths, so this kernel is sized for
-// latency (thousands of small CTAs), not for the tensor pipe.
+// K5: packed varlen multi-head attention on tensor cores for short NMT
+// sentences (lengths up to 256), head_dim 64, bf16 in / out, fp32 softmax.
+//
+// Warp-level bf16 MMA (mma.sync m16n8k16, fp32 accumulate) with ldmatrix
+// fragment loads from padded shared memory (72-element pitch: conflict-free
+// 16-byte rows).  Attention is ~1 % of the step's FLOPs at these lengths
+// (SURVEY §2.3 K5): the kernels are sized for latency -- whole sequences
+// resident in smem, thousands of small CTAs -- not for the tcgen05 pipe.
+//
+// Work unit: CTA = (group of consecutive sequences, head).  The host packs
+// short sentences so one CTA's tile holds up to `cap` rows per side; every
+// sequence sits at a 32-row-aligned, zero-padded offset, and warps take
+// 16-row tiles of any sequence in the group round-robin.
+// forward : per query tile, online softmax over 32-key blocks (exp2 domain),
+//           O normalised once, natural-log LSE saved per (head, query).
+// backward: phase A (query tiles): D_i = sum_j p_ij dp_ij in fp32 (exact --
+//           not from the bf16-rounded O), then dQ = scale * dS K;
+//           phase B (key tiles): dV = P^T dO, dK = scale * dS^T Q,
+//           recomputing P / dP transposed.
+// Probabilities and dS enter the second MMA as a bf16 hi + lo pair (two MMAs),
+// so the products keep ~16 mantissa bits instead of bf16's 8.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -14,190 +27,423 @@
 
 namespace {
 
-constexpr int kHd = 64;       // head dim
-constexpr int kWords = 32;    // bf16 pairs per head row
-constexpr int kPitch = 33;    // padded smem row pitch (words)
-constexpr int kWarps = 4;
+constexpr int kHd = 64;
+constexpr int kP = 72;  // smem row pitch (bf16 elements)
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
 
-__device__ __forceinline__ float2 unpack(uint32_t w) {
-    return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const uint16_t* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const uint16_t* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void mma(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                    uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 __device__ __forceinline__ uint32_t pack(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
 }
-__device__ __forceinline__ float dot_row(const uint32_t* a, const uint32_t* b) {
-    float s = 0.f;
-#pragma unroll
-    for (int w = 0; w < kWords; ++w) {
-        const float2 x = unpack(a[w]), y = unpack(b[w]);
-        s = fmaf(x.x, y.x, s);
-        s = fmaf(x.y, y.y, s);
-    }
-    return s;
+__device__ __forceinline__ float quad_max(float v) {
+    v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 1));
+    return fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 2));
 }
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
+__device__ __forceinline__ float quad_sum(float v) {
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    return v + __shfl_xor_sync(0xffffffffu, v, 2);
 }
 
-// rows [0, n) of a head slice -> smem with pitch kPitch (words)
-__device__ __forceinline__ void stage(uint32_t* dst, const uint16_t* src, int64_t ld, int n) {
-    for (int idx = threadIdx.x; idx < n * kWords; idx += blockDim.x) {
-        const int r = idx / kWords, w = idx % kWords;
-        dst[r * kPitch + w] = reinterpret_cast<const uint32_t*>(src + r * ld)[w];
+// rows [0, n) of a 64-wide head slice -> smem (pitch kP), rows [n, npad) zeroed
+__device__ __forceinline__ void stage(uint16_t* dst, const uint16_t* src, int64_t ld, int n,
+                                      int npad, int tid, int nthr) {
+    for (int idx = tid; idx < npad * 8; idx += nthr) {
+        const int r = idx >> 3, c = idx & 7;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (r < n) v = *reinterpret_cast<const uint4*>(src + r * ld + c * 8);
+        *reinterpret_cast<uint4*>(dst + r * kP + c * 8) = v;
     }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) attn_fwd_kernel(const mm_attn_args a) {
-    extern __shared__ uint32_t sm[];
-    const int seq = blockIdx.x, h = blockIdx.y;
-    const int q0 = a.cu_q[seq], lq = a.cu_q[seq + 1] - q0;
-    const int k0 = a.cu_k[seq], lk = a.cu_k[seq + 1] - k0;
-    uint32_t* Ks = sm;
-    uint32_t* Vs = Ks + a.max_k * kPitch;
-    uint32_t* Qs = Vs + a.max_k * kPitch;             // per-warp query row
-    float* Ps = reinterpret_cast<float*>(Qs + kWarps * kWords);  // per-warp probs
-    stage(Ks, a.k + int64_t(k0) * a.ldk + h * kHd, a.ldk, lk);
-    stage(Vs, a.v + int64_t(k0) * a.ldv + h * kHd, a.ldv, lk);
+// A fragments (16 rows x 64 cols, 4 k-steps) of a row-major smem tile
+__device__ __forceinline__ void load_a(uint32_t (&f)[4][4], const uint16_t* base, int lane) {
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+        ldsm_x4(f[kk], base + (lane & 15) * kP + kk * 16 + (lane >> 4) * 8);
+}
+
+// acc[nt] (+)= A(16x64) * B^T where B rows n0..n0+31 (row-major [n][k], k = 64)
+__device__ __forceinline__ void mma_abt(float (&acc)[4][4], const uint32_t (&a)[4][4],
+                                        const uint16_t* b, int n0, int lane) {
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+        for (int kk2 = 0; kk2 < 2; ++kk2) {
+            uint32_t r[4];
+            ldsm_x4(r, b + (n0 + nt * 8 + (lane & 7)) * kP + kk2 * 32 + (lane >> 3) * 8);
+            mma(acc[nt], a[2 * kk2], r[0], r[1]);
+            mma(acc[nt], a[2 * kk2 + 1], r[2], r[3]);
+        }
+    }
+}
+
+// out[8][4] (+)= P(16 x 32, fp32 accumulators -> bf16 A fragments) * B where
+// B rows k0..k0+31 are row-major [k][n] (n = 64): ldmatrix.trans fragments
+__device__ __forceinline__ void mma_pb(float (&out)[8][4], const float (&p)[4][4],
+                                       const uint16_t* b, int k0, int lane) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const float v[8] = {p[2 * j][0], p[2 * j][1], p[2 * j][2], p[2 * j][3],
+                            p[2 * j + 1][0], p[2 * j + 1][1], p[2 * j + 1][2], p[2 * j + 1][3]};
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            hi[i] = pack(v[2 * i], v[2 * i + 1]);
+            const float h0 = __uint_as_float(hi[i] << 16), h1 = __uint_as_float(hi[i] & 0xffff0000u);
+            lo[i] = pack(v[2 * i] - h0, v[2 * i + 1] - h1);
+        }
+#pragma unroll
+        for (int np = 0; np < 4; ++np) {
+            uint32_t r[4];
+            ldsm_x4_t(r, b + (k0 + j * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * kP + np * 16 +
+                             (lane >> 4) * 8);
+            mma(out[2 * np], hi, r[0], r[1]);
+            mma(out[2 * np + 1], hi, r[2], r[3]);
+            mma(out[2 * np], lo, r[0], r[1]);
+            mma(out[2 * np + 1], lo, r[2], r[3]);
+        }
+    }
+}
+
+__device__ __forceinline__ void zero(float (&x)[4][4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i][0] = x[i][1] = x[i][2] = x[i][3] = 0.f;
+}
+
+// ---------------------------------------------------------------------------
+constexpr int kMaxSeqPerGroup = 16;
+
+struct Group {
+    int n;                       // sequences in the group
+    int q0[kMaxSeqPerGroup], lq[kMaxSeqPerGroup], qoff[kMaxSeqPerGroup];
+    int k0[kMaxSeqPerGroup], lk[kMaxSeqPerGroup], koff[kMaxSeqPerGroup];
+};
+
+__device__ __forceinline__ void load_group(Group& G, const mm_attn_args& a) {
+    const int first = a.groups[2 * blockIdx.x], n = a.groups[2 * blockIdx.x + 1];
+    G.n = n;
+    int qo = 0, ko = 0;
+    for (int i = 0; i < n; ++i) {
+        const int sq = first + i;
+        G.q0[i] = a.cu_q[sq];
+        G.lq[i] = a.cu_q[sq + 1] - G.q0[i];
+        G.k0[i] = a.cu_k[sq];
+        G.lk[i] = a.cu_k[sq + 1] - G.k0[i];
+        G.qoff[i] = qo;
+        G.koff[i] = ko;
+        qo += (G.lq[i] + 31) & ~31;
+        ko += (G.lk[i] + 31) & ~31;
+    }
+}
+
+// tile -> (sequence, 16-row tile start); tiles enumerate the group's
+// sequences in order (lens = G.lq for query tiles, G.lk for key tiles)
+__device__ __forceinline__ bool tile_of(const Group& G, const int* lens, int tile, int& s,
+                                        int& r0) {
+    for (s = 0; s < G.n; ++s) {
+        const int nt = (lens[s] + 15) >> 4;
+        if (tile < nt) {
+            r0 = tile * 16;
+            return true;
+        }
+        tile -= nt;
+    }
+    return false;
+}
+
+__device__ __forceinline__ int n_tiles(const Group& G, const int* lens) {
+    int t = 0;
+    for (int s = 0; s < G.n; ++s) t += (lens[s] + 15) >> 4;
+    return t;
+}
+
+__device__ void stage_group(uint16_t* Qs, uint16_t* Ks, uint16_t* Vs, uint16_t* dOs,
+                            const Group& G, const mm_attn_args& a, int h, int nthr) {
+    for (int i = 0; i < G.n; ++i) {
+        const int pq = (G.lq[i] + 31) & ~31, pk = (G.lk[i] + 31) & ~31;
+        if (Qs) stage(Qs + G.qoff[i] * kP, a.q + int64_t(G.q0[i]) * a.ldq + h * kHd, a.ldq, G.lq[i], pq, threadIdx.x, nthr);
+        if (dOs) stage(dOs + G.qoff[i] * kP, a.d_o + int64_t(G.q0[i]) * a.ldo + h * kHd, a.ldo, G.lq[i], pq, threadIdx.x, nthr);
+        stage(Ks + G.koff[i] * kP, a.k + int64_t(G.k0[i]) * a.ldk + h * kHd, a.ldk, G.lk[i], pk, threadIdx.x, nthr);
+        stage(Vs + G.koff[i] * kP, a.v + int64_t(G.k0[i]) * a.ldv + h * kHd, a.ldv, G.lk[i], pk, threadIdx.x, nthr);
+    }
+}
+
+constexpr int kFwdWarps = 4;
+
+__global__ void __launch_bounds__(kFwdWarps * 32) attn_fwd_kernel(const mm_attn_args a) {
+    extern __shared__ __align__(16) uint16_t sm[];
+    __shared__ Group G;
+    const int h = blockIdx.y;
+    if (threadIdx.x == 0) load_group(G, a);
+    __syncthreads();
+    uint16_t* Qs = sm;
+    uint16_t* Ks = Qs + a.cap * kP;
+    uint16_t* Vs = Ks + a.cap * kP;
+    stage_group(Qs, Ks, Vs, nullptr, G, a, h, kFwdWarps * 32);
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t* qrow = Qs + warp * kWords;
-    float* P = Ps + warp * a.max_k;
-    for (int i = warp; i < lq; i += kWarps) {
-        qrow[lane] = reinterpret_cast<const uint32_t*>(a.q + int64_t(q0 + i) * a.ldq + h * kHd)[lane];
-        __syncwarp();
-        const int kend = a.causal ? min(lk, i + 1) : lk;
-        float mx = -INFINITY;
-        for (int j = lane; j < kend; j += 32) {
-            const float s = dot_row(qrow, Ks + j * kPitch) * a.scale;
-            P[j] = s;
-            mx = fmaxf(mx, s);
+    const int g = lane >> 2, t = lane & 3;
+    const float c = a.scale * kLog2e;
+    const int ntiles = n_tiles(G, G.lq);
+    for (int tile = warp; tile < ntiles; tile += kFwdWarps) {
+        int sidx, r0;
+        tile_of(G, G.lq, tile, sidx, r0);
+        const int lq = G.lq[sidx], lk = G.lk[sidx], q0 = G.q0[sidx];
+        const uint16_t* Kseq = Ks + G.koff[sidx] * kP;
+        const uint16_t* Vseq = Vs + G.koff[sidx] * kP;
+        uint32_t qf[4][4];
+        load_a(qf, Qs + (G.qoff[sidx] + r0) * kP, lane);
+        const int row0 = r0 + g, row1 = row0 + 8;
+        const int kend = a.causal ? min(lk, r0 + 16) : lk;
+        float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+        float o[8][4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+        for (int kb = 0; kb < kend; kb += 32) {
+            float s[4][4];
+            zero(s);
+            mma_abt(s, qf, Kseq, kb, lane);
+            float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int key = kb + nt * 8 + 2 * t + (e & 1);
+                    const int row = e < 2 ? row0 : row1;
+                    float v = s[nt][e] * c;
+                    if (key >= lk || (a.causal && key > row)) v = -INFINITY;
+                    s[nt][e] = v;
+                    mx[e >> 1] = fmaxf(mx[e >> 1], v);
+                }
+            float corr[2], mref[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const float mn = fmaxf(m[i], quad_max(mx[i]));
+                mref[i] = mn == -INFINITY ? 0.f : mn;
+                corr[i] = exp2f(m[i] - mref[i]);  // m = -inf -> 0
+                m[i] = mn;
+            }
+            float sum[2] = {0.f, 0.f};
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float p = exp2f(s[nt][e] - mref[e >> 1]);
+                    s[nt][e] = p;
+                    sum[e >> 1] += p;
+                }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                o[i][0] *= corr[0]; o[i][1] *= corr[0];
+                o[i][2] *= corr[1]; o[i][3] *= corr[1];
+            }
+            l[0] = l[0] * corr[0] + sum[0];
+            l[1] = l[1] * corr[1] + sum[1];
+            mma_pb(o, s, Vseq, kb, lane);
         }
-        mx = warp_max(mx);
-        float sum = 0.f;
-        for (int j = lane; j < kend; j += 32) {
-            const float e = __expf(P[j] - mx);
-            P[j] = e;
-            sum += e;
+        l[0] = quad_sum(l[0]);
+        l[1] = quad_sum(l[1]);
+        const float inv0 = 1.f / l[0], inv1 = 1.f / l[1];
+        uint16_t* out0 = a.o + int64_t(q0 + row0) * a.ldo + h * kHd;
+        uint16_t* out1 = a.o + int64_t(q0 + row1) * a.ldo + h * kHd;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+            if (row0 < lq)
+                *reinterpret_cast<uint32_t*>(out0 + nt * 8 + 2 * t) = pack(o[nt][0] * inv0, o[nt][1] * inv0);
+            if (row1 < lq)
+                *reinterpret_cast<uint32_t*>(out1 + nt * 8 + 2 * t) = pack(o[nt][2] * inv1, o[nt][3] * inv1);
         }
-        sum = warp_sum(sum);
-        __syncwarp();
-        float ox = 0.f, oy = 0.f;
-        for (int j = 0; j < kend; ++j) {
-            const float2 v = unpack(Vs[j * kPitch + lane]);
-            ox = fmaf(P[j], v.x, ox);
-            oy = fmaf(P[j], v.y, oy);
+        if (t == 0) {
+            if (row0 < lq) a.lse[int64_t(h) * a.total_q + q0 + row0] = (m[0] + log2f(l[0])) * kLn2;
+            if (row1 < lq) a.lse[int64_t(h) * a.total_q + q0 + row1] = (m[1] + log2f(l[1])) * kLn2;
         }
-        const float inv = 1.f / sum;
-        reinterpret_cast<uint32_t*>(a.o + int64_t(q0 + i) * a.ldo + h * kHd)[lane] =
-            pack(ox * inv, oy * inv);
-        if (lane == 0) a.lse[int64_t(h) * a.total_q + q0 + i] = mx + __logf(sum);
-        __syncwarp();
     }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) attn_bwd_kernel(const mm_attn_args a) {
-    extern __shared__ uint32_t sm[];
-    const int seq = blockIdx.x, h = blockIdx.y;
-    const int q0 = a.cu_q[seq], lq = a.cu_q[seq + 1] - q0;
-    const int k0 = a.cu_k[seq], lk = a.cu_k[seq + 1] - k0;
-    const int mrow = max(a.max_q, a.max_k);
-    uint32_t* Qs = sm;
-    uint32_t* dOs = Qs + a.max_q * kPitch;
-    uint32_t* Ks = dOs + a.max_q * kPitch;
-    uint32_t* Vs = Ks + a.max_k * kPitch;
-    float* lse = reinterpret_cast<float*>(Vs + a.max_k * kPitch);
-    float* Dd = lse + a.max_q;
-    float* Pw = Dd + a.max_q;            // per warp: P then DS, mrow each
-    stage(Qs, a.q + int64_t(q0) * a.ldq + h * kHd, a.ldq, lq);
-    stage(dOs, a.d_o + int64_t(q0) * a.ldo + h * kHd, a.ldo, lq);
-    stage(Ks, a.k + int64_t(k0) * a.ldk + h * kHd, a.ldk, lk);
-    stage(Vs, a.v + int64_t(k0) * a.ldv + h * kHd, a.ldv, lk);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < lq; i += blockDim.x) lse[i] = a.lse[int64_t(h) * a.total_q + q0 + i];
+// ---------------------------------------------------------------------------
+constexpr int kBwdWarps = 8;
+
+__global__ void __launch_bounds__(kBwdWarps * 32) attn_bwd_kernel(const mm_attn_args a) {
+    extern __shared__ __align__(16) uint16_t sm[];
+    __shared__ Group G;
+    const int h = blockIdx.y;
+    if (threadIdx.x == 0) load_group(G, a);
     __syncthreads();
-    float* P = Pw + warp * 2 * mrow;
-    float* DS = P + mrow;
-    // phase A: D_i = sum_j p_ij dp_ij computed exactly in fp32 (not from the
-    // bf16-rounded O: dp - D cancels strongly in cross attention), then
-    // dQ_i = scale * sum_j p_ij (dp_ij - D_i) K_j
-    for (int i = warp; i < lq; i += kWarps) {
-        const int kend = a.causal ? min(lk, i + 1) : lk;
-        const uint32_t* qi = Qs + i * kPitch;
-        const uint32_t* di = dOs + i * kPitch;
-        float part = 0.f;
-        for (int j = lane; j < kend; j += 32) {
-            const float p = __expf(dot_row(qi, Ks + j * kPitch) * a.scale - lse[i]);
-            const float dp = dot_row(di, Vs + j * kPitch);
-            P[j] = p;
-            DS[j] = dp;
-            part = fmaf(p, dp, part);
-        }
-        const float Di = warp_sum(part);
-        if (lane == 0) Dd[i] = Di;
-        for (int j = lane; j < kend; j += 32) DS[j] = P[j] * (DS[j] - Di);
-        __syncwarp();
-        float gx = 0.f, gy = 0.f;
-        for (int j = 0; j < kend; ++j) {
-            const float2 kk = unpack(Ks[j * kPitch + lane]);
-            gx = fmaf(DS[j], kk.x, gx);
-            gy = fmaf(DS[j], kk.y, gy);
-        }
-        reinterpret_cast<uint32_t*>(a.dq + int64_t(q0 + i) * a.ld_dq + h * kHd)[lane] =
-            pack(gx * a.scale, gy * a.scale);
-        __syncwarp();
+    uint16_t* Qs = sm;
+    uint16_t* dOs = Qs + a.cap * kP;
+    uint16_t* Ks = dOs + a.cap * kP;
+    uint16_t* Vs = Ks + a.cap * kP;
+    float* lse2 = reinterpret_cast<float*>(Vs + a.cap * kP);  // lse * log2(e), per smem row
+    float* Dd = lse2 + a.cap;
+    const int nthr = kBwdWarps * 32;
+    stage_group(Qs, Ks, Vs, dOs, G, a, h, nthr);
+    for (int i = 0; i < G.n; ++i) {
+        const int pq = (G.lq[i] + 31) & ~31;
+        for (int r = threadIdx.x; r < pq; r += nthr)
+            lse2[G.qoff[i] + r] = r < G.lq[i] ? a.lse[int64_t(h) * a.total_q + G.q0[i] + r] * kLog2e : 0.f;
     }
-    __syncthreads();  // every D_i is needed by every warp in phase B
-    // phase B: dV_j = sum_i p_ij dO_i ; dK_j = scale * sum_i ds_ij Q_i
-    for (int j = warp; j < lk; j += kWarps) {
-        const int ibeg = a.causal ? j : 0;
-        const uint32_t* kj = Ks + j * kPitch;
-        const uint32_t* vj = Vs + j * kPitch;
-        for (int i = ibeg + lane; i < lq; i += 32) {
-            const float p = __expf(dot_row(Qs + i * kPitch, kj) * a.scale - lse[i]);
-            const float dp = dot_row(dOs + i * kPitch, vj);
-            P[i] = p;
-            DS[i] = p * (dp - Dd[i]);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const float c = a.scale * kLog2e;
+
+    // ---------------- phase A: D and dQ (warps over 16-query tiles)
+    const int nqt = n_tiles(G, G.lq);
+    for (int tile = warp; tile < nqt; tile += kBwdWarps) {
+        int sidx, qt;
+        tile_of(G, G.lq, tile, sidx, qt);
+        const int lq = G.lq[sidx], lk = G.lk[sidx], q0 = G.q0[sidx], qo = G.qoff[sidx];
+        const uint16_t* Kseq = Ks + G.koff[sidx] * kP;
+        const uint16_t* Vseq = Vs + G.koff[sidx] * kP;
+        uint32_t qf[4][4], df[4][4];
+        load_a(qf, Qs + (qo + qt) * kP, lane);
+        load_a(df, dOs + (qo + qt) * kP, lane);
+        const int row0 = qt + g, row1 = row0 + 8;
+        const float l20 = lse2[qo + row0], l21 = lse2[qo + row1];
+        const int kend = a.causal ? min(lk, qt + 16) : lk;
+        float dpart[2] = {0.f, 0.f};
+        for (int pass = 0; pass < 2; ++pass) {
+            float dq[8][4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dq[i][0] = dq[i][1] = dq[i][2] = dq[i][3] = 0.f;
+            const float D0 = dpart[0], D1 = dpart[1];
+            for (int kb = 0; kb < kend; kb += 32) {
+                float s[4][4], dp[4][4];
+                zero(s);
+                zero(dp);
+                mma_abt(s, qf, Kseq, kb, lane);
+                mma_abt(dp, df, Vseq, kb, lane);
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int key = kb + nt * 8 + 2 * t + (e & 1);
+                        const int row = e < 2 ? row0 : row1;
+                        float p = exp2f(s[nt][e] * c - (e < 2 ? l20 : l21));
+                        if (key >= lk || (a.causal && key > row) || row >= lq) p = 0.f;
+                        if (pass == 0) dpart[e >> 1] = fmaf(p, dp[nt][e], dpart[e >> 1]);
+                        else s[nt][e] = p * (dp[nt][e] - (e < 2 ? D0 : D1));  // dS
+                    }
+                if (pass == 1) mma_pb(dq, s, Kseq, kb, lane);
+            }
+            if (pass == 0) {
+                dpart[0] = quad_sum(dpart[0]);
+                dpart[1] = quad_sum(dpart[1]);
+                if (t == 0) {
+                    Dd[qo + row0] = dpart[0];
+                    Dd[qo + row1] = dpart[1];
+                }
+            } else {
+                uint16_t* o0 = a.dq + int64_t(q0 + row0) * a.ld_dq + h * kHd;
+                uint16_t* o1 = a.dq + int64_t(q0 + row1) * a.ld_dq + h * kHd;
+#pragma unroll
+                for (int nt = 0; nt < 8; ++nt) {
+                    if (row0 < lq)
+                        *reinterpret_cast<uint32_t*>(o0 + nt * 8 + 2 * t) =
+                            pack(dq[nt][0] * a.scale, dq[nt][1] * a.scale);
+                    if (row1 < lq)
+                        *reinterpret_cast<uint32_t*>(o1 + nt * 8 + 2 * t) =
+                            pack(dq[nt][2] * a.scale, dq[nt][3] * a.scale);
+                }
+            }
         }
-        __syncwarp();
-        float vx = 0.f, vy = 0.f, kx = 0.f, ky = 0.f;
-        for (int i = ibeg; i < lq; ++i) {
-            const float2 d = unpack(dOs[i * kPitch + lane]);
-            const float2 q = unpack(Qs[i * kPitch + lane]);
-            vx = fmaf(P[i], d.x, vx);
-            vy = fmaf(P[i], d.y, vy);
-            kx = fmaf(DS[i], q.x, kx);
-            ky = fmaf(DS[i], q.y, ky);
+    }
+    __syncthreads();
+
+    // ---------------- phase B: dK, dV (warps over 16-key tiles)
+    const int nkt = n_tiles(G, G.lk);
+    for (int tile = warp; tile < nkt; tile += kBwdWarps) {
+        int sidx, kt;
+        tile_of(G, G.lk, tile, sidx, kt);
+        const int lq = G.lq[sidx], lk = G.lk[sidx], k0 = G.k0[sidx], qo = G.qoff[sidx];
+        const uint16_t* Qseq = Qs + qo * kP;
+        const uint16_t* dOseq = dOs + qo * kP;
+        uint32_t kf[4][4], vf[4][4];
+        load_a(kf, Ks + (G.koff[sidx] + kt) * kP, lane);
+        load_a(vf, Vs + (G.koff[sidx] + kt) * kP, lane);
+        const int key0 = kt + g, key1 = key0 + 8;
+        float dk[8][4], dv[8][4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            dk[i][0] = dk[i][1] = dk[i][2] = dk[i][3] = 0.f;
+            dv[i][0] = dv[i][1] = dv[i][2] = dv[i][3] = 0.f;
         }
-        reinterpret_cast<uint32_t*>(a.dv + int64_t(k0 + j) * a.ld_dv + h * kHd)[lane] = pack(vx, vy);
-        reinterpret_cast<uint32_t*>(a.dk + int64_t(k0 + j) * a.ld_dk + h * kHd)[lane] =
-            pack(kx * a.scale, ky * a.scale);
-        __syncwarp();
+        const int qbeg = a.causal ? (kt & ~31) : 0;
+        for (int qb = qbeg; qb < lq; qb += 32) {
+            float st[4][4], dpt[4][4];
+            zero(st);
+            zero(dpt);
+            mma_abt(st, kf, Qseq, qb, lane);    // S^T = K Q^T
+            mma_abt(dpt, vf, dOseq, qb, lane);  // dP^T = V dO^T
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int q = qb + nt * 8 + 2 * t + (e & 1);
+                    const int key = e < 2 ? key0 : key1;
+                    float p = 0.f;
+                    if (q < lq && key < lk && !(a.causal && key > q))
+                        p = exp2f(st[nt][e] * c - lse2[qo + q]);
+                    st[nt][e] = p;
+                    dpt[nt][e] = p * (dpt[nt][e] - Dd[qo + q]);
+                }
+            mma_pb(dv, st, dOseq, qb, lane);   // dV += P^T dO
+            mma_pb(dk, dpt, Qseq, qb, lane);   // dK += dS^T Q
+        }
+        uint16_t* v0 = a.dv + int64_t(k0 + key0) * a.ld_dv + h * kHd;
+        uint16_t* v1 = a.dv + int64_t(k0 + key1) * a.ld_dv + h * kHd;
+        uint16_t* kk0 = a.dk + int64_t(k0 + key0) * a.ld_dk + h * kHd;
+        uint16_t* kk1 = a.dk + int64_t(k0 + key1) * a.ld_dk + h * kHd;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+            if (key0 < lk) {
+                *reinterpret_cast<uint32_t*>(v0 + nt * 8 + 2 * t) = pack(dv[nt][0], dv[nt][1]);
+                *reinterpret_cast<uint32_t*>(kk0 + nt * 8 + 2 * t) =
+                    pack(dk[nt][0] * a.scale, dk[nt][1] * a.scale);
+            }
+            if (key1 < lk) {
+                *reinterpret_cast<uint32_t*>(v1 + nt * 8 + 2 * t) = pack(dv[nt][2], dv[nt][3]);
+                *reinterpret_cast<uint32_t*>(kk1 + nt * 8 + 2 * t) =
+                    pack(dk[nt][2] * a.scale, dk[nt][3] * a.scale);
+            }
+        }
     }
 }
 
-size_t fwd_smem(const mm_attn_args& a) {
-    return (size_t(2) * a.max_k * kPitch + kWarps * kWords) * 4 + size_t(kWarps) * a.max_k * 4;
-}
-size_t bwd_smem(const mm_attn_args& a) {
-    const int mrow = std::max(a.max_q, a.max_k);
-    return (size_t(2) * a.max_q * kPitch + size_t(2) * a.max_k * kPitch) * 4 +
-           size_t(2) * a.max_q * 4 + size_t(kWarps) * 2 * mrow * 4;
-}
+size_t fwd_smem(const mm_attn_args& a) { return size_t(3) * a.cap * kP * 2; }
+size_t bwd_smem(const mm_attn_args& a) { return size_t(4) * a.cap * kP * 2 + size_t(2) * a.cap * 4; }
 
 int check(const mm_attn_args* a, bool bwd) {
     MM_CHECK_ARG(a != nullptr, "args is NULL");
     MM_CHECK_ARG(a->head_dim == kHd, "head_dim must be 64 (got %d)", a->head_dim);
     MM_CHECK_ARG(a->q && a->k && a->v && a->o && a->lse && a->cu_q && a->cu_k, "NULL tensor");
     MM_CHECK_ARG(a->n_seq >= 0 && a->heads > 0 && a->max_q > 0 && a->max_k > 0, "bad sizes");
-    MM_CHECK_ARG(a->max_q <= 1024 && a->max_k <= 1024, "sequence longer than 1024");
+    MM_CHECK_ARG(a->max_q <= 256 && a->max_k <= 256, "sequence longer than 256");
+    MM_CHECK_ARG(a->groups && a->n_groups > 0 && a->cap >= 32 && a->cap % 32 == 0 && a->cap <= 256,
+                 "bad attention work groups (cap %d)", a->cap);
+    MM_CHECK_ARG((a->ldq | a->ldk | a->ldv | a->ldo) % 8 == 0, "row strides must be multiples of 8");
     MM_CHECK_ARG(!bwd || (a->d_o && a->dq && a->dk && a->dv), "NULL gradient tensor");
     return 0;
 }
@@ -210,7 +456,7 @@ extern "C" int mm_attention_fwd(const mm_attn_args* a, void* stream) {
     const size_t smem = fwd_smem(*a);
     MM_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-    attn_fwd_kernel<<<dim3(a->n_seq, a->heads), kWarps * 32, smem, mm::as_stream(stream)>>>(*a);
+    attn_fwd_kernel<<<dim3(a->n_groups, a->heads), kFwdWarps * 32, smem, mm::as_stream(stream)>>>(*a);
     MM_LAUNCH_CHECK("attn_fwd_kernel");
     return 0;
 }
@@ -222,7 +468,7 @@ extern "C" int mm_attention_bwd(const mm_attn_args* a, void* stream) {
     MM_CHECK_ARG(smem <= 227 * 1024, "attention backward needs %zu B of smem", smem);
     MM_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-    attn_bwd_kernel<<<dim3(a->n_seq, a->heads), kWarps * 32, smem, mm::as_stream(stream)>>>(*a);
+    attn_bwd_kernel<<<dim3(a->n_groups, a->heads), kBwdWarps * 32, smem, mm::as_stream(stream)>>>(*a);
     MM_LAUNCH_CHECK("attn_bwd_kernel");
     return 0;
 }

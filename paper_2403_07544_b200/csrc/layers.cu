@@ -293,25 +293,43 @@ __global__ void __launch_bounds__(kXentThreads) xent_kernel(const uint16_t* logi
 }
 
 // ----------------------------------------------------------------------------
-// out[c] += sum_r x[r, c] (bias gradients).  A thread owns a column pair, a
-// block covers 512 columns x a 64-row slab; slab sums go out with atomics.
-constexpr int kColRows = 64;
-
+// out[c] += sum_r x[r, c] (bias gradients).  Block = 32 column octets (256
+// columns, one 128-bit load per row per thread) x 8 row lanes; the grid has
+// enough row slabs to fill every SM; per-block partials are reduced over the
+// row lanes in smem and leave with one atomic per column.
 __global__ void __launch_bounds__(256) colsum_kernel(const uint16_t* __restrict__ x, float* out,
-                                                     int64_t rows, int cols) {
-    const int cp = blockIdx.x * 256 + threadIdx.x;  // column pair
-    if (2 * cp >= cols) return;
-    const int64_t r0 = int64_t(blockIdx.y) * kColRows;
-    const int64_t r1 = min(rows, r0 + kColRows);
-    float a = 0.f, b = 0.f;
-    const uint32_t* xp = reinterpret_cast<const uint32_t*>(x);
-    for (int64_t r = r0; r < r1; ++r) {
-        const uint32_t w = __ldg(xp + r * (cols / 2) + cp);
-        a += bf2f(w & 0xffff);
-        b += bf2f(w >> 16);
+                                                     int64_t rows, int cols, int64_t slab) {
+    __shared__ float red[8][256 + 8];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int c8 = blockIdx.x * 32 + tx;
+    const bool live = 8 * c8 < cols;
+    const int64_t r0 = int64_t(blockIdx.y) * slab;
+    const int64_t r1 = min(rows, r0 + slab);
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (live) {
+        const uint4* xp = reinterpret_cast<const uint4*>(x);
+        const int64_t pitch = cols / 8;
+#pragma unroll 2
+        for (int64_t r = r0 + ty; r < r1; r += 8) {
+            const uint4 w = __ldg(xp + r * pitch + c8);
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                acc[2 * e] += bf2f(ws[e] & 0xffff);
+                acc[2 * e + 1] += bf2f(ws[e] >> 16);
+            }
+        }
     }
-    atomicAdd(out + 2 * cp, a);
-    atomicAdd(out + 2 * cp + 1, b);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[ty][tx * 8 + e] = acc[e];
+    __syncthreads();
+    const int col = blockIdx.x * 256 + threadIdx.x;
+    if (col < cols) {
+        float s = 0.f;
+#pragma unroll
+        for (int y = 0; y < 8; ++y) s += red[y][threadIdx.x];
+        atomicAdd(out + col, s);
+    }
 }
 
 __global__ void cast_kernel(const float* __restrict__ x, uint16_t* __restrict__ y, int64_t n4) {
@@ -409,10 +427,14 @@ extern "C" int mm_xent_fwd_bwd(const uint16_t* logits, const int32_t* labels, ui
 
 extern "C" int mm_colsum_bf16(const uint16_t* x, float* out, int64_t rows, int cols,
                               void* stream) {
-    MM_CHECK_ARG(x && out && cols % 2 == 0, "bad arguments");
+    MM_CHECK_ARG(x && out && cols % 8 == 0, "cols must be a multiple of 8");
     if (rows == 0) return 0;
-    dim3 grid((cols / 2 + 255) / 256, static_cast<unsigned>((rows + kColRows - 1) / kColRows));
-    colsum_kernel<<<grid, 256, 0, mm::as_stream(stream)>>>(x, out, rows, cols);
+    const int64_t gx = (cols + 255) / 256;
+    int64_t slabs = std::max<int64_t>(1, std::min<int64_t>((rows + 15) / 16, (2 * mm::num_sms() + gx - 1) / gx));
+    const int64_t slab = (rows + slabs - 1) / slabs;
+    slabs = (rows + slab - 1) / slab;
+    dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(slabs));
+    colsum_kernel<<<grid, 256, 0, mm::as_stream(stream)>>>(x, out, rows, cols, slab);
     MM_LAUNCH_CHECK("colsum_kernel");
     return 0;
 }

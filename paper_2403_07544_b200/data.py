@@ -112,3 +112,30 @@ def make_batch(rng: np.random.Generator, spec, vocab: int, sentences: Optional[i
     src_pos = np.concatenate([np.arange(n) for n in ls]).astype(np.int32)
     tgt_pos = np.concatenate([np.arange(n) for n in lt]).astype(np.int32)
     return Batch(src, src_pos, cu_s, tgt_in, tgt_pos, labels, cu_t)
+
+
+ATTN_CAP = 128  # rows per CTA group (each side), see include/mmb200.h
+
+
+def attention_groups(cu_q: np.ndarray, cu_k: np.ndarray, cap: int = ATTN_CAP):
+    """Greedy packing of consecutive sequences into attention CTA groups:
+    each sequence takes ceil(len/32)*32 rows; a group holds at most ``cap``
+    rows per side (a longer sequence gets a group of its own).  Returns
+    (int32 [2*n_groups] of (first, count), rows footprint of the largest group)."""
+    lq = np.diff(cu_q).astype(np.int64)
+    lk = np.diff(cu_k).astype(np.int64)
+    pq = (lq + 31) // 32 * 32
+    pk = (lk + 31) // 32 * 32
+    out = []
+    foot = 0
+    i, n = 0, len(lq)
+    while i < n:
+        j, sq, sk = i, 0, 0
+        while j < n and (j == i or (sq + pq[j] <= cap and sk + pk[j] <= cap)):
+            sq += pq[j]
+            sk += pk[j]
+            j += 1
+        out += [i, j - i]
+        foot = max(foot, sq, sk)
+        i = j
+    return np.asarray(out, dtype=np.int32), int(foot)

@@ -29,10 +29,11 @@ import torch
 
 from . import _native, ops
 from .configs import ModelShape
-from .data import Batch
+from .data import Batch, attention_groups
 from .domain import ClusterTopology, ModuleKey, Side, TaskSpec
 from .model import LN_EPS, ModuleState, module_layouts
-from .plan import Multiplexer, build_plan, embedding_keys, ready_flags
+from .plan import (Multiplexer, build_plan, embedding_keys, exchange_order, ready_flags,
+                   task_modules)
 
 
 @dataclasses.dataclass
@@ -45,28 +46,37 @@ class AdamConfig:
 
 
 class DeviceBatch:
-    """A packed batch resident in HBM (one H2D copy from a pinned buffer)."""
+    """A packed batch resident in HBM: one H2D copy of one pinned int32 buffer
+    holding the token streams, offsets and the attention work groups."""
 
     FIELDS = ("src", "src_pos", "cu_src", "tgt_in", "tgt_pos", "labels", "cu_tgt")
 
     def __init__(self, b: Batch, device, pinned: Optional[torch.Tensor] = None,
                  non_blocking: bool = True):
-        arrs = b.host_arrays()
-        sizes = [len(arrs[f]) for f in self.FIELDS]
+        arrs = dict(b.host_arrays())
+        groups = {}
+        for name, (cq, ck) in (("attn_src", (b.cu_src, b.cu_src)), ("attn_tgt", (b.cu_tgt, b.cu_tgt)),
+                               ("attn_cross", (b.cu_tgt, b.cu_src))):
+            g, cap = attention_groups(cq, ck)
+            arrs[name] = g
+            groups[name] = (len(g) // 2, cap)
+        names = list(self.FIELDS) + list(groups)
+        sizes = [len(arrs[f]) for f in names]
         total = sum(sizes)
         host = pinned if pinned is not None and pinned.numel() >= total else \
             torch.empty(total, dtype=torch.int32, pin_memory=True)
         flat = host.numpy()
         off = 0
-        for f, n in zip(self.FIELDS, sizes):
+        for f, n in zip(names, sizes):
             flat[off:off + n] = arrs[f]
             off += n
         self.h2d_bytes = total * 4
         dev = torch.empty(total, dtype=torch.int32, device=device)
         dev.copy_(host[:total], non_blocking=non_blocking)
         off = 0
-        for f, n in zip(self.FIELDS, sizes):
-            setattr(self, f, dev[off:off + n])
+        for f, n in zip(names, sizes):
+            view = dev[off:off + n]
+            setattr(self, f, (view,) + groups[f] if f in groups else view)
             off += n
         self.n_seq = b.n_seq
         self.n_src, self.n_tgt = b.n_src, b.n_tgt
@@ -189,7 +199,7 @@ class Engine:
         return ops.attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, self.shape.heads, max_q,
                                   max_k, causal, **kw)
 
-    def _self_block_fwd(self, st, p, x, cu, n_seq, max_len, causal, sv):
+    def _self_block_fwd(self, st, p, x, cu, n_seq, max_len, causal, sv, groups=None):
         d = self.shape.d_model
         T = x.shape[0]
         h, mean, rstd = self._ln(st, p + "ln1", x)
@@ -198,11 +208,11 @@ class Engine:
         a = torch.empty(T, d, device=self.device, dtype=torch.bfloat16)
         lse = torch.empty(self.shape.heads, T, device=self.device)
         ops.attention_fwd(self._attn_args(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], a, lse, cu,
-                                          cu, n_seq, max_len, max_len, causal))
+                                          cu, n_seq, max_len, max_len, causal, groups=groups))
         out = torch.empty_like(x)
         ops.gemm(a, st.w(p + "out.w"), out, epilogue=ops.EPI_F32_RESID, bias=st.f32(p + "out.b"),
                  resid=x)
-        sv.append(("self", x, h, mean, rstd, qkv, a, lse))
+        sv.append(("self", x, h, mean, rstd, qkv, a, lse, groups))
         return out
 
     def _cross_block_fwd(self, st, p, x, mem, db, sv):
@@ -216,7 +226,8 @@ class Engine:
         a = torch.empty(T, d, device=self.device, dtype=torch.bfloat16)
         lse = torch.empty(self.shape.heads, T, device=self.device)
         ops.attention_fwd(self._attn_args(q, kv[:, :d], kv[:, d:], a, lse, db.cu_tgt, db.cu_src,
-                                          db.n_seq, db.max_tgt, db.max_src, False))
+                                          db.n_seq, db.max_tgt, db.max_src, False,
+                                          groups=getattr(db, "attn_cross", None)))
         out = torch.empty_like(x)
         ops.gemm(a, st.w(p + "cout.w"), out, epilogue=ops.EPI_F32_RESID, bias=st.f32(p + "cout.b"),
                  resid=x)
@@ -254,7 +265,7 @@ class Engine:
         self._ln_bwd(st, p + "ln2", dh, x_in, mean, rstd, dx, dx_bf)
 
     def _self_bwd(self, st, p, rec, dx, dx_bf, cu, n_seq, max_len, causal):
-        _, x_in, h, mean, rstd, qkv, a, lse = rec
+        _, x_in, h, mean, rstd, qkv, a, lse, groups = rec
         d = self.shape.d_model
         T = x_in.shape[0]
         ops.gemm(dx_bf, a, st.g(p + "out.w"), a_kmajor=False, b_kmajor=False,
@@ -265,7 +276,8 @@ class Engine:
         dqkv = torch.empty(T, 3 * d, device=self.device, dtype=torch.bfloat16)
         ops.attention_bwd(self._attn_args(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], a, lse, cu,
                                           cu, n_seq, max_len, max_len, causal, d_o=da,
-                                          dq=dqkv[:, :d], dk=dqkv[:, d:2 * d], dv=dqkv[:, 2 * d:]))
+                                          dq=dqkv[:, :d], dk=dqkv[:, d:2 * d], dv=dqkv[:, 2 * d:],
+                                          groups=groups))
         ops.gemm(dqkv, h, st.g(p + "qkv.w"), a_kmajor=False, b_kmajor=False,
                  epilogue=ops.EPI_F32_ACCUM)
         ops.colsum(dqkv, st.g(p + "qkv.b"))
@@ -286,7 +298,8 @@ class Engine:
         dkv = torch.empty(S, 2 * d, device=self.device, dtype=torch.bfloat16)
         ops.attention_bwd(self._attn_args(q, kv[:, :d], kv[:, d:], a, lse, db.cu_tgt, db.cu_src,
                                           db.n_seq, db.max_tgt, db.max_src, False, d_o=da, dq=dq,
-                                          dk=dkv[:, :d], dv=dkv[:, d:]))
+                                          dk=dkv[:, :d], dv=dkv[:, d:],
+                                          groups=getattr(db, "attn_cross", None)))
         self._tr(p + "dckv", dkv)
         self._tr(p + "dca", da)
         self._tr(p + "dcx_out", dx)
@@ -317,7 +330,8 @@ class Engine:
             st = self.states[key]
             for i in range(st.layout.n_layers):
                 sv = []
-                x = self._self_block_fwd(st, f"l{i}.", x, db.cu_src, db.n_seq, db.max_src, False, sv)
+                x = self._self_block_fwd(st, f"l{i}.", x, db.cu_src, db.n_seq, db.max_src, False, sv,
+                                         db.attn_src)
                 self._tr(f"enc_l{i}_attn", x)
                 x = self._ffn_fwd(st, f"l{i}.", x, sv)
                 self._tr(f"enc_l{i}_ffn", x)
@@ -335,7 +349,8 @@ class Engine:
             st = self.states[key]
             for i in range(st.layout.n_layers):
                 sv = []
-                y = self._self_block_fwd(st, f"l{i}.", y, db.cu_tgt, db.n_seq, db.max_tgt, True, sv)
+                y = self._self_block_fwd(st, f"l{i}.", y, db.cu_tgt, db.n_seq, db.max_tgt, True, sv,
+                                         db.attn_tgt)
                 y = self._cross_block_fwd(st, f"l{i}.", y, mem, db, sv)
                 y = self._ffn_fwd(st, f"l{i}.", y, sv)
                 dec_saved.append((st, f"l{i}.", sv))
@@ -381,25 +396,27 @@ class Engine:
         ops.embed_bwd(db.src, dx, emb_e.g("emb"), self.scale)
 
     # ------------------------------------------------------------------ step
-    def zero_grads(self) -> None:
-        """DeviceState.reset (syncsim.py:108-111): zero every hosted bucket."""
-        for st in self.states.values():
-            ops.memset(st.grad, 0)
+    def zero_grads(self, keys=None) -> None:
+        """DeviceState.reset (syncsim.py:108-111).  Only buckets that will be
+        written this step need zeroing: K3 never reads a module with n = 0,
+        and a module's bucket is zeroed before its first use in a step."""
+        for k in (self.states if keys is None else keys):
+            ops.memset(self.states[k].grad, 0)
 
     def step(self, step_idx: int, batches: Sequence[DeviceBatch]) -> dict:
         """One optimizer step: len(batches) micro-batches (accum_count), then
         the Algorithm-1 exchange and the fused update.  Returns host-side
         bookkeeping; the loss stays on device in ``self.loss_sum``."""
-        self.zero_grads()
         ops.memset(self.loss_sum, 0)
         used: set[ModuleKey] = set()
         picked = []
         for db in batches:
             task = self.mux.pick(step_idx)
             picked.append(task.id)
+            fresh = [k for k in task_modules(task) if k not in used]
+            self.zero_grads(fresh)
+            used.update(fresh)
             self.forward_backward(task, db, self.loss_sum)
-            used.update(task.modules())
-            used.update(embedding_keys(task))
         flags = ready_flags(self.plan, self.rank, used)
         if self.comm is not None:
             self.flags_dev.copy_(torch.tensor(flags, dtype=torch.int32), non_blocking=True)
@@ -407,19 +424,17 @@ class Engine:
             counts = self.n_ready_dev.tolist()  # host needs n to post the right collectives
         else:
             counts = flags
-        self.exchange_and_update(counts)
+        self.exchange_and_update(counts, used)
         return {"tasks": picked, "ready": dict(zip(self.plan.keys, counts))}
 
-    def exchange_and_update(self, counts: Sequence[int]) -> None:
+    def exchange_and_update(self, counts: Sequence[int], used=frozenset()) -> None:
         items = []
         if self.comm is not None:
-            for k in self.plan.keys:  # sorted ModuleKey = global issue order
-                g = tuple(self.plan.groups[k])
-                n = counts[self.index[k]]
-                if len(g) < 2 or n < 1 or k not in self.states:
-                    continue
-                grp = self.comm.by_set.get(g)
+            for k in exchange_order(self.plan, counts, self.rank):
+                grp = self.comm.by_set.get(tuple(self.plan.groups[k]))
                 st = self.states[k]
+                if k not in used:  # contribute the zero of Algorithm 1
+                    ops.memset(st.grad, 0)
                 items.append(_native.ReduceItem(group=grp, buf=st.grad.data_ptr(),
                                                 n_elems=st.grad.numel(), dtype=0))
             self.comm.reduce(items)

@@ -41,6 +41,7 @@ class AttnArgs(ctypes.Structure):
         ("n_seq", ctypes.c_int32), ("heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
         ("causal", ctypes.c_int32), ("max_q", ctypes.c_int32), ("max_k", ctypes.c_int32),
         ("scale", ctypes.c_float), ("total_q", ctypes.c_int32),
+        ("groups", ctypes.c_void_p), ("n_groups", ctypes.c_int32), ("cap", ctypes.c_int32),
     ]
 
 
@@ -158,8 +159,16 @@ def cast_bf16(x, y) -> None:
 
 
 def attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, heads, max_q, max_k, causal,
-                   d_o=None, dq=None, dk=None, dv=None) -> AttnArgs:
+                   d_o=None, dq=None, dk=None, dv=None, groups=None) -> AttnArgs:
+    """groups: (device int32 tensor [2*n_groups], n_groups, cap) from
+    data.attention_groups; built here from cu_q / cu_k when omitted."""
     hd = 64
+    if groups is None:
+        from .data import attention_groups
+        import numpy as _np
+        gh, cap = attention_groups(_np.asarray(cu_q.cpu()), _np.asarray(cu_k.cpu()))
+        groups = (torch.from_numpy(gh).to(q.device), len(gh) // 2, cap)
+    gt, n_groups, cap = groups
     return AttnArgs(
         q=q.data_ptr(), k=k.data_ptr(), v=v.data_ptr(), o=o.data_ptr(), lse=lse.data_ptr(),
         d_o=_ptr(d_o), dq=_ptr(dq), dk=_ptr(dk), dv=_ptr(dv),
@@ -168,7 +177,8 @@ def attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, heads, max_q, max_k, caus
         ld_dq=dq.stride(0) if dq is not None else 0, ld_dk=dk.stride(0) if dk is not None else 0,
         ld_dv=dv.stride(0) if dv is not None else 0,
         n_seq=n_seq, heads=heads, head_dim=hd, causal=int(causal), max_q=max_q, max_k=max_k,
-        scale=1.0 / math.sqrt(hd), total_q=q.shape[0])
+        scale=1.0 / math.sqrt(hd), total_q=q.shape[0],
+        groups=gt.data_ptr(), n_groups=n_groups, cap=cap)
 
 
 def attention_fwd(args: AttnArgs) -> None:

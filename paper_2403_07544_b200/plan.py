@@ -120,3 +120,14 @@ def ready_counts_all(plan: ModulePlan, used_by_rank: dict[int, set]) -> list[int
         for i, f in enumerate(ready_flags(plan, r, used)):
             tot[i] += f
     return tot
+
+
+def exchange_order(plan: ModulePlan, counts, rank: int) -> list[ModuleKey]:
+    """Modules this rank must post a group reduction for, in the global issue
+    order (sorted ModuleKey): hosted here, group of >= 2 ranks, n >= 1.  Every
+    member of a group derives the same list from the same world-summed counts,
+    so collectives on overlapping sub-communicators never cross."""
+    idx = plan.index()
+    mine = plan.hosted.get(rank, frozenset())
+    return [k for k in plan.keys
+            if k in mine and len(plan.groups[k]) >= 2 and counts[idx[k]] >= 1]

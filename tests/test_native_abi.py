@@ -1,0 +1,98 @@
+"""The C-ABI library loads on a CPU-only host, exports every entry point the
+header declares, and K9 (the allocator's comm-cost kernel) is bit-identical
+to the reference's kernel (golden vectors from _cost_py.py, the oracle's C
+restatement and -- when built -- the reference's own compiled Cython)."""
+import ctypes
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2403_07544_b200 import _native
+from paper_2403_07544_b200.allocator import comm_cost_kernel
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def golden():
+    with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+        return json.load(f)
+
+
+def test_library_loads_and_exports_every_symbol():
+    lib = _native.lib()
+    syms = _native.symbols()
+    assert len(syms) >= 25
+    for name in syms:
+        assert hasattr(lib, name), name
+    assert lib.mm_abi_version() == _native.ABI_VERSION
+
+
+def test_header_version_matches_binding():
+    with open(os.path.join(ROOT, "include", "mmb200.h")) as f:
+        txt = f.read()
+    assert f"#define MMB200_ABI_VERSION {_native.ABI_VERSION}" in txt
+
+
+def test_struct_layouts():
+    # offsets the C side relies on (include/mmb200.h)
+    assert ctypes.sizeof(_native.SyncModule) == 8 * 8 + 8 + 8 + 4 + 4
+    assert ctypes.sizeof(_native.AdamModule) == 5 * 8 + 8 + 4 + 4 + 4 + 4
+    assert ctypes.sizeof(_native.AdamHyper) == 7 * 4
+    assert ctypes.sizeof(_native.ReduceItem) == 8 + 8 + 8 + 4 + 4
+
+
+def test_argument_errors_are_reported():
+    lib = _native.lib()
+    total = ctypes.c_double()
+    st = lib.mm_comm_cost(None, -1, None, None, None, None, 0, 1.0, 4.0, None, ctypes.byref(total))
+    assert st == -1
+    assert b"negative" in lib.mm_last_error()
+
+
+def _case_arrays(c):
+    params = np.array([float.fromhex(x) for x in c["params"]])
+    return (params, np.array(c["off"], np.int64), np.array(c["idx"], np.int64),
+            np.array(c["task_dev"], np.int64), np.array(c["dev_node"], np.int64),
+            float.fromhex(c["w_intra"]), float.fromhex(c["w_inter"]))
+
+
+def test_comm_cost_bit_exact_vs_reference_golden(golden):
+    for c in golden["allocator"]["kernel"]:
+        p, off, idx, td, dn, wi, we = _case_arrays(c)
+        out = np.zeros(len(p))
+        total = comm_cost_kernel(p, off, idx, td, dn, wi, we, out)
+        assert total.hex() == c["total"]
+        assert [x.hex() for x in out] == c["per_module"]
+
+
+def test_comm_cost_vs_oracle_c_and_reference_build(golden):
+    from oracle import build_ref
+    build_ref.build()
+    lib = ctypes.CDLL(build_ref.ORACLE_SO)
+    lib.oracle_comm_cost.restype = ctypes.c_double
+    ref_kernel = build_ref.load_reference_kernel()  # None on the GPU box
+    dp = ctypes.POINTER(ctypes.c_double)
+    ip = ctypes.POINTER(ctypes.c_int64)
+    for c in golden["allocator"]["kernel"]:
+        p, off, idx, td, dn, wi, we = _case_arrays(c)
+        o1, o2 = np.zeros(len(p)), np.zeros(len(p))
+        t1 = comm_cost_kernel(p, off, idx, td, dn, wi, we, o1)
+        t2 = lib.oracle_comm_cost(p.ctypes.data_as(dp), len(p), off.ctypes.data_as(ip),
+                                  idx.ctypes.data_as(ip), td.ctypes.data_as(ip),
+                                  dn.ctypes.data_as(ip), len(dn), ctypes.c_double(wi),
+                                  ctypes.c_double(we), o2.ctypes.data_as(dp))
+        assert t1 == t2 and np.array_equal(o1, o2)
+        if ref_kernel is not None:
+            o3 = np.zeros(len(p))
+            assert ref_kernel(p, off, idx, td, dn, wi, we, o3) == t1
+            assert np.array_equal(o3, o1)
+
+
+def test_comm_cost_rejects_bad_device():
+    out = np.zeros(1)
+    with pytest.raises(_native.MMError):
+        comm_cost_kernel(np.ones(1), np.array([0, 1]), np.array([0]), np.array([5]),
+                         np.array([0, 0]), 1.0, 4.0, out)
