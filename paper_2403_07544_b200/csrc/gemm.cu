@@ -10,9 +10,12 @@
 //               K=16) from smem descriptors into a double-buffered TMEM
 //               accumulator, tcgen05.commit releases smem stages / signals the
 //               epilogue; this warp also owns the TMEM allocation
-//   warps 2..5  epilogue: tcgen05.ld (32 lanes x 32 columns per warp access),
-//               fused bias / ReLU / ReLU-backward mask / residual add /
-//               fp32 accumulate, 128-bit global stores
+//   warps 2..5  epilogue: tcgen05.ld (32 lanes x 32 columns per access),
+//               fused bias (warp-shuffle broadcast) / ReLU / ReLU-backward
+//               mask / residual add, staged through a per-warp swizzled smem
+//               box and written by TMA (cp.async.bulk.tensor store; fp32
+//               accumulation -- wgrad into the grad bucket, split-K partials --
+//               uses the TMA reduce-add, so no read-modify-write or atomics)
 // Operands may be K-major or MN-major (transpose bits of the instruction
 // descriptor), which is what lets forward, dgrad and wgrad all run without a
 // transpose pass:
@@ -37,14 +40,21 @@ constexpr int UMMA_K = 16;
 constexpr int kThreads = 192;
 constexpr int kEpiWarp0 = 2;
 
+constexpr int kEpiWarps = 4;
+constexpr int kEpiBufBytes = 32 * 128;                    // 32 rows x 128 B box
+constexpr int kEpiSmem = kEpiWarps * 2 * kEpiBufBytes;    // double-buffered per warp
+constexpr int kSmemLimit = 232448;
+
 template <int BN>
 struct Cfg {
-    static constexpr int kStages = BN == 256 ? 4 : 6;
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
-    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kStagesFit = (kSmemLimit - kEpiSmem - 1024 - 256) / kStageBytes;
+    static constexpr int kStages = kStagesFit > 6 ? 6 : kStagesFit;
+    static constexpr int kTmemCols = BN == 128 ? 256 : 512;  // 2 accumulators, power of 2
+    static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 + 256;
+    static_assert(kSmem <= kSmemLimit, "smem budget");
 };
 
 struct Params {
@@ -68,24 +78,22 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// Epilogue for one row segment of 32 columns held in registers.
-__device__ __forceinline__ void epilogue_chunk(const Params& p, int64_t row, int64_t col0,
-                                               float (&acc)[32], bool atomic) {
-    if (row >= p.m) return;
+// Epilogue math for one row (this thread) x 32 columns held in registers.
+__device__ __forceinline__ void epilogue_math(const Params& p, int64_t row, int64_t col0,
+                                              float (&acc)[32], int lane) {
     const int ep = p.epilogue;
-    const int64_t ncols = (p.n - col0) < 32 ? (p.n - col0) : 32;
-    if (ncols <= 0) return;
     if (p.bias && (ep == MM_EPI_BF16 || ep == MM_EPI_BF16_RELU || ep == MM_EPI_F32 ||
                    ep == MM_EPI_F32_RESID)) {
+        const float bv = (col0 + lane < p.n) ? __ldg(p.bias + col0 + lane) : 0.f;
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-            if (j < ncols) acc[j] += __ldg(p.bias + col0 + j);
+        for (int j = 0; j < 32; ++j) acc[j] += __shfl_sync(0xffffffffu, bv, j);
     }
     if (ep == MM_EPI_BF16_RELU) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) acc[j] = fmaxf(acc[j], 0.f);
     }
-    const bool full = ncols == 32;
+    if (row >= p.m) return;
+    const bool full = col0 + 32 <= p.n;
     if (ep == MM_EPI_BF16_DRELU) {
         const uint16_t* aux = reinterpret_cast<const uint16_t*>(p.aux) + row * p.ldd + col0;
         if (full) {
@@ -102,32 +110,11 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, int64_t row, int
                 }
             }
         } else {
-            for (int j = 0; j < ncols; ++j)
-                if (bf16_to_f(aux[j]) <= 0.f) acc[j] = 0.f;
-        }
-    }
-    if (ep == MM_EPI_BF16 || ep == MM_EPI_BF16_RELU || ep == MM_EPI_BF16_DRELU) {
-        uint16_t* out = reinterpret_cast<uint16_t*>(p.d) + row * p.ldd + col0;
-        if (full) {
-            uint4* o4 = reinterpret_cast<uint4*>(out);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint4 w;
-                w.x = pack2(acc[q * 8 + 0], acc[q * 8 + 1]);
-                w.y = pack2(acc[q * 8 + 2], acc[q * 8 + 3]);
-                w.z = pack2(acc[q * 8 + 4], acc[q * 8 + 5]);
-                w.w = pack2(acc[q * 8 + 6], acc[q * 8 + 7]);
-                o4[q] = w;
-            }
-        } else {
-            for (int j = 0; j < ncols; ++j) {
-                __nv_bfloat16 h = __float2bfloat16_rn(acc[j]);
-                out[j] = *reinterpret_cast<uint16_t*>(&h);
-            }
+            for (int j = 0; j < 32; ++j)
+                if (col0 + j < p.n && bf16_to_f(aux[j]) <= 0.f) acc[j] = 0.f;
         }
-        return;
     }
-    float* out = reinterpret_cast<float*>(p.d) + row * p.ldd + col0;
     if (ep == MM_EPI_F32_RESID) {
         const float* res = p.resid + row * p.ldd + col0;
         if (full) {
@@ -138,52 +125,51 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, int64_t row, int
                 acc[q * 4 + 2] += r.z; acc[q * 4 + 3] += r.w;
             }
         } else {
-            for (int j = 0; j < ncols; ++j) acc[j] += res[j];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (col0 + j < p.n) acc[j] += res[j];
         }
     }
-    if (ep == MM_EPI_F32_ACCUM) {
-        if (full) {
+}
+
+// Write this thread's 32 values as row `r` of a 32-row staging box laid out
+// in the tensor map's swizzle (bf16: 64 B rows, SWIZZLE_64B; fp32: 128 B
+// rows, SWIZZLE_128B).  A warp's 16-byte stores then spread over all banks.
+__device__ __forceinline__ void stage_row(uint8_t* buf, int r, const float (&acc)[32], bool bf16) {
+    if (bf16) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                float4* o = reinterpret_cast<float4*>(out + q * 4);
-                float4 v = make_float4(acc[q * 4], acc[q * 4 + 1], acc[q * 4 + 2], acc[q * 4 + 3]);
-                if (atomic) {
-                    atomicAdd(o, v);
-                } else {
-                    float4 c = *o;
-                    c.x += v.x; c.y += v.y; c.z += v.z; c.w += v.w;
-                    *o = c;
-                }
-            }
-        } else {
-            for (int j = 0; j < ncols; ++j) {
-                if (atomic) atomicAdd(out + j, acc[j]);
-                else out[j] += acc[j];
-            }
+        for (int q = 0; q < 4; ++q) {
+            uint4 w;
+            w.x = pack2(acc[q * 8 + 0], acc[q * 8 + 1]);
+            w.y = pack2(acc[q * 8 + 2], acc[q * 8 + 3]);
+            w.z = pack2(acc[q * 8 + 4], acc[q * 8 + 5]);
+            w.w = pack2(acc[q * 8 + 6], acc[q * 8 + 7]);
+            const int phys = q ^ ((r >> 1) & 3);
+            *reinterpret_cast<uint4*>(buf + r * 64 + phys * 16) = w;
         }
-        return;
-    }
-    if (full) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-            *reinterpret_cast<float4*>(out + q * 4) =
-                make_float4(acc[q * 4], acc[q * 4 + 1], acc[q * 4 + 2], acc[q * 4 + 3]);
     } else {
-        for (int j = 0; j < ncols; ++j) out[j] = acc[j];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int phys = q ^ (r & 7);
+            *reinterpret_cast<float4*>(buf + r * 128 + phys * 16) =
+                make_float4(acc[q * 4], acc[q * 4 + 1], acc[q * 4 + 2], acc[q * 4 + 3]);
+        }
     }
 }
 
 template <int BN, int A_MN, int B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
-                        const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ Params p) {
+                        const __grid_constant__ CUtensorMap tmap_b,
+                        const __grid_constant__ CUtensorMap tmap_d, const __grid_constant__ Params p) {
     using C = Cfg<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     uint8_t* smem_a = smem;
     uint8_t* smem_b = smem + C::kStages * C::kABytes;
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    uint8_t* smem_epi = smem + C::kStages * C::kStageBytes;  // 1024-aligned
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_epi + kEpiSmem);
     uint64_t* empty_bar = full_bar + C::kStages;
     uint64_t* tfull_bar = empty_bar + C::kStages;
     uint64_t* tempty_bar = tfull_bar + 2;
@@ -195,6 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         tc::tma_prefetch(&tmap_a);
         tc::tma_prefetch(&tmap_b);
+        tc::tma_prefetch(&tmap_d);
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < C::kStages; ++s) {
@@ -294,8 +281,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
         // ------------------------------------------------------------ epilogue
         const int lane_grp = warp & 3;  // TMEM lanes this warp may access
-        const int row_in_tile = lane_grp * 32 + lane;
-        const bool atomic = p.splits > 1;
+        const bool out_bf16 = p.epilogue == MM_EPI_BF16 || p.epilogue == MM_EPI_BF16_RELU ||
+                              p.epilogue == MM_EPI_BF16_DRELU;
+        const bool reduce = p.epilogue == MM_EPI_F32_ACCUM;
+        uint8_t* bufs = smem_epi + (warp - kEpiWarp0) * 2 * kEpiBufBytes;
+        int nbuf = 0;
         int local = 0;
         for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
             const int tile = u / p.splits;
@@ -304,21 +294,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t acc_phase = (local >> 1) & 1;
             tc::mbar_wait(&tfull_bar[acc], acc_phase);
             tc::tc_fence_after();
-            const int64_t row = int64_t(tm) * BM + row_in_tile;
+            const int row0 = tm * BM + lane_grp * 32;  // this warp's first row
+            const int64_t row = int64_t(row0) + lane;
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) + acc * BN;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
+                const int col0 = tn * BN + c * 32;
+                if (col0 >= p.n) break;
                 uint32_t v[32];
                 tc::tmem_ld_32x32(t_row + c * 32, v);
                 tc::tmem_ld_wait();
                 float f[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-                epilogue_chunk(p, row, int64_t(tn) * BN + c * 32, f, atomic);
+                epilogue_math(p, row, col0, f, lane);
+                uint8_t* buf = bufs + nbuf * kEpiBufBytes;
+                if (lane == 0) tc::bulk_wait_read<1>();  // the store that last read `buf` is done
+                __syncwarp();
+                stage_row(buf, lane, f, out_bf16);
+                tc::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    if (reduce) tc::tma_reduce_add_2d(&tmap_d, buf, col0, row0);
+                    else tc::tma_store_2d(&tmap_d, buf, col0, row0);
+                    tc::bulk_commit();
+                }
+                nbuf ^= 1;
             }
             tc::tc_fence_before();
             tc::mbar_arrive(&tempty_bar[acc]);
         }
+        if (lane == 0) tc::bulk_wait_all();
     }
     __syncthreads();
     if (warp == 1) {
@@ -344,22 +350,23 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-// 2D bf16 tensor map over a row-major [outer, inner] matrix with row stride
-// `ld` elements; box = {64 (inner), box_outer}, 128-byte swizzle, OOB -> 0.
+// 2D tensor map over a row-major [outer, inner] matrix with row stride `ld`
+// elements, box {box_inner, box_outer}; OOB loads read 0, OOB stores clip.
 int make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int64_t ld,
-             int box_outer) {
+             int box_outer, int box_inner = 64, bool fp32 = false,
+             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     auto enc = get_encode();
     if (!enc) {
         mm::set_error("cuTensorMapEncodeTiled unavailable");
         return mm::kCuda;
     }
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
-    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_outer)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * (fp32 ? 4 : 2))};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
-                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+    CUresult r = enc(map, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                     2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         mm::set_error("cuTensorMapEncodeTiled failed (%d): inner=%lld outer=%lld ld=%lld box=%d",
@@ -370,7 +377,8 @@ int make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, i
 }
 
 template <int BN, int A_MN, int B_MN>
-int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t s) {
+int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md, const Params& p,
+           cudaStream_t s) {
     auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
@@ -379,18 +387,18 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaSt
         attr_set = true;
     }
     const int grid = std::min(p.units, mm::num_sms());
-    kern<<<grid, kThreads, Cfg<BN>::kSmem, s>>>(ma, mb, p);
+    kern<<<grid, kThreads, Cfg<BN>::kSmem, s>>>(ma, mb, md, p);
     MM_LAUNCH_CHECK("gemm_tcgen05_kernel");
     return 0;
 }
 
 template <int BN>
-int dispatch(int a_mn, int b_mn, const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
-             cudaStream_t s) {
-    if (!a_mn && !b_mn) return launch<BN, 0, 0>(ma, mb, p, s);
-    if (!a_mn && b_mn) return launch<BN, 0, 1>(ma, mb, p, s);
-    if (a_mn && !b_mn) return launch<BN, 1, 0>(ma, mb, p, s);
-    return launch<BN, 1, 1>(ma, mb, p, s);
+int dispatch(int a_mn, int b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
+             const CUtensorMap& md, const Params& p, cudaStream_t s) {
+    if (!a_mn && !b_mn) return launch<BN, 0, 0>(ma, mb, md, p, s);
+    if (!a_mn && b_mn) return launch<BN, 0, 1>(ma, mb, md, p, s);
+    if (a_mn && !b_mn) return launch<BN, 1, 0>(ma, mb, md, p, s);
+    return launch<BN, 1, 1>(ma, mb, md, p, s);
 }
 
 }  // namespace
@@ -414,15 +422,23 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
     const int a_mn = a->a_kmajor ? 0 : 1;
     const int b_mn = a->b_kmajor ? 0 : 1;
 
-    // tile width: 256 when it still yields ~a full wave, else 128
+    // tile width: minimise (waves of persistent CTAs) x (tile width)
     const int64_t tiles_m = (a->m + BM - 1) / BM;
     const int sms = mm::num_sms();
     int bn = 128;
-    if (a->n >= 256 && tiles_m * ((a->n + 255) / 256) >= sms) bn = 256;
+    {
+        double best = 1e300;
+        for (int cand : {256, 192, 128}) {
+            if (cand > 128 && a->n <= cand - 64) continue;
+            const int64_t t = tiles_m * ((a->n + cand - 1) / cand);
+            const double cost = double((t + sms - 1) / sms) * cand;
+            if (cost < best - 1e-9) { best = cost; bn = cand; }
+        }
+    }
     const int64_t tiles_n = (a->n + bn - 1) / bn;
     const int num_kb = static_cast<int>((a->k + BK - 1) / BK);
     const int64_t tiles = tiles_m * tiles_n;
-    // split K (fp32 accumulate only) until there are ~2 units per SM
+    // split K (fp32 accumulate only: partials meet in the TMA reduce-add)
     int splits = 1;
     if (a->epilogue == MM_EPI_F32_ACCUM) {
         while (tiles * splits * 2 <= 2 * sms && splits * 2 <= num_kb / 2) splits *= 2;
@@ -431,7 +447,7 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
     splits = (num_kb + kb_per - 1) / kb_per;  // no empty splits
     MM_CHECK_ARG(tiles * splits < (int64_t(1) << 31), "GEMM too large");
 
-    CUtensorMap ma, mb;
+    CUtensorMap ma, mb, md;
     int st;
     // A: K-major [M, K] rows of lda; MN-major [K, M] rows of lda
     st = a_mn ? make_map(&ma, a->a, a->m, a->k, a->lda, BK)
@@ -439,6 +455,10 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
     if (st) return st;
     st = b_mn ? make_map(&mb, a->b, a->n, a->k, a->ldb, BK)
               : make_map(&mb, a->b, a->k, a->n, a->ldb, bn);
+    if (st) return st;
+    // D: 32 x 32 boxes, swizzle matching the staging layout
+    st = make_map(&md, a->d, a->n, a->m, a->ldd, 32, 32, !out_bf16,
+                  out_bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
     if (st) return st;
 
     Params p{};
@@ -453,6 +473,7 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
     p.num_kb = num_kb;
     p.units = static_cast<int>(tiles * splits);
     cudaStream_t s = mm::as_stream(stream);
-    return bn == 256 ? dispatch<256>(a_mn, b_mn, ma, mb, p, s)
-                     : dispatch<128>(a_mn, b_mn, ma, mb, p, s);
+    if (bn == 256) return dispatch<256>(a_mn, b_mn, ma, mb, md, p, s);
+    if (bn == 192) return dispatch<192>(a_mn, b_mn, ma, mb, md, p, s);
+    return dispatch<128>(a_mn, b_mn, ma, mb, md, p, s);
 }
