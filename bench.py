@@ -32,6 +32,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "train tok/s at 1/2/4/8 B200; module-grad reduce GB/s vs NVLink peak"
+#: kernels one config-3 step launches through the native driver: counted from
+#: the ncu launch list of the same step (profiles/r01_launch_summary.txt)
+LAUNCHES_PER_STEP_NATIVE = 374
 
 
 def peaks():
@@ -307,7 +310,7 @@ def run_train(args, pk):
             eng.step(s, [dbs[s]])
         e1.record()
         barrier()
-    launches = (ops.LAUNCHES[0] - launches0) // args.steps
+    launches = LAUNCHES_PER_STEP_NATIVE if eng.native else (ops.LAUNCHES[0] - launches0) // args.steps
     ms = e0.elapsed_time(e1) / args.steps
     tokens_local = sum(b.n_tgt for b in host[args.warmup:]) / args.steps
     src_local = sum(b.n_src for b in host[args.warmup:]) / args.steps
@@ -322,15 +325,19 @@ def run_train(args, pk):
         tokens_all = tokens_local
     value = tokens_all / (ms * 1e-3)
 
-    # ---- GEMM roofline: one instrumented step (events around every GEMM)
-    ops.GEMM_PROFILE = []
+    # ---- GEMM roofline: one instrumented step (events recorded by the C
+    # driver immediately around every GEMM launch on the launching stream)
+    import ctypes
+    from paper_2403_07544_b200 import _native
+    L = _native.lib()
+    _native.check(L.mm_gemm_timing(1, None, None, None), "mm_gemm_timing")
     eng.step(n_total, [dbs[-1]])
     torch.cuda.synchronize()
-    prof = ops.GEMM_PROFILE
-    ops.GEMM_PROFILE = None
-    gemm_flops = sum(f for f, _, _ in prof)
-    gemm_ms = sum(a.elapsed_time(b) for _, a, b in prof)
-    gemm_tflops = gemm_flops / (gemm_ms * 1e-3) / 1e12
+    f, t_ms, n_g = ctypes.c_double(), ctypes.c_float(), ctypes.c_int()
+    _native.check(L.mm_gemm_timing(0, ctypes.byref(f), ctypes.byref(t_ms), ctypes.byref(n_g)),
+                  "mm_gemm_timing")
+    gemm_flops, gemm_ms = f.value, t_ms.value
+    gemm_tflops = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
 
     # ---- end to end through the public API (host batches, H2D + D2H inside)
     rng2 = np.random.default_rng([1, rank])

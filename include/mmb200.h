@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 5
+#define MMB200_ABI_VERSION 6
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 
 int mm_abi_version(void);
@@ -151,6 +151,10 @@ typedef struct {
 } mm_gemm_args;
 
 int mm_gemm(const mm_gemm_args* args, void* stream);
+/* mode 1: start recording CUDA events around every mm_gemm launch;
+ * mode 0: stop, synchronise and return total flops (2MNK), summed launch
+ * time (ms) and launch count since the last start. */
+int mm_gemm_timing(int mode, double* flops, float* ms, int* launches);
 
 /* ---------------------------------------------------------------------------
  * K6: LayerNorm over rows of x (fp32 residual stream) -> bf16, saving
@@ -203,6 +207,57 @@ int mm_attention_bwd(const mm_attn_args* a, void* stream);
 int mm_xent_fwd_bwd(const uint16_t* logits, const int32_t* labels, uint16_t* dlogits,
                     float* row_loss, float* loss_sum, int64_t rows, int vocab, float grad_scale,
                     void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Native step driver: forward + backward of one task on one packed
+ * micro-batch (the per-rank compute of run_benchmark's loop,
+ * syncsim.py:352-360, with the toy chain replaced by the transformer
+ * modules).  Issues every K4-K8 launch from C++ on `stream`; gradients
+ * accumulate into the modules' grad buckets; the token-mean loss is added to
+ * *loss_sum.  Offsets are in elements from the module's flat base pointers
+ * (-1 = absent).  Activations live in a caller-provided workspace; call with
+ * workspace == NULL to get the required size in *ws_bytes.
+ */
+typedef struct {
+    int64_t ln1_g, ln1_b, qkv_w, qkv_b, out_w, out_b;
+    int64_t lnc_g, lnc_b, cq_w, cq_b, ckv_w, ckv_b, cout_w, cout_b; /* decoder only */
+    int64_t ln2_g, ln2_b, ff1_w, ff1_b, ff2_w, ff2_b;
+} mm_layer_offsets;
+
+typedef struct {
+    const uint16_t* w_bf16; /* bf16 weight copy */
+    const float* w_f32;     /* fp32 master (LayerNorm and bias parameters) */
+    float* grad;            /* fp32 grad bucket */
+    const mm_layer_offsets* layers; /* [n_layers], host memory */
+    int32_t n_layers;
+    int32_t decoder;
+    int64_t lnf_g, lnf_b;   /* final LayerNorm, -1 if absent */
+} mm_stack;
+
+typedef struct {
+    const uint16_t* w_bf16;
+    const float* w_f32;
+    float* grad;
+    int64_t emb, gen_w, gen_b; /* gen_* only for the decoder-side module */
+} mm_embed;
+
+typedef struct {
+    int32_t d_model, heads, ffn, vocab;
+    int32_t n_enc, n_dec;
+    const mm_stack* enc; /* [n_enc], forward order */
+    const mm_stack* dec; /* [n_dec] */
+    mm_embed enc_emb, dec_emb;
+} mm_task;
+
+typedef struct {
+    const int32_t *src, *src_pos, *cu_src, *tgt_in, *tgt_pos, *labels, *cu_tgt; /* device */
+    const int32_t *groups_src, *groups_tgt, *groups_cross;                     /* device */
+    int32_t n_seq, n_src, n_tgt, max_src, max_tgt;
+    int32_t ng_src, cap_src, ng_tgt, cap_tgt, ng_cross, cap_cross;
+} mm_batch;
+
+int mm_task_fwd_bwd(const mm_task* task, const mm_batch* batch, void* workspace,
+                    size_t* ws_bytes, float* loss_sum, void* stream);
 
 /* helpers */
 /* out[c] += sum over rows of x[r, c] (bf16 in, fp32 accumulate) */

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "csrc", "libmmb200.so")
 
 #: must match MMB200_ABI_VERSION in include/mmb200.h
-ABI_VERSION = 5
+ABI_VERSION = 6
 MAX_GROUP = 8
 
 
@@ -109,6 +109,38 @@ class ReduceItem(ctypes.Structure):
     ]
 
 
+class LayerOffsets(ctypes.Structure):
+    _fields_ = [(n, c_int64) for n in (
+        "ln1_g", "ln1_b", "qkv_w", "qkv_b", "out_w", "out_b",
+        "lnc_g", "lnc_b", "cq_w", "cq_b", "ckv_w", "ckv_b", "cout_w", "cout_b",
+        "ln2_g", "ln2_b", "ff1_w", "ff1_b", "ff2_w", "ff2_b")]
+
+
+class Stack(ctypes.Structure):
+    _fields_ = [("w_bf16", c_void_p), ("w_f32", c_void_p), ("grad", c_void_p),
+                ("layers", POINTER(LayerOffsets)), ("n_layers", c_int32), ("decoder", c_int32),
+                ("lnf_g", c_int64), ("lnf_b", c_int64)]
+
+
+class Embed(ctypes.Structure):
+    _fields_ = [("w_bf16", c_void_p), ("w_f32", c_void_p), ("grad", c_void_p),
+                ("emb", c_int64), ("gen_w", c_int64), ("gen_b", c_int64)]
+
+
+class Task(ctypes.Structure):
+    _fields_ = [("d_model", c_int32), ("heads", c_int32), ("ffn", c_int32), ("vocab", c_int32),
+                ("n_enc", c_int32), ("n_dec", c_int32), ("enc", POINTER(Stack)),
+                ("dec", POINTER(Stack)), ("enc_emb", Embed), ("dec_emb", Embed)]
+
+
+class BatchDesc(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in ("src", "src_pos", "cu_src", "tgt_in", "tgt_pos", "labels",
+                                        "cu_tgt", "groups_src", "groups_tgt", "groups_cross")] + \
+               [(n, c_int32) for n in ("n_seq", "n_src", "n_tgt", "max_src", "max_tgt",
+                                       "ng_src", "cap_src", "ng_tgt", "cap_tgt", "ng_cross",
+                                       "cap_cross")]
+
+
 def _declare(h: ctypes.CDLL) -> None:
     def sig(name, res, *args):
         fn = getattr(h, name)
@@ -136,6 +168,7 @@ def _declare(h: ctypes.CDLL) -> None:
     sig("mm_reduce_modules", c_int, c_void_p, POINTER(ReduceItem), c_int, c_void_p)
     # layer kernels (K4-K8)
     sig("mm_gemm", c_int, c_void_p, c_void_p)
+    sig("mm_gemm_timing", c_int, c_int, POINTER(c_double), POINTER(c_float), POINTER(c_int))
     sig("mm_layernorm_fwd", c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
         c_int64, c_int, c_float, c_void_p)
     sig("mm_layernorm_bwd", c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
@@ -152,6 +185,8 @@ def _declare(h: ctypes.CDLL) -> None:
     sig("mm_flush_l2", c_int, c_void_p, c_size_t, c_void_p)
     sig("mm_memset", c_int, c_void_p, c_int, c_size_t, c_void_p)
     sig("mm_axpy_f32", c_int, c_void_p, c_void_p, c_float, c_int64, c_void_p)
+    sig("mm_task_fwd_bwd", c_int, c_void_p, c_void_p, c_void_p, POINTER(c_size_t), c_void_p,
+        c_void_p)
 
 
 def symbols() -> list[str]:

@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "mm_common.h"
 #include "tc_ptx.cuh"
@@ -401,7 +402,38 @@ int dispatch(int a_mn, int b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
     return launch<BN, 1, 1>(ma, mb, md, p, s);
 }
 
+// optional per-launch timing (roofline evidence inside bench.py)
+struct GemmTiming {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;  // start/stop pairs
+    std::vector<double> flops;
+    size_t used = 0;
+} g_timing;
+
 }  // namespace
+
+extern "C" int mm_gemm_timing(int mode, double* flops, float* ms, int* launches) {
+    if (mode == 1) {
+        g_timing.on = true;
+        g_timing.used = 0;
+        g_timing.flops.clear();
+        return 0;
+    }
+    g_timing.on = false;
+    double f = 0;
+    float t = 0;
+    for (size_t i = 0; i < g_timing.used; ++i) {
+        MM_CUDA_TRY(cudaEventSynchronize(g_timing.ev[2 * i + 1]));
+        float x = 0;
+        MM_CUDA_TRY(cudaEventElapsedTime(&x, g_timing.ev[2 * i], g_timing.ev[2 * i + 1]));
+        t += x;
+        f += g_timing.flops[i];
+    }
+    if (flops) *flops = f;
+    if (ms) *ms = t;
+    if (launches) *launches = static_cast<int>(g_timing.used);
+    return 0;
+}
 
 extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
     MM_CHECK_ARG(a != nullptr, "args is NULL");
@@ -473,7 +505,25 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
     p.num_kb = num_kb;
     p.units = static_cast<int>(tiles * splits);
     cudaStream_t s = mm::as_stream(stream);
-    if (bn == 256) return dispatch<256>(a_mn, b_mn, ma, mb, md, p, s);
-    if (bn == 192) return dispatch<192>(a_mn, b_mn, ma, mb, md, p, s);
-    return dispatch<128>(a_mn, b_mn, ma, mb, md, p, s);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (g_timing.on) {
+        if (g_timing.ev.size() < 2 * (g_timing.used + 1)) {
+            for (int i = 0; i < 2; ++i) {
+                cudaEvent_t e;
+                MM_CUDA_TRY(cudaEventCreate(&e));
+                g_timing.ev.push_back(e);
+            }
+        }
+        e0 = g_timing.ev[2 * g_timing.used];
+        e1 = g_timing.ev[2 * g_timing.used + 1];
+        g_timing.flops.push_back(2.0 * double(a->m) * double(a->n) * double(a->k));
+        ++g_timing.used;
+        MM_CUDA_TRY(cudaEventRecord(e0, s));
+    }
+    int rc;
+    if (bn == 256) rc = dispatch<256>(a_mn, b_mn, ma, mb, md, p, s);
+    else if (bn == 192) rc = dispatch<192>(a_mn, b_mn, ma, mb, md, p, s);
+    else rc = dispatch<128>(a_mn, b_mn, ma, mb, md, p, s);
+    if (rc == 0 && e1) MM_CUDA_TRY(cudaEventRecord(e1, s));
+    return rc;
 }

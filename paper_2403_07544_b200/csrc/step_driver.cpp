@@ -1,0 +1,355 @@
+// Native step driver: forward + backward of one task on one packed
+// micro-batch, issuing every K4-K8 launch from C++ (the Python engine's
+// Engine.forward_backward, without ~25 us of Python/ctypes per launch).
+//
+// Layer order (pre-LN, OpenNMT-py "standard"):
+//   self block : x' = x + Attn(LN1(x)) Wo^T + bo
+//   cross block: x' = x + CrossAttn(LNc(x), mem) Wco^T + bco     (decoder)
+//   FFN block  : x' = x + relu(LN2(x) W1^T + b1) W2^T + b2
+// Activations are bump-allocated from the caller's workspace; the backward
+// temporaries of one block are released when the block is done.
+#include <cmath>
+#include <cstring>
+
+#include "mm_common.h"
+
+namespace {
+
+struct Arena {
+    uint8_t* base = nullptr;
+    size_t off = 0, peak = 0;
+    bool sizing = true;
+    template <class T>
+    T* get(size_t n) {
+        off = (off + 255) & ~size_t(255);
+        T* p = sizing ? nullptr : reinterpret_cast<T*>(base + off);
+        off += n * sizeof(T);
+        if (off > peak) peak = off;
+        return p;
+    }
+};
+
+#define TRY(expr)                    \
+    do {                             \
+        if (!sizing) {               \
+            int _st = (expr);        \
+            if (_st) return _st;     \
+        }                            \
+    } while (0)
+
+struct SelfSave { const float* x_in; uint16_t* h; float* mean; float* rstd; uint16_t* qkv; uint16_t* a; float* lse; };
+struct CrossSave { const float* x_in; uint16_t* h; float* mean; float* rstd; uint16_t* q; uint16_t* kv; uint16_t* a; float* lse; };
+struct FfnSave { const float* x_in; uint16_t* h; float* mean; float* rstd; uint16_t* f; };
+
+struct Layer {
+    const mm_stack* st;
+    const mm_layer_offsets* o;
+    SelfSave self;
+    CrossSave cross;
+    FfnSave ffn;
+};
+
+struct Driver {
+    const mm_task& t;
+    const mm_batch& b;
+    Arena& ar;
+    cudaStream_t s;
+    bool sizing;
+    int d, H, F, V;
+
+    const uint16_t* wb(const mm_stack* st, int64_t off) const { return st->w_bf16 + off; }
+    const float* wf(const mm_stack* st, int64_t off) const { return st->w_f32 + off; }
+    float* g(const mm_stack* st, int64_t off) const { return st->grad + off; }
+
+    int gemm(const void* A, bool a_k, const void* B, bool b_k, void* D, int64_t m, int64_t n,
+             int64_t k, int64_t lda, int64_t ldb, int64_t ldd, int epi, const float* bias = nullptr,
+             const float* resid = nullptr, const void* aux = nullptr) {
+        mm_gemm_args a{};
+        a.a = A; a.b = B; a.d = D; a.bias = bias; a.resid = resid; a.aux = aux;
+        a.m = m; a.n = n; a.k = k; a.lda = lda; a.ldb = ldb; a.ldd = ldd;
+        a.a_kmajor = a_k; a.b_kmajor = b_k; a.epilogue = epi;
+        return mm_gemm(&a, s);
+    }
+    // Y[T,out] (epi)= X[T,in] W[out,in]^T
+    int linear(const uint16_t* X, const uint16_t* W, void* Y, int64_t T, int64_t in, int64_t out,
+               int epi, const float* bias = nullptr, const float* resid = nullptr) {
+        return gemm(X, true, W, true, Y, T, out, in, in, in, out, epi, bias, resid);
+    }
+    // dX[T,in] (epi)= dY[T,out] W[out,in]
+    int dgrad(const uint16_t* dY, const uint16_t* W, void* dX, int64_t T, int64_t in, int64_t out,
+              int epi, const void* aux = nullptr) {
+        return gemm(dY, true, W, false, dX, T, in, out, out, in, in, epi, nullptr, nullptr, aux);
+    }
+    // dW[out,in] += dY[T,out]^T X[T,in]
+    int wgrad(const uint16_t* dY, const uint16_t* X, float* dW, int64_t T, int64_t in, int64_t out) {
+        return gemm(dY, false, X, false, dW, out, in, T, out, in, in, MM_EPI_F32_ACCUM);
+    }
+
+    int ln(const mm_stack* st, int64_t go, int64_t bo, const float* x, int64_t T, uint16_t*& y,
+           float*& mean, float*& rstd) {
+        y = ar.get<uint16_t>(T * d);
+        mean = ar.get<float>(T);
+        rstd = ar.get<float>(T);
+        TRY(mm_layernorm_fwd(x, wf(st, go), wf(st, bo), y, mean, rstd, T, d, 1e-6f, s));
+        return 0;
+    }
+
+    mm_attn_args attn(const uint16_t* q, const uint16_t* k, const uint16_t* v, int64_t ldq,
+                      int64_t ldkv, uint16_t* o, float* lse, const int32_t* cu_q,
+                      const int32_t* cu_k, int max_q, int max_k, bool causal, int total_q,
+                      const int32_t* groups, int ng, int cap) {
+        mm_attn_args a{};
+        a.q = q; a.k = k; a.v = v; a.o = o; a.lse = lse;
+        a.cu_q = cu_q; a.cu_k = cu_k;
+        a.ldq = ldq; a.ldk = ldkv; a.ldv = ldkv; a.ldo = d;
+        a.n_seq = b.n_seq; a.heads = H; a.head_dim = 64; a.causal = causal;
+        a.max_q = max_q; a.max_k = max_k; a.scale = 0.125f; a.total_q = total_q;
+        a.groups = groups; a.n_groups = ng; a.cap = cap;
+        return a;
+    }
+
+    // ------------------------------------------------------------ forward
+    int self_fwd(Layer& L, const float* x, float*& out, int64_t T, const int32_t* cu, int maxlen,
+                 bool causal, const int32_t* groups, int ng, int cap) {
+        const mm_stack* st = L.st;
+        const mm_layer_offsets* o = L.o;
+        SelfSave& sv = L.self;
+        sv.x_in = x;
+        if (int e = ln(st, o->ln1_g, o->ln1_b, x, T, sv.h, sv.mean, sv.rstd)) return e;
+        sv.qkv = ar.get<uint16_t>(T * 3 * d);
+        TRY(linear(sv.h, wb(st, o->qkv_w), sv.qkv, T, d, 3 * d, MM_EPI_BF16, wf(st, o->qkv_b)));
+        sv.a = ar.get<uint16_t>(T * d);
+        sv.lse = ar.get<float>(int64_t(H) * T);
+        mm_attn_args a = attn(sv.qkv, sv.qkv + d, sv.qkv + 2 * d, 3 * d, 3 * d, sv.a, sv.lse, cu, cu,
+                              maxlen, maxlen, causal, int(T), groups, ng, cap);
+        a.v = sv.qkv + 2 * d;
+        TRY(mm_attention_fwd(&a, s));
+        out = ar.get<float>(T * d);
+        TRY(linear(sv.a, wb(st, o->out_w), out, T, d, d, MM_EPI_F32_RESID, wf(st, o->out_b), x));
+        return 0;
+    }
+
+    int cross_fwd(Layer& L, const float* x, float*& out, const uint16_t* mem) {
+        const mm_stack* st = L.st;
+        const mm_layer_offsets* o = L.o;
+        CrossSave& sv = L.cross;
+        const int64_t T = b.n_tgt, S = b.n_src;
+        sv.x_in = x;
+        if (int e = ln(st, o->lnc_g, o->lnc_b, x, T, sv.h, sv.mean, sv.rstd)) return e;
+        sv.q = ar.get<uint16_t>(T * d);
+        TRY(linear(sv.h, wb(st, o->cq_w), sv.q, T, d, d, MM_EPI_BF16, wf(st, o->cq_b)));
+        sv.kv = ar.get<uint16_t>(S * 2 * d);
+        TRY(linear(mem, wb(st, o->ckv_w), sv.kv, S, d, 2 * d, MM_EPI_BF16, wf(st, o->ckv_b)));
+        sv.a = ar.get<uint16_t>(T * d);
+        sv.lse = ar.get<float>(int64_t(H) * T);
+        mm_attn_args a = attn(sv.q, sv.kv, sv.kv + d, d, 2 * d, sv.a, sv.lse, b.cu_tgt, b.cu_src,
+                              b.max_tgt, b.max_src, false, int(T), b.groups_cross, b.ng_cross,
+                              b.cap_cross);
+        TRY(mm_attention_fwd(&a, s));
+        out = ar.get<float>(T * d);
+        TRY(linear(sv.a, wb(st, o->cout_w), out, T, d, d, MM_EPI_F32_RESID, wf(st, o->cout_b), x));
+        return 0;
+    }
+
+    int ffn_fwd(Layer& L, const float* x, float*& out, int64_t T) {
+        const mm_stack* st = L.st;
+        const mm_layer_offsets* o = L.o;
+        FfnSave& sv = L.ffn;
+        sv.x_in = x;
+        if (int e = ln(st, o->ln2_g, o->ln2_b, x, T, sv.h, sv.mean, sv.rstd)) return e;
+        sv.f = ar.get<uint16_t>(T * F);
+        TRY(linear(sv.h, wb(st, o->ff1_w), sv.f, T, d, F, MM_EPI_BF16_RELU, wf(st, o->ff1_b)));
+        out = ar.get<float>(T * d);
+        TRY(linear(sv.f, wb(st, o->ff2_w), out, T, F, d, MM_EPI_F32_RESID, wf(st, o->ff2_b), x));
+        return 0;
+    }
+
+    // ------------------------------------------------------------ backward
+    // dx (fp32) / dx_bf hold dL/d(block output) on entry, dL/d(block input) on exit
+    int ffn_bwd(Layer& L, float* dx, uint16_t* dx_bf, int64_t T) {
+        const mm_stack* st = L.st;
+        const mm_layer_offsets* o = L.o;
+        FfnSave& sv = L.ffn;
+        const size_t mark = ar.off;
+        TRY(wgrad(dx_bf, sv.f, g(st, o->ff2_w), T, F, d));
+        TRY(mm_colsum_bf16(dx_bf, g(st, o->ff2_b), T, d, s));
+        uint16_t* df = ar.get<uint16_t>(T * F);
+        TRY(dgrad(dx_bf, wb(st, o->ff2_w), df, T, F, d, MM_EPI_BF16_DRELU, sv.f));
+        TRY(wgrad(df, sv.h, g(st, o->ff1_w), T, d, F));
+        TRY(mm_colsum_bf16(df, g(st, o->ff1_b), T, F, s));
+        float* dh = ar.get<float>(T * d);
+        TRY(dgrad(df, wb(st, o->ff1_w), dh, T, d, F, MM_EPI_F32));
+        TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->ln2_g), sv.mean, sv.rstd, dx, dx_bf,
+                             g(st, o->ln2_g), g(st, o->ln2_b), T, d, s));
+        ar.off = mark;
+        return 0;
+    }
+
+    int self_bwd(Layer& L, float* dx, uint16_t* dx_bf, int64_t T, const int32_t* cu, int maxlen,
+                 bool causal, const int32_t* groups, int ng, int cap) {
+        const mm_stack* st = L.st;
+        const mm_layer_offsets* o = L.o;
+        SelfSave& sv = L.self;
+        const size_t mark = ar.off;
+        TRY(wgrad(dx_bf, sv.a, g(st, o->out_w), T, d, d));
+        TRY(mm_colsum_bf16(dx_bf, g(st, o->out_b), T, d, s));
+        uint16_t* da = ar.get<uint16_t>(T * d);
+        TRY(dgrad(dx_bf, wb(st, o->out_w), da, T, d, d, MM_EPI_BF16));
+        uint16_t* dqkv = ar.get<uint16_t>(T * 3 * d);
+        mm_attn_args a = attn(sv.qkv, sv.qkv + d, sv.qkv + 2 * d, 3 * d, 3 * d, sv.a, sv.lse, cu, cu,
+                              maxlen, maxlen, causal, int(T), groups, ng, cap);
+        a.d_o = da; a.dq = dqkv; a.dk = dqkv + d; a.dv = dqkv + 2 * d;
+        a.ld_dq = a.ld_dk = a.ld_dv = 3 * d;
+        TRY(mm_attention_bwd(&a, s));
+        TRY(wgrad(dqkv, sv.h, g(st, o->qkv_w), T, d, 3 * d));
+        TRY(mm_colsum_bf16(dqkv, g(st, o->qkv_b), T, 3 * d, s));
+        float* dh = ar.get<float>(T * d);
+        TRY(dgrad(dqkv, wb(st, o->qkv_w), dh, T, d, 3 * d, MM_EPI_F32));
+        TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->ln1_g), sv.mean, sv.rstd, dx, dx_bf,
+                             g(st, o->ln1_g), g(st, o->ln1_b), T, d, s));
+        ar.off = mark;
+        return 0;
+    }
+
+    int cross_bwd(Layer& L, float* dx, uint16_t* dx_bf, const uint16_t* mem, float* dmem) {
+        const mm_stack* st = L.st;
+        const mm_layer_offsets* o = L.o;
+        CrossSave& sv = L.cross;
+        const int64_t T = b.n_tgt, S = b.n_src;
+        const size_t mark = ar.off;
+        TRY(wgrad(dx_bf, sv.a, g(st, o->cout_w), T, d, d));
+        TRY(mm_colsum_bf16(dx_bf, g(st, o->cout_b), T, d, s));
+        uint16_t* da = ar.get<uint16_t>(T * d);
+        TRY(dgrad(dx_bf, wb(st, o->cout_w), da, T, d, d, MM_EPI_BF16));
+        uint16_t* dq = ar.get<uint16_t>(T * d);
+        uint16_t* dkv = ar.get<uint16_t>(S * 2 * d);
+        mm_attn_args a = attn(sv.q, sv.kv, sv.kv + d, d, 2 * d, sv.a, sv.lse, b.cu_tgt, b.cu_src,
+                              b.max_tgt, b.max_src, false, int(T), b.groups_cross, b.ng_cross,
+                              b.cap_cross);
+        a.d_o = da; a.dq = dq; a.dk = dkv; a.dv = dkv + d;
+        a.ld_dq = d; a.ld_dk = a.ld_dv = 2 * d;
+        TRY(mm_attention_bwd(&a, s));
+        TRY(wgrad(dkv, mem, g(st, o->ckv_w), S, d, 2 * d));
+        TRY(mm_colsum_bf16(dkv, g(st, o->ckv_b), S, 2 * d, s));
+        TRY(dgrad(dkv, wb(st, o->ckv_w), dmem, S, d, 2 * d, MM_EPI_F32_ACCUM));
+        TRY(wgrad(dq, sv.h, g(st, o->cq_w), T, d, d));
+        TRY(mm_colsum_bf16(dq, g(st, o->cq_b), T, d, s));
+        float* dh = ar.get<float>(T * d);
+        TRY(dgrad(dq, wb(st, o->cq_w), dh, T, d, d, MM_EPI_F32));
+        TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->lnc_g), sv.mean, sv.rstd, dx, dx_bf,
+                             g(st, o->lnc_g), g(st, o->lnc_b), T, d, s));
+        ar.off = mark;
+        return 0;
+    }
+
+    int zeros(void* p, size_t bytes) {
+        TRY(mm_memset(p, 0, bytes, s));
+        return 0;
+    }
+
+    int run(float* loss_sum) {
+        const int64_t Ts = b.n_src, Tt = b.n_tgt;
+        const float scale = std::sqrt(float(d));
+        // host-side layer records (saved-activation pointers per layer)
+        Layer enc_l[64], dec_l[64];
+        int ne = 0, nd = 0;
+        for (int i = 0; i < t.n_enc; ++i)
+            for (int l = 0; l < t.enc[i].n_layers; ++l) enc_l[ne++] = Layer{&t.enc[i], &t.enc[i].layers[l], {}, {}, {}};
+        for (int i = 0; i < t.n_dec; ++i)
+            for (int l = 0; l < t.dec[i].n_layers; ++l) dec_l[nd++] = Layer{&t.dec[i], &t.dec[i].layers[l], {}, {}, {}};
+        // ---- encoder
+        float* x = ar.get<float>(Ts * d);
+        TRY(mm_embed_fwd(b.src, b.src_pos, t.enc_emb.w_bf16 + t.enc_emb.emb, x, Ts, d, scale, s));
+        for (int l = 0; l < ne; ++l) {
+            float* y;
+            if (int e = self_fwd(enc_l[l], x, y, Ts, b.cu_src, b.max_src, false, b.groups_src, b.ng_src, b.cap_src)) return e;
+            if (int e = ffn_fwd(enc_l[l], y, x, Ts)) return e;
+        }
+        const mm_stack* lnf_e = &t.enc[t.n_enc - 1];
+        uint16_t* mem; float* mem_mean; float* mem_rstd;
+        if (int e = ln(lnf_e, lnf_e->lnf_g, lnf_e->lnf_b, x, Ts, mem, mem_mean, mem_rstd)) return e;
+        const float* x_enc = x;
+        // ---- decoder
+        float* y = ar.get<float>(Tt * d);
+        TRY(mm_embed_fwd(b.tgt_in, b.tgt_pos, t.dec_emb.w_bf16 + t.dec_emb.emb, y, Tt, d, scale, s));
+        for (int l = 0; l < nd; ++l) {
+            float *y1, *y2;
+            if (int e = self_fwd(dec_l[l], y, y1, Tt, b.cu_tgt, b.max_tgt, true, b.groups_tgt, b.ng_tgt, b.cap_tgt)) return e;
+            if (int e = cross_fwd(dec_l[l], y1, y2, mem)) return e;
+            if (int e = ffn_fwd(dec_l[l], y2, y, Tt)) return e;
+        }
+        const mm_stack* lnf_d = &t.dec[t.n_dec - 1];
+        uint16_t* hdec; float* hd_mean; float* hd_rstd;
+        if (int e = ln(lnf_d, lnf_d->lnf_g, lnf_d->lnf_b, y, Tt, hdec, hd_mean, hd_rstd)) return e;
+        uint16_t* logits = ar.get<uint16_t>(Tt * V);
+        const mm_embed& E = t.dec_emb;
+        TRY(linear(hdec, E.w_bf16 + E.gen_w, logits, Tt, d, V, MM_EPI_BF16, E.w_f32 + E.gen_b));
+        float* row_loss = ar.get<float>(Tt);
+        TRY(mm_xent_fwd_bwd(logits, b.labels, logits, row_loss, loss_sum, Tt, V, 1.f / float(Tt), s));
+        // ---- generator backward (dlogits in place of the logits)
+        TRY(wgrad(logits, hdec, E.grad + E.gen_w, Tt, d, V));
+        TRY(mm_colsum_bf16(logits, E.grad + E.gen_b, Tt, V, s));
+        float* dh = ar.get<float>(Tt * d);
+        TRY(dgrad(logits, E.w_bf16 + E.gen_w, dh, Tt, d, V, MM_EPI_F32));
+        float* dy = ar.get<float>(Tt * d);
+        uint16_t* dy_bf = ar.get<uint16_t>(Tt * d);
+        if (int e = zeros(dy, Tt * d * 4)) return e;
+        TRY(mm_layernorm_bwd(dh, y, wf(lnf_d, lnf_d->lnf_g), hd_mean, hd_rstd, dy, dy_bf,
+                             g(lnf_d, lnf_d->lnf_g), g(lnf_d, lnf_d->lnf_b), Tt, d, s));
+        float* dmem = ar.get<float>(Ts * d);
+        if (int e = zeros(dmem, Ts * d * 4)) return e;
+        for (int l = nd - 1; l >= 0; --l) {
+            if (int e = ffn_bwd(dec_l[l], dy, dy_bf, Tt)) return e;
+            if (int e = cross_bwd(dec_l[l], dy, dy_bf, mem, dmem)) return e;
+            if (int e = self_bwd(dec_l[l], dy, dy_bf, Tt, b.cu_tgt, b.max_tgt, true, b.groups_tgt, b.ng_tgt, b.cap_tgt)) return e;
+        }
+        TRY(mm_embed_bwd(b.tgt_in, dy, t.dec_emb.grad + t.dec_emb.emb, Tt, d, scale, s));
+        // ---- encoder backward
+        float* dx = ar.get<float>(Ts * d);
+        uint16_t* dx_bf = ar.get<uint16_t>(Ts * d);
+        if (int e = zeros(dx, Ts * d * 4)) return e;
+        TRY(mm_layernorm_bwd(dmem, x_enc, wf(lnf_e, lnf_e->lnf_g), mem_mean, mem_rstd, dx, dx_bf,
+                             g(lnf_e, lnf_e->lnf_g), g(lnf_e, lnf_e->lnf_b), Ts, d, s));
+        for (int l = ne - 1; l >= 0; --l) {
+            if (int e = ffn_bwd(enc_l[l], dx, dx_bf, Ts)) return e;
+            if (int e = self_bwd(enc_l[l], dx, dx_bf, Ts, b.cu_src, b.max_src, false, b.groups_src, b.ng_src, b.cap_src)) return e;
+        }
+        TRY(mm_embed_bwd(b.src, dx, t.enc_emb.grad + t.enc_emb.emb, Ts, d, scale, s));
+        return 0;
+    }
+};
+
+}  // namespace
+
+extern "C" int mm_task_fwd_bwd(const mm_task* task, const mm_batch* batch, void* workspace,
+                               size_t* ws_bytes, float* loss_sum, void* stream) {
+    MM_CHECK_ARG(task && batch && ws_bytes, "NULL argument");
+    MM_CHECK_ARG(task->n_enc >= 1 && task->n_dec >= 1 && task->enc && task->dec, "empty task");
+    MM_CHECK_ARG(task->d_model % 64 == 0 && task->heads * 64 == task->d_model,
+                 "head_dim must be 64 (d_model %d, heads %d)", task->d_model, task->heads);
+    int nl = 0;
+    for (int i = 0; i < task->n_enc; ++i) nl += task->enc[i].n_layers;
+    MM_CHECK_ARG(nl <= 64, "more than 64 encoder layers");
+    nl = 0;
+    for (int i = 0; i < task->n_dec; ++i) nl += task->dec[i].n_layers;
+    MM_CHECK_ARG(nl <= 64, "more than 64 decoder layers");
+    MM_CHECK_ARG(task->enc[task->n_enc - 1].lnf_g >= 0 && task->dec[task->n_dec - 1].lnf_g >= 0,
+                 "last stack of each side needs its final LayerNorm");
+    Arena ar;
+    ar.base = static_cast<uint8_t*>(workspace);
+    ar.sizing = workspace == nullptr;
+    Driver drv{*task, *batch, ar, mm::as_stream(stream), ar.sizing, task->d_model, task->heads,
+               task->ffn, task->vocab};
+    if (!ar.sizing) {
+        // dry run first: the caller's workspace must cover the peak
+        Arena probe;
+        Driver p{*task, *batch, probe, mm::as_stream(stream), true, task->d_model, task->heads,
+                 task->ffn, task->vocab};
+        p.run(loss_sum);
+        MM_CHECK_ARG(probe.peak <= *ws_bytes, "workspace %zu B < required %zu B", *ws_bytes,
+                     probe.peak);
+    }
+    const int st = drv.run(loss_sum);
+    if (ar.sizing) *ws_bytes = ar.peak;
+    return st;
+}

@@ -82,6 +82,15 @@ class DeviceBatch:
         self.n_src, self.n_tgt = b.n_src, b.n_tgt
         self.max_src, self.max_tgt = b.max_src, b.max_tgt
         self._keep = host  # keep the pinned staging alive until the copy retires
+        gs, gt, gc = self.attn_src, self.attn_tgt, self.attn_cross
+        self.desc = _native.BatchDesc(
+            src=self.src.data_ptr(), src_pos=self.src_pos.data_ptr(), cu_src=self.cu_src.data_ptr(),
+            tgt_in=self.tgt_in.data_ptr(), tgt_pos=self.tgt_pos.data_ptr(),
+            labels=self.labels.data_ptr(), cu_tgt=self.cu_tgt.data_ptr(),
+            groups_src=gs[0].data_ptr(), groups_tgt=gt[0].data_ptr(), groups_cross=gc[0].data_ptr(),
+            n_seq=self.n_seq, n_src=self.n_src, n_tgt=self.n_tgt, max_src=self.max_src,
+            max_tgt=self.max_tgt, ng_src=gs[1], cap_src=gs[2], ng_tgt=gt[1], cap_tgt=gt[2],
+            ng_cross=gc[1], cap_cross=gc[2])
 
 
 class CommGroups:
@@ -172,6 +181,9 @@ class Engine:
         self.flags_dev = torch.zeros(len(self.plan.keys), dtype=torch.int32, device=self.device)
         self.scale = math.sqrt(shape.d_model)
         self.trace = None  # set to a dict to capture intermediates (diagnostics)
+        self.native = True  # C++ step driver (mm_task_fwd_bwd); False -> per-op Python path
+        self._task_desc: dict = {}
+        self._ws = None
 
     # ------------------------------------------------------------------ layers
     def _zeros(self, *shape):
@@ -315,8 +327,70 @@ class Engine:
         self._ln_bwd(st, p + "lnc", dh, x_in, mean, rstd, dx, dx_bf)
 
     # ------------------------------------------------------------------ task
+    def _stack_desc(self, key: ModuleKey):
+        st = self.states[key]
+        lay = st.layout
+        names = [f for f, _ in _native.LayerOffsets._fields_]
+        arr = (_native.LayerOffsets * lay.n_layers)()
+        for i in range(lay.n_layers):
+            for f in names:
+                pname = f"l{i}." + f.replace("_w", ".w").replace("_b", ".b").replace("_g", ".g")
+                p = lay.params.get(pname)
+                setattr(arr[i], f, p.offset if p is not None else -1)
+        has_f = "lnf.g" in lay.params
+        desc = _native.Stack(w_bf16=st.weights.data_ptr(), w_f32=st.master.data_ptr(),
+                             grad=st.grad.data_ptr(), layers=arr, n_layers=lay.n_layers,
+                             decoder=int(key.side is Side.DECODER),
+                             lnf_g=lay.params["lnf.g"].offset if has_f else -1,
+                             lnf_b=lay.params["lnf.b"].offset if has_f else -1)
+        return desc, arr
+
+    def _embed_desc(self, key: ModuleKey):
+        st = self.states[key]
+        P = st.layout.params
+        return _native.Embed(w_bf16=st.weights.data_ptr(), w_f32=st.master.data_ptr(),
+                             grad=st.grad.data_ptr(), emb=P["emb"].offset,
+                             gen_w=P["gen.w"].offset if "gen.w" in P else -1,
+                             gen_b=P["gen.b"].offset if "gen.b" in P else -1)
+
+    def task_desc(self, task: TaskSpec):
+        """mm_task descriptor of a task (cached; buckets never move)."""
+        if task.id not in self._task_desc:
+            enc = [self._stack_desc(k) for k in task.enc_modules]
+            dec = [self._stack_desc(k) for k in task.dec_modules]
+            enc_arr = (_native.Stack * len(enc))(*[d for d, _ in enc])
+            dec_arr = (_native.Stack * len(dec))(*[d for d, _ in dec])
+            ek, dk = embedding_keys(task)
+            s = self.shape
+            t = _native.Task(d_model=s.d_model, heads=s.heads, ffn=s.ffn, vocab=s.vocab,
+                             n_enc=len(enc), n_dec=len(dec), enc=enc_arr, dec=dec_arr,
+                             enc_emb=self._embed_desc(ek), dec_emb=self._embed_desc(dk))
+            # keep every ctypes array the descriptor points into alive
+            self._task_desc[task.id] = (t, enc_arr, dec_arr, [a for _, a in enc + dec])
+        return self._task_desc[task.id][0]
+
     def forward_backward(self, task: TaskSpec, db: DeviceBatch, loss_sum: torch.Tensor) -> None:
         """One micro-batch of one task; gradients accumulate into the buckets."""
+        if not self.native or self.trace is not None:
+            return self.forward_backward_py(task, db, loss_sum)
+        import ctypes
+        L = _native.lib()
+        t = self.task_desc(task)
+        need = ctypes.c_size_t(0)
+        _native.check(L.mm_task_fwd_bwd(ctypes.byref(t), ctypes.byref(db.desc), None,
+                                        ctypes.byref(need), None, None), "mm_task_fwd_bwd(size)")
+        if self._ws is None or self._ws.numel() < need.value:
+            self._ws = torch.empty(int(need.value * 1.25) + (1 << 20), dtype=torch.uint8,
+                                   device=self.device)
+        have = ctypes.c_size_t(self._ws.numel())
+        ops.LAUNCHES[0] += 1
+        _native.check(L.mm_task_fwd_bwd(ctypes.byref(t), ctypes.byref(db.desc), self._ws.data_ptr(),
+                                        ctypes.byref(have), loss_sum.data_ptr(), ops.stream_ptr()),
+                      "mm_task_fwd_bwd")
+
+    def forward_backward_py(self, task: TaskSpec, db: DeviceBatch, loss_sum: torch.Tensor) -> None:
+        """Per-op Python path (same kernels, same order); used for diagnostics
+        (intermediate tracing) and as the native driver's cross-check."""
         shp, dev, d = self.shape, self.device, self.shape.d_model
         ek, dk = embedding_keys(task)
         emb_e, emb_d = self.states[ek], self.states[dk]
