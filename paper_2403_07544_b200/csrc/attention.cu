@@ -66,14 +66,23 @@ __device__ __forceinline__ float quad_sum(float v) {
     return v + __shfl_xor_sync(0xffffffffu, v, 2);
 }
 
-// rows [0, n) of a 64-wide head slice -> smem (pitch kP), rows [n, npad) zeroed
+// rows [0, n) of a 64-wide head slice -> smem (pitch kP), rows [n, npad) zeroed.
+// cp.async (16 B, L2-only) so every copy of the CTA is in flight at once; the
+// caller waits with cp_async_wait_all() + __syncthreads().
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
 __device__ __forceinline__ void stage(uint16_t* dst, const uint16_t* src, int64_t ld, int n,
                                       int npad, int tid, int nthr) {
     for (int idx = tid; idx < npad * 8; idx += nthr) {
         const int r = idx >> 3, c = idx & 7;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (r < n) v = *reinterpret_cast<const uint4*>(src + r * ld + c * 8);
-        *reinterpret_cast<uint4*>(dst + r * kP + c * 8) = v;
+        const bool valid = r < n;
+        cp_async16(dst + r * kP + c * 8, valid ? src + r * ld + c * 8 : src, valid);
     }
 }
 
@@ -141,21 +150,28 @@ struct Group {
     int k0[kMaxSeqPerGroup], lk[kMaxSeqPerGroup], koff[kMaxSeqPerGroup];
 };
 
-__device__ __forceinline__ void load_group(Group& G, const mm_attn_args& a) {
+// called by warp 0: lane i loads sequence i of the group, offsets by warp scan
+__device__ __forceinline__ void load_group(Group& G, const mm_attn_args& a, int lane) {
     const int first = a.groups[2 * blockIdx.x], n = a.groups[2 * blockIdx.x + 1];
-    G.n = n;
-    int qo = 0, ko = 0;
-    for (int i = 0; i < n; ++i) {
-        const int sq = first + i;
-        G.q0[i] = a.cu_q[sq];
-        G.lq[i] = a.cu_q[sq + 1] - G.q0[i];
-        G.k0[i] = a.cu_k[sq];
-        G.lk[i] = a.cu_k[sq + 1] - G.k0[i];
-        G.qoff[i] = qo;
-        G.koff[i] = ko;
-        qo += (G.lq[i] + 31) & ~31;
-        ko += (G.lk[i] + 31) & ~31;
+    int q0 = 0, lq = 0, k0 = 0, lk = 0;
+    if (lane < n) {
+        q0 = a.cu_q[first + lane];
+        lq = a.cu_q[first + lane + 1] - q0;
+        k0 = a.cu_k[first + lane];
+        lk = a.cu_k[first + lane + 1] - k0;
     }
+    int pq = (lq + 31) & ~31, pk = (lk + 31) & ~31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {  // inclusive scan
+        const int xq = __shfl_up_sync(0xffffffffu, pq, o), xk = __shfl_up_sync(0xffffffffu, pk, o);
+        if (lane >= o) { pq += xq; pk += xk; }
+    }
+    if (lane < n) {
+        G.q0[lane] = q0; G.lq[lane] = lq; G.k0[lane] = k0; G.lk[lane] = lk;
+        G.qoff[lane] = pq - ((lq + 31) & ~31);
+        G.koff[lane] = pk - ((lk + 31) & ~31);
+    }
+    if (lane == 0) G.n = n;
 }
 
 // tile -> (sequence, 16-row tile start); tiles enumerate the group's
@@ -196,12 +212,13 @@ __global__ void __launch_bounds__(kFwdWarps * 32) attn_fwd_kernel(const mm_attn_
     extern __shared__ __align__(16) uint16_t sm[];
     __shared__ Group G;
     const int h = blockIdx.y;
-    if (threadIdx.x == 0) load_group(G, a);
+    if (threadIdx.x < 32) load_group(G, a, threadIdx.x);
     __syncthreads();
     uint16_t* Qs = sm;
     uint16_t* Ks = Qs + a.cap * kP;
     uint16_t* Vs = Ks + a.cap * kP;
     stage_group(Qs, Ks, Vs, nullptr, G, a, h, kFwdWarps * 32);
+    cp_async_wait_all();
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
@@ -289,7 +306,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) attn_bwd_kernel(const mm_attn_
     extern __shared__ __align__(16) uint16_t sm[];
     __shared__ Group G;
     const int h = blockIdx.y;
-    if (threadIdx.x == 0) load_group(G, a);
+    if (threadIdx.x < 32) load_group(G, a, threadIdx.x);
     __syncthreads();
     uint16_t* Qs = sm;
     uint16_t* dOs = Qs + a.cap * kP;
@@ -304,6 +321,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) attn_bwd_kernel(const mm_attn_
         for (int r = threadIdx.x; r < pq; r += nthr)
             lse2[G.qoff[i] + r] = r < G.lq[i] ? a.lse[int64_t(h) * a.total_q + G.q0[i] + r] * kLog2e : 0.f;
     }
+    cp_async_wait_all();
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;

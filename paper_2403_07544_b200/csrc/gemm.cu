@@ -38,10 +38,10 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle row of bf16
 constexpr int UMMA_K = 16;
-constexpr int kThreads = 192;
 constexpr int kEpiWarp0 = 2;
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, each half the columns
+constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
 
-constexpr int kEpiWarps = 4;
 constexpr int kEpiBufBytes = 32 * 128;                    // 32 rows x 128 B box
 constexpr int kEpiSmem = kEpiWarps * 2 * kEpiBufBytes;    // double-buffered per warp
 constexpr int kSmemLimit = 232448;
@@ -80,12 +80,17 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 }
 
 // Epilogue math for one row (this thread) x 32 columns held in registers.
-__device__ __forceinline__ void epilogue_math(const Params& p, int64_t row, int64_t col0,
-                                              float (&acc)[32], int lane) {
+__device__ __forceinline__ bool has_bias(const Params& p) {
     const int ep = p.epilogue;
-    if (p.bias && (ep == MM_EPI_BF16 || ep == MM_EPI_BF16_RELU || ep == MM_EPI_F32 ||
-                   ep == MM_EPI_F32_RESID)) {
-        const float bv = (col0 + lane < p.n) ? __ldg(p.bias + col0 + lane) : 0.f;
+    return p.bias && (ep == MM_EPI_BF16 || ep == MM_EPI_BF16_RELU || ep == MM_EPI_F32 ||
+                      ep == MM_EPI_F32_RESID);
+}
+
+// bv: this lane's bias value for column col0 + lane (preloaded per tile)
+__device__ __forceinline__ void epilogue_math(const Params& p, int64_t row, int64_t col0,
+                                              float (&acc)[32], float bv) {
+    const int ep = p.epilogue;
+    if (has_bias(p)) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) acc[j] += __shfl_sync(0xffffffffu, bv, j);
     }
@@ -191,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             tc::mbar_init(&tfull_bar[a], 1);
-            tc::mbar_init(&tempty_bar[a], 128);
+            tc::mbar_init(&tempty_bar[a], kEpiWarps * 32);
         }
         tc::fence_barrier_init();
     }
@@ -281,10 +286,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ------------------------------------------------------------ epilogue
-        const int lane_grp = warp & 3;  // TMEM lanes this warp may access
+        const int lane_grp = warp & 3;                   // TMEM lanes this warp may access
+        const int half = (warp - kEpiWarp0) >> 2;        // which half of the tile's columns
+        constexpr int kChunks = BN / 32 / 2;             // 32-column chunks per warp
         const bool out_bf16 = p.epilogue == MM_EPI_BF16 || p.epilogue == MM_EPI_BF16_RELU ||
                               p.epilogue == MM_EPI_BF16_DRELU;
         const bool reduce = p.epilogue == MM_EPI_F32_ACCUM;
+        const bool bias = has_bias(p);
         uint8_t* bufs = smem_epi + (warp - kEpiWarp0) * 2 * kEpiBufBytes;
         int nbuf = 0;
         int local = 0;
@@ -293,34 +301,44 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
+            const int cbase = tn * BN + half * (BN / 2);
+            // bias for this warp's columns, fetched before waiting on the MMAs
+            float bv[kChunks];
+#pragma unroll
+            for (int c = 0; c < kChunks; ++c) {
+                const int col = cbase + c * 32 + lane;
+                bv[c] = (bias && col < p.n) ? __ldg(p.bias + col) : 0.f;
+            }
             tc::mbar_wait(&tfull_bar[acc], acc_phase);
             tc::tc_fence_after();
             const int row0 = tm * BM + lane_grp * 32;  // this warp's first row
             const int64_t row = int64_t(row0) + lane;
-            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) + acc * BN;
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                const int col0 = tn * BN + c * 32;
-                if (col0 >= p.n) break;
-                uint32_t v[32];
-                tc::tmem_ld_32x32(t_row + c * 32, v);
-                tc::tmem_ld_wait();
-                float f[32];
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) + acc * BN +
+                                   half * (BN / 2);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-                epilogue_math(p, row, col0, f, lane);
-                uint8_t* buf = bufs + nbuf * kEpiBufBytes;
-                if (lane == 0) tc::bulk_wait_read<1>();  // the store that last read `buf` is done
-                __syncwarp();
-                stage_row(buf, lane, f, out_bf16);
-                tc::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    if (reduce) tc::tma_reduce_add_2d(&tmap_d, buf, col0, row0);
-                    else tc::tma_store_2d(&tmap_d, buf, col0, row0);
-                    tc::bulk_commit();
+            for (int c = 0; c < kChunks; ++c) {
+                const int col0 = cbase + c * 32;
+                if (col0 < p.n) {
+                    uint32_t v[32];
+                    tc::tmem_ld_32x32(t_row + c * 32, v);
+                    tc::tmem_ld_wait();
+                    float f[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+                    epilogue_math(p, row, col0, f, bv[c]);
+                    uint8_t* buf = bufs + nbuf * kEpiBufBytes;
+                    if (lane == 0) tc::bulk_wait_read<1>();  // the store that last read `buf` is done
+                    __syncwarp();
+                    stage_row(buf, lane, f, out_bf16);
+                    tc::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (reduce) tc::tma_reduce_add_2d(&tmap_d, buf, col0, row0);
+                        else tc::tma_store_2d(&tmap_d, buf, col0, row0);
+                        tc::bulk_commit();
+                    }
+                    nbuf ^= 1;
                 }
-                nbuf ^= 1;
             }
             tc::tc_fence_before();
             tc::mbar_arrive(&tempty_bar[acc]);
@@ -454,7 +472,7 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
     const int a_mn = a->a_kmajor ? 0 : 1;
     const int b_mn = a->b_kmajor ? 0 : 1;
 
-    // tile width: minimise (waves of persistent CTAs) x (tile width)
+    // tile width: minimise waves x (tile width + per-tile overhead ~ 64 columns)
     const int64_t tiles_m = (a->m + BM - 1) / BM;
     const int sms = mm::num_sms();
     int bn = 128;
@@ -463,7 +481,7 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
         for (int cand : {256, 192, 128}) {
             if (cand > 128 && a->n <= cand - 64) continue;
             const int64_t t = tiles_m * ((a->n + cand - 1) / cand);
-            const double cost = double((t + sms - 1) / sms) * cand;
+            const double cost = double((t + sms - 1) / sms) * (cand + 64);
             if (cost < best - 1e-9) { best = cost; bn = cand; }
         }
     }
