@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 6
+#define MMB200_ABI_VERSION 7
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 
 int mm_abi_version(void);
@@ -148,6 +148,9 @@ typedef struct {
     int32_t a_kmajor, b_kmajor;
     int32_t epilogue;
     int32_t pad;
+    /* optional: dbias[m] += sum_k A[m, k] (the bias gradient of a wgrad
+     * dW = dY^T X, whose A operand is dY); requires MN-major A */
+    float* dbias;
 } mm_gemm_args;
 
 int mm_gemm(const mm_gemm_args* args, void* stream);

@@ -40,7 +40,8 @@ constexpr int BK = 64;  // one 128-byte swizzle row of bf16
 constexpr int UMMA_K = 16;
 constexpr int kEpiWarp0 = 2;
 constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, each half the columns
-constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
+constexpr int kBiasWarp = kEpiWarp0 + kEpiWarps;  // second consumer of every smem stage
+constexpr int kThreads = (kBiasWarp + 1) * 32;
 
 constexpr int kEpiBufBytes = 32 * 128;                    // 32 rows x 128 B box
 constexpr int kEpiSmem = kEpiWarps * 2 * kEpiBufBytes;    // double-buffered per warp
@@ -65,6 +66,7 @@ struct Params {
     const float* bias;
     const float* resid;
     const __nv_bfloat16* aux;
+    float* dbias;
     int epilogue;
     int tiles_m, tiles_n, splits, kb_per_split, num_kb;
     int units;
@@ -192,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < C::kStages; ++s) {
             tc::mbar_init(&full_bar[s], 1);
-            tc::mbar_init(&empty_bar[s], 1);
+            tc::mbar_init(&empty_bar[s], 2);  // MMA commit + bias warp
         }
         for (int a = 0; a < 2; ++a) {
             tc::mbar_init(&tfull_bar[a], 1);
@@ -283,6 +285,49 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (lane == 0) tc::mma_commit(&tfull_bar[acc]);
             __syncwarp();
+        }
+    } else if (warp == kBiasWarp) {
+        // ------------------------------------------------------------ bias-grad warp
+        // Second consumer of every smem stage.  For a wgrad (A = dY, MN-major)
+        // with dbias set, dbias[m] += sum_k dY[k, m]: the tiles_n CTAs that load
+        // the same A rows share the work -- N-column tn sums the k-blocks with
+        // kb % tiles_n == tn, so every k-block is summed exactly once.  Lane owns M = 4*lane..4*lane+3
+        // (box lane/16, 16B chunk (lane%16)/2, half lane%2; rows are K,
+        // 128B-swizzled).  Every stage is released here too (empty count 2).
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            const int tile = u / p.splits, split = u % p.splits;
+            const int kb0 = split * p.kb_per_split;
+            const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+            const bool bias_sum = A_MN && p.dbias != nullptr;
+            const int tn = tile / p.tiles_m;
+            float bsum[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int kb = kb0; kb < kb1; ++kb) {
+                tc::mbar_wait(&full_bar[stage], phase);
+                if (bias_sum && kb % p.tiles_n == tn) {
+                    const uint8_t* box = smem_a + stage * C::kABytes + (lane >> 4) * 64 * BK * 2;
+                    const int chunk = (lane & 15) >> 1, sub = (lane & 1) * 8;
+#pragma unroll 8
+                    for (int r = 0; r < BK; ++r) {
+                        const uint2 w = *reinterpret_cast<const uint2*>(
+                            box + r * 128 + ((chunk ^ (r & 7)) * 16) + sub);
+                        bsum[0] += bf16_to_f(w.x & 0xffff);
+                        bsum[1] += bf16_to_f(w.x >> 16);
+                        bsum[2] += bf16_to_f(w.y & 0xffff);
+                        bsum[3] += bf16_to_f(w.y >> 16);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&empty_bar[stage]);
+                if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+            }
+            if (bias_sum) {
+                const int64_t m = int64_t(tile % p.tiles_m) * BM + 4 * lane;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (m + i < p.m) atomicAdd(p.dbias + m + i, bsum[i]);
+            }
         }
     } else {
         // ------------------------------------------------------------ epilogue
@@ -469,6 +514,7 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
                  "D must be 16-byte aligned with 16-byte row stride");
     MM_CHECK_ARG(a->epilogue != MM_EPI_F32_RESID || a->resid, "RESID epilogue needs resid");
     MM_CHECK_ARG(a->epilogue != MM_EPI_BF16_DRELU || a->aux, "DRELU epilogue needs aux");
+    MM_CHECK_ARG(a->dbias == nullptr || !a->a_kmajor, "dbias needs an MN-major A operand");
     const int a_mn = a->a_kmajor ? 0 : 1;
     const int b_mn = a->b_kmajor ? 0 : 1;
 
@@ -515,6 +561,7 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
     p.m = a->m; p.n = a->n; p.k = a->k; p.ldd = a->ldd;
     p.d = a->d; p.bias = a->bias; p.resid = a->resid;
     p.aux = reinterpret_cast<const __nv_bfloat16*>(a->aux);
+    p.dbias = a->dbias;
     p.epilogue = a->epilogue;
     p.tiles_m = static_cast<int>(tiles_m);
     p.tiles_n = static_cast<int>(tiles_n);

@@ -63,9 +63,9 @@ struct Driver {
 
     int gemm(const void* A, bool a_k, const void* B, bool b_k, void* D, int64_t m, int64_t n,
              int64_t k, int64_t lda, int64_t ldb, int64_t ldd, int epi, const float* bias = nullptr,
-             const float* resid = nullptr, const void* aux = nullptr) {
+             const float* resid = nullptr, const void* aux = nullptr, float* dbias = nullptr) {
         mm_gemm_args a{};
-        a.a = A; a.b = B; a.d = D; a.bias = bias; a.resid = resid; a.aux = aux;
+        a.a = A; a.b = B; a.d = D; a.bias = bias; a.resid = resid; a.aux = aux; a.dbias = dbias;
         a.m = m; a.n = n; a.k = k; a.lda = lda; a.ldb = ldb; a.ldd = ldd;
         a.a_kmajor = a_k; a.b_kmajor = b_k; a.epilogue = epi;
         return mm_gemm(&a, s);
@@ -80,9 +80,11 @@ struct Driver {
               int epi, const void* aux = nullptr) {
         return gemm(dY, true, W, false, dX, T, in, out, out, in, in, epi, nullptr, nullptr, aux);
     }
-    // dW[out,in] += dY[T,out]^T X[T,in]
-    int wgrad(const uint16_t* dY, const uint16_t* X, float* dW, int64_t T, int64_t in, int64_t out) {
-        return gemm(dY, false, X, false, dW, out, in, T, out, in, in, MM_EPI_F32_ACCUM);
+    // dW[out,in] += dY[T,out]^T X[T,in];  db[out] += sum_t dY[t,out] (fused)
+    int wgrad(const uint16_t* dY, const uint16_t* X, float* dW, int64_t T, int64_t in, int64_t out,
+              float* db) {
+        return gemm(dY, false, X, false, dW, out, in, T, out, in, in, MM_EPI_F32_ACCUM, nullptr,
+                    nullptr, nullptr, db);
     }
 
     int ln(const mm_stack* st, int64_t go, int64_t bo, const float* x, int64_t T, uint16_t*& y,
@@ -171,12 +173,10 @@ struct Driver {
         const mm_layer_offsets* o = L.o;
         FfnSave& sv = L.ffn;
         const size_t mark = ar.off;
-        TRY(wgrad(dx_bf, sv.f, g(st, o->ff2_w), T, F, d));
-        TRY(mm_colsum_bf16(dx_bf, g(st, o->ff2_b), T, d, s));
+        TRY(wgrad(dx_bf, sv.f, g(st, o->ff2_w), T, F, d, g(st, o->ff2_b)));
         uint16_t* df = ar.get<uint16_t>(T * F);
         TRY(dgrad(dx_bf, wb(st, o->ff2_w), df, T, F, d, MM_EPI_BF16_DRELU, sv.f));
-        TRY(wgrad(df, sv.h, g(st, o->ff1_w), T, d, F));
-        TRY(mm_colsum_bf16(df, g(st, o->ff1_b), T, F, s));
+        TRY(wgrad(df, sv.h, g(st, o->ff1_w), T, d, F, g(st, o->ff1_b)));
         float* dh = ar.get<float>(T * d);
         TRY(dgrad(df, wb(st, o->ff1_w), dh, T, d, F, MM_EPI_F32));
         TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->ln2_g), sv.mean, sv.rstd, dx, dx_bf,
@@ -191,8 +191,7 @@ struct Driver {
         const mm_layer_offsets* o = L.o;
         SelfSave& sv = L.self;
         const size_t mark = ar.off;
-        TRY(wgrad(dx_bf, sv.a, g(st, o->out_w), T, d, d));
-        TRY(mm_colsum_bf16(dx_bf, g(st, o->out_b), T, d, s));
+        TRY(wgrad(dx_bf, sv.a, g(st, o->out_w), T, d, d, g(st, o->out_b)));
         uint16_t* da = ar.get<uint16_t>(T * d);
         TRY(dgrad(dx_bf, wb(st, o->out_w), da, T, d, d, MM_EPI_BF16));
         uint16_t* dqkv = ar.get<uint16_t>(T * 3 * d);
@@ -201,8 +200,7 @@ struct Driver {
         a.d_o = da; a.dq = dqkv; a.dk = dqkv + d; a.dv = dqkv + 2 * d;
         a.ld_dq = a.ld_dk = a.ld_dv = 3 * d;
         TRY(mm_attention_bwd(&a, s));
-        TRY(wgrad(dqkv, sv.h, g(st, o->qkv_w), T, d, 3 * d));
-        TRY(mm_colsum_bf16(dqkv, g(st, o->qkv_b), T, 3 * d, s));
+        TRY(wgrad(dqkv, sv.h, g(st, o->qkv_w), T, d, 3 * d, g(st, o->qkv_b)));
         float* dh = ar.get<float>(T * d);
         TRY(dgrad(dqkv, wb(st, o->qkv_w), dh, T, d, 3 * d, MM_EPI_F32));
         TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->ln1_g), sv.mean, sv.rstd, dx, dx_bf,
@@ -217,8 +215,7 @@ struct Driver {
         CrossSave& sv = L.cross;
         const int64_t T = b.n_tgt, S = b.n_src;
         const size_t mark = ar.off;
-        TRY(wgrad(dx_bf, sv.a, g(st, o->cout_w), T, d, d));
-        TRY(mm_colsum_bf16(dx_bf, g(st, o->cout_b), T, d, s));
+        TRY(wgrad(dx_bf, sv.a, g(st, o->cout_w), T, d, d, g(st, o->cout_b)));
         uint16_t* da = ar.get<uint16_t>(T * d);
         TRY(dgrad(dx_bf, wb(st, o->cout_w), da, T, d, d, MM_EPI_BF16));
         uint16_t* dq = ar.get<uint16_t>(T * d);
@@ -229,11 +226,9 @@ struct Driver {
         a.d_o = da; a.dq = dq; a.dk = dkv; a.dv = dkv + d;
         a.ld_dq = d; a.ld_dk = a.ld_dv = 2 * d;
         TRY(mm_attention_bwd(&a, s));
-        TRY(wgrad(dkv, mem, g(st, o->ckv_w), S, d, 2 * d));
-        TRY(mm_colsum_bf16(dkv, g(st, o->ckv_b), S, 2 * d, s));
+        TRY(wgrad(dkv, mem, g(st, o->ckv_w), S, d, 2 * d, g(st, o->ckv_b)));
         TRY(dgrad(dkv, wb(st, o->ckv_w), dmem, S, d, 2 * d, MM_EPI_F32_ACCUM));
-        TRY(wgrad(dq, sv.h, g(st, o->cq_w), T, d, d));
-        TRY(mm_colsum_bf16(dq, g(st, o->cq_b), T, d, s));
+        TRY(wgrad(dq, sv.h, g(st, o->cq_w), T, d, d, g(st, o->cq_b)));
         float* dh = ar.get<float>(T * d);
         TRY(dgrad(dq, wb(st, o->cq_w), dh, T, d, d, MM_EPI_F32));
         TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->lnc_g), sv.mean, sv.rstd, dx, dx_bf,
@@ -287,8 +282,7 @@ struct Driver {
         float* row_loss = ar.get<float>(Tt);
         TRY(mm_xent_fwd_bwd(logits, b.labels, logits, row_loss, loss_sum, Tt, V, 1.f / float(Tt), s));
         // ---- generator backward (dlogits in place of the logits)
-        TRY(wgrad(logits, hdec, E.grad + E.gen_w, Tt, d, V));
-        TRY(mm_colsum_bf16(logits, E.grad + E.gen_b, Tt, V, s));
+        TRY(wgrad(logits, hdec, E.grad + E.gen_w, Tt, d, V, E.grad + E.gen_b));
         float* dh = ar.get<float>(Tt * d);
         TRY(dgrad(logits, E.w_bf16 + E.gen_w, dh, Tt, d, V, MM_EPI_F32));
         float* dy = ar.get<float>(Tt * d);

@@ -265,13 +265,11 @@ class Engine:
         _, x_in, h, mean, rstd, f = rec
         T = x_in.shape[0]
         ops.gemm(dx_bf, f, st.g(p + "ff2.w"), a_kmajor=False, b_kmajor=False,
-                 epilogue=ops.EPI_F32_ACCUM)
-        ops.colsum(dx_bf, st.g(p + "ff2.b"))
+                 epilogue=ops.EPI_F32_ACCUM, dbias=st.g(p + "ff2.b"))
         df = torch.empty(T, self.shape.ffn, device=self.device, dtype=torch.bfloat16)
         ops.gemm(dx_bf, st.w(p + "ff2.w"), df, b_kmajor=False, epilogue=ops.EPI_BF16_DRELU, aux=f)
         ops.gemm(df, h, st.g(p + "ff1.w"), a_kmajor=False, b_kmajor=False,
-                 epilogue=ops.EPI_F32_ACCUM)
-        ops.colsum(df, st.g(p + "ff1.b"))
+                 epilogue=ops.EPI_F32_ACCUM, dbias=st.g(p + "ff1.b"))
         dh = torch.empty(T, self.shape.d_model, device=self.device)
         ops.gemm(df, st.w(p + "ff1.w"), dh, b_kmajor=False, epilogue=ops.EPI_F32)
         self._ln_bwd(st, p + "ln2", dh, x_in, mean, rstd, dx, dx_bf)
@@ -281,8 +279,7 @@ class Engine:
         d = self.shape.d_model
         T = x_in.shape[0]
         ops.gemm(dx_bf, a, st.g(p + "out.w"), a_kmajor=False, b_kmajor=False,
-                 epilogue=ops.EPI_F32_ACCUM)
-        ops.colsum(dx_bf, st.g(p + "out.b"))
+                 epilogue=ops.EPI_F32_ACCUM, dbias=st.g(p + "out.b"))
         da = torch.empty(T, d, device=self.device, dtype=torch.bfloat16)
         ops.gemm(dx_bf, st.w(p + "out.w"), da, b_kmajor=False, epilogue=ops.EPI_BF16)
         dqkv = torch.empty(T, 3 * d, device=self.device, dtype=torch.bfloat16)
@@ -291,8 +288,7 @@ class Engine:
                                           dq=dqkv[:, :d], dk=dqkv[:, d:2 * d], dv=dqkv[:, 2 * d:],
                                           groups=groups))
         ops.gemm(dqkv, h, st.g(p + "qkv.w"), a_kmajor=False, b_kmajor=False,
-                 epilogue=ops.EPI_F32_ACCUM)
-        ops.colsum(dqkv, st.g(p + "qkv.b"))
+                 epilogue=ops.EPI_F32_ACCUM, dbias=st.g(p + "qkv.b"))
         dh = torch.empty(T, d, device=self.device)
         ops.gemm(dqkv, st.w(p + "qkv.w"), dh, b_kmajor=False, epilogue=ops.EPI_F32)
         self._ln_bwd(st, p + "ln1", dh, x_in, mean, rstd, dx, dx_bf)
@@ -302,8 +298,7 @@ class Engine:
         d = self.shape.d_model
         T, S = x_in.shape[0], mem.shape[0]
         ops.gemm(dx_bf, a, st.g(p + "cout.w"), a_kmajor=False, b_kmajor=False,
-                 epilogue=ops.EPI_F32_ACCUM)
-        ops.colsum(dx_bf, st.g(p + "cout.b"))
+                 epilogue=ops.EPI_F32_ACCUM, dbias=st.g(p + "cout.b"))
         da = torch.empty(T, d, device=self.device, dtype=torch.bfloat16)
         ops.gemm(dx_bf, st.w(p + "cout.w"), da, b_kmajor=False, epilogue=ops.EPI_BF16)
         dq = torch.empty(T, d, device=self.device, dtype=torch.bfloat16)
@@ -316,12 +311,10 @@ class Engine:
         self._tr(p + "dca", da)
         self._tr(p + "dcx_out", dx)
         ops.gemm(dkv, mem, st.g(p + "ckv.w"), a_kmajor=False, b_kmajor=False,
-                 epilogue=ops.EPI_F32_ACCUM)
-        ops.colsum(dkv, st.g(p + "ckv.b"))
+                 epilogue=ops.EPI_F32_ACCUM, dbias=st.g(p + "ckv.b"))
         ops.gemm(dkv, st.w(p + "ckv.w"), dmem, b_kmajor=False, epilogue=ops.EPI_F32_ACCUM)
         ops.gemm(dq, h, st.g(p + "cq.w"), a_kmajor=False, b_kmajor=False,
-                 epilogue=ops.EPI_F32_ACCUM)
-        ops.colsum(dq, st.g(p + "cq.b"))
+                 epilogue=ops.EPI_F32_ACCUM, dbias=st.g(p + "cq.b"))
         dh = torch.empty(T, d, device=self.device)
         ops.gemm(dq, st.w(p + "cq.w"), dh, b_kmajor=False, epilogue=ops.EPI_F32)
         self._ln_bwd(st, p + "lnc", dh, x_in, mean, rstd, dx, dx_bf)
@@ -441,8 +434,7 @@ class Engine:
         self._tr("dlogits", dlogits)
         # ---- generator backward
         ops.gemm(dlogits, hdec, emb_d.g("gen.w"), a_kmajor=False, b_kmajor=False,
-                 epilogue=ops.EPI_F32_ACCUM)
-        ops.colsum(dlogits, emb_d.g("gen.b"))
+                 epilogue=ops.EPI_F32_ACCUM, dbias=emb_d.g("gen.b"))
         dh = torch.empty(Tt, d, device=dev)
         ops.gemm(dlogits, emb_d.w("gen.w"), dh, b_kmajor=False, epilogue=ops.EPI_F32)
         del logits, dlogits

@@ -26,6 +26,7 @@ class GemmArgs(ctypes.Structure):
         ("lda", ctypes.c_int64), ("ldb", ctypes.c_int64), ("ldd", ctypes.c_int64),
         ("a_kmajor", ctypes.c_int32), ("b_kmajor", ctypes.c_int32),
         ("epilogue", ctypes.c_int32), ("pad", ctypes.c_int32),
+        ("dbias", ctypes.c_void_p),
     ]
 
 
@@ -73,7 +74,8 @@ def _rowstride(t: torch.Tensor, name: str) -> int:
 
 
 def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bool = True,
-         b_kmajor: bool = True, epilogue: int = EPI_BF16, bias=None, resid=None, aux=None) -> None:
+         b_kmajor: bool = True, epilogue: int = EPI_BF16, bias=None, resid=None, aux=None,
+         dbias=None) -> None:
     """d[M,N] (epilogue)= op(a) @ op(b)^T on tcgen05.
 
     a: [M,K] if a_kmajor else [K,M]; b: [N,K] if b_kmajor else [K,N] (bf16).
@@ -91,7 +93,8 @@ def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bool = 
     args = GemmArgs(a=a.data_ptr(), b=b.data_ptr(), d=d.data_ptr(), bias=_ptr(bias),
                     resid=_ptr(resid), aux=_ptr(aux), m=m, n=n, k=k,
                     lda=_rowstride(a, "a"), ldb=_rowstride(b, "b"), ldd=_rowstride(d, "d"),
-                    a_kmajor=int(a_kmajor), b_kmajor=int(b_kmajor), epilogue=epilogue)
+                    a_kmajor=int(a_kmajor), b_kmajor=int(b_kmajor), epilogue=epilogue,
+                    dbias=_ptr(dbias))
     if resid is not None and _rowstride(resid, "resid") != args.ldd:
         raise ValueError("resid must share d's row stride")
     if aux is not None and _rowstride(aux, "aux") != args.ldd:

@@ -72,9 +72,12 @@ def test_gemm_wgrad_accumulate(cuda, shape):
     dy = torch.randn(t, n_out, device=cuda, generator=g).bfloat16()
     x = torch.randn(t, n_in, device=cuda, generator=g).bfloat16()
     dw = torch.randn(n_out, n_in, device=cuda, generator=g)
+    db = torch.randn(n_out, device=cuda, generator=g)
     ref = dw + dy.float().t() @ x.float()
-    ops.gemm(dy, x, dw, a_kmajor=False, b_kmajor=False, epilogue=ops.EPI_F32_ACCUM)
+    ref_b = db + dy.float().sum(0)
+    ops.gemm(dy, x, dw, a_kmajor=False, b_kmajor=False, epilogue=ops.EPI_F32_ACCUM, dbias=db)
     assert rel_err(dw, ref) < 2e-3
+    assert rel_err(db, ref_b) < 1e-4  # fused bias gradient (column sums of dY)
 
 
 def test_layernorm(cuda):

@@ -1,0 +1,45 @@
+"""Back-to-back GEMM timing per shape (CUDA events), for kernel tuning."""
+import os, sys
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2403_07544_b200 import ops
+dev = torch.device("cuda:0")
+T = 4096
+cases = [  # name, m, n, k, a_k, b_k, epi
+    ("fwd qkv", T, 1536, 512, True, True, ops.EPI_BF16),
+    ("fwd out", T, 512, 512, True, True, ops.EPI_F32),
+    ("fwd ff1", T, 2048, 512, True, True, ops.EPI_BF16_RELU),
+    ("fwd ff2", T, 512, 2048, True, True, ops.EPI_F32),
+    ("fwd gen", T, 32000, 512, True, True, ops.EPI_BF16),
+    ("dgrad out", T, 512, 512, True, False, ops.EPI_F32),
+    ("dgrad ff2", T, 2048, 512, True, False, ops.EPI_BF16),
+    ("dgrad ff1", T, 512, 2048, True, False, ops.EPI_F32),
+    ("dgrad gen", T, 512, 32000, True, False, ops.EPI_F32),
+    ("wgrad out", 512, 512, T, False, False, ops.EPI_F32_ACCUM),
+    ("wgrad qkv", 1536, 512, T, False, False, ops.EPI_F32_ACCUM),
+    ("wgrad ff1", 2048, 512, T, False, False, ops.EPI_F32_ACCUM),
+    ("wgrad ff2", 512, 2048, T, False, False, ops.EPI_F32_ACCUM),
+    ("wgrad gen", 32000, 512, T, False, False, ops.EPI_F32_ACCUM),
+    ("tiny", 128, 128, 64, True, True, ops.EPI_F32),
+]
+sel = sys.argv[1:] or None
+for name, m, n, k, ak, bk, epi in cases:
+    if sel and not any(s in name for s in sel):
+        continue
+    A = torch.randn(m, k, device=dev).bfloat16() if ak else torch.randn(k, m, device=dev).bfloat16()
+    B = torch.randn(n, k, device=dev).bfloat16() if bk else torch.randn(k, n, device=dev).bfloat16()
+    bf = epi in (ops.EPI_BF16, ops.EPI_BF16_RELU, ops.EPI_BF16_DRELU)
+    D = torch.zeros(m, n, device=dev, dtype=torch.bfloat16 if bf else torch.float32)
+    bias = torch.zeros(n, device=dev) if epi in (ops.EPI_BF16, ops.EPI_BF16_RELU) else None
+    for _ in range(3):
+        ops.gemm(A, B, D, a_kmajor=ak, b_kmajor=bk, epilogue=epi, bias=bias)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_it = 50
+    e0.record()
+    for _ in range(n_it):
+        ops.gemm(A, B, D, a_kmajor=ak, b_kmajor=bk, epilogue=epi, bias=bias)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / n_it
+    print(f"{name:10s} {m:6d}x{n:6d}x{k:6d}  {us:8.2f} us  {2*m*n*k/us/1e6:8.1f} TFLOP/s")
