@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) attn_fwd_kernel(const mm_attn_
 // ---------------------------------------------------------------------------
 constexpr int kBwdWarps = 8;
 
-__global__ void __launch_bounds__(kBwdWarps * 32) attn_bwd_kernel(const mm_attn_args a) {
+__global__ void __launch_bounds__(kBwdWarps * 32, 2) attn_bwd_kernel(const mm_attn_args a) {
     extern __shared__ __align__(16) uint16_t sm[];
     __shared__ Group G;
     const int h = blockIdx.y;
@@ -398,53 +398,52 @@ __global__ void __launch_bounds__(kBwdWarps * 32) attn_bwd_kernel(const mm_attn_
         const int lq = G.lq[sidx], lk = G.lk[sidx], k0 = G.k0[sidx], qo = G.qoff[sidx];
         const uint16_t* Qseq = Qs + qo * kP;
         const uint16_t* dOseq = dOs + qo * kP;
-        uint32_t kf[4][4], vf[4][4];
+        uint32_t kf[4][4];
         load_a(kf, Ks + (G.koff[sidx] + kt) * kP, lane);
-        load_a(vf, Vs + (G.koff[sidx] + kt) * kP, lane);
         const int key0 = kt + g, key1 = key0 + 8;
-        float dk[8][4], dv[8][4];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            dk[i][0] = dk[i][1] = dk[i][2] = dk[i][3] = 0.f;
-            dv[i][0] = dv[i][1] = dv[i][2] = dv[i][3] = 0.f;
-        }
         const int qbeg = a.causal ? (kt & ~31) : 0;
-        for (int qb = qbeg; qb < lq; qb += 32) {
-            float st[4][4], dpt[4][4];
-            zero(st);
-            zero(dpt);
-            mma_abt(st, kf, Qseq, qb, lane);    // S^T = K Q^T
-            mma_abt(dpt, vf, dOseq, qb, lane);  // dP^T = V dO^T
+        // two passes keep the live set under 128 registers: pass 0 dV = P^T dO,
+        // pass 1 dK = dS^T Q (S^T recomputed; the MMAs are cheap here)
+        for (int pass = 0; pass < 2; ++pass) {
+            float acc[8][4];
 #pragma unroll
-            for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int q = qb + nt * 8 + 2 * t + (e & 1);
-                    const int key = e < 2 ? key0 : key1;
-                    float p = 0.f;
-                    if (q < lq && key < lk && !(a.causal && key > q))
-                        p = exp2f(st[nt][e] * c - lse2[qo + q]);
-                    st[nt][e] = p;
-                    dpt[nt][e] = p * (dpt[nt][e] - Dd[qo + q]);
+            for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+            uint32_t vf[4][4];
+            if (pass == 1) load_a(vf, Vs + (G.koff[sidx] + kt) * kP, lane);
+            for (int qb = qbeg; qb < lq; qb += 32) {
+                float st[4][4], dpt[4][4];
+                zero(st);
+                mma_abt(st, kf, Qseq, qb, lane);    // S^T = K Q^T
+                if (pass == 1) {
+                    zero(dpt);
+                    mma_abt(dpt, vf, dOseq, qb, lane);  // dP^T = V dO^T
                 }
-            mma_pb(dv, st, dOseq, qb, lane);   // dV += P^T dO
-            mma_pb(dk, dpt, Qseq, qb, lane);   // dK += dS^T Q
-        }
-        uint16_t* v0 = a.dv + int64_t(k0 + key0) * a.ld_dv + h * kHd;
-        uint16_t* v1 = a.dv + int64_t(k0 + key1) * a.ld_dv + h * kHd;
-        uint16_t* kk0 = a.dk + int64_t(k0 + key0) * a.ld_dk + h * kHd;
-        uint16_t* kk1 = a.dk + int64_t(k0 + key1) * a.ld_dk + h * kHd;
 #pragma unroll
-        for (int nt = 0; nt < 8; ++nt) {
-            if (key0 < lk) {
-                *reinterpret_cast<uint32_t*>(v0 + nt * 8 + 2 * t) = pack(dv[nt][0], dv[nt][1]);
-                *reinterpret_cast<uint32_t*>(kk0 + nt * 8 + 2 * t) =
-                    pack(dk[nt][0] * a.scale, dk[nt][1] * a.scale);
+                for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int q = qb + nt * 8 + 2 * t + (e & 1);
+                        const int key = e < 2 ? key0 : key1;
+                        float p = 0.f;
+                        if (q < lq && key < lk && !(a.causal && key > q))
+                            p = exp2f(st[nt][e] * c - lse2[qo + q]);
+                        if (pass == 0) st[nt][e] = p;
+                        else dpt[nt][e] = p * (dpt[nt][e] - Dd[qo + q]);
+                    }
+                if (pass == 0) mma_pb(acc, st, dOseq, qb, lane);   // dV += P^T dO
+                else mma_pb(acc, dpt, Qseq, qb, lane);              // dK += dS^T Q
             }
-            if (key1 < lk) {
-                *reinterpret_cast<uint32_t*>(v1 + nt * 8 + 2 * t) = pack(dv[nt][2], dv[nt][3]);
-                *reinterpret_cast<uint32_t*>(kk1 + nt * 8 + 2 * t) =
-                    pack(dk[nt][2] * a.scale, dk[nt][3] * a.scale);
+            const float sc = pass == 0 ? 1.f : a.scale;
+            uint16_t* base = pass == 0 ? a.dv : a.dk;
+            const int64_t ld = pass == 0 ? a.ld_dv : a.ld_dk;
+            uint16_t* o0 = base + int64_t(k0 + key0) * ld + h * kHd;
+            uint16_t* o1 = base + int64_t(k0 + key1) * ld + h * kHd;
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+                if (key0 < lk)
+                    *reinterpret_cast<uint32_t*>(o0 + nt * 8 + 2 * t) = pack(acc[nt][0] * sc, acc[nt][1] * sc);
+                if (key1 < lk)
+                    *reinterpret_cast<uint32_t*>(o1 + nt * 8 + 2 * t) = pack(acc[nt][2] * sc, acc[nt][3] * sc);
             }
         }
     }
