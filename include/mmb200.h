@@ -158,6 +158,9 @@ int mm_gemm(const mm_gemm_args* args, void* stream);
  * mode 0: stop, synchronise and return total flops (2MNK), summed launch
  * time (ms) and launch count since the last start. */
 int mm_gemm_timing(int mode, double* flops, float* ms, int* launches);
+/* diagnostics: per-CTA %globaltimer stamps of every later mm_gemm launch into
+ * dev_buf[8 * cta + slot] (NULL disables); see gemm.cu for the slots */
+int mm_gemm_trace(unsigned long long* dev_buf);
 
 /* ---------------------------------------------------------------------------
  * K6: LayerNorm over rows of x (fp32 residual stream) -> bf16, saving

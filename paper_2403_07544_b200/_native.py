@@ -169,6 +169,7 @@ def _declare(h: ctypes.CDLL) -> None:
     # layer kernels (K4-K8)
     sig("mm_gemm", c_int, c_void_p, c_void_p)
     sig("mm_gemm_timing", c_int, c_int, POINTER(c_double), POINTER(c_float), POINTER(c_int))
+    sig("mm_gemm_trace", c_int, c_void_p)
     sig("mm_layernorm_fwd", c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
         c_int64, c_int, c_float, c_void_p)
     sig("mm_layernorm_bwd", c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) attn_fwd_kernel(const mm_attn_
     extern __shared__ __align__(16) uint16_t sm[];
     __shared__ Group G;
     const int h = blockIdx.y;
+    pdl_wait();
     if (threadIdx.x < 32) load_group(G, a, threadIdx.x);
     __syncthreads();
     uint16_t* Qs = sm;
@@ -306,6 +307,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 2) attn_bwd_kernel(const mm_at
     extern __shared__ __align__(16) uint16_t sm[];
     __shared__ Group G;
     const int h = blockIdx.y;
+    pdl_wait();
     if (threadIdx.x < 32) load_group(G, a, threadIdx.x);
     __syncthreads();
     uint16_t* Qs = sm;
@@ -473,7 +475,8 @@ extern "C" int mm_attention_fwd(const mm_attn_args* a, void* stream) {
     const size_t smem = fwd_smem(*a);
     MM_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-    attn_fwd_kernel<<<dim3(a->n_groups, a->heads), kFwdWarps * 32, smem, mm::as_stream(stream)>>>(*a);
+    MM_CUDA_TRY(mm::launch_pdl(attn_fwd_kernel, dim3(a->n_groups, a->heads), dim3(kFwdWarps * 32),
+                               smem, mm::as_stream(stream), *a));
     MM_LAUNCH_CHECK("attn_fwd_kernel");
     return 0;
 }
@@ -485,7 +488,8 @@ extern "C" int mm_attention_bwd(const mm_attn_args* a, void* stream) {
     MM_CHECK_ARG(smem <= 227 * 1024, "attention backward needs %zu B of smem", smem);
     MM_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-    attn_bwd_kernel<<<dim3(a->n_groups, a->heads), kBwdWarps * 32, smem, mm::as_stream(stream)>>>(*a);
+    MM_CUDA_TRY(mm::launch_pdl(attn_bwd_kernel, dim3(a->n_groups, a->heads), dim3(kBwdWarps * 32),
+                               smem, mm::as_stream(stream), *a));
     MM_LAUNCH_CHECK("attn_bwd_kernel");
     return 0;
 }

@@ -27,6 +27,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -67,10 +68,24 @@ struct Params {
     const float* resid;
     const __nv_bfloat16* aux;
     float* dbias;
+    unsigned long long* trace;  // optional per-CTA phase timestamps (diagnostics)
     int epilogue;
     int tiles_m, tiles_n, splits, kb_per_split, num_kb;
     int units;
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// trace slots per CTA: 0 entry, 1 setup done, 2 first stage full (MMA warp),
+// 3 last commit issued, 4 first tfull seen (epilogue warp 2), 5 epilogue
+// done (warp 2), 6 stores drained (warp 2), 7 exit
+#define MM_TRACE(slot)                                                                   \
+    do {                                                                                 \
+        if (p.trace) p.trace[blockIdx.x * 8 + (slot)] = gtime();                         \
+    } while (0)
 
 __device__ __forceinline__ float bf16_to_f(uint16_t h) {
     return __uint_as_float(static_cast<uint32_t>(h) << 16);
@@ -185,6 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) MM_TRACE(0);
 
     if (warp == 0 && lane == 0) {
         tc::tma_prefetch(&tmap_a);
@@ -207,6 +223,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) MM_TRACE(1);
+    pdl_wait();  // everything above overlapped the previous kernel's tail
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
@@ -263,6 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kb = kb0; kb < kb1; ++kb) {
                 tc::mbar_wait(&full_bar[stage], phase);
                 tc::tc_fence_after();
+                if (lane == 0 && local == 0 && kb == kb0) MM_TRACE(2);
                 if (lane == 0) {
                     const uint32_t sa = tc::smem_u32(smem_a + stage * C::kABytes);
                     const uint32_t sb = tc::smem_u32(smem_b + stage * C::kBBytes);
@@ -284,6 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (++stage == C::kStages) { stage = 0; phase ^= 1; }
             }
             if (lane == 0) tc::mma_commit(&tfull_bar[acc]);
+            if (lane == 0) MM_TRACE(3);
             __syncwarp();
         }
     } else if (warp == kBiasWarp) {
@@ -356,6 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tc::mbar_wait(&tfull_bar[acc], acc_phase);
             tc::tc_fence_after();
+            if (warp == kEpiWarp0 && lane == 0 && local == 0) MM_TRACE(4);
             const int row0 = tm * BM + lane_grp * 32;  // this warp's first row
             const int64_t row = int64_t(row0) + lane;
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) + acc * BN +
@@ -388,13 +409,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::tc_fence_before();
             tc::mbar_arrive(&tempty_bar[acc]);
         }
+        if (warp == kEpiWarp0 && lane == 0) MM_TRACE(5);
         if (lane == 0) tc::bulk_wait_all();
+        if (warp == kEpiWarp0 && lane == 0) MM_TRACE(6);
     }
+    pdl_trigger();
     __syncthreads();
     if (warp == 1) {
         tc::tc_fence_after();
         tc::tmem_dealloc(tmem_base, C::kTmemCols);
     }
+    if (threadIdx.x == 0) MM_TRACE(7);
 }
 
 // ----------------------------------------------------------------------------
@@ -451,7 +476,7 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md, 
         attr_set = true;
     }
     const int grid = std::min(p.units, mm::num_sms());
-    kern<<<grid, kThreads, Cfg<BN>::kSmem, s>>>(ma, mb, md, p);
+    MM_CUDA_TRY(mm::launch_pdl(kern, dim3(grid), dim3(kThreads), Cfg<BN>::kSmem, s, ma, mb, md, p));
     MM_LAUNCH_CHECK("gemm_tcgen05_kernel");
     return 0;
 }
@@ -465,6 +490,8 @@ int dispatch(int a_mn, int b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
     return launch<BN, 1, 1>(ma, mb, md, p, s);
 }
 
+unsigned long long* g_trace_buf = nullptr;  // set by mm_gemm_trace (diagnostics)
+
 // optional per-launch timing (roofline evidence inside bench.py)
 struct GemmTiming {
     bool on = false;
@@ -474,6 +501,13 @@ struct GemmTiming {
 } g_timing;
 
 }  // namespace
+
+// diagnostics: device buffer of >= 8 * num_SMs u64 for per-CTA phase stamps of
+// subsequent mm_gemm launches (NULL disables)
+extern "C" int mm_gemm_trace(unsigned long long* dev_buf) {
+    g_trace_buf = dev_buf;
+    return 0;
+}
 
 extern "C" int mm_gemm_timing(int mode, double* flops, float* ms, int* launches) {
     if (mode == 1) {
@@ -531,6 +565,10 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
             if (cost < best - 1e-9) { best = cost; bn = cand; }
         }
     }
+    if (const char* force = std::getenv("MM_GEMM_BN")) {  // diagnostics
+        const int f = std::atoi(force);
+        if (f == 128 || f == 192 || f == 256) bn = f;
+    }
     const int64_t tiles_n = (a->n + bn - 1) / bn;
     const int num_kb = static_cast<int>((a->k + BK - 1) / BK);
     const int64_t tiles = tiles_m * tiles_n;
@@ -562,6 +600,7 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
     p.d = a->d; p.bias = a->bias; p.resid = a->resid;
     p.aux = reinterpret_cast<const __nv_bfloat16*>(a->aux);
     p.dbias = a->dbias;
+    p.trace = g_trace_buf;
     p.epilogue = a->epilogue;
     p.tiles_m = static_cast<int>(tiles_m);
     p.tiles_n = static_cast<int>(tiles_n);

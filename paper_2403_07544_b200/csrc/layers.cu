@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x
                                                      const float* __restrict__ beta,
                                                      uint16_t* __restrict__ y, float* mean_out,
                                                      float* rstd_out, int64_t rows, float eps) {
+    pdl_wait();
     constexpr int V = COLS / 128;
     const int lane = threadIdx.x & 31;
     const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ d
                                                      const float* __restrict__ rstd, float* dx,
                                                      uint16_t* dx_bf16, float* dgamma,
                                                      float* dbeta, int64_t rows) {
+    pdl_wait();
     constexpr int V = COLS / 128;
     __shared__ float red_g[8][COLS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -157,6 +159,7 @@ __global__ void __launch_bounds__(256) embed_fwd_kernel(const int32_t* __restric
                                                         const uint16_t* __restrict__ table,
                                                         float* __restrict__ out, int64_t rows,
                                                         int cols, float scale) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
     if (row >= rows) return;
@@ -186,6 +189,7 @@ __global__ void __launch_bounds__(256) embed_bwd_kernel(const int32_t* __restric
                                                         const float* __restrict__ dout,
                                                         float* dtable, int64_t rows, int cols,
                                                         float scale) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
     if (row >= rows) return;
@@ -211,6 +215,7 @@ __global__ void __launch_bounds__(kXentThreads) xent_kernel(const uint16_t* logi
                                                             uint16_t* dlogits, float* row_loss,
                                                             float* loss_sum, int vocab,
                                                             float grad_scale) {
+    pdl_wait();
     __shared__ float sm_m[kXentThreads / 32], sm_s[kXentThreads / 32];
     const int64_t row = blockIdx.x;
     const int label = labels[row];
@@ -299,6 +304,7 @@ __global__ void __launch_bounds__(kXentThreads) xent_kernel(const uint16_t* logi
 // row lanes in smem and leave with one atomic per column.
 __global__ void __launch_bounds__(256) colsum_kernel(const uint16_t* __restrict__ x, float* out,
                                                      int64_t rows, int cols, int64_t slab) {
+    pdl_wait();
     __shared__ float red[8][256 + 8];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int c8 = blockIdx.x * 32 + tx;
@@ -333,6 +339,7 @@ __global__ void __launch_bounds__(256) colsum_kernel(const uint16_t* __restrict_
 }
 
 __global__ void cast_kernel(const float* __restrict__ x, uint16_t* __restrict__ y, int64_t n4) {
+    pdl_wait();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4;
          i += int64_t(gridDim.x) * blockDim.x) {
         const float4 v = reinterpret_cast<const float4*>(x)[i];
@@ -353,13 +360,13 @@ extern "C" int mm_layernorm_fwd(const float* x, const float* gamma, const float*
     const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
     auto s = mm::as_stream(stream);
     if (cols == 512)
-        ln_fwd_kernel<512><<<grid, 256, 0, s>>>(x, gamma, beta, y, mean, rstd, rows, eps);
+        MM_CUDA_TRY(mm::launch_pdl(ln_fwd_kernel<512>, dim3(grid), dim3(256), 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
     else if (cols == 1024)
-        ln_fwd_kernel<1024><<<grid, 256, 0, s>>>(x, gamma, beta, y, mean, rstd, rows, eps);
+        MM_CUDA_TRY(mm::launch_pdl(ln_fwd_kernel<1024>, dim3(grid), dim3(256), 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
     else if (cols == 128)
-        ln_fwd_kernel<128><<<grid, 256, 0, s>>>(x, gamma, beta, y, mean, rstd, rows, eps);
+        MM_CUDA_TRY(mm::launch_pdl(ln_fwd_kernel<128>, dim3(grid), dim3(256), 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
     else if (cols == 256)
-        ln_fwd_kernel<256><<<grid, 256, 0, s>>>(x, gamma, beta, y, mean, rstd, rows, eps);
+        MM_CUDA_TRY(mm::launch_pdl(ln_fwd_kernel<256>, dim3(grid), dim3(256), 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
     else {
         mm::set_error("layernorm: cols=%d unsupported (128/256/512/1024)", cols);
         return mm::kUnsupported;
@@ -376,13 +383,13 @@ extern "C" int mm_layernorm_bwd(const float* dy, const float* x, const float* ga
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((rows + 7) / 8, 4 * mm::num_sms()));
     auto s = mm::as_stream(stream);
     if (cols == 512)
-        ln_bwd_kernel<512><<<grid, 256, 0, s>>>(dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows);
+        MM_CUDA_TRY(mm::launch_pdl(ln_bwd_kernel<512>, dim3(grid), dim3(256), 0, s, dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows));
     else if (cols == 1024)
-        ln_bwd_kernel<1024><<<grid, 256, 0, s>>>(dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows);
+        MM_CUDA_TRY(mm::launch_pdl(ln_bwd_kernel<1024>, dim3(grid), dim3(256), 0, s, dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows));
     else if (cols == 128)
-        ln_bwd_kernel<128><<<grid, 256, 0, s>>>(dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows);
+        MM_CUDA_TRY(mm::launch_pdl(ln_bwd_kernel<128>, dim3(grid), dim3(256), 0, s, dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows));
     else if (cols == 256)
-        ln_bwd_kernel<256><<<grid, 256, 0, s>>>(dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows);
+        MM_CUDA_TRY(mm::launch_pdl(ln_bwd_kernel<256>, dim3(grid), dim3(256), 0, s, dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows));
     else {
         mm::set_error("layernorm: cols=%d unsupported (128/256/512/1024)", cols);
         return mm::kUnsupported;
@@ -396,8 +403,7 @@ extern "C" int mm_embed_fwd(const int32_t* ids, const int32_t* pos, const uint16
     MM_CHECK_ARG(ids && pos && table && out, "NULL argument");
     MM_CHECK_ARG(cols % 4 == 0, "cols must be a multiple of 4");
     if (rows == 0) return 0;
-    embed_fwd_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, mm::as_stream(stream)>>>(
-        ids, pos, table, out, rows, cols, scale);
+    MM_CUDA_TRY(mm::launch_pdl(embed_fwd_kernel, dim3(static_cast<unsigned>((rows + 7) / 8)), dim3(256), 0, mm::as_stream(stream), ids, pos, table, out, rows, cols, scale));
     MM_LAUNCH_CHECK("embed_fwd_kernel");
     return 0;
 }
@@ -407,8 +413,7 @@ extern "C" int mm_embed_bwd(const int32_t* ids, const float* dout, float* dtable
     MM_CHECK_ARG(ids && dout && dtable, "NULL argument");
     MM_CHECK_ARG(cols % 4 == 0, "cols must be a multiple of 4");
     if (rows == 0) return 0;
-    embed_bwd_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, mm::as_stream(stream)>>>(
-        ids, dout, dtable, rows, cols, scale);
+    MM_CUDA_TRY(mm::launch_pdl(embed_bwd_kernel, dim3(static_cast<unsigned>((rows + 7) / 8)), dim3(256), 0, mm::as_stream(stream), ids, dout, dtable, rows, cols, scale));
     MM_LAUNCH_CHECK("embed_bwd_kernel");
     return 0;
 }
@@ -419,8 +424,7 @@ extern "C" int mm_xent_fwd_bwd(const uint16_t* logits, const int32_t* labels, ui
     MM_CHECK_ARG(logits && labels && dlogits && row_loss, "NULL argument");
     MM_CHECK_ARG(vocab % 8 == 0, "vocab must be a multiple of 8");
     if (rows == 0) return 0;
-    xent_kernel<<<static_cast<unsigned>(rows), kXentThreads, 0, mm::as_stream(stream)>>>(
-        logits, labels, dlogits, row_loss, loss_sum, vocab, grad_scale);
+    MM_CUDA_TRY(mm::launch_pdl(xent_kernel, dim3(static_cast<unsigned>(rows)), dim3(kXentThreads), 0, mm::as_stream(stream), logits, labels, dlogits, row_loss, loss_sum, vocab, grad_scale));
     MM_LAUNCH_CHECK("xent_kernel");
     return 0;
 }
@@ -434,7 +438,7 @@ extern "C" int mm_colsum_bf16(const uint16_t* x, float* out, int64_t rows, int c
     const int64_t slab = (rows + slabs - 1) / slabs;
     slabs = (rows + slab - 1) / slab;
     dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(slabs));
-    colsum_kernel<<<grid, 256, 0, mm::as_stream(stream)>>>(x, out, rows, cols, slab);
+    MM_CUDA_TRY(mm::launch_pdl(colsum_kernel, dim3(grid), dim3(256), 0, mm::as_stream(stream), x, out, rows, cols, slab));
     MM_LAUNCH_CHECK("colsum_kernel");
     return 0;
 }
@@ -444,7 +448,7 @@ extern "C" int mm_cast_f32_bf16(const float* x, uint16_t* y, int64_t n, void* st
     if (n == 0) return 0;
     const int64_t n4 = n / 4;
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n4 + 255) / 256, 8 * mm::num_sms()));
-    cast_kernel<<<grid, 256, 0, mm::as_stream(stream)>>>(x, y, n4);
+    MM_CUDA_TRY(mm::launch_pdl(cast_kernel, dim3(grid), dim3(256), 0, mm::as_stream(stream), x, y, n4));
     MM_LAUNCH_CHECK("cast_kernel");
     return 0;
 }

@@ -40,6 +40,7 @@ __device__ __forceinline__ int find_module(const int64_t* begin, int n, int64_t 
 }
 
 __global__ void __launch_bounds__(kThreads) sync_emulated_kernel(const __grid_constant__ SyncTable t) {
+    pdl_wait();
     const int64_t chunk = blockIdx.x;
     const int m = find_module(t.chunk_begin, t.n_mods, chunk);
     const mm_sync_module& md = t.mod[m];
@@ -127,6 +128,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 }
 
 __global__ void __launch_bounds__(kThreads) fused_update_kernel(const __grid_constant__ AdamTable t) {
+    pdl_wait();
     const int64_t chunk = blockIdx.x;
     const int mi = find_module(t.chunk_begin, t.n_mods, chunk);
     const mm_adam_module& md = t.mod[mi];
@@ -190,6 +192,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 __global__ void axpy_kernel(float* __restrict__ y, const float* __restrict__ x, float alpha,
                             int64_t n) {
+    pdl_wait();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x)
         y[i] = fmaf(alpha, x[i], y[i]);
@@ -229,7 +232,8 @@ extern "C" int mm_sync_emulated(const mm_sync_module* mods, int n_mods, int only
         }
         t.chunk_begin[t.n_mods] = chunks;
         if (chunks == 0) continue;
-        sync_emulated_kernel<<<(unsigned)chunks, kThreads, 0, mm::as_stream(stream)>>>(t);
+        MM_CUDA_TRY(mm::launch_pdl(sync_emulated_kernel, dim3((unsigned)chunks), dim3(kThreads), 0,
+                                   mm::as_stream(stream), t));
         MM_LAUNCH_CHECK("sync_emulated_kernel");
     }
     return 0;
@@ -265,7 +269,8 @@ extern "C" int mm_fused_update(const mm_adam_module* mods, int n_mods, const mm_
         t.n_mods = used;
         t.chunk_begin[used] = chunks;
         if (chunks == 0) continue;
-        fused_update_kernel<<<(unsigned)chunks, kThreads, 0, mm::as_stream(stream)>>>(t);
+        MM_CUDA_TRY(mm::launch_pdl(fused_update_kernel, dim3((unsigned)chunks), dim3(kThreads), 0,
+                                   mm::as_stream(stream), t));
         MM_LAUNCH_CHECK("fused_update_kernel");
     }
     return 0;
@@ -280,7 +285,8 @@ extern "C" int mm_axpy_f32(float* y, const float* x, float alpha, int64_t n, voi
     MM_CHECK_ARG((y && x) || n == 0, "NULL pointer");
     if (n == 0) return 0;
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 8 * mm::num_sms()));
-    axpy_kernel<<<grid, 256, 0, mm::as_stream(stream)>>>(y, x, alpha, n);
+    MM_CUDA_TRY(mm::launch_pdl(axpy_kernel, dim3(grid), dim3(256), 0, mm::as_stream(stream), y, x,
+                               alpha, n));
     MM_LAUNCH_CHECK("axpy_kernel");
     return 0;
 }
