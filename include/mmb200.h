@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 7
+#define MMB200_ABI_VERSION 8
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 
 int mm_abi_version(void);
@@ -147,7 +147,10 @@ typedef struct {
     int64_t lda, ldb, ldd; /* row strides in elements */
     int32_t a_kmajor, b_kmajor;
     int32_t epilogue;
-    int32_t pad;
+    /* 1: B was not written by the immediately preceding kernel on the stream
+     * (weights; earlier activations), so its first stages may be fetched
+     * before griddepcontrol.wait */
+    int32_t b_prefetch;
     /* optional: dbias[m] += sum_k A[m, k] (the bias gradient of a wgrad
      * dW = dY^T X, whose A operand is dY); requires MN-major A */
     float* dbias;

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "csrc", "libmmb200.so")
 
 #: must match MMB200_ABI_VERSION in include/mmb200.h
-ABI_VERSION = 7
+ABI_VERSION = 8
 MAX_GROUP = 8
 
 

@@ -70,6 +70,7 @@ struct Params {
     float* dbias;
     unsigned long long* trace;  // optional per-CTA phase timestamps (diagnostics)
     int epilogue;
+    int b_prefetch;
     int tiles_m, tiles_n, splits, kb_per_split, num_kb;
     int units;
 };
@@ -224,40 +225,64 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) MM_TRACE(1);
-    pdl_wait();  // everything above overlapped the previous kernel's tail
+    // griddepcontrol.wait: roles that read or write global memory wait for the
+    // previous kernel; everything above (barrier init, TMEM allocation,
+    // descriptor prefetch) and the B prefetch below overlap its tail
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
+            auto load_a = [&](int stage, int m0, int k0) {
+                uint8_t* sa = smem_a + stage * C::kABytes;
+                if (A_MN) {
+#pragma unroll
+                    for (int c = 0; c < BM / 64; ++c)
+                        tc::tma_load_2d(sa + c * 64 * BK * 2, &tmap_a, &full_bar[stage], m0 + c * 64, k0);
+                } else {
+                    tc::tma_load_2d(sa, &tmap_a, &full_bar[stage], k0, m0);
+                }
+            };
+            auto load_b = [&](int stage, int n0, int k0) {
+                uint8_t* sb = smem_b + stage * C::kBBytes;
+                if (B_MN) {
+#pragma unroll
+                    for (int c = 0; c < BN / 64; ++c)
+                        tc::tma_load_2d(sb + c * 64 * BK * 2, &tmap_b, &full_bar[stage], n0 + c * 64, k0);
+                } else {
+                    tc::tma_load_2d(sb, &tmap_b, &full_bar[stage], k0, n0);
+                }
+            };
+            // B stages of the first unit that do not depend on the previous kernel
+            int pre = 0;
+            if (p.b_prefetch && (int)blockIdx.x < p.units) {
+                const int u = blockIdx.x;
+                const int tile = u / p.splits, split = u % p.splits;
+                const int kb0 = split * p.kb_per_split;
+                const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+                pre = min(C::kStages, kb1 - kb0);
+                for (int i = 0; i < pre; ++i) {
+                    tc::mbar_expect_tx(&full_bar[i], C::kStageBytes);
+                    load_b(i, (tile / p.tiles_m) * BN, (kb0 + i) * BK);
+                }
+            }
+            pdl_wait();
             int stage = 0;
             uint32_t phase = 0;
+            int issued = 0;
             for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
                 const int tile = u / p.splits, split = u % p.splits;
                 const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
                 const int kb0 = split * p.kb_per_split;
                 const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
                 const int m0 = tm * BM, n0 = tn * BN;
-                for (int kb = kb0; kb < kb1; ++kb) {
-                    tc::mbar_wait(&empty_bar[stage], phase ^ 1);
-                    tc::mbar_expect_tx(&full_bar[stage], C::kStageBytes);
-                    uint8_t* sa = smem_a + stage * C::kABytes;
-                    uint8_t* sb = smem_b + stage * C::kBBytes;
-                    const int k0 = kb * BK;
-                    if (A_MN) {
-#pragma unroll
-                        for (int c = 0; c < BM / 64; ++c)
-                            tc::tma_load_2d(sa + c * 64 * BK * 2, &tmap_a, &full_bar[stage],
-                                            m0 + c * 64, k0);
+                for (int kb = kb0; kb < kb1; ++kb, ++issued) {
+                    if (issued < pre) {  // expect_tx and B already issued
+                        load_a(stage, m0, kb * BK);
                     } else {
-                        tc::tma_load_2d(sa, &tmap_a, &full_bar[stage], k0, m0);
-                    }
-                    if (B_MN) {
-#pragma unroll
-                        for (int c = 0; c < BN / 64; ++c)
-                            tc::tma_load_2d(sb + c * 64 * BK * 2, &tmap_b, &full_bar[stage],
-                                            n0 + c * 64, k0);
-                    } else {
-                        tc::tma_load_2d(sb, &tmap_b, &full_bar[stage], k0, n0);
+                        tc::mbar_wait(&empty_bar[stage], phase ^ 1);
+                        tc::mbar_expect_tx(&full_bar[stage], C::kStageBytes);
+                        load_a(stage, m0, kb * BK);
+                        load_b(stage, n0, kb * BK);
                     }
                     if (++stage == C::kStages) { stage = 0; phase ^= 1; }
                 }
@@ -314,6 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // kb % tiles_n == tn, so every k-block is summed exactly once.  Lane owns M = 4*lane..4*lane+3
         // (box lane/16, 16B chunk (lane%16)/2, half lane%2; rows are K,
         // 128B-swizzled).  Every stage is released here too (empty count 2).
+        pdl_wait();
         int stage = 0;
         uint32_t phase = 0;
         for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
@@ -351,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ------------------------------------------------------------ epilogue
+        pdl_wait();
         const int lane_grp = warp & 3;                   // TMEM lanes this warp may access
         const int half = (warp - kEpiWarp0) >> 2;        // which half of the tile's columns
         constexpr int kChunks = BN / 32 / 2;             // 32-column chunks per warp
@@ -600,6 +627,7 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
     p.d = a->d; p.bias = a->bias; p.resid = a->resid;
     p.aux = reinterpret_cast<const __nv_bfloat16*>(a->aux);
     p.dbias = a->dbias;
+    p.b_prefetch = a->b_prefetch;
     p.trace = g_trace_buf;
     p.epilogue = a->epilogue;
     p.tiles_m = static_cast<int>(tiles_m);

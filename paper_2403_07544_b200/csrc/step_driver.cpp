@@ -68,6 +68,7 @@ struct Driver {
         a.a = A; a.b = B; a.d = D; a.bias = bias; a.resid = resid; a.aux = aux; a.dbias = dbias;
         a.m = m; a.n = n; a.k = k; a.lda = lda; a.ldb = ldb; a.ldd = ldd;
         a.a_kmajor = a_k; a.b_kmajor = b_k; a.epilogue = epi;
+        a.b_prefetch = 1;  // B is a weight or an earlier forward activation
         return mm_gemm(&a, s);
     }
     // Y[T,out] (epi)= X[T,in] W[out,in]^T

@@ -25,7 +25,7 @@ class GemmArgs(ctypes.Structure):
         ("m", ctypes.c_int64), ("n", ctypes.c_int64), ("k", ctypes.c_int64),
         ("lda", ctypes.c_int64), ("ldb", ctypes.c_int64), ("ldd", ctypes.c_int64),
         ("a_kmajor", ctypes.c_int32), ("b_kmajor", ctypes.c_int32),
-        ("epilogue", ctypes.c_int32), ("pad", ctypes.c_int32),
+        ("epilogue", ctypes.c_int32), ("b_prefetch", ctypes.c_int32),
         ("dbias", ctypes.c_void_p),
     ]
 
