@@ -181,7 +181,26 @@ __device__ __forceinline__ void stage_row(uint8_t* buf, int r, const float (&acc
     }
 }
 
-template <int BN, int A_MN, int B_MN>
+// Work unit of a cluster of CL CTAs stacked along M: (M-tile pair, N-tile,
+// K-split); CTA rank r of the cluster takes M-tile tmp * CL + r.  All CTAs of
+// a cluster walk the same unit sequence, so the B tile they share (TMA
+// multicast, each CTA loading 1/CL of it) is always the same.
+struct Unit {
+    int tm, tn, kb0, kb1;
+};
+template <int CL>
+__device__ __forceinline__ Unit decode(const Params& p, int u, int rank) {
+    const int tp = u / p.splits, split = u % p.splits;
+    const int tiles_mp = (p.tiles_m + CL - 1) / CL;
+    Unit w;
+    w.tm = (tp % tiles_mp) * CL + rank;
+    w.tn = tp / tiles_mp;
+    w.kb0 = split * p.kb_per_split;
+    w.kb1 = min(p.num_kb, w.kb0 + p.kb_per_split);
+    return w;
+}
+
+template <int BN, int A_MN, int B_MN, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
                         const __grid_constant__ CUtensorMap tmap_b,
@@ -211,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < C::kStages; ++s) {
             tc::mbar_init(&full_bar[s], 1);
-            tc::mbar_init(&empty_bar[s], 2);  // MMA commit + bias warp
+            tc::mbar_init(&empty_bar[s], 2 * CL);  // MMA commit + bias warp, per cluster CTA
         }
         for (int a = 0; a < 2; ++a) {
             tc::mbar_init(&tfull_bar[a], 1);
@@ -221,8 +240,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (warp == 1) tc::tmem_alloc(tmem_slot, C::kTmemCols);
     tc::tc_fence_before();
-    __syncthreads();
+    if constexpr (CL > 1) tc::cluster_sync();  // peers' barriers exist before any multicast
+    else __syncthreads();
     tc::tc_fence_after();
+    const int rank = CL > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;
+    const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+    constexpr uint16_t kMask = (1u << CL) - 1;
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) MM_TRACE(1);
     // griddepcontrol.wait: roles that read or write global memory wait for the
@@ -242,40 +265,46 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc::tma_load_2d(sa, &tmap_a, &full_bar[stage], k0, m0);
                 }
             };
+            // this CTA's share of the B tile: K-major rows [rank*BN/CL, +BN/CL)
+            // (one box), or MN-major 64-column boxes c with c % CL == rank;
+            // multicast into every CTA of the cluster
             auto load_b = [&](int stage, int n0, int k0) {
                 uint8_t* sb = smem_b + stage * C::kBBytes;
                 if (B_MN) {
 #pragma unroll
-                    for (int c = 0; c < BN / 64; ++c)
-                        tc::tma_load_2d(sb + c * 64 * BK * 2, &tmap_b, &full_bar[stage], n0 + c * 64, k0);
+                    for (int c = 0; c < BN / 64; ++c) {
+                        if (c % CL != rank) continue;
+                        if constexpr (CL > 1)
+                            tc::tma_load_2d_mc(sb + c * 64 * BK * 2, &tmap_b, &full_bar[stage], n0 + c * 64, k0, kMask);
+                        else
+                            tc::tma_load_2d(sb + c * 64 * BK * 2, &tmap_b, &full_bar[stage], n0 + c * 64, k0);
+                    }
                 } else {
-                    tc::tma_load_2d(sb, &tmap_b, &full_bar[stage], k0, n0);
+                    constexpr int kRows = BN / CL;
+                    if constexpr (CL > 1)
+                        tc::tma_load_2d_mc(sb + rank * kRows * 128, &tmap_b, &full_bar[stage], k0, n0 + rank * kRows, kMask);
+                    else
+                        tc::tma_load_2d(sb, &tmap_b, &full_bar[stage], k0, n0);
                 }
             };
             // B stages of the first unit that do not depend on the previous kernel
             int pre = 0;
-            if (p.b_prefetch && (int)blockIdx.x < p.units) {
-                const int u = blockIdx.x;
-                const int tile = u / p.splits, split = u % p.splits;
-                const int kb0 = split * p.kb_per_split;
-                const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
-                pre = min(C::kStages, kb1 - kb0);
+            if (p.b_prefetch && cid < p.units) {
+                const Unit w = decode<CL>(p, cid, rank);
+                pre = min(C::kStages, w.kb1 - w.kb0);
                 for (int i = 0; i < pre; ++i) {
                     tc::mbar_expect_tx(&full_bar[i], C::kStageBytes);
-                    load_b(i, (tile / p.tiles_m) * BN, (kb0 + i) * BK);
+                    load_b(i, w.tn * BN, (w.kb0 + i) * BK);
                 }
             }
             pdl_wait();
             int stage = 0;
             uint32_t phase = 0;
             int issued = 0;
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-                const int tile = u / p.splits, split = u % p.splits;
-                const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
-                const int kb0 = split * p.kb_per_split;
-                const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
-                const int m0 = tm * BM, n0 = tn * BN;
-                for (int kb = kb0; kb < kb1; ++kb, ++issued) {
+            for (int u = cid; u < p.units; u += ncl) {
+                const Unit w = decode<CL>(p, u, rank);
+                const int m0 = w.tm * BM, n0 = w.tn * BN;
+                for (int kb = w.kb0; kb < w.kb1; ++kb, ++issued) {
                     if (issued < pre) {  // expect_tx and B already issued
                         load_a(stage, m0, kb * BK);
                     } else {
@@ -294,10 +323,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         int stage = 0;
         uint32_t phase = 0;
         int local = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
-            const int split = u % p.splits;
-            const int kb0 = split * p.kb_per_split;
-            const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        for (int u = cid; u < p.units; u += ncl, ++local) {
+            const Unit w = decode<CL>(p, u, rank);
+            const int kb0 = w.kb0, kb1 = w.kb1;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             tc::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -322,7 +350,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  : tc::umma_desc_sw128(sb + k * 32, 16, 1024);
                         tc::mma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
                     }
-                    tc::mma_commit(&empty_bar[stage]);
+                    if constexpr (CL > 1) tc::mma_commit_mc(&empty_bar[stage], kMask);
+                    else tc::mma_commit(&empty_bar[stage]);
                 }
                 __syncwarp();
                 if (++stage == C::kStages) { stage = 0; phase ^= 1; }
@@ -342,12 +371,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         pdl_wait();
         int stage = 0;
         uint32_t phase = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-            const int tile = u / p.splits, split = u % p.splits;
-            const int kb0 = split * p.kb_per_split;
-            const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        for (int u = cid; u < p.units; u += ncl) {
+            const Unit w = decode<CL>(p, u, rank);
+            const int kb0 = w.kb0, kb1 = w.kb1, tn = w.tn;
             const bool bias_sum = A_MN && p.dbias != nullptr;
-            const int tn = tile / p.tiles_m;
             float bsum[4] = {0.f, 0.f, 0.f, 0.f};
             for (int kb = kb0; kb < kb1; ++kb) {
                 tc::mbar_wait(&full_bar[stage], phase);
@@ -365,11 +392,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&empty_bar[stage]);
+                if (lane == 0) {
+                    if constexpr (CL > 1) {
+#pragma unroll
+                        for (int c = 0; c < CL; ++c) tc::mbar_arrive_cluster(&empty_bar[stage], c);
+                    } else {
+                        tc::mbar_arrive(&empty_bar[stage]);
+                    }
+                }
                 if (++stage == C::kStages) { stage = 0; phase ^= 1; }
             }
             if (bias_sum) {
-                const int64_t m = int64_t(tile % p.tiles_m) * BM + 4 * lane;
+                const int64_t m = int64_t(w.tm) * BM + 4 * lane;
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
                     if (m + i < p.m) atomicAdd(p.dbias + m + i, bsum[i]);
@@ -388,9 +422,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* bufs = smem_epi + (warp - kEpiWarp0) * 2 * kEpiBufBytes;
         int nbuf = 0;
         int local = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
-            const int tile = u / p.splits;
-            const int tm = tile % p.tiles_m, tn = tile / p.tiles_m;
+        for (int u = cid; u < p.units; u += ncl, ++local) {
+            const Unit w = decode<CL>(p, u, rank);
+            const int tm = w.tm, tn = w.tn;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             const int cbase = tn * BN + half * (BN / 2);
@@ -446,6 +480,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tc_fence_after();
         tc::tmem_dealloc(tmem_base, C::kTmemCols);
     }
+    // no CTA leaves while a peer may still arrive on its barriers
+    if constexpr (CL > 1) tc::cluster_sync();
     if (threadIdx.x == 0) MM_TRACE(7);
 }
 
@@ -492,29 +528,31 @@ int make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, i
     return 0;
 }
 
-template <int BN, int A_MN, int B_MN>
+template <int BN, int A_MN, int B_MN, int CL>
 int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md, const Params& p,
            cudaStream_t s) {
-    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN>;
+    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, CL>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg<BN>::kSmem));
         attr_set = true;
     }
-    const int grid = std::min(p.units, mm::num_sms());
-    MM_CUDA_TRY(mm::launch_pdl(kern, dim3(grid), dim3(kThreads), Cfg<BN>::kSmem, s, ma, mb, md, p));
+    // persistent: one CTA per SM, in clusters of CL CTAs (p.units counts cluster units)
+    const int clusters = std::min(p.units, mm::num_sms() / CL);
+    MM_CUDA_TRY(mm::launch_pdl_cluster(kern, dim3(clusters * CL), dim3(kThreads), Cfg<BN>::kSmem, s,
+                                       unsigned(CL), ma, mb, md, p));
     MM_LAUNCH_CHECK("gemm_tcgen05_kernel");
     return 0;
 }
 
-template <int BN>
+template <int BN, int CL>
 int dispatch(int a_mn, int b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
              const CUtensorMap& md, const Params& p, cudaStream_t s) {
-    if (!a_mn && !b_mn) return launch<BN, 0, 0>(ma, mb, md, p, s);
-    if (!a_mn && b_mn) return launch<BN, 0, 1>(ma, mb, md, p, s);
-    if (a_mn && !b_mn) return launch<BN, 1, 0>(ma, mb, md, p, s);
-    return launch<BN, 1, 1>(ma, mb, md, p, s);
+    if (!a_mn && !b_mn) return launch<BN, 0, 0, CL>(ma, mb, md, p, s);
+    if (!a_mn && b_mn) return launch<BN, 0, 1, CL>(ma, mb, md, p, s);
+    if (a_mn && !b_mn) return launch<BN, 1, 0, CL>(ma, mb, md, p, s);
+    return launch<BN, 1, 1, CL>(ma, mb, md, p, s);
 }
 
 unsigned long long* g_trace_buf = nullptr;  // set by mm_gemm_trace (diagnostics)
@@ -598,7 +636,14 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
     }
     const int64_t tiles_n = (a->n + bn - 1) / bn;
     const int num_kb = static_cast<int>((a->k + BK - 1) / BK);
-    const int64_t tiles = tiles_m * tiles_n;
+    // Optional 2-CTA clusters stacked along M sharing the B tile by TMA
+    // multicast (an odd last pair computes an out-of-range tile: zero-filled
+    // loads, clipped stores).  Off by default: measured 2-2.5x slower k-loops
+    // on B200 at cluster size 2 (the stage coupling costs more than the
+    // multicast saves); MM_GEMM_CLUSTER=2 enables it for experiments.
+    const char* cl_env = std::getenv("MM_GEMM_CLUSTER");
+    const int cl = (tiles_m >= 2 && cl_env && std::atoi(cl_env) == 2) ? 2 : 1;
+    const int64_t tiles = ((tiles_m + cl - 1) / cl) * cl * tiles_n;
     // split K (fp32 accumulate only: partials meet in the TMA reduce-add)
     int splits = 1;
     if (a->epilogue == MM_EPI_F32_ACCUM) {
@@ -615,7 +660,7 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
               : make_map(&ma, a->a, a->k, a->m, a->lda, BM);
     if (st) return st;
     st = b_mn ? make_map(&mb, a->b, a->n, a->k, a->ldb, BK)
-              : make_map(&mb, a->b, a->k, a->n, a->ldb, bn);
+              : make_map(&mb, a->b, a->k, a->n, a->ldb, bn / cl);
     if (st) return st;
     // D: 32 x 32 boxes, swizzle matching the staging layout
     st = make_map(&md, a->d, a->n, a->m, a->ldd, 32, 32, !out_bf16,
@@ -635,7 +680,7 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
     p.splits = splits;
     p.kb_per_split = kb_per;
     p.num_kb = num_kb;
-    p.units = static_cast<int>(tiles * splits);
+    p.units = static_cast<int>(tiles / cl * splits);  // cluster units
     cudaStream_t s = mm::as_stream(stream);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (g_timing.on) {
@@ -653,9 +698,15 @@ extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
         MM_CUDA_TRY(cudaEventRecord(e0, s));
     }
     int rc;
-    if (bn == 256) rc = dispatch<256>(a_mn, b_mn, ma, mb, md, p, s);
-    else if (bn == 192) rc = dispatch<192>(a_mn, b_mn, ma, mb, md, p, s);
-    else rc = dispatch<128>(a_mn, b_mn, ma, mb, md, p, s);
+    if (cl == 2) {
+        if (bn == 256) rc = dispatch<256, 2>(a_mn, b_mn, ma, mb, md, p, s);
+        else if (bn == 192) rc = dispatch<192, 2>(a_mn, b_mn, ma, mb, md, p, s);
+        else rc = dispatch<128, 2>(a_mn, b_mn, ma, mb, md, p, s);
+    } else {
+        if (bn == 256) rc = dispatch<256, 1>(a_mn, b_mn, ma, mb, md, p, s);
+        else if (bn == 192) rc = dispatch<192, 1>(a_mn, b_mn, ma, mb, md, p, s);
+        else rc = dispatch<128, 1>(a_mn, b_mn, ma, mb, md, p, s);
+    }
     if (rc == 0 && e1) MM_CUDA_TRY(cudaEventRecord(e1, s));
     return rc;
 }
