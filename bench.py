@@ -286,7 +286,8 @@ def run_train(args, pk):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
         store = dist.distributed_c10d._get_default_store()
-    wl = {"config3": configs.config3, "config5": configs.config5}[args.config](world)
+    wl = {"config3": configs.config3, "config4": configs.config4,
+          "config5": configs.config5}[args.config](world)
     trainer = Trainer(wl.tasks, wl.topo, wl.shape, rank=rank, world=world, device=dev, seed=0,
                       store=store)
     eng = trainer.engine
@@ -402,7 +403,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="train", choices=["train", "reduce"])
-    ap.add_argument("--config", default="config3", choices=["config3", "config5"])
+    ap.add_argument("--config", default="config3", choices=["config3", "config4", "config5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -255,3 +255,31 @@ def test_native_driver_matches_python_path(cuda):
     for k in grads[0]:
         if np.abs(grads[1][k]).max() > 0:
             assert rel_norm(grads[0][k], grads[1][k]) < 1e-3, str(k)
+
+
+def test_partially_shared_encoder_vs_oracle(cuda):
+    """Config-4 structure (language encoder stack + shared FULL encoder stack,
+    group decoders) at a small shape: two encoder positions per task, a
+    module shared by every task, gradients vs the bf16-faithful oracle."""
+    import itertools
+    from paper_2403_07544_b200.engine import DeviceBatch, Engine
+    from paper_2403_07544_b200.sharing import ArchSpec, SharingPattern as SP
+    shape = configs.SHAPE_CFG1_GPU
+    langs = ["aa", "bb", "cc", "dd"]
+    groups = {"aa": "g0", "bb": "g0", "cc": "g1", "dd": "g1"}
+    arch = ArchSpec(((SP.LANGUAGE, 1), (SP.FULL, 1)), ((SP.TGT_GROUP, 2),))
+    tasks = [configs._task(arch, s, t, DeviceId(0, 0), groups) for s, t in itertools.permutations(langs, 2)]
+    eng = Engine(tasks, ClusterTopology(1, 1, len(tasks)), shape, device=cuda)
+    hb = batches_for(1, 2, shape, seed=11)[0]
+    m0 = {k: st.master.cpu().numpy().copy() for k, st in eng.states.items()}
+    info = eng.step(0, [DeviceBatch(b, cuda) for b in hb])
+    torch.cuda.synchronize()
+    by_id = {t.id: t for t in tasks}
+    picked = [by_id[t] for t in info["tasks"]]
+    assert all(len(t.enc_modules) == 2 for t in picked)
+    eff = {k: effective_weights(eng.layouts[k], v) for k, v in m0.items()}
+    grads, used, losses = OT.local_grads(list(zip(picked, hb)), eff, eng.layouts, shape,
+                                         embedding_keys, bf16=True)
+    assert abs(eng.loss_sum.item() - sum(losses)) / sum(losses) < 1e-3
+    for k in used:
+        assert rel_norm(eng.states[k].grad.cpu().numpy(), grads[k].numpy()) < TOL_MODEL, str(k)
