@@ -27,8 +27,11 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 }
 
 // ----------------------------------------------------------------------------
-// LayerNorm: one warp per row; lane owns columns {4*lane + 128*i}.  COLS/128
-// float4 per lane held in registers (COLS in {512, 1024} for the configs).
+// LayerNorm: a warp owns R rows at a time (all their loads issued before any
+// reduction, for memory-level parallelism); lane owns columns
+// {4*lane + 128*i}, COLS/128 float4 per row in registers.
+constexpr int kLnRows = 2;
+
 template <int COLS>
 __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x,
                                                      const float* __restrict__ gamma,
@@ -38,38 +41,45 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x
     pdl_wait();
     constexpr int V = COLS / 128;
     const int lane = threadIdx.x & 31;
-    const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (row >= rows) return;
-    const float4* xr = reinterpret_cast<const float4*>(x + row * COLS);
-    float4 v[V];
-    float s = 0.f;
+    const int64_t row0 = (int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5)) * kLnRows;
+    float4 v[kLnRows][V];
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-        v[i] = xr[lane + 32 * i];
-        s += v[i].x + v[i].y + v[i].z + v[i].w;
-    }
-    const float mu = warp_sum(s) * (1.f / COLS);
-    float q = 0.f;
+    for (int r = 0; r < kLnRows; ++r) {
+        const int64_t row = min(row0 + r, rows - 1);
+        const float4* xr = reinterpret_cast<const float4*>(x + row * COLS);
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-        const float a = v[i].x - mu, b = v[i].y - mu, c = v[i].z - mu, d = v[i].w - mu;
-        q += a * a + b * b + c * c + d * d;
+        for (int i = 0; i < V; ++i) v[r][i] = xr[lane + 32 * i];
     }
-    const float rs = rsqrtf(warp_sum(q) * (1.f / COLS) + eps);
-    uint2* yr = reinterpret_cast<uint2*>(y + row * COLS);
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-        const int c = 4 * lane + 128 * i;
-        const float4 g = *reinterpret_cast<const float4*>(gamma + c);
-        const float4 b = *reinterpret_cast<const float4*>(beta + c);
-        uint2 o;
-        o.x = pack2((v[i].x - mu) * rs * g.x + b.x, (v[i].y - mu) * rs * g.y + b.y);
-        o.y = pack2((v[i].z - mu) * rs * g.z + b.z, (v[i].w - mu) * rs * g.w + b.w);
-        yr[lane + 32 * i] = o;
-    }
-    if (lane == 0) {
-        mean_out[row] = mu;
-        rstd_out[row] = rs;
+    for (int r = 0; r < kLnRows; ++r) {
+        const int64_t row = row0 + r;
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < V; ++i) s += v[r][i].x + v[r][i].y + v[r][i].z + v[r][i].w;
+        const float mu = warp_sum(s) * (1.f / COLS);
+        float q = 0.f;
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            const float a = v[r][i].x - mu, b = v[r][i].y - mu, c = v[r][i].z - mu, d = v[r][i].w - mu;
+            q += a * a + b * b + c * c + d * d;
+        }
+        const float rs = rsqrtf(warp_sum(q) * (1.f / COLS) + eps);
+        if (row >= rows) continue;
+        uint2* yr = reinterpret_cast<uint2*>(y + row * COLS);
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            const int c = 4 * lane + 128 * i;
+            const float4 g = __ldg(reinterpret_cast<const float4*>(gamma + c));
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(beta + c));
+            uint2 o;
+            o.x = pack2((v[r][i].x - mu) * rs * g.x + bb.x, (v[r][i].y - mu) * rs * g.y + bb.y);
+            o.y = pack2((v[r][i].z - mu) * rs * g.z + bb.z, (v[r][i].w - mu) * rs * g.w + bb.w);
+            yr[lane + 32 * i] = o;
+        }
+        if (lane == 0) {
+            mean_out[row] = mu;
+            rstd_out[row] = rs;
+        }
     }
 }
 
@@ -78,7 +88,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x
 // dgamma += sum(dy*xhat), dbeta += sum(dy) accumulated per lane across the
 // block's rows, reduced over warps in smem, one atomicAdd per column per block.
 template <int COLS>
-__global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ dy,
+__global__ void __launch_bounds__(256, (COLS <= 512 ? 2 : 1)) ln_bwd_kernel(const float* __restrict__ dy,
                                                      const float* __restrict__ x,
                                                      const float* __restrict__ gamma,
                                                      const float* __restrict__ mean,
@@ -87,48 +97,72 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ d
                                                      float* dbeta, int64_t rows) {
     pdl_wait();
     constexpr int V = COLS / 128;
+    constexpr int R = COLS <= 512 ? kLnRows : 1;  // rows per warp batch (register budget)
     __shared__ float red_g[8][COLS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float4 ag[V], ab[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) ag[i] = ab[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t row = int64_t(blockIdx.x) * 8 + warp; row < rows; row += int64_t(gridDim.x) * 8) {
-        const float mu = mean[row], rs = rstd[row];
-        const float4* dyr = reinterpret_cast<const float4*>(dy + row * COLS);
-        const float4* xr = reinterpret_cast<const float4*>(x + row * COLS);
-        float4 g[V], xh[V];
-        float s1 = 0.f, s2 = 0.f;
+    const int64_t stride = int64_t(gridDim.x) * 8 * R;
+    for (int64_t row0 = (int64_t(blockIdx.x) * 8 + warp) * R; row0 < rows; row0 += stride) {
+        float4 d[R][V], xv[R][V];
+        float mu[R], rs[R];
 #pragma unroll
-        for (int i = 0; i < V; ++i) {
-            const int c = 4 * lane + 128 * i;
-            const float4 d = dyr[lane + 32 * i];
-            const float4 xv = xr[lane + 32 * i];
-            const float4 gm = *reinterpret_cast<const float4*>(gamma + c);
-            xh[i] = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs,
-                                (xv.w - mu) * rs);
-            g[i] = make_float4(d.x * gm.x, d.y * gm.y, d.z * gm.z, d.w * gm.w);
-            s1 += g[i].x + g[i].y + g[i].z + g[i].w;
-            s2 += g[i].x * xh[i].x + g[i].y * xh[i].y + g[i].z * xh[i].z + g[i].w * xh[i].w;
-            ag[i].x += d.x * xh[i].x; ag[i].y += d.y * xh[i].y;
-            ag[i].z += d.z * xh[i].z; ag[i].w += d.w * xh[i].w;
-            ab[i].x += d.x; ab[i].y += d.y; ab[i].z += d.z; ab[i].w += d.w;
+        for (int r = 0; r < R; ++r) {  // every dy / x load of the batch first
+            const int64_t row = min(row0 + r, rows - 1);
+            mu[r] = mean[row];
+            rs[r] = rstd[row];
+            const float4* dyr = reinterpret_cast<const float4*>(dy + row * COLS);
+            const float4* xr = reinterpret_cast<const float4*>(x + row * COLS);
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                d[r][i] = dyr[lane + 32 * i];
+                xv[r][i] = xr[lane + 32 * i];
+            }
         }
-        const float m1 = warp_sum(s1) * (1.f / COLS), m2 = warp_sum(s2) * (1.f / COLS);
-        float4* dxr = reinterpret_cast<float4*>(dx + row * COLS);
-        uint2* dbr = reinterpret_cast<uint2*>(dx_bf16 + row * COLS);
 #pragma unroll
-        for (int i = 0; i < V; ++i) {
-            float4 o = dxr[lane + 32 * i];
-            o.x += rs * (g[i].x - m1 - xh[i].x * m2);
-            o.y += rs * (g[i].y - m1 - xh[i].y * m2);
-            o.z += rs * (g[i].z - m1 - xh[i].z * m2);
-            o.w += rs * (g[i].w - m1 - xh[i].w * m2);
-            dxr[lane + 32 * i] = o;
-            if (dx_bf16) {
-                uint2 b;
-                b.x = pack2(o.x, o.y);
-                b.y = pack2(o.z, o.w);
-                dbr[lane + 32 * i] = b;
+        for (int r = 0; r < R; ++r) {
+            const int64_t row = row0 + r;
+            const bool live = row < rows;
+            float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                float4& xh = xv[r][i];
+                xh = make_float4((xh.x - mu[r]) * rs[r], (xh.y - mu[r]) * rs[r],
+                                 (xh.z - mu[r]) * rs[r], (xh.w - mu[r]) * rs[r]);
+                const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma + 4 * lane + 128 * i));
+                const float4 g = make_float4(d[r][i].x * gm.x, d[r][i].y * gm.y,
+                                             d[r][i].z * gm.z, d[r][i].w * gm.w);
+                s1 += g.x + g.y + g.z + g.w;
+                s2 += g.x * xh.x + g.y * xh.y + g.z * xh.z + g.w * xh.w;
+                if (live) {
+                    ag[i].x += d[r][i].x * xh.x; ag[i].y += d[r][i].y * xh.y;
+                    ag[i].z += d[r][i].z * xh.z; ag[i].w += d[r][i].w * xh.w;
+                    ab[i].x += d[r][i].x; ab[i].y += d[r][i].y; ab[i].z += d[r][i].z; ab[i].w += d[r][i].w;
+                }
+                d[r][i] = g;  // keep dxhat
+            }
+            const float m1 = warp_sum(s1) * (1.f / COLS), m2 = warp_sum(s2) * (1.f / COLS);
+            if (!live) continue;
+            float4* dxr = reinterpret_cast<float4*>(dx + row * COLS);
+            uint2* dbr = reinterpret_cast<uint2*>(dx_bf16 + row * COLS);
+            float4 o[V];
+#pragma unroll
+            for (int i = 0; i < V; ++i) o[i] = dxr[lane + 32 * i];
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                float4 w = o[i];
+                w.x += rs[r] * (d[r][i].x - m1 - xv[r][i].x * m2);
+                w.y += rs[r] * (d[r][i].y - m1 - xv[r][i].y * m2);
+                w.z += rs[r] * (d[r][i].z - m1 - xv[r][i].z * m2);
+                w.w += rs[r] * (d[r][i].w - m1 - xv[r][i].w * m2);
+                dxr[lane + 32 * i] = w;
+                if (dx_bf16) {
+                    uint2 b;
+                    b.x = pack2(w.x, w.y);
+                    b.y = pack2(w.z, w.w);
+                    dbr[lane + 32 * i] = b;
+                }
             }
         }
     }
@@ -142,10 +176,10 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ d
         __syncthreads();
         float* dst = pass == 0 ? dgamma : dbeta;
         for (int c = threadIdx.x; c < COLS; c += 256) {
-            float s = 0.f;
+            float sum = 0.f;
 #pragma unroll
-            for (int w = 0; w < 8; ++w) s += red_g[w][c];
-            atomicAdd(dst + c, s);
+            for (int w = 0; w < 8; ++w) sum += red_g[w][c];
+            atomicAdd(dst + c, sum);
         }
         __syncthreads();
     }
@@ -357,7 +391,7 @@ extern "C" int mm_layernorm_fwd(const float* x, const float* gamma, const float*
                                 void* stream) {
     MM_CHECK_ARG(x && gamma && beta && y && mean && rstd, "NULL argument");
     if (rows == 0) return 0;
-    const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
+    const unsigned grid = static_cast<unsigned>((rows + 8 * kLnRows - 1) / (8 * kLnRows));
     auto s = mm::as_stream(stream);
     if (cols == 512)
         MM_CUDA_TRY(mm::launch_pdl(ln_fwd_kernel<512>, dim3(grid), dim3(256), 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
@@ -380,7 +414,8 @@ extern "C" int mm_layernorm_bwd(const float* dy, const float* x, const float* ga
                                 float* dgamma, float* dbeta, int64_t rows, int cols, void* stream) {
     MM_CHECK_ARG(dy && x && gamma && mean && rstd && dx && dgamma && dbeta, "NULL argument");
     if (rows == 0) return 0;
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((rows + 7) / 8, 4 * mm::num_sms()));
+    const unsigned grid = static_cast<unsigned>(
+        std::min<int64_t>((rows + 8 * kLnRows - 1) / (8 * kLnRows), 4 * mm::num_sms()));
     auto s = mm::as_stream(stream);
     if (cols == 512)
         MM_CUDA_TRY(mm::launch_pdl(ln_bwd_kernel<512>, dim3(grid), dim3(256), 0, s, dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows));
