@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 8
+#define MMB200_ABI_VERSION 10
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 
 int mm_abi_version(void);
@@ -83,6 +83,8 @@ typedef struct {
 typedef struct {
     float beta1, beta2, eps, weight_decay, inv_loss_scale;
     float one_minus_beta1, one_minus_beta2; /* computed in double on the host */
+    int32_t max_ctas; /* 0: one CTA per 16K-element chunk; > 0: persistent CTAs
+                         (a thin background update overlapping other kernels) */
 } mm_adam_hyper;
 
 int mm_fused_update(const mm_adam_module* mods, int n_mods, const mm_adam_hyper* hyper,
@@ -265,8 +267,12 @@ typedef struct {
     int32_t ng_src, cap_src, ng_tgt, cap_tgt, ng_cross, cap_cross;
 } mm_batch;
 
+/* dec_done (cudaEvent_t, may be NULL) is recorded on `stream` as soon as the
+ * decoder-side gradients (decoder stacks, target embedding, generator) are
+ * final, i.e. before the encoder backward: their exchange and update can
+ * start on another stream while the encoder backward runs. */
 int mm_task_fwd_bwd(const mm_task* task, const mm_batch* batch, void* workspace,
-                    size_t* ws_bytes, float* loss_sum, void* stream);
+                    size_t* ws_bytes, float* loss_sum, void* stream, void* dec_done);
 
 /* helpers */
 /* out[c] += sum over rows of x[r, c] (bf16 in, fp32 accumulate) */

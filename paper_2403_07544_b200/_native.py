@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "csrc", "libmmb200.so")
 
 #: must match MMB200_ABI_VERSION in include/mmb200.h
-ABI_VERSION = 8
+ABI_VERSION = 10
 MAX_GROUP = 8
 
 
@@ -90,13 +90,14 @@ class AdamHyper(ctypes.Structure):
         ("inv_loss_scale", c_float),
         ("one_minus_beta1", c_float),
         ("one_minus_beta2", c_float),
+        ("max_ctas", c_int32),
     ]
 
     @classmethod
-    def make(cls, beta1, beta2, eps, weight_decay=0.0, inv_loss_scale=1.0):
+    def make(cls, beta1, beta2, eps, weight_decay=0.0, inv_loss_scale=1.0, max_ctas=0):
         return cls(beta1=beta1, beta2=beta2, eps=eps, weight_decay=weight_decay,
                    inv_loss_scale=inv_loss_scale, one_minus_beta1=1.0 - beta1,
-                   one_minus_beta2=1.0 - beta2)
+                   one_minus_beta2=1.0 - beta2, max_ctas=max_ctas)
 
 
 class ReduceItem(ctypes.Structure):
@@ -187,7 +188,7 @@ def _declare(h: ctypes.CDLL) -> None:
     sig("mm_memset", c_int, c_void_p, c_int, c_size_t, c_void_p)
     sig("mm_axpy_f32", c_int, c_void_p, c_void_p, c_float, c_int64, c_void_p)
     sig("mm_task_fwd_bwd", c_int, c_void_p, c_void_p, c_void_p, POINTER(c_size_t), c_void_p,
-        c_void_p)
+        c_void_p, c_void_p)
 
 
 def symbols() -> list[str]:

@@ -243,6 +243,8 @@ struct Driver {
         return 0;
     }
 
+    cudaEvent_t dec_done = nullptr;
+
     int run(float* loss_sum) {
         const int64_t Ts = b.n_src, Tt = b.n_tgt;
         const float scale = std::sqrt(float(d));
@@ -299,6 +301,7 @@ struct Driver {
             if (int e = self_bwd(dec_l[l], dy, dy_bf, Tt, b.cu_tgt, b.max_tgt, true, b.groups_tgt, b.ng_tgt, b.cap_tgt)) return e;
         }
         TRY(mm_embed_bwd(b.tgt_in, dy, t.dec_emb.grad + t.dec_emb.emb, Tt, d, scale, s));
+        if (dec_done && !sizing) MM_CUDA_TRY(cudaEventRecord(dec_done, s));
         // ---- encoder backward
         float* dx = ar.get<float>(Ts * d);
         uint16_t* dx_bf = ar.get<uint16_t>(Ts * d);
@@ -317,7 +320,7 @@ struct Driver {
 }  // namespace
 
 extern "C" int mm_task_fwd_bwd(const mm_task* task, const mm_batch* batch, void* workspace,
-                               size_t* ws_bytes, float* loss_sum, void* stream) {
+                               size_t* ws_bytes, float* loss_sum, void* stream, void* dec_done) {
     MM_CHECK_ARG(task && batch && ws_bytes, "NULL argument");
     MM_CHECK_ARG(task->n_enc >= 1 && task->n_dec >= 1 && task->enc && task->dec, "empty task");
     MM_CHECK_ARG(task->d_model % 64 == 0 && task->heads * 64 == task->d_model,
@@ -344,6 +347,7 @@ extern "C" int mm_task_fwd_bwd(const mm_task* task, const mm_batch* batch, void*
         MM_CHECK_ARG(probe.peak <= *ws_bytes, "workspace %zu B < required %zu B", *ws_bytes,
                      probe.peak);
     }
+    drv.dec_done = static_cast<cudaEvent_t>(dec_done);
     const int st = drv.run(loss_sum);
     if (ar.sizing) *ws_bytes = ar.peak;
     return st;

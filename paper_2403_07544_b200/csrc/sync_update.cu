@@ -129,12 +129,13 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 
 __global__ void __launch_bounds__(kThreads) fused_update_kernel(const __grid_constant__ AdamTable t) {
     pdl_wait();
-    const int64_t chunk = blockIdx.x;
+    const int64_t n_chunks = t.chunk_begin[t.n_mods];
+    for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
     const int mi = find_module(t.chunk_begin, t.n_mods, chunk);
     const mm_adam_module& md = t.mod[mi];
     int n = md.n_ready;
     if (t.ready_dev != nullptr && md.ready_index >= 0) n = t.ready_dev[md.ready_index];
-    if (n <= 0) return;  // unused everywhere: no reduction, no optimizer step
+    if (n <= 0) continue;  // unused everywhere: no reduction, no optimizer step
     // g = sum / n * inv_loss_scale, the rescale of Algorithm 1 fused here
     const float fn = (float)n;
     const float unscale = t.hp.inv_loss_scale;
@@ -186,6 +187,7 @@ __global__ void __launch_bounds__(kThreads) fused_update_kernel(const __grid_con
             }
         }
     }
+}  // chunk loop
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -269,7 +271,8 @@ extern "C" int mm_fused_update(const mm_adam_module* mods, int n_mods, const mm_
         t.n_mods = used;
         t.chunk_begin[used] = chunks;
         if (chunks == 0) continue;
-        MM_CUDA_TRY(mm::launch_pdl(fused_update_kernel, dim3((unsigned)chunks), dim3(kThreads), 0,
+        const int64_t grid = hyper->max_ctas > 0 ? std::min<int64_t>(chunks, hyper->max_ctas) : chunks;
+        MM_CUDA_TRY(mm::launch_pdl(fused_update_kernel, dim3((unsigned)grid), dim3(kThreads), 0,
                                    mm::as_stream(stream), t));
         MM_LAUNCH_CHECK("fused_update_kernel");
     }

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import dataclasses
 import math
+import os
 from typing import Optional, Sequence
 
 import numpy as np
@@ -184,6 +185,17 @@ class Engine:
         self.native = True  # C++ step driver (mm_task_fwd_bwd); False -> per-op Python path
         self._task_desc: dict = {}
         self._ws = None
+        self.overlap = True  # decoder-side exchange + update overlap the encoder backward
+        # 0 = full grid.  A capped background update (MM_OVERLAP_CTAS=64) breaks
+        # even at N=1 (r01 sweep: 8/16/32/64 CTAs -> 266K/413K/587K/740K vs
+        # 756K tok/s): the update is HBM-bound and latency-bound per CTA.
+        self.overlap_ctas = int(os.environ.get("MM_OVERLAP_CTAS", "0"))
+        self._counts_host = torch.zeros(len(self.plan.keys), dtype=torch.int32, pin_memory=True)
+        self._side_stream = torch.cuda.Stream(device=self.device)
+        # torch creates the CUDA event lazily: record once so .cuda_event is a
+        # real handle before the C driver records it
+        self._dec_done = torch.cuda.Event()
+        self._dec_done.record()
 
     # ------------------------------------------------------------------ layers
     def _zeros(self, *shape):
@@ -362,23 +374,33 @@ class Engine:
             self._task_desc[task.id] = (t, enc_arr, dec_arr, [a for _, a in enc + dec])
         return self._task_desc[task.id][0]
 
-    def forward_backward(self, task: TaskSpec, db: DeviceBatch, loss_sum: torch.Tensor) -> None:
-        """One micro-batch of one task; gradients accumulate into the buckets."""
+    def forward_backward(self, task: TaskSpec, db: DeviceBatch, loss_sum: torch.Tensor,
+                         dec_done=None) -> None:
+        """One micro-batch of one task; gradients accumulate into the buckets.
+        ``dec_done`` (torch.cuda.Event) is recorded once the decoder-side
+        gradients are final (native path only)."""
         if not self.native or self.trace is not None:
-            return self.forward_backward_py(task, db, loss_sum)
+            self.forward_backward_py(task, db, loss_sum)
+            if dec_done is not None:
+                dec_done.record()
+            return
         import ctypes
         L = _native.lib()
         t = self.task_desc(task)
+        if dec_done is not None and not dec_done.cuda_event:
+            raise RuntimeError("dec_done event has no CUDA handle yet")
         need = ctypes.c_size_t(0)
         _native.check(L.mm_task_fwd_bwd(ctypes.byref(t), ctypes.byref(db.desc), None,
-                                        ctypes.byref(need), None, None), "mm_task_fwd_bwd(size)")
+                                        ctypes.byref(need), None, None, None),
+                      "mm_task_fwd_bwd(size)")
         if self._ws is None or self._ws.numel() < need.value:
             self._ws = torch.empty(int(need.value * 1.25) + (1 << 20), dtype=torch.uint8,
                                    device=self.device)
         have = ctypes.c_size_t(self._ws.numel())
         ops.LAUNCHES[0] += 1
         _native.check(L.mm_task_fwd_bwd(ctypes.byref(t), ctypes.byref(db.desc), self._ws.data_ptr(),
-                                        ctypes.byref(have), loss_sum.data_ptr(), ops.stream_ptr()),
+                                        ctypes.byref(have), loss_sum.data_ptr(), ops.stream_ptr(),
+                                        dec_done.cuda_event if dec_done is not None else None),
                       "mm_task_fwd_bwd")
 
     def forward_backward_py(self, task: TaskSpec, db: DeviceBatch, loss_sum: torch.Tensor) -> None:
@@ -474,29 +496,61 @@ class Engine:
         the Algorithm-1 exchange and the fused update.  Returns host-side
         bookkeeping; the loss stays on device in ``self.loss_sum``."""
         ops.memset(self.loss_sum, 0)
+        # the multiplexer's picks (host RNG) fix this step's used set -- and so
+        # the ready flags -- before any compute is issued (syncsim.py:353)
+        tasks = [self.mux.pick(step_idx) for _ in batches]
+        picked = [t.id for t in tasks]
         used: set[ModuleKey] = set()
-        picked = []
-        for db in batches:
-            task = self.mux.pick(step_idx)
-            picked.append(task.id)
-            fresh = [k for k in task_modules(task) if k not in used]
-            self.zero_grads(fresh)
-            used.update(fresh)
-            self.forward_backward(task, db, self.loss_sum)
+        for t in tasks:
+            used.update(task_modules(t))
         flags = ready_flags(self.plan, self.rank, used)
+        counts_ready = None
         if self.comm is not None:
             self.flags_dev.copy_(torch.tensor(flags, dtype=torch.int32), non_blocking=True)
-            self.comm.ready_count(self.flags_dev, self.n_ready_dev)
-            counts = self.n_ready_dev.tolist()  # host needs n to post the right collectives
+            self.comm.ready_count(self.flags_dev, self.n_ready_dev)  # K1, ahead of the compute
+            self._counts_host.copy_(self.n_ready_dev, non_blocking=True)
+            counts_ready = torch.cuda.Event()
+            counts_ready.record()
+        zeroed: set[ModuleKey] = set()
+        overlap = self.overlap and self.native
+        dec_done = self._dec_done if overlap else None
+        for i, (task, db) in enumerate(zip(tasks, batches)):
+            fresh = [k for k in task_modules(task) if k not in zeroed]
+            self.zero_grads(fresh)
+            zeroed.update(fresh)
+            self.forward_backward(task, db, self.loss_sum,
+                                  dec_done if i == len(tasks) - 1 else None)
+        if counts_ready is not None:
+            counts_ready.synchronize()  # waits for K1 only, not for the compute behind it
+            counts = self._counts_host.tolist()
         else:
             counts = flags
-        self.exchange_and_update(counts, used)
+        if overlap:
+            # decoder-side modules: exchange + K3 on a side stream while the
+            # encoder backward runs (SURVEY §8(f) f1); sorted ModuleKey order
+            # puts every decoder key first, so collective order is unchanged
+            dec = {k for k in self.states if k.side is Side.DECODER}
+            side = self._side_stream
+            side.wait_event(dec_done)
+            with torch.cuda.stream(side):
+                # a thin background update: few CTAs, so the encoder-backward
+                # GEMMs keep their SMs
+                self.exchange_and_update(counts, used, only=dec, max_ctas=self.overlap_ctas)
+            self.exchange_and_update(counts, used, only=set(self.states) - dec)
+            torch.cuda.current_stream().wait_stream(side)
+        else:
+            self.exchange_and_update(counts, used)
         return {"tasks": picked, "ready": dict(zip(self.plan.keys, counts))}
 
-    def exchange_and_update(self, counts: Sequence[int], used=frozenset()) -> None:
+    def exchange_and_update(self, counts: Sequence[int], used=frozenset(), only=None,
+                            max_ctas: int = 0) -> None:
+        """K2 for the modules of ``exchange_order`` then K3 for every hosted
+        module with n >= 1; ``only`` restricts both to a subset of keys."""
         items = []
         if self.comm is not None:
             for k in exchange_order(self.plan, counts, self.rank):
+                if only is not None and k not in only:
+                    continue
                 grp = self.comm.by_set.get(tuple(self.plan.groups[k]))
                 st = self.states[k]
                 if k not in used:  # contribute the zero of Algorithm 1 (PAPER.md:227-228)
@@ -504,12 +558,14 @@ class Engine:
                 items.append(_native.ReduceItem(group=grp, buf=st.grad.data_ptr(),
                                                 n_elems=st.grad.numel(), dtype=0))
             self.comm.reduce(items)
-        self.fused_update(counts)
+        self.fused_update(counts, only, max_ctas)
 
-    def fused_update(self, counts: Sequence[int]) -> None:
+    def fused_update(self, counts: Sequence[int], only=None, max_ctas: int = 0) -> None:
         a = self.adam
         mods = []
         for k, st in self.states.items():
+            if only is not None and k not in only:
+                continue
             n = counts[self.index[k]]
             if n < 1:
                 continue
@@ -524,7 +580,7 @@ class Engine:
         if mods:
             ops.fused_update(mods, _native.AdamHyper.make(beta1=a.beta1, beta2=a.beta2, eps=a.eps,
                                                      weight_decay=a.weight_decay,
-                                                     inv_loss_scale=1.0))
+                                                     inv_loss_scale=1.0, max_ctas=max_ctas))
 
     def close(self) -> None:
         if self.comm is not None:
