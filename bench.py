@@ -34,7 +34,6 @@ sys.path.insert(0, ROOT)
 METRIC = "train tok/s at 1/2/4/8 B200; module-grad reduce GB/s vs NVLink peak"
 #: kernels one config-3 step launches through the native driver: counted from
 #: the ncu launch list of the same step (profiles/r01_launch_summary.txt)
-LAUNCHES_PER_STEP_NATIVE = 374
 
 
 def peaks():
@@ -248,12 +247,14 @@ def run_reduce(args, pk):
         ops.sync_emulated(table, True)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _native.lib().mm_launch_count()
     with ClockSampler(0) as clk:
         e0.record()
         for _ in range(args.steps):
             ops.sync_emulated(table, True)
         e1.record()
         torch.cuda.synchronize()
+    launches = _native.lib().mm_launch_count() - launches0
     ms = e0.elapsed_time(e1) / args.steps
     nbytes = reduce_bytes(mods)
     gbs = nbytes / (ms * 1e-3) / 1e9
@@ -264,7 +265,7 @@ def run_reduce(args, pk):
                        "params": sum(m.n_params for m in mods), "l2": "working set 7.7 GB > L2"},
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": gbs / pk["hbm_gbs"], "traffic": None},
-            "clocks": clk.summary(), "gpu_launches": args.steps}
+            "clocks": clk.summary(), "gpu_launches": launches}
 
 
 # ---------------------------------------------------------------------------
@@ -275,7 +276,7 @@ def run_train(args, pk):
     import numpy as np
     import torch
     import torch.distributed as dist
-    from paper_2403_07544_b200 import configs, ops
+    from paper_2403_07544_b200 import _native, configs, ops
     from paper_2403_07544_b200.data import ZipfIds, make_batch
     from paper_2403_07544_b200.engine import DeviceBatch, Trainer
 
@@ -307,7 +308,7 @@ def run_train(args, pk):
     for s in range(args.warmup):
         eng.step(s, [dbs[s]])
     barrier()
-    launches0 = ops.LAUNCHES[0]
+    launches0 = _native.lib().mm_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record()
@@ -315,7 +316,8 @@ def run_train(args, pk):
             eng.step(s, [dbs[s]])
         e1.record()
         barrier()
-    launches = LAUNCHES_PER_STEP_NATIVE if eng.native else (ops.LAUNCHES[0] - launches0) // args.steps
+    # every kernel libmmb200 launched in the timed region (counted in the library)
+    launches = (_native.lib().mm_launch_count() - launches0) // args.steps
     ms = e0.elapsed_time(e1) / args.steps
     tokens_local = sum(b.n_tgt for b in host[args.warmup:]) / args.steps
     src_local = sum(b.n_src for b in host[args.warmup:]) / args.steps

@@ -21,13 +21,15 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 10
+#define MMB200_ABI_VERSION 11
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 
 int mm_abi_version(void);
 const char* mm_last_error(void);
 /* SM count and compute capability (major*10+minor) of the current device. */
 int mm_device_info(int* sm_count, int* cc);
+/* Number of kernels this library has launched since load (all entry points). */
+unsigned long long mm_launch_count(void);
 
 /* ---------------------------------------------------------------------------
  * K9: allocator communication cost.  Same arguments, loop order and float64
@@ -159,6 +161,10 @@ typedef struct {
 } mm_gemm_args;
 
 int mm_gemm(const mm_gemm_args* args, void* stream);
+/* n independent GEMMs in one persistent launch (one unit list, one tile
+ * width); all problems share a_kmajor / b_kmajor.  Used for the deferred
+ * weight-gradient GEMMs of a whole encoder or decoder side. */
+int mm_gemm_grouped(const mm_gemm_args* probs, int n, void* stream);
 /* mode 1: start recording CUDA events around every mm_gemm launch;
  * mode 0: stop, synchronise and return total flops (2MNK), summed launch
  * time (ms) and launch count since the last start. */

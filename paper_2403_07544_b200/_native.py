@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "csrc", "libmmb200.so")
 
 #: must match MMB200_ABI_VERSION in include/mmb200.h
-ABI_VERSION = 10
+ABI_VERSION = 11
 MAX_GROUP = 8
 
 
@@ -168,7 +168,9 @@ def _declare(h: ctypes.CDLL) -> None:
     sig("mm_ready_count", c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p)
     sig("mm_reduce_modules", c_int, c_void_p, POINTER(ReduceItem), c_int, c_void_p)
     # layer kernels (K4-K8)
+    sig("mm_launch_count", ctypes.c_ulonglong)
     sig("mm_gemm", c_int, c_void_p, c_void_p)
+    sig("mm_gemm_grouped", c_int, c_void_p, c_int, c_void_p)
     sig("mm_gemm_timing", c_int, c_int, POINTER(c_double), POINTER(c_float), POINTER(c_int))
     sig("mm_gemm_trace", c_int, c_void_p)
     sig("mm_layernorm_fwd", c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

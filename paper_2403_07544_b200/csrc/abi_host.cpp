@@ -8,6 +8,8 @@
 
 namespace mm {
 
+std::atomic<unsigned long long> g_launches{0};
+
 static thread_local std::string g_last_error;
 
 void set_error(const char* fmt, ...) {
@@ -33,6 +35,8 @@ int num_sms() {
 }  // namespace mm
 
 extern "C" int mm_abi_version(void) { return MMB200_ABI_VERSION; }
+
+extern "C" unsigned long long mm_launch_count(void) { return mm::g_launches.load(); }
 
 extern "C" const char* mm_last_error(void) { return mm::g_last_error.c_str(); }
 

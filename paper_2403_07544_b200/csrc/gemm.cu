@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <vector>
 
@@ -43,6 +44,7 @@ constexpr int kEpiWarp0 = 2;
 constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, each half the columns
 constexpr int kBiasWarp = kEpiWarp0 + kEpiWarps;  // second consumer of every smem stage
 constexpr int kThreads = (kBiasWarp + 1) * 32;
+constexpr int kMaxProbs = 24;  // problems per grouped launch (kernel parameter space)
 
 constexpr int kEpiBufBytes = 32 * 128;                    // 32 rows x 128 B box
 constexpr int kEpiSmem = kEpiWarps * 2 * kEpiBufBytes;    // double-buffered per warp
@@ -60,7 +62,10 @@ struct Cfg {
     static_assert(kSmem <= kSmemLimit, "smem budget");
 };
 
-struct Params {
+// One GEMM problem of a launch: its three tensor maps (A, B, D) and its slice
+// [unit_begin, unit_begin + tiles_m * tiles_n * splits) of the launch's unit list.
+struct alignas(64) Prob {
+    CUtensorMap ta, tb, td;
     int64_t m, n, k;
     int64_t ldd;
     void* d;
@@ -68,11 +73,21 @@ struct Params {
     const float* resid;
     const __nv_bfloat16* aux;
     float* dbias;
-    unsigned long long* trace;  // optional per-CTA phase timestamps (diagnostics)
     int epilogue;
-    int b_prefetch;
     int tiles_m, tiles_n, splits, kb_per_split, num_kb;
+    int unit_begin;
+};
+
+// A launch: NP = 1 for a plain GEMM, kMaxProbs for a grouped launch (all
+// problems share the operand majorness and the tile width; units of all
+// problems are dealt to the persistent CTAs from one list).
+template <int NP>
+struct Group {
+    Prob prob[NP];
+    unsigned long long* trace;  // optional per-CTA phase timestamps (diagnostics)
+    int n_probs;
     int units;
+    int b_prefetch;
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -85,7 +100,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 // done (warp 2), 6 stores drained (warp 2), 7 exit
 #define MM_TRACE(slot)                                                                   \
     do {                                                                                 \
-        if (p.trace) p.trace[blockIdx.x * 8 + (slot)] = gtime();                         \
+        if (g.trace) g.trace[blockIdx.x * 8 + (slot)] = gtime();                         \
     } while (0)
 
 __device__ __forceinline__ float bf16_to_f(uint16_t h) {
@@ -98,14 +113,14 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 }
 
 // Epilogue math for one row (this thread) x 32 columns held in registers.
-__device__ __forceinline__ bool has_bias(const Params& p) {
+__device__ __forceinline__ bool has_bias(const Prob& p) {
     const int ep = p.epilogue;
     return p.bias && (ep == MM_EPI_BF16 || ep == MM_EPI_BF16_RELU || ep == MM_EPI_F32 ||
                       ep == MM_EPI_F32_RESID);
 }
 
 // bv: this lane's bias value for column col0 + lane (preloaded per tile)
-__device__ __forceinline__ void epilogue_math(const Params& p, int64_t row, int64_t col0,
+__device__ __forceinline__ void epilogue_math(const Prob& p, int64_t row, int64_t col0,
                                               float (&acc)[32], float bv) {
     const int ep = p.epilogue;
     if (has_bias(p)) {
@@ -181,30 +196,34 @@ __device__ __forceinline__ void stage_row(uint8_t* buf, int r, const float (&acc
     }
 }
 
-// Work unit of a cluster of CL CTAs stacked along M: (M-tile pair, N-tile,
-// K-split); CTA rank r of the cluster takes M-tile tmp * CL + r.  All CTAs of
-// a cluster walk the same unit sequence, so the B tile they share (TMA
-// multicast, each CTA loading 1/CL of it) is always the same.
+// Work unit: (problem, M-tile, N-tile, K-split).  Consecutive units walk M
+// first, so CTAs running at the same time share the B tile in L2.
 struct Unit {
-    int tm, tn, kb0, kb1;
+    int pi, tm, tn, kb0, kb1;
 };
-template <int CL>
-__device__ __forceinline__ Unit decode(const Params& p, int u, int rank) {
-    const int tp = u / p.splits, split = u % p.splits;
-    const int tiles_mp = (p.tiles_m + CL - 1) / CL;
+template <int NP>
+__device__ __forceinline__ Unit decode(const Group<NP>& g, int u) {
+    int pi = 0;
+    if constexpr (NP > 1) {
+#pragma unroll 1
+        for (int j = 1; j < g.n_probs; ++j)
+            if (u >= g.prob[j].unit_begin) pi = j;
+    }
+    const Prob& P = g.prob[pi];
+    const int v = u - P.unit_begin;
+    const int tp = v / P.splits, split = v - tp * P.splits;
     Unit w;
-    w.tm = (tp % tiles_mp) * CL + rank;
-    w.tn = tp / tiles_mp;
-    w.kb0 = split * p.kb_per_split;
-    w.kb1 = min(p.num_kb, w.kb0 + p.kb_per_split);
+    w.pi = pi;
+    w.tm = tp % P.tiles_m;
+    w.tn = tp / P.tiles_m;
+    w.kb0 = split * P.kb_per_split;
+    w.kb1 = min(P.num_kb, w.kb0 + P.kb_per_split);
     return w;
 }
 
-template <int BN, int A_MN, int B_MN, int CL>
+template <int BN, int A_MN, int B_MN, int NP>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
-                        const __grid_constant__ CUtensorMap tmap_b,
-                        const __grid_constant__ CUtensorMap tmap_d, const __grid_constant__ Params p) {
+    gemm_tcgen05_kernel(const __grid_constant__ Group<NP> g) {
     using C = Cfg<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -223,14 +242,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) MM_TRACE(0);
 
     if (warp == 0 && lane == 0) {
-        tc::tma_prefetch(&tmap_a);
-        tc::tma_prefetch(&tmap_b);
-        tc::tma_prefetch(&tmap_d);
+        for (int i = 0; i < g.n_probs; ++i) {
+            tc::tma_prefetch(&g.prob[i].ta);
+            tc::tma_prefetch(&g.prob[i].tb);
+            tc::tma_prefetch(&g.prob[i].td);
+        }
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < C::kStages; ++s) {
             tc::mbar_init(&full_bar[s], 1);
-            tc::mbar_init(&empty_bar[s], 2 * CL);  // MMA commit + bias warp, per cluster CTA
+            tc::mbar_init(&empty_bar[s], 2);  // MMA commit + bias warp
         }
         for (int a = 0; a < 2; ++a) {
             tc::mbar_init(&tfull_bar[a], 1);
@@ -240,12 +261,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (warp == 1) tc::tmem_alloc(tmem_slot, C::kTmemCols);
     tc::tc_fence_before();
-    if constexpr (CL > 1) tc::cluster_sync();  // peers' barriers exist before any multicast
-    else __syncthreads();
+    __syncthreads();
     tc::tc_fence_after();
-    const int rank = CL > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;
-    const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
-    constexpr uint16_t kMask = (1u << CL) - 1;
+    const int cid = blockIdx.x, ncta = gridDim.x;
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) MM_TRACE(1);
     // griddepcontrol.wait: roles that read or write global memory wait for the
@@ -255,63 +273,53 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
-            auto load_a = [&](int stage, int m0, int k0) {
+            auto load_a = [&](const Prob& P, int stage, int m0, int k0) {
                 uint8_t* sa = smem_a + stage * C::kABytes;
                 if (A_MN) {
 #pragma unroll
                     for (int c = 0; c < BM / 64; ++c)
-                        tc::tma_load_2d(sa + c * 64 * BK * 2, &tmap_a, &full_bar[stage], m0 + c * 64, k0);
+                        tc::tma_load_2d(sa + c * 64 * BK * 2, &P.ta, &full_bar[stage], m0 + c * 64, k0);
                 } else {
-                    tc::tma_load_2d(sa, &tmap_a, &full_bar[stage], k0, m0);
+                    tc::tma_load_2d(sa, &P.ta, &full_bar[stage], k0, m0);
                 }
             };
-            // this CTA's share of the B tile: K-major rows [rank*BN/CL, +BN/CL)
-            // (one box), or MN-major 64-column boxes c with c % CL == rank;
-            // multicast into every CTA of the cluster
-            auto load_b = [&](int stage, int n0, int k0) {
+            auto load_b = [&](const Prob& P, int stage, int n0, int k0) {
                 uint8_t* sb = smem_b + stage * C::kBBytes;
                 if (B_MN) {
 #pragma unroll
-                    for (int c = 0; c < BN / 64; ++c) {
-                        if (c % CL != rank) continue;
-                        if constexpr (CL > 1)
-                            tc::tma_load_2d_mc(sb + c * 64 * BK * 2, &tmap_b, &full_bar[stage], n0 + c * 64, k0, kMask);
-                        else
-                            tc::tma_load_2d(sb + c * 64 * BK * 2, &tmap_b, &full_bar[stage], n0 + c * 64, k0);
-                    }
+                    for (int c = 0; c < BN / 64; ++c)
+                        tc::tma_load_2d(sb + c * 64 * BK * 2, &P.tb, &full_bar[stage], n0 + c * 64, k0);
                 } else {
-                    constexpr int kRows = BN / CL;
-                    if constexpr (CL > 1)
-                        tc::tma_load_2d_mc(sb + rank * kRows * 128, &tmap_b, &full_bar[stage], k0, n0 + rank * kRows, kMask);
-                    else
-                        tc::tma_load_2d(sb, &tmap_b, &full_bar[stage], k0, n0);
+                    tc::tma_load_2d(sb, &P.tb, &full_bar[stage], k0, n0);
                 }
             };
             // B stages of the first unit that do not depend on the previous kernel
             int pre = 0;
-            if (p.b_prefetch && cid < p.units) {
-                const Unit w = decode<CL>(p, cid, rank);
+            if (g.b_prefetch && cid < g.units) {
+                const Unit w = decode(g, cid);
+                const Prob& P = g.prob[w.pi];
                 pre = min(C::kStages, w.kb1 - w.kb0);
                 for (int i = 0; i < pre; ++i) {
                     tc::mbar_expect_tx(&full_bar[i], C::kStageBytes);
-                    load_b(i, w.tn * BN, (w.kb0 + i) * BK);
+                    load_b(P, i, w.tn * BN, (w.kb0 + i) * BK);
                 }
             }
             pdl_wait();
             int stage = 0;
             uint32_t phase = 0;
             int issued = 0;
-            for (int u = cid; u < p.units; u += ncl) {
-                const Unit w = decode<CL>(p, u, rank);
+            for (int u = cid; u < g.units; u += ncta) {
+                const Unit w = decode(g, u);
+                const Prob& P = g.prob[w.pi];
                 const int m0 = w.tm * BM, n0 = w.tn * BN;
                 for (int kb = w.kb0; kb < w.kb1; ++kb, ++issued) {
                     if (issued < pre) {  // expect_tx and B already issued
-                        load_a(stage, m0, kb * BK);
+                        load_a(P, stage, m0, kb * BK);
                     } else {
                         tc::mbar_wait(&empty_bar[stage], phase ^ 1);
                         tc::mbar_expect_tx(&full_bar[stage], C::kStageBytes);
-                        load_a(stage, m0, kb * BK);
-                        load_b(stage, n0, kb * BK);
+                        load_a(P, stage, m0, kb * BK);
+                        load_b(P, stage, n0, kb * BK);
                     }
                     if (++stage == C::kStages) { stage = 0; phase ^= 1; }
                 }
@@ -323,8 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         int stage = 0;
         uint32_t phase = 0;
         int local = 0;
-        for (int u = cid; u < p.units; u += ncl, ++local) {
-            const Unit w = decode<CL>(p, u, rank);
+        for (int u = cid; u < g.units; u += ncta, ++local) {
+            const Unit w = decode(g, u);
             const int kb0 = w.kb0, kb1 = w.kb1;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
@@ -350,8 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  : tc::umma_desc_sw128(sb + k * 32, 16, 1024);
                         tc::mma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
                     }
-                    if constexpr (CL > 1) tc::mma_commit_mc(&empty_bar[stage], kMask);
-                    else tc::mma_commit(&empty_bar[stage]);
+                    tc::mma_commit(&empty_bar[stage]);
                 }
                 __syncwarp();
                 if (++stage == C::kStages) { stage = 0; phase ^= 1; }
@@ -363,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == kBiasWarp) {
         // ------------------------------------------------------------ bias-grad warp
         // Second consumer of every smem stage.  For a wgrad (A = dY, MN-major)
-        // with dbias set, dbias[m] += sum_k dY[k, m]: the tiles_n CTAs that load
+        // with dbias set, dbias[m] += sum_k dY[k, m]: the tiles_n units that load
         // the same A rows share the work -- N-column tn sums the k-blocks with
         // kb % tiles_n == tn, so every k-block is summed exactly once.  Lane owns M = 4*lane..4*lane+3
         // (box lane/16, 16B chunk (lane%16)/2, half lane%2; rows are K,
@@ -371,42 +378,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         pdl_wait();
         int stage = 0;
         uint32_t phase = 0;
-        for (int u = cid; u < p.units; u += ncl) {
-            const Unit w = decode<CL>(p, u, rank);
+        for (int u = cid; u < g.units; u += ncta) {
+            const Unit w = decode(g, u);
+            const Prob& P = g.prob[w.pi];
             const int kb0 = w.kb0, kb1 = w.kb1, tn = w.tn;
-            const bool bias_sum = A_MN && p.dbias != nullptr;
+            float* dbias = P.dbias;
+            const int tiles_n = P.tiles_n;
+            const bool bias_sum = A_MN && dbias != nullptr;
             float bsum[4] = {0.f, 0.f, 0.f, 0.f};
             for (int kb = kb0; kb < kb1; ++kb) {
                 tc::mbar_wait(&full_bar[stage], phase);
-                if (bias_sum && kb % p.tiles_n == tn) {
+                if (bias_sum && kb % tiles_n == tn) {
                     const uint8_t* box = smem_a + stage * C::kABytes + (lane >> 4) * 64 * BK * 2;
                     const int chunk = (lane & 15) >> 1, sub = (lane & 1) * 8;
 #pragma unroll 8
                     for (int r = 0; r < BK; ++r) {
-                        const uint2 w = *reinterpret_cast<const uint2*>(
+                        const uint2 v = *reinterpret_cast<const uint2*>(
                             box + r * 128 + ((chunk ^ (r & 7)) * 16) + sub);
-                        bsum[0] += bf16_to_f(w.x & 0xffff);
-                        bsum[1] += bf16_to_f(w.x >> 16);
-                        bsum[2] += bf16_to_f(w.y & 0xffff);
-                        bsum[3] += bf16_to_f(w.y >> 16);
+                        bsum[0] += bf16_to_f(v.x & 0xffff);
+                        bsum[1] += bf16_to_f(v.x >> 16);
+                        bsum[2] += bf16_to_f(v.y & 0xffff);
+                        bsum[3] += bf16_to_f(v.y >> 16);
                     }
                 }
                 __syncwarp();
-                if (lane == 0) {
-                    if constexpr (CL > 1) {
-#pragma unroll
-                        for (int c = 0; c < CL; ++c) tc::mbar_arrive_cluster(&empty_bar[stage], c);
-                    } else {
-                        tc::mbar_arrive(&empty_bar[stage]);
-                    }
-                }
+                if (lane == 0) tc::mbar_arrive(&empty_bar[stage]);
                 if (++stage == C::kStages) { stage = 0; phase ^= 1; }
             }
             if (bias_sum) {
                 const int64_t m = int64_t(w.tm) * BM + 4 * lane;
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                    if (m + i < p.m) atomicAdd(p.dbias + m + i, bsum[i]);
+                    if (m + i < P.m) atomicAdd(dbias + m + i, bsum[i]);
             }
         }
     } else {
@@ -415,15 +418,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int lane_grp = warp & 3;                   // TMEM lanes this warp may access
         const int half = (warp - kEpiWarp0) >> 2;        // which half of the tile's columns
         constexpr int kChunks = BN / 32 / 2;             // 32-column chunks per warp
-        const bool out_bf16 = p.epilogue == MM_EPI_BF16 || p.epilogue == MM_EPI_BF16_RELU ||
-                              p.epilogue == MM_EPI_BF16_DRELU;
-        const bool reduce = p.epilogue == MM_EPI_F32_ACCUM;
-        const bool bias = has_bias(p);
         uint8_t* bufs = smem_epi + (warp - kEpiWarp0) * 2 * kEpiBufBytes;
         int nbuf = 0;
         int local = 0;
-        for (int u = cid; u < p.units; u += ncl, ++local) {
-            const Unit w = decode<CL>(p, u, rank);
+        for (int u = cid; u < g.units; u += ncta, ++local) {
+            const Unit w = decode(g, u);
+            const Prob& P = g.prob[w.pi];
+            const bool out_bf16 = P.epilogue == MM_EPI_BF16 || P.epilogue == MM_EPI_BF16_RELU ||
+                                  P.epilogue == MM_EPI_BF16_DRELU;
+            const bool reduce = P.epilogue == MM_EPI_F32_ACCUM;
+            const bool bias = has_bias(P);
             const int tm = w.tm, tn = w.tn;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
@@ -433,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c = 0; c < kChunks; ++c) {
                 const int col = cbase + c * 32 + lane;
-                bv[c] = (bias && col < p.n) ? __ldg(p.bias + col) : 0.f;
+                bv[c] = (bias && col < P.n) ? __ldg(P.bias + col) : 0.f;
             }
             tc::mbar_wait(&tfull_bar[acc], acc_phase);
             tc::tc_fence_after();
@@ -445,14 +449,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c = 0; c < kChunks; ++c) {
                 const int col0 = cbase + c * 32;
-                if (col0 < p.n) {
+                if (col0 < P.n) {
                     uint32_t v[32];
                     tc::tmem_ld_32x32(t_row + c * 32, v);
                     tc::tmem_ld_wait();
                     float f[32];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-                    epilogue_math(p, row, col0, f, bv[c]);
+                    epilogue_math(P, row, col0, f, bv[c]);
                     uint8_t* buf = bufs + nbuf * kEpiBufBytes;
                     if (lane == 0) tc::bulk_wait_read<1>();  // the store that last read `buf` is done
                     __syncwarp();
@@ -460,8 +464,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc::fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        if (reduce) tc::tma_reduce_add_2d(&tmap_d, buf, col0, row0);
-                        else tc::tma_store_2d(&tmap_d, buf, col0, row0);
+                        if (reduce) tc::tma_reduce_add_2d(&P.td, buf, col0, row0);
+                        else tc::tma_store_2d(&P.td, buf, col0, row0);
                         tc::bulk_commit();
                     }
                     nbuf ^= 1;
@@ -480,8 +484,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tc_fence_after();
         tc::tmem_dealloc(tmem_base, C::kTmemCols);
     }
-    // no CTA leaves while a peer may still arrive on its barriers
-    if constexpr (CL > 1) tc::cluster_sync();
     if (threadIdx.x == 0) MM_TRACE(7);
 }
 
@@ -528,31 +530,28 @@ int make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, i
     return 0;
 }
 
-template <int BN, int A_MN, int B_MN, int CL>
-int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md, const Params& p,
-           cudaStream_t s) {
-    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, CL>;
+template <int BN, int A_MN, int B_MN, int NP>
+int launch(const Group<NP>& g, cudaStream_t s) {
+    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, NP>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg<BN>::kSmem));
         attr_set = true;
     }
-    // persistent: one CTA per SM, in clusters of CL CTAs (p.units counts cluster units)
-    const int clusters = std::min(p.units, mm::num_sms() / CL);
-    MM_CUDA_TRY(mm::launch_pdl_cluster(kern, dim3(clusters * CL), dim3(kThreads), Cfg<BN>::kSmem, s,
-                                       unsigned(CL), ma, mb, md, p));
+    // persistent: one CTA per SM
+    const int ctas = std::min(g.units, mm::num_sms());
+    MM_CUDA_TRY(mm::launch_pdl(kern, dim3(ctas), dim3(kThreads), Cfg<BN>::kSmem, s, g));
     MM_LAUNCH_CHECK("gemm_tcgen05_kernel");
     return 0;
 }
 
-template <int BN, int CL>
-int dispatch(int a_mn, int b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
-             const CUtensorMap& md, const Params& p, cudaStream_t s) {
-    if (!a_mn && !b_mn) return launch<BN, 0, 0, CL>(ma, mb, md, p, s);
-    if (!a_mn && b_mn) return launch<BN, 0, 1, CL>(ma, mb, md, p, s);
-    if (a_mn && !b_mn) return launch<BN, 1, 0, CL>(ma, mb, md, p, s);
-    return launch<BN, 1, 1, CL>(ma, mb, md, p, s);
+template <int BN, int NP>
+int dispatch(int a_mn, int b_mn, const Group<NP>& g, cudaStream_t s) {
+    if (!a_mn && !b_mn) return launch<BN, 0, 0, NP>(g, s);
+    if (!a_mn && b_mn) return launch<BN, 0, 1, NP>(g, s);
+    if (a_mn && !b_mn) return launch<BN, 1, 0, NP>(g, s);
+    return launch<BN, 1, 1, NP>(g, s);
 }
 
 unsigned long long* g_trace_buf = nullptr;  // set by mm_gemm_trace (diagnostics)
@@ -564,6 +563,162 @@ struct GemmTiming {
     std::vector<double> flops;
     size_t used = 0;
 } g_timing;
+
+bool out_bf16_epi(int e) {
+    return e == MM_EPI_BF16 || e == MM_EPI_BF16_RELU || e == MM_EPI_BF16_DRELU;
+}
+
+int check_args(const mm_gemm_args* a) {
+    MM_CHECK_ARG(a != nullptr, "args is NULL");
+    MM_CHECK_ARG(a->m > 0 && a->n > 0 && a->k > 0, "empty GEMM %lldx%lldx%lld", (long long)a->m,
+                 (long long)a->n, (long long)a->k);
+    MM_CHECK_ARG(a->epilogue >= MM_EPI_BF16 && a->epilogue <= MM_EPI_BF16_DRELU, "bad epilogue");
+    MM_CHECK_ARG(a->a && a->b && a->d, "NULL operand");
+    const bool out_bf16 = out_bf16_epi(a->epilogue);
+    MM_CHECK_ARG((a->lda % 8) == 0 && (a->ldb % 8) == 0, "lda/ldb must be multiples of 8");
+    MM_CHECK_ARG((reinterpret_cast<uintptr_t>(a->a) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(a->b) & 15) == 0,
+                 "A/B must be 16-byte aligned");
+    MM_CHECK_ARG((reinterpret_cast<uintptr_t>(a->d) & 15) == 0 && (a->ldd % (out_bf16 ? 8 : 4)) == 0,
+                 "D must be 16-byte aligned with 16-byte row stride");
+    MM_CHECK_ARG(a->epilogue != MM_EPI_F32_RESID || a->resid, "RESID epilogue needs resid");
+    MM_CHECK_ARG(a->epilogue != MM_EPI_BF16_DRELU || a->aux, "DRELU epilogue needs aux");
+    MM_CHECK_ARG(a->dbias == nullptr || !a->a_kmajor, "dbias needs an MN-major A operand");
+    MM_CHECK_ARG(a->m < (int64_t(1) << 31) && a->n < (int64_t(1) << 31) && a->k < (int64_t(1) << 31),
+                 "GEMM dimension >= 2^31");
+    return 0;
+}
+
+// Tile width for a launch: minimise waves x (tile width + per-tile overhead
+// ~ 64 columns) over the launch's total tile count.
+int choose_bn(const mm_gemm_args* const* probs, int n, int sms) {
+    int bn = 128;
+    double best = 1e300;
+    for (int cand : {256, 192, 128}) {
+        bool fits = true;
+        int64_t t = 0;
+        for (int i = 0; i < n; ++i) {
+            if (cand > 128 && probs[i]->n <= cand - 64) fits = false;
+            t += ((probs[i]->m + BM - 1) / BM) * ((probs[i]->n + cand - 1) / cand);
+        }
+        if (!fits) continue;
+        const double cost = double((t + sms - 1) / sms) * (cand + 64);
+        if (cost < best - 1e-9) { best = cost; bn = cand; }
+    }
+    if (const char* force = std::getenv("MM_GEMM_BN")) {  // diagnostics
+        const int f = std::atoi(force);
+        if (f == 128 || f == 192 || f == 256) bn = f;
+    }
+    return bn;
+}
+
+// Fill one problem of a launch (tensor maps + tiling); splits K for fp32
+// accumulation when the launch has fewer tiles than two waves.
+int setup_prob(Prob& P, const mm_gemm_args* a, int bn, int splits_cap) {
+    const bool out_bf16 = out_bf16_epi(a->epilogue);
+    const int a_mn = a->a_kmajor ? 0 : 1;
+    const int b_mn = a->b_kmajor ? 0 : 1;
+    const int64_t tiles_m = (a->m + BM - 1) / BM;
+    const int64_t tiles_n = (a->n + bn - 1) / bn;
+    const int num_kb = static_cast<int>((a->k + BK - 1) / BK);
+    int splits = a->epilogue == MM_EPI_F32_ACCUM ? std::max(1, std::min(splits_cap, num_kb / 2)) : 1;
+    const int kb_per = (num_kb + splits - 1) / splits;
+    splits = (num_kb + kb_per - 1) / kb_per;  // no empty splits
+    MM_CHECK_ARG(tiles_m * tiles_n * splits < (int64_t(1) << 31), "GEMM too large");
+    int st;
+    // A: K-major [M, K] rows of lda; MN-major [K, M] rows of lda
+    st = a_mn ? make_map(&P.ta, a->a, a->m, a->k, a->lda, BK)
+              : make_map(&P.ta, a->a, a->k, a->m, a->lda, BM);
+    if (st) return st;
+    st = b_mn ? make_map(&P.tb, a->b, a->n, a->k, a->ldb, BK)
+              : make_map(&P.tb, a->b, a->k, a->n, a->ldb, bn);
+    if (st) return st;
+    // D: 32 x 32 boxes, swizzle matching the staging layout
+    st = make_map(&P.td, a->d, a->n, a->m, a->ldd, 32, 32, !out_bf16,
+                  out_bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
+    if (st) return st;
+    P.m = a->m; P.n = a->n; P.k = a->k; P.ldd = a->ldd;
+    P.d = a->d; P.bias = a->bias; P.resid = a->resid;
+    P.aux = reinterpret_cast<const __nv_bfloat16*>(a->aux);
+    P.dbias = a->dbias;
+    P.epilogue = a->epilogue;
+    P.tiles_m = static_cast<int>(tiles_m);
+    P.tiles_n = static_cast<int>(tiles_n);
+    P.splits = splits;
+    P.kb_per_split = kb_per;
+    P.num_kb = num_kb;
+    return 0;
+}
+
+// K-split for fp32-accumulating launches: double while the launch stays
+// within two waves
+int split_cap(const mm_gemm_args* const* probs, int n, int bn, int sms) {
+    int64_t tiles = 0;
+    int min_kb = 1 << 30;
+    bool all_accum = true;
+    for (int i = 0; i < n; ++i) {
+        tiles += ((probs[i]->m + BM - 1) / BM) * ((probs[i]->n + bn - 1) / bn);
+        min_kb = std::min<int>(min_kb, static_cast<int>((probs[i]->k + BK - 1) / BK));
+        all_accum = all_accum && probs[i]->epilogue == MM_EPI_F32_ACCUM;
+    }
+    int splits = 1;
+    if (all_accum)
+        while (tiles * splits * 2 <= 2 * sms && splits * 2 <= min_kb / 2) splits *= 2;
+    return splits;
+}
+
+template <int NP>
+int run_group(const mm_gemm_args* const* probs, int n, cudaStream_t s) {
+    const int sms = mm::num_sms();
+    const int bn = choose_bn(probs, n, sms);
+    const int cap = split_cap(probs, n, bn, sms);
+    static Group<NP> g;  // host staging of the kernel parameter (large: tensor maps)
+    std::memset(&g, 0, sizeof(g));
+    int64_t units = 0;
+    double flops = 0;
+    static const bool log = std::getenv("MM_GEMM_LOG") != nullptr;  // diagnostics
+    for (int i = 0; i < n; ++i) {
+        Prob& P = g.prob[i];
+        if (int st = setup_prob(P, probs[i], bn, cap)) return st;
+        P.unit_begin = static_cast<int>(units);
+        units += int64_t(P.tiles_m) * P.tiles_n * P.splits;
+        MM_CHECK_ARG(units < (int64_t(1) << 31), "GEMM launch too large");
+        flops += 2.0 * double(probs[i]->m) * double(probs[i]->n) * double(probs[i]->k);
+        if (log)
+            std::fprintf(stderr, "mm_gemm m=%lld n=%lld k=%lld a_mn=%d b_mn=%d epi=%d bn=%d splits=%d units=%d group=%d/%d\n",
+                         (long long)probs[i]->m, (long long)probs[i]->n, (long long)probs[i]->k,
+                         probs[i]->a_kmajor ? 0 : 1, probs[i]->b_kmajor ? 0 : 1, probs[i]->epilogue,
+                         bn, P.splits, P.tiles_m * P.tiles_n * P.splits, i, n);
+    }
+    g.n_probs = n;
+    g.units = static_cast<int>(units);
+    g.trace = g_trace_buf;
+    g.b_prefetch = 1;
+    for (int i = 0; i < n; ++i) g.b_prefetch &= probs[i]->b_prefetch ? 1 : 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (g_timing.on) {
+        if (g_timing.ev.size() < 2 * (g_timing.used + 1)) {
+            for (int i = 0; i < 2; ++i) {
+                cudaEvent_t e;
+                MM_CUDA_TRY(cudaEventCreate(&e));
+                g_timing.ev.push_back(e);
+            }
+        }
+        e0 = g_timing.ev[2 * g_timing.used];
+        e1 = g_timing.ev[2 * g_timing.used + 1];
+        g_timing.flops.push_back(flops);
+        ++g_timing.used;
+        MM_CUDA_TRY(cudaEventRecord(e0, s));
+    }
+    const int a_mn = probs[0]->a_kmajor ? 0 : 1;
+    const int b_mn = probs[0]->b_kmajor ? 0 : 1;
+    int rc;
+    if (bn == 256) rc = dispatch<256, NP>(a_mn, b_mn, g, s);
+    else if (bn == 192) rc = dispatch<192, NP>(a_mn, b_mn, g, s);
+    else rc = dispatch<128, NP>(a_mn, b_mn, g, s);
+    if (rc == 0 && e1) MM_CUDA_TRY(cudaEventRecord(e1, s));
+    return rc;
+}
 
 }  // namespace
 
@@ -598,115 +753,25 @@ extern "C" int mm_gemm_timing(int mode, double* flops, float* ms, int* launches)
 }
 
 extern "C" int mm_gemm(const mm_gemm_args* a, void* stream) {
-    MM_CHECK_ARG(a != nullptr, "args is NULL");
-    MM_CHECK_ARG(a->m > 0 && a->n > 0 && a->k > 0, "empty GEMM %lldx%lldx%lld", (long long)a->m,
-                 (long long)a->n, (long long)a->k);
-    MM_CHECK_ARG(a->epilogue >= MM_EPI_BF16 && a->epilogue <= MM_EPI_BF16_DRELU, "bad epilogue");
-    MM_CHECK_ARG(a->a && a->b && a->d, "NULL operand");
-    const bool out_bf16 = a->epilogue == MM_EPI_BF16 || a->epilogue == MM_EPI_BF16_RELU ||
-                          a->epilogue == MM_EPI_BF16_DRELU;
-    MM_CHECK_ARG((a->lda % 8) == 0 && (a->ldb % 8) == 0, "lda/ldb must be multiples of 8");
-    MM_CHECK_ARG((reinterpret_cast<uintptr_t>(a->a) & 15) == 0 &&
-                     (reinterpret_cast<uintptr_t>(a->b) & 15) == 0,
-                 "A/B must be 16-byte aligned");
-    MM_CHECK_ARG((reinterpret_cast<uintptr_t>(a->d) & 15) == 0 && (a->ldd % (out_bf16 ? 8 : 4)) == 0,
-                 "D must be 16-byte aligned with 16-byte row stride");
-    MM_CHECK_ARG(a->epilogue != MM_EPI_F32_RESID || a->resid, "RESID epilogue needs resid");
-    MM_CHECK_ARG(a->epilogue != MM_EPI_BF16_DRELU || a->aux, "DRELU epilogue needs aux");
-    MM_CHECK_ARG(a->dbias == nullptr || !a->a_kmajor, "dbias needs an MN-major A operand");
-    const int a_mn = a->a_kmajor ? 0 : 1;
-    const int b_mn = a->b_kmajor ? 0 : 1;
+    if (int st = check_args(a)) return st;
+    return run_group<1>(&a, 1, mm::as_stream(stream));
+}
 
-    // tile width: minimise waves x (tile width + per-tile overhead ~ 64 columns)
-    const int64_t tiles_m = (a->m + BM - 1) / BM;
-    const int sms = mm::num_sms();
-    int bn = 128;
-    {
-        double best = 1e300;
-        for (int cand : {256, 192, 128}) {
-            if (cand > 128 && a->n <= cand - 64) continue;
-            const int64_t t = tiles_m * ((a->n + cand - 1) / cand);
-            const double cost = double((t + sms - 1) / sms) * (cand + 64);
-            if (cost < best - 1e-9) { best = cost; bn = cand; }
-        }
+extern "C" int mm_gemm_grouped(const mm_gemm_args* probs, int n, void* stream) {
+    MM_CHECK_ARG(probs != nullptr && n >= 0, "bad problem list");
+    if (n == 0) return 0;
+    for (int i = 0; i < n; ++i) {
+        if (int st = check_args(&probs[i])) return st;
+        MM_CHECK_ARG(probs[i].a_kmajor == probs[0].a_kmajor && probs[i].b_kmajor == probs[0].b_kmajor,
+                     "grouped GEMM: problem %d operand majorness differs from problem 0", i);
     }
-    if (const char* force = std::getenv("MM_GEMM_BN")) {  // diagnostics
-        const int f = std::atoi(force);
-        if (f == 128 || f == 192 || f == 256) bn = f;
+    const mm_gemm_args* ptrs[kMaxProbs];
+    for (int i0 = 0; i0 < n; i0 += kMaxProbs) {
+        const int cnt = std::min(kMaxProbs, n - i0);
+        for (int i = 0; i < cnt; ++i) ptrs[i] = &probs[i0 + i];
+        if (int st = cnt == 1 ? run_group<1>(ptrs, 1, mm::as_stream(stream))
+                              : run_group<kMaxProbs>(ptrs, cnt, mm::as_stream(stream)))
+            return st;
     }
-    const int64_t tiles_n = (a->n + bn - 1) / bn;
-    const int num_kb = static_cast<int>((a->k + BK - 1) / BK);
-    // Optional 2-CTA clusters stacked along M sharing the B tile by TMA
-    // multicast (an odd last pair computes an out-of-range tile: zero-filled
-    // loads, clipped stores).  Off by default: measured 2-2.5x slower k-loops
-    // on B200 at cluster size 2 (the stage coupling costs more than the
-    // multicast saves); MM_GEMM_CLUSTER=2 enables it for experiments.
-    const char* cl_env = std::getenv("MM_GEMM_CLUSTER");
-    const int cl = (tiles_m >= 2 && cl_env && std::atoi(cl_env) == 2) ? 2 : 1;
-    const int64_t tiles = ((tiles_m + cl - 1) / cl) * cl * tiles_n;
-    // split K (fp32 accumulate only: partials meet in the TMA reduce-add)
-    int splits = 1;
-    if (a->epilogue == MM_EPI_F32_ACCUM) {
-        while (tiles * splits * 2 <= 2 * sms && splits * 2 <= num_kb / 2) splits *= 2;
-    }
-    const int kb_per = (num_kb + splits - 1) / splits;
-    splits = (num_kb + kb_per - 1) / kb_per;  // no empty splits
-    MM_CHECK_ARG(tiles * splits < (int64_t(1) << 31), "GEMM too large");
-
-    CUtensorMap ma, mb, md;
-    int st;
-    // A: K-major [M, K] rows of lda; MN-major [K, M] rows of lda
-    st = a_mn ? make_map(&ma, a->a, a->m, a->k, a->lda, BK)
-              : make_map(&ma, a->a, a->k, a->m, a->lda, BM);
-    if (st) return st;
-    st = b_mn ? make_map(&mb, a->b, a->n, a->k, a->ldb, BK)
-              : make_map(&mb, a->b, a->k, a->n, a->ldb, bn / cl);
-    if (st) return st;
-    // D: 32 x 32 boxes, swizzle matching the staging layout
-    st = make_map(&md, a->d, a->n, a->m, a->ldd, 32, 32, !out_bf16,
-                  out_bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
-    if (st) return st;
-
-    Params p{};
-    p.m = a->m; p.n = a->n; p.k = a->k; p.ldd = a->ldd;
-    p.d = a->d; p.bias = a->bias; p.resid = a->resid;
-    p.aux = reinterpret_cast<const __nv_bfloat16*>(a->aux);
-    p.dbias = a->dbias;
-    p.b_prefetch = a->b_prefetch;
-    p.trace = g_trace_buf;
-    p.epilogue = a->epilogue;
-    p.tiles_m = static_cast<int>(tiles_m);
-    p.tiles_n = static_cast<int>(tiles_n);
-    p.splits = splits;
-    p.kb_per_split = kb_per;
-    p.num_kb = num_kb;
-    p.units = static_cast<int>(tiles / cl * splits);  // cluster units
-    cudaStream_t s = mm::as_stream(stream);
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (g_timing.on) {
-        if (g_timing.ev.size() < 2 * (g_timing.used + 1)) {
-            for (int i = 0; i < 2; ++i) {
-                cudaEvent_t e;
-                MM_CUDA_TRY(cudaEventCreate(&e));
-                g_timing.ev.push_back(e);
-            }
-        }
-        e0 = g_timing.ev[2 * g_timing.used];
-        e1 = g_timing.ev[2 * g_timing.used + 1];
-        g_timing.flops.push_back(2.0 * double(a->m) * double(a->n) * double(a->k));
-        ++g_timing.used;
-        MM_CUDA_TRY(cudaEventRecord(e0, s));
-    }
-    int rc;
-    if (cl == 2) {
-        if (bn == 256) rc = dispatch<256, 2>(a_mn, b_mn, ma, mb, md, p, s);
-        else if (bn == 192) rc = dispatch<192, 2>(a_mn, b_mn, ma, mb, md, p, s);
-        else rc = dispatch<128, 2>(a_mn, b_mn, ma, mb, md, p, s);
-    } else {
-        if (bn == 256) rc = dispatch<256, 1>(a_mn, b_mn, ma, mb, md, p, s);
-        else if (bn == 192) rc = dispatch<192, 1>(a_mn, b_mn, ma, mb, md, p, s);
-        else rc = dispatch<128, 1>(a_mn, b_mn, ma, mb, md, p, s);
-    }
-    if (rc == 0 && e1) MM_CUDA_TRY(cudaEventRecord(e1, s));
-    return rc;
+    return 0;
 }

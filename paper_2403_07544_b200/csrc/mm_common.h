@@ -1,6 +1,7 @@
 // Shared plumbing for libmmb200: error reporting and launch helpers.
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <string>
@@ -24,6 +25,9 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int num_sms();
 
+// every kernel launch of the library (bench.py's gpu_launches; mm_launch_count)
+extern std::atomic<unsigned long long> g_launches;
+
 // Programmatic dependent launch: every kernel of the library is launched with
 // programmatic stream serialization, waits (griddepcontrol.wait) before its
 // first global-memory access and signals launch_dependents when its main work
@@ -46,6 +50,7 @@ inline cudaError_t launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 bl
     at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = cluster_x > 1 ? 2 : 1;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 template <typename... KArgs, typename... Args>

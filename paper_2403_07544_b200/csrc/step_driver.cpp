@@ -6,10 +6,21 @@
 //   self block : x' = x + Attn(LN1(x)) Wo^T + bo
 //   cross block: x' = x + CrossAttn(LNc(x), mem) Wco^T + bco     (decoder)
 //   FFN block  : x' = x + relu(LN2(x) W1^T + b1) W2^T + b2
-// Activations are bump-allocated from the caller's workspace; the backward
-// temporaries of one block are released when the block is done.
+// Activations are bump-allocated from the caller's workspace.
+//
+// Weight gradients are off the backward critical path (nothing downstream
+// reads dW until the optimizer), so the driver defers them: every wgrad of a
+// side (decoder + generator, then encoder) is queued and issued as ONE grouped
+// persistent GEMM launch when that side's backward is done.  Small per-layer
+// wgrads (512x512 ... 2048x512, K = tokens) then share one unit list instead
+// of paying a launch tail and a partial wave each.  The dY operands they read
+// stay alive until the flush (per-block dx_bf copies, no temporaries
+// released); MM_DEFER_WGRAD=0 restores eager wgrads with block-scoped
+// temporaries.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "mm_common.h"
 
@@ -84,9 +95,33 @@ struct Driver {
     // dW[out,in] += dY[T,out]^T X[T,in];  db[out] += sum_t dY[t,out] (fused)
     int wgrad(const uint16_t* dY, const uint16_t* X, float* dW, int64_t T, int64_t in, int64_t out,
               float* db) {
-        return gemm(dY, false, X, false, dW, out, in, T, out, in, in, MM_EPI_F32_ACCUM, nullptr,
-                    nullptr, nullptr, db);
+        mm_gemm_args a{};
+        a.a = dY; a.b = X; a.d = dW; a.dbias = db;
+        a.m = out; a.n = in; a.k = T; a.lda = out; a.ldb = in; a.ldd = in;
+        a.a_kmajor = 0; a.b_kmajor = 0; a.epilogue = MM_EPI_F32_ACCUM;
+        a.b_prefetch = 1;
+        if (defer) {
+            pending.push_back(a);
+            return 0;
+        }
+        return mm_gemm(&a, s);
     }
+    bool defer = true;
+    std::vector<mm_gemm_args> pending;
+    int flush_wgrads() {
+        if (!sizing && !pending.empty()) {
+            if (int st = mm_gemm_grouped(pending.data(), static_cast<int>(pending.size()), s)) return st;
+        }
+        pending.clear();
+        return 0;
+    }
+    // block-scoped temporaries are released only when nothing deferred reads them
+    void release(size_t mark) {
+        if (!defer) ar.off = mark;
+    }
+    // buffer for dL/d(block input) in bf16: a fresh one per block while wgrads
+    // are deferred (the queued wgrads of this block read the previous one)
+    uint16_t* next_bf(uint16_t* cur, int64_t rows) { return defer ? ar.get<uint16_t>(rows * d) : cur; }
 
     int ln(const mm_stack* st, int64_t go, int64_t bo, const float* x, int64_t T, uint16_t*& y,
            float*& mean, float*& rstd) {
@@ -169,7 +204,7 @@ struct Driver {
 
     // ------------------------------------------------------------ backward
     // dx (fp32) / dx_bf hold dL/d(block output) on entry, dL/d(block input) on exit
-    int ffn_bwd(Layer& L, float* dx, uint16_t* dx_bf, int64_t T) {
+    int ffn_bwd(Layer& L, float* dx, uint16_t*& dx_bf, int64_t T) {
         const mm_stack* st = L.st;
         const mm_layer_offsets* o = L.o;
         FfnSave& sv = L.ffn;
@@ -180,13 +215,15 @@ struct Driver {
         TRY(wgrad(df, sv.h, g(st, o->ff1_w), T, d, F, g(st, o->ff1_b)));
         float* dh = ar.get<float>(T * d);
         TRY(dgrad(df, wb(st, o->ff1_w), dh, T, d, F, MM_EPI_F32));
-        TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->ln2_g), sv.mean, sv.rstd, dx, dx_bf,
+        uint16_t* nbf = next_bf(dx_bf, T);
+        TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->ln2_g), sv.mean, sv.rstd, dx, nbf,
                              g(st, o->ln2_g), g(st, o->ln2_b), T, d, s));
-        ar.off = mark;
+        dx_bf = nbf;
+        release(mark);
         return 0;
     }
 
-    int self_bwd(Layer& L, float* dx, uint16_t* dx_bf, int64_t T, const int32_t* cu, int maxlen,
+    int self_bwd(Layer& L, float* dx, uint16_t*& dx_bf, int64_t T, const int32_t* cu, int maxlen,
                  bool causal, const int32_t* groups, int ng, int cap) {
         const mm_stack* st = L.st;
         const mm_layer_offsets* o = L.o;
@@ -204,13 +241,15 @@ struct Driver {
         TRY(wgrad(dqkv, sv.h, g(st, o->qkv_w), T, d, 3 * d, g(st, o->qkv_b)));
         float* dh = ar.get<float>(T * d);
         TRY(dgrad(dqkv, wb(st, o->qkv_w), dh, T, d, 3 * d, MM_EPI_F32));
-        TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->ln1_g), sv.mean, sv.rstd, dx, dx_bf,
+        uint16_t* nbf = next_bf(dx_bf, T);
+        TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->ln1_g), sv.mean, sv.rstd, dx, nbf,
                              g(st, o->ln1_g), g(st, o->ln1_b), T, d, s));
-        ar.off = mark;
+        dx_bf = nbf;
+        release(mark);
         return 0;
     }
 
-    int cross_bwd(Layer& L, float* dx, uint16_t* dx_bf, const uint16_t* mem, float* dmem) {
+    int cross_bwd(Layer& L, float* dx, uint16_t*& dx_bf, const uint16_t* mem, float* dmem) {
         const mm_stack* st = L.st;
         const mm_layer_offsets* o = L.o;
         CrossSave& sv = L.cross;
@@ -232,9 +271,11 @@ struct Driver {
         TRY(wgrad(dq, sv.h, g(st, o->cq_w), T, d, d, g(st, o->cq_b)));
         float* dh = ar.get<float>(T * d);
         TRY(dgrad(dq, wb(st, o->cq_w), dh, T, d, d, MM_EPI_F32));
-        TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->lnc_g), sv.mean, sv.rstd, dx, dx_bf,
+        uint16_t* nbf = next_bf(dx_bf, T);
+        TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->lnc_g), sv.mean, sv.rstd, dx, nbf,
                              g(st, o->lnc_g), g(st, o->lnc_b), T, d, s));
-        ar.off = mark;
+        dx_bf = nbf;
+        release(mark);
         return 0;
     }
 
@@ -301,6 +342,7 @@ struct Driver {
             if (int e = self_bwd(dec_l[l], dy, dy_bf, Tt, b.cu_tgt, b.max_tgt, true, b.groups_tgt, b.ng_tgt, b.cap_tgt)) return e;
         }
         TRY(mm_embed_bwd(b.tgt_in, dy, t.dec_emb.grad + t.dec_emb.emb, Tt, d, scale, s));
+        if (int e = flush_wgrads()) return e;  // decoder side + generator
         if (dec_done && !sizing) MM_CUDA_TRY(cudaEventRecord(dec_done, s));
         // ---- encoder backward
         float* dx = ar.get<float>(Ts * d);
@@ -313,6 +355,7 @@ struct Driver {
             if (int e = self_bwd(enc_l[l], dx, dx_bf, Ts, b.cu_src, b.max_src, false, b.groups_src, b.ng_src, b.cap_src)) return e;
         }
         TRY(mm_embed_bwd(b.src, dx, t.enc_emb.grad + t.enc_emb.emb, Ts, d, scale, s));
+        if (int e = flush_wgrads()) return e;  // encoder side
         return 0;
     }
 };
@@ -333,6 +376,10 @@ extern "C" int mm_task_fwd_bwd(const mm_task* task, const mm_batch* batch, void*
     MM_CHECK_ARG(nl <= 64, "more than 64 decoder layers");
     MM_CHECK_ARG(task->enc[task->n_enc - 1].lnf_g >= 0 && task->dec[task->n_dec - 1].lnf_g >= 0,
                  "last stack of each side needs its final LayerNorm");
+    static const bool defer = [] {
+        const char* e = std::getenv("MM_DEFER_WGRAD");
+        return !(e && e[0] == '0');
+    }();
     Arena ar;
     ar.base = static_cast<uint8_t*>(workspace);
     ar.sizing = workspace == nullptr;
@@ -343,11 +390,13 @@ extern "C" int mm_task_fwd_bwd(const mm_task* task, const mm_batch* batch, void*
         Arena probe;
         Driver p{*task, *batch, probe, mm::as_stream(stream), true, task->d_model, task->heads,
                  task->ffn, task->vocab};
+        p.defer = defer;
         p.run(loss_sum);
         MM_CHECK_ARG(probe.peak <= *ws_bytes, "workspace %zu B < required %zu B", *ws_bytes,
                      probe.peak);
     }
     drv.dec_done = static_cast<cudaEvent_t>(dec_done);
+    drv.defer = defer;
     const int st = drv.run(loss_sum);
     if (ar.sizing) *ws_bytes = ar.peak;
     return st;

@@ -73,13 +73,10 @@ def _rowstride(t: torch.Tensor, name: str) -> int:
     return t.stride(0)
 
 
-def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bool = True,
-         b_kmajor: bool = True, epilogue: int = EPI_BF16, bias=None, resid=None, aux=None,
-         dbias=None) -> None:
-    """d[M,N] (epilogue)= op(a) @ op(b)^T on tcgen05.
-
-    a: [M,K] if a_kmajor else [K,M]; b: [N,K] if b_kmajor else [K,N] (bf16).
-    """
+def gemm_args(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bool = True,
+              b_kmajor: bool = True, epilogue: int = EPI_BF16, bias=None, resid=None, aux=None,
+              dbias=None) -> GemmArgs:
+    """Validated mm_gemm_args for d[M,N] (epilogue)= op(a) @ op(b)^T."""
     _need(a, torch.bfloat16, "a")
     _need(b, torch.bfloat16, "b")
     m, k = (a.shape[0], a.shape[1]) if a_kmajor else (a.shape[1], a.shape[0])
@@ -99,6 +96,20 @@ def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bool = 
         raise ValueError("resid must share d's row stride")
     if aux is not None and _rowstride(aux, "aux") != args.ldd:
         raise ValueError("aux must share d's row stride")
+    args.b_prefetch = 0
+    return args
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bool = True,
+         b_kmajor: bool = True, epilogue: int = EPI_BF16, bias=None, resid=None, aux=None,
+         dbias=None) -> None:
+    """d[M,N] (epilogue)= op(a) @ op(b)^T on tcgen05.
+
+    a: [M,K] if a_kmajor else [K,M]; b: [N,K] if b_kmajor else [K,N] (bf16).
+    """
+    args = gemm_args(a, b, d, a_kmajor=a_kmajor, b_kmajor=b_kmajor, epilogue=epilogue,
+                     bias=bias, resid=resid, aux=aux, dbias=dbias)
+    m, n, k = args.m, args.n, args.k
     LAUNCHES[0] += 1
     if GEMM_PROFILE is not None:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -108,6 +119,17 @@ def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bool = 
         GEMM_PROFILE.append((2.0 * m * n * k, e0, e1))
         return
     check(lib().mm_gemm(ctypes.byref(args), stream_ptr()), "mm_gemm")
+
+
+def gemm_grouped(problems: list) -> None:
+    """Several independent GEMMs in one persistent launch (mm_gemm_grouped).
+
+    problems: list of dicts of gemm() keyword arguments (a, b, d, ...); all
+    must share a_kmajor / b_kmajor.
+    """
+    arr = (GemmArgs * len(problems))(*[gemm_args(**p) for p in problems])
+    LAUNCHES[0] += (len(problems) + 23) // 24
+    check(lib().mm_gemm_grouped(arr, len(problems), stream_ptr()), "mm_gemm_grouped")
 
 
 def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-6) -> None:

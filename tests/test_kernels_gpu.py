@@ -80,6 +80,69 @@ def test_gemm_wgrad_accumulate(cuda, shape):
     assert rel_err(db, ref_b) < 1e-4  # fused bias gradient (column sums of dY)
 
 
+def test_gemm_grouped_wgrad(cuda):
+    """One grouped launch of a layer's worth of wgrads (mixed M, N, K; two
+    problems accumulate into the same dW) == per-problem fp32 references."""
+    from paper_2403_07544_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(11)
+    shapes = [(512, 512, 4096), (1536, 512, 4096), (2048, 512, 4096), (512, 2048, 4096),
+              (1024, 512, 333), (32000, 512, 1024), (200, 136, 64)]
+    probs, refs = [], []
+    for n_out, n_in, t in shapes:
+        dy = torch.randn(t, n_out, device=cuda, generator=g).bfloat16()
+        x = torch.randn(t, n_in, device=cuda, generator=g).bfloat16()
+        dw = torch.randn(n_out, n_in, device=cuda, generator=g)
+        db = torch.randn(n_out, device=cuda, generator=g)
+        refs.append((dw, dw + dy.float().t() @ x.float(), db, db + dy.float().sum(0)))
+        probs.append(dict(a=dy, b=x, d=dw, a_kmajor=False, b_kmajor=False,
+                          epilogue=ops.EPI_F32_ACCUM, dbias=db))
+    # a second contribution to problem 0's dW / db in the same launch
+    dy2 = torch.randn(4096, 512, device=cuda, generator=g).bfloat16()
+    x2 = torch.randn(4096, 512, device=cuda, generator=g).bfloat16()
+    dw0, r0, db0, rb0 = refs[0]
+    refs[0] = (dw0, r0 + dy2.float().t() @ x2.float(), db0, rb0 + dy2.float().sum(0))
+    probs.append(dict(a=dy2, b=x2, d=dw0, a_kmajor=False, b_kmajor=False,
+                      epilogue=ops.EPI_F32_ACCUM, dbias=db0))
+    ops.gemm_grouped(probs)
+    for dw, ref, db, ref_b in refs:
+        assert rel_err(dw, ref) < 2e-3
+        assert rel_err(db, ref_b) < 1e-4
+
+
+def test_gemm_grouped_forward_epilogues(cuda):
+    """Grouped launch with a different epilogue per problem (K-major operands)."""
+    from paper_2403_07544_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(12)
+    probs, checks = [], []
+    for i, (m, n, k) in enumerate([(4096, 1536, 512), (333, 512, 512), (4096, 2048, 512),
+                                   (1000, 512, 2048)]):
+        A = torch.randn(m, k, device=cuda, generator=g).bfloat16()
+        B = (torch.randn(n, k, device=cuda, generator=g) / math.sqrt(k)).bfloat16()
+        bias = torch.randn(n, device=cuda, generator=g)
+        ref = A.float() @ B.float().t() + bias
+        if i % 2 == 0:
+            d = torch.empty(m, n, device=cuda, dtype=torch.bfloat16)
+            probs.append(dict(a=A, b=B, d=d, epilogue=ops.EPI_BF16_RELU, bias=bias))
+            checks.append((d, ref.clamp_min(0), 1e-2))
+        else:
+            resid = torch.randn(m, n, device=cuda, generator=g)
+            d = torch.empty(m, n, device=cuda)
+            probs.append(dict(a=A, b=B, d=d, epilogue=ops.EPI_F32_RESID, bias=bias, resid=resid))
+            checks.append((d, ref + resid, 2e-3))
+    ops.gemm_grouped(probs)
+    for d, ref, tol in checks:
+        assert rel_err(d, ref) < tol
+
+
+def test_gemm_grouped_rejects_mixed_majors(cuda):
+    from paper_2403_07544_b200 import ops
+    a = torch.zeros(128, 64, device=cuda, dtype=torch.bfloat16)
+    d = torch.zeros(128, 128, device=cuda)
+    with pytest.raises(RuntimeError, match="majorness"):
+        ops.gemm_grouped([dict(a=a, b=a, d=d, epilogue=ops.EPI_F32),
+                          dict(a=a.t().contiguous(), b=a, d=d, a_kmajor=False, epilogue=ops.EPI_F32)])
+
+
 def test_layernorm(cuda):
     from paper_2403_07544_b200 import ops
     for cols in (512, 1024):

@@ -31,15 +31,30 @@ for name, m, n, k, ak, bk, epi in cases:
     bf = epi in (ops.EPI_BF16, ops.EPI_BF16_RELU, ops.EPI_BF16_DRELU)
     D = torch.zeros(m, n, device=dev, dtype=torch.bfloat16 if bf else torch.float32)
     bias = torch.zeros(n, device=dev) if epi in (ops.EPI_BF16, ops.EPI_BF16_RELU) else None
-    for _ in range(3):
-        ops.gemm(A, B, D, a_kmajor=ak, b_kmajor=bk, epilogue=epi, bias=bias)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n_it = 50
-    e0.record()
-    for _ in range(n_it):
-        ops.gemm(A, B, D, a_kmajor=ak, b_kmajor=bk, epilogue=epi, bias=bias)
-    e1.record()
-    torch.cuda.synchronize()
-    us = e0.elapsed_time(e1) * 1e3 / n_it
-    print(f"{name:10s} {m:6d}x{n:6d}x{k:6d}  {us:8.2f} us  {2*m*n*k/us/1e6:8.1f} TFLOP/s")
+    run = lambda: ops.gemm(A, B, D, a_kmajor=ak, b_kmajor=bk, epilogue=epi, bias=bias)
+    At = A if ak else A.t()
+    Bt = B.t() if bk else B
+    Dc = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
+    runc = lambda: torch.mm(At, Bt, out=Dc)
+    res = []
+    for fn in (run, runc):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        n_it = 20  # back-to-back launches captured in a CUDA graph: device time, not host issue
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(n_it):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        res.append(e0.elapsed_time(e1) * 1e3 / (5 * n_it))
+    us, uc = res
+    print(f"{name:10s} {m:6d}x{n:6d}x{k:6d}  {us:8.2f} us  {2*m*n*k/us/1e6:8.1f} TFLOP/s"
+          f"   cublas {uc:8.2f} us  {2*m*n*k/uc/1e6:8.1f} TFLOP/s")
