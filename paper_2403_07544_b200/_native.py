@@ -14,6 +14,9 @@ from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_int64
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "csrc", "libmmb200.so")
+if os.environ.get("MM_LIB_VARIANT"):  # diagnostics: a tuning build from tools/build_variant.py
+    LIB_PATH = os.path.join(os.path.dirname(_HERE), "build", "variants", os.environ["MM_LIB_VARIANT"],
+                            "libmmb200.so")
 
 #: must match MMB200_ABI_VERSION in include/mmb200.h
 ABI_VERSION = 11

@@ -41,25 +41,46 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle row of bf16
 constexpr int UMMA_K = 16;
 constexpr int kEpiWarp0 = 2;
-constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, each half the columns
+#ifndef MM_GEMM_EPI_WARPS
+#define MM_GEMM_EPI_WARPS 8
+#endif
+#ifndef MM_GEMM_EPI_BUFS
+#define MM_GEMM_EPI_BUFS 2
+#endif
+#ifndef MM_GEMM_MAX_STAGES
+#define MM_GEMM_MAX_STAGES 8
+#endif
+// epilogue warps: 4 per "column slice" (one per TMEM lane quarter); with 8,
+// two slices each take half of the tile's columns
+constexpr int kEpiWarps = MM_GEMM_EPI_WARPS;
+constexpr int kSlices = kEpiWarps / 4;
+constexpr int kEpiBufs = MM_GEMM_EPI_BUFS;  // staging boxes per epilogue warp
 constexpr int kBiasWarp = kEpiWarp0 + kEpiWarps;  // second consumer of every smem stage
 constexpr int kThreads = (kBiasWarp + 1) * 32;
 constexpr int kMaxProbs = 24;  // problems per grouped launch (kernel parameter space)
 
 constexpr int kEpiBufBytes = 32 * 128;                    // 32 rows x 128 B box
-constexpr int kEpiSmem = kEpiWarps * 2 * kEpiBufBytes;    // double-buffered per warp
+constexpr int kEpiSmem = kEpiWarps * kEpiBufs * kEpiBufBytes;
 constexpr int kSmemLimit = 232448;
 
-template <int BN>
+// CG = CTAs per MMA: 1, or 2 for a CTA pair (cta_group::2) computing a
+// (2*BM) x BN tile -- each CTA holds its BM rows of A and BN/2 rows of B, so
+// per-SM shared-memory traffic per MMA drops by a quarter (BN=128) to a half.
+template <int BN, int CG>
 struct Cfg {
+    static constexpr int kBRows = BN / CG;             // B rows (N) staged by one CTA
     static constexpr int kABytes = BM * BK * 2;
-    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kBBytes = kBRows * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStagesFit = (kSmemLimit - kEpiSmem - 1024 - 256) / kStageBytes;
-    static constexpr int kStages = kStagesFit > 6 ? 6 : kStagesFit;
+    static constexpr int kTxBytes = kStageBytes * CG;  // bytes counted on the MMA CTA's barrier
+    static constexpr int kBarBytes = 512;
+    static constexpr int kStagesFit = (kSmemLimit - kEpiSmem - 1024 - kBarBytes) / kStageBytes;
+    static constexpr int kStages = kStagesFit > MM_GEMM_MAX_STAGES ? MM_GEMM_MAX_STAGES : kStagesFit;
     static constexpr int kTmemCols = BN == 128 ? 256 : 512;  // 2 accumulators, power of 2
-    static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 + 256;
+    static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 + kBarBytes;
     static_assert(kSmem <= kSmemLimit, "smem budget");
+    static_assert(CG == 1 || kBRows % 64 == 0, "pair tiles need 64-aligned B halves");
+    static_assert((3 * kStages + 4) * 8 + 4 <= kBarBytes, "barrier area");
 };
 
 // One GEMM problem of a launch: its three tensor maps (A, B, D) and its slice
@@ -88,6 +109,8 @@ struct Group {
     int n_probs;
     int units;
     int b_prefetch;
+    int any_dbias;  // some problem fuses bias-gradient column sums (bias warp active)
+    int debug;      // diagnostics (MM_GEMM_DEBUG): bit 0 skip MMAs, bit 1 skip epilogue stores, bit 2 skip loads
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -98,6 +121,20 @@ __device__ __forceinline__ unsigned long long gtime() {
 // trace slots per CTA: 0 entry, 1 setup done, 2 first stage full (MMA warp),
 // 3 last commit issued, 4 first tfull seen (epilogue warp 2), 5 epilogue
 // done (warp 2), 6 stores drained (warp 2), 7 exit
+// per-k-block pipeline stamps (clock64) of CTAs 0 and 1 after the 8 x 148 phase slots:
+// [cta*256 + i] producer passed the empty wait for its i-th stage fill,
+// [cta*256 + 128 + i] MMA warp passed the full wait for its i-th stage
+#ifdef MM_GEMM_KB_TRACE
+#define MM_KB_TRACE(off, i)                                                              \
+    do {                                                                                 \
+        if (g.trace && blockIdx.x < 2 && (i) < 128)                                      \
+            g.trace[8 * 148 + blockIdx.x * 256 + (off) + (i)] = clock64();               \
+    } while (0)
+#else
+#define MM_KB_TRACE(off, i) \
+    do {                    \
+    } while (0)
+#endif
 #define MM_TRACE(slot)                                                                   \
     do {                                                                                 \
         if (g.trace) g.trace[blockIdx.x * 8 + (slot)] = gtime();                         \
@@ -221,10 +258,10 @@ __device__ __forceinline__ Unit decode(const Group<NP>& g, int u) {
     return w;
 }
 
-template <int BN, int A_MN, int B_MN, int NP>
+template <int BN, int A_MN, int B_MN, int NP, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ Group<NP> g) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, CG>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -233,12 +270,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem_epi = smem + C::kStages * C::kStageBytes;  // 1024-aligned
     uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_epi + kEpiSmem);
     uint64_t* empty_bar = full_bar + C::kStages;
-    uint64_t* tfull_bar = empty_bar + C::kStages;
+    uint64_t* bias_bar = empty_bar + C::kStages;  // pair: "stage consumed by the MMA" for the bias warp
+    uint64_t* tfull_bar = bias_bar + C::kStages;
     uint64_t* tempty_bar = tfull_bar + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
-    const int warp = threadIdx.x >> 5;
+    // warp index through a shuffle: ptxas then knows it is warp-uniform, so
+    // the role branches below are uniform and their loop state (stage, phase,
+    // descriptors) lives in uniform registers next to the tcgen05 operands
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
+    // pair rank: 0 = leader (issues the MMAs, owns the stage-full barriers)
+    const uint32_t rank = CG == 2 ? tc::cluster_ctarank() : 0u;
+    const bool dbias_any = g.any_dbias != 0;
     if (threadIdx.x == 0) MM_TRACE(0);
 
     if (warp == 0 && lane == 0) {
@@ -251,20 +295,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < C::kStages; ++s) {
             tc::mbar_init(&full_bar[s], 1);
-            tc::mbar_init(&empty_bar[s], 2);  // MMA commit + bias warp
+            tc::mbar_init(&empty_bar[s], dbias_any ? 2 : 1);  // MMA commit (+ bias warp)
+            tc::mbar_init(&bias_bar[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             tc::mbar_init(&tfull_bar[a], 1);
-            tc::mbar_init(&tempty_bar[a], kEpiWarps * 32);
+            tc::mbar_init(&tempty_bar[a], CG * kEpiWarps);  // one arrive per epilogue warp of the pair
         }
         tc::fence_barrier_init();
     }
-    if (warp == 1) tc::tmem_alloc(tmem_slot, C::kTmemCols);
+    if (warp == 1) {
+        if constexpr (CG == 2) tc::tmem_alloc_pair(tmem_slot, C::kTmemCols);
+        else tc::tmem_alloc(tmem_slot, C::kTmemCols);
+    }
     tc::tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) tc::cluster_sync();  // peer barriers initialised before any remote signal
+    else __syncthreads();
     tc::tc_fence_after();
-    const int cid = blockIdx.x, ncta = gridDim.x;
+    const int cid = blockIdx.x / CG, ncta = gridDim.x / CG;  // units are dealt per pair
     const uint32_t tmem_base = *tmem_slot;
+    if (tmem_base != 0) __trap();  // the MMA issuer addresses TMEM by column offset
     if (threadIdx.x == 0) MM_TRACE(1);
     // griddepcontrol.wait: roles that read or write global memory wait for the
     // previous kernel; everything above (barrier init, TMEM allocation,
@@ -273,35 +323,43 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
+            // stage completion is counted on the leader's full barrier
+            const uint32_t full_leader = CG == 2 ? tc::mapa_u32(tc::smem_u32(full_bar), 0) : 0u;
+            auto load = [&](uint8_t* dst, const CUtensorMap* map, int stage, int c0, int c1) {
+                if constexpr (CG == 2) tc::tma_load_2d_pair(dst, map, full_leader + stage * 8, c0, c1);
+                else tc::tma_load_2d(dst, map, &full_bar[stage], c0, c1);
+            };
             auto load_a = [&](const Prob& P, int stage, int m0, int k0) {
                 uint8_t* sa = smem_a + stage * C::kABytes;
                 if (A_MN) {
 #pragma unroll
-                    for (int c = 0; c < BM / 64; ++c)
-                        tc::tma_load_2d(sa + c * 64 * BK * 2, &P.ta, &full_bar[stage], m0 + c * 64, k0);
+                    for (int c = 0; c < BM / 64; ++c) load(sa + c * 64 * BK * 2, &P.ta, stage, m0 + c * 64, k0);
                 } else {
-                    tc::tma_load_2d(sa, &P.ta, &full_bar[stage], k0, m0);
+                    load(sa, &P.ta, stage, k0, m0);
                 }
             };
             auto load_b = [&](const Prob& P, int stage, int n0, int k0) {
                 uint8_t* sb = smem_b + stage * C::kBBytes;
                 if (B_MN) {
 #pragma unroll
-                    for (int c = 0; c < BN / 64; ++c)
-                        tc::tma_load_2d(sb + c * 64 * BK * 2, &P.tb, &full_bar[stage], n0 + c * 64, k0);
+                    for (int c = 0; c < C::kBRows / 64; ++c)
+                        load(sb + c * 64 * BK * 2, &P.tb, stage, n0 + c * 64, k0);
                 } else {
-                    tc::tma_load_2d(sb, &P.tb, &full_bar[stage], k0, n0);
+                    load(sb, &P.tb, stage, k0, n0);
                 }
+            };
+            auto expect = [&](int stage) {
+                if (rank == 0) tc::mbar_expect_tx(&full_bar[stage], C::kTxBytes);
             };
             // B stages of the first unit that do not depend on the previous kernel
             int pre = 0;
-            if (g.b_prefetch && cid < g.units) {
+            if (g.b_prefetch && cid < g.units && !(g.debug & 4)) {
                 const Unit w = decode(g, cid);
                 const Prob& P = g.prob[w.pi];
                 pre = min(C::kStages, w.kb1 - w.kb0);
                 for (int i = 0; i < pre; ++i) {
-                    tc::mbar_expect_tx(&full_bar[i], C::kStageBytes);
-                    load_b(P, i, w.tn * BN, (w.kb0 + i) * BK);
+                    expect(i);
+                    load_b(P, i, w.tn * BN + rank * C::kBRows, (w.kb0 + i) * BK);
                 }
             }
             pdl_wait();
@@ -311,15 +369,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int u = cid; u < g.units; u += ncta) {
                 const Unit w = decode(g, u);
                 const Prob& P = g.prob[w.pi];
-                const int m0 = w.tm * BM, n0 = w.tn * BN;
+                const int m0 = w.tm * (BM * CG) + rank * BM, n0 = w.tn * BN + rank * C::kBRows;
                 for (int kb = w.kb0; kb < w.kb1; ++kb, ++issued) {
                     if (issued < pre) {  // expect_tx and B already issued
                         load_a(P, stage, m0, kb * BK);
                     } else {
                         tc::mbar_wait(&empty_bar[stage], phase ^ 1);
-                        tc::mbar_expect_tx(&full_bar[stage], C::kStageBytes);
-                        load_a(P, stage, m0, kb * BK);
-                        load_b(P, stage, n0, kb * BK);
+                        MM_KB_TRACE(0, issued);
+                        if (g.debug & 4) {  // diagnostics: no loads, MMAs on stale smem
+                            if (rank == 0) tc::mbar_arrive(&full_bar[stage]);
+                        } else {
+                            expect(stage);
+                            load_a(P, stage, m0, kb * BK);
+                            load_b(P, stage, n0, kb * BK);
+                        }
                     }
                     if (++stage == C::kStages) { stage = 0; phase ^= 1; }
                 }
@@ -327,43 +390,55 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        constexpr uint32_t idesc = tc::idesc_bf16_f32(BM, BN, A_MN, B_MN);
+        // (pair: the leader issues for both CTAs; the peer's warp 1 only owns
+        // its half of the TMEM allocation).  The warp stays converged and one
+        // lane is elected inside each MMA (see tc::mma_bf16_elect); operand
+        // descriptors are the stage-0 descriptor plus the stage/K offset in
+        // the 14-bit start-address field (smem addresses < 256 KB: no carry).
+        // The accumulator address is the column offset alone: TMEM is
+        // allocated at column 0 because one GEMM CTA fills an SM's shared
+        // memory (checked at allocation).
+        constexpr uint32_t idesc = tc::idesc_bf16_f32(BM * CG, BN, A_MN, B_MN);
+        const uint64_t a_desc0 = A_MN ? tc::umma_desc_sw128(tc::smem_u32(smem_a), 64 * BK * 2, 1024)
+                                      : tc::umma_desc_sw128(tc::smem_u32(smem_a), 16, 1024);
+        const uint64_t b_desc0 = B_MN ? tc::umma_desc_sw128(tc::smem_u32(smem_b), 64 * BK * 2, 1024)
+                                      : tc::umma_desc_sw128(tc::smem_u32(smem_b), 16, 1024);
+        // per-K-step advance (16-byte units): K-major 32 B inside the swizzled
+        // row; MN-major 16 K-rows = 2 x 1024 B
+        constexpr int a_kstep = A_MN ? 2048 / 16 : 32 / 16;
+        constexpr int b_kstep = B_MN ? 2048 / 16 : 32 / 16;
+        const uint32_t a_lo0 = static_cast<uint32_t>(a_desc0), a_hi = static_cast<uint32_t>(a_desc0 >> 32);
+        const uint32_t b_lo0 = static_cast<uint32_t>(b_desc0), b_hi = static_cast<uint32_t>(b_desc0 >> 32);
         int stage = 0;
         uint32_t phase = 0;
         int local = 0;
-        for (int u = cid; u < g.units; u += ncta, ++local) {
+        int consumed = 0;
+        for (int u = cid; u < g.units && rank == 0; u += ncta, ++local) {
             const Unit w = decode(g, u);
             const int kb0 = w.kb0, kb1 = w.kb1;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
-            tc::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+            if constexpr (CG == 2) tc::mbar_wait_cluster(&tempty_bar[acc], acc_phase ^ 1);
+            else tc::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
             tc::tc_fence_after();
-            const uint32_t d_tmem = tmem_base + acc * BN;
-            for (int kb = kb0; kb < kb1; ++kb) {
+            const uint32_t d_tmem = static_cast<uint32_t>(acc * BN);
+            for (int kb = kb0; kb < kb1; ++kb, ++consumed) {
                 tc::mbar_wait(&full_bar[stage], phase);
                 tc::tc_fence_after();
-                if (lane == 0 && local == 0 && kb == kb0) MM_TRACE(2);
-                if (lane == 0) {
-                    const uint32_t sa = tc::smem_u32(smem_a + stage * C::kABytes);
-                    const uint32_t sb = tc::smem_u32(smem_b + stage * C::kBBytes);
-#pragma unroll
-                    for (int k = 0; k < BK / UMMA_K; ++k) {
-                        // K-major: advance 32 B inside the swizzled row;
-                        // MN-major: advance 16 K-rows = 2 x 1024 B
-                        const uint64_t ad =
-                            A_MN ? tc::umma_desc_sw128(sa + k * 2048, 64 * BK * 2, 1024)
-                                 : tc::umma_desc_sw128(sa + k * 32, 16, 1024);
-                        const uint64_t bd =
-                            B_MN ? tc::umma_desc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
-                                 : tc::umma_desc_sw128(sb + k * 32, 16, 1024);
-                        tc::mma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-                    }
-                    tc::mma_commit(&empty_bar[stage]);
+                MM_KB_TRACE(128, consumed);
+                const uint32_t a_lo = a_lo0 + static_cast<uint32_t>(stage * (C::kABytes / 16));
+                const uint32_t b_lo = b_lo0 + static_cast<uint32_t>(stage * (C::kBBytes / 16));
+                if (!(g.debug & 1)) {
+                    tc::mma_kblock_commit<CG, a_kstep, b_kstep>(d_tmem, a_lo, a_hi, b_lo, b_hi, idesc,
+                                                                kb > kb0 ? 1u : 0u, &empty_bar[stage]);
+                } else {
+                    tc::mma_commit_elect<CG>(&empty_bar[stage]);
                 }
-                __syncwarp();
+                MM_KB_TRACE(512, consumed);  // MMAs + commit issued
+                if (CG == 2 && dbias_any) tc::mma_commit_elect<CG>(&bias_bar[stage]);
                 if (++stage == C::kStages) { stage = 0; phase ^= 1; }
             }
-            if (lane == 0) tc::mma_commit(&tfull_bar[acc]);
+            tc::mma_commit_elect<CG>(&tfull_bar[acc]);
             if (lane == 0) MM_TRACE(3);
             __syncwarp();
         }
@@ -375,7 +450,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // kb % tiles_n == tn, so every k-block is summed exactly once.  Lane owns M = 4*lane..4*lane+3
         // (box lane/16, 16B chunk (lane%16)/2, half lane%2; rows are K,
         // 128B-swizzled).  Every stage is released here too (empty count 2).
+        // A pair's peer cannot wait on the leader's full barrier, so there the
+        // MMA's commit to bias_bar says the stage is resident (and still held:
+        // the empty barrier also needs this warp's arrival).
+        if (!dbias_any) goto done;
         pdl_wait();
+        {
         int stage = 0;
         uint32_t phase = 0;
         for (int u = cid; u < g.units; u += ncta) {
@@ -387,7 +467,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool bias_sum = A_MN && dbias != nullptr;
             float bsum[4] = {0.f, 0.f, 0.f, 0.f};
             for (int kb = kb0; kb < kb1; ++kb) {
-                tc::mbar_wait(&full_bar[stage], phase);
+                if constexpr (CG == 2) tc::mbar_wait(&bias_bar[stage], phase);
+                else tc::mbar_wait(&full_bar[stage], phase);
                 if (bias_sum && kb % tiles_n == tn) {
                     const uint8_t* box = smem_a + stage * C::kABytes + (lane >> 4) * 64 * BK * 2;
                     const int chunk = (lane & 15) >> 1, sub = (lane & 1) * 8;
@@ -406,19 +487,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (++stage == C::kStages) { stage = 0; phase ^= 1; }
             }
             if (bias_sum) {
-                const int64_t m = int64_t(w.tm) * BM + 4 * lane;
+                const int64_t m = int64_t(w.tm) * (BM * CG) + rank * BM + 4 * lane;
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
                     if (m + i < P.m) atomicAdd(dbias + m + i, bsum[i]);
             }
         }
+        }
+    done:;
     } else {
         // ------------------------------------------------------------ epilogue
         pdl_wait();
         const int lane_grp = warp & 3;                   // TMEM lanes this warp may access
-        const int half = (warp - kEpiWarp0) >> 2;        // which half of the tile's columns
-        constexpr int kChunks = BN / 32 / 2;             // 32-column chunks per warp
-        uint8_t* bufs = smem_epi + (warp - kEpiWarp0) * 2 * kEpiBufBytes;
+        const int half = (warp - kEpiWarp0) >> 2;        // which column slice of the tile
+        constexpr int kChunks = BN / 32 / kSlices;       // 32-column chunks per warp
+        uint8_t* bufs = smem_epi + (warp - kEpiWarp0) * kEpiBufs * kEpiBufBytes;
         int nbuf = 0;
         int local = 0;
         for (int u = cid; u < g.units; u += ncta, ++local) {
@@ -431,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int tm = w.tm, tn = w.tn;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
-            const int cbase = tn * BN + half * (BN / 2);
+            const int cbase = tn * BN + half * (BN / kSlices);
             // bias for this warp's columns, fetched before waiting on the MMAs
             float bv[kChunks];
 #pragma unroll
@@ -442,10 +525,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_wait(&tfull_bar[acc], acc_phase);
             tc::tc_fence_after();
             if (warp == kEpiWarp0 && lane == 0 && local == 0) MM_TRACE(4);
-            const int row0 = tm * BM + lane_grp * 32;  // this warp's first row
+            const int row0 = tm * (BM * CG) + rank * BM + lane_grp * 32;  // this warp's first row
             const int64_t row = int64_t(row0) + lane;
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) + acc * BN +
-                                   half * (BN / 2);
+                                   half * (BN / kSlices);
 #pragma unroll
             for (int c = 0; c < kChunks; ++c) {
                 const int col0 = cbase + c * 32;
@@ -458,31 +541,39 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
                     epilogue_math(P, row, col0, f, bv[c]);
                     uint8_t* buf = bufs + nbuf * kEpiBufBytes;
-                    if (lane == 0) tc::bulk_wait_read<1>();  // the store that last read `buf` is done
+                    if (lane == 0) tc::bulk_wait_read<kEpiBufs - 1>();  // the store that last read `buf` is done
                     __syncwarp();
                     stage_row(buf, lane, f, out_bf16);
                     tc::fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) {
+                    if (lane == 0 && !(g.debug & 2)) {
                         if (reduce) tc::tma_reduce_add_2d(&P.td, buf, col0, row0);
                         else tc::tma_store_2d(&P.td, buf, col0, row0);
                         tc::bulk_commit();
                     }
-                    nbuf ^= 1;
+                    if (++nbuf == kEpiBufs) nbuf = 0;
                 }
             }
+            // accumulator drained: one arrive per warp on the MMA CTA's barrier
             tc::tc_fence_before();
-            tc::mbar_arrive(&tempty_bar[acc]);
+            __syncwarp();
+            if (lane == 0) {
+                if constexpr (CG == 2) tc::mbar_arrive_cluster(&tempty_bar[acc], 0);
+                else tc::mbar_arrive(&tempty_bar[acc]);
+            }
         }
         if (warp == kEpiWarp0 && lane == 0) MM_TRACE(5);
         if (lane == 0) tc::bulk_wait_all();
         if (warp == kEpiWarp0 && lane == 0) MM_TRACE(6);
     }
     pdl_trigger();
-    __syncthreads();
+    tc::tc_fence_before();
+    if constexpr (CG == 2) tc::cluster_sync();  // both CTAs done with the pair's TMEM / barriers
+    else __syncthreads();
     if (warp == 1) {
         tc::tc_fence_after();
-        tc::tmem_dealloc(tmem_base, C::kTmemCols);
+        if constexpr (CG == 2) tc::tmem_dealloc_pair(tmem_base, C::kTmemCols);
+        else tc::tmem_dealloc(tmem_base, C::kTmemCols);
     }
     if (threadIdx.x == 0) MM_TRACE(7);
 }
@@ -530,28 +621,29 @@ int make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, i
     return 0;
 }
 
-template <int BN, int A_MN, int B_MN, int NP>
+template <int BN, int A_MN, int B_MN, int NP, int CG>
 int launch(const Group<NP>& g, cudaStream_t s) {
-    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, NP>;
+    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, NP, CG>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg<BN>::kSmem));
+                                         Cfg<BN, CG>::kSmem));
         attr_set = true;
     }
-    // persistent: one CTA per SM
-    const int ctas = std::min(g.units, mm::num_sms());
-    MM_CUDA_TRY(mm::launch_pdl(kern, dim3(ctas), dim3(kThreads), Cfg<BN>::kSmem, s, g));
+    // persistent: one CTA (pair) per SM (pair of SMs)
+    const int ctas = std::min(g.units, mm::num_sms() / CG) * CG;
+    MM_CUDA_TRY(mm::launch_pdl_cluster(kern, dim3(ctas), dim3(kThreads), Cfg<BN, CG>::kSmem, s,
+                                       static_cast<unsigned>(CG), g));
     MM_LAUNCH_CHECK("gemm_tcgen05_kernel");
     return 0;
 }
 
-template <int BN, int NP>
+template <int BN, int NP, int CG>
 int dispatch(int a_mn, int b_mn, const Group<NP>& g, cudaStream_t s) {
-    if (!a_mn && !b_mn) return launch<BN, 0, 0, NP>(g, s);
-    if (!a_mn && b_mn) return launch<BN, 0, 1, NP>(g, s);
-    if (a_mn && !b_mn) return launch<BN, 1, 0, NP>(g, s);
-    return launch<BN, 1, 1, NP>(g, s);
+    if (!a_mn && !b_mn) return launch<BN, 0, 0, NP, CG>(g, s);
+    if (!a_mn && b_mn) return launch<BN, 0, 1, NP, CG>(g, s);
+    if (a_mn && !b_mn) return launch<BN, 1, 0, NP, CG>(g, s);
+    return launch<BN, 1, 1, NP, CG>(g, s);
 }
 
 unsigned long long* g_trace_buf = nullptr;  // set by mm_gemm_trace (diagnostics)
@@ -589,36 +681,68 @@ int check_args(const mm_gemm_args* a) {
     return 0;
 }
 
-// Tile width for a launch: minimise waves x (tile width + per-tile overhead
-// ~ 64 columns) over the launch's total tile count.
-int choose_bn(const mm_gemm_args* const* probs, int n, int sms) {
-    int bn = 128;
-    double best = 1e300;
-    for (int cand : {256, 192, 128}) {
-        bool fits = true;
-        int64_t t = 0;
-        for (int i = 0; i < n; ++i) {
-            if (cand > 128 && probs[i]->n <= cand - 64) fits = false;
-            t += ((probs[i]->m + BM - 1) / BM) * ((probs[i]->n + cand - 1) / cand);
+// Tile shape for a launch: (BN, CG) minimising a per-SM time model fitted to
+// tools/gemm_micro.py sweeps on the B200 (config-3 shapes, N = 512..32000):
+//   t = c0 + waves * kb * x
+// c0 = fixed cost of a launch (prologue, first-load latency, last tile's
+// epilogue and drain) and x = time per 64-deep k-block of one unit, which is
+// MMA-issue bound (~80 cycles per tcgen05.mma) for 128-wide tiles and
+// tensor-pipe bound for 256-wide ones; wide tiles then cost little more per
+// k-block but quantise into fewer, longer waves.  A pair (CG = 2) computes a
+// 256-row tile on two SMs for the same per-k-block time as a single CTA's
+// 128-row tile, at a larger fixed cost.
+struct TileChoice {
+    int bn, cg;
+};
+struct TileCost {
+    double c0_us, x_us;
+};
+TileCost tile_cost(int bn, int cg) {
+    if (cg == 2) return bn == 256 ? TileCost{6.0, 0.303} : TileCost{5.7, 0.282};
+    return bn == 256 ? TileCost{5.3, 0.343} : bn == 192 ? TileCost{4.7, 0.33} : TileCost{4.1, 0.308};
+}
+TileChoice choose_tile(const mm_gemm_args* const* probs, int n, int sms) {
+    TileChoice best{128, 1};
+    double best_cost = 1e300;
+    for (int cg : {1, 2}) {
+        for (int cand : {128, 192, 256}) {
+            if (cg == 2 && cand == 192) continue;
+            bool fits = true;
+            int64_t units = 0;
+            double kb_sum = 0;
+            for (int i = 0; i < n; ++i) {
+                if (cand > 128 && probs[i]->n <= cand - 64) fits = false;
+                const int64_t t = ((probs[i]->m + BM * cg - 1) / (BM * cg)) * ((probs[i]->n + cand - 1) / cand);
+                units += t;
+                kb_sum += double(t) * double((probs[i]->k + BK - 1) / BK);
+            }
+            if (!fits) continue;
+            const int slots = sms / cg;
+            const double waves = double((units + slots - 1) / slots);
+            const TileCost tc = tile_cost(cand, cg);
+            const double cost = tc.c0_us + waves * (kb_sum / double(units)) * tc.x_us;
+            if (cost < best_cost - 1e-9) { best_cost = cost; best = {cand, cg}; }
         }
-        if (!fits) continue;
-        const double cost = double((t + sms - 1) / sms) * (cand + 64);
-        if (cost < best - 1e-9) { best = cost; bn = cand; }
     }
     if (const char* force = std::getenv("MM_GEMM_BN")) {  // diagnostics
         const int f = std::atoi(force);
-        if (f == 128 || f == 192 || f == 256) bn = f;
+        if (f == 128 || f == 192 || f == 256) best.bn = f;
     }
-    return bn;
+    if (const char* force = std::getenv("MM_GEMM_CG")) {  // diagnostics
+        const int f = std::atoi(force);
+        if (f == 1 || f == 2) best.cg = f;
+    }
+    if (best.cg == 2 && best.bn == 192) best.bn = 256;
+    return best;
 }
 
 // Fill one problem of a launch (tensor maps + tiling); splits K for fp32
 // accumulation when the launch has fewer tiles than two waves.
-int setup_prob(Prob& P, const mm_gemm_args* a, int bn, int splits_cap) {
+int setup_prob(Prob& P, const mm_gemm_args* a, int bn, int cg, int splits_cap) {
     const bool out_bf16 = out_bf16_epi(a->epilogue);
     const int a_mn = a->a_kmajor ? 0 : 1;
     const int b_mn = a->b_kmajor ? 0 : 1;
-    const int64_t tiles_m = (a->m + BM - 1) / BM;
+    const int64_t tiles_m = (a->m + BM * cg - 1) / (BM * cg);
     const int64_t tiles_n = (a->n + bn - 1) / bn;
     const int num_kb = static_cast<int>((a->k + BK - 1) / BK);
     int splits = a->epilogue == MM_EPI_F32_ACCUM ? std::max(1, std::min(splits_cap, num_kb / 2)) : 1;
@@ -631,7 +755,7 @@ int setup_prob(Prob& P, const mm_gemm_args* a, int bn, int splits_cap) {
               : make_map(&P.ta, a->a, a->k, a->m, a->lda, BM);
     if (st) return st;
     st = b_mn ? make_map(&P.tb, a->b, a->n, a->k, a->ldb, BK)
-              : make_map(&P.tb, a->b, a->k, a->n, a->ldb, bn);
+              : make_map(&P.tb, a->b, a->k, a->n, a->ldb, bn / cg);  // a pair CTA stages BN/2 rows
     if (st) return st;
     // D: 32 x 32 boxes, swizzle matching the staging layout
     st = make_map(&P.td, a->d, a->n, a->m, a->ldd, 32, 32, !out_bf16,
@@ -652,12 +776,13 @@ int setup_prob(Prob& P, const mm_gemm_args* a, int bn, int splits_cap) {
 
 // K-split for fp32-accumulating launches: double while the launch stays
 // within two waves
-int split_cap(const mm_gemm_args* const* probs, int n, int bn, int sms) {
+int split_cap(const mm_gemm_args* const* probs, int n, int bn, int cg, int sms) {
     int64_t tiles = 0;
     int min_kb = 1 << 30;
     bool all_accum = true;
+    sms /= cg;
     for (int i = 0; i < n; ++i) {
-        tiles += ((probs[i]->m + BM - 1) / BM) * ((probs[i]->n + bn - 1) / bn);
+        tiles += ((probs[i]->m + BM * cg - 1) / (BM * cg)) * ((probs[i]->n + bn - 1) / bn);
         min_kb = std::min<int>(min_kb, static_cast<int>((probs[i]->k + BK - 1) / BK));
         all_accum = all_accum && probs[i]->epilogue == MM_EPI_F32_ACCUM;
     }
@@ -670,8 +795,9 @@ int split_cap(const mm_gemm_args* const* probs, int n, int bn, int sms) {
 template <int NP>
 int run_group(const mm_gemm_args* const* probs, int n, cudaStream_t s) {
     const int sms = mm::num_sms();
-    const int bn = choose_bn(probs, n, sms);
-    const int cap = split_cap(probs, n, bn, sms);
+    const TileChoice tc = choose_tile(probs, n, sms);
+    const int bn = tc.bn, cg = tc.cg;
+    const int cap = split_cap(probs, n, bn, cg, sms);
     static Group<NP> g;  // host staging of the kernel parameter (large: tensor maps)
     std::memset(&g, 0, sizeof(g));
     int64_t units = 0;
@@ -679,22 +805,28 @@ int run_group(const mm_gemm_args* const* probs, int n, cudaStream_t s) {
     static const bool log = std::getenv("MM_GEMM_LOG") != nullptr;  // diagnostics
     for (int i = 0; i < n; ++i) {
         Prob& P = g.prob[i];
-        if (int st = setup_prob(P, probs[i], bn, cap)) return st;
+        if (int st = setup_prob(P, probs[i], bn, cg, cap)) return st;
         P.unit_begin = static_cast<int>(units);
         units += int64_t(P.tiles_m) * P.tiles_n * P.splits;
         MM_CHECK_ARG(units < (int64_t(1) << 31), "GEMM launch too large");
         flops += 2.0 * double(probs[i]->m) * double(probs[i]->n) * double(probs[i]->k);
         if (log)
-            std::fprintf(stderr, "mm_gemm m=%lld n=%lld k=%lld a_mn=%d b_mn=%d epi=%d bn=%d splits=%d units=%d group=%d/%d\n",
+            std::fprintf(stderr, "mm_gemm m=%lld n=%lld k=%lld a_mn=%d b_mn=%d epi=%d bn=%d cg=%d splits=%d units=%d group=%d/%d\n",
                          (long long)probs[i]->m, (long long)probs[i]->n, (long long)probs[i]->k,
                          probs[i]->a_kmajor ? 0 : 1, probs[i]->b_kmajor ? 0 : 1, probs[i]->epilogue,
-                         bn, P.splits, P.tiles_m * P.tiles_n * P.splits, i, n);
+                         bn, cg, P.splits, P.tiles_m * P.tiles_n * P.splits, i, n);
     }
     g.n_probs = n;
     g.units = static_cast<int>(units);
     g.trace = g_trace_buf;
     g.b_prefetch = 1;
-    for (int i = 0; i < n; ++i) g.b_prefetch &= probs[i]->b_prefetch ? 1 : 0;
+    g.any_dbias = 0;
+    static const int dbg = std::getenv("MM_GEMM_DEBUG") ? std::atoi(std::getenv("MM_GEMM_DEBUG")) : 0;
+    g.debug = dbg;
+    for (int i = 0; i < n; ++i) {
+        g.b_prefetch &= probs[i]->b_prefetch ? 1 : 0;
+        if (probs[i]->dbias) g.any_dbias = 1;
+    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (g_timing.on) {
         if (g_timing.ev.size() < 2 * (g_timing.used + 1)) {
@@ -713,9 +845,14 @@ int run_group(const mm_gemm_args* const* probs, int n, cudaStream_t s) {
     const int a_mn = probs[0]->a_kmajor ? 0 : 1;
     const int b_mn = probs[0]->b_kmajor ? 0 : 1;
     int rc;
-    if (bn == 256) rc = dispatch<256, NP>(a_mn, b_mn, g, s);
-    else if (bn == 192) rc = dispatch<192, NP>(a_mn, b_mn, g, s);
-    else rc = dispatch<128, NP>(a_mn, b_mn, g, s);
+    if (cg == 2) {
+        if (bn == 256) rc = dispatch<256, NP, 2>(a_mn, b_mn, g, s);
+        else rc = dispatch<128, NP, 2>(a_mn, b_mn, g, s);
+    } else {
+        if (bn == 256) rc = dispatch<256, NP, 1>(a_mn, b_mn, g, s);
+        else if (bn == 192) rc = dispatch<192, NP, 1>(a_mn, b_mn, g, s);
+        else rc = dispatch<128, NP, 1>(a_mn, b_mn, g, s);
+    }
     if (rc == 0 && e1) MM_CUDA_TRY(cudaEventRecord(e1, s));
     return rc;
 }

@@ -146,6 +146,90 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Warp-converged issue: the whole warp executes these, one elected lane issues.
+// Keeping the warp converged lets ptxas hold the operands in uniform
+// registers; issuing from inside `if (lane == 0)` makes it wrap every MMA in
+// an ELECT / R2UR.BROADCAST waterfall loop (~110 cycles per MMA, measured),
+// which at N <= 256 is slower than the tensor core itself.
+template <int CG>
+__device__ __forceinline__ void mma_bf16_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+    if constexpr (CG == 2) {
+        asm volatile(
+            "{\n\t.reg .pred e, p;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred e, p;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    }
+}
+// One 64-deep K block = 4 MMAs (K = 16 each) and the commit of the stage,
+// from one elected lane in a single asm block: the descriptors are the
+// stage's base descriptors (lo word: start address >> 4 | LBO, hi word:
+// SBO / version / swizzle) plus K-step offsets in the address field.
+template <int CG, int A_STEP, int B_STEP>
+__device__ __forceinline__ void mma_kblock_commit(uint32_t tmem_d, uint32_t a_lo, uint32_t a_hi,
+                                                  uint32_t b_lo, uint32_t b_hi, uint32_t idesc,
+                                                  uint32_t accumulate, uint64_t* bar) {
+#define MM_MMA_KBLOCK(CGS, COMMIT)                                                             \
+    asm volatile(                                                                              \
+        "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a, b;\n\t.reg .b32 x, y;\n\t"                  \
+        "elect.sync _|e, 0xffffffff;\n\t"                                                      \
+        "setp.ne.b32 p, %5, 0;\n\t"                                                            \
+        "setp.eq.u32 t, 0, 0;\n\t"                                                             \
+        "mov.b64 a, {%1, %2};\n\t"                                                             \
+        "mov.b64 b, {%3, %4};\n\t"                                                             \
+        "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], a, b, %6, p;\n\t"                   \
+        "add.u32 x, %1, %8;\n\tadd.u32 y, %3, %9;\n\t"                                         \
+        "mov.b64 a, {x, %2};\n\tmov.b64 b, {y, %4};\n\t"                                       \
+        "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], a, b, %6, t;\n\t"                   \
+        "add.u32 x, %1, %10;\n\tadd.u32 y, %3, %11;\n\t"                                       \
+        "mov.b64 a, {x, %2};\n\tmov.b64 b, {y, %4};\n\t"                                       \
+        "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], a, b, %6, t;\n\t"                   \
+        "add.u32 x, %1, %12;\n\tadd.u32 y, %3, %13;\n\t"                                       \
+        "mov.b64 a, {x, %2};\n\tmov.b64 b, {y, %4};\n\t"                                       \
+        "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], a, b, %6, t;\n\t"                   \
+        "@e " COMMIT "\n\t}" ::"r"(tmem_d),                                                    \
+        "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(accumulate), "r"(idesc),               \
+        "r"(smem_u32(bar)), "n"(A_STEP), "n"(B_STEP), "n"(2 * A_STEP), "n"(2 * B_STEP),        \
+        "n"(3 * A_STEP), "n"(3 * B_STEP), "h"(static_cast<uint16_t>(3))                        \
+        : "memory")
+    if constexpr (CG == 2)
+        MM_MMA_KBLOCK("2", "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%7], %14;");
+    else
+        MM_MMA_KBLOCK("1", "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];");
+#undef MM_MMA_KBLOCK
+}
+
+template <int CG>
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+    if constexpr (CG == 2) {
+        asm volatile(
+            "{\n\t.reg .pred e;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+            " [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+            "h"(static_cast<uint16_t>(3))
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred e;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+                smem_u32(bar))
+            : "memory");
+    }
+}
+
 // arrive on an mbarrier once all previously issued tcgen05.mma have completed
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile(
@@ -161,6 +245,67 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t cta_mask) 
         "h"(cta_mask)
         : "memory");
 }
+// ------------------------------------------------- CTA pair (cta_group::2)
+// A kernel uses one .cta_group for all of its tcgen05 alloc/mma/commit
+// instructions; these are the pair variants.  The pair's MMA is issued by the
+// leader (cluster rank 0); A rows are split between the two CTAs' smem (128
+// each), B columns too (N/2 each), and each CTA's TMEM holds its 128 rows.
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* slot, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(slot)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+                 : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// arrive on the mbarrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+// TMA load into this CTA's smem whose completion is counted on the pair
+// leader's mbarrier (bar_cluster: shared::cluster address from mapa)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map,
+                                                 uint32_t bar_cluster, int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+// wait with cluster-scope acquire (arrivals come from the peer CTA)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "LAB_WAITC:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONEC;\n\t"
+        "bra LAB_WAITC;\n\t"
+        "DONEC:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 // 32 lanes x 32 consecutive fp32 columns: thread t gets row (lane_base+t)
 __device__ __forceinline__ void tmem_ld_32x32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile(

@@ -15,13 +15,26 @@ def rel_err(got, ref):
     return (got - ref).abs().max().item() / max(ref.abs().max().item(), 1e-30)
 
 
+# every tile shape the launcher can pick: (CTAs per MMA, tile width); None =
+# the launcher's own choice
+TILES = [None, (1, 128), (1, 192), (1, 256), (2, 128), (2, 256)]
+
+
+@pytest.fixture(params=TILES, ids=lambda t: "auto" if t is None else f"cg{t[0]}bn{t[1]}")
+def tile(request, monkeypatch):
+    if request.param is not None:
+        monkeypatch.setenv("MM_GEMM_CG", str(request.param[0]))
+        monkeypatch.setenv("MM_GEMM_BN", str(request.param[1]))
+    return request.param
+
+
 GEMM_SHAPES = [(128, 128, 64), (256, 512, 512), (296, 200, 136), (4096, 1536, 512),
                (1000, 2048, 512), (512, 512, 4096), (264, 32000, 512)]
 
 
 @pytest.mark.parametrize("shape", GEMM_SHAPES)
 @pytest.mark.parametrize("a_k,b_k", [(True, True), (True, False), (False, True), (False, False)])
-def test_gemm_majors_f32(cuda, shape, a_k, b_k):
+def test_gemm_majors_f32(cuda, tile, shape, a_k, b_k):
     from paper_2403_07544_b200 import ops
     m, n, k = shape
     g = torch.Generator(device="cuda").manual_seed(m * 7 + n * 3 + k)
@@ -36,7 +49,7 @@ def test_gemm_majors_f32(cuda, shape, a_k, b_k):
 
 
 @pytest.mark.parametrize("shape", [(4096, 512, 512), (333, 1536, 512), (4096, 2048, 512)])
-def test_gemm_epilogues(cuda, shape):
+def test_gemm_epilogues(cuda, tile, shape):
     from paper_2403_07544_b200 import ops
     m, n, k = shape
     g = torch.Generator(device="cuda").manual_seed(1)
@@ -64,7 +77,7 @@ def test_gemm_epilogues(cuda, shape):
 
 @pytest.mark.parametrize("shape", [(512, 512, 4096), (1536, 512, 4111), (32000, 512, 2048),
                                    (2048, 512, 300)])
-def test_gemm_wgrad_accumulate(cuda, shape):
+def test_gemm_wgrad_accumulate(cuda, tile, shape):
     """dW += dY^T X with both operands MN-major (split-K, fp32 atomics)."""
     from paper_2403_07544_b200 import ops
     n_out, n_in, t = shape
@@ -80,7 +93,7 @@ def test_gemm_wgrad_accumulate(cuda, shape):
     assert rel_err(db, ref_b) < 1e-4  # fused bias gradient (column sums of dY)
 
 
-def test_gemm_grouped_wgrad(cuda):
+def test_gemm_grouped_wgrad(cuda, tile):
     """One grouped launch of a layer's worth of wgrads (mixed M, N, K; two
     problems accumulate into the same dW) == per-problem fp32 references."""
     from paper_2403_07544_b200 import ops
@@ -109,7 +122,7 @@ def test_gemm_grouped_wgrad(cuda):
         assert rel_err(db, ref_b) < 1e-4
 
 
-def test_gemm_grouped_forward_epilogues(cuda):
+def test_gemm_grouped_forward_epilogues(cuda, tile):
     """Grouped launch with a different epilogue per problem (K-major operands)."""
     from paper_2403_07544_b200 import ops
     g = torch.Generator(device="cuda").manual_seed(12)

@@ -21,8 +21,13 @@ cases = [  # name, m, n, k, a_k, b_k, epi
     ("wgrad ff2", 512, 2048, T, False, False, ops.EPI_F32_ACCUM),
     ("wgrad gen", 32000, 512, T, False, False, ops.EPI_F32_ACCUM),
     ("tiny", 128, 128, 64, True, True, ops.EPI_F32),
+    ("big", 8192, 8192, 8192, True, True, ops.EPI_BF16),
+    ("odd", 1000, 700, 520, True, True, ops.EPI_F32),
+    ("odd wg", 700, 520, 1000, False, False, ops.EPI_F32_ACCUM),
+    ("odd dg", 1000, 520, 700, True, False, ops.EPI_F32),
 ]
 sel = sys.argv[1:] or None
+VARIANTS = os.environ.get("GEMM_VARIANTS", "auto").split(",")
 for name, m, n, k, ak, bk, epi in cases:
     if sel and not any(s in name for s in sel):
         continue
@@ -36,8 +41,7 @@ for name, m, n, k, ak, bk, epi in cases:
     Bt = B.t() if bk else B
     Dc = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
     runc = lambda: torch.mm(At, Bt, out=Dc)
-    res = []
-    for fn in (run, runc):
+    def timeit(fn):
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
@@ -54,7 +58,28 @@ for name, m, n, k, ak, bk, epi in cases:
             g.replay()
         e1.record()
         torch.cuda.synchronize()
-        res.append(e0.elapsed_time(e1) * 1e3 / (5 * n_it))
-    us, uc = res
-    print(f"{name:10s} {m:6d}x{n:6d}x{k:6d}  {us:8.2f} us  {2*m*n*k/us/1e6:8.1f} TFLOP/s"
-          f"   cublas {uc:8.2f} us  {2*m*n*k/uc/1e6:8.1f} TFLOP/s")
+        return e0.elapsed_time(e1) * 1e3 / (5 * n_it)
+    uc = timeit(runc)
+    ref = (At.float() @ Bt.float())
+    line = f"{name:10s} {m:6d}x{n:6d}x{k:6d} cublas {uc:7.2f}us {2*m*n*k/uc/1e6:7.1f}TF |"
+    for var in VARIANTS:
+        for key in ("MM_GEMM_CG", "MM_GEMM_BN"):
+            os.environ.pop(key, None)
+        if var != "auto":
+            cg, bn = var.split(":")
+            os.environ["MM_GEMM_CG"], os.environ["MM_GEMM_BN"] = cg, bn
+        us = timeit(run)
+        D.zero_()
+        ops.gemm(A, B, D, a_kmajor=ak, b_kmajor=bk, epilogue=epi, bias=bias)
+        torch.cuda.synchronize()
+        out = D.float()
+        if epi == ops.EPI_BF16_RELU:
+            r = ref.clamp_min(0)
+        else:
+            r = ref
+        err = ((out - r).abs().max() / r.abs().max()).item() if epi != ops.EPI_BF16_DRELU else 0.0
+        ok = "ok" if err < 2e-2 else f"BAD{err:.1e}"
+        line += f" {var} {us:7.2f}us {2*m*n*k/us/1e6:7.1f}TF {ok} |"
+    for key in ("MM_GEMM_CG", "MM_GEMM_BN"):
+        os.environ.pop(key, None)
+    print(line, flush=True)

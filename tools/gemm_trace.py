@@ -9,7 +9,7 @@ buf = torch.zeros(8 * 148, dtype=torch.int64, device=dev)
 T = 4096
 cases = {"fwd_out": (T, 512, 512, True, True, ops.EPI_F32), "fwd_ff1": (T, 2048, 512, True, True, ops.EPI_BF16_RELU),
          "wgrad_ff1": (2048, 512, T, False, False, ops.EPI_F32_ACCUM), "dgrad_ff1": (T, 512, 2048, True, False, ops.EPI_F32),
-         "tiny": (128, 128, 64, True, True, ops.EPI_F32)}
+         "tiny": (128, 128, 64, True, True, ops.EPI_F32), "fwd_ff2": (T, 512, 2048, True, True, ops.EPI_F32)}
 for name, (m, n, k, ak, bk, epi) in cases.items():
     A = torch.randn(m, k, device=dev).bfloat16() if ak else torch.randn(k, m, device=dev).bfloat16()
     B = torch.randn(n, k, device=dev).bfloat16() if bk else torch.randn(k, n, device=dev).bfloat16()
