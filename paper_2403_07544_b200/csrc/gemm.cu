@@ -110,8 +110,12 @@ struct Group {
     int units;
     int b_prefetch;
     int any_dbias;  // some problem fuses bias-gradient column sums (bias warp active)
-    int debug;      // diagnostics (MM_GEMM_DEBUG): bit 0 skip MMAs, bit 1 skip epilogue stores, bit 2 skip loads
 };
+// diagnostics build (tools/build_variant.py -DMM_GEMM_DEBUG=bits): bit 0 skip
+// MMAs, bit 1 skip epilogue stores, bit 2 skip loads
+#ifndef MM_GEMM_DEBUG
+#define MM_GEMM_DEBUG 0
+#endif
 
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -353,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             };
             // B stages of the first unit that do not depend on the previous kernel
             int pre = 0;
-            if (g.b_prefetch && cid < g.units && !(g.debug & 4)) {
+            if (g.b_prefetch && cid < g.units && !(MM_GEMM_DEBUG & 4)) {
                 const Unit w = decode(g, cid);
                 const Prob& P = g.prob[w.pi];
                 pre = min(C::kStages, w.kb1 - w.kb0);
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     } else {
                         tc::mbar_wait(&empty_bar[stage], phase ^ 1);
                         MM_KB_TRACE(0, issued);
-                        if (g.debug & 4) {  // diagnostics: no loads, MMAs on stale smem
+                        if (MM_GEMM_DEBUG & 4) {  // diagnostics: no loads, MMAs on stale smem
                             if (rank == 0) tc::mbar_arrive(&full_bar[stage]);
                         } else {
                             expect(stage);
@@ -428,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 MM_KB_TRACE(128, consumed);
                 const uint32_t a_lo = a_lo0 + static_cast<uint32_t>(stage * (C::kABytes / 16));
                 const uint32_t b_lo = b_lo0 + static_cast<uint32_t>(stage * (C::kBBytes / 16));
-                if (!(g.debug & 1)) {
+                if (!(MM_GEMM_DEBUG & 1)) {
                     tc::mma_kblock_commit<CG, a_kstep, b_kstep>(d_tmem, a_lo, a_hi, b_lo, b_hi, idesc,
                                                                 kb > kb0 ? 1u : 0u, &empty_bar[stage]);
                 } else {
@@ -546,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     stage_row(buf, lane, f, out_bf16);
                     tc::fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0 && !(g.debug & 2)) {
+                    if (lane == 0 && !(MM_GEMM_DEBUG & 2)) {
                         if (reduce) tc::tma_reduce_add_2d(&P.td, buf, col0, row0);
                         else tc::tma_store_2d(&P.td, buf, col0, row0);
                         tc::bulk_commit();
@@ -698,29 +702,42 @@ struct TileCost {
     double c0_us, x_us;
 };
 TileCost tile_cost(int bn, int cg) {
-    if (cg == 2) return bn == 256 ? TileCost{6.0, 0.303} : TileCost{5.7, 0.282};
-    return bn == 256 ? TileCost{5.3, 0.343} : bn == 192 ? TileCost{4.7, 0.33} : TileCost{4.1, 0.308};
+    if (cg == 2) return bn == 256 ? TileCost{5.97, 0.301} : TileCost{5.44, 0.194};
+    return bn == 256 ? TileCost{5.27, 0.305} : bn == 192 ? TileCost{4.64, 0.248} : TileCost{4.16, 0.179};
 }
+constexpr double kAccumWaveUs = 0.9;  // extra per wave of fp32 reduce-add (split-K / wgrad) epilogues
+
+int split_cap(const mm_gemm_args* const* probs, int n, int bn, int cg, int sms);
+
 TileChoice choose_tile(const mm_gemm_args* const* probs, int n, int sms) {
     TileChoice best{128, 1};
     double best_cost = 1e300;
     for (int cg : {1, 2}) {
         for (int cand : {128, 192, 256}) {
             if (cg == 2 && cand == 192) continue;
-            bool fits = true;
+            bool fits = true, accum = true;
+            for (int i = 0; i < n; ++i) {
+                if (cand > 128 && probs[i]->n <= cand - 64) fits = false;
+                accum = accum && probs[i]->epilogue == MM_EPI_F32_ACCUM;
+            }
+            if (!fits) continue;
+            const int cap = split_cap(probs, n, cand, cg, sms);
             int64_t units = 0;
             double kb_sum = 0;
             for (int i = 0; i < n; ++i) {
-                if (cand > 128 && probs[i]->n <= cand - 64) fits = false;
                 const int64_t t = ((probs[i]->m + BM * cg - 1) / (BM * cg)) * ((probs[i]->n + cand - 1) / cand);
-                units += t;
-                kb_sum += double(t) * double((probs[i]->k + BK - 1) / BK);
+                const int num_kb = static_cast<int>((probs[i]->k + BK - 1) / BK);
+                int splits = probs[i]->epilogue == MM_EPI_F32_ACCUM ? std::max(1, std::min(cap, num_kb / 2)) : 1;
+                const int kb_per = (num_kb + splits - 1) / splits;
+                splits = (num_kb + kb_per - 1) / kb_per;
+                units += t * splits;
+                kb_sum += double(t * splits) * kb_per;
             }
-            if (!fits) continue;
             const int slots = sms / cg;
             const double waves = double((units + slots - 1) / slots);
             const TileCost tc = tile_cost(cand, cg);
-            const double cost = tc.c0_us + waves * (kb_sum / double(units)) * tc.x_us;
+            const double cost =
+                tc.c0_us + waves * ((kb_sum / double(units)) * tc.x_us + (accum ? kAccumWaveUs : 0.0));
             if (cost < best_cost - 1e-9) { best_cost = cost; best = {cand, cg}; }
         }
     }
@@ -821,8 +838,6 @@ int run_group(const mm_gemm_args* const* probs, int n, cudaStream_t s) {
     g.trace = g_trace_buf;
     g.b_prefetch = 1;
     g.any_dbias = 0;
-    static const int dbg = std::getenv("MM_GEMM_DEBUG") ? std::atoi(std::getenv("MM_GEMM_DEBUG")) : 0;
-    g.debug = dbg;
     for (int i = 0; i < n; ++i) {
         g.b_prefetch &= probs[i]->b_prefetch ? 1 : 0;
         if (probs[i]->dbias) g.any_dbias = 1;
