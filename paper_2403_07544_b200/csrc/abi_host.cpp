@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Host-side entry points of libmmb200: version / error reporting, device
 // info and K9 (the allocator's communication-cost kernel).
 #include <algorithm>
@@ -19,6 +20,11 @@ void set_error(const char* fmt, ...) {
     vsnprintf(buf, sizeof(buf), fmt, ap);
     va_end(ap);
     g_last_error = buf;
+}
+
+bool pdl_enabled() {
+    static const bool on = std::getenv("MM_NO_PDL") == nullptr;
+    return on;
 }
 
 int num_sms() {

@@ -320,8 +320,13 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 2) attn_bwd_kernel(const mm_at
     stage_group(Qs, Ks, Vs, dOs, G, a, h, nthr);
     for (int i = 0; i < G.n; ++i) {
         const int pq = (G.lq[i] + 31) & ~31;
-        for (int r = threadIdx.x; r < pq; r += nthr)
+        for (int r = threadIdx.x; r < pq; r += nthr) {
             lse2[G.qoff[i] + r] = r < G.lq[i] ? a.lse[int64_t(h) * a.total_q + G.q0[i] + r] * kLog2e : 0.f;
+            // phase A writes D only for rows of its 16-row tiles; phase B reads
+            // it for every row of a 32-row block (as 0 * (dP - D) past lq), so
+            // the padding rows must hold a finite value, not stale smem
+            Dd[G.qoff[i] + r] = 0.f;
+        }
     }
     cp_async_wait_all();
     __syncthreads();

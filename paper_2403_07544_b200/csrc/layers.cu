@@ -3,7 +3,11 @@
 // with 128-bit vector accesses and warp-shuffle reductions.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "mm_common.h"
+#include "tc_ptx.cuh"
 
 namespace {
 
@@ -331,6 +335,135 @@ __global__ void __launch_bounds__(kXentThreads) xent_kernel(const uint16_t* logi
     }
 }
 
+// Persistent variant (one CTA per SM, vocab <= kXentSmemVocab): each CTA
+// walks rows b, b + grid, ...; a 1-D bulk copy (TMA) streams the NEXT row into
+// the other half of a double-buffered smem row while the current row is
+// reduced and its dlogits written, so HBM reads overlap the math.  The math is
+// kept to one MUFU exp per logit (the exps stay in registers between the sum
+// and the write pass -- two exps per logit are SFU-bound at ~60 us for a
+// 4096 x 32000 batch on B200's 16 MUFU/clk/SM) and a packed bf16x2 max.
+constexpr int kXentSmemVocab = kXentThreads * 8 * 8;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float xent_block_reduce(float v, float* sm, bool is_max) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = is_max ? warp_max(v) : warp_sum(v);
+    __syncthreads();  // sm free (previous reduction consumed)
+    if (lane == 0) sm[warp] = v;
+    __syncthreads();
+    float r = is_max ? -INFINITY : 0.f;
+#pragma unroll
+    for (int j = 0; j < kXentThreads / 32; ++j) r = is_max ? fmaxf(r, sm[j]) : r + sm[j];
+    return r;
+}
+
+__global__ void __launch_bounds__(kXentThreads, 1) xent_stream_kernel(const uint16_t* logits,
+                                                                      const int32_t* __restrict__ labels,
+                                                                      uint16_t* dlogits, float* row_loss,
+                                                                      float* loss_sum, int64_t rows,
+                                                                      int vocab, float grad_scale) {
+    constexpr int VPT = kXentSmemVocab / kXentThreads / 8;  // 8-logit vectors per thread
+    constexpr float kL2e = 1.4426950408889634f;
+    extern __shared__ __align__(128) uint8_t xsm[];
+    __shared__ uint64_t bar[2];
+    __shared__ float red[kXentThreads / 32];
+    uint16_t* const buf0 = reinterpret_cast<uint16_t*>(xsm);
+    const uint32_t bytes = static_cast<uint32_t>(vocab) * 2u;
+    const int nv = vocab / 8;
+    if (threadIdx.x == 0) {
+        tc::mbar_init(&bar[0], 1);
+        tc::mbar_init(&bar[1], 1);
+        tc::fence_barrier_init();
+    }
+    // each buffer is kXentSmemVocab wide; the tail past the vocab holds bf16
+    // -inf (exp -> 0), so every thread's VPT vectors are unconditional
+    for (int c = vocab + threadIdx.x; c < kXentSmemVocab; c += kXentThreads)
+        buf0[c] = buf0[kXentSmemVocab + c] = 0xff80u;
+    __syncthreads();
+    pdl_wait();
+    const int64_t first = blockIdx.x, step = gridDim.x;
+    if (threadIdx.x == 0 && first < rows) {
+        tc::mbar_expect_tx(&bar[0], bytes);
+        tc::bulk_load_1d(buf0, logits + first * int64_t(vocab), bytes, &bar[0]);
+    }
+    int it = 0;
+    for (int64_t row = first; row < rows; row += step, ++it) {
+        const int b = it & 1;
+        // prefetch the next row into the other buffer (its previous row was
+        // fully consumed before the trailing __syncthreads of the last iteration)
+        if (threadIdx.x == 0 && row + step < rows) {
+            tc::mbar_expect_tx(&bar[b ^ 1], bytes);
+            tc::bulk_load_1d(buf0 + (b ^ 1) * kXentSmemVocab, logits + (row + step) * int64_t(vocab), bytes, &bar[b ^ 1]);
+        }
+        const int label = labels[row];
+        tc::mbar_wait(&bar[b], static_cast<uint32_t>((it >> 1) & 1));
+        const uint16_t* lrow = buf0 + b * kXentSmemVocab;
+        const uint4* lr = reinterpret_cast<const uint4*>(lrow);
+        uint4* dr = reinterpret_cast<uint4*>(dlogits + row * int64_t(vocab));
+        if (label < 0) {
+            for (int v = threadIdx.x; v < nv; v += kXentThreads) dr[v] = make_uint4(0, 0, 0, 0);
+            if (threadIdx.x == 0) row_loss[row] = 0.f;
+            __syncthreads();
+            continue;
+        }
+        // pass 1: row max (packed bf16x2 max)
+        __nv_bfloat162 m2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            const uint4 w = lr[threadIdx.x + i * kXentThreads];
+            m2 = __hmax2(m2, __hmax2(__hmax2(*reinterpret_cast<const __nv_bfloat162*>(&w.x),
+                                             *reinterpret_cast<const __nv_bfloat162*>(&w.y)),
+                                     __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&w.z),
+                                             *reinterpret_cast<const __nv_bfloat162*>(&w.w))));
+        }
+        const float gm = xent_block_reduce(fmaxf(__low2float(m2), __high2float(m2)), red, true);
+        const float gm2 = gm * kL2e;
+        // pass 2: one exp per logit, kept in registers
+        float p[VPT][8];
+        float sacc = 0.f;
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            const uint4 w = lr[threadIdx.x + i * kXentThreads];
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                p[i][2 * e] = ex2_approx(fmaf(bf2f(ws[e] & 0xffff), kL2e, -gm2));
+                p[i][2 * e + 1] = ex2_approx(fmaf(bf2f(ws[e] >> 16), kL2e, -gm2));
+                sacc += p[i][2 * e] + p[i][2 * e + 1];
+            }
+        }
+        const float gs = xent_block_reduce(sacc, red, false);
+        const float sc = grad_scale / gs;
+        if (threadIdx.x == 0) {
+            const float l = gm + __logf(gs) - bf2f(lrow[label]);
+            row_loss[row] = l;
+            if (loss_sum) atomicAdd(loss_sum, l * grad_scale);  // token mean when scale = 1/rows
+        }
+        // pass 3: dlogits = softmax * scale, then the label's -scale
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            uint32_t o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                __nv_bfloat162 h = __floats2bfloat162_rn(p[i][2 * e] * sc, p[i][2 * e + 1] * sc);
+                o[e] = *reinterpret_cast<uint32_t*>(&h);
+            }
+            const int v = threadIdx.x + i * kXentThreads;
+            if (v < nv) dr[v] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+        if (threadIdx.x == (label >> 3) % kXentThreads) {  // the thread that stored the label's vector
+            const float pl = ex2_approx(fmaf(bf2f(lrow[label]), kL2e, -gm2));  // == its p, recomputed
+            reinterpret_cast<uint16_t*>(dr)[label] = f2bf(pl * sc - grad_scale);
+        }
+        __syncthreads();  // buffer b fully read before it is refilled
+    }
+}
+
 // ----------------------------------------------------------------------------
 // out[c] += sum_r x[r, c] (bias gradients).  Block = 32 column octets (256
 // columns, one 128-bit load per row per thread) x 8 row lanes; the grid has
@@ -459,7 +592,18 @@ extern "C" int mm_xent_fwd_bwd(const uint16_t* logits, const int32_t* labels, ui
     MM_CHECK_ARG(logits && labels && dlogits && row_loss, "NULL argument");
     MM_CHECK_ARG(vocab % 8 == 0, "vocab must be a multiple of 8");
     if (rows == 0) return 0;
-    MM_CUDA_TRY(mm::launch_pdl(xent_kernel, dim3(static_cast<unsigned>(rows)), dim3(kXentThreads), 0, mm::as_stream(stream), logits, labels, dlogits, row_loss, loss_sum, vocab, grad_scale));
+    static const bool force_rowwise = std::getenv("MM_XENT_ROWWISE") != nullptr;  // diagnostics
+    if (vocab <= kXentSmemVocab && !force_rowwise) {
+        const size_t smem = size_t(2) * kXentSmemVocab * 2;
+        MM_CUDA_TRY(cudaFuncSetAttribute(xent_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(rows, mm::num_sms()));
+        MM_CUDA_TRY(mm::launch_pdl(xent_stream_kernel, dim3(grid), dim3(kXentThreads), smem,
+                                   mm::as_stream(stream), logits, labels, dlogits, row_loss, loss_sum,
+                                   rows, vocab, grad_scale));
+    } else {
+        MM_CUDA_TRY(mm::launch_pdl(xent_kernel, dim3(static_cast<unsigned>(rows)), dim3(kXentThreads), 0, mm::as_stream(stream), logits, labels, dlogits, row_loss, loss_sum, vocab, grad_scale));
+    }
     MM_LAUNCH_CHECK("xent_kernel");
     return 0;
 }

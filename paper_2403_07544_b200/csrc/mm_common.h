@@ -25,6 +25,9 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int num_sms();
 
+// programmatic dependent launch on (default) or off (MM_NO_PDL=1, diagnostics)
+bool pdl_enabled();
+
 // every kernel launch of the library (bench.py's gpu_launches; mm_launch_count)
 extern std::atomic<unsigned long long> g_launches;
 
@@ -43,7 +46,7 @@ inline cudaError_t launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 bl
     cfg.stream = s;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     at[1].id = cudaLaunchAttributeClusterDimension;
     at[1].val.clusterDim.x = cluster_x;
     at[1].val.clusterDim.y = 1;
