@@ -72,15 +72,27 @@ struct Driver {
     const float* wf(const mm_stack* st, int64_t off) const { return st->w_f32 + off; }
     float* g(const mm_stack* st, int64_t off) const { return st->grad + off; }
 
-    int gemm(const void* A, bool a_k, const void* B, bool b_k, void* D, int64_t m, int64_t n,
-             int64_t k, int64_t lda, int64_t ldb, int64_t ldd, int epi, const float* bias = nullptr,
-             const float* resid = nullptr, const void* aux = nullptr, float* dbias = nullptr) {
+    static mm_gemm_args make_args(const void* A, bool a_k, const void* B, bool b_k, void* D, int64_t m,
+                                  int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldd, int epi,
+                                  const float* bias = nullptr, const float* resid = nullptr,
+                                  const void* aux = nullptr, float* dbias = nullptr) {
         mm_gemm_args a{};
         a.a = A; a.b = B; a.d = D; a.bias = bias; a.resid = resid; a.aux = aux; a.dbias = dbias;
         a.m = m; a.n = n; a.k = k; a.lda = lda; a.ldb = ldb; a.ldd = ldd;
         a.a_kmajor = a_k; a.b_kmajor = b_k; a.epilogue = epi;
         a.b_prefetch = 1;  // B is a weight or an earlier forward activation
+        return a;
+    }
+    int gemm(const void* A, bool a_k, const void* B, bool b_k, void* D, int64_t m, int64_t n,
+             int64_t k, int64_t lda, int64_t ldb, int64_t ldd, int epi, const float* bias = nullptr,
+             const float* resid = nullptr, const void* aux = nullptr, float* dbias = nullptr) {
+        const mm_gemm_args a = make_args(A, a_k, B, b_k, D, m, n, k, lda, ldb, ldd, epi, bias, resid, aux, dbias);
         return mm_gemm(&a, s);
+    }
+    // dX[T,in] (epi)= dY[T,out] W[out,in] as a problem of a grouped launch
+    static mm_gemm_args dgrad_args(const uint16_t* dY, const uint16_t* W, void* dX, int64_t T, int64_t in,
+                                   int64_t out, int epi) {
+        return make_args(dY, true, W, false, dX, T, in, out, out, in, in, epi);
     }
     // Y[T,out] (epi)= X[T,in] W[out,in]^T
     int linear(const uint16_t* X, const uint16_t* W, void* Y, int64_t T, int64_t in, int64_t out,
@@ -176,8 +188,8 @@ struct Driver {
         if (int e = ln(st, o->lnc_g, o->lnc_b, x, T, sv.h, sv.mean, sv.rstd)) return e;
         sv.q = ar.get<uint16_t>(T * d);
         TRY(linear(sv.h, wb(st, o->cq_w), sv.q, T, d, d, MM_EPI_BF16, wf(st, o->cq_b)));
-        sv.kv = ar.get<uint16_t>(S * 2 * d);
-        TRY(linear(mem, wb(st, o->ckv_w), sv.kv, S, d, 2 * d, MM_EPI_BF16, wf(st, o->ckv_b)));
+        // sv.kv: computed for every decoder layer in one grouped launch (kv_all)
+        (void)mem; (void)S;
         sv.a = ar.get<uint16_t>(T * d);
         sv.lse = ar.get<float>(int64_t(H) * T);
         mm_attn_args a = attn(sv.q, sv.kv, sv.kv + d, d, 2 * d, sv.a, sv.lse, b.cu_tgt, b.cu_src,
@@ -267,10 +279,13 @@ struct Driver {
         a.ld_dq = d; a.ld_dk = a.ld_dv = 2 * d;
         TRY(mm_attention_bwd(&a, s));
         TRY(wgrad(dkv, mem, g(st, o->ckv_w), S, d, 2 * d, g(st, o->ckv_b)));
-        TRY(dgrad(dkv, wb(st, o->ckv_w), dmem, S, d, 2 * d, MM_EPI_F32_ACCUM));
         TRY(wgrad(dq, sv.h, g(st, o->cq_w), T, d, d, g(st, o->cq_b)));
         float* dh = ar.get<float>(T * d);
-        TRY(dgrad(dq, wb(st, o->cq_w), dh, T, d, d, MM_EPI_F32));
+        // the two independent dgrads of the block (memory side, query side)
+        // share one grouped launch
+        const mm_gemm_args dg[2] = {dgrad_args(dkv, wb(st, o->ckv_w), dmem, S, d, 2 * d, MM_EPI_F32_ACCUM),
+                                    dgrad_args(dq, wb(st, o->cq_w), dh, T, d, d, MM_EPI_F32)};
+        TRY(mm_gemm_grouped(dg, 2, s));
         uint16_t* nbf = next_bf(dx_bf, T);
         TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->lnc_g), sv.mean, sv.rstd, dx, nbf,
                              g(st, o->lnc_g), g(st, o->lnc_b), T, d, s));
@@ -308,7 +323,18 @@ struct Driver {
         uint16_t* mem; float* mem_mean; float* mem_rstd;
         if (int e = ln(lnf_e, lnf_e->lnf_g, lnf_e->lnf_b, x, Ts, mem, mem_mean, mem_rstd)) return e;
         const float* x_enc = x;
-        // ---- decoder
+        // ---- decoder: every layer's cross-attention K/V projection of the
+        // encoder memory in one grouped launch (they depend on mem only)
+        {
+            mm_gemm_args kv[64];
+            for (int l = 0; l < nd; ++l) {
+                CrossSave& sv = dec_l[l].cross;
+                sv.kv = ar.get<uint16_t>(Ts * 2 * d);
+                kv[l] = make_args(mem, true, wb(dec_l[l].st, dec_l[l].o->ckv_w), true, sv.kv, Ts, 2 * d, d,
+                                  d, d, 2 * d, MM_EPI_BF16, wf(dec_l[l].st, dec_l[l].o->ckv_b));
+            }
+            TRY(mm_gemm_grouped(kv, nd, s));
+        }
         float* y = ar.get<float>(Tt * d);
         TRY(mm_embed_fwd(b.tgt_in, b.tgt_pos, t.dec_emb.w_bf16 + t.dec_emb.emb, y, Tt, d, scale, s));
         for (int l = 0; l < nd; ++l) {

@@ -194,7 +194,7 @@ def attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, heads, max_q, max_k, caus
         gh, cap = attention_groups(_np.asarray(cu_q.cpu()), _np.asarray(cu_k.cpu()))
         groups = (torch.from_numpy(gh).to(q.device), len(gh) // 2, cap)
     gt, n_groups, cap = groups
-    return AttnArgs(
+    args = AttnArgs(
         q=q.data_ptr(), k=k.data_ptr(), v=v.data_ptr(), o=o.data_ptr(), lse=lse.data_ptr(),
         d_o=_ptr(d_o), dq=_ptr(dq), dk=_ptr(dk), dv=_ptr(dv),
         cu_q=cu_q.data_ptr(), cu_k=cu_k.data_ptr(),
@@ -204,6 +204,10 @@ def attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, heads, max_q, max_k, caus
         n_seq=n_seq, heads=heads, head_dim=hd, causal=int(causal), max_q=max_q, max_k=max_k,
         scale=1.0 / math.sqrt(hd), total_q=q.shape[0],
         groups=gt.data_ptr(), n_groups=n_groups, cap=cap)
+    # the struct holds raw pointers: keep the device group table (possibly
+    # built here) alive as long as the args are
+    args._keep = (gt,)
+    return args
 
 
 def attention_fwd(args: AttnArgs) -> None:
