@@ -53,6 +53,13 @@ __device__ __forceinline__ void mma(float (&c)[4], const uint32_t (&a)[4], uint3
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// 2^x on the SFU, flush-to-zero (exp2f without fast-math adds subnormal
+// handling around MUFU.EX2); -inf -> +0
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ uint32_t pack(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
@@ -73,6 +80,9 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool vali
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
                  "r"(valid ? 16 : 0)
                  : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -152,7 +162,7 @@ struct Group {
 
 // called by warp 0: lane i loads sequence i of the group, offsets by warp scan
 __device__ __forceinline__ void load_group(Group& G, const mm_attn_args& a, int lane) {
-    const int first = a.groups[2 * blockIdx.x], n = a.groups[2 * blockIdx.x + 1];
+    const int first = a.groups[2 * blockIdx.y], n = a.groups[2 * blockIdx.y + 1];
     int q0 = 0, lq = 0, k0 = 0, lk = 0;
     if (lane < n) {
         q0 = a.cu_q[first + lane];
@@ -211,9 +221,11 @@ constexpr int kFwdWarps = 4;
 __global__ void __launch_bounds__(kFwdWarps * 32) attn_fwd_kernel(const mm_attn_args a) {
     extern __shared__ __align__(16) uint16_t sm[];
     __shared__ Group G;
-    const int h = blockIdx.y;
-    pdl_wait();
+    const int h = blockIdx.x;  // heads fastest: a group's CTAs run together and share its rows' DRAM pages
+    // the group table and sequence offsets come from the step's host upload,
+    // not from the previous kernel: read them before griddepcontrol.wait
     if (threadIdx.x < 32) load_group(G, a, threadIdx.x);
+    pdl_wait();
     __syncthreads();
     uint16_t* Qs = sm;
     uint16_t* Ks = Qs + a.cap * kP;
@@ -260,7 +272,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) attn_fwd_kernel(const mm_attn_
             for (int i = 0; i < 2; ++i) {
                 const float mn = fmaxf(m[i], quad_max(mx[i]));
                 mref[i] = mn == -INFINITY ? 0.f : mn;
-                corr[i] = exp2f(m[i] - mref[i]);  // m = -inf -> 0
+                corr[i] = ex2(m[i] - mref[i]);  // m = -inf -> 0
                 m[i] = mn;
             }
             float sum[2] = {0.f, 0.f};
@@ -268,7 +280,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) attn_fwd_kernel(const mm_attn_
             for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const float p = exp2f(s[nt][e] - mref[e >> 1]);
+                    const float p = ex2(s[nt][e] - mref[e >> 1]);
                     s[nt][e] = p;
                     sum[e >> 1] += p;
                 }
@@ -303,12 +315,30 @@ __global__ void __launch_bounds__(kFwdWarps * 32) attn_fwd_kernel(const mm_attn_
 // ---------------------------------------------------------------------------
 constexpr int kBwdWarps = 8;
 
+#ifdef MM_ATTN_TRACE  // diagnostics build: per-CTA phase stamps of the last backward launch
+__device__ unsigned long long g_attn_trace[8192 * 4];
+#define ATTN_STAMP(i)                                                                         \
+    do {                                                                                      \
+        if (threadIdx.x == 0) {                                                               \
+            unsigned long long t_;                                                            \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+            const int cta_ = blockIdx.y * gridDim.x + blockIdx.x;                             \
+            if (cta_ < 8192) g_attn_trace[cta_ * 4 + (i)] = t_;                               \
+        }                                                                                     \
+    } while (0)
+#else
+#define ATTN_STAMP(i) \
+    do {              \
+    } while (0)
+#endif
+
 __global__ void __launch_bounds__(kBwdWarps * 32, 2) attn_bwd_kernel(const mm_attn_args a) {
     extern __shared__ __align__(16) uint16_t sm[];
     __shared__ Group G;
-    const int h = blockIdx.y;
+    const int h = blockIdx.x;  // heads fastest: a group's CTAs run together and share its rows' DRAM pages
+    if (threadIdx.x < 32) load_group(G, a, threadIdx.x);  // host-uploaded: before the wait
     pdl_wait();
-    if (threadIdx.x < 32) load_group(G, a, threadIdx.x);
+    ATTN_STAMP(0);
     __syncthreads();
     uint16_t* Qs = sm;
     uint16_t* dOs = Qs + a.cap * kP;
@@ -321,7 +351,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 2) attn_bwd_kernel(const mm_at
     for (int i = 0; i < G.n; ++i) {
         const int pq = (G.lq[i] + 31) & ~31;
         for (int r = threadIdx.x; r < pq; r += nthr) {
-            lse2[G.qoff[i] + r] = r < G.lq[i] ? a.lse[int64_t(h) * a.total_q + G.q0[i] + r] * kLog2e : 0.f;
+            // lse rides the same cp.async batch (4-byte copies); padding rows 0
+            if (r < G.lq[i]) cp_async4(lse2 + G.qoff[i] + r, a.lse + int64_t(h) * a.total_q + G.q0[i] + r);
+            else lse2[G.qoff[i] + r] = 0.f;
             // phase A writes D only for rows of its 16-row tiles; phase B reads
             // it for every row of a 32-row block (as 0 * (dP - D) past lq), so
             // the padding rows must hold a finite value, not stale smem
@@ -330,6 +362,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 2) attn_bwd_kernel(const mm_at
     }
     cp_async_wait_all();
     __syncthreads();
+    for (int r = threadIdx.x; r < a.cap; r += nthr) lse2[r] *= kLog2e;  // natural log -> log2 domain
+    __syncthreads();
+    ATTN_STAMP(1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
     const float c = a.scale * kLog2e;
@@ -360,14 +395,19 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 2) attn_bwd_kernel(const mm_at
                 zero(dp);
                 mma_abt(s, qf, Kseq, kb, lane);
                 mma_abt(dp, df, Vseq, kb, lane);
+                // a block fully inside the sequence (and below the causal
+                // diagonal of both rows) needs no per-element masks
+                const bool full = kb + 32 <= lk && row1 < lq && (!a.causal || kb + 31 <= row0);
 #pragma unroll
                 for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const int key = kb + nt * 8 + 2 * t + (e & 1);
-                        const int row = e < 2 ? row0 : row1;
-                        float p = exp2f(s[nt][e] * c - (e < 2 ? l20 : l21));
-                        if (key >= lk || (a.causal && key > row) || row >= lq) p = 0.f;
+                        float p = ex2(s[nt][e] * c - (e < 2 ? l20 : l21));
+                        if (!full) {
+                            const int key = kb + nt * 8 + 2 * t + (e & 1);
+                            const int row = e < 2 ? row0 : row1;
+                            if (key >= lk || (a.causal && key > row) || row >= lq) p = 0.f;
+                        }
                         if (pass == 0) dpart[e >> 1] = fmaf(p, dp[nt][e], dpart[e >> 1]);
                         else s[nt][e] = p * (dp[nt][e] - (e < 2 ? D0 : D1));  // dS
                     }
@@ -396,6 +436,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 2) attn_bwd_kernel(const mm_at
         }
     }
     __syncthreads();
+    ATTN_STAMP(2);
 
     // ---------------- phase B: dK, dV (warps over 16-key tiles)
     const int nkt = n_tiles(G, G.lk);
@@ -433,7 +474,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 2) attn_bwd_kernel(const mm_at
                         const int key = e < 2 ? key0 : key1;
                         float p = 0.f;
                         if (q < lq && key < lk && !(a.causal && key > q))
-                            p = exp2f(st[nt][e] * c - lse2[qo + q]);
+                            p = ex2(st[nt][e] * c - lse2[qo + q]);
                         if (pass == 0) st[nt][e] = p;
                         else dpt[nt][e] = p * (dpt[nt][e] - Dd[qo + q]);
                     }
@@ -454,6 +495,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 2) attn_bwd_kernel(const mm_at
             }
         }
     }
+    __syncthreads();
+    ATTN_STAMP(3);
 }
 
 size_t fwd_smem(const mm_attn_args& a) { return size_t(3) * a.cap * kP * 2; }
@@ -474,13 +517,20 @@ int check(const mm_attn_args* a, bool bwd) {
 
 }  // namespace
 
+#ifdef MM_ATTN_TRACE
+extern "C" int mm_attn_trace_read(unsigned long long* host, int n) {
+    MM_CUDA_TRY(cudaMemcpyFromSymbol(host, g_attn_trace, sizeof(unsigned long long) * n));
+    return 0;
+}
+#endif
+
 extern "C" int mm_attention_fwd(const mm_attn_args* a, void* stream) {
     if (int st = check(a, false)) return st;
     if (a->n_seq == 0) return 0;
     const size_t smem = fwd_smem(*a);
     MM_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-    MM_CUDA_TRY(mm::launch_pdl(attn_fwd_kernel, dim3(a->n_groups, a->heads), dim3(kFwdWarps * 32),
+    MM_CUDA_TRY(mm::launch_pdl(attn_fwd_kernel, dim3(a->heads, a->n_groups), dim3(kFwdWarps * 32),
                                smem, mm::as_stream(stream), *a));
     MM_LAUNCH_CHECK("attn_fwd_kernel");
     return 0;
@@ -493,7 +543,7 @@ extern "C" int mm_attention_bwd(const mm_attn_args* a, void* stream) {
     MM_CHECK_ARG(smem <= 227 * 1024, "attention backward needs %zu B of smem", smem);
     MM_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-    MM_CUDA_TRY(mm::launch_pdl(attn_bwd_kernel, dim3(a->n_groups, a->heads), dim3(kBwdWarps * 32),
+    MM_CUDA_TRY(mm::launch_pdl(attn_bwd_kernel, dim3(a->heads, a->n_groups), dim3(kBwdWarps * 32),
                                smem, mm::as_stream(stream), *a));
     MM_LAUNCH_CHECK("attn_bwd_kernel");
     return 0;
