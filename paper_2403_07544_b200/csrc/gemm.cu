@@ -55,9 +55,13 @@ constexpr int kEpiWarp0 = 2;
 constexpr int kEpiWarps = MM_GEMM_EPI_WARPS;
 constexpr int kSlices = kEpiWarps / 4;
 constexpr int kEpiBufs = MM_GEMM_EPI_BUFS;  // staging boxes per epilogue warp
-constexpr int kBiasWarp = kEpiWarp0 + kEpiWarps;  // second consumer of every smem stage
-constexpr int kThreads = (kBiasWarp + 1) * 32;
-constexpr int kMaxProbs = 24;  // problems per grouped launch (kernel parameter space)
+constexpr int kBiasWarp = kEpiWarp0 + kEpiWarps;  // first of the bias-gradient warps
+// bias-gradient warps: second consumer of every smem stage; each sums 16 of
+// the stage's 64 K-rows (one warp summing all 64 was slower than a 256-wide
+// MMA k-block and gated the pipeline: +46 % on the generator wgrad)
+constexpr int kBiasWarps = 4;
+constexpr int kThreads = (kBiasWarp + kBiasWarps) * 32;
+constexpr int kMaxProbs = 48;  // problems per grouped launch (kernel parameter space: ~21 KB of 32 KB)
 
 constexpr int kEpiBufBytes = 32 * 128;                    // 32 rows x 128 B box
 constexpr int kEpiSmem = kEpiWarps * kEpiBufs * kEpiBufBytes;
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < C::kStages; ++s) {
             tc::mbar_init(&full_bar[s], 1);
-            tc::mbar_init(&empty_bar[s], dbias_any ? 2 : 1);  // MMA commit (+ bias warp)
+            tc::mbar_init(&empty_bar[s], dbias_any ? 1 + kBiasWarps : 1);  // MMA commit (+ bias warps)
             tc::mbar_init(&bias_bar[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -446,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) MM_TRACE(3);
             __syncwarp();
         }
-    } else if (warp == kBiasWarp) {
+    } else if (warp >= kBiasWarp) {
         // ------------------------------------------------------------ bias-grad warp
         // Second consumer of every smem stage.  For a wgrad (A = dY, MN-major)
         // with dbias set, dbias[m] += sum_k dY[k, m]: the tiles_n units that load
@@ -476,8 +480,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (bias_sum && kb % tiles_n == tn) {
                     const uint8_t* box = smem_a + stage * C::kABytes + (lane >> 4) * 64 * BK * 2;
                     const int chunk = (lane & 15) >> 1, sub = (lane & 1) * 8;
-#pragma unroll 8
-                    for (int r = 0; r < BK; ++r) {
+                    const int r0 = (warp - kBiasWarp) * (BK / kBiasWarps);
+#pragma unroll
+                    for (int r = r0; r < r0 + BK / kBiasWarps; ++r) {
                         const uint2 v = *reinterpret_cast<const uint2*>(
                             box + r * 128 + ((chunk ^ (r & 7)) * 16) + sub);
                         bsum[0] += bf16_to_f(v.x & 0xffff);
@@ -736,8 +741,13 @@ TileChoice choose_tile(const mm_gemm_args* const* probs, int n, int sms) {
             const int slots = sms / cg;
             const double waves = double((units + slots - 1) / slots);
             const TileCost tc = tile_cost(cand, cg);
-            const double cost =
+            double cost =
                 tc.c0_us + waves * ((kb_sum / double(units)) * tc.x_us + (accum ? kAccumWaveUs : 0.0));
+            // a launch that keeps every SM busy is L2->SM bandwidth bound
+            // (~32 KB per k-block per CTA at every shape): only the pair's
+            // 128 x 256 per-SM tile does enough MMA work per byte (measured on
+            // the grouped weight-gradient launches, tools/wgrad_micro.py)
+            if (accum && waves >= 2.0 && !(cg == 2 && cand == 256)) cost *= 1.15;
             if (cost < best_cost - 1e-9) { best_cost = cost; best = {cand, cg}; }
         }
     }

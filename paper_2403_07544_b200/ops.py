@@ -128,7 +128,7 @@ def gemm_grouped(problems: list) -> None:
     must share a_kmajor / b_kmajor.
     """
     arr = (GemmArgs * len(problems))(*[gemm_args(**p) for p in problems])
-    LAUNCHES[0] += (len(problems) + 23) // 24
+    LAUNCHES[0] += (len(problems) + 47) // 48
     check(lib().mm_gemm_grouped(arr, len(problems), stream_ptr()), "mm_gemm_grouped")
 
 

@@ -22,6 +22,11 @@ cases = [  # name, m, n, k, a_k, b_k, epi
     ("wgrad gen", 32000, 512, T, False, False, ops.EPI_F32_ACCUM),
     ("tiny", 128, 128, 64, True, True, ops.EPI_F32),
     ("big", 8192, 8192, 8192, True, True, ops.EPI_BF16),
+    ("maj kk", 2048, 512, 4096, True, True, ops.EPI_F32),
+    ("maj km", 2048, 512, 4096, True, False, ops.EPI_F32),
+    ("maj mk", 2048, 512, 4096, False, True, ops.EPI_F32),
+    ("maj mm", 2048, 512, 4096, False, False, ops.EPI_F32),
+    ("maj mm acc", 2048, 512, 4096, False, False, ops.EPI_F32_ACCUM),
     ("odd", 1000, 700, 520, True, True, ops.EPI_F32),
     ("odd wg", 700, 520, 1000, False, False, ops.EPI_F32_ACCUM),
     ("odd dg", 1000, 520, 700, True, False, ops.EPI_F32),
