@@ -434,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::mbar_wait(&full_bar[stage], phase);
                 tc::tc_fence_after();
                 MM_KB_TRACE(128, consumed);
+                if (consumed == 0 && lane == 0) MM_TRACE(2);
                 const uint32_t a_lo = a_lo0 + static_cast<uint32_t>(stage * (C::kABytes / 16));
                 const uint32_t b_lo = b_lo0 + static_cast<uint32_t>(stage * (C::kBBytes / 16));
                 if (!(MM_GEMM_DEBUG & 1)) {
@@ -572,7 +573,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         if (warp == kEpiWarp0 && lane == 0) MM_TRACE(5);
-        if (lane == 0) tc::bulk_wait_all();
+        // the CTA may exit once its staging boxes have been READ: the global
+        // writes themselves complete with the grid (what griddepcontrol.wait
+        // of the next kernel and stream order wait for), as in CUTLASS's
+        // tma_store_wait
+        if (lane == 0) tc::bulk_wait_read<0>();
         if (warp == kEpiWarp0 && lane == 0) MM_TRACE(6);
     }
     pdl_trigger();

@@ -190,6 +190,13 @@ class Engine:
         # even at N=1 (r01 sweep: 8/16/32/64 CTAs -> 266K/413K/587K/740K vs
         # 756K tok/s): the update is HBM-bound and latency-bound per CTA.
         self.overlap_ctas = int(os.environ.get("MM_OVERLAP_CTAS", "0"))
+        # Cross-step deferral (single rank): the encoder-side update of step k
+        # runs on the side stream under step k+1's compute; step k+1 waits for
+        # it only if it uses one of the modules being updated (a module's
+        # update always completes before its next read or gradient reset).
+        self.defer_update = world == 1 and os.environ.get("MM_DEFER_UPDATE", "1") != "0"
+        self._pending_event = None            # side-stream event: every issued update done
+        self._pending_mods: set = set()       # modules whose update may still be running
         self._counts_host = torch.zeros(len(self.plan.keys), dtype=torch.int32, pin_memory=True)
         self._side_stream = torch.cuda.Stream(device=self.device)
         # torch creates the CUDA event lazily: record once so .cuda_event is a
@@ -503,6 +510,8 @@ class Engine:
         used: set[ModuleKey] = set()
         for t in tasks:
             used.update(task_modules(t))
+        if self._pending_mods & used:  # a module of this step is still being updated
+            self.sync_updates()
         flags = ready_flags(self.plan, self.rank, used)
         counts_ready = None
         if self.comm is not None:
@@ -536,11 +545,31 @@ class Engine:
                 # a thin background update: few CTAs, so the encoder-backward
                 # GEMMs keep their SMs
                 self.exchange_and_update(counts, used, only=dec, max_ctas=self.overlap_ctas)
-            self.exchange_and_update(counts, used, only=set(self.states) - dec)
-            torch.cuda.current_stream().wait_stream(side)
+            rest = set(self.states) - dec
+            if self.defer_update:
+                side.wait_stream(torch.cuda.current_stream())  # this step's gradients final
+                with torch.cuda.stream(side):
+                    self.exchange_and_update(counts, used, only=rest, max_ctas=self.overlap_ctas)
+                ev = torch.cuda.Event()
+                ev.record(side)
+                self._pending_event = ev
+                self._pending_mods |= {k for k in self.states if counts[self.index[k]] >= 1}
+            else:
+                self.exchange_and_update(counts, used, only=rest)
+                torch.cuda.current_stream().wait_stream(side)
         else:
             self.exchange_and_update(counts, used)
         return {"tasks": picked, "ready": dict(zip(self.plan.keys, counts))}
+
+    def sync_updates(self) -> None:
+        """Order the current stream after every issued optimizer update (the
+        deferred ones of earlier steps included); host reads of module state
+        (weights, moments, step counts on the device) must call this or a
+        device-wide synchronize first."""
+        if self._pending_event is not None:
+            torch.cuda.current_stream().wait_event(self._pending_event)
+            self._pending_event = None
+        self._pending_mods = set()
 
     def exchange_and_update(self, counts: Sequence[int], used=frozenset(), only=None,
                             max_ctas: int = 0) -> None:
@@ -583,6 +612,7 @@ class Engine:
                                                      inv_loss_scale=1.0, max_ctas=max_ctas))
 
     def close(self) -> None:
+        self.sync_updates()
         if self.comm is not None:
             self.comm.close()
             self.comm = None

@@ -28,7 +28,7 @@ for name, (m, n, k, ak, bk, epi) in cases.items():
     t = t[t[:, 0] > 0]
     base = t[:, 0].min()
     r = (t - base) / 1e3  # us
-    print(f"{name:10s} ctas={len(t)}  entry spread {r[:,0].max():.2f}us | setup {np.median(r[:,1]-r[:,0]):.2f} | "
-          f"first-full {np.median(r[:,2]-r[:,1]):.2f} | mma-all {np.median(r[:,3]-r[:,2]):.2f} | "
-          f"tfull-wait {np.median(r[:,4]-r[:,3]):.2f} | epi {np.median(r[:,5]-r[:,4]):.2f} | drain {np.median(r[:,6]-r[:,5]):.2f} | "
-          f"exit {np.median(r[:,7]-r[:,6]):.2f} | end max {r[:,7].max():.2f}us")
+    med = lambda a, b: np.median(r[:, b] - r[:, a])
+    print(f"{name:10s} ctas={len(t)} entry-spread {r[:,0].max():.2f} | setup {med(0,1):.2f} | first-full {med(1,2):.2f} | "
+          f"mainloop {med(2,3):.2f} | mma-drain {med(3,4):.2f} | epi {med(4,5):.2f} | store-drain {med(5,6):.2f} | "
+          f"exit {med(6,7):.2f} | end max {r[:,7].max():.2f} us")
