@@ -48,6 +48,22 @@ def peaks():
             "source": "fallback (B200_PROFILING.md)"}
 
 
+def gemm_traffic(config: str):
+    """DRAM bytes (read + write) of one config-3 step's GEMM launches from the
+    committed ncu capture (profiles/r01_gemm_traffic.json, tools/gemm_traffic.py;
+    cold-cache, serialised launches) next to the algorithmic FLOPs of the same
+    step; None for other workloads (not captured)."""
+    path = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
+    if config != "config3" or not os.path.exists(path):
+        return None
+    with open(path) as f:
+        t = json.load(f)
+    return {"dram_bytes_per_step": t["dram_bytes_per_step"], "launches": t["gemm_launches"],
+            "dram_bytes_per_launch": t["dram_bytes_per_launch"],
+            "algorithmic_flops_per_step": t["algorithmic_flops_per_step"],
+            "flops_per_dram_byte": t["flops_per_dram_byte"], "source": "profiles/r01_gemm_traffic.json"}
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -378,7 +394,7 @@ def run_train(args, pk):
                    "l2": "working set per step > 126 MB L2 (weights+activations ~1.5 GB); no flush"},
         "roofline": {"bound": "tensor", "achieved": gemm_tflops,
                      "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
-                     "frac": gemm_tflops / pk["bf16_tflops_sustained"], "traffic": None,
+                     "frac": gemm_tflops / pk["bf16_tflops_sustained"], "traffic": gemm_traffic(args.config),
                      "kernel": "gemm_tcgen05_kernel (all GEMM launches of one step)",
                      "gemm_ms_per_step": gemm_ms, "gemm_share_of_step": gemm_ms / ms,
                      "peak_source": pk["source"] + ", sustained"},
