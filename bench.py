@@ -355,11 +355,18 @@ def run_train(args, pk):
     from paper_2403_07544_b200 import _native
     L = _native.lib()
     _native.check(L.mm_gemm_timing(1, None, None, None), "mm_gemm_timing")
+    _native.check(L.mm_step_timing(1, None, None), "mm_step_timing")
     eng.step(n_total, [dbs[-1]])
+    eng.sync_updates()
     torch.cuda.synchronize()
     f, t_ms, n_g = ctypes.c_double(), ctypes.c_float(), ctypes.c_int()
     _native.check(L.mm_gemm_timing(0, ctypes.byref(f), ctypes.byref(t_ms), ctypes.byref(n_g)),
                   "mm_gemm_timing")
+    cat_ms, cat_n = (ctypes.c_float * 8)(), (ctypes.c_int * 8)()
+    _native.check(L.mm_step_timing(0, cat_ms, cat_n), "mm_step_timing")
+    cats = ["layernorm_fwd", "layernorm_bwd", "attention_fwd", "attention_bwd", "cross_entropy",
+            "embedding", "memset", "other"]
+    breakdown = {c: round(cat_ms[i], 4) for i, c in enumerate(cats) if cat_n[i]}
     gemm_flops, gemm_ms = f.value, t_ms.value
     gemm_tflops = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
 
@@ -397,6 +404,7 @@ def run_train(args, pk):
                      "frac": gemm_tflops / pk["bf16_tflops_sustained"], "traffic": gemm_traffic(args.config),
                      "kernel": "gemm_tcgen05_kernel (all GEMM launches of one step)",
                      "gemm_ms_per_step": gemm_ms, "gemm_share_of_step": gemm_ms / ms,
+                     "other_kernels_ms_per_step": breakdown,
                      "peak_source": pk["source"] + ", sustained"},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_value, "unit": "tok/s", "h2d_bytes_per_step": h2d // args.steps,

@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 11
+#define MMB200_ABI_VERSION 12
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 
 int mm_abi_version(void);
@@ -172,6 +172,18 @@ int mm_gemm_timing(int mode, double* flops, float* ms, int* launches);
 /* diagnostics: per-CTA %globaltimer stamps of every later mm_gemm launch into
  * dev_buf[8 * cta + slot] (NULL disables); see gemm.cu for the slots */
 int mm_gemm_trace(unsigned long long* dev_buf);
+/* Host: greedy packing of consecutive sequences into attention work groups
+ * (<= cap rows per side, 32-row aligned per sequence); out holds 2 * n_seq
+ * int32 (first, count) pairs; *foot = rows of the largest group.  Replaces
+ * the per-batch numpy loop of data.attention_groups on the step's host path. */
+int mm_attention_groups(const int32_t* cu_q, const int32_t* cu_k, int n_seq, int cap,
+                        int32_t* out, int* n_groups, int* foot);
+/* diagnostics: mode 1 starts recording CUDA events around the non-GEMM
+ * launches mm_task_fwd_bwd issues; mode 0 stops, synchronises and returns the
+ * summed time (ms) and launch count per category: 0 LayerNorm fwd, 1 LayerNorm
+ * bwd, 2 attention fwd, 3 attention bwd, 4 cross-entropy, 5 embedding,
+ * 6 memset, 7 other (8 entries each). */
+int mm_step_timing(int mode, float* ms, int* launches);
 
 /* ---------------------------------------------------------------------------
  * K6: LayerNorm over rows of x (fp32 residual stream) -> bf16, saving

@@ -19,7 +19,7 @@ if os.environ.get("MM_LIB_VARIANT"):  # diagnostics: a tuning build from tools/b
                             "libmmb200.so")
 
 #: must match MMB200_ABI_VERSION in include/mmb200.h
-ABI_VERSION = 11
+ABI_VERSION = 12
 MAX_GROUP = 8
 
 
@@ -175,6 +175,9 @@ def _declare(h: ctypes.CDLL) -> None:
     sig("mm_gemm", c_int, c_void_p, c_void_p)
     sig("mm_gemm_grouped", c_int, c_void_p, c_int, c_void_p)
     sig("mm_gemm_timing", c_int, c_int, POINTER(c_double), POINTER(c_float), POINTER(c_int))
+    sig("mm_step_timing", c_int, c_int, POINTER(c_float), POINTER(c_int))
+    sig("mm_attention_groups", c_int, c_void_p, c_void_p, c_int, c_int, c_void_p, POINTER(c_int),
+        POINTER(c_int))
     sig("mm_gemm_trace", c_int, c_void_p)
     sig("mm_layernorm_fwd", c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
         c_int64, c_int, c_float, c_void_p)

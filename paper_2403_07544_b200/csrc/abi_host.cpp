@@ -1,6 +1,7 @@
-#include <cstdlib>
 // Host-side entry points of libmmb200: version / error reporting, device
-// info and K9 (the allocator's communication-cost kernel).
+// info, K9 (the allocator's communication-cost kernel) and the attention
+// work-group packing of a micro-batch.
+#include <cstdlib>
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -102,5 +103,37 @@ extern "C" int mm_comm_cost(const double* params, int64_t n_modules, const int64
         acc += c;
     }
     *total = acc;
+    return 0;
+}
+
+// Greedy packing of consecutive sequences into attention CTA groups (the
+// host half of K5; data.attention_groups is the same algorithm in numpy and
+// the cross-check): each sequence takes ceil(len / 32) * 32 rows per side; a
+// group holds at most `cap` rows per side, a longer sequence gets a group of
+// its own.  out[2 g] = first sequence, out[2 g + 1] = count (out holds
+// 2 * n_seq entries); *foot = rows of the largest group (either side).
+extern "C" int mm_attention_groups(const int32_t* cu_q, const int32_t* cu_k, int n_seq, int cap,
+                                   int32_t* out, int* n_groups, int* foot) {
+    MM_CHECK_ARG(cu_q && cu_k && out && n_groups && foot, "NULL argument");
+    MM_CHECK_ARG(n_seq >= 0 && cap > 0, "bad sizes");
+    int g = 0, fp = 0;
+    for (int i = 0; i < n_seq;) {
+        int j = i, sq = 0, sk = 0;
+        while (j < n_seq) {
+            const int pq = (cu_q[j + 1] - cu_q[j] + 31) / 32 * 32;
+            const int pk = (cu_k[j + 1] - cu_k[j] + 31) / 32 * 32;
+            if (j != i && (sq + pq > cap || sk + pk > cap)) break;
+            sq += pq;
+            sk += pk;
+            ++j;
+        }
+        out[2 * g] = i;
+        out[2 * g + 1] = j - i;
+        ++g;
+        fp = std::max(fp, std::max(sq, sk));
+        i = j;
+    }
+    *n_groups = g;
+    *foot = fp;
     return 0;
 }

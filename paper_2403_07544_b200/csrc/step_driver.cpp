@@ -26,6 +26,36 @@
 
 namespace {
 
+// diagnostics: CUDA events around the non-GEMM launches (mm_step_timing)
+struct StepTiming {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> cat;
+    size_t used = 0;
+} g_step_timing;
+
+struct TimedScope {
+    cudaStream_t s;
+    cudaEvent_t e1 = nullptr;
+    TimedScope(int c, cudaStream_t st) : s(st) {
+        StepTiming& t = g_step_timing;
+        if (!t.on) return;
+        while (t.ev.size() < 2 * (t.used + 1)) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            t.ev.push_back(e);
+        }
+        cudaEventRecord(t.ev[2 * t.used], s);
+        e1 = t.ev[2 * t.used + 1];
+        t.cat.resize(t.used + 1);
+        t.cat[t.used] = c;
+        ++t.used;
+    }
+    ~TimedScope() {
+        if (e1) cudaEventRecord(e1, s);
+    }
+};
+
 struct Arena {
     uint8_t* base = nullptr;
     size_t off = 0, peak = 0;
@@ -39,6 +69,15 @@ struct Arena {
         return p;
     }
 };
+
+#define TIMED(c, expr)                             \
+    do {                                           \
+        if (!sizing) {                             \
+            TimedScope _ts((c), s);                \
+            int _st = (expr);                      \
+            if (_st) return _st;                   \
+        }                                          \
+    } while (0)
 
 #define TRY(expr)                    \
     do {                             \
@@ -140,7 +179,7 @@ struct Driver {
         y = ar.get<uint16_t>(T * d);
         mean = ar.get<float>(T);
         rstd = ar.get<float>(T);
-        TRY(mm_layernorm_fwd(x, wf(st, go), wf(st, bo), y, mean, rstd, T, d, 1e-6f, s));
+        TIMED(0, mm_layernorm_fwd(x, wf(st, go), wf(st, bo), y, mean, rstd, T, d, 1e-6f, s));
         return 0;
     }
 
@@ -173,7 +212,7 @@ struct Driver {
         mm_attn_args a = attn(sv.qkv, sv.qkv + d, sv.qkv + 2 * d, 3 * d, 3 * d, sv.a, sv.lse, cu, cu,
                               maxlen, maxlen, causal, int(T), groups, ng, cap);
         a.v = sv.qkv + 2 * d;
-        TRY(mm_attention_fwd(&a, s));
+        TIMED(2, mm_attention_fwd(&a, s));
         out = ar.get<float>(T * d);
         TRY(linear(sv.a, wb(st, o->out_w), out, T, d, d, MM_EPI_F32_RESID, wf(st, o->out_b), x));
         return 0;
@@ -195,7 +234,7 @@ struct Driver {
         mm_attn_args a = attn(sv.q, sv.kv, sv.kv + d, d, 2 * d, sv.a, sv.lse, b.cu_tgt, b.cu_src,
                               b.max_tgt, b.max_src, false, int(T), b.groups_cross, b.ng_cross,
                               b.cap_cross);
-        TRY(mm_attention_fwd(&a, s));
+        TIMED(2, mm_attention_fwd(&a, s));
         out = ar.get<float>(T * d);
         TRY(linear(sv.a, wb(st, o->cout_w), out, T, d, d, MM_EPI_F32_RESID, wf(st, o->cout_b), x));
         return 0;
@@ -228,7 +267,7 @@ struct Driver {
         float* dh = ar.get<float>(T * d);
         TRY(dgrad(df, wb(st, o->ff1_w), dh, T, d, F, MM_EPI_F32));
         uint16_t* nbf = next_bf(dx_bf, T);
-        TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->ln2_g), sv.mean, sv.rstd, dx, nbf,
+        TIMED(1, mm_layernorm_bwd(dh, sv.x_in, wf(st, o->ln2_g), sv.mean, sv.rstd, dx, nbf,
                              g(st, o->ln2_g), g(st, o->ln2_b), T, d, s));
         dx_bf = nbf;
         release(mark);
@@ -249,12 +288,12 @@ struct Driver {
                               maxlen, maxlen, causal, int(T), groups, ng, cap);
         a.d_o = da; a.dq = dqkv; a.dk = dqkv + d; a.dv = dqkv + 2 * d;
         a.ld_dq = a.ld_dk = a.ld_dv = 3 * d;
-        TRY(mm_attention_bwd(&a, s));
+        TIMED(3, mm_attention_bwd(&a, s));
         TRY(wgrad(dqkv, sv.h, g(st, o->qkv_w), T, d, 3 * d, g(st, o->qkv_b)));
         float* dh = ar.get<float>(T * d);
         TRY(dgrad(dqkv, wb(st, o->qkv_w), dh, T, d, 3 * d, MM_EPI_F32));
         uint16_t* nbf = next_bf(dx_bf, T);
-        TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->ln1_g), sv.mean, sv.rstd, dx, nbf,
+        TIMED(1, mm_layernorm_bwd(dh, sv.x_in, wf(st, o->ln1_g), sv.mean, sv.rstd, dx, nbf,
                              g(st, o->ln1_g), g(st, o->ln1_b), T, d, s));
         dx_bf = nbf;
         release(mark);
@@ -277,7 +316,7 @@ struct Driver {
                               b.cap_cross);
         a.d_o = da; a.dq = dq; a.dk = dkv; a.dv = dkv + d;
         a.ld_dq = d; a.ld_dk = a.ld_dv = 2 * d;
-        TRY(mm_attention_bwd(&a, s));
+        TIMED(3, mm_attention_bwd(&a, s));
         TRY(wgrad(dkv, mem, g(st, o->ckv_w), S, d, 2 * d, g(st, o->ckv_b)));
         TRY(wgrad(dq, sv.h, g(st, o->cq_w), T, d, d, g(st, o->cq_b)));
         float* dh = ar.get<float>(T * d);
@@ -287,7 +326,7 @@ struct Driver {
                                     dgrad_args(dq, wb(st, o->cq_w), dh, T, d, d, MM_EPI_F32)};
         TRY(mm_gemm_grouped(dg, 2, s));
         uint16_t* nbf = next_bf(dx_bf, T);
-        TRY(mm_layernorm_bwd(dh, sv.x_in, wf(st, o->lnc_g), sv.mean, sv.rstd, dx, nbf,
+        TIMED(1, mm_layernorm_bwd(dh, sv.x_in, wf(st, o->lnc_g), sv.mean, sv.rstd, dx, nbf,
                              g(st, o->lnc_g), g(st, o->lnc_b), T, d, s));
         dx_bf = nbf;
         release(mark);
@@ -295,7 +334,7 @@ struct Driver {
     }
 
     int zeros(void* p, size_t bytes) {
-        TRY(mm_memset(p, 0, bytes, s));
+        TIMED(6, mm_memset(p, 0, bytes, s));
         return 0;
     }
 
@@ -313,7 +352,7 @@ struct Driver {
             for (int l = 0; l < t.dec[i].n_layers; ++l) dec_l[nd++] = Layer{&t.dec[i], &t.dec[i].layers[l], {}, {}, {}};
         // ---- encoder
         float* x = ar.get<float>(Ts * d);
-        TRY(mm_embed_fwd(b.src, b.src_pos, t.enc_emb.w_bf16 + t.enc_emb.emb, x, Ts, d, scale, s));
+        TIMED(5, mm_embed_fwd(b.src, b.src_pos, t.enc_emb.w_bf16 + t.enc_emb.emb, x, Ts, d, scale, s));
         for (int l = 0; l < ne; ++l) {
             float* y;
             if (int e = self_fwd(enc_l[l], x, y, Ts, b.cu_src, b.max_src, false, b.groups_src, b.ng_src, b.cap_src)) return e;
@@ -336,7 +375,7 @@ struct Driver {
             TRY(mm_gemm_grouped(kv, nd, s));
         }
         float* y = ar.get<float>(Tt * d);
-        TRY(mm_embed_fwd(b.tgt_in, b.tgt_pos, t.dec_emb.w_bf16 + t.dec_emb.emb, y, Tt, d, scale, s));
+        TIMED(5, mm_embed_fwd(b.tgt_in, b.tgt_pos, t.dec_emb.w_bf16 + t.dec_emb.emb, y, Tt, d, scale, s));
         for (int l = 0; l < nd; ++l) {
             float *y1, *y2;
             if (int e = self_fwd(dec_l[l], y, y1, Tt, b.cu_tgt, b.max_tgt, true, b.groups_tgt, b.ng_tgt, b.cap_tgt)) return e;
@@ -350,7 +389,7 @@ struct Driver {
         const mm_embed& E = t.dec_emb;
         TRY(linear(hdec, E.w_bf16 + E.gen_w, logits, Tt, d, V, MM_EPI_BF16, E.w_f32 + E.gen_b));
         float* row_loss = ar.get<float>(Tt);
-        TRY(mm_xent_fwd_bwd(logits, b.labels, logits, row_loss, loss_sum, Tt, V, 1.f / float(Tt), s));
+        TIMED(4, mm_xent_fwd_bwd(logits, b.labels, logits, row_loss, loss_sum, Tt, V, 1.f / float(Tt), s));
         // ---- generator backward (dlogits in place of the logits)
         TRY(wgrad(logits, hdec, E.grad + E.gen_w, Tt, d, V, E.grad + E.gen_b));
         float* dh = ar.get<float>(Tt * d);
@@ -358,7 +397,7 @@ struct Driver {
         float* dy = ar.get<float>(Tt * d);
         uint16_t* dy_bf = ar.get<uint16_t>(Tt * d);
         if (int e = zeros(dy, Tt * d * 4)) return e;
-        TRY(mm_layernorm_bwd(dh, y, wf(lnf_d, lnf_d->lnf_g), hd_mean, hd_rstd, dy, dy_bf,
+        TIMED(1, mm_layernorm_bwd(dh, y, wf(lnf_d, lnf_d->lnf_g), hd_mean, hd_rstd, dy, dy_bf,
                              g(lnf_d, lnf_d->lnf_g), g(lnf_d, lnf_d->lnf_b), Tt, d, s));
         float* dmem = ar.get<float>(Ts * d);
         if (int e = zeros(dmem, Ts * d * 4)) return e;
@@ -367,26 +406,50 @@ struct Driver {
             if (int e = cross_bwd(dec_l[l], dy, dy_bf, mem, dmem)) return e;
             if (int e = self_bwd(dec_l[l], dy, dy_bf, Tt, b.cu_tgt, b.max_tgt, true, b.groups_tgt, b.ng_tgt, b.cap_tgt)) return e;
         }
-        TRY(mm_embed_bwd(b.tgt_in, dy, t.dec_emb.grad + t.dec_emb.emb, Tt, d, scale, s));
+        TIMED(5, mm_embed_bwd(b.tgt_in, dy, t.dec_emb.grad + t.dec_emb.emb, Tt, d, scale, s));
         if (int e = flush_wgrads()) return e;  // decoder side + generator
         if (dec_done && !sizing) MM_CUDA_TRY(cudaEventRecord(dec_done, s));
         // ---- encoder backward
         float* dx = ar.get<float>(Ts * d);
         uint16_t* dx_bf = ar.get<uint16_t>(Ts * d);
         if (int e = zeros(dx, Ts * d * 4)) return e;
-        TRY(mm_layernorm_bwd(dmem, x_enc, wf(lnf_e, lnf_e->lnf_g), mem_mean, mem_rstd, dx, dx_bf,
+        TIMED(1, mm_layernorm_bwd(dmem, x_enc, wf(lnf_e, lnf_e->lnf_g), mem_mean, mem_rstd, dx, dx_bf,
                              g(lnf_e, lnf_e->lnf_g), g(lnf_e, lnf_e->lnf_b), Ts, d, s));
         for (int l = ne - 1; l >= 0; --l) {
             if (int e = ffn_bwd(enc_l[l], dx, dx_bf, Ts)) return e;
             if (int e = self_bwd(enc_l[l], dx, dx_bf, Ts, b.cu_src, b.max_src, false, b.groups_src, b.ng_src, b.cap_src)) return e;
         }
-        TRY(mm_embed_bwd(b.src, dx, t.enc_emb.grad + t.enc_emb.emb, Ts, d, scale, s));
+        TIMED(5, mm_embed_bwd(b.src, dx, t.enc_emb.grad + t.enc_emb.emb, Ts, d, scale, s));
         if (int e = flush_wgrads()) return e;  // encoder side
         return 0;
     }
 };
 
 }  // namespace
+
+extern "C" int mm_step_timing(int mode, float* ms, int* launches) {
+    StepTiming& t = g_step_timing;
+    if (mode == 1) {
+        t.on = true;
+        t.used = 0;
+        return 0;
+    }
+    t.on = false;
+    for (int c = 0; c < 8; ++c) {
+        if (ms) ms[c] = 0.f;
+        if (launches) launches[c] = 0;
+    }
+    for (size_t i = 0; i < t.used; ++i) {
+        MM_CUDA_TRY(cudaEventSynchronize(t.ev[2 * i + 1]));
+        float x = 0.f;
+        MM_CUDA_TRY(cudaEventElapsedTime(&x, t.ev[2 * i], t.ev[2 * i + 1]));
+        const int c = t.cat[i] < 8 ? t.cat[i] : 7;
+        if (ms) ms[c] += x;
+        if (launches) launches[c] += 1;
+    }
+    t.used = 0;
+    return 0;
+}
 
 extern "C" int mm_task_fwd_bwd(const mm_task* task, const mm_batch* batch, void* workspace,
                                size_t* ws_bytes, float* loss_sum, void* stream, void* dec_done) {

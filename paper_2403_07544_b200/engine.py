@@ -30,7 +30,7 @@ import torch
 
 from . import _native, ops
 from .configs import ModelShape
-from .data import Batch, attention_groups
+from .data import ATTN_CAP, Batch, attention_groups
 from .domain import ClusterTopology, ModuleKey, Side, TaskSpec
 from .model import LN_EPS, ModuleState, module_layouts
 from .plan import (Multiplexer, build_plan, embedding_keys, exchange_order, ready_flags,
@@ -46,6 +46,21 @@ class AdamConfig:
     weight_decay: float = 0.0
 
 
+def native_attention_groups(cu_q: np.ndarray, cu_k: np.ndarray, cap: int = ATTN_CAP):
+    """data.attention_groups through the C ABI (mm_attention_groups): the
+    numpy loop cost ~0.12 ms per table on every step's host path."""
+    import ctypes
+    cq = np.ascontiguousarray(cu_q, dtype=np.int32)
+    ck = np.ascontiguousarray(cu_k, dtype=np.int32)
+    n = len(cq) - 1
+    out = np.empty(2 * max(n, 1), dtype=np.int32)
+    ng, foot = ctypes.c_int(), ctypes.c_int()
+    _native.check(_native.lib().mm_attention_groups(cq.ctypes.data, ck.ctypes.data, n, cap,
+                                                    out.ctypes.data, ctypes.byref(ng), ctypes.byref(foot)),
+                  "mm_attention_groups")
+    return out[:2 * ng.value], foot.value
+
+
 class DeviceBatch:
     """A packed batch resident in HBM: one H2D copy of one pinned int32 buffer
     holding the token streams, offsets and the attention work groups."""
@@ -58,7 +73,7 @@ class DeviceBatch:
         groups = {}
         for name, (cq, ck) in (("attn_src", (b.cu_src, b.cu_src)), ("attn_tgt", (b.cu_tgt, b.cu_tgt)),
                                ("attn_cross", (b.cu_tgt, b.cu_src))):
-            g, cap = attention_groups(cq, ck)
+            g, cap = native_attention_groups(cq, ck)
             arrs[name] = g
             groups[name] = (len(g) // 2, cap)
         names = list(self.FIELDS) + list(groups)

@@ -96,3 +96,22 @@ def test_comm_cost_rejects_bad_device():
     with pytest.raises(_native.MMError):
         comm_cost_kernel(np.ones(1), np.array([0, 1]), np.array([0]), np.array([5]),
                          np.array([0, 0]), 1.0, 4.0, out)
+
+
+def test_attention_groups_native_matches_numpy():
+    """mm_attention_groups (host C++, on the step's path) == data.attention_groups."""
+    import numpy as np
+    from paper_2403_07544_b200.data import attention_groups
+    from paper_2403_07544_b200.engine import native_attention_groups
+    rng = np.random.default_rng(7)
+    for trial in range(200):
+        n = int(rng.integers(0, 60))
+        hi = int(rng.choice([8, 40, 128, 256]))
+        lq = rng.integers(1, hi + 1, size=n)
+        lk = rng.integers(1, hi + 1, size=n) if trial % 2 else lq
+        cq = np.concatenate([[0], np.cumsum(lq)]).astype(np.int32)
+        ck = np.concatenate([[0], np.cumsum(lk)]).astype(np.int32)
+        for cap in (64, 128, 256):
+            g1, f1 = attention_groups(cq, ck, cap)
+            g2, f2 = native_attention_groups(cq, ck, cap)
+            assert np.array_equal(g1, g2) and f1 == f2, (trial, cap)
