@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) attn_fwd_kernel(const mm_attn_
     // the group table and sequence offsets come from the step's host upload,
     // not from the previous kernel: read them before griddepcontrol.wait
     if (threadIdx.x < 32) load_group(G, a, threadIdx.x);
-    pdl_wait();
+    pdl_wait_release();
     __syncthreads();
     uint16_t* Qs = sm;
     uint16_t* Ks = Qs + a.cap * kP;
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 2) attn_bwd_kernel(const mm_at
     __shared__ Group G;
     const int h = blockIdx.x;  // heads fastest: a group's CTAs run together and share its rows' DRAM pages
     if (threadIdx.x < 32) load_group(G, a, threadIdx.x);  // host-uploaded: before the wait
-    pdl_wait();
+    pdl_wait_release();
     ATTN_STAMP(0);
     __syncthreads();
     uint16_t* Qs = sm;

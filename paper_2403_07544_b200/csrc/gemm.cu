@@ -534,6 +534,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tc::mbar_wait(&tfull_bar[acc], acc_phase);
             tc::tc_fence_after();
+            // last tile's accumulator is final: let the dependent grid launch
+            // (its blocks sit in griddepcontrol.wait until this grid is done)
+            if (u + ncta >= g.units) pdl_trigger();
             if (warp == kEpiWarp0 && lane == 0 && local == 0) MM_TRACE(4);
             const int row0 = tm * (BM * CG) + rank * BM + lane_grp * 32;  // this warp's first row
             const int64_t row = int64_t(row0) + lane;

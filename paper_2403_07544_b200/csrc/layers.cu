@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x
                                                      const float* __restrict__ beta,
                                                      uint16_t* __restrict__ y, float* mean_out,
                                                      float* rstd_out, int64_t rows, float eps) {
-    pdl_wait();
+    pdl_wait_release();
     constexpr int V = COLS / 128;
     const int lane = threadIdx.x & 31;
     const int64_t row0 = (int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5)) * kLnRows;
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256, (COLS <= 512 ? 2 : 1)) ln_bwd_kernel(cons
                                                      const float* __restrict__ rstd, float* dx,
                                                      uint16_t* dx_bf16, float* dgamma,
                                                      float* dbeta, int64_t rows) {
-    pdl_wait();
+    pdl_wait_release();
     constexpr int V = COLS / 128;
     constexpr int R = COLS <= 512 ? kLnRows : 1;  // rows per warp batch (register budget)
     __shared__ float red_g[8][COLS];
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(256) embed_fwd_kernel(const int32_t* __restric
                                                         const uint16_t* __restrict__ table,
                                                         float* __restrict__ out, int64_t rows,
                                                         int cols, float scale) {
-    pdl_wait();
+    pdl_wait_release();
     const int lane = threadIdx.x & 31;
     const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
     if (row >= rows) return;
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(256) embed_bwd_kernel(const int32_t* __restric
                                                         const float* __restrict__ dout,
                                                         float* dtable, int64_t rows, int cols,
                                                         float scale) {
-    pdl_wait();
+    pdl_wait_release();
     const int lane = threadIdx.x & 31;
     const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
     if (row >= rows) return;
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kXentThreads) xent_kernel(const uint16_t* logi
                                                             uint16_t* dlogits, float* row_loss,
                                                             float* loss_sum, int vocab,
                                                             float grad_scale) {
-    pdl_wait();
+    pdl_wait_release();
     __shared__ float sm_m[kXentThreads / 32], sm_s[kXentThreads / 32];
     const int64_t row = blockIdx.x;
     const int label = labels[row];
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kXentThreads, 1) xent_stream_kernel(const uint
     for (int c = vocab + threadIdx.x; c < kXentSmemVocab; c += kXentThreads)
         buf0[c] = buf0[kXentSmemVocab + c] = 0xff80u;
     __syncthreads();
-    pdl_wait();
+    pdl_wait_release();
     const int64_t first = blockIdx.x, step = gridDim.x;
     if (threadIdx.x == 0 && first < rows) {
         tc::mbar_expect_tx(&bar[0], bytes);
@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(kXentThreads, 1) xent_stream_kernel(const uint
 // row lanes in smem and leave with one atomic per column.
 __global__ void __launch_bounds__(256) colsum_kernel(const uint16_t* __restrict__ x, float* out,
                                                      int64_t rows, int cols, int64_t slab) {
-    pdl_wait();
+    pdl_wait_release();
     __shared__ float red[8][256 + 8];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int c8 = blockIdx.x * 32 + tx;
@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(256) colsum_kernel(const uint16_t* __restrict_
 }
 
 __global__ void cast_kernel(const float* __restrict__ x, uint16_t* __restrict__ y, int64_t n4) {
-    pdl_wait();
+    pdl_wait_release();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4;
          i += int64_t(gridDim.x) * blockDim.x) {
         const float4 v = reinterpret_cast<const float4*>(x)[i];

@@ -69,6 +69,15 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// Small memory-bound kernels release their dependent right after their own
+// wait: the next kernel (typically a GEMM, one 225 KB CTA per SM) then gets
+// its CTAs resident beside this grid's blocks and runs its prologue (barrier
+// init, TMEM allocation, descriptor prefetch, weight-tile prefetch) before
+// its griddepcontrol.wait -- which still waits for this whole grid.
+__device__ __forceinline__ void pdl_wait_release() {
+    pdl_wait();
+    pdl_trigger();
+}
 #endif
 
 #define MM_CHECK_ARG(cond, ...)              \
