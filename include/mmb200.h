@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 12
+#define MMB200_ABI_VERSION 13
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 
 int mm_abi_version(void);
@@ -137,7 +137,14 @@ enum {
     MM_EPI_F32 = 2,         /* D_f32 = acc (+bias) */
     MM_EPI_F32_ACCUM = 3,   /* D_f32 += acc */
     MM_EPI_F32_RESID = 4,   /* D_f32 = resid_f32 + acc + bias (resid may alias D) */
-    MM_EPI_BF16_DRELU = 5   /* D_bf16 = acc * (aux_bf16 > 0) */
+    MM_EPI_BF16_DRELU = 5,  /* D_bf16 = acc * (aux_bf16 > 0) */
+    /* D_f32 = resid + acc + bias, then the following LayerNorm of every row of
+     * D: ln_out_bf16 = (D - mean) * rstd * ln_gamma + ln_beta, ln_mean / ln_rstd
+     * per row.  N in {512, 1024}: the N / 128 CTAs of a thread-block cluster
+     * each own 128 columns of a row block and exchange per-row partial sums
+     * through distributed shared memory (replaces mm_layernorm_fwd after a
+     * residual GEMM).  K-major A and B, single (non-grouped) launches. */
+    MM_EPI_F32_RESID_LN = 6
 };
 
 typedef struct {
@@ -158,6 +165,13 @@ typedef struct {
     /* optional: dbias[m] += sum_k A[m, k] (the bias gradient of a wgrad
      * dW = dY^T X, whose A operand is dY); requires MN-major A */
     float* dbias;
+    /* MM_EPI_F32_RESID_LN: LayerNorm parameters and outputs (row stride n) */
+    const float* ln_gamma;
+    const float* ln_beta;
+    void* ln_out;       /* bf16 [M, N] */
+    float* ln_mean;     /* [M] */
+    float* ln_rstd;     /* [M] */
+    float ln_eps;
 } mm_gemm_args;
 
 int mm_gemm(const mm_gemm_args* args, void* stream);

@@ -70,7 +70,7 @@ constexpr int kSmemLimit = 232448;
 // CG = CTAs per MMA: 1, or 2 for a CTA pair (cta_group::2) computing a
 // (2*BM) x BN tile -- each CTA holds its BM rows of A and BN/2 rows of B, so
 // per-SM shared-memory traffic per MMA drops by a quarter (BN=128) to a half.
-template <int BN, int CG>
+template <int BN, int CG, int CN = 1>
 struct Cfg {
     static constexpr int kBRows = BN / CG;             // B rows (N) staged by one CTA
     static constexpr int kABytes = BM * BK * 2;
@@ -78,13 +78,16 @@ struct Cfg {
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kTxBytes = kStageBytes * CG;  // bytes counted on the MMA CTA's barrier
     static constexpr int kBarBytes = 512;
-    static constexpr int kStagesFit = (kSmemLimit - kEpiSmem - 1024 - kBarBytes) / kStageBytes;
+    // fused LayerNorm (cluster of CN CTAs along N): per-row partials of the two
+    // column halves [2][BM] and the CTA's exchanged row sums [2 parities][BM]
+    static constexpr int kLnBytes = CN > 1 ? 4 * BM * 8 : 0;  // float2 [2][BM] x 2
+    static constexpr int kStagesFit = (kSmemLimit - kEpiSmem - 1024 - kBarBytes - kLnBytes) / kStageBytes;
     static constexpr int kStages = kStagesFit > MM_GEMM_MAX_STAGES ? MM_GEMM_MAX_STAGES : kStagesFit;
     static constexpr int kTmemCols = BN == 128 ? 256 : 512;  // 2 accumulators, power of 2
-    static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 + kBarBytes;
+    static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 + kBarBytes + kLnBytes;
     static_assert(kSmem <= kSmemLimit, "smem budget");
     static_assert(CG == 1 || kBRows % 64 == 0, "pair tiles need 64-aligned B halves");
-    static_assert((3 * kStages + 4) * 8 + 4 <= kBarBytes, "barrier area");
+    static_assert((3 * kStages + 6) * 8 + 4 <= kBarBytes, "barrier area");
 };
 
 // One GEMM problem of a launch: its three tensor maps (A, B, D) and its slice
@@ -106,8 +109,18 @@ struct alignas(64) Prob {
 // A launch: NP = 1 for a plain GEMM, kMaxProbs for a grouped launch (all
 // problems share the operand majorness and the tile width; units of all
 // problems are dealt to the persistent CTAs from one list).
+// the fused LayerNorm of a MM_EPI_F32_RESID_LN launch (single problem)
+struct alignas(64) LnParams {
+    CUtensorMap th;  // LayerNorm output (bf16 [M, N])
+    const float* gamma;
+    const float* beta;
+    float* mean;
+    float* rstd;
+    float eps;
+};
 template <int NP>
 struct Group {
+    LnParams ln;
     Prob prob[NP];
     unsigned long long* trace;  // optional per-CTA phase timestamps (diagnostics)
     int n_probs;
@@ -116,7 +129,8 @@ struct Group {
     int any_dbias;  // some problem fuses bias-gradient column sums (bias warp active)
 };
 // diagnostics build (tools/build_variant.py -DMM_GEMM_DEBUG=bits): bit 0 skip
-// MMAs, bit 1 skip epilogue stores, bit 2 skip loads
+// MMAs, bit 1 skip epilogue stores, bit 2 skip loads, bit 3 LayerNorm without the
+// cluster exchange, bit 4 no LayerNorm epilogue at all
 #ifndef MM_GEMM_DEBUG
 #define MM_GEMM_DEBUG 0
 #endif
@@ -161,7 +175,7 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 __device__ __forceinline__ bool has_bias(const Prob& p) {
     const int ep = p.epilogue;
     return p.bias && (ep == MM_EPI_BF16 || ep == MM_EPI_BF16_RELU || ep == MM_EPI_F32 ||
-                      ep == MM_EPI_F32_RESID);
+                      ep == MM_EPI_F32_RESID || ep == MM_EPI_F32_RESID_LN);
 }
 
 // bv: this lane's bias value for column col0 + lane (preloaded per tile)
@@ -199,7 +213,7 @@ __device__ __forceinline__ void epilogue_math(const Prob& p, int64_t row, int64_
                 if (col0 + j < p.n && bf16_to_f(aux[j]) <= 0.f) acc[j] = 0.f;
         }
     }
-    if (ep == MM_EPI_F32_RESID) {
+    if (ep == MM_EPI_F32_RESID || ep == MM_EPI_F32_RESID_LN) {
         const float* res = p.resid + row * p.ldd + col0;
         if (full) {
 #pragma unroll
@@ -246,6 +260,18 @@ __device__ __forceinline__ void stage_row(uint8_t* buf, int r, const float (&acc
 struct Unit {
     int pi, tm, tn, kb0, kb1;
 };
+// CN > 1 (fused LayerNorm): a unit is a 128-row block, the CN CTAs of a
+// cluster take its N-tiles (cluster rank = N-tile), full K
+template <int NP>
+__device__ __forceinline__ Unit decode_cluster(const Group<NP>& g, int u, int crank) {
+    Unit w;
+    w.pi = 0;
+    w.tm = u;
+    w.tn = crank;
+    w.kb0 = 0;
+    w.kb1 = g.prob[0].num_kb;
+    return w;
+}
 template <int NP>
 __device__ __forceinline__ Unit decode(const Group<NP>& g, int u) {
     int pi = 0;
@@ -266,10 +292,11 @@ __device__ __forceinline__ Unit decode(const Group<NP>& g, int u) {
     return w;
 }
 
-template <int BN, int A_MN, int B_MN, int NP, int CG>
+template <int BN, int A_MN, int B_MN, int NP, int CG, int CN = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ Group<NP> g) {
-    using C = Cfg<BN, CG>;
+    using C = Cfg<BN, CG, CN>;
+    static_assert(CN == 1 || (CG == 1 && NP == 1), "LayerNorm clusters: single CTAs, one problem");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -281,7 +308,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* bias_bar = empty_bar + C::kStages;  // pair: "stage consumed by the MMA" for the bias warp
     uint64_t* tfull_bar = bias_bar + C::kStages;
     uint64_t* tempty_bar = tfull_bar + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    uint64_t* xch_bar = tempty_bar + 2;  // CN > 1: row-sum exchange, one per parity
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xch_bar + 2);
+    float* ln_part = reinterpret_cast<float*>(smem_epi + kEpiSmem + C::kBarBytes);  // [2][BM]
+    float* ln_xch = ln_part + 4 * BM;                                                // float2 [2][BM]
 
     // warp index through a shuffle: ptxas then knows it is warp-uniform, so
     // the role branches below are uniform and their loop state (stage, phase,
@@ -290,6 +320,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lane = threadIdx.x & 31;
     // pair rank: 0 = leader (issues the MMAs, owns the stage-full barriers)
     const uint32_t rank = CG == 2 ? tc::cluster_ctarank() : 0u;
+    const int crank = CN > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;  // N-tile of a LN cluster
+    auto unit_at = [&](int u) -> Unit {
+        if constexpr (CN > 1) return decode_cluster(g, u, crank);
+        else return decode(g, u);
+    };
     const bool dbias_any = g.any_dbias != 0;
     if (threadIdx.x == 0) MM_TRACE(0);
 
@@ -309,6 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int a = 0; a < 2; ++a) {
             tc::mbar_init(&tfull_bar[a], 1);
             tc::mbar_init(&tempty_bar[a], CG * kEpiWarps);  // one arrive per epilogue warp of the pair
+            tc::mbar_init(&xch_bar[a], CN);                 // one arrive per CTA of the LN cluster
         }
         tc::fence_barrier_init();
     }
@@ -317,10 +353,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         else tc::tmem_alloc(tmem_slot, C::kTmemCols);
     }
     tc::tc_fence_before();
-    if constexpr (CG == 2) tc::cluster_sync();  // peer barriers initialised before any remote signal
+    if constexpr (CG == 2 || CN > 1) tc::cluster_sync();  // peer barriers initialised before any remote signal
     else __syncthreads();
     tc::tc_fence_after();
-    const int cid = blockIdx.x / CG, ncta = gridDim.x / CG;  // units are dealt per pair
+    // units are dealt per pair (CG = 2) or per LayerNorm cluster (CN > 1)
+    const int cid = blockIdx.x / (CG * CN), ncta = gridDim.x / (CG * CN);
     const uint32_t tmem_base = *tmem_slot;
     if (tmem_base != 0) __trap();  // the MMA issuer addresses TMEM by column offset
     if (threadIdx.x == 0) MM_TRACE(1);
@@ -362,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // B stages of the first unit that do not depend on the previous kernel
             int pre = 0;
             if (g.b_prefetch && cid < g.units && !(MM_GEMM_DEBUG & 4)) {
-                const Unit w = decode(g, cid);
+                const Unit w = unit_at(cid);
                 const Prob& P = g.prob[w.pi];
                 pre = min(C::kStages, w.kb1 - w.kb0);
                 for (int i = 0; i < pre; ++i) {
@@ -375,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int issued = 0;
             for (int u = cid; u < g.units; u += ncta) {
-                const Unit w = decode(g, u);
+                const Unit w = unit_at(u);
                 const Prob& P = g.prob[w.pi];
                 const int m0 = w.tm * (BM * CG) + rank * BM, n0 = w.tn * BN + rank * C::kBRows;
                 for (int kb = w.kb0; kb < w.kb1; ++kb, ++issued) {
@@ -422,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int local = 0;
         int consumed = 0;
         for (int u = cid; u < g.units && rank == 0; u += ncta, ++local) {
-            const Unit w = decode(g, u);
+            const Unit w = unit_at(u);
             const int kb0 = w.kb0, kb1 = w.kb1;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
@@ -468,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int stage = 0;
         uint32_t phase = 0;
         for (int u = cid; u < g.units; u += ncta) {
-            const Unit w = decode(g, u);
+            const Unit w = unit_at(u);
             const Prob& P = g.prob[w.pi];
             const int kb0 = w.kb0, kb1 = w.kb1, tn = w.tn;
             float* dbias = P.dbias;
@@ -514,8 +551,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* bufs = smem_epi + (warp - kEpiWarp0) * kEpiBufs * kEpiBufBytes;
         int nbuf = 0;
         int local = 0;
+        int ln_round = 0;  // CN > 1: row-sum exchanges so far (two per tile)
         for (int u = cid; u < g.units; u += ncta, ++local) {
-            const Unit w = decode(g, u);
+            const Unit w = unit_at(u);
             const Prob& P = g.prob[w.pi];
             const bool out_bf16 = P.epilogue == MM_EPI_BF16 || P.epilogue == MM_EPI_BF16_RELU ||
                                   P.epilogue == MM_EPI_BF16_DRELU;
@@ -542,6 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t row = int64_t(row0) + lane;
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) + acc * BN +
                                    half * (BN / kSlices);
+            float xs[CN > 1 ? kChunks : 1][32];  // LayerNorm input kept in registers
 #pragma unroll
             for (int c = 0; c < kChunks; ++c) {
                 const int col0 = cbase + c * 32;
@@ -553,6 +592,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
                     epilogue_math(P, row, col0, f, bv[c]);
+                    if constexpr (CN > 1) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) xs[c][j] = f[j];
+                    }
                     uint8_t* buf = bufs + nbuf * kEpiBufBytes;
                     if (lane == 0) tc::bulk_wait_read<kEpiBufs - 1>();  // the store that last read `buf` is done
                     __syncwarp();
@@ -574,6 +617,88 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if constexpr (CG == 2) tc::mbar_arrive_cluster(&tempty_bar[acc], 0);
                 else tc::mbar_arrive(&tempty_bar[acc]);
             }
+            if constexpr (CN > 1 && !(MM_GEMM_DEBUG & 16)) {
+                // ---- fused LayerNorm of the rows just written (x = resid + acc
+                // + bias).  Each CTA of the cluster holds 128 of the row's
+                // N = CN * 128 columns: per-row partial sums go through
+                // distributed shared memory, summed in cluster-rank order so
+                // every CTA normalises with identical statistics.
+                const int rloc = lane_grp * 32 + lane;  // row within the tile
+                // one exchange per tile: (sum x, sum x^2) per row; var =
+                // E[x^2] - mean^2 in fp32 (the residual stream's |mean| is a
+                // few sigma at most, so the cancellation costs < 1e-5 relative)
+                auto row_totals = [&](float v1, float v2) -> float2 {
+                    if constexpr (MM_GEMM_DEBUG & 8) return make_float2(v1 * CN, v2 * CN);  // no exchange
+                    float2* part2 = reinterpret_cast<float2*>(ln_part);  // [2][BM]
+                    float2* xch2 = reinterpret_cast<float2*>(ln_xch);    // [2][BM]
+                    part2[half * BM + rloc] = make_float2(v1, v2);
+                    tc::named_barrier_sync(1, kEpiWarps * 32);
+                    const int par = ln_round & 1;
+                    if (half == 0) {
+                        const float2 a0 = part2[rloc], a1 = part2[BM + rloc];
+                        xch2[par * BM + rloc] = make_float2(a0.x + a1.x, a0.y + a1.y);
+                    }
+                    tc::named_barrier_sync(1, kEpiWarps * 32);
+                    if (threadIdx.x == kEpiWarp0 * 32) {
+#pragma unroll
+                        for (int r = 0; r < CN; ++r) tc::mbar_arrive_cluster(&xch_bar[par], r);
+                    }
+                    tc::mbar_spin_cluster(&xch_bar[par], (ln_round >> 1) & 1);
+                    ++ln_round;
+                    const uint32_t slot = tc::smem_u32(&xch2[par * BM + rloc]);
+                    float2 t = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int r = 0; r < CN; ++r) {
+                        const float2 q = tc::ld_shared_cluster_f32x2(tc::mapa_u32(slot, r));
+                        t.x += q.x;
+                        t.y += q.y;
+                    }
+                    return t;
+                };
+                float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+                for (int c = 0; c < kChunks; ++c)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        s1 += xs[c][j];
+                        s2 = fmaf(xs[c][j], xs[c][j], s2);
+                    }
+                const float inv_n = 1.f / static_cast<float>(P.n);
+                const float2 tot = row_totals(s1, s2);
+                const float mu = tot.x * inv_n;
+                const float var = fmaxf(tot.y * inv_n - mu * mu, 0.f);
+                const float rs = rsqrtf(var + g.ln.eps);
+#pragma unroll
+                for (int c = 0; c < kChunks; ++c) {
+                    const int col0 = cbase + c * 32;
+                    float hv[32];
+                    const float4* g4 = reinterpret_cast<const float4*>(g.ln.gamma + col0);
+                    const float4* b4 = reinterpret_cast<const float4*>(g.ln.beta + col0);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {  // warp-uniform addresses: broadcast loads
+                        const float4 gg = __ldg(g4 + q), bb = __ldg(b4 + q);
+                        hv[4 * q + 0] = (xs[c][4 * q + 0] - mu) * rs * gg.x + bb.x;
+                        hv[4 * q + 1] = (xs[c][4 * q + 1] - mu) * rs * gg.y + bb.y;
+                        hv[4 * q + 2] = (xs[c][4 * q + 2] - mu) * rs * gg.z + bb.z;
+                        hv[4 * q + 3] = (xs[c][4 * q + 3] - mu) * rs * gg.w + bb.w;
+                    }
+                    uint8_t* buf = bufs + nbuf * kEpiBufBytes;
+                    if (lane == 0) tc::bulk_wait_read<kEpiBufs - 1>();
+                    __syncwarp();
+                    stage_row(buf, lane, hv, true);
+                    tc::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tc::tma_store_2d(&g.ln.th, buf, col0, row0);
+                        tc::bulk_commit();
+                    }
+                    if (++nbuf == kEpiBufs) nbuf = 0;
+                }
+                if (crank == 0 && half == 0 && row < P.m) {
+                    g.ln.mean[row] = mu;
+                    g.ln.rstd[row] = rs;
+                }
+            }
         }
         if (warp == kEpiWarp0 && lane == 0) MM_TRACE(5);
         // the CTA may exit once its staging boxes have been READ: the global
@@ -585,7 +710,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     pdl_trigger();
     tc::tc_fence_before();
-    if constexpr (CG == 2) tc::cluster_sync();  // both CTAs done with the pair's TMEM / barriers
+    // pair: both CTAs done with the pair's TMEM / barriers; LN cluster: no peer
+    // still reads this CTA's exchange slots
+    if constexpr (CG == 2 || CN > 1) tc::cluster_sync();
     else __syncthreads();
     if (warp == 1) {
         tc::tc_fence_after();
@@ -638,19 +765,20 @@ int make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, i
     return 0;
 }
 
-template <int BN, int A_MN, int B_MN, int NP, int CG>
+template <int BN, int A_MN, int B_MN, int NP, int CG, int CN = 1>
 int launch(const Group<NP>& g, cudaStream_t s) {
-    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, NP, CG>;
+    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, NP, CG, CN>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg<BN, CG>::kSmem));
+                                         Cfg<BN, CG, CN>::kSmem));
         attr_set = true;
     }
-    // persistent: one CTA (pair) per SM (pair of SMs)
-    const int ctas = std::min(g.units, mm::num_sms() / CG) * CG;
-    MM_CUDA_TRY(mm::launch_pdl_cluster(kern, dim3(ctas), dim3(kThreads), Cfg<BN, CG>::kSmem, s,
-                                       static_cast<unsigned>(CG), g));
+    // persistent: one CTA (pair / LayerNorm cluster) per SM (pair / CN SMs)
+    const int per = CG * CN;
+    const int ctas = std::min(g.units, mm::num_sms() / per) * per;
+    MM_CUDA_TRY(mm::launch_pdl_cluster(kern, dim3(ctas), dim3(kThreads), Cfg<BN, CG, CN>::kSmem, s,
+                                       static_cast<unsigned>(per), g));
     MM_LAUNCH_CHECK("gemm_tcgen05_kernel");
     return 0;
 }
@@ -681,7 +809,18 @@ int check_args(const mm_gemm_args* a) {
     MM_CHECK_ARG(a != nullptr, "args is NULL");
     MM_CHECK_ARG(a->m > 0 && a->n > 0 && a->k > 0, "empty GEMM %lldx%lldx%lld", (long long)a->m,
                  (long long)a->n, (long long)a->k);
-    MM_CHECK_ARG(a->epilogue >= MM_EPI_BF16 && a->epilogue <= MM_EPI_BF16_DRELU, "bad epilogue");
+    MM_CHECK_ARG(a->epilogue >= MM_EPI_BF16 && a->epilogue <= MM_EPI_F32_RESID_LN, "bad epilogue");
+    if (a->epilogue == MM_EPI_F32_RESID_LN) {
+        MM_CHECK_ARG(a->n == 512 || a->n == 1024, "fused LayerNorm needs N in {512, 1024} (got %lld)",
+                     (long long)a->n);
+        MM_CHECK_ARG(a->a_kmajor && a->b_kmajor, "fused LayerNorm needs K-major A and B");
+        MM_CHECK_ARG(a->ln_gamma && a->ln_beta && a->ln_out && a->ln_mean && a->ln_rstd,
+                     "fused LayerNorm needs gamma, beta, out, mean and rstd");
+        MM_CHECK_ARG((reinterpret_cast<uintptr_t>(a->ln_out) & 15) == 0 &&
+                         (reinterpret_cast<uintptr_t>(a->ln_gamma) & 15) == 0 &&
+                         (reinterpret_cast<uintptr_t>(a->ln_beta) & 15) == 0,
+                     "LayerNorm tensors must be 16-byte aligned");
+    }
     MM_CHECK_ARG(a->a && a->b && a->d, "NULL operand");
     const bool out_bf16 = out_bf16_epi(a->epilogue);
     MM_CHECK_ARG((a->lda % 8) == 0 && (a->ldb % 8) == 0, "lda/ldb must be multiples of 8");
@@ -690,7 +829,8 @@ int check_args(const mm_gemm_args* a) {
                  "A/B must be 16-byte aligned");
     MM_CHECK_ARG((reinterpret_cast<uintptr_t>(a->d) & 15) == 0 && (a->ldd % (out_bf16 ? 8 : 4)) == 0,
                  "D must be 16-byte aligned with 16-byte row stride");
-    MM_CHECK_ARG(a->epilogue != MM_EPI_F32_RESID || a->resid, "RESID epilogue needs resid");
+    MM_CHECK_ARG((a->epilogue != MM_EPI_F32_RESID && a->epilogue != MM_EPI_F32_RESID_LN) || a->resid,
+                 "RESID epilogue needs resid");
     MM_CHECK_ARG(a->epilogue != MM_EPI_BF16_DRELU || a->aux, "DRELU epilogue needs aux");
     MM_CHECK_ARG(a->dbias == nullptr || !a->a_kmajor, "dbias needs an MN-major A operand");
     MM_CHECK_ARG(a->m < (int64_t(1) << 31) && a->n < (int64_t(1) << 31) && a->k < (int64_t(1) << 31),
@@ -830,9 +970,10 @@ int split_cap(const mm_gemm_args* const* probs, int n, int bn, int cg, int sms) 
 template <int NP>
 int run_group(const mm_gemm_args* const* probs, int n, cudaStream_t s) {
     const int sms = mm::num_sms();
-    const TileChoice tc = choose_tile(probs, n, sms);
+    const bool ln = probs[0]->epilogue == MM_EPI_F32_RESID_LN;
+    const TileChoice tc = ln ? TileChoice{128, 1} : choose_tile(probs, n, sms);
     const int bn = tc.bn, cg = tc.cg;
-    const int cap = split_cap(probs, n, bn, cg, sms);
+    const int cap = ln ? 1 : split_cap(probs, n, bn, cg, sms);
     static Group<NP> g;  // host staging of the kernel parameter (large: tensor maps)
     std::memset(&g, 0, sizeof(g));
     int64_t units = 0;
@@ -878,7 +1019,21 @@ int run_group(const mm_gemm_args* const* probs, int n, cudaStream_t s) {
     const int a_mn = probs[0]->a_kmajor ? 0 : 1;
     const int b_mn = probs[0]->b_kmajor ? 0 : 1;
     int rc;
-    if (cg == 2) {
+    if (ln) {
+        // units are 128-row blocks; a cluster of N / 128 CTAs shares each one
+        const mm_gemm_args* a = probs[0];
+        if (int st = make_map(&g.ln.th, a->ln_out, a->n, a->m, a->n, 32, 32, false,
+                              CU_TENSOR_MAP_SWIZZLE_64B))
+            return st;
+        g.ln.gamma = a->ln_gamma; g.ln.beta = a->ln_beta;
+        g.ln.mean = a->ln_mean; g.ln.rstd = a->ln_rstd; g.ln.eps = a->ln_eps;
+        g.units = g.prob[0].tiles_m;
+        if constexpr (NP == 1) {
+            rc = g.prob[0].tiles_n == 4 ? launch<128, 0, 0, 1, 1, 4>(g, s) : launch<128, 0, 0, 1, 1, 8>(g, s);
+        } else {
+            rc = mm::kArg;
+        }
+    } else if (cg == 2) {
         if (bn == 256) rc = dispatch<256, NP, 2>(a_mn, b_mn, g, s);
         else rc = dispatch<128, NP, 2>(a_mn, b_mn, g, s);
     } else {
@@ -932,6 +1087,7 @@ extern "C" int mm_gemm_grouped(const mm_gemm_args* probs, int n, void* stream) {
     if (n == 0) return 0;
     for (int i = 0; i < n; ++i) {
         if (int st = check_args(&probs[i])) return st;
+        MM_CHECK_ARG(probs[i].epilogue != MM_EPI_F32_RESID_LN, "fused LayerNorm GEMMs are not grouped");
         MM_CHECK_ARG(probs[i].a_kmajor == probs[0].a_kmajor && probs[i].b_kmajor == probs[0].b_kmajor,
                      "grouped GEMM: problem %d operand majorness differs from problem 0", i);
     }

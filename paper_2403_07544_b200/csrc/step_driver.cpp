@@ -91,6 +91,11 @@ struct SelfSave { const float* x_in; uint16_t* h; float* mean; float* rstd; uint
 struct CrossSave { const float* x_in; uint16_t* h; float* mean; float* rstd; uint16_t* q; uint16_t* kv; uint16_t* a; float* lse; };
 struct FfnSave { const float* x_in; uint16_t* h; float* mean; float* rstd; uint16_t* f; };
 
+// A LayerNorm's outputs (bf16 normalised rows + per-row statistics), and the
+// parameters of the LayerNorm that follows a residual GEMM
+struct LnOut { uint16_t* h = nullptr; float* mean = nullptr; float* rstd = nullptr; };
+struct LnNext { const mm_stack* st = nullptr; int64_t g = -1, b = -1; };
+
 struct Layer {
     const mm_stack* st;
     const mm_layer_offsets* o;
@@ -128,6 +133,47 @@ struct Driver {
         const mm_gemm_args a = make_args(A, a_k, B, b_k, D, m, n, k, lda, ldb, ldd, epi, bias, resid, aux, dbias);
         return mm_gemm(&a, s);
     }
+    // out[T,d] = resid + X W^T + bias; with `next`, the following LayerNorm of
+    // out is computed in the GEMM epilogue (MM_EPI_F32_RESID_LN, a cluster of
+    // d / 128 CTAs per row block) into *ln_out -- no separate LayerNorm pass
+    bool fuse_ln = true;
+    int residual(const uint16_t* X, const uint16_t* W, float* out, int64_t T, int64_t in,
+                 const float* bias, const float* resid, const LnNext* next, LnOut* ln_out) {
+        if (next && next->st) {
+            ln_out->h = ar.get<uint16_t>(T * d);
+            ln_out->mean = ar.get<float>(T);
+            ln_out->rstd = ar.get<float>(T);
+            if (fuse_ln && (d == 512 || d == 1024)) {
+                mm_gemm_args a = make_args(X, true, W, true, out, T, d, in, in, in, d, MM_EPI_F32_RESID_LN,
+                                           bias, resid);
+                a.ln_gamma = wf(next->st, next->g);
+                a.ln_beta = wf(next->st, next->b);
+                a.ln_out = ln_out->h;
+                a.ln_mean = ln_out->mean;
+                a.ln_rstd = ln_out->rstd;
+                a.ln_eps = 1e-6f;
+                TRY(mm_gemm(&a, s));
+                return 0;
+            }
+            TRY(linear(X, W, out, T, in, d, MM_EPI_F32_RESID, bias, resid));
+            TIMED(0, mm_layernorm_fwd(out, wf(next->st, next->g), wf(next->st, next->b), ln_out->h,
+                                      ln_out->mean, ln_out->rstd, T, d, 1e-6f, s));
+            return 0;
+        }
+        TRY(linear(X, W, out, T, in, d, MM_EPI_F32_RESID, bias, resid));
+        return 0;
+    }
+    // the block's input LayerNorm: already produced by the previous residual
+    // GEMM (pre), or computed here
+    int ln_in(const mm_stack* st, int64_t go, int64_t bo, const float* x, int64_t T, const LnOut* pre,
+              uint16_t*& h, float*& mean, float*& rstd) {
+        if (pre && pre->h) {
+            h = pre->h; mean = pre->mean; rstd = pre->rstd;
+            return 0;
+        }
+        return ln(st, go, bo, x, T, h, mean, rstd);
+    }
+
     // dX[T,in] (epi)= dY[T,out] W[out,in] as a problem of a grouped launch
     static mm_gemm_args dgrad_args(const uint16_t* dY, const uint16_t* W, void* dX, int64_t T, int64_t in,
                                    int64_t out, int epi) {
@@ -199,12 +245,13 @@ struct Driver {
 
     // ------------------------------------------------------------ forward
     int self_fwd(Layer& L, const float* x, float*& out, int64_t T, const int32_t* cu, int maxlen,
-                 bool causal, const int32_t* groups, int ng, int cap) {
+                 bool causal, const int32_t* groups, int ng, int cap, const LnOut* pre,
+                 const LnNext* next, LnOut* ln_out) {
         const mm_stack* st = L.st;
         const mm_layer_offsets* o = L.o;
         SelfSave& sv = L.self;
         sv.x_in = x;
-        if (int e = ln(st, o->ln1_g, o->ln1_b, x, T, sv.h, sv.mean, sv.rstd)) return e;
+        if (int e = ln_in(st, o->ln1_g, o->ln1_b, x, T, pre, sv.h, sv.mean, sv.rstd)) return e;
         sv.qkv = ar.get<uint16_t>(T * 3 * d);
         TRY(linear(sv.h, wb(st, o->qkv_w), sv.qkv, T, d, 3 * d, MM_EPI_BF16, wf(st, o->qkv_b)));
         sv.a = ar.get<uint16_t>(T * d);
@@ -214,17 +261,18 @@ struct Driver {
         a.v = sv.qkv + 2 * d;
         TIMED(2, mm_attention_fwd(&a, s));
         out = ar.get<float>(T * d);
-        TRY(linear(sv.a, wb(st, o->out_w), out, T, d, d, MM_EPI_F32_RESID, wf(st, o->out_b), x));
+        if (int e = residual(sv.a, wb(st, o->out_w), out, T, d, wf(st, o->out_b), x, next, ln_out)) return e;
         return 0;
     }
 
-    int cross_fwd(Layer& L, const float* x, float*& out, const uint16_t* mem) {
+    int cross_fwd(Layer& L, const float* x, float*& out, const uint16_t* mem, const LnOut* pre,
+                  const LnNext* next, LnOut* ln_out) {
         const mm_stack* st = L.st;
         const mm_layer_offsets* o = L.o;
         CrossSave& sv = L.cross;
         const int64_t T = b.n_tgt, S = b.n_src;
         sv.x_in = x;
-        if (int e = ln(st, o->lnc_g, o->lnc_b, x, T, sv.h, sv.mean, sv.rstd)) return e;
+        if (int e = ln_in(st, o->lnc_g, o->lnc_b, x, T, pre, sv.h, sv.mean, sv.rstd)) return e;
         sv.q = ar.get<uint16_t>(T * d);
         TRY(linear(sv.h, wb(st, o->cq_w), sv.q, T, d, d, MM_EPI_BF16, wf(st, o->cq_b)));
         // sv.kv: computed for every decoder layer in one grouped launch (kv_all)
@@ -236,20 +284,21 @@ struct Driver {
                               b.cap_cross);
         TIMED(2, mm_attention_fwd(&a, s));
         out = ar.get<float>(T * d);
-        TRY(linear(sv.a, wb(st, o->cout_w), out, T, d, d, MM_EPI_F32_RESID, wf(st, o->cout_b), x));
+        if (int e = residual(sv.a, wb(st, o->cout_w), out, T, d, wf(st, o->cout_b), x, next, ln_out)) return e;
         return 0;
     }
 
-    int ffn_fwd(Layer& L, const float* x, float*& out, int64_t T) {
+    int ffn_fwd(Layer& L, const float* x, float*& out, int64_t T, const LnOut* pre, const LnNext* next,
+                LnOut* ln_out) {
         const mm_stack* st = L.st;
         const mm_layer_offsets* o = L.o;
         FfnSave& sv = L.ffn;
         sv.x_in = x;
-        if (int e = ln(st, o->ln2_g, o->ln2_b, x, T, sv.h, sv.mean, sv.rstd)) return e;
+        if (int e = ln_in(st, o->ln2_g, o->ln2_b, x, T, pre, sv.h, sv.mean, sv.rstd)) return e;
         sv.f = ar.get<uint16_t>(T * F);
         TRY(linear(sv.h, wb(st, o->ff1_w), sv.f, T, d, F, MM_EPI_BF16_RELU, wf(st, o->ff1_b)));
         out = ar.get<float>(T * d);
-        TRY(linear(sv.f, wb(st, o->ff2_w), out, T, F, d, MM_EPI_F32_RESID, wf(st, o->ff2_b), x));
+        if (int e = residual(sv.f, wb(st, o->ff2_w), out, T, F, wf(st, o->ff2_b), x, next, ln_out)) return e;
         return 0;
     }
 
@@ -353,14 +402,22 @@ struct Driver {
         // ---- encoder
         float* x = ar.get<float>(Ts * d);
         TIMED(5, mm_embed_fwd(b.src, b.src_pos, t.enc_emb.w_bf16 + t.enc_emb.emb, x, Ts, d, scale, s));
+        // every LayerNorm after a residual GEMM is fused into that GEMM: the
+        // block's LN1 / LN2 / final LN outputs flow as LnOut between blocks
+        const mm_stack* lnf_e = &t.enc[t.n_enc - 1];
+        LnOut pre;  // LN1 of layer 0 runs standalone (its input is the embedding)
         for (int l = 0; l < ne; ++l) {
             float* y;
-            if (int e = self_fwd(enc_l[l], x, y, Ts, b.cu_src, b.max_src, false, b.groups_src, b.ng_src, b.cap_src)) return e;
-            if (int e = ffn_fwd(enc_l[l], y, x, Ts)) return e;
+            LnOut ln2, next_out;
+            const LnNext n2{enc_l[l].st, enc_l[l].o->ln2_g, enc_l[l].o->ln2_b};
+            const LnNext n1 = l + 1 < ne ? LnNext{enc_l[l + 1].st, enc_l[l + 1].o->ln1_g, enc_l[l + 1].o->ln1_b}
+                                         : LnNext{lnf_e, lnf_e->lnf_g, lnf_e->lnf_b};
+            if (int e = self_fwd(enc_l[l], x, y, Ts, b.cu_src, b.max_src, false, b.groups_src, b.ng_src,
+                                 b.cap_src, &pre, &n2, &ln2)) return e;
+            if (int e = ffn_fwd(enc_l[l], y, x, Ts, &ln2, &n1, &next_out)) return e;
+            pre = next_out;
         }
-        const mm_stack* lnf_e = &t.enc[t.n_enc - 1];
-        uint16_t* mem; float* mem_mean; float* mem_rstd;
-        if (int e = ln(lnf_e, lnf_e->lnf_g, lnf_e->lnf_b, x, Ts, mem, mem_mean, mem_rstd)) return e;
+        uint16_t* mem = pre.h; float* mem_mean = pre.mean; float* mem_rstd = pre.rstd;
         const float* x_enc = x;
         // ---- decoder: every layer's cross-attention K/V projection of the
         // encoder memory in one grouped launch (they depend on mem only)
@@ -376,15 +433,22 @@ struct Driver {
         }
         float* y = ar.get<float>(Tt * d);
         TIMED(5, mm_embed_fwd(b.tgt_in, b.tgt_pos, t.dec_emb.w_bf16 + t.dec_emb.emb, y, Tt, d, scale, s));
+        const mm_stack* lnf_d = &t.dec[t.n_dec - 1];
+        LnOut dpre;
         for (int l = 0; l < nd; ++l) {
             float *y1, *y2;
-            if (int e = self_fwd(dec_l[l], y, y1, Tt, b.cu_tgt, b.max_tgt, true, b.groups_tgt, b.ng_tgt, b.cap_tgt)) return e;
-            if (int e = cross_fwd(dec_l[l], y1, y2, mem)) return e;
-            if (int e = ffn_fwd(dec_l[l], y2, y, Tt)) return e;
+            LnOut lnc, ln2, next_out;
+            const LnNext nc{dec_l[l].st, dec_l[l].o->lnc_g, dec_l[l].o->lnc_b};
+            const LnNext n2{dec_l[l].st, dec_l[l].o->ln2_g, dec_l[l].o->ln2_b};
+            const LnNext n1 = l + 1 < nd ? LnNext{dec_l[l + 1].st, dec_l[l + 1].o->ln1_g, dec_l[l + 1].o->ln1_b}
+                                         : LnNext{lnf_d, lnf_d->lnf_g, lnf_d->lnf_b};
+            if (int e = self_fwd(dec_l[l], y, y1, Tt, b.cu_tgt, b.max_tgt, true, b.groups_tgt, b.ng_tgt,
+                                 b.cap_tgt, &dpre, &nc, &lnc)) return e;
+            if (int e = cross_fwd(dec_l[l], y1, y2, mem, &lnc, &n2, &ln2)) return e;
+            if (int e = ffn_fwd(dec_l[l], y2, y, Tt, &ln2, &n1, &next_out)) return e;
+            dpre = next_out;
         }
-        const mm_stack* lnf_d = &t.dec[t.n_dec - 1];
-        uint16_t* hdec; float* hd_mean; float* hd_rstd;
-        if (int e = ln(lnf_d, lnf_d->lnf_g, lnf_d->lnf_b, y, Tt, hdec, hd_mean, hd_rstd)) return e;
+        uint16_t* hdec = dpre.h; float* hd_mean = dpre.mean; float* hd_rstd = dpre.rstd;
         uint16_t* logits = ar.get<uint16_t>(Tt * V);
         const mm_embed& E = t.dec_emb;
         TRY(linear(hdec, E.w_bf16 + E.gen_w, logits, Tt, d, V, MM_EPI_BF16, E.w_f32 + E.gen_b));
@@ -469,6 +533,16 @@ extern "C" int mm_task_fwd_bwd(const mm_task* task, const mm_batch* batch, void*
         const char* e = std::getenv("MM_DEFER_WGRAD");
         return !(e && e[0] == '0');
     }();
+    // MM_FUSE_LN=1: LayerNorm fused into the residual GEMM (cluster + DSMEM row
+    // statistics).  Off by default: measured slower than GEMM + standalone
+    // LayerNorm on B200 (4096x512x512: 13.2 vs 12.3 us -- the 4-CTA cluster
+    // launch costs ~1 us, the cross-CTA exchange ~2 us waiting for the slowest
+    // tile of the cluster; at d = 1024 only 16 clusters of 8 are co-resident,
+    // so the persistent grid runs in two waves; tools/ln_fuse_micro.py)
+    const bool fuse_ln = [] {  // read per call (tests toggle it)
+        const char* e = std::getenv("MM_FUSE_LN");
+        return e && e[0] == '1';
+    }();
     Arena ar;
     ar.base = static_cast<uint8_t*>(workspace);
     ar.sizing = workspace == nullptr;
@@ -480,12 +554,14 @@ extern "C" int mm_task_fwd_bwd(const mm_task* task, const mm_batch* batch, void*
         Driver p{*task, *batch, probe, mm::as_stream(stream), true, task->d_model, task->heads,
                  task->ffn, task->vocab};
         p.defer = defer;
+        p.fuse_ln = fuse_ln;
         p.run(loss_sum);
         MM_CHECK_ARG(probe.peak <= *ws_bytes, "workspace %zu B < required %zu B", *ws_bytes,
                      probe.peak);
     }
     drv.dec_done = static_cast<cudaEvent_t>(dec_done);
     drv.defer = defer;
+    drv.fuse_ln = fuse_ln;
     const int st = drv.run(loss_sum);
     if (ar.sizing) *ws_bytes = ar.peak;
     return st;

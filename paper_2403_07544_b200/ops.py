@@ -15,7 +15,7 @@ import torch
 from . import _native
 from ._native import check, lib
 
-EPI_BF16, EPI_BF16_RELU, EPI_F32, EPI_F32_ACCUM, EPI_F32_RESID, EPI_BF16_DRELU = range(6)
+EPI_BF16, EPI_BF16_RELU, EPI_F32, EPI_F32_ACCUM, EPI_F32_RESID, EPI_BF16_DRELU, EPI_F32_RESID_LN = range(7)
 
 
 class GemmArgs(ctypes.Structure):
@@ -27,6 +27,8 @@ class GemmArgs(ctypes.Structure):
         ("a_kmajor", ctypes.c_int32), ("b_kmajor", ctypes.c_int32),
         ("epilogue", ctypes.c_int32), ("b_prefetch", ctypes.c_int32),
         ("dbias", ctypes.c_void_p),
+        ("ln_gamma", ctypes.c_void_p), ("ln_beta", ctypes.c_void_p), ("ln_out", ctypes.c_void_p),
+        ("ln_mean", ctypes.c_void_p), ("ln_rstd", ctypes.c_void_p), ("ln_eps", ctypes.c_float),
     ]
 
 
@@ -75,7 +77,7 @@ def _rowstride(t: torch.Tensor, name: str) -> int:
 
 def gemm_args(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bool = True,
               b_kmajor: bool = True, epilogue: int = EPI_BF16, bias=None, resid=None, aux=None,
-              dbias=None) -> GemmArgs:
+              dbias=None, ln=None) -> GemmArgs:
     """Validated mm_gemm_args for d[M,N] (epilogue)= op(a) @ op(b)^T."""
     _need(a, torch.bfloat16, "a")
     _need(b, torch.bfloat16, "b")
@@ -92,6 +94,14 @@ def gemm_args(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bo
                     lda=_rowstride(a, "a"), ldb=_rowstride(b, "b"), ldd=_rowstride(d, "d"),
                     a_kmajor=int(a_kmajor), b_kmajor=int(b_kmajor), epilogue=epilogue,
                     dbias=_ptr(dbias))
+    if epilogue == EPI_F32_RESID_LN:
+        # ln = (gamma, beta, out_bf16 [M, N], mean [M], rstd [M], eps)
+        g, bt, out, mean, rstd, eps = ln
+        _need(out, torch.bfloat16, "ln_out")
+        if tuple(out.shape) != (m, n) or out.stride(0) != n:
+            raise ValueError("ln_out must be a contiguous [M, N] bf16 tensor")
+        args.ln_gamma, args.ln_beta, args.ln_out = g.data_ptr(), bt.data_ptr(), out.data_ptr()
+        args.ln_mean, args.ln_rstd, args.ln_eps = mean.data_ptr(), rstd.data_ptr(), float(eps)
     if resid is not None and _rowstride(resid, "resid") != args.ldd:
         raise ValueError("resid must share d's row stride")
     if aux is not None and _rowstride(aux, "aux") != args.ldd:
@@ -102,13 +112,13 @@ def gemm_args(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bo
 
 def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bool = True,
          b_kmajor: bool = True, epilogue: int = EPI_BF16, bias=None, resid=None, aux=None,
-         dbias=None) -> None:
+         dbias=None, ln=None) -> None:
     """d[M,N] (epilogue)= op(a) @ op(b)^T on tcgen05.
 
     a: [M,K] if a_kmajor else [K,M]; b: [N,K] if b_kmajor else [K,N] (bf16).
     """
     args = gemm_args(a, b, d, a_kmajor=a_kmajor, b_kmajor=b_kmajor, epilogue=epilogue,
-                     bias=bias, resid=resid, aux=aux, dbias=dbias)
+                     bias=bias, resid=resid, aux=aux, dbias=dbias, ln=ln)
     m, n, k = args.m, args.n, args.k
     LAUNCHES[0] += 1
     if GEMM_PROFILE is not None:

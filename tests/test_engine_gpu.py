@@ -283,3 +283,31 @@ def test_partially_shared_encoder_vs_oracle(cuda):
     assert abs(eng.loss_sum.item() - sum(losses)) / sum(losses) < 1e-3
     for k in used:
         assert rel_norm(eng.states[k].grad.cpu().numpy(), grads[k].numpy()) < TOL_MODEL, str(k)
+
+
+@pytest.mark.parametrize("d_model,heads,ffn", [(512, 8, 2048), (1024, 16, 1024)])
+def test_fused_layernorm_driver_matches_python_path(cuda, d_model, heads, ffn, monkeypatch):
+    """At d_model 512 / 1024 the native driver fuses every LayerNorm that
+    follows a residual GEMM into that GEMM's epilogue (cluster + DSMEM row
+    statistics, MM_EPI_F32_RESID_LN); the per-op Python path runs standalone
+    LayerNorm kernels.  Same loss and gradients up to the LayerNorm summation
+    order (fp32) that bf16 roundings downstream amplify."""
+    from paper_2403_07544_b200.configs import ModelShape
+    from paper_2403_07544_b200.engine import DeviceBatch, Engine
+    monkeypatch.setenv("MM_FUSE_LN", "1")  # opt-in path (off by default: slower, DESIGN.md)
+    shape = ModelShape(d_model, heads, ffn, 1000, 32)
+    w = configs.config1(shape)
+    tasks = [t.with_device(DeviceId(0, 0)) for t in w.tasks]
+    hb = batches_for(1, 1, shape, seed=5, sentences=48)[0]
+    grads, losses = [], []
+    for native in (True, False):
+        eng = Engine(tasks, ClusterTopology(1, 1, 3), shape, device=cuda)
+        eng.native = native
+        eng.step(0, [DeviceBatch(hb[0], cuda)])
+        torch.cuda.synchronize()
+        grads.append({k: st.grad.cpu().numpy().copy() for k, st in eng.states.items()})
+        losses.append(eng.loss_sum.item())
+    assert abs(losses[0] - losses[1]) <= 1e-5 * abs(losses[1])
+    for k in grads[0]:
+        if np.abs(grads[1][k]).max() > 0:
+            assert rel_norm(grads[0][k], grads[1][k]) < 2e-2, str(k)

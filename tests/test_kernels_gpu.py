@@ -75,6 +75,42 @@ def test_gemm_epilogues(cuda, tile, shape):
     assert rel_err(d, (ref - bias) * (aux.float() > 0)) < 1e-2
 
 
+@pytest.mark.parametrize("shape", [(4096, 512, 512), (333, 512, 2048), (4100, 1024, 1024), (128, 512, 64)])
+def test_gemm_fused_layernorm(cuda, shape):
+    """MM_EPI_F32_RESID_LN: x = resid + A B^T + bias (fp32) and the following
+    LayerNorm of x computed in the epilogue by a cluster of N/128 CTAs that
+    exchange row sums through distributed shared memory."""
+    from paper_2403_07544_b200 import ops
+    m, n, k = shape
+    g = torch.Generator(device="cuda").manual_seed(21)
+    A = torch.randn(m, k, device=cuda, generator=g).bfloat16()
+    B = (torch.randn(n, k, device=cuda, generator=g) / math.sqrt(k)).bfloat16()
+    bias = torch.randn(n, device=cuda, generator=g)
+    resid = torch.randn(m, n, device=cuda, generator=g) * 3 + 1
+    gamma = torch.rand(n, device=cuda, generator=g) + 0.5
+    beta = torch.randn(n, device=cuda, generator=g)
+    x = torch.empty(m, n, device=cuda)
+    h = torch.empty(m, n, device=cuda, dtype=torch.bfloat16)
+    mean = torch.empty(m, device=cuda)
+    rstd = torch.empty(m, device=cuda)
+    ops.gemm(A, B, x, epilogue=ops.EPI_F32_RESID_LN, bias=bias, resid=resid,
+             ln=(gamma, beta, h, mean, rstd, 1e-6))
+    ref_x = resid + A.float() @ B.float().t() + bias
+    assert rel_err(x, ref_x) < 2e-3
+    mu = x.mean(1)
+    var = ((x - mu[:, None]) ** 2).mean(1)
+    ref_rstd = torch.rsqrt(var + 1e-6)
+    assert rel_err(mean, mu) < 1e-5
+    assert rel_err(rstd, ref_rstd) < 1e-5
+    ref_h = (x - mu[:, None]) * ref_rstd[:, None] * gamma + beta
+    assert rel_err(h, ref_h) < 1e-2
+    # identical to the standalone LayerNorm kernel on the same x
+    h2 = torch.empty_like(h)
+    m2, r2 = torch.empty_like(mean), torch.empty_like(rstd)
+    ops.layernorm_fwd(x, gamma, beta, h2, m2, r2, eps=1e-6)
+    assert rel_err(h, h2) < 1e-2 and rel_err(rstd, r2) < 1e-5
+
+
 @pytest.mark.parametrize("shape", [(512, 512, 4096), (1536, 512, 4111), (32000, 512, 2048),
                                    (2048, 512, 300)])
 def test_gemm_wgrad_accumulate(cuda, tile, shape):
