@@ -570,6 +570,11 @@ class Engine:
                 self._pending_event = ev
                 self._pending_mods |= {k for k in self.states if counts[self.index[k]] >= 1}
             else:
+                if self.comm is not None:
+                    # a decoder and an encoder module may share a member set and
+                    # so a communicator: keep each communicator's collectives
+                    # in one stream order on every rank
+                    torch.cuda.current_stream().wait_stream(side)
                 self.exchange_and_update(counts, used, only=rest)
                 torch.cuda.current_stream().wait_stream(side)
         else:
