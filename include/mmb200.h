@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 13
+#define MMB200_ABI_VERSION 14
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 
 int mm_abi_version(void);
@@ -237,6 +237,8 @@ typedef struct {
     const int32_t* groups; /* [2 * n_groups] */
     int32_t n_groups;
     int32_t cap;
+    int32_t total_k;       /* key rows (the K / V tensors' extent, for TMA maps) */
+    int32_t flags;         /* internal: 0 */
 } mm_attn_args;
 
 int mm_attention_fwd(const mm_attn_args* a, void* stream);

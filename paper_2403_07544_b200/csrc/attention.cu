@@ -19,11 +19,16 @@
 //           recomputing P / dP transposed.
 // Probabilities and dS enter the second MMA as a bf16 hi + lo pair (two MMAs),
 // so the products keep ~16 mantissa bits instead of bf16's 8.
+#include <cuda.h>
 #include <cuda_bf16.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <mutex>
 
 #include "mm_common.h"
+#include "tc_ptx.cuh"
 
 namespace {
 
@@ -326,7 +331,19 @@ __device__ unsigned long long g_attn_trace[8192 * 4];
             if (cta_ < 8192) g_attn_trace[cta_ * 4 + (i)] = t_;                               \
         }                                                                                     \
     } while (0)
+#define ATTN_STAMP_LANE0(i)                                                                   \
+    do {                                                                                      \
+        if ((threadIdx.x & 31) == 0) {                                                        \
+            unsigned long long t_;                                                            \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+            const int cta_ = blockIdx.y * gridDim.x + blockIdx.x;                             \
+            if (cta_ < 8192) g_attn_trace[cta_ * 4 + (i)] = t_;                               \
+        }                                                                                     \
+    } while (0)
 #else
+#define ATTN_STAMP_LANE0(i) \
+    do {                    \
+    } while (0)
 #define ATTN_STAMP(i) \
     do {              \
     } while (0)
@@ -337,6 +354,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 2) attn_bwd_kernel(const mm_at
     __shared__ Group G;
     const int h = blockIdx.x;  // heads fastest: a group's CTAs run together and share its rows' DRAM pages
     if (threadIdx.x < 32) load_group(G, a, threadIdx.x);  // host-uploaded: before the wait
+    if (a.flags & 1) {  // groups of <= 128 rows per side went to the tcgen05 kernel
+        const int first = a.groups[2 * blockIdx.y], n = a.groups[2 * blockIdx.y + 1];
+        if (a.cu_q[first + n] - a.cu_q[first] <= 128 && a.cu_k[first + n] - a.cu_k[first] <= 128) return;
+    }
     pdl_wait_release();
     ATTN_STAMP(0);
     __syncthreads();
@@ -499,6 +520,283 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 2) attn_bwd_kernel(const mm_at
     ATTN_STAMP(3);
 }
 
+// ===========================================================================
+// Backward on tcgen05 (groups whose sequences fit one 128-row block per side)
+//
+// One CTA per (head, group): TMA stages the group's Q, K, V, dO rows (one
+// 128-row x 64-column SW128 box each -- rows past the group are other
+// tokens, masked by sequence id); the MMA warp computes S = Q K^T and
+// dP = dO V^T into TMEM (128 columns each); eight warps turn them into P, the
+// exact fp32 D_i = sum_j P_ij dP_ij and dS = P (dP - D), written to shared
+// memory as bf16 hi + lo pairs in the SW128 K-major layout -- the same bytes
+// serve as the K-major A of dQ = dS K and as the MN-major A of dV = P^T dO and
+// dK = dS^T Q -- then the MMA warp issues the three products (hi and lo) into
+// TMEM and the eight warps scale, convert and store dQ / dK / dV.  Sequence
+// masks come from the group's offsets (no padding rows).
+namespace tca {
+
+constexpr int kRows = 128;
+constexpr int kTile = kRows * 128;         // 128 rows x 64 bf16 (one SW128 box)
+constexpr int kPTile = 2 * kTile;          // 128 rows x 128 keys (two 64-key regions)
+constexpr int kEpiW0 = 2, kEpiW = 16;  // 4 warps per TMEM lane quarter, 32 keys each
+constexpr int kThreads = (kEpiW0 + kEpiW) * 32;
+constexpr int kSmemBytes = 4 * kTile + 4 * kPTile + 4096 + 1024;  // + meta + alignment
+
+struct alignas(64) BwdParams {
+    CUtensorMap mq, mk, mv, mdo;
+    const int32_t* cu_q;
+    const int32_t* cu_k;
+    const int32_t* groups;
+    const float* lse;
+    uint16_t* dq;
+    uint16_t* dk;
+    uint16_t* dv;
+    int64_t ld_dq, ld_dk, ld_dv;
+    int total_q, causal;
+    float scale;
+};
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// 32 values of a row (4 16-byte chunks from chunk c0) as bf16 hi (+ lo
+// residual) into a SW128 K-major region: row r at r*128, 16-byte chunk c at
+// (c ^ (r & 7)) * 16
+__device__ __forceinline__ void store_row_hilo(uint8_t* hi, uint8_t* lo, int r, int c0, const float (&v)[32]) {
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+        uint32_t h[4], l[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float a = v[cc * 8 + 2 * e], b = v[cc * 8 + 2 * e + 1];
+            h[e] = pack_bf16(a, b);
+            const float ah = __uint_as_float(h[e] << 16), bh = __uint_as_float(h[e] & 0xffff0000u);
+            l[e] = pack_bf16(a - ah, b - bh);
+        }
+        const int off = r * 128 + (((c0 + cc) ^ (r & 7)) * 16);
+        *reinterpret_cast<uint4*>(hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4*>(lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
+    }
+}
+
+__device__ __forceinline__ uint64_t desc(const void* p, uint32_t lbo) {
+    return tc::umma_desc_sw128(tc::smem_u32(p), lbo, 1024);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_constant__ BwdParams p) {
+    extern __shared__ uint8_t smraw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    uint8_t* Qs = sm;
+    uint8_t* Ks = Qs + kTile;
+    uint8_t* Vs = Ks + kTile;
+    uint8_t* dOs = Vs + kTile;
+    uint8_t* Ph = dOs + kTile;   // regions: keys 0-63 at +0, keys 64-127 at +kTile
+    uint8_t* Pl = Ph + kPTile;
+    uint8_t* Sh = Pl + kPTile;   // dS hi
+    uint8_t* Sl = Sh + kPTile;   // dS lo
+    int* kseg = reinterpret_cast<int*>(Sl + kPTile);  // [128] sequence of key row (-1: none)
+    int* kpos = kseg + kRows;                          // [128] position in its sequence
+    float* dpart = reinterpret_cast<float*>(kpos + kRows);  // [4][128] D partials
+    uint64_t* bars = reinterpret_cast<uint64_t*>(dpart + 4 * kRows);
+    uint64_t* tma_bar = bars;
+    uint64_t* s_bar = bars + 1;
+    uint64_t* p_bar = bars + 2;
+    uint64_t* g_bar = bars + 3;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+
+    const int h = blockIdx.x, grp = blockIdx.y;
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+    const int lane = threadIdx.x & 31;
+    // group metadata: host-uploaded, so read before griddepcontrol.wait
+    const int first = p.groups[2 * grp], nseq = p.groups[2 * grp + 1];
+    const int q_lo = p.cu_q[first], nq = p.cu_q[first + nseq] - q_lo;
+    const int k_lo = p.cu_k[first], nk = p.cu_k[first + nseq] - k_lo;
+    if (nq > kRows || nk > kRows) return;  // a longer sequence: the mma.sync kernel's group
+    if (warp == 1 && lane == 0) {
+        tc::mbar_init(tma_bar, 1);
+        tc::mbar_init(s_bar, 1);
+        tc::mbar_init(p_bar, kEpiW);
+        tc::mbar_init(g_bar, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, 256);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    ATTN_STAMP(0);
+
+    if (warp == 0) {
+        if (lane == 0) {
+            pdl_wait();
+            tc::mbar_expect_tx(tma_bar, 4 * kTile);
+            tc::tma_load_2d(Qs, &p.mq, tma_bar, h * 64, q_lo);
+            tc::tma_load_2d(Ks, &p.mk, tma_bar, h * 64, k_lo);
+            tc::tma_load_2d(Vs, &p.mv, tma_bar, h * 64, k_lo);
+            tc::tma_load_2d(dOs, &p.mdo, tma_bar, h * 64, q_lo);
+        }
+    } else if (warp == 1) {
+        // ---- S = Q K^T (cols 0-127), dP = dO V^T (cols 128-255)
+        tc::mbar_wait(tma_bar, 0);
+        tc::tc_fence_after();
+        // (warp-converged issue, one lane elected inside each instruction: see
+        // tc::mma_bf16_elect; tmem is warp-uniform)
+        constexpr uint32_t id_s = tc::idesc_bf16_f32(128, 128, 0, 0);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            tc::mma_bf16_elect<1>(tmem, desc(Qs + kk * 32, 16), desc(Ks + kk * 32, 16), id_s, kk > 0);
+            tc::mma_bf16_elect<1>(tmem + 128, desc(dOs + kk * 32, 16), desc(Vs + kk * 32, 16), id_s, kk > 0);
+        }
+        tc::mma_commit_elect<1>(s_bar);
+        // ---- dV = P^T dO (cols 0-63), dK = dS^T Q (64-127), dQ = dS K (128-191)
+        tc::mbar_wait(p_bar, 0);
+        tc::tc_fence_after();
+        constexpr uint32_t id_mn = tc::idesc_bf16_f32(128, 64, 1, 1);  // A and B MN-major
+        constexpr uint32_t id_km = tc::idesc_bf16_f32(128, 64, 0, 1);  // A K-major, B MN-major
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {  // bf16 hi, then lo
+            const uint8_t* P = part ? Pl : Ph;
+            const uint8_t* S = part ? Sl : Sh;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {  // K = 128 query rows
+                const uint32_t acc = (part > 0 || kk > 0) ? 1u : 0u;
+                tc::mma_bf16_elect<1>(tmem + 0, desc(P + kk * 2048, kTile), desc(dOs + kk * 2048, kTile), id_mn, acc);
+                tc::mma_bf16_elect<1>(tmem + 64, desc(S + kk * 2048, kTile), desc(Qs + kk * 2048, kTile), id_mn, acc);
+            }
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {  // K = 128 keys
+                const uint32_t acc = (part > 0 || kk > 0) ? 1u : 0u;
+                tc::mma_bf16_elect<1>(tmem + 128, desc(S + (kk >> 2) * kTile + (kk & 3) * 32, 16),
+                                      desc(Ks + kk * 2048, kTile), id_km, acc);
+            }
+        }
+        tc::mma_commit_elect<1>(g_bar);
+    } else {
+        // ---- sixteen warps: warp%4 = TMEM lane quarter (query rows), kc = 32-key chunk
+        const int quarter = warp & 3, kc = (warp - kEpiW0) >> 2;
+        const int i = quarter * 32 + lane;  // query row within the group
+        const bool vrow = i < nq;
+        // this row's keys: one contiguous range of the group's key rows (its
+        // own sequence; causal: up to its position)
+        int klo = 0, khi = 0;
+        if (vrow) {
+            for (int s2 = 0; s2 < nseq; ++s2) {
+                const int a = p.cu_q[first + s2] - q_lo, b = p.cu_q[first + s2 + 1] - q_lo;
+                if (i >= a && i < b) {
+                    klo = p.cu_k[first + s2] - k_lo;
+                    khi = p.causal ? klo + (i - a) + 1 : p.cu_k[first + s2 + 1] - k_lo;
+                }
+            }
+        }
+        pdl_wait();
+        const float l2 = vrow ? p.lse[int64_t(h) * p.total_q + q_lo + i] * kLog2e : 0.f;
+        const float c = p.scale * kLog2e;
+        tc::mbar_wait(s_bar, 0);
+        tc::tc_fence_after();
+        if (warp == kEpiW0) ATTN_STAMP_LANE0(1);
+        const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+        const int key0 = kc * 32;
+        float pv[32], dpv[32];
+        // a chunk no row of this warp attends to is all zeros (warp-uniform skip)
+        const bool any = __any_sync(0xffffffffu, klo < key0 + 32 && khi > key0);
+        if (any) {
+            uint32_t sv[32], dv[32];
+            tc::tmem_ld_32x32(trow + key0, sv);
+            tc::tmem_ld_32x32(trow + 128 + key0, dv);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int key = key0 + j;
+                pv[j] = (key >= klo && key < khi) ? ex2(fmaf(__uint_as_float(sv[j]), c, -l2)) : 0.f;
+                dpv[j] = __uint_as_float(dv[j]);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) pv[j] = dpv[j] = 0.f;
+        }
+        float dsum = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) dsum = fmaf(pv[j], dpv[j], dsum);
+        dpart[kc * kRows + i] = dsum;
+        tc::named_barrier_sync(1, kEpiW * 32);
+        const float D = (dpart[i] + dpart[kRows + i]) + (dpart[2 * kRows + i] + dpart[3 * kRows + i]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) dpv[j] = pv[j] * (dpv[j] - D);  // dS
+        // keys kc*32..+32: region kc/2, 16-byte chunks (kc&1)*4 .. +4 of the row
+        store_row_hilo(Ph + (kc >> 1) * kTile, Pl + (kc >> 1) * kTile, i, (kc & 1) * 4, pv);
+        store_row_hilo(Sh + (kc >> 1) * kTile, Sl + (kc >> 1) * kTile, i, (kc & 1) * 4, dpv);
+        tc::fence_proxy_async_smem();  // generic stores -> visible to the tensor core
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(p_bar);
+        if (warp == kEpiW0) ATTN_STAMP_LANE0(2);
+        // ---- gradients out of TMEM: this warp's 16 of each output's 64 columns
+        tc::mbar_wait(g_bar, 0);
+        tc::tc_fence_after();
+        auto emit = [&](uint32_t col, uint16_t* base, int64_t ld, int row_lo, bool vr, float sc) {
+            uint32_t v[16];
+            tc::tmem_ld_32x16(trow + col + kc * 16, v);
+            tc::tmem_ld_wait();
+            if (!vr) return;
+            uint4* dst = reinterpret_cast<uint4*>(base + int64_t(row_lo + i) * ld + h * 64 + kc * 16);
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                dst[q] = make_uint4(pack_bf16(__uint_as_float(v[8 * q + 0]) * sc, __uint_as_float(v[8 * q + 1]) * sc),
+                                    pack_bf16(__uint_as_float(v[8 * q + 2]) * sc, __uint_as_float(v[8 * q + 3]) * sc),
+                                    pack_bf16(__uint_as_float(v[8 * q + 4]) * sc, __uint_as_float(v[8 * q + 5]) * sc),
+                                    pack_bf16(__uint_as_float(v[8 * q + 6]) * sc, __uint_as_float(v[8 * q + 7]) * sc));
+        };
+        emit(0, p.dv, p.ld_dv, k_lo, i < nk, 1.f);        // TMEM lane = key row
+        emit(64, p.dk, p.ld_dk, k_lo, i < nk, p.scale);
+        emit(128, p.dq, p.ld_dq, q_lo, vrow, p.scale);     // TMEM lane = query row
+        if (warp == kEpiW0) ATTN_STAMP_LANE0(3);
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc(tmem, 256);
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    return fn;
+}
+
+// [rows, 64-column head slices] bf16 view with row stride ld: 128-row x 64-col SW128 boxes
+int head_map(CUtensorMap* m, const void* base, int64_t rows, int64_t ld, int64_t cols) {
+    auto enc = encoder();
+    if (!enc) {
+        mm::set_error("cuTensorMapEncodeTiled unavailable");
+        return mm::kCuda;
+    }
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+    cuuint32_t box[2] = {64, 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        mm::set_error("attention tensor map (%d): rows=%lld ld=%lld", (int)r, (long long)rows, (long long)ld);
+        return mm::kCuda;
+    }
+    return 0;
+}
+
+}  // namespace tca
+
 size_t fwd_smem(const mm_attn_args& a) { return size_t(3) * a.cap * kP * 2; }
 size_t bwd_smem(const mm_attn_args& a) { return size_t(4) * a.cap * kP * 2 + size_t(2) * a.cap * 4; }
 
@@ -539,6 +837,35 @@ extern "C" int mm_attention_fwd(const mm_attn_args* a, void* stream) {
 extern "C" int mm_attention_bwd(const mm_attn_args* a, void* stream) {
     if (int st = check(a, true)) return st;
     if (a->n_seq == 0) return 0;
+    static const bool mma_sync_only = std::getenv("MM_ATTN_MMA_SYNC") != nullptr;  // diagnostics
+    if (!mma_sync_only && a->total_k > 0) {
+        // tcgen05 kernel for every group that fits one 128-row block per side
+        tca::BwdParams bp{};
+        const int64_t cols = int64_t(a->heads) * kHd;
+        if (int st = tca::head_map(&bp.mq, a->q, a->total_q, a->ldq, cols)) return st;
+        if (int st = tca::head_map(&bp.mk, a->k, a->total_k, a->ldk, cols)) return st;
+        if (int st = tca::head_map(&bp.mv, a->v, a->total_k, a->ldv, cols)) return st;
+        if (int st = tca::head_map(&bp.mdo, a->d_o, a->total_q, a->ldo, cols)) return st;
+        bp.cu_q = a->cu_q; bp.cu_k = a->cu_k; bp.groups = a->groups; bp.lse = a->lse;
+        bp.dq = a->dq; bp.dk = a->dk; bp.dv = a->dv;
+        bp.ld_dq = a->ld_dq; bp.ld_dk = a->ld_dk; bp.ld_dv = a->ld_dv;
+        bp.total_q = a->total_q; bp.causal = a->causal; bp.scale = a->scale;
+        static bool attr = false;
+        if (!attr) {
+            MM_CUDA_TRY(cudaFuncSetAttribute(tca::attn_bwd_tc_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, tca::kSmemBytes));
+            attr = true;
+        }
+        MM_CUDA_TRY(mm::launch_pdl(tca::attn_bwd_tc_kernel, dim3(a->heads, a->n_groups), dim3(tca::kThreads),
+                                   tca::kSmemBytes, mm::as_stream(stream), bp));
+        MM_LAUNCH_CHECK("attn_bwd_tc_kernel");
+        if (a->cap <= tca::kRows) return 0;
+    }
+    // groups with a sequence longer than 128 rows (or the diagnostics path):
+    // the mma.sync kernel, skipping groups the tcgen05 kernel took
+    mm_attn_args b = *a;
+    b.flags = (!mma_sync_only && a->total_k > 0) ? 1 : 0;
+    a = &b;
     const size_t smem = bwd_smem(*a);
     MM_CHECK_ARG(smem <= 227 * 1024, "attention backward needs %zu B of smem", smem);
     MM_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -109,7 +109,10 @@ __global__ void __launch_bounds__(256, (COLS <= 512 ? 2 : 1)) ln_bwd_kernel(cons
     for (int i = 0; i < V; ++i) ag[i] = ab[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int64_t stride = int64_t(gridDim.x) * 8 * R;
     for (int64_t row0 = (int64_t(blockIdx.x) * 8 + warp) * R; row0 < rows; row0 += stride) {
-        float4 d[R][V], xv[R][V];
+        // wide rows (one row per warp batch): the residual-gradient row is
+        // fetched with dy and x, one DRAM round trip per row instead of two
+        constexpr bool kPreDx = R == 1;
+        float4 d[R][V], xv[R][V], opre[kPreDx ? V : 1];
         float mu[R], rs[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {  // every dy / x load of the batch first
@@ -122,6 +125,11 @@ __global__ void __launch_bounds__(256, (COLS <= 512 ? 2 : 1)) ln_bwd_kernel(cons
             for (int i = 0; i < V; ++i) {
                 d[r][i] = dyr[lane + 32 * i];
                 xv[r][i] = xr[lane + 32 * i];
+            }
+            if constexpr (kPreDx) {
+                const float4* dxr = reinterpret_cast<const float4*>(dx + row * COLS);
+#pragma unroll
+                for (int i = 0; i < V; ++i) opre[i] = dxr[lane + 32 * i];
             }
         }
 #pragma unroll
@@ -152,7 +160,7 @@ __global__ void __launch_bounds__(256, (COLS <= 512 ? 2 : 1)) ln_bwd_kernel(cons
             uint2* dbr = reinterpret_cast<uint2*>(dx_bf16 + row * COLS);
             float4 o[V];
 #pragma unroll
-            for (int i = 0; i < V; ++i) o[i] = dxr[lane + 32 * i];
+            for (int i = 0; i < V; ++i) o[i] = kPreDx ? opre[kPreDx ? i : 0] : dxr[lane + 32 * i];
 #pragma unroll
             for (int i = 0; i < V; ++i) {
                 float4 w = o[i];

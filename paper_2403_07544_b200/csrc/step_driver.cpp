@@ -240,6 +240,7 @@ struct Driver {
         a.n_seq = b.n_seq; a.heads = H; a.head_dim = 64; a.causal = causal;
         a.max_q = max_q; a.max_k = max_k; a.scale = 0.125f; a.total_q = total_q;
         a.groups = groups; a.n_groups = ng; a.cap = cap;
+        a.total_k = cu_k == cu_q ? total_q : int(b.n_src);
         return a;
     }
 

@@ -45,6 +45,7 @@ class AttnArgs(ctypes.Structure):
         ("causal", ctypes.c_int32), ("max_q", ctypes.c_int32), ("max_k", ctypes.c_int32),
         ("scale", ctypes.c_float), ("total_q", ctypes.c_int32),
         ("groups", ctypes.c_void_p), ("n_groups", ctypes.c_int32), ("cap", ctypes.c_int32),
+        ("total_k", ctypes.c_int32), ("flags", ctypes.c_int32),
     ]
 
 
@@ -213,7 +214,7 @@ def attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, heads, max_q, max_k, caus
         ld_dv=dv.stride(0) if dv is not None else 0,
         n_seq=n_seq, heads=heads, head_dim=hd, causal=int(causal), max_q=max_q, max_k=max_k,
         scale=1.0 / math.sqrt(hd), total_q=q.shape[0],
-        groups=gt.data_ptr(), n_groups=n_groups, cap=cap)
+        groups=gt.data_ptr(), n_groups=n_groups, cap=cap, total_k=k.shape[0])
     # the struct holds raw pointers: keep the device group table (possibly
     # built here) alive as long as the args are
     args._keep = (gt,)

@@ -63,7 +63,7 @@ if os.environ.get("MM_LIB_VARIANT") == "attn_trace":
     t = np.array(buf, dtype=np.float64).reshape(n, 4)
     t0 = t[:, 0].min()
     r = (t - t0) / 1e3
-    print("ctas", n, "start spread %.2f" % r[:, 0].max(), "stage %.2f" % np.median(r[:, 1] - r[:, 0]),
+    print("ctas", n, "start spread %.2f" % r[:, 0].max(), "stage(tc: to S ready) %.2f" % np.median(r[:, 1] - r[:, 0]),
           "phaseA %.2f" % np.median(r[:, 2] - r[:, 1]), "phaseB %.2f" % np.median(r[:, 3] - r[:, 2]),
           "cta life %.2f" % np.median(r[:, 3] - r[:, 0]), "end %.2f" % r[:, 3].max())
     print("phaseA p90 %.2f max %.2f; phaseB p90 %.2f max %.2f" % (np.percentile(r[:, 2] - r[:, 1], 90), (r[:, 2] - r[:, 1]).max(), np.percentile(r[:, 3] - r[:, 2], 90), (r[:, 3] - r[:, 2]).max()))
