@@ -230,6 +230,10 @@ __global__ void __launch_bounds__(kFwdWarps * 32) attn_fwd_kernel(const mm_attn_
     // the group table and sequence offsets come from the step's host upload,
     // not from the previous kernel: read them before griddepcontrol.wait
     if (threadIdx.x < 32) load_group(G, a, threadIdx.x);
+    if (a.flags & 1) {  // groups of <= 128 rows per side went to the tcgen05 kernel
+        const int first = a.groups[2 * blockIdx.y], n = a.groups[2 * blockIdx.y + 1];
+        if (a.cu_q[first + n] - a.cu_q[first] <= 128 && a.cu_k[first + n] - a.cu_k[first] <= 128) return;
+    }
     pdl_wait_release();
     __syncthreads();
     uint16_t* Qs = sm;
@@ -564,7 +568,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 // 32 values of a row (4 16-byte chunks from chunk c0) as bf16 hi (+ lo
 // residual) into a SW128 K-major region: row r at r*128, 16-byte chunk c at
 // (c ^ (r & 7)) * 16
-__device__ __forceinline__ void store_row_hilo(uint8_t* hi, uint8_t* lo, int r, int c0, const float (&v)[32]) {
+__device__ __forceinline__ void store_row_hilo(uint8_t* hi, uint8_t* lo, int r, int c0, const float* v) {
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
         uint32_t h[4], l[4];
@@ -761,6 +765,178 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
     }
 }
 
+// ---------------------------------------------------------------------------
+// Forward on tcgen05: S = Q K^T in TMEM, eight warps (two per TMEM lane
+// quarter, 64 keys each) build P = softmax(S) as bf16 hi + lo over the dead
+// Q / K tiles, O = P V (hi and lo) in TMEM, then O and lse out.  80 KB of
+// shared memory: two CTAs per SM.
+constexpr int kFwdEpiW = 8;
+constexpr int kFwdThreads = (kEpiW0 + kFwdEpiW) * 32;
+constexpr int kFwdSmemBytes = 3 * kTile + kPTile + 2048 + 1024;  // Q K V, P lo (2 regions), meta, align
+
+struct alignas(64) FwdParams {
+    CUtensorMap mq, mk, mv;
+    const int32_t* cu_q;
+    const int32_t* cu_k;
+    const int32_t* groups;
+    float* lse;
+    uint16_t* o;
+    int64_t ldo;
+    int total_q, causal;
+    float scale;
+};
+
+__global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_tc_kernel(const __grid_constant__ FwdParams p) {
+    extern __shared__ uint8_t smraw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    uint8_t* Qs = sm;             // Q, K: after S = Q K^T, the P hi regions (keys 0-63, 64-127)
+    uint8_t* Ks = Qs + kTile;
+    uint8_t* Vs = Ks + kTile;
+    uint8_t* Pl = Vs + kTile;     // P lo: two regions
+    uint8_t* Ph = Qs;
+    float* red = reinterpret_cast<float*>(Pl + kPTile);  // [2][128] row partials
+    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * kRows);
+    uint64_t* tma_bar = bars;
+    uint64_t* s_bar = bars + 1;
+    uint64_t* p_bar = bars + 2;
+    uint64_t* o_bar = bars + 3;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+
+    const int h = blockIdx.x, grp = blockIdx.y;
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+    const int lane = threadIdx.x & 31;
+    const int first = p.groups[2 * grp], nseq = p.groups[2 * grp + 1];
+    const int q_lo = p.cu_q[first], nq = p.cu_q[first + nseq] - q_lo;
+    const int k_lo = p.cu_k[first], nk = p.cu_k[first + nseq] - k_lo;
+    if (nq > kRows || nk > kRows) return;  // the mma.sync kernel's group
+    if (warp == 1 && lane == 0) {
+        tc::mbar_init(tma_bar, 1);
+        tc::mbar_init(s_bar, 1);
+        tc::mbar_init(p_bar, kFwdEpiW);
+        tc::mbar_init(o_bar, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, 256);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            pdl_wait();
+            tc::mbar_expect_tx(tma_bar, 3 * kTile);
+            tc::tma_load_2d(Qs, &p.mq, tma_bar, h * 64, q_lo);
+            tc::tma_load_2d(Ks, &p.mk, tma_bar, h * 64, k_lo);
+            tc::tma_load_2d(Vs, &p.mv, tma_bar, h * 64, k_lo);
+        }
+    } else if (warp == 1) {
+        tc::mbar_wait(tma_bar, 0);
+        tc::tc_fence_after();
+        constexpr uint32_t id_s = tc::idesc_bf16_f32(128, 128, 0, 0);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+            tc::mma_bf16_elect<1>(tmem, desc(Qs + kk * 32, 16), desc(Ks + kk * 32, 16), id_s, kk > 0);
+        tc::mma_commit_elect<1>(s_bar);
+        tc::mbar_wait(p_bar, 0);
+        tc::tc_fence_after();
+        constexpr uint32_t id_o = tc::idesc_bf16_f32(128, 64, 0, 1);  // P K-major, V MN-major
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+            const uint8_t* P = part ? Pl : Ph;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+                tc::mma_bf16_elect<1>(tmem + 128, desc(P + (kk >> 2) * kTile + (kk & 3) * 32, 16),
+                                      desc(Vs + kk * 2048, kTile), id_o, (part > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit_elect<1>(o_bar);
+    } else {
+        const int quarter = warp & 3, kh = (warp - kEpiW0) >> 2;
+        const int i = quarter * 32 + lane;
+        const bool vrow = i < nq;
+        int klo = 0, khi = 0;
+        if (vrow) {
+            for (int s2 = 0; s2 < nseq; ++s2) {
+                const int a = p.cu_q[first + s2] - q_lo, b = p.cu_q[first + s2 + 1] - q_lo;
+                if (i >= a && i < b) {
+                    klo = p.cu_k[first + s2] - k_lo;
+                    khi = p.causal ? klo + (i - a) + 1 : p.cu_k[first + s2 + 1] - k_lo;
+                }
+            }
+        }
+        const float c = p.scale * kLog2e;
+        tc::mbar_wait(s_bar, 0);
+        tc::tc_fence_after();
+        const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+        float pv[64];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+            const int key0 = kh * 64 + ch * 32;
+            if (__any_sync(0xffffffffu, klo < key0 + 32 && khi > key0)) {
+                uint32_t sv[32];
+                tc::tmem_ld_32x32(trow + key0, sv);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int key = key0 + j;
+                    const float v = (key >= klo && key < khi) ? __uint_as_float(sv[j]) * c : -INFINITY;
+                    pv[ch * 32 + j] = v;
+                    mx = fmaxf(mx, v);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) pv[ch * 32 + j] = -INFINITY;
+            }
+        }
+        red[kh * kRows + i] = mx;
+        tc::named_barrier_sync(1, kFwdEpiW * 32);
+        const float m = fmaxf(red[i], red[kRows + i]);
+        const float mref = m == -INFINITY ? 0.f : m;
+        float sum = 0.f;
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+            pv[j] = ex2(pv[j] - mref);  // -inf -> 0
+            sum += pv[j];
+        }
+        tc::named_barrier_sync(1, kFwdEpiW * 32);  // every max read before the slots are reused
+        red[kh * kRows + i] = sum;
+        tc::named_barrier_sync(1, kFwdEpiW * 32);
+        const float l = red[i] + red[kRows + i];
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+        for (int j = 0; j < 64; ++j) pv[j] *= inv;
+        // P over the (consumed) Q / K tiles: keys kh*64.. = region kh
+        store_row_hilo(Ph + kh * kTile, Pl + kh * kTile, i, 0, pv);
+        store_row_hilo(Ph + kh * kTile, Pl + kh * kTile, i, 4, pv + 32);
+        tc::fence_proxy_async_smem();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(p_bar);
+        if (vrow && kh == 0) p.lse[int64_t(h) * p.total_q + q_lo + i] = (mref + log2f(l)) * kLn2;
+        tc::mbar_wait(o_bar, 0);
+        tc::tc_fence_after();
+        uint32_t v[32];
+        tc::tmem_ld_32x32(trow + 128 + kh * 32, v);
+        tc::tmem_ld_wait();
+        if (vrow) {
+            uint4* dst = reinterpret_cast<uint4*>(p.o + int64_t(q_lo + i) * p.ldo + h * 64 + kh * 32);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                dst[q] = make_uint4(pack_bf16(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1])),
+                                    pack_bf16(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3])),
+                                    pack_bf16(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5])),
+                                    pack_bf16(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7])));
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc(tmem, 256);
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -825,6 +1001,35 @@ extern "C" int mm_attn_trace_read(unsigned long long* host, int n) {
 extern "C" int mm_attention_fwd(const mm_attn_args* a, void* stream) {
     if (int st = check(a, false)) return st;
     if (a->n_seq == 0) return 0;
+    // The tcgen05 forward is opt-in (MM_ATTN_TC_FWD=1): measured slower than
+    // the mma.sync kernel at config-3 shapes (13.1 vs 10.0 us: 83 KB of smem
+    // and 256 TMEM columns allow two CTAs per SM against four, and the
+    // forward has too little MMA work per CTA to amortise that).
+    const char* tcf = std::getenv("MM_ATTN_TC_FWD");
+    const bool use_tc = tcf && tcf[0] == '1';
+    mm_attn_args b = *a;
+    if (use_tc && a->total_k > 0) {
+        tca::FwdParams fp{};
+        const int64_t cols = int64_t(a->heads) * kHd;
+        if (int st = tca::head_map(&fp.mq, a->q, a->total_q, a->ldq, cols)) return st;
+        if (int st = tca::head_map(&fp.mk, a->k, a->total_k, a->ldk, cols)) return st;
+        if (int st = tca::head_map(&fp.mv, a->v, a->total_k, a->ldv, cols)) return st;
+        fp.cu_q = a->cu_q; fp.cu_k = a->cu_k; fp.groups = a->groups; fp.lse = a->lse;
+        fp.o = a->o; fp.ldo = a->ldo;
+        fp.total_q = a->total_q; fp.causal = a->causal; fp.scale = a->scale;
+        static bool attr = false;
+        if (!attr) {
+            MM_CUDA_TRY(cudaFuncSetAttribute(tca::attn_fwd_tc_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, tca::kFwdSmemBytes));
+            attr = true;
+        }
+        MM_CUDA_TRY(mm::launch_pdl(tca::attn_fwd_tc_kernel, dim3(a->heads, a->n_groups), dim3(tca::kFwdThreads),
+                                   tca::kFwdSmemBytes, mm::as_stream(stream), fp));
+        MM_LAUNCH_CHECK("attn_fwd_tc_kernel");
+        if (a->cap <= tca::kRows) return 0;
+        b.flags = 1;  // the mma.sync kernel takes only groups with a longer sequence
+    }
+    a = &b;
     const size_t smem = fwd_smem(*a);
     MM_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));

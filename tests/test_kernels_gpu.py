@@ -302,8 +302,14 @@ def poison_smem(cuda):
     ops.xent(logits, labels, logits, torch.empty(rows, device=cuda), 1.0)
 
 
+@pytest.mark.parametrize("tc_fwd", [False, True], ids=["fwd_mma_sync", "fwd_tcgen05"])
 @pytest.mark.parametrize("causal,maxlen", [(True, 128), (False, 128), (True, 256)])
-def test_attention(cuda, causal, maxlen):
+def test_attention(cuda, causal, maxlen, tc_fwd, monkeypatch):
+    """Forward (mma.sync, or the opt-in tcgen05 kernel) and backward (tcgen05
+    for groups within 128 rows, mma.sync for longer sequences) vs an fp32
+    PyTorch reference."""
+    if tc_fwd:
+        monkeypatch.setenv("MM_ATTN_TC_FWD", "1")
     from paper_2403_07544_b200 import ops
     rng = np.random.default_rng(maxlen + causal)
     heads, d = 8, 512
