@@ -558,6 +558,7 @@ struct alignas(64) BwdParams {
     int64_t ld_dq, ld_dk, ld_dv;
     int total_q, causal;
     float scale;
+    int n_groups, heads;
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -589,6 +590,11 @@ __device__ __forceinline__ uint64_t desc(const void* p, uint32_t lbo) {
     return tc::umma_desc_sw128(tc::smem_u32(p), lbo, 1024);
 }
 
+// Persistent: CTA b takes units (group, head) b, b + grid, ... (heads fastest);
+// the producer loads unit n+1's tiles as soon as unit n's MMAs have consumed
+// them (g_bar), so the TMA latency hides behind unit n's output phase; TMEM
+// is double-buffered by unit parity (unit n+1's S / dP cannot overwrite the
+// dV / dK / dQ of unit n that the warps are still reading).
 __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_constant__ BwdParams p) {
     extern __shared__ uint8_t smraw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -600,9 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
     uint8_t* Pl = Ph + kPTile;
     uint8_t* Sh = Pl + kPTile;   // dS hi
     uint8_t* Sl = Sh + kPTile;   // dS lo
-    int* kseg = reinterpret_cast<int*>(Sl + kPTile);  // [128] sequence of key row (-1: none)
-    int* kpos = kseg + kRows;                          // [128] position in its sequence
-    float* dpart = reinterpret_cast<float*>(kpos + kRows);  // [4][128] D partials
+    float* dpart = reinterpret_cast<float*>(Sl + kPTile);  // [4][128] D partials
     uint64_t* bars = reinterpret_cast<uint64_t*>(dpart + 4 * kRows);
     uint64_t* tma_bar = bars;
     uint64_t* s_bar = bars + 1;
@@ -610,14 +614,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
     uint64_t* g_bar = bars + 3;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
 
-    const int h = blockIdx.x, grp = blockIdx.y;
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
-    // group metadata: host-uploaded, so read before griddepcontrol.wait
-    const int first = p.groups[2 * grp], nseq = p.groups[2 * grp + 1];
-    const int q_lo = p.cu_q[first], nq = p.cu_q[first + nseq] - q_lo;
-    const int k_lo = p.cu_k[first], nk = p.cu_k[first + nseq] - k_lo;
-    if (nq > kRows || nk > kRows) return;  // a longer sequence: the mma.sync kernel's group
+    const int units = p.n_groups * p.heads;
     if (warp == 1 && lane == 0) {
         tc::mbar_init(tma_bar, 1);
         tc::mbar_init(s_bar, 1);
@@ -625,143 +624,177 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
         tc::mbar_init(g_bar, 1);
         tc::fence_barrier_init();
     }
-    if (warp == 1) tc::tmem_alloc(tmem_slot, 256);
+    if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem0 = *tmem_slot;
     ATTN_STAMP(0);
+    // unit -> group metadata (host-uploaded: may be read before griddepcontrol.wait)
+    struct U { int first, nseq, q_lo, nq, k_lo, nk, h; };
+    auto unit = [&](int u) -> U {
+        U x;
+        const int grp = u / p.heads;
+        x.h = u - grp * p.heads;
+        x.first = p.groups[2 * grp];
+        x.nseq = p.groups[2 * grp + 1];
+        x.q_lo = p.cu_q[x.first];
+        x.nq = p.cu_q[x.first + x.nseq] - x.q_lo;
+        x.k_lo = p.cu_k[x.first];
+        x.nk = p.cu_k[x.first + x.nseq] - x.k_lo;
+        return x;
+    };
+    auto mine = [&](const U& x) { return x.nq <= kRows && x.nk <= kRows; };  // else: mma.sync kernel
 
     if (warp == 0) {
         if (lane == 0) {
             pdl_wait();
-            tc::mbar_expect_tx(tma_bar, 4 * kTile);
-            tc::tma_load_2d(Qs, &p.mq, tma_bar, h * 64, q_lo);
-            tc::tma_load_2d(Ks, &p.mk, tma_bar, h * 64, k_lo);
-            tc::tma_load_2d(Vs, &p.mv, tma_bar, h * 64, k_lo);
-            tc::tma_load_2d(dOs, &p.mdo, tma_bar, h * 64, q_lo);
+            int n = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                const U x = unit(u);
+                if (!mine(x)) continue;
+                if (n > 0) tc::mbar_wait(g_bar, (n - 1) & 1);  // unit n-1's MMAs consumed the tiles
+                tc::mbar_expect_tx(tma_bar, 4 * kTile);
+                tc::tma_load_2d(Qs, &p.mq, tma_bar, x.h * 64, x.q_lo);
+                tc::tma_load_2d(Ks, &p.mk, tma_bar, x.h * 64, x.k_lo);
+                tc::tma_load_2d(Vs, &p.mv, tma_bar, x.h * 64, x.k_lo);
+                tc::tma_load_2d(dOs, &p.mdo, tma_bar, x.h * 64, x.q_lo);
+                ++n;
+            }
         }
     } else if (warp == 1) {
-        // ---- S = Q K^T (cols 0-127), dP = dO V^T (cols 128-255)
-        tc::mbar_wait(tma_bar, 0);
-        tc::tc_fence_after();
-        // (warp-converged issue, one lane elected inside each instruction: see
-        // tc::mma_bf16_elect; tmem is warp-uniform)
-        constexpr uint32_t id_s = tc::idesc_bf16_f32(128, 128, 0, 0);
+        int n = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            const U x = unit(u);
+            if (!mine(x)) continue;
+            const uint32_t tmem = tmem0 + (n & 1) * 256;
+            // ---- S = Q K^T (cols 0-127), dP = dO V^T (cols 128-255)
+            tc::mbar_wait(tma_bar, n & 1);
+            tc::tc_fence_after();
+            constexpr uint32_t id_s = tc::idesc_bf16_f32(128, 128, 0, 0);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-            tc::mma_bf16_elect<1>(tmem, desc(Qs + kk * 32, 16), desc(Ks + kk * 32, 16), id_s, kk > 0);
-            tc::mma_bf16_elect<1>(tmem + 128, desc(dOs + kk * 32, 16), desc(Vs + kk * 32, 16), id_s, kk > 0);
-        }
-        tc::mma_commit_elect<1>(s_bar);
-        // ---- dV = P^T dO (cols 0-63), dK = dS^T Q (64-127), dQ = dS K (128-191)
-        tc::mbar_wait(p_bar, 0);
-        tc::tc_fence_after();
-        constexpr uint32_t id_mn = tc::idesc_bf16_f32(128, 64, 1, 1);  // A and B MN-major
-        constexpr uint32_t id_km = tc::idesc_bf16_f32(128, 64, 0, 1);  // A K-major, B MN-major
-#pragma unroll
-        for (int part = 0; part < 2; ++part) {  // bf16 hi, then lo
-            const uint8_t* P = part ? Pl : Ph;
-            const uint8_t* S = part ? Sl : Sh;
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {  // K = 128 query rows
-                const uint32_t acc = (part > 0 || kk > 0) ? 1u : 0u;
-                tc::mma_bf16_elect<1>(tmem + 0, desc(P + kk * 2048, kTile), desc(dOs + kk * 2048, kTile), id_mn, acc);
-                tc::mma_bf16_elect<1>(tmem + 64, desc(S + kk * 2048, kTile), desc(Qs + kk * 2048, kTile), id_mn, acc);
+            for (int kk = 0; kk < 4; ++kk) {
+                tc::mma_bf16_elect<1>(tmem, desc(Qs + kk * 32, 16), desc(Ks + kk * 32, 16), id_s, kk > 0);
+                tc::mma_bf16_elect<1>(tmem + 128, desc(dOs + kk * 32, 16), desc(Vs + kk * 32, 16), id_s, kk > 0);
             }
+            tc::mma_commit_elect<1>(s_bar);
+            // ---- dV = P^T dO (cols 0-63), dK = dS^T Q (64-127), dQ = dS K (128-191)
+            tc::mbar_wait(p_bar, n & 1);
+            tc::tc_fence_after();
+            constexpr uint32_t id_mn = tc::idesc_bf16_f32(128, 64, 1, 1);  // A and B MN-major
+            constexpr uint32_t id_km = tc::idesc_bf16_f32(128, 64, 0, 1);  // A K-major, B MN-major
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {  // K = 128 keys
-                const uint32_t acc = (part > 0 || kk > 0) ? 1u : 0u;
-                tc::mma_bf16_elect<1>(tmem + 128, desc(S + (kk >> 2) * kTile + (kk & 3) * 32, 16),
-                                      desc(Ks + kk * 2048, kTile), id_km, acc);
+            for (int part = 0; part < 2; ++part) {  // bf16 hi, then lo
+                const uint8_t* P = part ? Pl : Ph;
+                const uint8_t* S = part ? Sl : Sh;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {  // K = 128 query rows
+                    const uint32_t acc = (part > 0 || kk > 0) ? 1u : 0u;
+                    tc::mma_bf16_elect<1>(tmem + 0, desc(P + kk * 2048, kTile), desc(dOs + kk * 2048, kTile), id_mn, acc);
+                    tc::mma_bf16_elect<1>(tmem + 64, desc(S + kk * 2048, kTile), desc(Qs + kk * 2048, kTile), id_mn, acc);
+                }
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {  // K = 128 keys
+                    const uint32_t acc = (part > 0 || kk > 0) ? 1u : 0u;
+                    tc::mma_bf16_elect<1>(tmem + 128, desc(S + (kk >> 2) * kTile + (kk & 3) * 32, 16),
+                                          desc(Ks + kk * 2048, kTile), id_km, acc);
+                }
             }
+            tc::mma_commit_elect<1>(g_bar);
+            ++n;
         }
-        tc::mma_commit_elect<1>(g_bar);
     } else {
         // ---- sixteen warps: warp%4 = TMEM lane quarter (query rows), kc = 32-key chunk
         const int quarter = warp & 3, kc = (warp - kEpiW0) >> 2;
         const int i = quarter * 32 + lane;  // query row within the group
-        const bool vrow = i < nq;
-        // this row's keys: one contiguous range of the group's key rows (its
-        // own sequence; causal: up to its position)
-        int klo = 0, khi = 0;
-        if (vrow) {
-            for (int s2 = 0; s2 < nseq; ++s2) {
-                const int a = p.cu_q[first + s2] - q_lo, b = p.cu_q[first + s2 + 1] - q_lo;
-                if (i >= a && i < b) {
-                    klo = p.cu_k[first + s2] - k_lo;
-                    khi = p.causal ? klo + (i - a) + 1 : p.cu_k[first + s2 + 1] - k_lo;
+        const float c = p.scale * kLog2e;
+        pdl_wait();
+        int n = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            const U x = unit(u);
+            if (!mine(x)) continue;
+            const uint32_t trow = tmem0 + (n & 1) * 256 + (static_cast<uint32_t>(quarter * 32) << 16);
+            const bool vrow = i < x.nq;
+            // this row's keys: one contiguous range of the group's key rows (its
+            // own sequence; causal: up to its position)
+            int klo = 0, khi = 0;
+            if (vrow) {
+                for (int s2 = 0; s2 < x.nseq; ++s2) {
+                    const int a = p.cu_q[x.first + s2] - x.q_lo, b = p.cu_q[x.first + s2 + 1] - x.q_lo;
+                    if (i >= a && i < b) {
+                        klo = p.cu_k[x.first + s2] - x.k_lo;
+                        khi = p.causal ? klo + (i - a) + 1 : p.cu_k[x.first + s2 + 1] - x.k_lo;
+                    }
                 }
             }
-        }
-        pdl_wait();
-        const float l2 = vrow ? p.lse[int64_t(h) * p.total_q + q_lo + i] * kLog2e : 0.f;
-        const float c = p.scale * kLog2e;
-        tc::mbar_wait(s_bar, 0);
-        tc::tc_fence_after();
-        if (warp == kEpiW0) ATTN_STAMP_LANE0(1);
-        const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-        const int key0 = kc * 32;
-        float pv[32], dpv[32];
-        // a chunk no row of this warp attends to is all zeros (warp-uniform skip)
-        const bool any = __any_sync(0xffffffffu, klo < key0 + 32 && khi > key0);
-        if (any) {
-            uint32_t sv[32], dv[32];
-            tc::tmem_ld_32x32(trow + key0, sv);
-            tc::tmem_ld_32x32(trow + 128 + key0, dv);
-            tc::tmem_ld_wait();
+            const float l2 = vrow ? p.lse[int64_t(x.h) * p.total_q + x.q_lo + i] * kLog2e : 0.f;
+            tc::mbar_wait(s_bar, n & 1);
+            tc::tc_fence_after();
+            if (warp == kEpiW0) ATTN_STAMP_LANE0(1);
+            const int key0 = kc * 32;
+            float pv[32], dpv[32];
+            // a chunk no row of this warp attends to is all zeros (warp-uniform skip)
+            const bool any = __any_sync(0xffffffffu, klo < key0 + 32 && khi > key0);
+            if (any) {
+                uint32_t sv[32], dv[32];
+                tc::tmem_ld_32x32(trow + key0, sv);
+                tc::tmem_ld_32x32(trow + 128 + key0, dv);
+                tc::tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const int key = key0 + j;
-                pv[j] = (key >= klo && key < khi) ? ex2(fmaf(__uint_as_float(sv[j]), c, -l2)) : 0.f;
-                dpv[j] = __uint_as_float(dv[j]);
+                for (int j = 0; j < 32; ++j) {
+                    const int key = key0 + j;
+                    pv[j] = (key >= klo && key < khi) ? ex2(fmaf(__uint_as_float(sv[j]), c, -l2)) : 0.f;
+                    dpv[j] = __uint_as_float(dv[j]);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) pv[j] = dpv[j] = 0.f;
             }
-        } else {
+            float dsum = 0.f;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) pv[j] = dpv[j] = 0.f;
+            for (int j = 0; j < 32; ++j) dsum = fmaf(pv[j], dpv[j], dsum);
+            dpart[kc * kRows + i] = dsum;
+            tc::named_barrier_sync(1, kEpiW * 32);
+            const float D = (dpart[i] + dpart[kRows + i]) + (dpart[2 * kRows + i] + dpart[3 * kRows + i]);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) dpv[j] = pv[j] * (dpv[j] - D);  // dS
+            // keys kc*32..+32: region kc/2, 16-byte chunks (kc&1)*4 .. +4 of the row
+            store_row_hilo(Ph + (kc >> 1) * kTile, Pl + (kc >> 1) * kTile, i, (kc & 1) * 4, pv);
+            store_row_hilo(Sh + (kc >> 1) * kTile, Sl + (kc >> 1) * kTile, i, (kc & 1) * 4, dpv);
+            tc::fence_proxy_async_smem();  // generic stores -> visible to the tensor core
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(p_bar);
+            if (warp == kEpiW0) ATTN_STAMP_LANE0(2);
+            // ---- gradients out of TMEM: this warp's 16 of each output's 64 columns
+            tc::mbar_wait(g_bar, n & 1);
+            tc::tc_fence_after();
+            auto emit = [&](uint32_t col, uint16_t* base, int64_t ld, int row_lo, bool vr, float sc) {
+                uint32_t v[16];
+                tc::tmem_ld_32x16(trow + col + kc * 16, v);
+                tc::tmem_ld_wait();
+                if (!vr) return;
+                uint4* dst = reinterpret_cast<uint4*>(base + int64_t(row_lo + i) * ld + x.h * 64 + kc * 16);
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+                    dst[q] = make_uint4(pack_bf16(__uint_as_float(v[8 * q + 0]) * sc, __uint_as_float(v[8 * q + 1]) * sc),
+                                        pack_bf16(__uint_as_float(v[8 * q + 2]) * sc, __uint_as_float(v[8 * q + 3]) * sc),
+                                        pack_bf16(__uint_as_float(v[8 * q + 4]) * sc, __uint_as_float(v[8 * q + 5]) * sc),
+                                        pack_bf16(__uint_as_float(v[8 * q + 6]) * sc, __uint_as_float(v[8 * q + 7]) * sc));
+            };
+            emit(0, p.dv, p.ld_dv, x.k_lo, i < x.nk, 1.f);        // TMEM lane = key row
+            emit(64, p.dk, p.ld_dk, x.k_lo, i < x.nk, p.scale);
+            emit(128, p.dq, p.ld_dq, x.q_lo, vrow, p.scale);      // TMEM lane = query row
+            if (warp == kEpiW0) ATTN_STAMP_LANE0(3);
+            tc::tc_fence_before();
+            ++n;
         }
-        float dsum = 0.f;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) dsum = fmaf(pv[j], dpv[j], dsum);
-        dpart[kc * kRows + i] = dsum;
-        tc::named_barrier_sync(1, kEpiW * 32);
-        const float D = (dpart[i] + dpart[kRows + i]) + (dpart[2 * kRows + i] + dpart[3 * kRows + i]);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) dpv[j] = pv[j] * (dpv[j] - D);  // dS
-        // keys kc*32..+32: region kc/2, 16-byte chunks (kc&1)*4 .. +4 of the row
-        store_row_hilo(Ph + (kc >> 1) * kTile, Pl + (kc >> 1) * kTile, i, (kc & 1) * 4, pv);
-        store_row_hilo(Sh + (kc >> 1) * kTile, Sl + (kc >> 1) * kTile, i, (kc & 1) * 4, dpv);
-        tc::fence_proxy_async_smem();  // generic stores -> visible to the tensor core
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(p_bar);
-        if (warp == kEpiW0) ATTN_STAMP_LANE0(2);
-        // ---- gradients out of TMEM: this warp's 16 of each output's 64 columns
-        tc::mbar_wait(g_bar, 0);
-        tc::tc_fence_after();
-        auto emit = [&](uint32_t col, uint16_t* base, int64_t ld, int row_lo, bool vr, float sc) {
-            uint32_t v[16];
-            tc::tmem_ld_32x16(trow + col + kc * 16, v);
-            tc::tmem_ld_wait();
-            if (!vr) return;
-            uint4* dst = reinterpret_cast<uint4*>(base + int64_t(row_lo + i) * ld + h * 64 + kc * 16);
-#pragma unroll
-            for (int q = 0; q < 2; ++q)
-                dst[q] = make_uint4(pack_bf16(__uint_as_float(v[8 * q + 0]) * sc, __uint_as_float(v[8 * q + 1]) * sc),
-                                    pack_bf16(__uint_as_float(v[8 * q + 2]) * sc, __uint_as_float(v[8 * q + 3]) * sc),
-                                    pack_bf16(__uint_as_float(v[8 * q + 4]) * sc, __uint_as_float(v[8 * q + 5]) * sc),
-                                    pack_bf16(__uint_as_float(v[8 * q + 6]) * sc, __uint_as_float(v[8 * q + 7]) * sc));
-        };
-        emit(0, p.dv, p.ld_dv, k_lo, i < nk, 1.f);        // TMEM lane = key row
-        emit(64, p.dk, p.ld_dk, k_lo, i < nk, p.scale);
-        emit(128, p.dq, p.ld_dq, q_lo, vrow, p.scale);     // TMEM lane = query row
-        if (warp == kEpiW0) ATTN_STAMP_LANE0(3);
     }
     tc::tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         tc::tc_fence_after();
-        tc::tmem_dealloc(tmem, 256);
+        tc::tmem_dealloc(tmem0, 512);
     }
 }
 
@@ -1055,14 +1088,16 @@ extern "C" int mm_attention_bwd(const mm_attn_args* a, void* stream) {
         bp.dq = a->dq; bp.dk = a->dk; bp.dv = a->dv;
         bp.ld_dq = a->ld_dq; bp.ld_dk = a->ld_dk; bp.ld_dv = a->ld_dv;
         bp.total_q = a->total_q; bp.causal = a->causal; bp.scale = a->scale;
+        bp.n_groups = a->n_groups; bp.heads = a->heads;
         static bool attr = false;
         if (!attr) {
             MM_CUDA_TRY(cudaFuncSetAttribute(tca::attn_bwd_tc_kernel,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, tca::kSmemBytes));
             attr = true;
         }
-        MM_CUDA_TRY(mm::launch_pdl(tca::attn_bwd_tc_kernel, dim3(a->heads, a->n_groups), dim3(tca::kThreads),
-                                   tca::kSmemBytes, mm::as_stream(stream), bp));
+        const int units = a->n_groups * a->heads;
+        MM_CUDA_TRY(mm::launch_pdl(tca::attn_bwd_tc_kernel, dim3(std::min(units, mm::num_sms())),
+                                   dim3(tca::kThreads), tca::kSmemBytes, mm::as_stream(stream), bp));
         MM_LAUNCH_CHECK("attn_bwd_tc_kernel");
         if (a->cap <= tca::kRows) return 0;
     }

@@ -56,7 +56,7 @@ if os.environ.get("MM_LIB_VARIANT") == "attn_trace":
     import ctypes
     from paper_2403_07544_b200 import _native
     L = _native.lib()
-    n = args.n_groups * heads
+    n = min(args.n_groups * heads, 148)  # persistent tcgen05 kernel: one CTA per SM
     buf = (ctypes.c_ulonglong * (n * 4))()
     ops.attention_bwd(args); torch.cuda.synchronize()
     L.mm_attn_trace_read(buf, n * 4)
