@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 14
+#define MMB200_ABI_VERSION 15
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 
 int mm_abi_version(void);
@@ -70,7 +70,7 @@ int mm_sync_emulated(const mm_sync_module* mods, int n_mods, int only_ready, voi
  * step_size = lr / (1 - beta1^t) and inv_sqrt_bc2 = 1 / sqrt(1 - beta2^t)).
  */
 typedef struct {
-    const float* grad;
+    float* grad; /* read (and zeroed when mm_adam_hyper.zero_grad) */
     float* master;
     float* exp_avg;
     float* exp_avg_sq;
@@ -87,6 +87,8 @@ typedef struct {
     float one_minus_beta1, one_minus_beta2; /* computed in double on the host */
     int32_t max_ctas; /* 0: one CTA per 16K-element chunk; > 0: persistent CTAs
                          (a thin background update overlapping other kernels) */
+    int32_t zero_grad; /* 1: write 0 to every gradient element it consumed, so the
+                          bucket is clean for the next step without a memset pass */
 } mm_adam_hyper;
 
 int mm_fused_update(const mm_adam_module* mods, int n_mods, const mm_adam_hyper* hyper,

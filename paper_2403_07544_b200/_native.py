@@ -19,7 +19,7 @@ if os.environ.get("MM_LIB_VARIANT"):  # diagnostics: a tuning build from tools/b
                             "libmmb200.so")
 
 #: must match MMB200_ABI_VERSION in include/mmb200.h
-ABI_VERSION = 14
+ABI_VERSION = 15
 MAX_GROUP = 8
 
 
@@ -94,13 +94,14 @@ class AdamHyper(ctypes.Structure):
         ("one_minus_beta1", c_float),
         ("one_minus_beta2", c_float),
         ("max_ctas", c_int32),
+        ("zero_grad", c_int32),
     ]
 
     @classmethod
-    def make(cls, beta1, beta2, eps, weight_decay=0.0, inv_loss_scale=1.0, max_ctas=0):
+    def make(cls, beta1, beta2, eps, weight_decay=0.0, inv_loss_scale=1.0, max_ctas=0, zero_grad=0):
         return cls(beta1=beta1, beta2=beta2, eps=eps, weight_decay=weight_decay,
                    inv_loss_scale=inv_loss_scale, one_minus_beta1=1.0 - beta1,
-                   one_minus_beta2=1.0 - beta2, max_ctas=max_ctas)
+                   one_minus_beta2=1.0 - beta2, max_ctas=max_ctas, zero_grad=zero_grad)
 
 
 class ReduceItem(ctypes.Structure):

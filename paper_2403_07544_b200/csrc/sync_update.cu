@@ -139,12 +139,14 @@ __global__ void __launch_bounds__(kThreads) fused_update_kernel(const __grid_con
     // g = sum / n * inv_loss_scale, the rescale of Algorithm 1 fused here
     const float fn = (float)n;
     const float unscale = t.hp.inv_loss_scale;
+    const bool zero_grad = t.hp.zero_grad != 0;
     const int64_t base = (chunk - t.chunk_begin[mi]) * kChunk;
     const int64_t end = min(base + kChunk, md.n_elems);
     const float ss = md.step_size, isb = md.inv_sqrt_bc2;
     if ((md.n_elems & 3) == 0) {
         const int64_t v0 = base >> 2, v1 = end >> 2;
         const float4* G = reinterpret_cast<const float4*>(md.grad);
+        float4* G0 = reinterpret_cast<float4*>(md.grad);
         float4* P = reinterpret_cast<float4*>(md.master);
         float4* M = reinterpret_cast<float4*>(md.exp_avg);
         float4* V = reinterpret_cast<float4*>(md.exp_avg_sq);
@@ -159,6 +161,7 @@ __global__ void __launch_bounds__(kThreads) fused_update_kernel(const __grid_con
                     m[u] = __ldcs(M + vi); s[u] = __ldcs(V + vi);
                 }
             }
+
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const int64_t vi = v + int64_t(u) * kThreads;
@@ -168,6 +171,7 @@ __global__ void __launch_bounds__(kThreads) fused_update_kernel(const __grid_con
                 adam_elem(__fdiv_rn(g[u].z, fn) * unscale, p[u].z, m[u].z, s[u].z, ss, isb, t.hp);
                 adam_elem(__fdiv_rn(g[u].w, fn) * unscale, p[u].w, m[u].w, s[u].w, ss, isb, t.hp);
                 __stcs(P + vi, p[u]); __stcs(M + vi, m[u]); __stcs(V + vi, s[u]);
+                if (zero_grad) __stcs(G0 + vi, make_float4(0.f, 0.f, 0.f, 0.f));  // lazy zeroing
                 if (B) {
                     uint2 b;
                     b.x = pack_bf16x2(p[u].x, p[u].y);
@@ -179,7 +183,9 @@ __global__ void __launch_bounds__(kThreads) fused_update_kernel(const __grid_con
     } else {
         for (int64_t i = base + threadIdx.x; i < end; i += kThreads) {
             float p = md.master[i], m = md.exp_avg[i], s = md.exp_avg_sq[i];
-            adam_elem(__fdiv_rn(md.grad[i], fn) * unscale, p, m, s, ss, isb, t.hp);
+            const float gi = md.grad[i];
+            if (zero_grad) md.grad[i] = 0.f;
+            adam_elem(__fdiv_rn(gi, fn) * unscale, p, m, s, ss, isb, t.hp);
             md.master[i] = p; md.exp_avg[i] = m; md.exp_avg_sq[i] = s;
             if (md.param_bf16) {
                 __nv_bfloat16 h = __float2bfloat16_rn(p);

@@ -311,3 +311,29 @@ def test_fused_layernorm_driver_matches_python_path(cuda, d_model, heads, ffn, m
     for k in grads[0]:
         if np.abs(grads[1][k]).max() > 0:
             assert rel_norm(grads[0][k], grads[1][k]) < 2e-2, str(k)
+
+
+def test_lazy_grad_zeroing_matches_memset(cuda):
+    """zero_in_update (the fused update zeroes the gradient it consumed, no
+    memset before the next use; Trainer's default) gives the same parameters
+    over several steps as zeroing every bucket before its first use."""
+    from paper_2403_07544_b200.engine import DeviceBatch, Engine
+    shape = configs.SHAPE_CFG1_GPU
+    w = configs.config1(shape)
+    tasks = [t.with_device(DeviceId(0, 0)) for t in w.tasks]
+    hb = batches_for(1, 4, shape, seed=9)[0]
+    masters = []
+    for lazy in (False, True):
+        eng = Engine(tasks, ClusterTopology(1, 1, 3), shape, device=cuda, seed=0)
+        eng.zero_in_update = lazy
+        for s, b in enumerate(hb):
+            eng.step(s, [DeviceBatch(b, cuda)])
+        eng.sync_updates()
+        torch.cuda.synchronize()
+        masters.append({k: st.master.cpu().numpy().copy() for k, st in eng.states.items()})
+        if lazy:  # every bucket an update consumed is clean again
+            for k, st in eng.states.items():
+                if k not in eng._dirty:
+                    assert float(st.grad.abs().max()) == 0.0, str(k)
+    for k in masters[0]:
+        assert rel(masters[1][k], masters[0][k]) < 1e-5, str(k)

@@ -40,7 +40,7 @@ def test_struct_layouts():
     # offsets the C side relies on (include/mmb200.h)
     assert ctypes.sizeof(_native.SyncModule) == 8 * 8 + 8 + 8 + 4 + 4
     assert ctypes.sizeof(_native.AdamModule) == 5 * 8 + 8 + 4 + 4 + 4 + 4
-    assert ctypes.sizeof(_native.AdamHyper) == 7 * 4 + 4
+    assert ctypes.sizeof(_native.AdamHyper) == 7 * 4 + 4 + 4  # + zero_grad
     assert ctypes.sizeof(_native.ReduceItem) == 8 + 8 + 8 + 4 + 4
 
 
