@@ -7,7 +7,9 @@ from paper_2403_07544_b200 import ops
 from paper_2403_07544_b200.data import attention_groups
 dev = torch.device("cuda:0")
 rng = np.random.default_rng(0)
-d, heads = 512, 8
+CFG5 = os.environ.get("ATTN_CFG") == "5"  # config-5 shapes: 16384 tokens, 16 heads, lognormal(3.2, 0.6) <= 256
+d, heads = (1024, 16) if CFG5 else (512, 8)
+MU, SIG, HI, TOK = (3.2, 0.6, 256, 16384) if CFG5 else (3.0, 0.5, 128, 4096)
 
 
 def lengths(total, mu, sigma, lo, hi):
@@ -33,8 +35,8 @@ def timeit(fn, n=20):
 
 
 for name, causal, cross in [("enc self", False, False), ("dec causal", True, False), ("dec cross", False, True)]:
-    lq = lengths(4096, 3.0, 0.5, 4, 128)
-    lk = lengths(4096, 3.0, 0.5, 4, 128)[:len(lq)] if cross else lq
+    lq = lengths(TOK, MU, SIG, 4, HI)
+    lk = lengths(TOK, MU, SIG, 4, HI)[:len(lq)] if cross else lq
     if cross and len(lk) < len(lq):
         lk = np.concatenate([lk, lq[len(lk):]])
     cu_q = np.concatenate([[0], np.cumsum(lq)]).astype(np.int32)
