@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 15
+#define MMB200_ABI_VERSION 16
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 
 int mm_abi_version(void);
@@ -118,11 +118,13 @@ typedef struct {
     void* buf;       /* in-place sum */
     int64_t n_elems;
     int32_t dtype;   /* 0 = fp32, 1 = bf16 */
-    int32_t pad;
+    int32_t root;    /* -1: sum-allreduce; >= 0: only that group rank used the module
+                        (n = 1), so its buffer already is the sum: broadcast from it */
 } mm_reduce_item;
 
-/* Sum-allreduce of every item on its group communicator, issued in array order
- * (callers pass sorted ModuleKey order) inside one ncclGroupStart/End. */
+/* Sum-allreduce (or, for n = 1, broadcast from the one ready member) of every
+ * item on its group communicator, issued in array order (callers pass sorted
+ * ModuleKey order) inside one ncclGroupStart/End. */
 int mm_reduce_modules(void* ctx, const mm_reduce_item* items, int n, void* stream);
 
 /* ---------------------------------------------------------------------------

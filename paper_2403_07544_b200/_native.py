@@ -19,7 +19,7 @@ if os.environ.get("MM_LIB_VARIANT"):  # diagnostics: a tuning build from tools/b
                             "libmmb200.so")
 
 #: must match MMB200_ABI_VERSION in include/mmb200.h
-ABI_VERSION = 15
+ABI_VERSION = 16
 MAX_GROUP = 8
 
 
@@ -110,7 +110,7 @@ class ReduceItem(ctypes.Structure):
         ("buf", c_void_p),
         ("n_elems", c_int64),
         ("dtype", c_int32),
-        ("pad", c_int32),
+        ("root", c_int32),  # -1: allreduce; >= 0: broadcast from this group rank (n = 1)
     ]
 
 

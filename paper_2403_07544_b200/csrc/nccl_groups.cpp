@@ -127,11 +127,22 @@ extern "C" int mm_reduce_modules(void* ctx, const mm_reduce_item* items, int n, 
         if (!it.group || it.n_elems == 0) continue;
         Group* g = static_cast<Group*>(it.group);
         const ncclDataType_t dt = it.dtype == 1 ? ncclBfloat16 : ncclFloat32;
-        ncclResult_t r = ncclAllReduce(it.buf, it.buf, (size_t)it.n_elems, dt, ncclSum, g->comm,
-                                       mm::as_stream(stream));
+        if (it.root >= g->size) {
+            ncclGroupEnd();
+            mm::set_error("reduce item root %d outside a group of %d", it.root, g->size);
+            return mm::kArg;
+        }
+        // n = 1: the single ready member's buffer is the Algorithm-1 sum (the
+        // others hold zeros), so a broadcast moves (g-1)/g of the allreduce's
+        // 2(g-1)/g bytes and gives bit-identical results
+        ncclResult_t r = it.root >= 0
+                             ? ncclBroadcast(it.buf, it.buf, (size_t)it.n_elems, dt, it.root, g->comm,
+                                             mm::as_stream(stream))
+                             : ncclAllReduce(it.buf, it.buf, (size_t)it.n_elems, dt, ncclSum, g->comm,
+                                             mm::as_stream(stream));
         if (r != ncclSuccess) {
             ncclGroupEnd();
-            return nccl_status(r, "ncclAllReduce");
+            return nccl_status(r, it.root >= 0 ? "ncclBroadcast" : "ncclAllReduce");
         }
     }
     MM_NCCL_TRY(ncclGroupEnd());

@@ -33,7 +33,7 @@ from .configs import ModelShape
 from .data import ATTN_CAP, Batch, attention_groups
 from .domain import ClusterTopology, ModuleKey, Side, TaskSpec
 from .model import LN_EPS, ModuleState, module_layouts
-from .plan import (Multiplexer, build_plan, embedding_keys, exchange_order, ready_flags,
+from .plan import (Multiplexer, build_plan, decode_ready, embedding_keys, exchange_order, ready_bits, ready_flags,
                    task_modules)
 
 
@@ -537,8 +537,11 @@ class Engine:
             self.sync_updates()
         flags = ready_flags(self.plan, self.rank, used)
         counts_ready = None
+        self._roots = None
         if self.comm is not None:
-            self.flags_dev.copy_(torch.tensor(flags, dtype=torch.int32), non_blocking=True)
+            # K1 on rank bitmasks: the world sum gives each module's ready set
+            bits = ready_bits(self.plan, self.rank, used)
+            self.flags_dev.copy_(torch.tensor(bits, dtype=torch.int32), non_blocking=True)
             self.comm.ready_count(self.flags_dev, self.n_ready_dev)  # K1, ahead of the compute
             self._counts_host.copy_(self.n_ready_dev, non_blocking=True)
             counts_ready = torch.cuda.Event()
@@ -555,7 +558,7 @@ class Engine:
                                   dec_done if i == len(tasks) - 1 else None)
         if counts_ready is not None:
             counts_ready.synchronize()  # waits for K1 only, not for the compute behind it
-            counts = self._counts_host.tolist()
+            counts, self._roots = decode_ready(self._counts_host.tolist())
         else:
             counts = flags
         if overlap:
@@ -606,16 +609,21 @@ class Engine:
         module with n >= 1; ``only`` restricts both to a subset of keys."""
         items = []
         if self.comm is not None:
+            idx = self.plan.index()
+            roots = getattr(self, "_roots", None)
             for k in exchange_order(self.plan, counts, self.rank):
                 if only is not None and k not in only:
                     continue
-                grp = self.comm.by_set.get(tuple(self.plan.groups[k]))
+                members = self.plan.groups[k]
+                grp = self.comm.by_set.get(tuple(members))
                 st = self.states[k]
-                if k not in used and k in self._dirty:  # contribute the zero of Algorithm 1 (PAPER.md:227-228)
+                # n = 1: broadcast the one ready member's buffer (it is the sum)
+                root = members.index(roots[idx[k]]) if roots is not None and counts[idx[k]] == 1 else -1
+                if root < 0 and k not in used and k in self._dirty:  # contribute the zero of Algorithm 1 (PAPER.md:227-228)
                     ops.memset(st.grad, 0)
                 self._dirty.add(k)  # receives the group's sum
                 items.append(_native.ReduceItem(group=grp, buf=st.grad.data_ptr(),
-                                                n_elems=st.grad.numel(), dtype=0))
+                                                n_elems=st.grad.numel(), dtype=0, root=root))
             self.comm.reduce(items)
         self.fused_update(counts, only, max_ctas)
 

@@ -113,6 +113,25 @@ def ready_flags(plan: ModulePlan, rank: int, used: Iterable[ModuleKey]) -> list[
     return [1 if (k in u and k in mine) else 0 for k in plan.keys]
 
 
+def ready_bits(plan: ModulePlan, rank: int, used: Iterable[ModuleKey]) -> list[int]:
+    """K1 contribution as a rank bitmask: bit `rank` set iff hosted here and
+    used this step.  Bits are disjoint across ranks, so the world sum-allreduce
+    returns each module's set of ready ranks: n = popcount, and for n = 1 the
+    one rank whose buffer already is the group sum (the broadcast root)."""
+    if rank >= 31:
+        raise ValueError("ready bitmasks hold ranks 0..30")
+    return [f << rank for f in ready_flags(plan, rank, used)]
+
+
+def decode_ready(bits) -> tuple[list[int], list[int]]:
+    """(counts, roots) from the world-summed ready bitmasks: counts[m] = number
+    of ready ranks; roots[m] = the single ready rank when counts[m] == 1, else -1."""
+    bits = [int(b) for b in bits]
+    counts = [bin(b).count("1") for b in bits]
+    roots = [b.bit_length() - 1 if c == 1 else -1 for b, c in zip(bits, counts)]
+    return counts, roots
+
+
 def ready_counts_all(plan: ModulePlan, used_by_rank: dict[int, set]) -> list[int]:
     """Sum of every rank's flags (what the world allreduce of K1 returns)."""
     tot = [0] * len(plan.keys)

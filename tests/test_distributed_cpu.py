@@ -25,8 +25,8 @@ def _worker(rank, world, port, out_dir):
     from paper_2403_07544_b200 import configs
     from paper_2403_07544_b200.data import make_batch
     from paper_2403_07544_b200.model import init_module, module_layouts
-    from paper_2403_07544_b200.plan import (Multiplexer, build_plan, embedding_keys,
-                                            exchange_order, ready_flags, task_modules)
+    from paper_2403_07544_b200.plan import (Multiplexer, build_plan, decode_ready, embedding_keys,
+                                            exchange_order, ready_bits, ready_flags, task_modules)
     wl = configs.config1()
     plan = build_plan(wl.tasks, wl.topo)
     layouts = module_layouts(plan, wl.shape)
@@ -42,12 +42,16 @@ def _worker(rank, world, port, out_dir):
             mine = {k: masters[k] for k in plan.hosted[rank]}
             grads, used, losses = OT.local_grads(list(zip(tasks, batches)), mine, layouts, wl.shape,
                                                  embedding_keys)
-            flags = torch.tensor(ready_flags(plan, rank, used), dtype=torch.int32)
-            dist.all_reduce(flags)  # K1
-            counts = flags.tolist()
-            for k in exchange_order(plan, counts, rank):  # K2, sorted ModuleKey order
-                dist.all_reduce(grads[k], group=subgroups[tuple(plan.groups[k])])
+            bits = torch.tensor(ready_bits(plan, rank, used), dtype=torch.int32)
+            dist.all_reduce(bits)  # K1 on rank bitmasks
+            counts, roots = decode_ready(bits.tolist())
             idx = plan.index()
+            for k in exchange_order(plan, counts, rank):  # K2, sorted ModuleKey order
+                g = subgroups[tuple(plan.groups[k])]
+                if counts[idx[k]] == 1:  # n = 1: the ready rank's buffer is the sum
+                    dist.broadcast(grads[k], src=roots[idx[k]], group=g)
+                else:
+                    dist.all_reduce(grads[k], group=g)
             synced = {str(k): (grads[k] / counts[idx[k]]).numpy()
                       for k in plan.hosted[rank] if counts[idx[k]] >= 1}
             results.append({"accum": accum, "step": step, "counts": counts,

@@ -153,3 +153,19 @@ def test_validate_config_and_unplaced():
     unplaced = TaskSpec(**{**wl.tasks[0].__dict__, "device": None})
     with pytest.raises(SimulationError):
         build_plan([unplaced], wl.topo)
+
+
+def test_ready_bitmask_decode():
+    """K1 on rank bitmasks: the world sum decodes to the ready counts the
+    flag sum gives, and names the single ready rank for n = 1 modules."""
+    import random
+    from paper_2403_07544_b200.plan import decode_ready
+    rng = random.Random(3)
+    for _ in range(200):
+        world = rng.randint(1, 8)
+        ready = [[rng.random() < 0.5 for _ in range(world)] for _ in range(12)]
+        bits = [sum(1 << r for r in range(world) if row[r]) for row in ready]
+        counts, roots = decode_ready(bits)
+        assert counts == [sum(row) for row in ready]
+        for row, c, r in zip(ready, counts, roots):
+            assert (r == row.index(True)) if c == 1 else (r == -1)
