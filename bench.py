@@ -284,6 +284,98 @@ def run_reduce(args, pk):
             "clocks": clk.summary(), "gpu_launches": launches}
 
 
+def run_exchange(args, pk):
+    """Config 2's whole reduce + update phase for all 8 ranks on one GPU:
+    option B (one mm_peer_update launch holding every rank's shards --
+    masked reads of the ready members' gradients, Adam on the owned shard,
+    bf16 weights into every member) against option A as the NCCL path does
+    it (sum into every member, then each member's replicated K3)."""
+    import torch
+    from paper_2403_07544_b200 import _native, ops
+    from paper_2403_07544_b200.configs import reduce_microbench
+    from paper_2403_07544_b200.peer import make_shard
+    dev = torch.device("cuda:0")
+    rng, mods = reduce_microbench()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    grads, weights, state = {}, {}, {}
+    for i, m in enumerate(mods):
+        for j in range(m.group):
+            t = torch.empty(m.n_params, device=dev)
+            if m.ready[j]:
+                t.normal_(generator=g)
+            else:
+                ops.memset(t, 0)
+            grads[(i, j)] = t
+            weights[(i, j)] = torch.empty(m.n_params, dtype=torch.bfloat16, device=dev)
+        # owners' shards are disjoint, so one master / m / v per module serves
+        # every emulated owner; option A keeps one replica per member
+        state[i] = [torch.zeros(m.n_params, device=dev) for _ in range(3)]
+    hp = _native.AdamHyper.make(beta1=0.9, beta2=0.998, eps=1e-8)
+    shards = []
+    for i, m in enumerate(mods):
+        mask = sum(1 << j for j, f in enumerate(m.ready) if f)
+        for j in range(m.group):
+            shards.append(make_shard([grads[(i, r)].data_ptr() for r in range(m.group)],
+                                     [weights[(i, r)].data_ptr() for r in range(m.group)], None,
+                                     *(t.data_ptr() for t in state[i]), m.n_params, j, mask,
+                                     1e-4, 1.0))
+
+    def option_b():
+        ops.peer_update(shards, hp)
+
+    sync_tab, adam_tab = [], []
+    for i, m in enumerate(mods):
+        sm = _native.SyncModule()
+        for j in range(m.group):
+            sm.bufs[j] = grads[(i, j)].data_ptr()
+        sm.out, sm.n_elems, sm.group_size = None, m.n_params, m.group
+        sm.used_mask = sum(1 << j for j, f in enumerate(m.ready) if f)
+        sync_tab.append(sm)
+        for j in range(m.group):  # replicated K3 (state replicas alias: traffic is what counts)
+            adam_tab.append(_native.AdamModule(
+                grad=grads[(i, j)].data_ptr(), master=state[i][0].data_ptr(),
+                exp_avg=state[i][1].data_ptr(), exp_avg_sq=state[i][2].data_ptr(),
+                param_bf16=weights[(i, j)].data_ptr(), n_elems=m.n_params, n_ready=1,
+                ready_index=-1, step_size=1e-4, inv_sqrt_bc2=1.0))
+
+    def option_a():
+        ops.sync_emulated(sync_tab, True)
+        ops.fused_update(adam_tab, hp)
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = _native.lib().mm_launch_count()
+        with ClockSampler(0) as clk:
+            e0.record()
+            for _ in range(args.steps):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / args.steps, _native.lib().mm_launch_count() - l0, clk
+
+    ms_a, _, _ = timed(option_a)
+    ms_b, launches, clk = timed(option_b)
+    # algorithmic HBM bytes of option B per module element: n ready fp32
+    # reads + 24 B of Adam state (master, m, v read + write) + g bf16 stores
+    nbytes = sum(m.n_params * (4 * m.n_ready + 24 + 2 * m.group) for m in mods)
+    gbs = nbytes / (ms_b * 1e-3) / 1e9
+    elems = sum(m.n_params for m in mods)
+    return {"metric": METRIC, "value": elems / (ms_b * 1e-3) / 1e9, "unit": "G module-params/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_b,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "config2 reduce + Adam + weight all-gather, option B, "
+                                   "8 ranks emulated in one GPU",
+                       "params": elems, "l2": "working set > 10 GB > L2",
+                       "option_a_ms": ms_a, "option_b_speedup": ms_a / ms_b},
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": gbs / pk["hbm_gbs"], "traffic": None},
+            "clocks": clk.summary(), "gpu_launches": launches}
+
+
 # ---------------------------------------------------------------------------
 # training step (configs 3-5)
 
@@ -430,15 +522,15 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="train", choices=["train", "reduce"])
+    ap.add_argument("--workload", default="train", choices=["train", "reduce", "exchange"])
     ap.add_argument("--config", default="config3", choices=["config3", "config4", "config5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
     pk = peaks()
-    if args.workload == "reduce":
-        line = run_reduce(args, pk)
+    if args.workload in ("reduce", "exchange"):
+        line = (run_reduce if args.workload == "reduce" else run_exchange)(args, pk)
         line["cpu_baseline"] = dict(zip(("value", "sample"), reduce_cpu_rate(3)), unit="GB/s",
                                     cores=1, kind="port")
         line["e2e"] = {"value": line["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,

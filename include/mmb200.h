@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 16
+#define MMB200_ABI_VERSION 17
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 
 int mm_abi_version(void);
@@ -126,6 +126,73 @@ typedef struct {
  * item on its group communicator, issued in array order (callers pass sorted
  * ModuleKey order) inside one ncclGroupStart/End. */
 int mm_reduce_modules(void* ctx, const mm_reduce_item* items, int n, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Option B of SURVEY §8(f) f1: K2 + K3 + the parameter all-gather as ONE
+ * streaming kernel over NVLink peer memory.  A module of group size g is cut
+ * into g contiguous shards; member r owns shard r and, for it:
+ *   total = sum over READY members j (ascending) of grad_j[shard]   -- masked
+ *           peer loads: unused members' buckets are never read, so they
+ *           need no zero fill (the 0 of Algorithm 1);
+ *   g = total / n * inv_loss_scale   (syncsim.py:148-149);
+ *   Adam on the owner's master / exp_avg / exp_avg_sq shard;
+ *   bf16(master) stored into EVERY member's weight bucket (the all-gather);
+ *   master fp32 also stored into other members' masters where non-NULL.
+ * Results are bit-identical to mm_sync_emulated(only_ready=1) followed by
+ * mm_fused_update (n_ready = 1) on the synced buffer.  mm_adam_hyper.zero_grad
+ * zeroes each ready member's shard after it is read (each element of each
+ * bucket has exactly one reader, its shard owner).  Peer pointers are CUDA-IPC mappings
+ * (mm_ipc_import) of the other ranks' buckets; with every "rank" resident on
+ * one GPU (tests, the config-2 bench) they are plain device pointers and one
+ * launch covers every member's shard -- the same kernel, no flag waits.
+ * Cross-rank ordering is by mm_peer_barrier before (gradients final) and
+ * after (peers done reading / writing this rank's buckets).
+ */
+typedef struct {
+    float* grad[MM_MAX_GROUP];      /* members' fp32 gradient buckets (whole module) */
+    uint16_t* param[MM_MAX_GROUP];  /* members' bf16 weight buckets, NULL = skip */
+    float* master_copy[MM_MAX_GROUP]; /* other members' fp32 masters, NULL = skip */
+    float* master;                  /* owner's fp32 master (whole module) */
+    float* exp_avg;
+    float* exp_avg_sq;
+    int64_t begin, end;             /* owned element range [begin, end) of the module */
+    int32_t group_size;
+    uint32_t ready_mask;            /* bit j: member j used the module this step */
+    float step_size, inv_sqrt_bc2;  /* as mm_adam_module */
+} mm_peer_shard;
+
+/* Shard r of g over n elements: [r*S, min(n, (r+1)*S)), S = ceil(n / g)
+ * rounded up to a multiple of 4 elements (16-byte vectors). */
+int64_t mm_peer_shard_begin(int64_t n_elems, int group_size, int member);
+
+int mm_peer_update(const mm_peer_shard* shards, int n, const mm_adam_hyper* hyper, void* stream);
+
+#define MM_PEER_MAX_RANKS 32
+/* Flag barrier over NVLink peer memory: for every peer i, store `epoch` into
+ * peer_flags[i][my_rank] (st.release.sys), then wait until
+ * local_flags[peer_rank[i]] >= epoch (ld.acquire.sys).  local_flags is this
+ * rank's MM_PEER_MAX_RANKS-entry uint32 array; peers hold IPC mappings of it.
+ * Epochs increase monotonically per rank pair.  A wait longer than
+ * timeout_ms traps (a CUDA error on the stream, never a silent hang). */
+typedef struct {
+    uint32_t* local_flags;
+    uint32_t* peer_flags[MM_PEER_MAX_RANKS];
+    int32_t peer_rank[MM_PEER_MAX_RANKS];
+    int32_t n_peers;
+    int32_t my_rank;
+    uint32_t epoch;
+    int32_t timeout_ms;
+} mm_peer_signal;
+
+int mm_peer_barrier(const mm_peer_signal* sig, void* stream);
+
+/* CUDA IPC for peer buckets.  export: handle of the allocation holding `ptr`
+ * and ptr's byte offset in it; import: map a peer's allocation (once per
+ * allocation, refcounted) and return base + offset; release: drop one
+ * reference of the mapping that holds `ptr`. */
+int mm_ipc_export(const void* ptr, uint8_t handle[64], uint64_t* offset);
+int mm_ipc_import(const uint8_t handle[64], uint64_t offset, void** ptr);
+int mm_ipc_release(void* ptr);
 
 /* ---------------------------------------------------------------------------
  * K4: bf16 GEMM on tcgen05 tensor cores (TMA-staged operands, fp32 TMEM

@@ -19,7 +19,7 @@ if os.environ.get("MM_LIB_VARIANT"):  # diagnostics: a tuning build from tools/b
                             "libmmb200.so")
 
 #: must match MMB200_ABI_VERSION in include/mmb200.h
-ABI_VERSION = 16
+ABI_VERSION = 17
 MAX_GROUP = 8
 
 
@@ -114,6 +114,40 @@ class ReduceItem(ctypes.Structure):
     ]
 
 
+class PeerShard(ctypes.Structure):
+    """mm_peer_shard: one member's owned shard of one module (option-B exchange)."""
+    _fields_ = [
+        ("grad", c_void_p * MAX_GROUP),
+        ("param", c_void_p * MAX_GROUP),
+        ("master_copy", c_void_p * MAX_GROUP),
+        ("master", c_void_p),
+        ("exp_avg", c_void_p),
+        ("exp_avg_sq", c_void_p),
+        ("begin", c_int64),
+        ("end", c_int64),
+        ("group_size", c_int32),
+        ("ready_mask", ctypes.c_uint32),
+        ("step_size", c_float),
+        ("inv_sqrt_bc2", c_float),
+    ]
+
+
+PEER_MAX_RANKS = 32
+
+
+class PeerSignal(ctypes.Structure):
+    """mm_peer_signal: the flag barrier over NVLink peer memory."""
+    _fields_ = [
+        ("local_flags", c_void_p),
+        ("peer_flags", c_void_p * PEER_MAX_RANKS),
+        ("peer_rank", c_int32 * PEER_MAX_RANKS),
+        ("n_peers", c_int32),
+        ("my_rank", c_int32),
+        ("epoch", ctypes.c_uint32),
+        ("timeout_ms", c_int32),
+    ]
+
+
 class LayerOffsets(ctypes.Structure):
     _fields_ = [(n, c_int64) for n in (
         "ln1_g", "ln1_b", "qkv_w", "qkv_b", "out_w", "out_b",
@@ -171,6 +205,13 @@ def _declare(h: ctypes.CDLL) -> None:
     sig("mm_group_destroy", c_int, c_void_p)
     sig("mm_ready_count", c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p)
     sig("mm_reduce_modules", c_int, c_void_p, POINTER(ReduceItem), c_int, c_void_p)
+    # option-B exchange: fused peer reduce + update + all-gather, flag barrier, IPC
+    sig("mm_peer_shard_begin", c_int64, c_int64, c_int, c_int)
+    sig("mm_peer_update", c_int, POINTER(PeerShard), c_int, POINTER(AdamHyper), c_void_p)
+    sig("mm_peer_barrier", c_int, POINTER(PeerSignal), c_void_p)
+    sig("mm_ipc_export", c_int, c_void_p, c_void_p, POINTER(ctypes.c_uint64))
+    sig("mm_ipc_import", c_int, c_void_p, ctypes.c_uint64, POINTER(c_void_p))
+    sig("mm_ipc_release", c_int, c_void_p)
     # layer kernels (K4-K8)
     sig("mm_launch_count", ctypes.c_ulonglong)
     sig("mm_gemm", c_int, c_void_p, c_void_p)

@@ -7,7 +7,14 @@ ranks, ascending; only ready members are read), then K3 runs per rank with
 the group ready counts.  This is the single-GPU stand-in for the NCCL path
 (the profiling recipe forbids running inter-dependent ranks as separate
 processes on one GPU) and gives the config-1 plumbing run on a B200.
+
+``exchange="peer"`` runs option B instead: one ``mm_peer_update`` launch
+holding EVERY emulated rank's shards (the multi-rank kernel emulated as one
+kernel over all ranks' data -- no flag barriers are needed inside a single
+launch), with the fp32 master replicated to every member so all emulated
+ranks hold complete masters; singletons keep the per-rank K3.
 """
+import math
 from __future__ import annotations
 
 from typing import Sequence
@@ -19,7 +26,11 @@ from .plan import ready_counts_all, task_modules
 
 
 class EmulatedCluster:
-    def __init__(self, tasks, topo, shape, world: int, device=None, seed: int = 0, **kw):
+    def __init__(self, tasks, topo, shape, world: int, device=None, seed: int = 0,
+                 exchange: str = "sync", **kw):
+        if exchange not in ("sync", "peer"):
+            raise ValueError(f"unknown exchange {exchange!r}")
+        self.exchange = exchange
         self.world = world
         self.ranks = [Engine(tasks, topo, shape, rank=r, world=1, device=device, seed=seed, **kw)
                       for r in range(world)]
@@ -44,6 +55,9 @@ class EmulatedCluster:
                 eng.forward_backward(task, db, eng.loss_sum)
             used_by_rank[r] = used
         counts = ready_counts_all(self.plan, used_by_rank)
+        if self.exchange == "peer":
+            self._peer_exchange(used_by_rank, counts)
+            return {"tasks": picks, "ready": dict(zip(self.plan.keys, counts))}
         table = []
         for k in self.plan.keys:
             members = self.plan.groups[k]
@@ -72,3 +86,33 @@ class EmulatedCluster:
                 per_rank.append(1 if (n >= 1 and len(self.plan.groups[k]) >= 2) else n)
             eng.fused_update(per_rank)
         return {"tasks": picks, "ready": dict(zip(self.plan.keys, counts))}
+
+    def _peer_exchange(self, used_by_rank, counts) -> None:
+        from .peer import make_shard
+        idx = self.plan.index()
+        shards = []
+        for k in self.plan.keys:
+            members = self.plan.groups[k]
+            if len(members) < 2:
+                continue
+            mask = sum(1 << j for j, r in enumerate(members) if k in used_by_rank.get(r, ()))
+            if not mask:
+                continue
+            sts = [self.ranks[r].states[k] for r in members]
+            for j, r in enumerate(members):
+                eng, st = self.ranks[r], sts[j]
+                a = eng.adam
+                st.step += 1
+                shards.append(make_shard(
+                    [s.grad.data_ptr() for s in sts], [s.weights.data_ptr() for s in sts],
+                    [s.master.data_ptr() for s in sts], st.master.data_ptr(),
+                    st.exp_avg.data_ptr(), st.exp_avg_sq.data_ptr(), st.master.numel(), j, mask,
+                    a.lr / (1.0 - a.beta1 ** st.step), 1.0 / math.sqrt(1.0 - a.beta2 ** st.step)))
+        a = self.ranks[0].adam
+        ops.peer_update(shards, _native.AdamHyper.make(beta1=a.beta1, beta2=a.beta2, eps=a.eps,
+                                                       weight_decay=a.weight_decay))
+        for r, eng in enumerate(self.ranks):
+            if r not in used_by_rank:
+                continue
+            singles = {k for k in eng.states if len(self.plan.groups[k]) < 2}
+            eng.fused_update(counts, only=singles)

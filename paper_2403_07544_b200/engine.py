@@ -173,7 +173,8 @@ class Engine:
 
     def __init__(self, tasks: Sequence[TaskSpec], topo: ClusterTopology, shape: ModelShape,
                  rank: int = 0, world: int = 1, device=None, seed: int = 0,
-                 adam: AdamConfig = AdamConfig(), store=None, masters=None):
+                 adam: AdamConfig = AdamConfig(), store=None, masters=None,
+                 exchange: Optional[str] = None):
         if shape.head_dim != 64:
             raise ValueError("the attention kernel is specialised for head_dim 64")
         self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
@@ -192,6 +193,17 @@ class Engine:
         self.adam = adam
         self.comm = CommGroups(self.plan, rank, world, self.device.index or 0, store) \
             if world > 1 else None
+        # K2 transport for world > 1: "nccl" (group all-reduce / broadcast, then
+        # the replicated K3) or "peer" (option B: one fused peer-memory kernel
+        # per exchange, paper_2403_07544_b200/peer.py)
+        self.exchange = exchange or os.environ.get("MM_EXCHANGE", "nccl")
+        if self.exchange not in ("nccl", "peer"):
+            raise ValueError(f"unknown exchange {self.exchange!r}")
+        self.peer = None
+        if world > 1 and self.exchange == "peer":
+            from .peer import PeerExchange
+            self.peer = PeerExchange(self, store)
+        self._bits = None
         self.loss_sum = torch.zeros(1, device=self.device)
         self.n_ready_dev = torch.zeros(len(self.plan.keys), dtype=torch.int32, device=self.device)
         self.flags_dev = torch.zeros(len(self.plan.keys), dtype=torch.int32, device=self.device)
@@ -558,7 +570,8 @@ class Engine:
                                   dec_done if i == len(tasks) - 1 else None)
         if counts_ready is not None:
             counts_ready.synchronize()  # waits for K1 only, not for the compute behind it
-            counts, self._roots = decode_ready(self._counts_host.tolist())
+            self._bits = self._counts_host.tolist()
+            counts, self._roots = decode_ready(self._bits)
         else:
             counts = flags
         if overlap:
@@ -607,6 +620,17 @@ class Engine:
                             max_ctas: int = 0) -> None:
         """K2 for the modules of ``exchange_order`` then K3 for every hosted
         module with n >= 1; ``only`` restricts both to a subset of keys."""
+        if self.peer is not None:
+            # option B: shared modules in one fused peer-memory kernel, then
+            # the local K3 for singletons
+            self.peer.run(self._bits, only=only, zero_grad=self.zero_in_update)
+            if self.zero_in_update:
+                self._dirty -= {k for k in self.states if len(self.plan.groups[k]) >= 2
+                                and (only is None or k in only)
+                                and (self._bits[self.index[k]] >> self.rank) & 1}
+            singles = {k for k in self.states if len(self.plan.groups[k]) < 2}
+            self.fused_update(counts, singles if only is None else singles & set(only), max_ctas)
+            return
         items = []
         if self.comm is not None:
             idx = self.plan.index()
@@ -654,6 +678,10 @@ class Engine:
 
     def close(self) -> None:
         self.sync_updates()
+        if self.peer is not None:
+            torch.cuda.synchronize(self.device)
+            self.peer.close()
+            self.peer = None
         if self.comm is not None:
             self.comm.close()
             self.comm = None

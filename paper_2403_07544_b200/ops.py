@@ -260,6 +260,49 @@ def sync_emulated(mods, only_ready: bool) -> None:
           "mm_sync_emulated")
 
 
+def peer_shard_begin(n_elems: int, group_size: int, member: int) -> int:
+    """First element of member's shard (mm_peer_shard_begin; shard r of g is
+    [begin(r), begin(r + 1)), begin(g) = n_elems)."""
+    return int(lib().mm_peer_shard_begin(n_elems, group_size, member))
+
+
+def peer_update(shards, hyper: "_native.AdamHyper") -> None:
+    """Option-B exchange: masked peer reduce + Adam + weight all-gather."""
+    if not shards:
+        return
+    arr = (_native.PeerShard * len(shards))(*shards)
+    LAUNCHES[0] += (len(shards) + 111) // 112
+    check(lib().mm_peer_update(arr, len(shards), ctypes.byref(hyper), stream_ptr()),
+          "mm_peer_update")
+
+
+def peer_barrier(sig: "_native.PeerSignal") -> None:
+    if sig.n_peers == 0:
+        return
+    LAUNCHES[0] += 1
+    check(lib().mm_peer_barrier(ctypes.byref(sig), stream_ptr()), "mm_peer_barrier")
+
+
+def ipc_export(t) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of t's allocation, t's byte offset in it)."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_uint64()
+    check(lib().mm_ipc_export(t.data_ptr(), h, ctypes.byref(off)), "mm_ipc_export")
+    return bytes(h.raw), int(off.value)
+
+
+def ipc_import(handle: bytes, offset: int) -> int:
+    """Device pointer of a peer's exported buffer (refcounted mapping)."""
+    assert len(handle) == 64
+    p = ctypes.c_void_p()
+    check(lib().mm_ipc_import(handle, offset, ctypes.byref(p)), "mm_ipc_import")
+    return int(p.value)
+
+
+def ipc_release(ptr: int) -> None:
+    check(lib().mm_ipc_release(ptr), "mm_ipc_release")
+
+
 def fused_update(mods, hyper: "_native.AdamHyper", ready_dev=None) -> None:
     arr = (_native.AdamModule * len(mods))(*mods)
     LAUNCHES[0] += 1

@@ -150,3 +150,38 @@ def exchange_order(plan: ModulePlan, counts, rank: int) -> list[ModuleKey]:
     mine = plan.hosted.get(rank, frozenset())
     return [k for k in plan.keys
             if k in mine and len(plan.groups[k]) >= 2 and counts[idx[k]] >= 1]
+
+
+def shard_begin(n_elems: int, group_size: int, member: int) -> int:
+    """First element of member's shard of a module (the host restatement of
+    mm_peer_shard_begin): S = ceil(n / g) rounded up to 4 elements, shard r =
+    [min(n, r*S), min(n, (r+1)*S))."""
+    s = -(-n_elems // group_size)
+    s = (s + 3) & ~3
+    return min(n_elems, s * member)
+
+
+def member_mask(bits: int, members: Sequence[int]) -> int:
+    """World-summed ready bitmask (rank bits) -> group bitmask (member bits,
+    member j = members[j], ascending ranks as in syncsim.py:337-340)."""
+    return sum(((int(bits) >> r) & 1) << j for j, r in enumerate(members))
+
+
+def peer_plan(plan: ModulePlan, rank: int, bits, only=None) -> list[tuple]:
+    """Option-B work of `rank` for one exchange: (key, members, member index,
+    group ready mask) for every hosted module with >= 2 members and n >= 1,
+    in sorted ModuleKey order.  Every member derives its own entry from the
+    same world-summed bits, so the shards of a module tile it exactly once."""
+    idx = plan.index()
+    mine = plan.hosted.get(rank, frozenset())
+    out = []
+    for k in plan.keys:
+        if k not in mine or (only is not None and k not in only):
+            continue
+        members = plan.groups[k]
+        if len(members) < 2:
+            continue
+        mask = member_mask(bits[idx[k]], members)
+        if mask:
+            out.append((k, members, members.index(rank), mask))
+    return out

@@ -337,3 +337,27 @@ def test_lazy_grad_zeroing_matches_memset(cuda):
                     assert float(st.grad.abs().max()) == 0.0, str(k)
     for k in masters[0]:
         assert rel(masters[1][k], masters[0][k]) < 1e-5, str(k)
+
+
+def test_config1_peer_exchange_bit_exact_vs_sync(cuda):
+    """Option B (one mm_peer_update launch over both emulated ranks' shards)
+    leaves every rank's weights and masters bit-identical to the sync +
+    per-rank K3 path over three steps of config 1."""
+    from paper_2403_07544_b200.cluster import EmulatedCluster
+    from paper_2403_07544_b200.engine import DeviceBatch
+    shape = configs.SHAPE_CFG1_GPU
+    w = configs.config1(shape)
+    runs = {}
+    for ex in ("sync", "peer"):
+        cl = EmulatedCluster(w.tasks, w.topo, shape, world=2, device=cuda, seed=0, exchange=ex)
+        for step in range(3):
+            hb = batches_for(2, 2, shape, seed=step)
+            cl.step(step, [[DeviceBatch(b, cuda) for b in hb[r]] for r in range(2)])
+        torch.cuda.synchronize()
+        runs[ex] = cl
+    for r in range(2):
+        for k, st in runs["sync"].ranks[r].states.items():
+            other = runs["peer"].ranks[r].states[k]
+            assert st.step == other.step, (r, str(k))
+            assert torch.equal(st.weights, other.weights), (r, str(k))
+            assert torch.equal(st.master, other.master), (r, str(k))

@@ -42,6 +42,36 @@ def test_struct_layouts():
     assert ctypes.sizeof(_native.AdamModule) == 5 * 8 + 8 + 4 + 4 + 4 + 4
     assert ctypes.sizeof(_native.AdamHyper) == 7 * 4 + 4 + 4  # + zero_grad
     assert ctypes.sizeof(_native.ReduceItem) == 8 + 8 + 8 + 4 + 4
+    assert ctypes.sizeof(_native.PeerShard) == 3 * 8 * 8 + 3 * 8 + 2 * 8 + 4 * 4
+    assert ctypes.sizeof(_native.PeerSignal) == 8 + 32 * 8 + 32 * 4 + 4 * 4
+
+
+def test_peer_shard_partition_matches_host_restatement():
+    """mm_peer_shard_begin (host code in the library) == plan.shard_begin, and
+    the g shards tile [0, n) with 16-byte aligned starts."""
+    from paper_2403_07544_b200.plan import shard_begin
+    L = _native.lib()
+    for n in (0, 1, 3, 4, 5, 7, 64, 1000, 100_003, 6_295_552, 56_000_001):
+        for g in range(1, 9):
+            bounds = [shard_begin(n, g, r) for r in range(g + 1)]
+            assert bounds == [L.mm_peer_shard_begin(n, g, r) for r in range(g + 1)]
+            assert bounds[0] == 0 and bounds[-1] == n
+            assert all(a <= b for a, b in zip(bounds, bounds[1:]))
+            assert all(b % 4 == 0 for b in bounds[:-1] if b < n)
+    assert L.mm_peer_shard_begin(10, 0, 0) == -1
+
+
+def test_peer_entry_points_reject_bad_arguments():
+    L = _native.lib()
+    sh = _native.PeerShard()
+    sh.group_size = 9
+    hp = _native.AdamHyper.make(0.9, 0.998, 1e-8)
+    assert L.mm_peer_update(ctypes.byref(sh), 1, ctypes.byref(hp), None) == -1
+    assert b"group size" in L.mm_last_error()
+    sig = _native.PeerSignal()
+    sig.n_peers = 33
+    assert L.mm_peer_barrier(ctypes.byref(sig), None) == -1
+    assert L.mm_ipc_release(ctypes.c_void_p(1234)) == -1
 
 
 def test_argument_errors_are_reported():

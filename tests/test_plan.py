@@ -169,3 +169,39 @@ def test_ready_bitmask_decode():
         assert counts == [sum(row) for row in ready]
         for row, c, r in zip(ready, counts, roots):
             assert (r == row.index(True)) if c == 1 else (r == -1)
+
+
+def test_peer_plan_shards_tile_every_module_once():
+    """Option B: from the same world-summed ready bits every member derives
+    its own shard of each shared module with n >= 1; over the members the
+    shards tile the module exactly once and all carry the same group mask."""
+    import random
+    from paper_2403_07544_b200 import configs
+    from paper_2403_07544_b200.plan import (Multiplexer, build_plan, member_mask, peer_plan,
+                                            ready_bits, shard_begin, task_modules)
+    w = configs.config5(world=8)  # sparse groups: sizes 1..4, many singletons
+    plan = build_plan(w.tasks, w.topo)
+    for step in range(3):
+        used = {}
+        for r in range(8):
+            mux = Multiplexer(plan, r, 0)
+            used[r] = set(task_modules(mux.pick(step)))
+        bits = [0] * len(plan.keys)
+        for r in range(8):
+            bits = [a + b for a, b in zip(bits, ready_bits(plan, r, used[r]))]
+        seen = {}
+        for r in range(8):
+            for k, members, j, mask in peer_plan(plan, r, bits):
+                assert members[j] == r and mask == member_mask(bits[plan.index()[k]], members)
+                seen.setdefault(k, []).append((j, mask))
+        n = 1000
+        for k, lst in seen.items():
+            g = len(plan.groups[k])
+            assert sorted(j for j, _ in lst) == list(range(g))
+            assert len({m for _, m in lst}) == 1
+            cover = sum(shard_begin(n, g, j + 1) - shard_begin(n, g, j) for j, _ in lst)
+            assert cover == n
+        for k in plan.keys:  # every shared module with a ready member is covered
+            i = plan.index()[k]
+            if len(plan.groups[k]) >= 2 and member_mask(bits[i], plan.groups[k]):
+                assert k in seen
