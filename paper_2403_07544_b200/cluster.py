@@ -14,8 +14,9 @@ kernel over all ranks' data -- no flag barriers are needed inside a single
 launch), with the fp32 master replicated to every member so all emulated
 ranks hold complete masters; singletons keep the per-rank K3.
 """
-import math
 from __future__ import annotations
+
+import math
 
 from typing import Sequence
 
@@ -38,6 +39,12 @@ class EmulatedCluster:
 
     def step(self, step_idx: int, batches: Sequence[Sequence[DeviceBatch]]) -> dict:
         """batches[r] = rank r's micro-batches for this step."""
+        used_by_rank, picks = self.compute(step_idx, batches)
+        counts = self.exchange_and_update(used_by_rank)
+        return {"tasks": picks, "ready": dict(zip(self.plan.keys, counts))}
+
+    def compute(self, step_idx: int, batches: Sequence[Sequence[DeviceBatch]]):
+        """Every rank's micro-batches: (used modules per rank, task picks)."""
         used_by_rank: dict[int, set] = {}
         picks = {}
         for r, eng in enumerate(self.ranks):
@@ -54,10 +61,14 @@ class EmulatedCluster:
                 used.update(fresh)
                 eng.forward_backward(task, db, eng.loss_sum)
             used_by_rank[r] = used
+        return used_by_rank, picks
+
+    def exchange_and_update(self, used_by_rank, exchange: str = None) -> list:
+        """Algorithm-1 exchange + optimizer update; returns the ready counts."""
         counts = ready_counts_all(self.plan, used_by_rank)
-        if self.exchange == "peer":
+        if (exchange or self.exchange) == "peer":
             self._peer_exchange(used_by_rank, counts)
-            return {"tasks": picks, "ready": dict(zip(self.plan.keys, counts))}
+            return counts
         table = []
         for k in self.plan.keys:
             members = self.plan.groups[k]
@@ -85,7 +96,7 @@ class EmulatedCluster:
                 n = counts[idx[k]]
                 per_rank.append(1 if (n >= 1 and len(self.plan.groups[k]) >= 2) else n)
             eng.fused_update(per_rank)
-        return {"tasks": picks, "ready": dict(zip(self.plan.keys, counts))}
+        return counts
 
     def _peer_exchange(self, used_by_rank, counts) -> None:
         from .peer import make_shard
