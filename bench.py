@@ -533,7 +533,7 @@ def main():
         line = (run_reduce if args.workload == "reduce" else run_exchange)(args, pk)
         line["cpu_baseline"] = dict(zip(("value", "sample"), reduce_cpu_rate(3)), unit="GB/s",
                                     cores=1, kind="port")
-        line["e2e"] = {"value": line["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+        line["e2e"] = {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
                        "d2h_bytes_per_step": 0, "note": "device-resident microbench"}
         print(json.dumps(line))
         return 0
