@@ -533,14 +533,15 @@ class Engine:
             ops.memset(self.states[k].grad, 0)
             self._dirty.discard(k)
 
-    def step(self, step_idx: int, batches: Sequence[DeviceBatch]) -> dict:
+    def step(self, step_idx: int, batches: Sequence[DeviceBatch], tasks=None) -> dict:
         """One optimizer step: len(batches) micro-batches (accum_count), then
         the Algorithm-1 exchange and the fused update.  Returns host-side
         bookkeeping; the loss stays on device in ``self.loss_sum``."""
         ops.memset(self.loss_sum, 0)
         # the multiplexer's picks (host RNG) fix this step's used set -- and so
         # the ready flags -- before any compute is issued (syncsim.py:353)
-        tasks = [self.mux.pick(step_idx) for _ in batches]
+        if tasks is None:  # else: picked by the caller (one pick per micro-batch, in order)
+            tasks = [self.mux.pick(step_idx) for _ in batches]
         picked = [t.id for t in tasks]
         used: set[ModuleKey] = set()
         for t in tasks:
@@ -720,9 +721,16 @@ class Trainer:
         self.h2d_bytes = sum(d.h2d_bytes for d in out)
         return out
 
-    def train_step(self, host_batches) -> float:
+    def train_step(self, host_batches=None, pipeline=None, accum: int = 1) -> float:
+        """host_batches: this rank's micro-batches (task-agnostic synthetic
+        data), or pipeline: a ``datapath.DataPipeline`` asked for the batch of
+        each task the multiplexer picks (``accum`` micro-batches)."""
+        tasks = None
+        if pipeline is not None:
+            tasks = [self.engine.mux.pick(self.step_idx) for _ in range(accum)]
+            host_batches = [pipeline.batch_for(t) for t in tasks]
         dbs = self.stage(host_batches)
-        self.engine.step(self.step_idx, dbs)
+        self.engine.step(self.step_idx, dbs, tasks=tasks)
         self.step_idx += 1
         self._loss_host.copy_(self.engine.loss_sum, non_blocking=True)
         torch.cuda.current_stream().synchronize()  # also retires the pinned staging

@@ -385,3 +385,32 @@ def test_config1_peer_exchange_bit_exact_vs_sync(cuda):
                     ts = want[owner][k][0]
                     assert torch.equal(st.weights[b:e_], ts[4][b:e_]), (step, r, str(k), j)
                     assert torch.equal(st.master[b:e_], ts[1][b:e_]), (step, r, str(k), j)
+
+
+def test_trainer_on_fullconfig_corpora(cuda, tmp_path):
+    """f2: the reference's FullConfig YAML + per-task corpora (pre-tokenized
+    ids) through DataPipeline -> Trainer.train_step: the batch of each
+    micro-batch comes from the task the multiplexer picked, in pick order."""
+    from paper_2403_07544_b200.datapath import DataPipeline, load_full_config
+    from paper_2403_07544_b200.engine import Trainer
+    from paper_2403_07544_b200.plan import Multiplexer, build_plan
+    cfg = load_full_config(os.path.join(ROOT, "tests", "golden", "fullconfig_config1.yaml"))
+    shape = configs.SHAPE_CFG1_GPU
+    rng = np.random.default_rng(0)
+    for t in cfg.task_list():
+        for p in (t.src_path, t.tgt_path):
+            os.makedirs(tmp_path / os.path.dirname(p), exist_ok=True)
+            with open(tmp_path / p, "w") as f:
+                for _ in range(200):  # some lines longer than max_len: clipped
+                    f.write(" ".join(map(str, rng.integers(4, shape.vocab, rng.integers(3, 50)))) + "\n")
+    pipe = DataPipeline(cfg.task_list(), tokens=256, root=str(tmp_path), capacity=24, pool=48,
+                        vocab=shape.vocab, max_len=shape.max_len)
+    seen = []
+    orig = pipe.batch_for
+    pipe.batch_for = lambda task: (seen.append(task.id), orig(task))[1]
+    tr = Trainer(cfg.task_list(), cfg.topology, shape, rank=0, world=1, device=cuda)
+    losses = [tr.train_step(pipeline=pipe, accum=2) for _ in range(3)]
+    tr.close()
+    assert all(np.isfinite(losses)) and all(l > 0 for l in losses)
+    mux = Multiplexer(build_plan(cfg.task_list(), cfg.topology), 0, 0)
+    assert seen == [mux.pick(s).id for s in range(3) for _ in range(2)]
