@@ -677,6 +677,51 @@ class Engine:
                                                      inv_loss_scale=1.0, max_ctas=max_ctas,
                                                      zero_grad=int(self.zero_in_update)))
 
+    # ------------------------------------------------------------- checkpoint
+    def save_checkpoint(self, root: str, extra: Optional[dict] = None) -> list[str]:
+        """Write this rank's share of a per-module checkpoint (f4,
+        ``checkpoint.py``): each module once per group by its lowest rank, or
+        with the peer exchange each member's own shard; plus this rank's
+        multiplexer state.  Returns the module files written."""
+        from . import checkpoint as C
+        from .plan import shard_begin
+        self.sync_updates()
+        torch.cuda.synchronize(self.device)
+        written = []
+        for k, st in self.states.items():
+            members = self.plan.groups[k]
+            n = st.master.numel()
+            host = {f: getattr(st, f).cpu().numpy() for f in C.FIELDS}
+            if self.peer is not None and len(members) >= 2:
+                j, g = members.index(self.rank), len(members)
+                b, e = shard_begin(n, g, j), shard_begin(n, g, j + 1)
+                written.append(C.write_module(root, k, {f: v[b:e] for f, v in host.items()},
+                                              st.step, n, (j, g, b, e)))
+            elif self.rank == members[0]:
+                written.append(C.write_module(root, k, host, st.step, n))
+        C.write_rank_state(root, self.rank, {"mux_rng": C.rng_to_json(self.mux.rng),
+                                             **(extra or {})})
+        return written
+
+    def load_checkpoint(self, root: str) -> dict:
+        """Restore every hosted module (master, moments, Adam step; bf16
+        weights re-cast from the master) and the multiplexer state; returns
+        this rank's extra host state."""
+        from . import checkpoint as C
+        self.sync_updates()
+        for k, st in self.states.items():
+            arrays, step = C.read_module(root, k, st.master.numel())
+            for f in C.FIELDS:
+                getattr(st, f).copy_(torch.from_numpy(arrays[f]))
+            st.step = step
+            ops.cast_bf16(st.master, st.weights)
+            ops.memset(st.grad, 0)
+            self._dirty.discard(k)
+        state = C.read_rank_state(root, self.rank)
+        C.rng_from_json(self.mux.rng, state.pop("mux_rng"))
+        torch.cuda.synchronize(self.device)
+        return state
+
     def close(self) -> None:
         self.sync_updates()
         if self.peer is not None:
@@ -735,6 +780,13 @@ class Trainer:
         self._loss_host.copy_(self.engine.loss_sum, non_blocking=True)
         torch.cuda.current_stream().synchronize()  # also retires the pinned staging
         return float(self._loss_host[0])
+
+    def save_checkpoint(self, root: str) -> list[str]:
+        """Every rank calls this after the same step (f4)."""
+        return self.engine.save_checkpoint(root, {"step_idx": self.step_idx})
+
+    def load_checkpoint(self, root: str) -> None:
+        self.step_idx = int(self.engine.load_checkpoint(root)["step_idx"])
 
     def close(self) -> None:
         self.engine.close()

@@ -414,3 +414,34 @@ def test_trainer_on_fullconfig_corpora(cuda, tmp_path):
     assert all(np.isfinite(losses)) and all(l > 0 for l in losses)
     mux = Multiplexer(build_plan(cfg.task_list(), cfg.topology), 0, 0)
     assert seen == [mux.pick(s).id for s in range(3) for _ in range(2)]
+
+
+def test_checkpoint_resume_bit_exact(cuda, tmp_path):
+    """f4: save after two steps, resume in a fresh trainer: restored state is
+    bit-identical, the multiplexer continues the same pick sequence and the
+    next step's loss matches (to the order of the cross-entropy's atomic
+    loss accumulation)."""
+    from paper_2403_07544_b200.engine import Trainer
+    shape = configs.SHAPE_CFG1_GPU
+    w = configs.config1(shape)
+    rng = np.random.default_rng(5)
+    batches = [[make_batch(rng, w.data, shape.vocab, sentences=16)] for _ in range(3)]
+    tr = Trainer(w.tasks, w.topo, shape, rank=0, world=1, device=cuda, seed=0)
+    for b in batches[:2]:
+        tr.train_step(b)
+    files = tr.save_checkpoint(str(tmp_path))
+    assert files and all(os.path.exists(f) for f in files)
+    saved = {k: (st.master.clone(), st.exp_avg.clone(), st.weights.clone(), st.step)
+             for k, st in tr.engine.states.items()}
+    next_pick = tr.engine.mux.rng.getstate()
+    loss3 = tr.train_step(batches[2])
+    tr.close()
+    tr2 = Trainer(w.tasks, w.topo, shape, rank=0, world=1, device=cuda, seed=123)  # other init
+    tr2.load_checkpoint(str(tmp_path))
+    assert tr2.step_idx == 2 and tr2.engine.mux.rng.getstate() == next_pick
+    for k, st in tr2.engine.states.items():
+        m, v, wgt, step = saved[k]
+        assert torch.equal(st.master, m) and torch.equal(st.exp_avg, v), str(k)
+        assert torch.equal(st.weights, wgt) and st.step == step, str(k)
+    assert abs(tr2.train_step(batches[2]) - loss3) <= 1e-6 * abs(loss3)
+    tr2.close()
