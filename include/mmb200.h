@@ -40,6 +40,17 @@ int mm_comm_cost(const double* params, int64_t n_modules, const int64_t* mod_tas
                  const int64_t* mod_task_idx, const int64_t* task_dev,
                  const int64_t* dev_node, int64_t n_devices, double w_intra, double w_inter,
                  double* out_per_module, double* total);
+/* f3: totals of n_moves candidate moves of one placement,
+ * evaluated in parallel on n_threads host threads (0 = all cores).  Move i
+ * is moves[3i..3i+2] = (kind, x, y): kind 0 relocates task x to device y,
+ * kind 1 swaps the devices of tasks x and y.  out[i] is bit-identical to
+ * mm_comm_cost's total on the moved placement, so a batched first-
+ * improvement search (allocator.local_search_batched) accepts exactly the
+ * moves of local_search (allocator.py:284-331). */
+int mm_comm_cost_moves(const double* params, int64_t n_modules, const int64_t* mod_task_off,
+                       const int64_t* mod_task_idx, const int64_t* task_dev, int64_t n_tasks,
+                       const int64_t* dev_node, int64_t n_devices, double w_intra, double w_inter,
+                       const int64_t* moves, int64_t n_moves, double* out, int n_threads);
 
 /* ---------------------------------------------------------------------------
  * Algorithm 1 over emulated devices that share one GPU: the literal

@@ -193,6 +193,9 @@ def _declare(h: ctypes.CDLL) -> None:
     sig("mm_comm_cost", c_int, POINTER(c_double), c_int64, POINTER(c_int64), POINTER(c_int64),
         POINTER(c_int64), POINTER(c_int64), c_int64, c_double, c_double, POINTER(c_double),
         POINTER(c_double))
+    sig("mm_comm_cost_moves", c_int, POINTER(c_double), c_int64, POINTER(c_int64), POINTER(c_int64),
+        POINTER(c_int64), c_int64, POINTER(c_int64), c_int64, c_double, c_double, POINTER(c_int64),
+        c_int64, POINTER(c_double), c_int)
     # Algorithm-1 sync, emulated devices on one GPU (sync_step syncsim.py:121-153)
     sig("mm_sync_emulated", c_int, POINTER(SyncModule), c_int, c_int, c_void_p)
     # K3 fused rescale + unscale + Adam + bf16 cast

@@ -112,11 +112,12 @@ def config4_tasks(world: int = 8) -> tuple[list[TaskSpec], ClusterTopology]:
 
 
 def config4(world: int = 8, budget: int = 10000) -> Workload:
-    from .allocator import initial_assignment, local_search
+    from .allocator import initial_assignment, local_search_batched
     from .sharing import enumerate_modules
     tasks, topo = config4_tasks(world)
     a0 = initial_assignment(tasks, topo, seed=0)
-    a = local_search(a0, tasks, enumerate_modules(tasks), topo, budget=budget, seed=0)
+    # batched evaluation: the same placement as local_search (f3), ~5x faster
+    a = local_search_batched(a0, tasks, enumerate_modules(tasks), topo, budget=budget, seed=0)
     placed = [t.with_device(a.placement[t.id]) for t in tasks]
     return Workload("config4", placed, topo, SHAPE_BASE,
                     DataSpec(8192, 3.0, 0.5, 4, 128, 1.1), world)

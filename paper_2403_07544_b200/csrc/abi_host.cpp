@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "mm_common.h"
@@ -103,6 +104,90 @@ extern "C" int mm_comm_cost(const double* params, int64_t n_modules, const int64
         acc += c;
     }
     *total = acc;
+    return 0;
+}
+
+// f3: cost of many candidate moves of one placement, on host threads.  Each
+// worker owns a copy of task_dev and the stamp arrays, applies a move, runs
+// the same loop as mm_comm_cost and reverts -- bit-identical totals, so the
+// batched local search accepts exactly the moves the sequential one does.
+namespace {
+double cost_of(const double* params, int64_t n_modules, const int64_t* off, const int64_t* idx,
+               const int64_t* task_dev, const int64_t* dev_node, double w_intra, double w_inter,
+               std::vector<int64_t>& dev_seen, std::vector<int64_t>& node_seen, int64_t stamp0) {
+    double acc = 0.0;
+    for (int64_t m = 0; m < n_modules; ++m) {
+        const int64_t st = stamp0 + m;
+        int64_t nd = 0, nn = 0;
+        for (int64_t j = off[m]; j < off[m + 1]; ++j) {
+            const int64_t d = task_dev[idx[j]];
+            if (dev_seen[d] == st) continue;
+            dev_seen[d] = st;
+            ++nd;
+            const int64_t node = dev_node[d];
+            if (node_seen[node] != st) {
+                node_seen[node] = st;
+                ++nn;
+            }
+        }
+        acc += nd > 0 ? params[m] * (w_intra * (double)(nd - 1) + (w_inter - w_intra) * (double)(nn - 1))
+                      : 0.0;
+    }
+    return acc;
+}
+}  // namespace
+
+extern "C" int mm_comm_cost_moves(const double* params, int64_t n_modules,
+                                  const int64_t* mod_task_off, const int64_t* mod_task_idx,
+                                  const int64_t* task_dev, int64_t n_tasks, const int64_t* dev_node,
+                                  int64_t n_devices, double w_intra, double w_inter,
+                                  const int64_t* moves, int64_t n_moves, double* out,
+                                  int n_threads) {
+    MM_CHECK_ARG(n_modules >= 0 && n_devices > 0 && n_tasks >= 0 && n_moves >= 0, "bad sizes");
+    MM_CHECK_ARG(n_moves == 0 || (moves && out), "NULL move arrays");
+    MM_CHECK_ARG(n_modules == 0 || (params && mod_task_off && mod_task_idx), "NULL module arrays");
+    MM_CHECK_ARG(n_tasks == 0 || task_dev, "NULL task_dev");
+    for (int64_t i = 0; i < n_tasks; ++i)
+        MM_CHECK_ARG(task_dev[i] >= 0 && task_dev[i] < n_devices, "task %lld on device %lld",
+                     (long long)i, (long long)task_dev[i]);
+    for (int64_t i = 0; i < n_moves; ++i) {
+        const int64_t k = moves[3 * i], x = moves[3 * i + 1], y = moves[3 * i + 2];
+        MM_CHECK_ARG((k == 0 || k == 1) && x >= 0 && x < n_tasks, "move %lld malformed", (long long)i);
+        MM_CHECK_ARG(k == 0 ? (y >= 0 && y < n_devices) : (y >= 0 && y < n_tasks),
+                     "move %lld target out of range", (long long)i);
+    }
+    int64_t max_node = 0;
+    for (int64_t i = 0; i < n_devices; ++i) max_node = std::max(max_node, dev_node[i]);
+    int T = n_threads > 0 ? n_threads : (int)std::max(1u, std::thread::hardware_concurrency());
+    T = (int)std::min<int64_t>(T, std::max<int64_t>(1, n_moves / 4));
+    auto work = [&](int t) {
+        std::vector<int64_t> dev(task_dev, task_dev + n_tasks);
+        std::vector<int64_t> dev_seen((size_t)n_devices, -1), node_seen((size_t)max_node + 1, -1);
+        int64_t stamp = 0;
+        for (int64_t i = t; i < n_moves; i += T) {
+            const int64_t k = moves[3 * i], x = moves[3 * i + 1], y = moves[3 * i + 2];
+            if (k == 0) {
+                const int64_t src = dev[x];
+                dev[x] = y;
+                out[i] = cost_of(params, n_modules, mod_task_off, mod_task_idx, dev.data(),
+                                 dev_node, w_intra, w_inter, dev_seen, node_seen, stamp);
+                dev[x] = src;
+            } else {
+                std::swap(dev[x], dev[y]);
+                out[i] = cost_of(params, n_modules, mod_task_off, mod_task_idx, dev.data(),
+                                 dev_node, w_intra, w_inter, dev_seen, node_seen, stamp);
+                std::swap(dev[x], dev[y]);
+            }
+            stamp += n_modules;  // fresh stamps: no reset of the seen arrays
+        }
+    };
+    if (T == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> pool;
+        for (int t = 0; t < T; ++t) pool.emplace_back(work, t);
+        for (auto& th : pool) th.join();
+    }
     return 0;
 }
 

@@ -121,3 +121,52 @@ def test_capacity_and_cover_errors():
              task("cc", "zz", ["y"], ["y"], intro=5000), task("dd", "zz", ["y"], ["y"], intro=5000)]
     topo = ClusterTopology(1, 2, 2)
     assert validate_assignment(initial_assignment(tasks, topo), tasks, topo) == []
+
+
+@pytest.mark.parametrize("window,threads", [(1, 1), (7, 2), (256, 0)])
+def test_batched_local_search_matches_reference_golden(golden, window, threads):
+    """f3: the batched move evaluation (mm_comm_cost_moves on host threads)
+    reproduces the reference's local_search results on every golden case."""
+    from paper_2403_07544_b200.allocator import local_search_batched
+    n = 0
+    for c in golden["allocator"]["cases"]:
+        if "error" in c:
+            continue
+        tasks = [mk(d) for d in c["tasks"]]
+        topo = ClusterTopology(*c["topo"])
+        a0 = initial_assignment(tasks, topo, seed=c["seed"])
+        a1 = local_search_batched(a0, tasks, enumerate_modules(tasks, 10), topo,
+                                  budget=c["budget"], seed=c["seed"], w_intra=1.0,
+                                  w_inter=c["w_inter"], window=window, threads=threads)
+        assert {k: str(v) for k, v in a1.placement.items()} == c["final"]
+        n += 1
+    assert n >= 20
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_batched_local_search_config4(golden, world):
+    from paper_2403_07544_b200.allocator import local_search_batched
+    rec = golden["groups_ready"][f"config4_w{world}"]
+    tasks, topo = configs.config4_tasks(world)
+    a0 = initial_assignment(tasks, topo, seed=0)
+    a = local_search_batched(a0, tasks, enumerate_modules(tasks), topo, budget=rec["budget"], seed=0)
+    assert {k: str(v) for k, v in sorted(a.placement.items())} == rec["placement"]
+
+
+def test_comm_cost_moves_equals_single_costs():
+    import numpy as np
+    from paper_2403_07544_b200.allocator import CostContext, comm_cost_moves
+    tasks, topo = configs.config4_tasks(8)
+    ctx = CostContext(tasks, enumerate_modules(tasks), topo)
+    rng = np.random.default_rng(0)
+    dev = rng.integers(0, topo.n_devices, len(ctx.tasks))
+    moves = [(0, int(rng.integers(len(dev))), int(rng.integers(topo.n_devices))) for _ in range(50)]
+    moves += [(1, int(a), int(b)) for a, b in rng.integers(0, len(dev), (50, 2))]
+    got = comm_cost_moves(ctx, dev, np.asarray(moves), threads=3)
+    for (k, x, y), c in zip(moves, got):
+        d = dev.copy()
+        if k == 0:
+            d[x] = y
+        else:
+            d[x], d[y] = d[y], d[x]
+        assert c.hex() == ctx.cost(d).hex()
