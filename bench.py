@@ -490,6 +490,7 @@ def run_train(args, pk):
                                f"{len(wl.tasks)} directions, {len(eng.plan.keys)} modules)",
                    "global_batch": int(tokens_all), "tokens": "target tokens per step",
                    "src_tokens_per_gpu": src_local, "parallelism": f"module-groups x{world}",
+                   "exchange": eng.exchange if world > 1 else "none (every group is a singleton)",
                    "l2": "working set per step > 126 MB L2 (weights+activations ~1.5 GB); no flush"},
         "roofline": {"bound": "tensor", "achieved": gemm_tflops,
                      "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
@@ -525,9 +526,13 @@ def main():
     ap.add_argument("--workload", default="train", choices=["train", "reduce", "exchange"])
     ap.add_argument("--config", default="config3", choices=["config3", "config4", "config5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default=None, choices=["nccl", "peer"],
+                    help="K2 transport for N > 1 (default nccl; peer = option-B kernel)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.exchange:
+        os.environ["MM_EXCHANGE"] = args.exchange
     pk = peaks()
     if args.workload in ("reduce", "exchange"):
         line = (run_reduce if args.workload == "reduce" else run_exchange)(args, pk)
