@@ -197,6 +197,86 @@ __global__ void __launch_bounds__(256, (COLS <= 512 ? 2 : 1)) ln_bwd_kernel(cons
     }
 }
 
+// Backward, one row per warp: dy, x AND the residual-gradient row dx are
+// all requested before the first reduction (one DRAM round trip per row), and
+// the dgamma / dbeta partials live in shared memory (a lane owns its columns,
+// plain read-modify-write, no conflicts) instead of registers, so the kernel
+// fits MINB CTAs per SM and the whole config-3 problem in one wave.
+template <int COLS, int MINB>
+__global__ void __launch_bounds__(256, MINB) ln_bwd_row_kernel(const float* __restrict__ dy,
+                                                               const float* __restrict__ x,
+                                                               const float* __restrict__ gamma,
+                                                               const float* __restrict__ mean,
+                                                               const float* __restrict__ rstd, float* dx,
+                                                               uint16_t* dx_bf16, float* dgamma,
+                                                               float* dbeta, int64_t rows) {
+    constexpr int V = COLS / 128;
+    extern __shared__ float4 red4[];  // [2][8 warps][COLS / 4]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float4* rg = red4 + warp * (COLS / 4);
+    float4* rb = red4 + (8 + warp) * (COLS / 4);
+#pragma unroll
+    for (int i = 0; i < V; ++i) rg[lane + 32 * i] = rb[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    pdl_wait_release();
+    for (int64_t row = int64_t(blockIdx.x) * 8 + warp; row < rows; row += int64_t(gridDim.x) * 8) {
+        const float4* dyr = reinterpret_cast<const float4*>(dy + row * COLS);
+        const float4* xr = reinterpret_cast<const float4*>(x + row * COLS);
+        float4* dxr = reinterpret_cast<float4*>(dx + row * COLS);
+        float4 d[V], xv[V], o[V];
+        const float mu = mean[row], rs = rstd[row];
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            d[i] = __ldcs(dyr + lane + 32 * i);
+            xv[i] = __ldcs(xr + lane + 32 * i);
+            o[i] = __ldcs(dxr + lane + 32 * i);
+        }
+        float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            float4& xh = xv[i];
+            xh = make_float4((xh.x - mu) * rs, (xh.y - mu) * rs, (xh.z - mu) * rs, (xh.w - mu) * rs);
+            float4 a = rg[lane + 32 * i], b = rb[lane + 32 * i];
+            a.x += d[i].x * xh.x; a.y += d[i].y * xh.y; a.z += d[i].z * xh.z; a.w += d[i].w * xh.w;
+            b.x += d[i].x; b.y += d[i].y; b.z += d[i].z; b.w += d[i].w;
+            rg[lane + 32 * i] = a;
+            rb[lane + 32 * i] = b;
+            const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma + 4 * lane + 128 * i));
+            d[i] = make_float4(d[i].x * gm.x, d[i].y * gm.y, d[i].z * gm.z, d[i].w * gm.w);  // dxhat
+            s1 += d[i].x + d[i].y + d[i].z + d[i].w;
+            s2 += d[i].x * xh.x + d[i].y * xh.y + d[i].z * xh.z + d[i].w * xh.w;
+        }
+        const float m1 = warp_sum(s1) * (1.f / COLS), m2 = warp_sum(s2) * (1.f / COLS);
+        uint2* dbr = reinterpret_cast<uint2*>(dx_bf16 + row * COLS);
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            float4 w = o[i];
+            w.x += rs * (d[i].x - m1 - xv[i].x * m2);
+            w.y += rs * (d[i].y - m1 - xv[i].y * m2);
+            w.z += rs * (d[i].z - m1 - xv[i].z * m2);
+            w.w += rs * (d[i].w - m1 - xv[i].w * m2);
+            dxr[lane + 32 * i] = w;
+            if (dx_bf16) {
+                uint2 b;
+                b.x = pack2(w.x, w.y);
+                b.y = pack2(w.z, w.w);
+                dbr[lane + 32 * i] = b;
+            }
+        }
+    }
+    __syncthreads();
+    // column sums over the 8 warps, one vector atomic per 4 columns per CTA
+    for (int c4 = threadIdx.x; c4 < 2 * (COLS / 4); c4 += 256) {
+        const int which = c4 / (COLS / 4), c = c4 - which * (COLS / 4);
+        float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            const float4 v = red4[(which * 8 + w) * (COLS / 4) + c];
+            sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+        }
+        atomicAdd(reinterpret_cast<float4*>(which ? dbeta : dgamma) + c, sum);
+    }
+}
+
 // ----------------------------------------------------------------------------
 // Embedding: out[r,:] = table[id[r],:] * scale + PE(pos[r]) (sinusoidal,
 // sin on even / cos on odd columns, OpenNMT layout).  One warp per row.
@@ -555,9 +635,28 @@ extern "C" int mm_layernorm_bwd(const float* dy, const float* x, const float* ga
                                 float* dgamma, float* dbeta, int64_t rows, int cols, void* stream) {
     MM_CHECK_ARG(dy && x && gamma && mean && rstd && dx && dgamma && dbeta, "NULL argument");
     if (rows == 0) return 0;
+    auto s = mm::as_stream(stream);
+    static const bool old_kernel = std::getenv("MM_LN_BWD_BATCHED") != nullptr;  // A/B diagnostics
+    if (cols == 512 && !old_kernel) {
+        // one row per warp, 2 CTAs/SM (3 CTAs/SM = 85 registers spills: 9.3 us;
+        // this 5.9 us vs 6.7 us for the batched kernel, graph back to back)
+        const int per_sm = 2;
+        const size_t smem = size_t(2) * 8 * cols * sizeof(float);
+        const unsigned g1 = static_cast<unsigned>(
+            std::min<int64_t>((rows + 7) / 8, int64_t(per_sm) * mm::num_sms()));
+        static bool attr = false;
+        if (!attr) {
+            MM_CUDA_TRY(cudaFuncSetAttribute(ln_bwd_row_kernel<512, 2>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            attr = true;
+        }
+        MM_CUDA_TRY(mm::launch_pdl(ln_bwd_row_kernel<512, 2>, dim3(g1), dim3(256), smem, s, dy, x, gamma,
+                                   mean, rstd, dx, dx_bf16, dgamma, dbeta, rows));
+        MM_LAUNCH_CHECK("ln_bwd_row_kernel");
+        return 0;
+    }
     const unsigned grid = static_cast<unsigned>(
         std::min<int64_t>((rows + 8 * kLnRows - 1) / (8 * kLnRows), 4 * mm::num_sms()));
-    auto s = mm::as_stream(stream);
     if (cols == 512)
         MM_CUDA_TRY(mm::launch_pdl(ln_bwd_kernel<512>, dim3(grid), dim3(256), 0, s, dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows));
     else if (cols == 1024)

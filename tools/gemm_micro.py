@@ -15,6 +15,7 @@ cases = [  # name, m, n, k, a_k, b_k, epi
     ("dgrad ff2", T, 2048, 512, True, False, ops.EPI_BF16),
     ("dgrad ff1", T, 512, 2048, True, False, ops.EPI_F32),
     ("dgrad gen", T, 512, 32000, True, False, ops.EPI_F32),
+    ("dgrad gen acc", T, 512, 32000, True, False, ops.EPI_F32_ACCUM),
     ("wgrad out", 512, 512, T, False, False, ops.EPI_F32_ACCUM),
     ("wgrad qkv", 1536, 512, T, False, False, ops.EPI_F32_ACCUM),
     ("wgrad ff1", 2048, 512, T, False, False, ops.EPI_F32_ACCUM),
