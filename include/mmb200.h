@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 17
+#define MMB200_ABI_VERSION 18
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 
 int mm_abi_version(void);
@@ -269,10 +269,12 @@ int mm_gemm_timing(int mode, double* flops, float* ms, int* launches);
  * dev_buf[8 * cta + slot] (NULL disables); see gemm.cu for the slots */
 int mm_gemm_trace(unsigned long long* dev_buf);
 /* Host: greedy packing of consecutive sequences into attention work groups
- * (<= cap rows per side, 32-row aligned per sequence); out holds 2 * n_seq
- * int32 (first, count) pairs; *foot = rows of the largest group.  Replaces
- * the per-batch numpy loop of data.attention_groups on the step's host path. */
-int mm_attention_groups(const int32_t* cu_q, const int32_t* cu_k, int n_seq, int cap,
+ * (<= cap rows per side, each sequence rounded up to `align` rows: 32 for
+ * the mma.sync kernels' shared-memory tiles, 1 for the tcgen05 backward);
+ * out holds 2 * n_seq int32 (first, count) pairs; *foot = rows of the
+ * largest group.  Replaces the per-batch numpy loop of
+ * data.attention_groups on the step's host path. */
+int mm_attention_groups(const int32_t* cu_q, const int32_t* cu_k, int n_seq, int cap, int align,
                         int32_t* out, int* n_groups, int* foot);
 /* diagnostics: mode 1 starts recording CUDA events around the non-GEMM
  * launches mm_task_fwd_bwd issues; mode 0 stops, synchronises and returns the
@@ -321,6 +323,13 @@ typedef struct {
     int32_t cap;
     int32_t total_k;       /* key rows (the K / V tensors' extent, for TMA maps) */
     int32_t flags;         /* internal: 0 */
+    /* optional: the same sequences packed WITHOUT the 32-row padding
+     * (mm_attention_groups with align = 1) for the tcgen05 backward, whose
+     * units load one contiguous 128-row box per side; NULL = use `groups`.
+     * Fewer, fuller units: 56 -> ~35 groups per config-3 table. */
+    const int32_t* tc_groups;
+    int32_t n_tc_groups;
+    int32_t pad0;
 } mm_attn_args;
 
 int mm_attention_fwd(const mm_attn_args* a, void* stream);
@@ -381,6 +390,8 @@ typedef struct {
     const int32_t *groups_src, *groups_tgt, *groups_cross;                     /* device */
     int32_t n_seq, n_src, n_tgt, max_src, max_tgt;
     int32_t ng_src, cap_src, ng_tgt, cap_tgt, ng_cross, cap_cross;
+    const int32_t *tcg_src, *tcg_tgt, *tcg_cross; /* unpadded groups (align 1), may be NULL */
+    int32_t ntc_src, ntc_tgt, ntc_cross, pad0;
 } mm_batch;
 
 /* dec_done (cudaEvent_t, may be NULL) is recorded on `stream` as soon as the

@@ -19,7 +19,7 @@ if os.environ.get("MM_LIB_VARIANT"):  # diagnostics: a tuning build from tools/b
                             "libmmb200.so")
 
 #: must match MMB200_ABI_VERSION in include/mmb200.h
-ABI_VERSION = 17
+ABI_VERSION = 18
 MAX_GROUP = 8
 
 
@@ -177,7 +177,9 @@ class BatchDesc(ctypes.Structure):
                                         "cu_tgt", "groups_src", "groups_tgt", "groups_cross")] + \
                [(n, c_int32) for n in ("n_seq", "n_src", "n_tgt", "max_src", "max_tgt",
                                        "ng_src", "cap_src", "ng_tgt", "cap_tgt", "ng_cross",
-                                       "cap_cross")]
+                                       "cap_cross")] + \
+               [(n, c_void_p) for n in ("tcg_src", "tcg_tgt", "tcg_cross")] + \
+               [(n, c_int32) for n in ("ntc_src", "ntc_tgt", "ntc_cross", "pad0")]
 
 
 def _declare(h: ctypes.CDLL) -> None:
@@ -221,7 +223,7 @@ def _declare(h: ctypes.CDLL) -> None:
     sig("mm_gemm_grouped", c_int, c_void_p, c_int, c_void_p)
     sig("mm_gemm_timing", c_int, c_int, POINTER(c_double), POINTER(c_float), POINTER(c_int))
     sig("mm_step_timing", c_int, c_int, POINTER(c_float), POINTER(c_int))
-    sig("mm_attention_groups", c_int, c_void_p, c_void_p, c_int, c_int, c_void_p, POINTER(c_int),
+    sig("mm_attention_groups", c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, POINTER(c_int),
         POINTER(c_int))
     sig("mm_gemm_trace", c_int, c_void_p)
     sig("mm_layernorm_fwd", c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

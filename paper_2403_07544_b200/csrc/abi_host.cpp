@@ -198,15 +198,15 @@ extern "C" int mm_comm_cost_moves(const double* params, int64_t n_modules,
 // its own.  out[2 g] = first sequence, out[2 g + 1] = count (out holds
 // 2 * n_seq entries); *foot = rows of the largest group (either side).
 extern "C" int mm_attention_groups(const int32_t* cu_q, const int32_t* cu_k, int n_seq, int cap,
-                                   int32_t* out, int* n_groups, int* foot) {
+                                   int align, int32_t* out, int* n_groups, int* foot) {
     MM_CHECK_ARG(cu_q && cu_k && out && n_groups && foot, "NULL argument");
-    MM_CHECK_ARG(n_seq >= 0 && cap > 0, "bad sizes");
+    MM_CHECK_ARG(n_seq >= 0 && cap > 0 && align >= 1, "bad sizes");
     int g = 0, fp = 0;
     for (int i = 0; i < n_seq;) {
         int j = i, sq = 0, sk = 0;
         while (j < n_seq) {
-            const int pq = (cu_q[j + 1] - cu_q[j] + 31) / 32 * 32;
-            const int pk = (cu_k[j + 1] - cu_k[j] + 31) / 32 * 32;
+            const int pq = (cu_q[j + 1] - cu_q[j] + align - 1) / align * align;
+            const int pk = (cu_k[j + 1] - cu_k[j] + align - 1) / align * align;
             if (j != i && (sq + pq > cap || sk + pk > cap)) break;
             sq += pq;
             sk += pk;

@@ -1084,18 +1084,22 @@ extern "C" int mm_attention_bwd(const mm_attn_args* a, void* stream) {
         if (int st = tca::head_map(&bp.mk, a->k, a->total_k, a->ldk, cols)) return st;
         if (int st = tca::head_map(&bp.mv, a->v, a->total_k, a->ldv, cols)) return st;
         if (int st = tca::head_map(&bp.mdo, a->d_o, a->total_q, a->ldo, cols)) return st;
-        bp.cu_q = a->cu_q; bp.cu_k = a->cu_k; bp.groups = a->groups; bp.lse = a->lse;
+        // unpadded groups when the caller built them: a unit is one 128-row
+        // TMA box per side, so the mma.sync kernels' 32-row padding only
+        // multiplies the units (config 3: ~35 instead of 56 groups per table)
+        const bool tcg = a->tc_groups != nullptr && a->n_tc_groups > 0;
+        bp.cu_q = a->cu_q; bp.cu_k = a->cu_k; bp.groups = tcg ? a->tc_groups : a->groups; bp.lse = a->lse;
         bp.dq = a->dq; bp.dk = a->dk; bp.dv = a->dv;
         bp.ld_dq = a->ld_dq; bp.ld_dk = a->ld_dk; bp.ld_dv = a->ld_dv;
         bp.total_q = a->total_q; bp.causal = a->causal; bp.scale = a->scale;
-        bp.n_groups = a->n_groups; bp.heads = a->heads;
+        bp.n_groups = tcg ? a->n_tc_groups : a->n_groups; bp.heads = a->heads;
         static bool attr = false;
         if (!attr) {
             MM_CUDA_TRY(cudaFuncSetAttribute(tca::attn_bwd_tc_kernel,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, tca::kSmemBytes));
             attr = true;
         }
-        const int units = a->n_groups * a->heads;
+        const int units = bp.n_groups * a->heads;
         MM_CUDA_TRY(mm::launch_pdl(tca::attn_bwd_tc_kernel, dim3(std::min(units, mm::num_sms())),
                                    dim3(tca::kThreads), tca::kSmemBytes, mm::as_stream(stream), bp));
         MM_LAUNCH_CHECK("attn_bwd_tc_kernel");

@@ -232,8 +232,10 @@ struct Driver {
     mm_attn_args attn(const uint16_t* q, const uint16_t* k, const uint16_t* v, int64_t ldq,
                       int64_t ldkv, uint16_t* o, float* lse, const int32_t* cu_q,
                       const int32_t* cu_k, int max_q, int max_k, bool causal, int total_q,
-                      const int32_t* groups, int ng, int cap) {
+                      const int32_t* groups, int ng, int cap, const int32_t* tcg = nullptr,
+                      int ntc = 0) {
         mm_attn_args a{};
+        a.tc_groups = tcg; a.n_tc_groups = ntc;
         a.q = q; a.k = k; a.v = v; a.o = o; a.lse = lse;
         a.cu_q = cu_q; a.cu_k = cu_k;
         a.ldq = ldq; a.ldk = ldkv; a.ldv = ldkv; a.ldo = d;
@@ -282,7 +284,7 @@ struct Driver {
         sv.lse = ar.get<float>(int64_t(H) * T);
         mm_attn_args a = attn(sv.q, sv.kv, sv.kv + d, d, 2 * d, sv.a, sv.lse, b.cu_tgt, b.cu_src,
                               b.max_tgt, b.max_src, false, int(T), b.groups_cross, b.ng_cross,
-                              b.cap_cross);
+                              b.cap_cross, b.tcg_cross, b.ntc_cross);
         TIMED(2, mm_attention_fwd(&a, s));
         out = ar.get<float>(T * d);
         if (int e = residual(sv.a, wb(st, o->cout_w), out, T, d, wf(st, o->cout_b), x, next, ln_out)) return e;
@@ -325,7 +327,7 @@ struct Driver {
     }
 
     int self_bwd(Layer& L, float* dx, uint16_t*& dx_bf, int64_t T, const int32_t* cu, int maxlen,
-                 bool causal, const int32_t* groups, int ng, int cap) {
+                 bool causal, const int32_t* groups, int ng, int cap, const int32_t* tcg, int ntc) {
         const mm_stack* st = L.st;
         const mm_layer_offsets* o = L.o;
         SelfSave& sv = L.self;
@@ -335,7 +337,7 @@ struct Driver {
         TRY(dgrad(dx_bf, wb(st, o->out_w), da, T, d, d, MM_EPI_BF16));
         uint16_t* dqkv = ar.get<uint16_t>(T * 3 * d);
         mm_attn_args a = attn(sv.qkv, sv.qkv + d, sv.qkv + 2 * d, 3 * d, 3 * d, sv.a, sv.lse, cu, cu,
-                              maxlen, maxlen, causal, int(T), groups, ng, cap);
+                              maxlen, maxlen, causal, int(T), groups, ng, cap, tcg, ntc);
         a.d_o = da; a.dq = dqkv; a.dk = dqkv + d; a.dv = dqkv + 2 * d;
         a.ld_dq = a.ld_dk = a.ld_dv = 3 * d;
         TIMED(3, mm_attention_bwd(&a, s));
@@ -363,7 +365,7 @@ struct Driver {
         uint16_t* dkv = ar.get<uint16_t>(S * 2 * d);
         mm_attn_args a = attn(sv.q, sv.kv, sv.kv + d, d, 2 * d, sv.a, sv.lse, b.cu_tgt, b.cu_src,
                               b.max_tgt, b.max_src, false, int(T), b.groups_cross, b.ng_cross,
-                              b.cap_cross);
+                              b.cap_cross, b.tcg_cross, b.ntc_cross);
         a.d_o = da; a.dq = dq; a.dk = dkv; a.dv = dkv + d;
         a.ld_dq = d; a.ld_dk = a.ld_dv = 2 * d;
         TIMED(3, mm_attention_bwd(&a, s));
@@ -469,7 +471,8 @@ struct Driver {
         for (int l = nd - 1; l >= 0; --l) {
             if (int e = ffn_bwd(dec_l[l], dy, dy_bf, Tt)) return e;
             if (int e = cross_bwd(dec_l[l], dy, dy_bf, mem, dmem)) return e;
-            if (int e = self_bwd(dec_l[l], dy, dy_bf, Tt, b.cu_tgt, b.max_tgt, true, b.groups_tgt, b.ng_tgt, b.cap_tgt)) return e;
+            if (int e = self_bwd(dec_l[l], dy, dy_bf, Tt, b.cu_tgt, b.max_tgt, true, b.groups_tgt, b.ng_tgt, b.cap_tgt,
+                                 b.tcg_tgt, b.ntc_tgt)) return e;
         }
         TIMED(5, mm_embed_bwd(b.tgt_in, dy, t.dec_emb.grad + t.dec_emb.emb, Tt, d, scale, s));
         if (int e = flush_wgrads()) return e;  // decoder side + generator
@@ -482,7 +485,8 @@ struct Driver {
                              g(lnf_e, lnf_e->lnf_g), g(lnf_e, lnf_e->lnf_b), Ts, d, s));
         for (int l = ne - 1; l >= 0; --l) {
             if (int e = ffn_bwd(enc_l[l], dx, dx_bf, Ts)) return e;
-            if (int e = self_bwd(enc_l[l], dx, dx_bf, Ts, b.cu_src, b.max_src, false, b.groups_src, b.ng_src, b.cap_src)) return e;
+            if (int e = self_bwd(enc_l[l], dx, dx_bf, Ts, b.cu_src, b.max_src, false, b.groups_src, b.ng_src, b.cap_src,
+                                 b.tcg_src, b.ntc_src)) return e;
         }
         TIMED(5, mm_embed_bwd(b.src, dx, t.enc_emb.grad + t.enc_emb.emb, Ts, d, scale, s));
         if (int e = flush_wgrads()) return e;  // encoder side

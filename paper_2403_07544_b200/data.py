@@ -117,15 +117,17 @@ def make_batch(rng: np.random.Generator, spec, vocab: int, sentences: Optional[i
 ATTN_CAP = 128  # rows per CTA group (each side), see include/mmb200.h
 
 
-def attention_groups(cu_q: np.ndarray, cu_k: np.ndarray, cap: int = ATTN_CAP):
+def attention_groups(cu_q: np.ndarray, cu_k: np.ndarray, cap: int = ATTN_CAP, align: int = 32):
     """Greedy packing of consecutive sequences into attention CTA groups:
-    each sequence takes ceil(len/32)*32 rows; a group holds at most ``cap``
-    rows per side (a longer sequence gets a group of its own).  Returns
-    (int32 [2*n_groups] of (first, count), rows footprint of the largest group)."""
+    each sequence takes ceil(len/align)*align rows (32 for the mma.sync
+    kernels' shared-memory tiles, 1 for the tcgen05 backward's 128-row TMA
+    boxes); a group holds at most ``cap`` rows per side (a longer sequence
+    gets a group of its own).  Returns (int32 [2*n_groups] of (first, count),
+    rows footprint of the largest group)."""
     lq = np.diff(cu_q).astype(np.int64)
     lk = np.diff(cu_k).astype(np.int64)
-    pq = (lq + 31) // 32 * 32
-    pk = (lk + 31) // 32 * 32
+    pq = (lq + align - 1) // align * align
+    pk = (lk + align - 1) // align * align
     out = []
     foot = 0
     i, n = 0, len(lq)

@@ -46,7 +46,8 @@ class AdamConfig:
     weight_decay: float = 0.0
 
 
-def native_attention_groups(cu_q: np.ndarray, cu_k: np.ndarray, cap: int = ATTN_CAP):
+def native_attention_groups(cu_q: np.ndarray, cu_k: np.ndarray, cap: int = ATTN_CAP,
+                            align: int = 32):
     """data.attention_groups through the C ABI (mm_attention_groups): the
     numpy loop cost ~0.12 ms per table on every step's host path."""
     import ctypes
@@ -55,7 +56,7 @@ def native_attention_groups(cu_q: np.ndarray, cu_k: np.ndarray, cap: int = ATTN_
     n = len(cq) - 1
     out = np.empty(2 * max(n, 1), dtype=np.int32)
     ng, foot = ctypes.c_int(), ctypes.c_int()
-    _native.check(_native.lib().mm_attention_groups(cq.ctypes.data, ck.ctypes.data, n, cap,
+    _native.check(_native.lib().mm_attention_groups(cq.ctypes.data, ck.ctypes.data, n, cap, align,
                                                     out.ctypes.data, ctypes.byref(ng), ctypes.byref(foot)),
                   "mm_attention_groups")
     return out[:2 * ng.value], foot.value
@@ -76,6 +77,10 @@ class DeviceBatch:
             g, cap = native_attention_groups(cq, ck)
             arrs[name] = g
             groups[name] = (len(g) // 2, cap)
+            # unpadded packing for the tcgen05 backward (fewer, fuller units)
+            t, _ = native_attention_groups(cq, ck, align=1)
+            arrs["tc" + name[4:]] = t
+            groups["tc" + name[4:]] = (len(t) // 2,)
         names = list(self.FIELDS) + list(groups)
         sizes = [len(arrs[f]) for f in names]
         total = sum(sizes)
@@ -94,12 +99,18 @@ class DeviceBatch:
             view = dev[off:off + n]
             setattr(self, f, (view,) + groups[f] if f in groups else view)
             off += n
+        # padded table -> its unpadded twin (the per-op Python path's lookup)
+        self.tc_of = {id(self.attn_src): self.tc_src, id(self.attn_tgt): self.tc_tgt,
+                      id(self.attn_cross): self.tc_cross}
         self.n_seq = b.n_seq
         self.n_src, self.n_tgt = b.n_src, b.n_tgt
         self.max_src, self.max_tgt = b.max_src, b.max_tgt
         self._keep = host  # keep the pinned staging alive until the copy retires
         gs, gt, gc = self.attn_src, self.attn_tgt, self.attn_cross
+        ts, tt, tc = self.tc_src, self.tc_tgt, self.tc_cross
         self.desc = _native.BatchDesc(
+            tcg_src=ts[0].data_ptr(), tcg_tgt=tt[0].data_ptr(), tcg_cross=tc[0].data_ptr(),
+            ntc_src=ts[1], ntc_tgt=tt[1], ntc_cross=tc[1],
             src=self.src.data_ptr(), src_pos=self.src_pos.data_ptr(), cu_src=self.cu_src.data_ptr(),
             tgt_in=self.tgt_in.data_ptr(), tgt_pos=self.tgt_pos.data_ptr(),
             labels=self.labels.data_ptr(), cu_tgt=self.cu_tgt.data_ptr(),
@@ -261,6 +272,8 @@ class Engine:
                           st.g(name + ".g"), st.g(name + ".b"))
 
     def _attn_args(self, q, k, v, o, lse, cu_q, cu_k, n_seq, max_q, max_k, causal, **kw):
+        if kw.get("d_o") is None:
+            kw.setdefault("tc_groups", False)  # forward: the padded tables only
         return ops.attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, self.shape.heads, max_q,
                                   max_k, causal, **kw)
 
@@ -327,6 +340,11 @@ class Engine:
         ops.gemm(df, st.w(p + "ff1.w"), dh, b_kmajor=False, epilogue=ops.EPI_F32)
         self._ln_bwd(st, p + "ln2", dh, x_in, mean, rstd, dx, dx_bf)
 
+    def _tc(self, groups):
+        """The unpadded twin of a staged padded group table (None: build it)."""
+        db = getattr(self, "_cur_db", None)
+        return None if groups is None or db is None else db.tc_of.get(id(groups))
+
     def _self_bwd(self, st, p, rec, dx, dx_bf, cu, n_seq, max_len, causal):
         _, x_in, h, mean, rstd, qkv, a, lse, groups = rec
         d = self.shape.d_model
@@ -339,7 +357,7 @@ class Engine:
         ops.attention_bwd(self._attn_args(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], a, lse, cu,
                                           cu, n_seq, max_len, max_len, causal, d_o=da,
                                           dq=dqkv[:, :d], dk=dqkv[:, d:2 * d], dv=dqkv[:, 2 * d:],
-                                          groups=groups))
+                                          groups=groups, tc_groups=self._tc(groups)))
         ops.gemm(dqkv, h, st.g(p + "qkv.w"), a_kmajor=False, b_kmajor=False,
                  epilogue=ops.EPI_F32_ACCUM, dbias=st.g(p + "qkv.b"))
         dh = torch.empty(T, d, device=self.device)
@@ -359,7 +377,8 @@ class Engine:
         ops.attention_bwd(self._attn_args(q, kv[:, :d], kv[:, d:], a, lse, db.cu_tgt, db.cu_src,
                                           db.n_seq, db.max_tgt, db.max_src, False, d_o=da, dq=dq,
                                           dk=dkv[:, :d], dv=dkv[:, d:],
-                                          groups=getattr(db, "attn_cross", None)))
+                                          groups=getattr(db, "attn_cross", None),
+                                          tc_groups=self._tc(getattr(db, "attn_cross", None))))
         self._tr(p + "dckv", dkv)
         self._tr(p + "dca", da)
         self._tr(p + "dcx_out", dx)
@@ -448,6 +467,7 @@ class Engine:
         """Per-op Python path (same kernels, same order); used for diagnostics
         (intermediate tracing) and as the native driver's cross-check."""
         shp, dev, d = self.shape, self.device, self.shape.d_model
+        self._cur_db = db
         ek, dk = embedding_keys(task)
         emb_e, emb_d = self.states[ek], self.states[dk]
         Ts, Tt = db.n_src, db.n_tgt

@@ -46,6 +46,7 @@ class AttnArgs(ctypes.Structure):
         ("scale", ctypes.c_float), ("total_q", ctypes.c_int32),
         ("groups", ctypes.c_void_p), ("n_groups", ctypes.c_int32), ("cap", ctypes.c_int32),
         ("total_k", ctypes.c_int32), ("flags", ctypes.c_int32),
+        ("tc_groups", ctypes.c_void_p), ("n_tc_groups", ctypes.c_int32), ("pad0", ctypes.c_int32),
     ]
 
 
@@ -195,16 +196,22 @@ def cast_bf16(x, y) -> None:
 
 
 def attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, heads, max_q, max_k, causal,
-                   d_o=None, dq=None, dk=None, dv=None, groups=None) -> AttnArgs:
+                   d_o=None, dq=None, dk=None, dv=None, groups=None, tc_groups=None) -> AttnArgs:
     """groups: (device int32 tensor [2*n_groups], n_groups, cap) from
-    data.attention_groups; built here from cu_q / cu_k when omitted."""
+    data.attention_groups (32-row aligned); tc_groups: the unpadded packing
+    (align = 1) for the tcgen05 backward.  Both are built here from cu_q /
+    cu_k when omitted; tc_groups=False keeps the backward on `groups`."""
     hd = 64
+    import numpy as _np
+    from .data import attention_groups
     if groups is None:
-        from .data import attention_groups
-        import numpy as _np
         gh, cap = attention_groups(_np.asarray(cu_q.cpu()), _np.asarray(cu_k.cpu()))
         groups = (torch.from_numpy(gh).to(q.device), len(gh) // 2, cap)
+    if tc_groups is None:
+        th, _ = attention_groups(_np.asarray(cu_q.cpu()), _np.asarray(cu_k.cpu()), align=1)
+        tc_groups = (torch.from_numpy(th).to(q.device), len(th) // 2)
     gt, n_groups, cap = groups
+    tt, n_tc = (None, 0) if tc_groups is False else tc_groups[:2]
     args = AttnArgs(
         q=q.data_ptr(), k=k.data_ptr(), v=v.data_ptr(), o=o.data_ptr(), lse=lse.data_ptr(),
         d_o=_ptr(d_o), dq=_ptr(dq), dk=_ptr(dk), dv=_ptr(dv),
@@ -214,10 +221,11 @@ def attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, heads, max_q, max_k, caus
         ld_dv=dv.stride(0) if dv is not None else 0,
         n_seq=n_seq, heads=heads, head_dim=hd, causal=int(causal), max_q=max_q, max_k=max_k,
         scale=1.0 / math.sqrt(hd), total_q=q.shape[0],
-        groups=gt.data_ptr(), n_groups=n_groups, cap=cap, total_k=k.shape[0])
-    # the struct holds raw pointers: keep the device group table (possibly
+        groups=gt.data_ptr(), n_groups=n_groups, cap=cap, total_k=k.shape[0],
+        tc_groups=tt.data_ptr() if tt is not None else None, n_tc_groups=n_tc)
+    # the struct holds raw pointers: keep the device group tables (possibly
     # built here) alive as long as the args are
-    args._keep = (gt,)
+    args._keep = (gt, tt)
     return args
 
 

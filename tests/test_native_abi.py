@@ -44,6 +44,8 @@ def test_struct_layouts():
     assert ctypes.sizeof(_native.ReduceItem) == 8 + 8 + 8 + 4 + 4
     assert ctypes.sizeof(_native.PeerShard) == 3 * 8 * 8 + 3 * 8 + 2 * 8 + 4 * 4
     assert ctypes.sizeof(_native.PeerSignal) == 8 + 32 * 8 + 32 * 4 + 4 * 4
+    from paper_2403_07544_b200 import ops
+    assert ctypes.sizeof(ops.AttnArgs) == 11 * 8 + 7 * 8 + 8 * 4 + 8 + 4 * 4 + 8 + 8
 
 
 def test_peer_shard_partition_matches_host_restatement():
@@ -142,6 +144,22 @@ def test_attention_groups_native_matches_numpy():
         cq = np.concatenate([[0], np.cumsum(lq)]).astype(np.int32)
         ck = np.concatenate([[0], np.cumsum(lk)]).astype(np.int32)
         for cap in (64, 128, 256):
-            g1, f1 = attention_groups(cq, ck, cap)
-            g2, f2 = native_attention_groups(cq, ck, cap)
-            assert np.array_equal(g1, g2) and f1 == f2, (trial, cap)
+            for align in (32, 1, 8):
+                g1, f1 = attention_groups(cq, ck, cap, align)
+                g2, f2 = native_attention_groups(cq, ck, cap, align)
+                assert np.array_equal(g1, g2) and f1 == f2, (trial, cap, align)
+        # the two packings route every sequence to exactly one backward kernel:
+        # a sequence of <= 128 rows per side sits in an unpadded group of <= 128
+        # rows (tcgen05) and in a padded group of <= 128 actual rows (skipped by
+        # mma.sync); a longer one is alone in both (mma.sync only)
+        gp, _ = attention_groups(cq, ck, 128, 32)
+        gt, _ = attention_groups(cq, ck, 128, 1)
+        def rows(g, cu):
+            return [int(cu[g[2 * i] + g[2 * i + 1]] - cu[g[2 * i]]) for i in range(len(g) // 2)]
+        tc_seqs = {s for i in range(len(gt) // 2)
+                   if rows(gt, cq)[i] <= 128 and rows(gt, ck)[i] <= 128
+                   for s in range(gt[2 * i], gt[2 * i] + gt[2 * i + 1])}
+        ms_seqs = {s for i in range(len(gp) // 2)
+                   if not (rows(gp, cq)[i] <= 128 and rows(gp, ck)[i] <= 128)
+                   for s in range(gp[2 * i], gp[2 * i] + gp[2 * i + 1])}
+        assert tc_seqs | ms_seqs == set(range(n)) and not (tc_seqs & ms_seqs), trial
