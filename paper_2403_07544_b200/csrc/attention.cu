@@ -1034,12 +1034,18 @@ extern "C" int mm_attn_trace_read(unsigned long long* host, int n) {
 extern "C" int mm_attention_fwd(const mm_attn_args* a, void* stream) {
     if (int st = check(a, false)) return st;
     if (a->n_seq == 0) return 0;
-    // The tcgen05 forward is opt-in (MM_ATTN_TC_FWD=1): measured slower than
-    // the mma.sync kernel at config-3 shapes (13.1 vs 10.0 us: 83 KB of smem
-    // and 256 TMEM columns allow two CTAs per SM against four, and the
-    // forward has too little MMA work per CTA to amortise that).
+    // On the padded (32-row aligned) groups the tcgen05 forward lost to the
+    // mma.sync kernel (13.1 vs 10.0 us: 83 KB of smem and 256 TMEM columns
+    // allow two CTAs per SM against four).
+    // With the unpadded group table (fewer, fuller units) the tcgen05 forward
+    // wins whenever its units fit one wave at two CTAs per SM (config 3 self
+    // attention: 8.3 vs 10.0 us); beyond that (config-3 cross attention: 40+
+    // groups x 8 heads) the mma.sync kernel's four CTAs per SM win (9.5 vs
+    // 11.7 us).  MM_ATTN_TC_FWD=1 / 0 forces either kernel (tests, A/B).
     const char* tcf = std::getenv("MM_ATTN_TC_FWD");
-    const bool use_tc = tcf && tcf[0] == '1';
+    const bool have_tcg = a->tc_groups != nullptr && a->n_tc_groups > 0;
+    const bool use_tc = tcf ? tcf[0] == '1'
+                            : have_tcg && int64_t(a->n_tc_groups) * a->heads <= 2 * int64_t(mm::num_sms());
     mm_attn_args b = *a;
     if (use_tc && a->total_k > 0) {
         tca::FwdParams fp{};
@@ -1047,7 +1053,8 @@ extern "C" int mm_attention_fwd(const mm_attn_args* a, void* stream) {
         if (int st = tca::head_map(&fp.mq, a->q, a->total_q, a->ldq, cols)) return st;
         if (int st = tca::head_map(&fp.mk, a->k, a->total_k, a->ldk, cols)) return st;
         if (int st = tca::head_map(&fp.mv, a->v, a->total_k, a->ldv, cols)) return st;
-        fp.cu_q = a->cu_q; fp.cu_k = a->cu_k; fp.groups = a->groups; fp.lse = a->lse;
+        const bool tcg = a->tc_groups != nullptr && a->n_tc_groups > 0;  // unpadded packing
+        fp.cu_q = a->cu_q; fp.cu_k = a->cu_k; fp.groups = tcg ? a->tc_groups : a->groups; fp.lse = a->lse;
         fp.o = a->o; fp.ldo = a->ldo;
         fp.total_q = a->total_q; fp.causal = a->causal; fp.scale = a->scale;
         static bool attr = false;
@@ -1056,7 +1063,8 @@ extern "C" int mm_attention_fwd(const mm_attn_args* a, void* stream) {
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, tca::kFwdSmemBytes));
             attr = true;
         }
-        MM_CUDA_TRY(mm::launch_pdl(tca::attn_fwd_tc_kernel, dim3(a->heads, a->n_groups), dim3(tca::kFwdThreads),
+        MM_CUDA_TRY(mm::launch_pdl(tca::attn_fwd_tc_kernel, dim3(a->heads, tcg ? a->n_tc_groups : a->n_groups),
+                                   dim3(tca::kFwdThreads),
                                    tca::kFwdSmemBytes, mm::as_stream(stream), fp));
         MM_LAUNCH_CHECK("attn_fwd_tc_kernel");
         if (a->cap <= tca::kRows) return 0;

@@ -248,8 +248,8 @@ struct Driver {
 
     // ------------------------------------------------------------ forward
     int self_fwd(Layer& L, const float* x, float*& out, int64_t T, const int32_t* cu, int maxlen,
-                 bool causal, const int32_t* groups, int ng, int cap, const LnOut* pre,
-                 const LnNext* next, LnOut* ln_out) {
+                 bool causal, const int32_t* groups, int ng, int cap, const int32_t* tcg, int ntc,
+                 const LnOut* pre, const LnNext* next, LnOut* ln_out) {
         const mm_stack* st = L.st;
         const mm_layer_offsets* o = L.o;
         SelfSave& sv = L.self;
@@ -260,7 +260,7 @@ struct Driver {
         sv.a = ar.get<uint16_t>(T * d);
         sv.lse = ar.get<float>(int64_t(H) * T);
         mm_attn_args a = attn(sv.qkv, sv.qkv + d, sv.qkv + 2 * d, 3 * d, 3 * d, sv.a, sv.lse, cu, cu,
-                              maxlen, maxlen, causal, int(T), groups, ng, cap);
+                              maxlen, maxlen, causal, int(T), groups, ng, cap, tcg, ntc);
         a.v = sv.qkv + 2 * d;
         TIMED(2, mm_attention_fwd(&a, s));
         out = ar.get<float>(T * d);
@@ -416,7 +416,7 @@ struct Driver {
             const LnNext n1 = l + 1 < ne ? LnNext{enc_l[l + 1].st, enc_l[l + 1].o->ln1_g, enc_l[l + 1].o->ln1_b}
                                          : LnNext{lnf_e, lnf_e->lnf_g, lnf_e->lnf_b};
             if (int e = self_fwd(enc_l[l], x, y, Ts, b.cu_src, b.max_src, false, b.groups_src, b.ng_src,
-                                 b.cap_src, &pre, &n2, &ln2)) return e;
+                                 b.cap_src, b.tcg_src, b.ntc_src, &pre, &n2, &ln2)) return e;
             if (int e = ffn_fwd(enc_l[l], y, x, Ts, &ln2, &n1, &next_out)) return e;
             pre = next_out;
         }
@@ -446,7 +446,7 @@ struct Driver {
             const LnNext n1 = l + 1 < nd ? LnNext{dec_l[l + 1].st, dec_l[l + 1].o->ln1_g, dec_l[l + 1].o->ln1_b}
                                          : LnNext{lnf_d, lnf_d->lnf_g, lnf_d->lnf_b};
             if (int e = self_fwd(dec_l[l], y, y1, Tt, b.cu_tgt, b.max_tgt, true, b.groups_tgt, b.ng_tgt,
-                                 b.cap_tgt, &dpre, &nc, &lnc)) return e;
+                                 b.cap_tgt, b.tcg_tgt, b.ntc_tgt, &dpre, &nc, &lnc)) return e;
             if (int e = cross_fwd(dec_l[l], y1, y2, mem, &lnc, &n2, &ln2)) return e;
             if (int e = ffn_fwd(dec_l[l], y2, y, Tt, &ln2, &n1, &next_out)) return e;
             dpre = next_out;

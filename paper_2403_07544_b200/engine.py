@@ -272,8 +272,10 @@ class Engine:
                           st.g(name + ".g"), st.g(name + ".b"))
 
     def _attn_args(self, q, k, v, o, lse, cu_q, cu_k, n_seq, max_q, max_k, causal, **kw):
-        if kw.get("d_o") is None:
-            kw.setdefault("tc_groups", False)  # forward: the padded tables only
+        if kw.get("d_o") is None and "tc_groups" not in kw:
+            kw["tc_groups"] = self._tc(kw.get("groups"))  # None -> built by attention_args
+            if kw["tc_groups"] is None and kw.get("groups") is not None:
+                kw["tc_groups"] = False  # staged padded table without a twin
         return ops.attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, self.shape.heads, max_q,
                                   max_k, causal, **kw)
 

@@ -307,7 +307,10 @@ def test_fused_layernorm_driver_matches_python_path(cuda, d_model, heads, ffn, m
         torch.cuda.synchronize()
         grads.append({k: st.grad.cpu().numpy().copy() for k, st in eng.states.items()})
         losses.append(eng.loss_sum.item())
-    assert abs(losses[0] - losses[1]) <= 1e-5 * abs(losses[1])
+    # 3e-5: the fused epilogue's LayerNorm row sums (DSMEM partials) round
+    # differently from the standalone kernel's, and every bf16 rounding
+    # downstream (the tcgen05 forward's bf16 P among them) can flip
+    assert abs(losses[0] - losses[1]) <= 3e-5 * abs(losses[1])
     for k in grads[0]:
         if np.abs(grads[1][k]).max() > 0:
             assert rel_norm(grads[0][k], grads[1][k]) < 2e-2, str(k)

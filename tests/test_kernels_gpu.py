@@ -308,8 +308,7 @@ def test_attention(cuda, causal, maxlen, tc_fwd, monkeypatch):
     """Forward (mma.sync, or the opt-in tcgen05 kernel) and backward (tcgen05
     for groups within 128 rows, mma.sync for longer sequences) vs an fp32
     PyTorch reference."""
-    if tc_fwd:
-        monkeypatch.setenv("MM_ATTN_TC_FWD", "1")
+    monkeypatch.setenv("MM_ATTN_TC_FWD", "1" if tc_fwd else "0")
     from paper_2403_07544_b200 import ops
     rng = np.random.default_rng(maxlen + causal)
     heads, d = 8, 512
