@@ -10,6 +10,7 @@ rng = np.random.default_rng(0)
 CFG5 = os.environ.get("ATTN_CFG") == "5"  # config-5 shapes: 16384 tokens, 16 heads, lognormal(3.2, 0.6) <= 256
 d, heads = (1024, 16) if CFG5 else (512, 8)
 MU, SIG, HI, TOK = (3.2, 0.6, 256, 16384) if CFG5 else (3.0, 0.5, 128, 4096)
+HI = int(os.environ.get("ATTN_HI", HI))  # length clip override (A/B of the long-sequence path)
 
 
 def lengths(total, mu, sigma, lo, hi):
