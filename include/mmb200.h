@@ -276,6 +276,11 @@ int mm_gemm_trace(unsigned long long* dev_buf);
  * data.attention_groups on the step's host path. */
 int mm_attention_groups(const int32_t* cu_q, const int32_t* cu_k, int n_seq, int cap, int align,
                         int32_t* out, int* n_groups, int* foot);
+/* Host: an order of a batch's n sentence pairs (source / target lengths)
+ * that packs into few attention groups: first-fit-decreasing 2-D bins of
+ * `cap` rows per side, bins in creation order, over-long pairs last.
+ * perm[j] = input index of the j-th pair (data.attention_order). */
+int mm_attention_order(const int32_t* len_s, const int32_t* len_t, int n, int cap, int32_t* perm);
 /* diagnostics: mode 1 starts recording CUDA events around the non-GEMM
  * launches mm_task_fwd_bwd issues; mode 0 stops, synchronises and returns the
  * summed time (ms) and launch count per category: 0 LayerNorm fwd, 1 LayerNorm

@@ -191,6 +191,44 @@ extern "C" int mm_comm_cost_moves(const double* params, int64_t n_modules,
     return 0;
 }
 
+// Order of a batch's sentence pairs for the attention work groups: first-fit
+// decreasing 2-D bin packing (capacity `cap` rows on both the source and the
+// target side), bins emitted in creation order, pairs longer than `cap` on
+// either side last in input order.  Consecutive packing (mm_attention_groups)
+// of this order needs no more groups than FFD has bins -- for config 3 about
+// 34 instead of ~41 cross-attention groups in input order.  The order only
+// permutes independent sentence pairs (the loss is a sum over them).
+extern "C" int mm_attention_order(const int32_t* len_s, const int32_t* len_t, int n, int cap,
+                                  int32_t* perm) {
+    MM_CHECK_ARG(n >= 0 && cap > 0 && (n == 0 || (len_s && len_t && perm)), "bad arguments");
+    std::vector<int> items, big;
+    for (int i = 0; i < n; ++i) (len_s[i] > cap || len_t[i] > cap ? big : items).push_back(i);
+    std::stable_sort(items.begin(), items.end(), [&](int x, int y) {
+        const int mx = std::max(len_s[x], len_t[x]), my = std::max(len_s[y], len_t[y]);
+        if (mx != my) return mx > my;
+        return len_s[x] + len_t[x] > len_s[y] + len_t[y];
+    });
+    std::vector<int> bs, bt;                 // bin fill per side
+    std::vector<std::vector<int>> bins;
+    for (int i : items) {
+        size_t b = 0;
+        while (b < bins.size() && (bs[b] + len_s[i] > cap || bt[b] + len_t[i] > cap)) ++b;
+        if (b == bins.size()) {
+            bins.emplace_back();
+            bs.push_back(0);
+            bt.push_back(0);
+        }
+        bins[b].push_back(i);
+        bs[b] += len_s[i];
+        bt[b] += len_t[i];
+    }
+    int k = 0;
+    for (const auto& bin : bins)
+        for (int i : bin) perm[k++] = i;
+    for (int i : big) perm[k++] = i;
+    return 0;
+}
+
 // Greedy packing of consecutive sequences into attention CTA groups (the
 // host half of K5; data.attention_groups is the same algorithm in numpy and
 // the cross-check): each sequence takes ceil(len / 32) * 32 rows per side; a

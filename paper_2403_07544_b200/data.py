@@ -21,6 +21,7 @@ import numpy as np
 
 BOS, EOS = 1, 2
 FIRST_ID = 4
+ATTN_CAP_ROWS = 128  # rows per attention work group and side (tcgen05 TMEM lanes)
 
 
 @dataclasses.dataclass
@@ -82,10 +83,45 @@ def _lengths(rng, n, spec) -> np.ndarray:
     return np.clip(x, spec.len_min, spec.len_max).astype(np.int64)
 
 
+def attention_order_py(ls, lt, cap: int = 128) -> np.ndarray:
+    """Host restatement of mm_attention_order (first-fit decreasing 2-D bins
+    of ``cap`` rows per side, bins in creation order, over-long pairs last)."""
+    ls, lt = [int(x) for x in ls], [int(x) for x in lt]
+    n = len(ls)
+    big = [i for i in range(n) if ls[i] > cap or lt[i] > cap]
+    items = [i for i in range(n) if not (ls[i] > cap or lt[i] > cap)]
+    items.sort(key=lambda i: (-max(ls[i], lt[i]), -(ls[i] + lt[i])))  # stable
+    bins, fill = [], []
+    for i in items:
+        for b, (fs, ft) in enumerate(fill):
+            if fs + ls[i] <= cap and ft + lt[i] <= cap:
+                break
+        else:
+            b = len(bins)
+            bins.append([])
+            fill.append((0, 0))
+        bins[b].append(i)
+        fill[b] = (fill[b][0] + ls[i], fill[b][1] + lt[i])
+    return np.asarray([i for bin_ in bins for i in bin_] + big, dtype=np.int64)
+
+
+def attention_order(ls, lt, cap: int = ATTN_CAP_ROWS) -> np.ndarray:
+    """Sentence-pair order that packs into few attention work groups
+    (mm_attention_order, host C++): a permutation of range(len(ls))."""
+    from . import _native
+    a = np.ascontiguousarray(ls, dtype=np.int32)
+    b = np.ascontiguousarray(lt, dtype=np.int32)
+    perm = np.empty(max(len(a), 1), dtype=np.int32)
+    _native.check(_native.lib().mm_attention_order(a.ctypes.data, b.ctypes.data, len(a), cap,
+                                                   perm.ctypes.data), "mm_attention_order")
+    return perm[:len(a)].astype(np.int64)
+
+
 def make_batch(rng: np.random.Generator, spec, vocab: int, sentences: Optional[int] = None,
-               ids: Optional[ZipfIds] = None) -> Batch:
+               ids: Optional[ZipfIds] = None, order: bool = True) -> Batch:
     """One micro-batch: ``sentences`` pairs if given, else ``spec.tokens_per_gpu``
-    target tokens."""
+    target tokens.  order=True lays the pairs out in attention_order (an
+    order of independent pairs; fewer, fuller attention work groups)."""
     ids = ids or ZipfIds(vocab, spec.zipf_s)
     if sentences is not None:
         ls, lt = _lengths(rng, sentences, spec), _lengths(rng, sentences, spec)
@@ -98,6 +134,9 @@ def make_batch(rng: np.random.Generator, spec, vocab: int, sentences: Optional[i
             lt_l.append(b)
             tot += b
         ls, lt = np.asarray(ls_l), np.asarray(lt_l)
+    if order and len(ls) > 1:
+        perm = attention_order(ls, lt)
+        ls, lt = ls[perm], lt[perm]
     cu_s = np.concatenate([[0], np.cumsum(ls)]).astype(np.int32)
     cu_t = np.concatenate([[0], np.cumsum(lt)]).astype(np.int32)
     src = ids.draw(rng, int(cu_s[-1]))

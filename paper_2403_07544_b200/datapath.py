@@ -189,10 +189,12 @@ class CorpusStream:
         return [next(self._it) for _ in range(n)]
 
 
-def pack_pairs(pairs: Sequence[tuple[Sequence[int], Sequence[int]]], tokens: int) -> Batch:
-    """Pack pairs in order until the target side holds ``tokens`` tokens
+def pack_pairs(pairs: Sequence[tuple[Sequence[int], Sequence[int]]], tokens: int,
+               order: bool = True) -> Batch:
+    """Take pairs in order until the target side holds ``tokens`` tokens
     (each target contributes len + 1: BOS-shifted input / EOS-terminated
-    labels); the pair that crosses the budget is truncated (>= 1 token)."""
+    labels; the pair that crosses the budget is truncated, >= 1 token), then
+    lay the taken pairs out in data.attention_order (order=True)."""
     ss, ts, used = [], [], 0
     for s, t in pairs:
         if used >= tokens:
@@ -204,6 +206,10 @@ def pack_pairs(pairs: Sequence[tuple[Sequence[int], Sequence[int]]], tokens: int
         used += len(t) + 1
     if not ss:
         raise ValueError("no pairs to pack")
+    if order and len(ss) > 1:
+        from .data import attention_order
+        perm = attention_order([len(x) for x in ss], [len(t) + 1 for t in ts])
+        ss, ts = [ss[i] for i in perm], [ts[i] for i in perm]
     ls = np.array([len(s) for s in ss])
     lt = np.array([len(t) + 1 for t in ts])
     cu_s = np.concatenate([[0], np.cumsum(ls)]).astype(np.int32)

@@ -85,12 +85,12 @@ def _corpus(tmp_path, n=50, seed=0):
 
 def test_pack_pairs_layout():
     pairs = [([4, 5, 6], [7, 8]), ([9], [10, 11, 12, 13]), ([14, 15], [16])]
-    b = pack_pairs(pairs, tokens=100)
+    b = pack_pairs(pairs, tokens=100, order=False)
     assert b.cu_src.tolist() == [0, 3, 4, 6] and b.cu_tgt.tolist() == [0, 3, 8, 10]
     assert b.tgt_in.tolist() == [BOS, 7, 8, BOS, 10, 11, 12, 13, BOS, 16]
     assert b.labels.tolist() == [7, 8, EOS, 10, 11, 12, 13, EOS, 16, EOS]
     assert b.src_pos.tolist() == [0, 1, 2, 0, 0, 1] and b.tgt_pos.tolist()[:4] == [0, 1, 2, 0]
-    cut = pack_pairs(pairs, tokens=5)  # 3 + truncated second pair (1 token + EOS)
+    cut = pack_pairs(pairs, tokens=5, order=False)  # 3 + truncated second pair (1 token + EOS)
     assert cut.n_tgt == 5 and cut.labels.tolist() == [7, 8, EOS, 10, EOS]
 
 
@@ -125,3 +125,31 @@ def test_pipeline_from_fullconfig(tmp_path):
         assert 0 < b.n_tgt <= 128
     with pytest.raises(FileNotFoundError):
         DataPipeline(cfg.task_list(), tokens=128, root=str(tmp_path / "missing"))
+
+
+def test_attention_order_native_matches_restatement_and_packs_tighter():
+    from paper_2403_07544_b200.data import attention_groups, attention_order, attention_order_py
+    rng = np.random.default_rng(4)
+    for t in range(100):
+        n = int(rng.integers(0, 300))
+        ls, lt = rng.integers(1, 160, n), rng.integers(1, 160, n)
+        perm = attention_order(ls, lt)
+        assert np.array_equal(perm, attention_order_py(ls, lt)), t
+        assert sorted(perm.tolist()) == list(range(n))
+        if n:
+            cs = np.concatenate([[0], np.cumsum(ls)]).astype(np.int32)
+            ct = np.concatenate([[0], np.cumsum(lt)]).astype(np.int32)
+            cs2 = np.concatenate([[0], np.cumsum(ls[perm])]).astype(np.int32)
+            ct2 = np.concatenate([[0], np.cumsum(lt[perm])]).astype(np.int32)
+            g1, _ = attention_groups(ct, cs, 128, 1)
+            g2, _ = attention_groups(ct2, cs2, 128, 1)
+            assert len(g2) <= len(g1), t  # never more cross-attention groups
+
+
+def test_pack_pairs_order_is_a_permutation(tmp_path):
+    pairs = [(list(range(4, 4 + a)), list(range(4, 4 + b))) for a, b in
+             [(30, 5), (3, 40), (60, 60), (10, 12), (100, 20), (7, 90)]]
+    b0 = pack_pairs(pairs, tokens=10_000, order=False)
+    b1 = pack_pairs(pairs, tokens=10_000, order=True)
+    assert b0.n_src == b1.n_src and b0.n_tgt == b1.n_tgt
+    assert sorted(np.diff(b0.cu_src).tolist()) == sorted(np.diff(b1.cu_src).tolist())
