@@ -276,6 +276,11 @@ int mm_gemm_trace(unsigned long long* dev_buf);
  * data.attention_groups on the step's host path. */
 int mm_attention_groups(const int32_t* cu_q, const int32_t* cu_k, int n_seq, int cap, int align,
                         int32_t* out, int* n_groups, int* foot);
+/* Host: the six tables of a packed batch in one call -- {self source, self
+ * target, cross (q = target, k = source)} x {align 32, align 1}; table t at
+ * out + 2 * n_seq * t, n_groups[t], foot[t]. */
+int mm_attention_tables(const int32_t* cu_src, const int32_t* cu_tgt, int n_seq, int cap,
+                        int32_t* out, int* n_groups, int* foot);
 /* Host: an order of a batch's n sentence pairs (source / target lengths)
  * that packs into few attention groups: first-fit-decreasing 2-D bins of
  * `cap` rows per side, bins in creation order, over-long pairs last.

@@ -191,6 +191,23 @@ extern "C" int mm_comm_cost_moves(const double* params, int64_t n_modules,
     return 0;
 }
 
+// All six work-group tables of a packed batch in one host call (the staging
+// path of every step): {self source, self target, cross} x {32-row aligned
+// (mma.sync), unpadded (tcgen05)}; table t is written at out + 2 * n_seq * t.
+extern "C" int mm_attention_tables(const int32_t* cu_src, const int32_t* cu_tgt, int n_seq, int cap,
+                                   int32_t* out, int* n_groups, int* foot) {
+    MM_CHECK_ARG(cu_src && cu_tgt && out && n_groups && foot, "NULL argument");
+    const int32_t* q[3] = {cu_src, cu_tgt, cu_tgt};
+    const int32_t* k[3] = {cu_src, cu_tgt, cu_src};
+    for (int t = 0; t < 6; ++t) {
+        const int side = t % 3, align = t < 3 ? 32 : 1;
+        if (int st = mm_attention_groups(q[side], k[side], n_seq, cap, align,
+                                         out + int64_t(2) * n_seq * t, n_groups + t, foot + t))
+            return st;
+    }
+    return 0;
+}
+
 // Order of a batch's sentence pairs for the attention work groups: first-fit
 // decreasing 2-D bin packing (capacity `cap` rows on both the source and the
 // target side), bins emitted in creation order, pairs longer than `cap` on

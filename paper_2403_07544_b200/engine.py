@@ -72,15 +72,19 @@ class DeviceBatch:
                  non_blocking: bool = True):
         arrs = dict(b.host_arrays())
         groups = {}
-        for name, (cq, ck) in (("attn_src", (b.cu_src, b.cu_src)), ("attn_tgt", (b.cu_tgt, b.cu_tgt)),
-                               ("attn_cross", (b.cu_tgt, b.cu_src))):
-            g, cap = native_attention_groups(cq, ck)
-            arrs[name] = g
-            groups[name] = (len(g) // 2, cap)
-            # unpadded packing for the tcgen05 backward (fewer, fuller units)
-            t, _ = native_attention_groups(cq, ck, align=1)
-            arrs["tc" + name[4:]] = t
-            groups["tc" + name[4:]] = (len(t) // 2,)
+        # the six work-group tables in one host call: padded (mma.sync) and
+        # unpadded (tcgen05: fewer, fuller units) for src / tgt / cross
+        n = b.n_seq
+        cs = np.ascontiguousarray(b.cu_src, dtype=np.int32)
+        ct = np.ascontiguousarray(b.cu_tgt, dtype=np.int32)
+        tab = np.empty(12 * max(n, 1), dtype=np.int32)
+        ng, foot = np.zeros(6, dtype=np.int32), np.zeros(6, dtype=np.int32)
+        _native.check(_native.lib().mm_attention_tables(cs.ctypes.data, ct.ctypes.data, n, ATTN_CAP,
+                                                        tab.ctypes.data, ng.ctypes.data,
+                                                        foot.ctypes.data), "mm_attention_tables")
+        for t, name in enumerate(("attn_src", "attn_tgt", "attn_cross", "tc_src", "tc_tgt", "tc_cross")):
+            arrs[name] = tab[2 * n * t:2 * n * t + 2 * int(ng[t])]
+            groups[name] = (int(ng[t]), int(foot[t])) if t < 3 else (int(ng[t]),)
         names = list(self.FIELDS) + list(groups)
         sizes = [len(arrs[f]) for f in names]
         total = sum(sizes)

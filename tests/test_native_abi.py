@@ -163,3 +163,24 @@ def test_attention_groups_native_matches_numpy():
                    if not (rows(gp, cq)[i] <= 128 and rows(gp, ck)[i] <= 128)
                    for s in range(gp[2 * i], gp[2 * i] + gp[2 * i + 1])}
         assert tc_seqs | ms_seqs == set(range(n)) and not (tc_seqs & ms_seqs), trial
+
+
+def test_attention_tables_one_call_matches_six():
+    """mm_attention_tables (the staging path's single host call) == the six
+    mm_attention_groups tables it stands for."""
+    import numpy as np
+    from paper_2403_07544_b200.engine import native_attention_groups
+    L = _native.lib()
+    rng = np.random.default_rng(11)
+    for trial in range(50):
+        n = int(rng.integers(1, 80))
+        cs = np.concatenate([[0], np.cumsum(rng.integers(1, 200, n))]).astype(np.int32)
+        ct = np.concatenate([[0], np.cumsum(rng.integers(1, 200, n))]).astype(np.int32)
+        tab = np.empty(12 * n, dtype=np.int32)
+        ng, foot = np.zeros(6, dtype=np.int32), np.zeros(6, dtype=np.int32)
+        assert L.mm_attention_tables(cs.ctypes.data, ct.ctypes.data, n, 128, tab.ctypes.data,
+                                     ng.ctypes.data, foot.ctypes.data) == 0
+        for t, (q, k, align) in enumerate([(cs, cs, 32), (ct, ct, 32), (ct, cs, 32),
+                                           (cs, cs, 1), (ct, ct, 1), (ct, cs, 1)]):
+            g, f = native_attention_groups(q, k, 128, align)
+            assert np.array_equal(tab[2 * n * t:2 * n * t + 2 * ng[t]], g) and foot[t] == f, (trial, t)
