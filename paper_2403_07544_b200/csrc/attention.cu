@@ -590,6 +590,21 @@ __device__ __forceinline__ uint64_t desc(const void* p, uint32_t lbo) {
     return tc::umma_desc_sw128(tc::smem_u32(p), lbo, 1024);
 }
 
+// -DMM_ATTN_WAITPROF (diagnostics build, tools/attn_waitprof.py): per-CTA
+// clock64 totals of the MMA warp's waits for tiles / P and the epilogue's
+// waits for S / the gradient MMAs
+#ifdef MM_ATTN_WAITPROF
+__device__ unsigned long long g_wp[148 * 8];
+#define WP_BEGIN(t) const long long t = clock64()
+#define WP_ADD(i, t)                                                                        \
+    do {                                                                                    \
+        if ((threadIdx.x & 31) == 0 && blockIdx.x < 148)                                    \
+            atomicAdd(&g_wp[blockIdx.x * 8 + (i)], (unsigned long long)(clock64() - (t)));  \
+    } while (0)
+#else
+#define WP_BEGIN(t) do { } while (0)
+#define WP_ADD(i, t) do { } while (0)
+#endif
 // Persistent: CTA b takes units (group, head) b, b + grid, ... (heads fastest);
 // the producer loads unit n+1's tiles as soon as unit n's MMAs have consumed
 // them (g_bar), so the TMA latency hides behind unit n's output phase; TMEM
@@ -669,7 +684,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
             if (!mine(x)) continue;
             const uint32_t tmem = tmem0 + (n & 1) * 256;
             // ---- S = Q K^T (cols 0-127), dP = dO V^T (cols 128-255)
+            WP_BEGIN(w0_);
             tc::mbar_wait(tma_bar, n & 1);
+            WP_ADD(0, w0_);
             tc::tc_fence_after();
             constexpr uint32_t id_s = tc::idesc_bf16_f32(128, 128, 0, 0);
 #pragma unroll
@@ -679,7 +696,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
             }
             tc::mma_commit_elect<1>(s_bar);
             // ---- dV = P^T dO (cols 0-63), dK = dS^T Q (64-127), dQ = dS K (128-191)
+            WP_BEGIN(w1_);
             tc::mbar_wait(p_bar, n & 1);
+            WP_ADD(1, w1_);
             tc::tc_fence_after();
             constexpr uint32_t id_mn = tc::idesc_bf16_f32(128, 64, 1, 1);  // A and B MN-major
             constexpr uint32_t id_km = tc::idesc_bf16_f32(128, 64, 0, 1);  // A K-major, B MN-major
@@ -728,7 +747,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
                 }
             }
             const float l2 = vrow ? p.lse[int64_t(x.h) * p.total_q + x.q_lo + i] * kLog2e : 0.f;
+            WP_BEGIN(w2_);
             tc::mbar_wait(s_bar, n & 1);
+            if (warp == kEpiW0) WP_ADD(2, w2_);
             tc::tc_fence_after();
             if (warp == kEpiW0) ATTN_STAMP_LANE0(1);
             const int key0 = kc * 32;
@@ -767,7 +788,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
             if (lane == 0) tc::mbar_arrive(p_bar);
             if (warp == kEpiW0) ATTN_STAMP_LANE0(2);
             // ---- gradients out of TMEM: this warp's 16 of each output's 64 columns
+            WP_BEGIN(w3_);
             tc::mbar_wait(g_bar, n & 1);
+            if (warp == kEpiW0) WP_ADD(3, w3_);
             tc::tc_fence_after();
             auto emit = [&](uint32_t col, uint16_t* base, int64_t ld, int row_lo, bool vr, float sc) {
                 uint32_t v[16];
@@ -1127,3 +1150,15 @@ extern "C" int mm_attention_bwd(const mm_attn_args* a, void* stream) {
     MM_LAUNCH_CHECK("attn_bwd_kernel");
     return 0;
 }
+
+#ifdef MM_ATTN_WAITPROF
+extern "C" int mm_attn_wp_read(unsigned long long* host, int zero) {
+    if (zero) {
+        static unsigned long long z[148 * 8] = {};
+        MM_CUDA_TRY(cudaMemcpyToSymbol(tca::g_wp, z, sizeof(z)));
+        return 0;
+    }
+    MM_CUDA_TRY(cudaMemcpyFromSymbol(host, tca::g_wp, sizeof(unsigned long long) * 148 * 8));
+    return 0;
+}
+#endif

@@ -1,5 +1,7 @@
-"""Per-unit wait-time breakdown of the tcgen05 attention backward (needs the
-attn_wp diagnostics variant: MM_LIB_VARIANT=attn_wp)."""
+"""Per-unit wait-time breakdown of the tcgen05 attention backward.  Needs the
+diagnostics build:
+  python tools/build_variant.py attn_wp -DMM_ATTN_WAITPROF attention.cu=paper_2403_07544_b200/csrc/attention.cu
+  MM_LIB_VARIANT=attn_wp python tools/attn_waitprof.py      (C5=1: config-5 shapes)"""
 import os, sys, ctypes
 import numpy as np, torch
 sys.path.insert(0, "/root/repo")
