@@ -215,3 +215,125 @@ def synthetic_uniform_tasks(arch_kind: str, n_gpus: int, topo: ClusterTopology) 
                             enc_modules=enc, dec_modules=dec, enc_layers=el, dec_layers=dl,
                             device=devices[i]))
     return out
+
+
+# ---------------------------------------------------------------------------
+# the trainer loop and the optimizer hook behind the reference's API
+
+
+def step_optimizer(module_buckets: Mapping, ready_counts: Mapping, adam=None) -> None:
+    """The optimizer hook SURVEY §8(b) adds to the reference's API: one fused
+    ``/ n`` + Adam + bf16-cast launch (K3, ``mm_fused_update``) over every
+    module bucket whose ready count n >= 1; n == 0 leaves the module untouched
+    (``grad = None`` semantics: no moment decay, no step count).  Buckets are
+    ``model.ModuleState`` objects (grad, master, exp_avg, exp_avg_sq, weights,
+    step) keyed by ModuleKey; the gradient must already be the group sum."""
+    import math
+    from .engine import AdamConfig
+    a = adam or AdamConfig()
+    mods = []
+    for key, st in module_buckets.items():
+        n = int(ready_counts.get(key, 0))
+        if n < 1:
+            continue
+        st.step += 1
+        mods.append(_native.AdamModule(
+            grad=st.grad.data_ptr(), master=st.master.data_ptr(), exp_avg=st.exp_avg.data_ptr(),
+            exp_avg_sq=st.exp_avg_sq.data_ptr(), param_bf16=st.weights.data_ptr(),
+            n_elems=st.master.numel(), n_ready=n, ready_index=-1,
+            step_size=a.lr / (1.0 - a.beta1 ** st.step),
+            inv_sqrt_bc2=1.0 / math.sqrt(1.0 - a.beta2 ** st.step)))
+    if mods:
+        ops.fused_update(mods, _native.AdamHyper.make(beta1=a.beta1, beta2=a.beta2, eps=a.eps,
+                                                      weight_decay=a.weight_decay))
+
+
+def run_benchmark(tasks: Sequence[TaskSpec], topo: ClusterTopology, steps: int, seed: int = 0,
+                  accum_count: int = 1, dim: int = 4, batch_tokens: int = 4096,
+                  compute_coeff: float = 2e-9, shape=None, device=None):
+    """``run_benchmark`` (syncsim.py:295-392) with the toy model replaced by
+    the real modular transformer: every device of ``topo`` that holds a task
+    is an emulated rank on this GPU (``cluster.EmulatedCluster``); each step
+    every rank draws ``accum_count`` micro-batches of ``batch_tokens`` target
+    tokens through the multiplexer (``Random(f"{seed}:{i}:mux")``, data
+    ``default_rng([seed, i])``), runs forward / backward, then the Algorithm-1
+    exchange and the fused update.
+
+    Ledger columns: ``ready_bytes`` / ``grad_bytes`` / ``tokens`` follow the
+    reference's definitions exactly (module sizes in the reference's
+    enumerate_modules convention, syncsim.py:318, 365-379); ``compute_time``
+    (max over devices) and ``comm_time`` (exchange + update) are MEASURED
+    with CUDA events instead of modeled, so ``dim`` and ``compute_coeff`` are
+    accepted for signature compatibility only.  Returns (CommLedger, summary
+    dict with the reference's keys)."""
+    import numpy as np
+    from . import configs
+    from .cluster import EmulatedCluster
+    from .data import ZipfIds, make_batch
+    from .engine import DeviceBatch
+    from .plan import ready_counts_all, task_modules
+    from .sharing import enumerate_modules
+    tasks = sorted(tasks, key=lambda t: t.id)
+    for t in tasks:
+        if t.device is None:
+            raise SimulationError(f"task {t.id} has no device assignment")
+    shape = shape or configs.SHAPE_CFG1_GPU
+    dev = torch.device(device or f"cuda:{torch.cuda.current_device()}")
+    modules = enumerate_modules(tasks)
+    world = max(topo.flat(t.device) for t in tasks) + 1
+    cl = EmulatedCluster(tasks, topo, shape, world=world, device=dev, seed=seed)
+    plan = cl.plan
+    spec = configs.DataSpec(batch_tokens, 3.0, 0.5, 4, shape.max_len, 1.1)
+    ids = ZipfIds(shape.vocab, spec.zipf_s)
+    ranks = sorted(plan.tasks_by_rank)
+    data_rngs = {i: np.random.default_rng([seed, i]) for i in ranks}
+    ledger = CommLedger()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    for step in range(steps):
+        used_by_rank, comp = {}, {}
+        step_tokens = 0
+        for i in ranks:
+            eng = cl.ranks[i]
+            ops.memset(eng.loss_sum, 0)
+            used: set = set()
+            e0, e1 = ev(), ev()
+            e0.record()
+            for _ in range(accum_count):
+                task = eng.mux.pick(step)
+                b = make_batch(data_rngs[i], spec, shape.vocab, ids=ids)
+                fresh = [k for k in task_modules(task) if k not in used]
+                eng.zero_grads(fresh)
+                used.update(fresh)
+                eng.forward_backward(task, DeviceBatch(b, dev), eng.loss_sum)
+                step_tokens += batch_tokens
+            e1.record()
+            used_by_rank[i] = used
+            comp[i] = (e0, e1)
+        c0, c1 = ev(), ev()
+        c0.record()
+        cl.exchange_and_update(used_by_rank)
+        c1.record()
+        torch.cuda.synchronize(dev)
+        counts = ready_counts_all(plan, used_by_rank)
+        idx = plan.index()
+        ready_bytes = grad_bytes = 0
+        for key in sorted(modules):
+            group = plan.groups.get(key, [])
+            if len(group) < 2:
+                continue
+            ready_bytes += READY_ENTRY_BYTES * len(group)
+            if counts[idx[key]] >= 1:
+                grad_bytes += GRAD_BYTES_PER_PARAM * modules[key].n_params
+        ledger.records.append(StepRecord(
+            step=step, ready_bytes=ready_bytes, grad_bytes=grad_bytes,
+            comm_time=c0.elapsed_time(c1) * 1e-3,
+            compute_time=max(a.elapsed_time(b) for a, b in comp.values()) * 1e-3 if comp else 0.0,
+            tokens=step_tokens))
+    summary = {
+        "steps": steps, "devices": len(ranks), "tasks": len(tasks), "modules": len(modules),
+        "total_tokens": ledger.total_tokens, "total_time_sec": ledger.total_time,
+        "tokens_per_sec": ledger.tokens_per_sec, "comm_time_fraction": ledger.comm_fraction,
+        "grad_allreduce_bytes": ledger.total_grad_bytes, "ready_sync_bytes": ledger.total_ready_bytes,
+    }
+    return ledger, summary
+
