@@ -89,6 +89,11 @@ def sync_step(devices: Sequence[DeviceState], only_ready: bool = False) -> dict:
                 raise SimulationError("buffers must be contiguous CUDA fp32 tensors")
             if b.shape != ref.shape:
                 raise SimulationError(f"module {key}: buffer shapes differ across devices")
+            if b.device != ref.device:
+                # the one-launch exchange reads every member's buffer from the
+                # launching GPU; real ranks exchange through engine.CommGroups
+                # (NCCL) or peer.PeerExchange instead
+                raise SimulationError(f"module {key}: buffers on different CUDA devices")
         out = torch.empty_like(ref)
         synced[key] = out
         m = _native.SyncModule()
