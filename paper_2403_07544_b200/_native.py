@@ -183,7 +183,11 @@ class BatchDesc(ctypes.Structure):
 
 
 def _declare(h: ctypes.CDLL) -> None:
+    variant = bool(os.environ.get("MM_LIB_VARIANT"))
+
     def sig(name, res, *args):
+        if variant and not hasattr(h, name):  # A/B builds of older sources (tools/)
+            return
         fn = getattr(h, name)
         fn.restype = res
         fn.argtypes = list(args)
