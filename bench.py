@@ -469,10 +469,10 @@ def run_train(args, pk):
     trainer.train_step([host2[0]])
     barrier()
     t0 = time.perf_counter()
-    h2d = 0
-    for b in host2[1:]:
-        trainer.train_step([b])
-        h2d += trainer.h2d_bytes
+    # public API, one step of host lookahead (staging of step k+1 overlaps step
+    # k on the GPU); every step copies its inputs H2D and reads its loss back
+    trainer.train_steps(([b] for b in host2[1:]), args.steps)
+    h2d = trainer.h2d_bytes * args.steps
     eng.sync_updates()
     barrier()
     e2e_s = (time.perf_counter() - t0) / args.steps

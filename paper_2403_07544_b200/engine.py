@@ -781,16 +781,42 @@ class Trainer:
         self._pinned = [torch.empty(pinned_elems, dtype=torch.int32, pin_memory=True)
                         for _ in range(4)]
         self._loss_host = torch.empty(1, dtype=torch.float32, pin_memory=True)
+        self._pin_next = 0  # rotating pinned staging buffer (reused >= 2 steps later)
         self.step_idx = 0
         self.h2d_bytes = 0
         self.d2h_bytes = 4
 
     def stage(self, batches) -> list:
         out = []
-        for i, b in enumerate(batches):
-            out.append(DeviceBatch(b, self.device, pinned=self._pinned[i % len(self._pinned)]))
+        for b in batches:
+            pin = self._pinned[self._pin_next % len(self._pinned)]
+            self._pin_next += 1
+            out.append(DeviceBatch(b, self.device, pinned=pin))
         self.h2d_bytes = sum(d.h2d_bytes for d in out)
         return out
+
+    def train_steps(self, step_batches, n_steps: int) -> list:
+        """``n_steps`` training steps over an iterable of per-step micro-batch
+        lists, with one step of lookahead: the host builds and stages step
+        k+1's batches (one H2D copy each, queued behind step k) while the GPU
+        runs step k; every step still reads its loss back.  Returns the losses."""
+        it = iter(step_batches)
+        losses = []
+        staged = self.stage(next(it)) if n_steps > 0 else None
+        h2d = [self.h2d_bytes]
+        for k in range(n_steps):
+            self.engine.step(self.step_idx, staged)
+            self.step_idx += 1
+            self._loss_host.copy_(self.engine.loss_sum, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            if k + 1 < n_steps:  # host work for step k+1 overlaps step k on the GPU
+                staged = self.stage(next(it))
+                h2d.append(self.h2d_bytes)
+            ev.synchronize()
+            losses.append(float(self._loss_host[0]))
+        self.h2d_bytes = sum(h2d) // max(1, len(h2d))
+        return losses
 
     def train_step(self, host_batches=None, pipeline=None, accum: int = 1) -> float:
         """host_batches: this rank's micro-batches (task-agnostic synthetic

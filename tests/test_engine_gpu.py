@@ -496,3 +496,20 @@ def test_step_optimizer_skips_unready_modules(cuda):
     torch.cuda.synchronize()
     assert sts[keys[0]].step == 1 and not torch.equal(sts[keys[0]].master, before[keys[0]])
     assert sts[keys[1]].step == 0 and torch.equal(sts[keys[1]].master, before[keys[1]])
+
+
+def test_train_steps_lookahead_matches_train_step(cuda):
+    """Trainer.train_steps (host lookahead staging) gives the same losses as
+    the same batches through train_step one at a time."""
+    from paper_2403_07544_b200.engine import Trainer
+    shape = configs.SHAPE_CFG1_GPU
+    w = configs.config1(shape)
+    rng = np.random.default_rng(3)
+    batches = [[make_batch(rng, w.data, shape.vocab, sentences=16)] for _ in range(4)]
+    tr = Trainer(w.tasks, w.topo, shape, rank=0, world=1, device=cuda, seed=0)
+    a = [tr.train_step(b) for b in batches]
+    tr.close()
+    tr = Trainer(w.tasks, w.topo, shape, rank=0, world=1, device=cuda, seed=0)
+    b = tr.train_steps(iter(batches), len(batches))
+    tr.close()
+    assert len(b) == 4 and all(abs(x - y) <= 1e-5 * abs(x) for x, y in zip(a, b))
