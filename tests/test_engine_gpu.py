@@ -513,3 +513,32 @@ def test_train_steps_lookahead_matches_train_step(cuda):
     b = tr.train_steps(iter(batches), len(batches))
     tr.close()
     assert len(b) == 4 and all(abs(x - y) <= 1e-5 * abs(x) for x, y in zip(a, b))
+
+
+def test_long_sequences_step_vs_oracle(cuda):
+    """A step whose batch mixes short sentences with ones longer than 128 rows
+    (config 5's tail): the tcgen05 attention kernels take the groups within
+    128 rows, the mma.sync kernels the rest, inside the native driver; loss
+    and module gradients against the bf16-faithful oracle."""
+    from paper_2403_07544_b200.configs import DataSpec, ModelShape
+    from paper_2403_07544_b200.engine import DeviceBatch, Engine
+    shape = ModelShape(128, 2, 256, 1000, 256)
+    w = configs.config1(shape)
+    tasks = [t.with_device(DeviceId(0, 0)) for t in w.tasks]
+    eng = Engine(tasks, ClusterTopology(1, 1, 3), shape, rank=0, world=1, device=cuda, seed=0)
+    spec = DataSpec(0, 0, 0, 20, 250, 0.0)  # uniform lengths 20..250 on both sides
+    hb = [make_batch(np.random.default_rng(11), spec, shape.vocab, sentences=10)]
+    assert max(np.diff(hb[0].cu_src).max(), np.diff(hb[0].cu_tgt).max()) > 128
+    masters0 = {k: st.master.cpu().numpy().copy() for k, st in eng.states.items()}
+    info = eng.step(0, [DeviceBatch(b, cuda) for b in hb])
+    torch.cuda.synchronize()
+    layouts = eng.layouts
+    eff = {k: effective_weights(layouts[k], v) for k, v in masters0.items()}
+    task_by_id = {t.id: t for t in tasks}
+    picked = [task_by_id[tid] for tid in info["tasks"]]
+    grads, used, losses = OT.local_grads(list(zip(picked, hb)), eff, layouts, shape,
+                                         embedding_keys, bf16=True)
+    assert abs(eng.loss_sum.item() - sum(losses)) / sum(losses) < 1e-3
+    for k, st in eng.states.items():
+        if k in used:
+            assert rel_norm(st.grad.cpu().numpy(), grads[k].numpy()) < TOL_MODEL, str(k)
