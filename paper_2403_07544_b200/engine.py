@@ -33,8 +33,8 @@ from .configs import ModelShape
 from .data import ATTN_CAP, Batch, attention_groups
 from .domain import ClusterTopology, ModuleKey, Side, TaskSpec
 from .model import LN_EPS, ModuleState, module_layouts
-from .plan import (Multiplexer, build_plan, decode_ready, embedding_keys, exchange_order, ready_bits, ready_flags,
-                   task_modules)
+from .plan import (Multiplexer, build_plan, decode_ready, embedding_keys, exchange_plan, ready_bits,
+                   ready_flags, task_modules)
 
 
 @dataclasses.dataclass
@@ -660,16 +660,10 @@ class Engine:
             return
         items = []
         if self.comm is not None:
-            idx = self.plan.index()
-            roots = getattr(self, "_roots", None)
-            for k in exchange_order(self.plan, counts, self.rank):
-                if only is not None and k not in only:
-                    continue
-                members = self.plan.groups[k]
+            for k, members, root in exchange_plan(self.plan, self.rank, self._bits, only):
                 grp = self.comm.by_set.get(tuple(members))
                 st = self.states[k]
-                # n = 1: broadcast the one ready member's buffer (it is the sum)
-                root = members.index(roots[idx[k]]) if roots is not None and counts[idx[k]] == 1 else -1
+                # root >= 0 (n = 1): broadcast the one ready member's buffer (it is the sum)
                 if root < 0 and k not in used and k in self._dirty:  # contribute the zero of Algorithm 1
                     ops.memset(st.grad, 0)
                 self._dirty.add(k)  # receives the group's sum

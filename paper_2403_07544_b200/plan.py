@@ -152,6 +152,24 @@ def exchange_order(plan: ModulePlan, counts, rank: int) -> list[ModuleKey]:
             if k in mine and len(plan.groups[k]) >= 2 and counts[idx[k]] >= 1]
 
 
+def exchange_plan(plan: ModulePlan, rank: int, bits, only=None) -> list[tuple]:
+    """K2 work of `rank` for the world-summed ready bitmasks: (key, members,
+    root) in the global issue order (``exchange_order``: sorted ModuleKey,
+    hosted here, >= 2 members, n >= 1); root = the member index of the single
+    ready rank when n = 1 (a broadcast from it), else -1 (a sum all-reduce).
+    The NCCL engine and the gloo tests issue exactly this list."""
+    counts, roots = decode_ready(bits)
+    idx = plan.index()
+    out = []
+    for k in exchange_order(plan, counts, rank):
+        if only is not None and k not in only:
+            continue
+        members = plan.groups[k]
+        i = idx[k]
+        out.append((k, members, members.index(roots[i]) if counts[i] == 1 else -1))
+    return out
+
+
 def shard_begin(n_elems: int, group_size: int, member: int) -> int:
     """First element of member's shard of a module (the host restatement of
     mm_peer_shard_begin): S = ceil(n / g) rounded up to 4 elements, shard r =

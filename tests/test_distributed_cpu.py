@@ -26,7 +26,7 @@ def _worker(rank, world, port, out_dir):
     from paper_2403_07544_b200.data import make_batch
     from paper_2403_07544_b200.model import init_module, module_layouts
     from paper_2403_07544_b200.plan import (Multiplexer, build_plan, decode_ready, embedding_keys,
-                                            exchange_order, ready_bits, ready_flags, task_modules)
+                                            exchange_plan, ready_bits, ready_flags, task_modules)
     wl = configs.config1()
     plan = build_plan(wl.tasks, wl.topo)
     layouts = module_layouts(plan, wl.shape)
@@ -44,12 +44,13 @@ def _worker(rank, world, port, out_dir):
                                                  embedding_keys)
             bits = torch.tensor(ready_bits(plan, rank, used), dtype=torch.int32)
             dist.all_reduce(bits)  # K1 on rank bitmasks
-            counts, roots = decode_ready(bits.tolist())
+            counts, _ = decode_ready(bits.tolist())
             idx = plan.index()
-            for k in exchange_order(plan, counts, rank):  # K2, sorted ModuleKey order
-                g = subgroups[tuple(plan.groups[k])]
-                if counts[idx[k]] == 1:  # n = 1: the ready rank's buffer is the sum
-                    dist.broadcast(grads[k], src=roots[idx[k]], group=g)
+            # K2: the engine's own item list (exchange_plan), sorted ModuleKey order
+            for k, members, root in exchange_plan(plan, rank, bits.tolist()):
+                g = subgroups[tuple(members)]
+                if root >= 0:  # n = 1: the ready member's buffer is the sum
+                    dist.broadcast(grads[k], src=members[root], group=g)
                 else:
                     dist.all_reduce(grads[k], group=g)
             synced = {str(k): (grads[k] / counts[idx[k]]).numpy()

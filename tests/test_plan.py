@@ -205,3 +205,32 @@ def test_peer_plan_shards_tile_every_module_once():
             i = plan.index()[k]
             if len(plan.groups[k]) >= 2 and member_mask(bits[i], plan.groups[k]):
                 assert k in seen
+
+
+def test_exchange_plan_is_consistent_across_members():
+    """Every member of a group derives the same K2 item (same key order, same
+    broadcast root) from the same world-summed bits: the precondition for
+    NCCL collectives on overlapping sub-communicators not to cross."""
+    from paper_2403_07544_b200 import configs
+    from paper_2403_07544_b200.plan import (Multiplexer, build_plan, decode_ready, exchange_plan,
+                                            ready_bits, task_modules)
+    w = configs.config5(world=8)
+    plan = build_plan(w.tasks, w.topo)
+    for step in range(4):
+        used = {r: set(task_modules(Multiplexer(plan, r, 0).pick(step))) for r in range(8)}
+        bits = [0] * len(plan.keys)
+        for r in range(8):
+            bits = [a + b for a, b in zip(bits, ready_bits(plan, r, used[r]))]
+        counts, roots = decode_ready(bits)
+        per_rank = {r: exchange_plan(plan, r, bits) for r in range(8)}
+        for k in plan.keys:
+            seen = {(members, root) for r in range(8) for kk, members, root in per_rank[r] if kk == k}
+            assert len(seen) <= 1, str(k)
+            if seen:
+                members, root = seen.pop()
+                assert (root >= 0) == (counts[plan.index()[k]] == 1)
+                if root >= 0:
+                    assert members[root] == roots[plan.index()[k]] and members[root] in members
+        for r in range(8):  # each rank's list is in sorted key order
+            keys = [k for k, _, _ in per_rank[r]]
+            assert keys == sorted(keys)
