@@ -224,7 +224,7 @@ def test_exchange_plan_is_consistent_across_members():
         counts, roots = decode_ready(bits)
         per_rank = {r: exchange_plan(plan, r, bits) for r in range(8)}
         for k in plan.keys:
-            seen = {(members, root) for r in range(8) for kk, members, root in per_rank[r] if kk == k}
+            seen = {(tuple(members), root) for r in range(8) for kk, members, root in per_rank[r] if kk == k}
             assert len(seen) <= 1, str(k)
             if seen:
                 members, root = seen.pop()
