@@ -902,6 +902,24 @@ TileChoice choose_tile(const mm_gemm_args* const* probs, int n, int sms) {
             if (cost < best_cost - 1e-9) { best_cost = cost; best = {cand, cg}; }
         }
     }
+    // diagnostics: per-shape overrides "N,K,Bmn=CG:BN;..." (single-problem
+    // launches; Bmn = 1 when B is MN-major), for step-level A/B of choices
+    static const char* ovr = std::getenv("MM_GEMM_OVERRIDE");
+    if (ovr && n == 1) {
+        const char* q = ovr;
+        while (*q) {
+            long on = 0, ok = 0, ob = 0, ocg = 0, obn = 0;
+            if (std::sscanf(q, "%ld,%ld,%ld=%ld:%ld", &on, &ok, &ob, &ocg, &obn) == 5 &&
+                on == probs[0]->n && ok == probs[0]->k && ob == (probs[0]->b_kmajor ? 0 : 1) &&
+                (ocg == 1 || ocg == 2) && (obn == 128 || obn == 192 || obn == 256)) {
+                best = {static_cast<int>(obn), static_cast<int>(ocg)};
+                break;
+            }
+            const char* semi = std::strchr(q, ';');
+            if (!semi) break;
+            q = semi + 1;
+        }
+    }
     if (const char* force = std::getenv("MM_GEMM_BN")) {  // diagnostics
         const int f = std::atoi(force);
         if (f == 128 || f == 192 || f == 256) best.bn = f;
