@@ -169,15 +169,17 @@ def run_reference(args):
     from paper_2403_07544_b200 import configs
     threads = os.cpu_count() or 1
     wl = configs.config3(1)
-    if args.workload == "reduce":
-        rate, sample = reduce_cpu_rate(args.steps)
-        line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "GB/s",
+    if args.workload in ("reduce", "exchange"):
+        rate, sample = (reduce_cpu_rate(args.steps) if args.workload == "reduce"
+                        else exchange_cpu_rate(min(args.steps, 3)))
+        unit = "GB/s" if args.workload == "reduce" else "G module-params/s"
+        line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": unit,
                 "higher_is_better": True, "n_gpus": args.gpus, "steps": args.steps,
                 "warmup": args.warmup, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": "config2 module-grad reduce (CPU, oracle sync_step)"},
-                "cpu_baseline": {"value": rate, "unit": "GB/s", "cores": 1, "kind": "port",
+                "config": {"workload": f"config2 module-grad {args.workload} (CPU, oracle)"},
+                "cpu_baseline": {"value": rate, "unit": unit, "cores": 1, "kind": "port",
                                  "sample": sample},
-                "e2e": {"value": rate, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "e2e": {"value": rate, "unit": unit, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return 0
@@ -230,6 +232,38 @@ def reduce_cpu_rate(n_steps, scale: float = 1 / 16):
         sync_step(devs)
     dt = (time.perf_counter() - t0) / max(1, n_steps)
     return reduce_bytes(mods) / dt / 1e9, f"config-2 generator at 1/16 size ({sum(m.n_params for m in mods)/1e6:.1f}M params), numpy, 1 core"
+
+
+def exchange_cpu_rate(n_steps, scale: float = 1 / 16):
+    """CPU counterpart of --workload exchange on a scaled config-2 instance:
+    the oracle's numpy sync_step plus a numpy Adam step of every module
+    (one replica, the owners' work) -> module parameters per second, 1 core."""
+    import numpy as np
+    from oracle.algorithm1 import Dev, sync_step
+    from paper_2403_07544_b200.configs import reduce_microbench
+    rng, mods = reduce_microbench(lo=1e6 * scale, hi=64e6 * scale)
+    devs = []
+    for r in range(8):
+        hosted = frozenset(i for i, m in enumerate(mods) if r in m.ranks)
+        bufs = {i: (rng.standard_normal(m.n_params, dtype=np.float32) if m.ready[r - m.start]
+                    else np.zeros(m.n_params, np.float32)) for i, m in enumerate(mods) if r in m.ranks}
+        used = {i for i, m in enumerate(mods) if r in m.ranks and m.ready[r - m.start]}
+        devs.append(Dev(r, hosted, bufs, used))
+    state = [[np.zeros(m.n_params, np.float32) for _ in range(3)] for m in mods]
+    b1, b2, eps, lr = np.float32(0.9), np.float32(0.998), np.float32(1e-8), np.float32(1e-4)
+    t0 = time.perf_counter()
+    for _ in range(max(1, n_steps)):
+        synced = sync_step(devs)
+        for i, (p, m, v) in enumerate(state):
+            g = synced[i]
+            m += (1 - b1) * (g - m)
+            v *= b2
+            v += (1 - b2) * g * g
+            p -= lr * m / (np.sqrt(v) + eps)
+    dt = (time.perf_counter() - t0) / max(1, n_steps)
+    elems = sum(m.n_params for m in mods)
+    return elems / dt / 1e9, (f"config-2 generator at 1/16 size ({elems / 1e6:.1f}M params): numpy "
+                              "sync_step + Adam, 1 core")
 
 
 def run_reduce(args, pk):
@@ -536,8 +570,12 @@ def main():
     pk = peaks()
     if args.workload in ("reduce", "exchange"):
         line = (run_reduce if args.workload == "reduce" else run_exchange)(args, pk)
-        line["cpu_baseline"] = dict(zip(("value", "sample"), reduce_cpu_rate(3)), unit="GB/s",
-                                    cores=1, kind="port")
+        if args.workload == "reduce":
+            line["cpu_baseline"] = dict(zip(("value", "sample"), reduce_cpu_rate(3)), unit="GB/s",
+                                        cores=1, kind="port")
+        else:
+            line["cpu_baseline"] = dict(zip(("value", "sample"), exchange_cpu_rate(2)),
+                                        unit="G module-params/s", cores=1, kind="port")
         line["e2e"] = {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
                        "d2h_bytes_per_step": 0, "note": "device-resident microbench"}
         print(json.dumps(line))
