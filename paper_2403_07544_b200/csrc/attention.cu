@@ -586,6 +586,29 @@ __device__ __forceinline__ void store_row_hilo(uint8_t* hi, uint8_t* lo, int r, 
     }
 }
 
+// bf16 hi only: dS for the dK / dQ products (as FlashAttention stores it)
+__device__ __forceinline__ void store_row_hi(uint8_t* hi, int r, int c0, const float* v) {
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+        uint32_t h[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) h[e] = pack_bf16(v[cc * 8 + 2 * e], v[cc * 8 + 2 * e + 1]);
+        const int off = r * 128 + (((c0 + cc) ^ (r & 7)) * 16);
+        *reinterpret_cast<uint4*>(hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
+    }
+}
+
+// dS = P (dP - D) enters dK = dS^T Q and dQ = dS K as bf16 (FlashAttention's
+// choice): its rounding (2^-9 relative) matches that of the bf16 dq / dk / dv
+// outputs themselves; -DMM_ATTN_DS_LO=1 restores the hi + lo pair (two more
+// MMA chains and a quarter of the smem stores: 16 vs 13.5 us per config-3
+// launch).  P keeps hi + lo: dropping it moved the cross / causal blocks
+// past 2e-3.
+#ifndef MM_ATTN_DS_LO
+#define MM_ATTN_DS_LO 0
+#endif
+constexpr bool kDsLo = MM_ATTN_DS_LO != 0;
+
 __device__ __forceinline__ uint64_t desc(const void* p, uint32_t lbo) {
     return tc::umma_desc_sw128(tc::smem_u32(p), lbo, 1024);
 }
@@ -710,13 +733,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
                 for (int kk = 0; kk < 8; ++kk) {  // K = 128 query rows
                     const uint32_t acc = (part > 0 || kk > 0) ? 1u : 0u;
                     tc::mma_bf16_elect<1>(tmem + 0, desc(P + kk * 2048, kTile), desc(dOs + kk * 2048, kTile), id_mn, acc);
-                    tc::mma_bf16_elect<1>(tmem + 64, desc(S + kk * 2048, kTile), desc(Qs + kk * 2048, kTile), id_mn, acc);
+                    if (kDsLo || part == 0)
+                        tc::mma_bf16_elect<1>(tmem + 64, desc(S + kk * 2048, kTile), desc(Qs + kk * 2048, kTile), id_mn, acc);
                 }
+                if (kDsLo || part == 0) {
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {  // K = 128 keys
-                    const uint32_t acc = (part > 0 || kk > 0) ? 1u : 0u;
-                    tc::mma_bf16_elect<1>(tmem + 128, desc(S + (kk >> 2) * kTile + (kk & 3) * 32, 16),
-                                          desc(Ks + kk * 2048, kTile), id_km, acc);
+                    for (int kk = 0; kk < 8; ++kk) {  // K = 128 keys
+                        const uint32_t acc = (part > 0 || kk > 0) ? 1u : 0u;
+                        tc::mma_bf16_elect<1>(tmem + 128, desc(S + (kk >> 2) * kTile + (kk & 3) * 32, 16),
+                                              desc(Ks + kk * 2048, kTile), id_km, acc);
+                    }
                 }
             }
             tc::mma_commit_elect<1>(g_bar);
@@ -781,7 +807,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
             for (int j = 0; j < 32; ++j) dpv[j] = pv[j] * (dpv[j] - D);  // dS
             // keys kc*32..+32: region kc/2, 16-byte chunks (kc&1)*4 .. +4 of the row
             store_row_hilo(Ph + (kc >> 1) * kTile, Pl + (kc >> 1) * kTile, i, (kc & 1) * 4, pv);
-            store_row_hilo(Sh + (kc >> 1) * kTile, Sl + (kc >> 1) * kTile, i, (kc & 1) * 4, dpv);
+            if (kDsLo) store_row_hilo(Sh + (kc >> 1) * kTile, Sl + (kc >> 1) * kTile, i, (kc & 1) * 4, dpv);
+            else store_row_hi(Sh + (kc >> 1) * kTile, i, (kc & 1) * 4, dpv);
             tc::fence_proxy_async_smem();  // generic stores -> visible to the tensor core
             tc::tc_fence_before();
             __syncwarp();
