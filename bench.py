@@ -126,7 +126,7 @@ def cpu_step_rate(workload, n_steps: int, threads: int, tokens: int = None):
     import numpy as np
     import torch
     from oracle import transformer as OT
-    from paper_2403_07544_b200.data import ZipfIds, make_batch
+    from paper_2403_07544_b200.data import ZipfIds, attention_order_py, make_batch
     from paper_2403_07544_b200.model import init_module, module_layouts
     from paper_2403_07544_b200.plan import Multiplexer, build_plan, embedding_keys
     torch.set_num_threads(threads)
@@ -143,7 +143,8 @@ def cpu_step_rate(workload, n_steps: int, threads: int, tokens: int = None):
     total_tok, total_t = 0, 0.0
     for step in range(n_steps):
         task = mux.pick(step)
-        batch = make_batch(rng, spec, workload.shape.vocab, ids=ids)
+        # the numpy restatement of the pair order: the CPU leg never maps libmmb200
+        batch = make_batch(rng, spec, workload.shape.vocab, ids=ids, order_fn=attention_order_py)
         keys = list(task.modules()) + list(embedding_keys(task))
         for k in keys:
             if k not in masters:
@@ -162,13 +163,32 @@ def cpu_step_rate(workload, n_steps: int, threads: int, tokens: int = None):
     return total_tok / total_t, total_t / n_steps, spec.tokens_per_gpu
 
 
+CPU_BASELINE_STEPS = 5  # the in-line cpu_baseline (~18 s on 16 cores)
+GEMM_STEPS = 3  # instrumented steps behind the roofline figures
+CPU_MAX_STEPS = 20  # the CPU arm times min(K, 20) full steps (~3.6 s each on 16 cores)
+DATA = "synthetic: Zipf(1.1) ids, lognormal lengths; random-init weights"
+
+
+def train_config(wl, world: int) -> dict:
+    """The workload's ``config`` object, identical in both arms."""
+    return {"workload": f"{wl.name} modular NMT ({wl.shape.d_model}d, {len(wl.tasks)} directions)",
+            "global_batch": wl.data.tokens_per_gpu * world, "tokens": "target tokens per step",
+            "parallelism": f"module-groups x{world}",
+            "l2": "working set per step > 126 MB L2 (weights+activations ~1.5 GB); no flush"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     from paper_2403_07544_b200 import configs
     threads = os.cpu_count() or 1
-    wl = configs.config3(1)
+    if args.config == "config4" and args.workload == "train":
+        # config 4's placement comes from the allocator (native cost kernel)
+        print(json.dumps({"impl": "reference", "unavailable": "CPU arm runs configs 3 and 5"}))
+        return 0
+    wl = {"config3": configs.config3, "config5": configs.config5}.get(args.config,
+                                                                      configs.config3)(args.gpus)
     if args.workload in ("reduce", "exchange"):
         rate, sample = (reduce_cpu_rate(args.steps) if args.workload == "reduce"
                         else exchange_cpu_rate(min(args.steps, 3)))
@@ -183,21 +203,24 @@ def run_reference(args):
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return 0
-    # bounded sample per step (1024 target tokens of the config-3 stream) so
-    # that --steps K --warmup W finishes within minutes on the host cores
-    sample_tokens = 1024
+    # the same workload as the GPU arm: full steps (4096 target tokens for
+    # config 3) of rank 0's stream; the step count is capped to stay within minutes
+    n_timed = max(1, min(args.steps, CPU_MAX_STEPS))
     if args.warmup:
-        cpu_step_rate(wl, 1, threads, tokens=sample_tokens)
-    rate, sec, tokens = cpu_step_rate(wl, max(1, min(args.steps, 60)), threads, tokens=sample_tokens)
+        cpu_step_rate(wl, 1, threads)
+    rate, sec, tokens = cpu_step_rate(wl, n_timed, threads)
+    from paper_2403_07544_b200 import _native
+    assert _native._lib is None, "the CPU reference arm must not load libmmb200"
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "tok/s",
             "higher_is_better": True, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": sec * 1e3, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic (Zipf 1.1, lognormal 3.0/0.5)",
-            "config": {"workload": "config3 transformer-base modular NMT, 1 rank (CPU oracle)",
-                       "tokens_per_step": tokens},
+            "vs_baseline": None, "dtype": "f32", "data": DATA,
+            "config": train_config(wl, args.gpus),
+            "cpu_steps_timed": n_timed,
             "cpu_baseline": {"value": rate, "unit": "tok/s", "cores": threads, "kind": "port",
-                             "sample": f"{max(1, min(args.steps, 60))} steps x {tokens} target "
-                                       "tokens of the config-3 stream, PyTorch-CPU fp32 oracle"},
+                             "sample": f"{n_timed} steps x {tokens} target tokens of rank 0's "
+                                       f"{wl.name} stream (multiplexer task, Adam update), "
+                                       "PyTorch-CPU fp32 oracle, no native library"},
             "e2e": {"value": rate, "unit": "tok/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -475,26 +498,33 @@ def run_train(args, pk):
         tokens_all = tokens_local
     value = tokens_all / (ms * 1e-3)
 
-    # ---- GEMM roofline: one instrumented step (events recorded by the C
-    # driver immediately around every GEMM launch on the launching stream)
+    # ---- GEMM roofline: every GEMM launch of GEMM_STEPS further steps stamps
+    # its own span on the device (%globaltimer, first CTA past
+    # griddepcontrol.wait -> last CTA exit; gemm.cu mm_gemm_timing): no event
+    # or host call between kernels, so the instrumented steps run like the
+    # timed ones (their step time is printed next to ms_per_step)
     import ctypes
-    from paper_2403_07544_b200 import _native
     L = _native.lib()
     _native.check(L.mm_gemm_timing(1, None, None, None), "mm_gemm_timing")
-    _native.check(L.mm_step_timing(1, None, None), "mm_step_timing")
-    eng.step(n_total, [dbs[-1]])
+    i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    i0.record()
+    for j in range(GEMM_STEPS):
+        eng.step(n_total + j, [dbs[args.warmup + j % args.steps]])
     eng.sync_updates()
+    i1.record()
     torch.cuda.synchronize()
+    instr_ms = i0.elapsed_time(i1) / GEMM_STEPS
     f, t_ms, n_g = ctypes.c_double(), ctypes.c_float(), ctypes.c_int()
     _native.check(L.mm_gemm_timing(0, ctypes.byref(f), ctypes.byref(t_ms), ctypes.byref(n_g)),
                   "mm_gemm_timing")
-    cat_ms, cat_n = (ctypes.c_float * 8)(), (ctypes.c_int * 8)()
-    _native.check(L.mm_step_timing(0, cat_ms, cat_n), "mm_step_timing")
-    cats = ["layernorm_fwd", "layernorm_bwd", "attention_fwd", "attention_bwd", "cross_entropy",
-            "embedding", "memset", "other"]
-    breakdown = {c: round(cat_ms[i], 4) for i, c in enumerate(cats) if cat_n[i]}
-    gemm_flops, gemm_ms = f.value, t_ms.value
+    gemm_flops, gemm_ms = f.value / GEMM_STEPS, t_ms.value / GEMM_STEPS
     gemm_tflops = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    clocks = clk.summary()
+    # burst peak (measured at max clocks) when the timed region held max SM
+    # clocks; the sustained (power-capped) peak otherwise
+    at_max = bool(clocks.get("sm_mhz") and clocks.get("sm_max_mhz")
+                  and clocks["sm_mhz"] >= 0.97 * clocks["sm_max_mhz"])
+    peak = pk["bf16_tflops"] if at_max else pk["bf16_tflops_sustained"]
 
     # ---- end to end through the public API (host batches, H2D + D2H inside)
     rng2 = np.random.default_rng([1, rank])
@@ -519,30 +549,35 @@ def run_train(args, pk):
         "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic: Zipf(1.1) ids, lognormal lengths; random-init weights",
-        "config": {"workload": f"{args.config} modular NMT ({wl.shape.d_model}d, "
-                               f"{len(wl.tasks)} directions, {len(eng.plan.keys)} modules)",
-                   "global_batch": int(tokens_all), "tokens": "target tokens per step",
-                   "src_tokens_per_gpu": src_local, "parallelism": f"module-groups x{world}",
-                   "exchange": eng.exchange if world > 1 else "none (every group is a singleton)",
-                   "l2": "working set per step > 126 MB L2 (weights+activations ~1.5 GB); no flush"},
-        "roofline": {"bound": "tensor", "achieved": gemm_tflops,
-                     "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
-                     "frac": gemm_tflops / pk["bf16_tflops_sustained"], "traffic": gemm_traffic(args.config),
-                     "kernel": "gemm_tcgen05_kernel (all GEMM launches of one step)",
-                     "gemm_ms_per_step": gemm_ms, "gemm_share_of_step": gemm_ms / ms,
-                     "other_kernels_ms_per_step": breakdown,
-                     "peak_source": pk["source"] + ", sustained"},
-        "clocks": clk.summary(),
+        "data": DATA,
+        "config": train_config(wl, world),
+        "src_tokens_per_gpu": src_local, "modules": len(eng.plan.keys),
+        "exchange": eng.exchange if world > 1 else "none (every group is a singleton)",
+        "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": peak, "unit": "TFLOP/s",
+                     "frac": gemm_tflops / peak, "traffic": gemm_traffic(args.config),
+                     "kernel": "gemm_tcgen05_kernel (all GEMM launches of a step)",
+                     "flops_per_step": gemm_flops, "gemm_launches_per_step": n_g.value / GEMM_STEPS,
+                     "gemm_ms_per_step": gemm_ms, "gemm_share_of_step": gemm_ms / instr_ms,
+                     "instrumented_ms_per_step": instr_ms,
+                     "gemm_time_source": "per-launch %globaltimer spans (first CTA past "
+                                         "griddepcontrol.wait -> last CTA exit), summed",
+                     "peak_used": "burst (timed region at max SM clock)" if at_max
+                                  else "sustained (SM clock below max)",
+                     "peak_burst": pk["bf16_tflops"], "peak_sustained": pk["bf16_tflops_sustained"],
+                     "frac_vs_burst": gemm_tflops / pk["bf16_tflops"],
+                     "frac_vs_sustained": gemm_tflops / pk["bf16_tflops_sustained"],
+                     "peak_source": pk["source"]},
+        "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": "tok/s", "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": 4},
         "gpu_launches": launches * args.steps,
     }
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        rate, sec, tok = cpu_step_rate(wl, 2, threads)
+        rate, sec, tok = cpu_step_rate(wl, CPU_BASELINE_STEPS, threads)
         line["cpu_baseline"] = {"value": rate, "unit": "tok/s", "cores": threads, "kind": "port",
-                                "sample": f"2 steps x {tok} target tokens, PyTorch-CPU fp32 oracle"}
+                                "sample": f"{CPU_BASELINE_STEPS} steps x {tok} target tokens of "
+                                          f"rank 0's {wl.name} stream, PyTorch-CPU fp32 oracle"}
     if rank == 0:
         print(json.dumps(line))
     trainer.close()

@@ -261,10 +261,17 @@ int mm_gemm(const mm_gemm_args* args, void* stream);
  * width); all problems share a_kmajor / b_kmajor.  Used for the deferred
  * weight-gradient GEMMs of a whole encoder or decoder side. */
 int mm_gemm_grouped(const mm_gemm_args* probs, int n, void* stream);
-/* mode 1: start recording CUDA events around every mm_gemm launch;
- * mode 0: stop, synchronise and return total flops (2MNK), summed launch
- * time (ms) and launch count since the last start. */
+/* mode 1: every later mm_gemm launch records its own span on the device
+ * (%globaltimer of the first CTA past griddepcontrol.wait -> the last CTA's
+ * exit; no events between kernels, programmatic dependent launch unchanged);
+ * mode 0 (after the caller synchronised): stop and return total flops
+ * (2MNK), summed launch spans (ms) and launch count since the last start. */
 int mm_gemm_timing(int mode, double* flops, float* ms, int* launches);
+/* diagnostics, after mm_gemm_timing(0): per-launch spans (ns, %globaltimer)
+ * lo[i] / hi[i], flops[i] and shape[4i..4i+3] = m, n, k of the launch's
+ * first problem and its problem count, for up to max launches. */
+int mm_gemm_spans(int max, unsigned long long* lo, unsigned long long* hi, double* flops,
+                  int* shape, int* count);
 /* diagnostics: per-CTA %globaltimer stamps of every later mm_gemm launch into
  * dev_buf[8 * cta + slot] (NULL disables); see gemm.cu for the slots */
 int mm_gemm_trace(unsigned long long* dev_buf);

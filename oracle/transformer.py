@@ -78,18 +78,48 @@ def sinusoid(pos: torch.Tensor, d: int) -> torch.Tensor:
     return pe
 
 
-def _attention(q, k, v, cu_q, cu_k, heads, causal):
+class _AttnRoundDS(torch.autograd.Function):
+    """softmax(q k^T * scale) v over one sequence ([H, L, hd] tensors) whose
+    backward rounds dS = P * (dP - D) to bf16 before the dQ / dK products --
+    where the engine's attention backward stores dS (attention.cu, phase A:
+    bf16 dS in shared memory, D = sum_j P_ij dP_ij exact in fp32)."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, scale, causal):
+        s = q @ k.transpose(1, 2) * scale
+        if causal:
+            lq, lk = s.shape[1], s.shape[2]
+            s = s.masked_fill(torch.ones(lq, lk, dtype=torch.bool).triu(1), float("-inf"))
+        p = torch.softmax(s, -1)
+        ctx.save_for_backward(q, k, v, p)
+        ctx.scale = scale
+        return p @ v
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, p = ctx.saved_tensors
+        dv = p.transpose(1, 2) @ do
+        dp = do @ v.transpose(1, 2)
+        ds = (p * (dp - (p * dp).sum(-1, keepdim=True))).bfloat16().float()
+        return ctx.scale * (ds @ k), ctx.scale * (ds.transpose(1, 2) @ q), dv, None, None
+
+
+def _attention(q, k, v, cu_q, cu_k, heads, causal, ds_bf16: bool = False):
     hd = q.shape[1] // heads
     outs = []
     for s in range(len(cu_q) - 1):
         qs = q[cu_q[s]:cu_q[s + 1]].view(-1, heads, hd).transpose(0, 1)
         ks = k[cu_k[s]:cu_k[s + 1]].view(-1, heads, hd).transpose(0, 1)
         vs = v[cu_k[s]:cu_k[s + 1]].view(-1, heads, hd).transpose(0, 1)
-        sc = qs @ ks.transpose(1, 2) / math.sqrt(hd)
-        if causal:
-            lq, lk = sc.shape[1], sc.shape[2]
-            sc = sc.masked_fill(torch.ones(lq, lk, dtype=torch.bool).triu(1), float("-inf"))
-        outs.append((torch.softmax(sc, -1) @ vs).transpose(0, 1).reshape(-1, heads * hd))
+        if ds_bf16:
+            o = _AttnRoundDS.apply(qs, ks, vs, 1.0 / math.sqrt(hd), causal)
+        else:
+            sc = qs @ ks.transpose(1, 2) / math.sqrt(hd)
+            if causal:
+                lq, lk = sc.shape[1], sc.shape[2]
+                sc = sc.masked_fill(torch.ones(lq, lk, dtype=torch.bool).triu(1), float("-inf"))
+            o = torch.softmax(sc, -1) @ vs
+        outs.append(o.transpose(0, 1).reshape(-1, heads * hd))
     return torch.cat(outs, 0)
 
 
@@ -109,7 +139,8 @@ def task_loss(task, batch, flats: dict, layouts: dict, shape, emb_keys, bf16: bo
     bf16=True rounds to bf16 exactly where the engine stores bf16 tensors:
     LayerNorm outputs, q/k/v, attention outputs, ReLU activations and logits
     (forward values) and the GEMM-input copies of every gradient -- residual
-    dx, dqkv, dq / dkv, d(attention out), d(ReLU pre-activation), dlogits --
+    dx, dqkv, dq / dkv, d(attention out), d(ReLU pre-activation), dlogits and
+    the attention backward's dS --
     while LayerNorm, softmax, the residual stream and all accumulations stay
     fp32 as in the kernels."""
     P = Precision(bf16)
@@ -126,7 +157,7 @@ def task_loss(task, batch, flats: dict, layouts: dict, shape, emb_keys, bf16: bo
         for i in range(lay.n_layers):
             p = f"l{i}."
             qkv = P.vg(_lin(P.v(_ln(x, f, lay, p + "ln1")), f, lay, p + "qkv"))
-            a = P.vg(_attention(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], cu_s, cu_s, H, False))
+            a = P.vg(_attention(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], cu_s, cu_s, H, False, P.bf16))
             x = x + P.g(_lin(a, f, lay, p + "out"))
             _keep(trace, f"enc_l{i}_attn", x)
             x = x + P.g(_lin(_ffn_act(P, x, f, lay, p), f, lay, p + "ff2"))
@@ -141,12 +172,12 @@ def task_loss(task, batch, flats: dict, layouts: dict, shape, emb_keys, bf16: bo
         for i in range(lay.n_layers):
             p = f"l{i}."
             qkv = P.vg(_lin(P.v(_ln(y, f, lay, p + "ln1")), f, lay, p + "qkv"))
-            a = P.vg(_attention(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], cu_t, cu_t, H, True))
+            a = P.vg(_attention(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], cu_t, cu_t, H, True, P.bf16))
             y = y + P.g(_lin(a, f, lay, p + "out"))
             _keep(trace, p + "cx_in", y)
             q = P.vg(_lin(P.v(_ln(y, f, lay, p + "lnc")), f, lay, p + "cq"))
             kv = P.vg(_lin(mem, f, lay, p + "ckv"))
-            a = P.vg(_attention(q, kv[:, :d], kv[:, d:], cu_t, cu_s, H, False))
+            a = P.vg(_attention(q, kv[:, :d], kv[:, d:], cu_t, cu_s, H, False, P.bf16))
             _keep(trace, p + "ckv", kv)
             _keep(trace, p + "ca", a)
             y = y + P.g(_lin(a, f, lay, p + "cout"))

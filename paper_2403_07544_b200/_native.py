@@ -226,6 +226,7 @@ def _declare(h: ctypes.CDLL) -> None:
     sig("mm_gemm", c_int, c_void_p, c_void_p)
     sig("mm_gemm_grouped", c_int, c_void_p, c_int, c_void_p)
     sig("mm_gemm_timing", c_int, c_int, POINTER(c_double), POINTER(c_float), POINTER(c_int))
+    sig("mm_gemm_spans", c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_int))
     sig("mm_step_timing", c_int, c_int, POINTER(c_float), POINTER(c_int))
     sig("mm_attention_order", c_int, c_void_p, c_void_p, c_int, c_int, c_void_p)
     sig("mm_attention_tables", c_int, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p)

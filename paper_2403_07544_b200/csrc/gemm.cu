@@ -126,6 +126,10 @@ struct Group {
     LnParams ln;
     Prob prob[NP];
     unsigned long long* trace;  // optional per-CTA phase timestamps (diagnostics)
+    // optional launch span (mm_gemm_timing): %globaltimer min over CTAs after
+    // griddepcontrol.wait -> *span_lo, max over CTAs at exit -> *span_hi
+    unsigned long long* span_lo;
+    unsigned long long* span_hi;
     int n_probs;
     int units;
     int b_prefetch;
@@ -411,6 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             pdl_wait();
+            if (g.span_lo) atomicMin(g.span_lo, gtime());
             int stage = 0;
             uint32_t phase = 0;
             int issued = 0;
@@ -723,6 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         else tc::tmem_dealloc(tmem_base, C::kTmemCols);
     }
     if (threadIdx.x == 0) MM_TRACE(7);
+    if (threadIdx.x == 0 && g.span_hi) atomicMax(g.span_hi, gtime());
 }
 
 // ----------------------------------------------------------------------------
@@ -796,11 +802,17 @@ int dispatch(int a_mn, int b_mn, const Group<NP>& g, cudaStream_t s) {
 
 unsigned long long* g_trace_buf = nullptr;  // set by mm_gemm_trace (diagnostics)
 
-// optional per-launch timing (roofline evidence inside bench.py)
+// optional per-launch timing (roofline evidence inside bench.py): every
+// launch records its own span on the device (%globaltimer: first CTA past
+// griddepcontrol.wait -> last CTA exit), so no event or host call sits
+// between kernels and programmatic dependent launch stays as in the
+// untimed step
 struct GemmTiming {
     bool on = false;
-    std::vector<cudaEvent_t> ev;  // start/stop pairs
+    unsigned long long* buf = nullptr;  // [cap] span starts, then [cap] span ends
+    size_t cap = 0;
     std::vector<double> flops;
+    std::vector<int> shape;  // m, n, k, problems per launch (first problem's shape)
     size_t used = 0;
 } g_timing;
 
@@ -1022,20 +1034,13 @@ int run_group(const mm_gemm_args* const* probs, int n, cudaStream_t s) {
         g.b_prefetch &= probs[i]->b_prefetch ? 1 : 0;
         if (probs[i]->dbias) g.any_dbias = 1;
     }
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (g_timing.on) {
-        if (g_timing.ev.size() < 2 * (g_timing.used + 1)) {
-            for (int i = 0; i < 2; ++i) {
-                cudaEvent_t e;
-                MM_CUDA_TRY(cudaEventCreate(&e));
-                g_timing.ev.push_back(e);
-            }
-        }
-        e0 = g_timing.ev[2 * g_timing.used];
-        e1 = g_timing.ev[2 * g_timing.used + 1];
+    g.span_lo = g.span_hi = nullptr;
+    if (g_timing.on && g_timing.used < g_timing.cap) {
+        g.span_lo = g_timing.buf + g_timing.used;
+        g.span_hi = g_timing.buf + g_timing.cap + g_timing.used;
         g_timing.flops.push_back(flops);
+        g_timing.shape.insert(g_timing.shape.end(), {int(probs[0]->m), int(probs[0]->n), int(probs[0]->k), n});
         ++g_timing.used;
-        MM_CUDA_TRY(cudaEventRecord(e0, s));
     }
     const int a_mn = probs[0]->a_kmajor ? 0 : 1;
     const int b_mn = probs[0]->b_kmajor ? 0 : 1;
@@ -1062,7 +1067,6 @@ int run_group(const mm_gemm_args* const* probs, int n, cudaStream_t s) {
         else if (bn == 192) rc = dispatch<192, NP, 1>(a_mn, b_mn, g, s);
         else rc = dispatch<128, NP, 1>(a_mn, b_mn, g, s);
     }
-    if (rc == 0 && e1) MM_CUDA_TRY(cudaEventRecord(e1, s));
     return rc;
 }
 
@@ -1077,24 +1081,53 @@ extern "C" int mm_gemm_trace(unsigned long long* dev_buf) {
 
 extern "C" int mm_gemm_timing(int mode, double* flops, float* ms, int* launches) {
     if (mode == 1) {
+        if (!g_timing.buf) {
+            g_timing.cap = 1 << 14;
+            MM_CUDA_TRY(cudaMalloc(&g_timing.buf, 2 * g_timing.cap * sizeof(unsigned long long)));
+        }
+        MM_CUDA_TRY(cudaMemset(g_timing.buf, 0xff, g_timing.cap * sizeof(unsigned long long)));
+        MM_CUDA_TRY(cudaMemset(g_timing.buf + g_timing.cap, 0, g_timing.cap * sizeof(unsigned long long)));
         g_timing.on = true;
         g_timing.used = 0;
         g_timing.flops.clear();
+        g_timing.shape.clear();
         return 0;
     }
+    // mode 0: stop; the caller has synchronised the launches' stream
     g_timing.on = false;
-    double f = 0;
-    float t = 0;
-    for (size_t i = 0; i < g_timing.used; ++i) {
-        MM_CUDA_TRY(cudaEventSynchronize(g_timing.ev[2 * i + 1]));
-        float x = 0;
-        MM_CUDA_TRY(cudaEventElapsedTime(&x, g_timing.ev[2 * i], g_timing.ev[2 * i + 1]));
-        t += x;
-        f += g_timing.flops[i];
+    double f = 0, t_ns = 0;
+    if (g_timing.used) {
+        std::vector<unsigned long long> h(2 * g_timing.cap);
+        MM_CUDA_TRY(cudaMemcpy(h.data(), g_timing.buf, h.size() * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < g_timing.used; ++i) {
+            const unsigned long long lo = h[i], hi = h[g_timing.cap + i];
+            if (hi > lo) t_ns += double(hi - lo);
+            f += g_timing.flops[i];
+        }
     }
     if (flops) *flops = f;
-    if (ms) *ms = t;
+    if (ms) *ms = static_cast<float>(t_ns * 1e-6);
     if (launches) *launches = static_cast<int>(g_timing.used);
+    return 0;
+}
+
+// diagnostics: the spans (ns, %globaltimer) of the launches recorded since the
+// last mm_gemm_timing(1), after mm_gemm_timing(0): lo[i], hi[i], flops[i] and
+// shape[4 i .. 4 i + 3] = m, n, k of the first problem, problems in the launch
+extern "C" int mm_gemm_spans(int max, unsigned long long* lo, unsigned long long* hi, double* flops,
+                             int* shape, int* count) {
+    const int n = static_cast<int>(std::min<size_t>(g_timing.used, static_cast<size_t>(max)));
+    if (n > 0) {
+        MM_CUDA_TRY(cudaMemcpy(lo, g_timing.buf, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        MM_CUDA_TRY(cudaMemcpy(hi, g_timing.buf + g_timing.cap, n * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost));
+        for (int i = 0; i < n; ++i) {
+            flops[i] = g_timing.flops[i];
+            for (int j = 0; j < 4; ++j) shape[4 * i + j] = g_timing.shape[4 * i + j];
+        }
+    }
+    *count = n;
     return 0;
 }
 

@@ -118,7 +118,7 @@ def attention_order(ls, lt, cap: int = ATTN_CAP_ROWS) -> np.ndarray:
 
 
 def make_batch(rng: np.random.Generator, spec, vocab: int, sentences: Optional[int] = None,
-               ids: Optional[ZipfIds] = None, order: bool = True) -> Batch:
+               ids: Optional[ZipfIds] = None, order: bool = True, order_fn=None) -> Batch:
     """One micro-batch: ``sentences`` pairs if given, else ``spec.tokens_per_gpu``
     target tokens.  order=True lays the pairs out in attention_order (an
     order of independent pairs; fewer, fuller attention work groups)."""
@@ -134,8 +134,17 @@ def make_batch(rng: np.random.Generator, spec, vocab: int, sentences: Optional[i
             lt_l.append(b)
             tot += b
         ls, lt = np.asarray(ls_l), np.asarray(lt_l)
+    return batch_from_lengths(rng, ls, lt, ids, order=order, order_fn=order_fn)
+
+
+def batch_from_lengths(rng: np.random.Generator, ls, lt, ids: ZipfIds, order: bool = True,
+                       order_fn=None) -> Batch:
+    """A packed batch of sentence pairs with the given source / target
+    lengths (ids drawn from ``ids``); ``order_fn`` replaces attention_order
+    (e.g. ``attention_order_py`` on a host without the native library)."""
+    ls, lt = np.asarray(ls, dtype=np.int64), np.asarray(lt, dtype=np.int64)
     if order and len(ls) > 1:
-        perm = attention_order(ls, lt)
+        perm = (order_fn or attention_order)(ls, lt)
         ls, lt = ls[perm], lt[perm]
     cu_s = np.concatenate([[0], np.cumsum(ls)]).astype(np.int32)
     cu_t = np.concatenate([[0], np.cumsum(lt)]).astype(np.int32)

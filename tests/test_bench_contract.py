@@ -47,3 +47,10 @@ def test_bench_gpu_line():
         assert k in d, k
     assert d["gpu_launches"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(d["roofline"])
+    r = d["roofline"]
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert abs(r["achieved"] - r["flops_per_step"] / (r["gemm_ms_per_step"] * 1e-3) / 1e12) < 1e-6 * r["achieved"]
+    assert r["gemm_ms_per_step"] < r["instrumented_ms_per_step"]
+    # the reference arm runs the same workload (driver's same_config check)
+    ref = json.loads(_run(["--impl", "reference", "--steps", "1", "--warmup", "0"])[-1])
+    assert ref["config"] == d["config"]

@@ -209,12 +209,12 @@ def test_block_vs_bf16_oracle(cuda, block):
     elif block == "cross":
         q = P.vg(OT._lin(P.v(OT._ln(xr, eff, lay, "l0.lnc")), eff, lay, "l0.cq"))
         kv = P.vg(OT._lin(mr, eff, lay, "l0.ckv"))
-        a = P.vg(OT._attention(q, kv[:, :d], kv[:, d:], cu.tolist(), cus.tolist(), H, False))
+        a = P.vg(OT._attention(q, kv[:, :d], kv[:, d:], cu.tolist(), cus.tolist(), H, False, True))
         o = xr + P.g(OT._lin(a, eff, lay, "l0.cout"))
     else:
         qkv = P.vg(OT._lin(P.v(OT._ln(xr, eff, lay, "l0.ln1")), eff, lay, "l0.qkv"))
         a = P.vg(OT._attention(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], cu.tolist(),
-                               cu.tolist(), H, block == "causal"))
+                               cu.tolist(), H, block == "causal", True))
         o = xr + P.g(OT._lin(a, eff, lay, "l0.out"))
     o.backward(dout)
     assert rel(out.cpu().numpy(), o.detach().numpy()) < 2e-3
@@ -227,11 +227,9 @@ def test_block_vs_bf16_oracle(cuda, block):
         ref = eff.grad[p.offset:p.offset + p.numel].numpy()
         if not name.startswith("l0.") or not np.abs(ref).max() > 0:
             continue
-        # 5e-3 (BASELINE's bf16 bound is 2e-2): parameter gradients sum over
-        # every token, and the attention backward's dS enters dQ / dK as bf16
-        # (FlashAttention's precision); cross-attention Q weights and LayerNorm
-        # gamma measured at 2.5-3.2e-3, every other tensor below 2e-3
-        assert rel(gg[p.offset:p.offset + p.numel], ref) < 5e-3, name
+        # the oracle rounds the attention backward's dS to bf16 where the
+        # engine stores it (oracle/transformer._AttnRoundDS)
+        assert rel(gg[p.offset:p.offset + p.numel], ref) < 2e-3, name
         checked += 1
     assert checked >= 4
 
