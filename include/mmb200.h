@@ -21,10 +21,16 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 18
+#define MMB200_ABI_VERSION 19
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
+/* emulated devices of one sync (mm_sync_emulated): the reference's multi-node
+ * scaling harness reaches 20 devices per group (syncsim.py:461-483) */
+#define MM_MAX_SYNC_GROUP 32
 
 int mm_abi_version(void);
+/* sizeof(T) of the descriptor struct named T (e.g. "mm_sync_module"), -1 if
+ * unknown: lets a binding check its struct mirrors against this build. */
+long long mm_abi_sizeof(const char* name);
 const char* mm_last_error(void);
 /* SM count and compute capability (major*10+minor) of the current device. */
 int mm_device_info(int* sm_count, int* cc);
@@ -62,7 +68,7 @@ int mm_comm_cost_moves(const double* params, int64_t n_modules, const int64_t* m
  * buffers are zero, which DeviceState.reset guarantees, syncsim.py:108-111).
  */
 typedef struct {
-    float* bufs[MM_MAX_GROUP]; /* member buffers, ascending device index */
+    float* bufs[MM_MAX_SYNC_GROUP]; /* member buffers, ascending device index */
     float* out;                /* optional synced copy, may be NULL */
     int64_t n_elems;
     int32_t group_size;
@@ -70,6 +76,10 @@ typedef struct {
 } mm_sync_module;
 
 int mm_sync_emulated(const mm_sync_module* mods, int n_mods, int only_ready, void* stream);
+/* The same over float64 buffers (the reference DeviceState's default dtype,
+ * syncsim.py:103-106): bufs / out address doubles; IEEE double adds in
+ * ascending member order, correctly rounded division. */
+int mm_sync_emulated_f64(const mm_sync_module* mods, int n_mods, int only_ready, void* stream);
 
 /* ---------------------------------------------------------------------------
  * K3: fused masked rescale + loss unscale + Adam + bf16 parameter cast on a
@@ -425,6 +435,7 @@ int mm_cast_f32_bf16(const float* x, uint16_t* y, int64_t n, void* stream);
 int mm_flush_l2(void* scratch, size_t bytes, void* stream);
 /* y += alpha * x (fp32): DeviceState.accumulate (syncsim.py:113-118) */
 int mm_axpy_f32(float* y, const float* x, float alpha, int64_t n, void* stream);
+int mm_axpy_f64(double* y, const double* x, double alpha, int64_t n, void* stream);
 /* stream-ordered byte fill (DeviceState.reset of the grad buckets, syncsim.py:108-111) */
 int mm_memset(void* ptr, int value, size_t bytes, void* stream);
 

@@ -104,6 +104,28 @@ def device_mean_oracle(runs, hosted: Mapping[int, frozenset], weights, target, d
     return res
 
 
+def random_toy_scenario(seed: int, dim: int = 3, accum_count: int = 1):
+    """A random multi-device toy-chain step for the device-mean check of
+    syncsim.py:156-187 (the same kind of instance the reference's own
+    randomized test draws, tests/test_syncsim.py:95-136): 2-8 devices, 2-16
+    tasks of 1-3 modules each from a pool of encoder / decoder keys.
+    Returns (weights, target, runs, hosted); runs = (device, chain, x)."""
+    from paper_2403_07544_b200.domain import ModuleKey, Side
+    rng = random.Random(seed)
+    nrng = np.random.default_rng(seed)
+    n_dev, n_tasks = rng.randint(2, 8), rng.randint(2, 16)
+    pool = sorted({ModuleKey(Side.ENCODER, i, f"g{rng.randrange(4)}") for i in range(3)}
+                  | {ModuleKey(Side.DECODER, 0, f"g{rng.randrange(4)}"),
+                     ModuleKey(Side.ENCODER, 0, "full"), ModuleKey(Side.DECODER, 1, "full")})
+    chains = [tuple(rng.sample(pool, rng.randint(1, 3))) for _ in range(n_tasks)]
+    where = [rng.randrange(n_dev) for _ in chains]
+    hosted = {d: frozenset(k for c, w in zip(chains, where) if w == d for k in c) for d in range(n_dev)}
+    hosted = {d: h for d, h in hosted.items() if h}
+    weights, target = toy_weights(pool, dim, seed)
+    runs = [(w, c, nrng.standard_normal(dim)) for _ in range(accum_count) for c, w in zip(chains, where)]
+    return weights, target, runs, hosted
+
+
 # --------------------------------------------------------------------------
 # multiplexer, group map and ready counts (syncsim.py:190-205, 313-363)
 

@@ -19,8 +19,9 @@ if os.environ.get("MM_LIB_VARIANT"):  # diagnostics: a tuning build from tools/b
                             "libmmb200.so")
 
 #: must match MMB200_ABI_VERSION in include/mmb200.h
-ABI_VERSION = 18
+ABI_VERSION = 19
 MAX_GROUP = 8
+MAX_SYNC_GROUP = 32
 
 
 class NativeLibraryError(RuntimeError):
@@ -61,7 +62,7 @@ def check(status: int, what: str) -> None:
 
 class SyncModule(ctypes.Structure):
     _fields_ = [
-        ("bufs", c_void_p * MAX_GROUP),
+        ("bufs", c_void_p * MAX_SYNC_GROUP),
         ("out", c_void_p),
         ("n_elems", c_int64),
         ("group_size", c_int32),
@@ -204,6 +205,7 @@ def _declare(h: ctypes.CDLL) -> None:
         c_int64, POINTER(c_double), c_int)
     # Algorithm-1 sync, emulated devices on one GPU (sync_step syncsim.py:121-153)
     sig("mm_sync_emulated", c_int, POINTER(SyncModule), c_int, c_int, c_void_p)
+    sig("mm_sync_emulated_f64", c_int, POINTER(SyncModule), c_int, c_int, c_void_p)
     # K3 fused rescale + unscale + Adam + bf16 cast
     sig("mm_fused_update", c_int, POINTER(AdamModule), c_int, POINTER(AdamHyper), c_void_p, c_void_p)
     # NCCL plumbing (K1/K2)
@@ -225,6 +227,7 @@ def _declare(h: ctypes.CDLL) -> None:
     sig("mm_launch_count", ctypes.c_ulonglong)
     sig("mm_gemm", c_int, c_void_p, c_void_p)
     sig("mm_gemm_grouped", c_int, c_void_p, c_int, c_void_p)
+    sig("mm_abi_sizeof", c_int64, c_char_p)
     sig("mm_gemm_timing", c_int, c_int, POINTER(c_double), POINTER(c_float), POINTER(c_int))
     sig("mm_gemm_spans", c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_int))
     sig("mm_step_timing", c_int, c_int, POINTER(c_float), POINTER(c_int))
@@ -249,6 +252,7 @@ def _declare(h: ctypes.CDLL) -> None:
     sig("mm_flush_l2", c_int, c_void_p, c_size_t, c_void_p)
     sig("mm_memset", c_int, c_void_p, c_int, c_size_t, c_void_p)
     sig("mm_axpy_f32", c_int, c_void_p, c_void_p, c_float, c_int64, c_void_p)
+    sig("mm_axpy_f64", c_int, c_void_p, c_void_p, c_double, c_int64, c_void_p)
     sig("mm_task_fwd_bwd", c_int, c_void_p, c_void_p, c_void_p, POINTER(c_size_t), c_void_p,
         c_void_p, c_void_p)
 

@@ -31,7 +31,7 @@ class EmulatedCluster:
                  exchange: str = "sync", **kw):
         if exchange not in ("sync", "peer"):
             raise ValueError(f"unknown exchange {exchange!r}")
-        self.exchange = exchange
+        self.exchange_kind = exchange
         self.world = world
         self.ranks = [Engine(tasks, topo, shape, rank=r, world=1, device=device, seed=seed, **kw)
                       for r in range(world)]
@@ -65,8 +65,19 @@ class EmulatedCluster:
 
     def exchange_and_update(self, used_by_rank, exchange: str = None) -> list:
         """Algorithm-1 exchange + optimizer update; returns the ready counts."""
+        counts = self.exchange(used_by_rank, exchange)
+        if (exchange or self.exchange_kind) != "peer":
+            for r in used_by_rank:
+                self.update_rank(r, counts)
+        return counts
+
+    def exchange(self, used_by_rank, exchange: str = None) -> list:
+        """The cross-rank part only: one mm_sync_emulated launch over every
+        shared module (sync), or option B's fused exchange + update of the
+        shared modules followed by each rank's singleton update (peer).
+        Returns the ready counts."""
         counts = ready_counts_all(self.plan, used_by_rank)
-        if (exchange or self.exchange) == "peer":
+        if (exchange or self.exchange_kind) == "peer":
             self._peer_exchange(used_by_rank, counts)
             return counts
         table = []
@@ -87,16 +98,17 @@ class EmulatedCluster:
             # the emulated kernel already divides by n and installs the mean on
             # every member; K3 then runs with n = 1 for those modules
             ops.sync_emulated(table, only_ready=True)
-        idx = self.plan.index()
-        for r, eng in enumerate(self.ranks):
-            if r not in used_by_rank:
-                continue
-            per_rank = []
-            for k in self.plan.keys:
-                n = counts[idx[k]]
-                per_rank.append(1 if (n >= 1 and len(self.plan.groups[k]) >= 2) else n)
-            eng.fused_update(per_rank)
         return counts
+
+    def update_rank(self, r: int, counts) -> None:
+        """Rank r's K3 after a sync exchange (shared modules already hold the
+        mean: n = 1; singletons divide by their own count)."""
+        idx = self.plan.index()
+        per_rank = []
+        for k in self.plan.keys:
+            n = counts[idx[k]]
+            per_rank.append(1 if (n >= 1 and len(self.plan.groups[k]) >= 2) else n)
+        self.ranks[r].fused_update(per_rank)
 
     def _peer_exchange(self, used_by_rank, counts) -> None:
         from .peer import make_shard

@@ -44,6 +44,19 @@ int num_sms() {
 
 extern "C" int mm_abi_version(void) { return MMB200_ABI_VERSION; }
 
+// sizeof of every descriptor struct of include/mmb200.h, by name (the
+// binding's ctypes mirrors are checked against these), -1 if unknown
+extern "C" long long mm_abi_sizeof(const char* name) {
+    if (!name) return -1;
+    const std::string n(name);
+#define MM_SZ(T) if (n == #T) return static_cast<long long>(sizeof(T));
+    MM_SZ(mm_sync_module) MM_SZ(mm_adam_module) MM_SZ(mm_adam_hyper) MM_SZ(mm_reduce_item)
+    MM_SZ(mm_peer_shard) MM_SZ(mm_peer_signal) MM_SZ(mm_gemm_args) MM_SZ(mm_attn_args)
+    MM_SZ(mm_layer_offsets) MM_SZ(mm_stack) MM_SZ(mm_embed) MM_SZ(mm_task) MM_SZ(mm_batch)
+#undef MM_SZ
+    return -1;
+}
+
 extern "C" unsigned long long mm_launch_count(void) { return mm::g_launches.load(); }
 
 extern "C" const char* mm_last_error(void) { return mm::g_last_error.c_str(); }

@@ -22,7 +22,7 @@ constexpr int64_t kChunk = int64_t(kThreads) * kVecPerThread * 4 * 4;  // 16384 
 // ---------------------------------------------------------------------------
 // emulated sync
 
-constexpr int kSyncMaxMods = 64;
+constexpr int kSyncMaxMods = 32;  // kernel-parameter table: 32 x 296 B
 
 struct SyncTable {
     mm_sync_module mod[kSyncMaxMods];
@@ -95,6 +95,52 @@ __global__ void __launch_bounds__(kThreads) sync_emulated_kernel(const __grid_co
             const float y = __fdiv_rn(acc, fn);
             for (int r = 0; r < g; ++r) md.bufs[r][i] = y;
             if (md.out) md.out[i] = y;
+        }
+    }
+}
+
+// fp64 buffers (the reference's default DeviceState dtype, syncsim.py:103-106):
+// the same chunk table, member pointers addressing doubles; 16-byte double2
+// accesses, IEEE double adds in ascending member order and __ddiv_rn
+__global__ void __launch_bounds__(kThreads) sync_emulated_f64_kernel(const __grid_constant__ SyncTable t) {
+    pdl_wait();
+    const int64_t chunk = blockIdx.x;
+    const int m = find_module(t.chunk_begin, t.n_mods, chunk);
+    const mm_sync_module& md = t.mod[m];
+    double* const* bufs = reinterpret_cast<double* const*>(md.bufs);
+    double* out = reinterpret_cast<double*>(md.out);
+    const int g = md.group_size;
+    const int n = __popc(md.used_mask);
+    const int64_t base = (chunk - t.chunk_begin[m]) * kChunk;
+    const int64_t end = min(base + kChunk, md.n_elems);
+    if (n == 0) {
+        if (out) for (int64_t i = base + threadIdx.x; i < end; i += kThreads) out[i] = 0.0;
+        return;
+    }
+    const uint32_t take = t.only_ready ? md.used_mask : ((g >= 32) ? 0xffffffffu : ((1u << g) - 1u));
+    const double fn = static_cast<double>(n);
+    if ((md.n_elems & 1) == 0) {
+        const int64_t v0 = base >> 1, v1 = end >> 1;
+        for (int64_t v = v0 + threadIdx.x; v < v1; v += kThreads) {
+            double2 acc = make_double2(0.0, 0.0);
+            for (int r = 0; r < g; ++r) {
+                if (!((take >> r) & 1u)) continue;
+                const double2 x = __ldcs(reinterpret_cast<const double2*>(bufs[r]) + v);
+                acc.x = __dadd_rn(acc.x, x.x);
+                acc.y = __dadd_rn(acc.y, x.y);
+            }
+            const double2 y = make_double2(__ddiv_rn(acc.x, fn), __ddiv_rn(acc.y, fn));
+            for (int r = 0; r < g; ++r) __stcs(reinterpret_cast<double2*>(bufs[r]) + v, y);
+            if (out) __stcs(reinterpret_cast<double2*>(out) + v, y);
+        }
+    } else {
+        for (int64_t i = base + threadIdx.x; i < end; i += kThreads) {
+            double acc = 0.0;
+            for (int r = 0; r < g; ++r)
+                if ((take >> r) & 1u) acc = __dadd_rn(acc, bufs[r][i]);
+            const double y = __ddiv_rn(acc, fn);
+            for (int r = 0; r < g; ++r) bufs[r][i] = y;
+            if (out) out[i] = y;
         }
     }
 }
@@ -191,10 +237,18 @@ __global__ void axpy_kernel(float* __restrict__ y, const float* __restrict__ x, 
         y[i] = fmaf(alpha, x[i], y[i]);
 }
 
+__global__ void axpy_f64_kernel(double* __restrict__ y, const double* __restrict__ x, double alpha,
+                                int64_t n) {
+    pdl_wait();
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        y[i] = fma(alpha, x[i], y[i]);
+}
+
 }  // namespace
 
-extern "C" int mm_sync_emulated(const mm_sync_module* mods, int n_mods, int only_ready,
-                                void* stream) {
+static int sync_emulated(const mm_sync_module* mods, int n_mods, int only_ready, bool f64,
+                         void* stream) {
     MM_CHECK_ARG(n_mods >= 0 && (n_mods == 0 || mods), "bad module table");
     for (int base = 0; base < n_mods; base += kSyncMaxMods) {
         SyncTable t{};
@@ -203,21 +257,22 @@ extern "C" int mm_sync_emulated(const mm_sync_module* mods, int n_mods, int only
         int64_t chunks = 0;
         for (int i = 0; i < t.n_mods; ++i) {
             const mm_sync_module& md = mods[base + i];
-            MM_CHECK_ARG(md.group_size >= 1 && md.group_size <= MM_MAX_GROUP,
+            MM_CHECK_ARG(md.group_size >= 1 && md.group_size <= MM_MAX_SYNC_GROUP,
                          "module %d: group size %d outside [1,%d]", base + i, md.group_size,
-                         MM_MAX_GROUP);
+                         MM_MAX_SYNC_GROUP);
             MM_CHECK_ARG(md.n_elems >= 0, "module %d: negative size", base + i);
-            MM_CHECK_ARG((md.used_mask >> md.group_size) == 0, "module %d: used bit beyond group",
+            MM_CHECK_ARG(md.group_size == 32 || (md.used_mask >> md.group_size) == 0, "module %d: used bit beyond group",
                          base + i);
             mm_sync_module c = md;
-            bool vec = (md.n_elems & 3) == 0 && (md.out == nullptr || aligned16(md.out));
+            const int64_t vmask = f64 ? 1 : 3;  // elements per 16-byte vector - 1
+            bool vec = (md.n_elems & vmask) == 0 && (md.out == nullptr || aligned16(md.out));
             for (int r = 0; r < md.group_size; ++r) {
                 MM_CHECK_ARG(md.bufs[r] != nullptr, "module %d: NULL member buffer", base + i);
                 vec = vec && aligned16(md.bufs[r]);
             }
             // the kernel takes the float4 path iff n_elems % 4 == 0, which needs
             // 16-byte aligned buffers (torch allocations are 256-byte aligned)
-            MM_CHECK_ARG(vec || (md.n_elems & 3) != 0,
+            MM_CHECK_ARG(vec || (md.n_elems & vmask) != 0,
                          "module %d: buffers must be 16-byte aligned", base + i);
             t.mod[i] = c;
             t.chunk_begin[i] = chunks;
@@ -225,11 +280,21 @@ extern "C" int mm_sync_emulated(const mm_sync_module* mods, int n_mods, int only
         }
         t.chunk_begin[t.n_mods] = chunks;
         if (chunks == 0) continue;
-        MM_CUDA_TRY(mm::launch_pdl(sync_emulated_kernel, dim3((unsigned)chunks), dim3(kThreads), 0,
-                                   mm::as_stream(stream), t));
-        MM_LAUNCH_CHECK("sync_emulated_kernel");
+        MM_CUDA_TRY(mm::launch_pdl(f64 ? sync_emulated_f64_kernel : sync_emulated_kernel,
+                                   dim3((unsigned)chunks), dim3(kThreads), 0, mm::as_stream(stream), t));
+        MM_LAUNCH_CHECK(f64 ? "sync_emulated_f64_kernel" : "sync_emulated_kernel");
     }
     return 0;
+}
+
+extern "C" int mm_sync_emulated(const mm_sync_module* mods, int n_mods, int only_ready,
+                                void* stream) {
+    return sync_emulated(mods, n_mods, only_ready, false, stream);
+}
+
+extern "C" int mm_sync_emulated_f64(const mm_sync_module* mods, int n_mods, int only_ready,
+                                    void* stream) {
+    return sync_emulated(mods, n_mods, only_ready, true, stream);
 }
 
 extern "C" int mm_fused_update(const mm_adam_module* mods, int n_mods, const mm_adam_hyper* hyper,
@@ -282,6 +347,16 @@ extern "C" int mm_axpy_f32(float* y, const float* x, float alpha, int64_t n, voi
     MM_CUDA_TRY(mm::launch_pdl(axpy_kernel, dim3(grid), dim3(256), 0, mm::as_stream(stream), y, x,
                                alpha, n));
     MM_LAUNCH_CHECK("axpy_kernel");
+    return 0;
+}
+
+extern "C" int mm_axpy_f64(double* y, const double* x, double alpha, int64_t n, void* stream) {
+    MM_CHECK_ARG((y && x) || n == 0, "NULL pointer");
+    if (n == 0) return 0;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 8 * mm::num_sms()));
+    MM_CUDA_TRY(mm::launch_pdl(axpy_f64_kernel, dim3(grid), dim3(256), 0, mm::as_stream(stream), y, x,
+                               alpha, n));
+    MM_LAUNCH_CHECK("axpy_f64_kernel");
     return 0;
 }
 

@@ -252,20 +252,30 @@ def memset(t: torch.Tensor, value: int = 0) -> None:
 
 
 def axpy(y: torch.Tensor, x: torch.Tensor, alpha: float) -> None:
-    _need(y, torch.float32, "y")
-    _need(x, torch.float32, "x")
+    """y += alpha * x over fp32 or fp64 CUDA tensors (mm_axpy_f32 / _f64)."""
+    dt = y.dtype if y.dtype in (torch.float32, torch.float64) else torch.float32
+    _need(y, dt, "y")
+    _need(x, dt, "x")
     if y.numel() != x.numel() or not (y.is_contiguous() and x.is_contiguous()):
         raise ValueError("axpy needs equal-size contiguous tensors")
     LAUNCHES[0] += 1
-    check(lib().mm_axpy_f32(y.data_ptr(), x.data_ptr(), alpha, y.numel(), stream_ptr()),
-          "mm_axpy_f32")
+    if dt == torch.float64:
+        check(lib().mm_axpy_f64(y.data_ptr(), x.data_ptr(), alpha, y.numel(), stream_ptr()),
+              "mm_axpy_f64")
+    else:
+        check(lib().mm_axpy_f32(y.data_ptr(), x.data_ptr(), alpha, y.numel(), stream_ptr()),
+              "mm_axpy_f32")
 
 
-def sync_emulated(mods, only_ready: bool) -> None:
+def sync_emulated(mods, only_ready: bool, f64: bool = False) -> None:
     arr = (_native.SyncModule * len(mods))(*mods)
     LAUNCHES[0] += 1
-    check(lib().mm_sync_emulated(arr, len(mods), int(only_ready), stream_ptr()),
-          "mm_sync_emulated")
+    if f64:
+        check(lib().mm_sync_emulated_f64(arr, len(mods), int(only_ready), stream_ptr()),
+              "mm_sync_emulated_f64")
+    else:
+        check(lib().mm_sync_emulated(arr, len(mods), int(only_ready), stream_ptr()),
+              "mm_sync_emulated")
 
 
 def peer_shard_begin(n_elems: int, group_size: int, member: int) -> int:

@@ -18,7 +18,9 @@ from __future__ import annotations
 
 import dataclasses
 import random
-from typing import Iterable, Mapping, Sequence
+from typing import Iterable, Mapping, Optional, Sequence
+
+import numpy as np
 
 import torch
 
@@ -33,43 +35,81 @@ READY_ENTRY_BYTES = 4
 
 @dataclasses.dataclass
 class DeviceState:
-    """One device: hosted modules, a CUDA fp32 buffer per hosted module and
-    the set of modules used this step (syncsim.py:90-118)."""
+    """One device: hosted modules, one buffer per hosted module and the set
+    of modules used this step (syncsim.py:90-118).
+
+    ``device=None`` (the reference's constructor): float64 numpy buffers on
+    the host, as the reference allocates them; ``accumulate`` and
+    ``sync_step`` still do every add / divide in the sm_100a kernels (the
+    arrays are staged through the GPU).  ``device="cuda"``: fp32 CUDA
+    buffers that stay resident.  Explicit ``buffers`` may be numpy arrays or
+    CUDA tensors, float32 or float64."""
 
     index: int
     hosted: frozenset
     dim: int
     buffers: dict = dataclasses.field(default_factory=dict)
     used: set = dataclasses.field(default_factory=set)
-    device: str = "cuda"
+    device: Optional[str] = None
 
     def __post_init__(self) -> None:
         if not self.buffers:
-            self.buffers = {k: torch.zeros(self.dim, self.dim, device=self.device)
-                            for k in sorted(self.hosted)}
+            if self.device is None:
+                self.buffers = {k: np.zeros((self.dim, self.dim)) for k in sorted(self.hosted)}
+            else:
+                self.buffers = {k: torch.zeros(self.dim, self.dim, device=self.device)
+                                for k in sorted(self.hosted)}
 
     def reset(self) -> None:
         for buf in self.buffers.values():
-            ops.memset(buf, 0)
+            if isinstance(buf, np.ndarray):
+                buf[...] = 0.0
+            else:
+                ops.memset(buf, 0)
         self.used.clear()
 
-    def accumulate(self, grads: Mapping[ModuleKey, torch.Tensor]) -> None:
+    def accumulate(self, grads: Mapping[ModuleKey, object]) -> None:
+        """buffers[key] += g for every (key, g); g may be a numpy array or a
+        tensor.  The add runs on the GPU (mm_axpy_f32 / _f64)."""
         for key, g in grads.items():
             if key not in self.hosted:
                 raise SimulationError(f"gradient for unhosted module {key}")
             buf = self.buffers[key]
-            if g.shape != buf.shape:
-                raise SimulationError(f"gradient shape {tuple(g.shape)} != {tuple(buf.shape)}")
-            ops.axpy(buf, g.to(buf.device, torch.float32).contiguous(), 1.0)
+            if tuple(np.shape(g)) != tuple(buf.shape):
+                raise SimulationError(f"gradient shape {tuple(np.shape(g))} != {tuple(buf.shape)}")
+            if isinstance(buf, np.ndarray):
+                dt = _torch_dtype(buf.dtype)
+                y = torch.from_numpy(np.ascontiguousarray(buf)).to("cuda", dt)
+                ops.axpy(y.view(-1), _as_cuda(g, dt, y.device).view(-1), 1.0)
+                buf[...] = y.cpu().numpy()
+            else:
+                ops.axpy(buf.view(-1), _as_cuda(g, buf.dtype, buf.device).view(-1), 1.0)
             self.used.add(key)
 
 
-def sync_step(devices: Sequence[DeviceState], only_ready: bool = False) -> dict:
-    """Algorithm 1 over all devices (syncsim.py:121-153), one kernel launch.
+def _torch_dtype(dt) -> torch.dtype:
+    if dt == np.float64:
+        return torch.float64
+    if dt == np.float32:
+        return torch.float32
+    raise SimulationError(f"buffers must be float32 or float64, got {dt}")
 
-    ``only_ready=True`` skips reading the buffers of members that did not
-    use the module (exact when those buffers are zero, as after ``reset``).
-    """
+
+def _as_cuda(x, dtype: torch.dtype, device) -> torch.Tensor:
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+    return t.to(device=device, dtype=dtype).contiguous()
+
+
+def sync_step(devices: Sequence[DeviceState], only_ready: bool = False) -> dict:
+    """Algorithm 1 over all devices (syncsim.py:121-153), one kernel launch
+    per dtype (mm_sync_emulated / mm_sync_emulated_f64).
+
+    Host (numpy) buffers are staged to the GPU and the results written back
+    as the reference does (every member's buffer replaced by the synced
+    value when n >= 1, untouched when n == 0); the returned synced values are
+    numpy arrays then, CUDA tensors for CUDA buffers.  ``only_ready=True``
+    skips reading the buffers of members that did not use the module (exact
+    when those buffers are zero, as after ``reset``)."""
     ordered = sorted(devices, key=lambda d: d.index)
     if len({d.index for d in ordered}) != len(ordered):
         raise SimulationError("duplicate device index")
@@ -77,16 +117,35 @@ def sync_step(devices: Sequence[DeviceState], only_ready: bool = False) -> dict:
         raise SimulationError("inconsistent module dimensions across devices")
     keys = sorted(set().union(*(d.hosted for d in ordered))) if ordered else []
     synced: dict = {}
-    table = []
+    tables = {torch.float32: [], torch.float64: []}
+    staged = {}   # (device index, key) -> CUDA tensor of a host buffer
+    host_out = {}
     for key in keys:
         members = [d for d in ordered if key in d.hosted]
-        if len(members) > _native.MAX_GROUP:
-            raise SimulationError(f"module {key}: {len(members)} hosts > {_native.MAX_GROUP}")
-        ref = members[0].buffers[key]
-        for d in members:
-            b = d.buffers[key]
-            if b.dtype != torch.float32 or not b.is_cuda or not b.is_contiguous():
-                raise SimulationError("buffers must be contiguous CUDA fp32 tensors")
+        if len(members) > _native.MAX_SYNC_GROUP:
+            raise SimulationError(f"module {key}: {len(members)} hosts > {_native.MAX_SYNC_GROUP}")
+        bufs = [d.buffers[key] for d in members]
+        host = [isinstance(b, np.ndarray) for b in bufs]
+        if any(host) and not all(host):
+            raise SimulationError(f"module {key}: host and device buffers mixed")
+        if any(host):
+            dt = _torch_dtype(bufs[0].dtype)
+            if any(_torch_dtype(b.dtype) != dt for b in bufs):
+                raise SimulationError(f"module {key}: buffer dtypes differ across devices")
+            dev_bufs = []
+            for d, b in zip(members, bufs):
+                t = torch.from_numpy(np.ascontiguousarray(b)).to("cuda", dt)
+                staged[(d.index, key)] = t
+                dev_bufs.append(t)
+        else:
+            dev_bufs = bufs
+            dt = bufs[0].dtype
+        ref = dev_bufs[0]
+        for b in dev_bufs:
+            if b.dtype not in (torch.float32, torch.float64) or not b.is_cuda or not b.is_contiguous():
+                raise SimulationError("buffers must be contiguous float32 / float64 tensors")
+            if b.dtype != ref.dtype:
+                raise SimulationError(f"module {key}: buffer dtypes differ across devices")
             if b.shape != ref.shape:
                 raise SimulationError(f"module {key}: buffer shapes differ across devices")
             if b.device != ref.device:
@@ -96,16 +155,25 @@ def sync_step(devices: Sequence[DeviceState], only_ready: bool = False) -> dict:
                 raise SimulationError(f"module {key}: buffers on different CUDA devices")
         out = torch.empty_like(ref)
         synced[key] = out
+        if any(host):
+            host_out[key] = members
         m = _native.SyncModule()
-        for r, d in enumerate(members):
-            m.bufs[r] = d.buffers[key].data_ptr()
+        for r, b in enumerate(dev_bufs):
+            m.bufs[r] = b.data_ptr()
         m.out = out.data_ptr()
         m.n_elems = ref.numel()
         m.group_size = len(members)
         m.used_mask = sum(1 << r for r, d in enumerate(members) if key in d.used)
-        table.append(m)
-    if table:
-        ops.sync_emulated(table, only_ready)
+        tables[ref.dtype].append(m)
+    for dt, table in tables.items():
+        if table:
+            ops.sync_emulated(table, only_ready, f64=dt == torch.float64)
+    for key, members in host_out.items():
+        val = synced[key].cpu().numpy()
+        synced[key] = val
+        if any(key in d.used for d in members):  # n >= 1: install on every member
+            for d in members:
+                d.buffers[key] = val.copy()
     return synced
 
 
@@ -255,7 +323,7 @@ def step_optimizer(module_buckets: Mapping, ready_counts: Mapping, adam=None) ->
 
 def run_benchmark(tasks: Sequence[TaskSpec], topo: ClusterTopology, steps: int, seed: int = 0,
                   accum_count: int = 1, dim: int = 4, batch_tokens: int = 4096,
-                  compute_coeff: float = 2e-9, shape=None, device=None):
+                  compute_coeff: float = 2e-9, shape=None, device=None, timing: str = "measured"):
     """``run_benchmark`` (syncsim.py:295-392) with the toy model replaced by
     the real modular transformer: every device of ``topo`` that holds a task
     is an emulated rank on this GPU (``cluster.EmulatedCluster``); each step
@@ -266,17 +334,27 @@ def run_benchmark(tasks: Sequence[TaskSpec], topo: ClusterTopology, steps: int, 
 
     Ledger columns: ``ready_bytes`` / ``grad_bytes`` / ``tokens`` follow the
     reference's definitions exactly (module sizes in the reference's
-    enumerate_modules convention, syncsim.py:318, 365-379); ``compute_time``
-    (max over devices) and ``comm_time`` (exchange + update) are MEASURED
-    with CUDA events instead of modeled, so ``dim`` and ``compute_coeff`` are
-    accepted for signature compatibility only.  Returns (CommLedger, summary
-    dict with the reference's keys)."""
+    enumerate_modules convention, syncsim.py:318, 365-379).  Times:
+
+    * ``timing="measured"``: CUDA events.  ``compute_time`` = max over ranks
+      of that rank's forward / backward plus its own K3 update (each rank
+      would run on its own GPU); ``comm_time`` = the cross-rank exchange
+      (one mm_sync_emulated launch over every shared module; with option B
+      the fused exchange + update).  ``dim`` and ``compute_coeff`` unused.
+    * ``timing="modeled"``: the reference's own cost model on the same run --
+      compute = compute_coeff * batch_tokens * layers per micro-batch (max
+      over devices), comm = the ring model per group with the link class it
+      spans (syncsim.py:355-392) -- so E(k) equals the reference's.
+
+    Returns (CommLedger, summary dict with the reference's keys)."""
+    if timing not in ("measured", "modeled"):
+        raise ValueError(f"unknown timing {timing!r}")
     import numpy as np
     from . import configs
     from .cluster import EmulatedCluster
     from .data import ZipfIds, make_batch
     from .engine import DeviceBatch
-    from .plan import ready_counts_all, task_modules
+    from .plan import task_modules
     from .sharing import enumerate_modules
     tasks = sorted(tasks, key=lambda t: t.id)
     for t in tasks:
@@ -294,8 +372,10 @@ def run_benchmark(tasks: Sequence[TaskSpec], topo: ClusterTopology, steps: int, 
     data_rngs = {i: np.random.default_rng([seed, i]) for i in ranks}
     ledger = CommLedger()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    layers = {t.id: sum(t.enc_layers) + sum(t.dec_layers) for t in tasks}
+    node_of = {i: i // topo.n_gpus_per_node for i in ranks}
     for step in range(steps):
-        used_by_rank, comp = {}, {}
+        used_by_rank, comp, modeled = {}, {}, {}
         step_tokens = 0
         for i in ranks:
             eng = cl.ranks[i]
@@ -303,6 +383,7 @@ def run_benchmark(tasks: Sequence[TaskSpec], topo: ClusterTopology, steps: int, 
             used: set = set()
             e0, e1 = ev(), ev()
             e0.record()
+            modeled[i] = 0.0
             for _ in range(accum_count):
                 task = eng.mux.pick(step)
                 b = make_batch(data_rngs[i], spec, shape.vocab, ids=ids)
@@ -311,29 +392,47 @@ def run_benchmark(tasks: Sequence[TaskSpec], topo: ClusterTopology, steps: int, 
                 used.update(fresh)
                 eng.forward_backward(task, DeviceBatch(b, dev), eng.loss_sum)
                 step_tokens += batch_tokens
+                modeled[i] += compute_coeff * batch_tokens * layers[task.id]
             e1.record()
             used_by_rank[i] = used
-            comp[i] = (e0, e1)
+            comp[i] = [(e0, e1)]
         c0, c1 = ev(), ev()
         c0.record()
-        cl.exchange_and_update(used_by_rank)
+        counts = cl.exchange(used_by_rank)
         c1.record()
+        if cl.exchange_kind != "peer":
+            for i in ranks:
+                u0, u1 = ev(), ev()
+                u0.record()
+                cl.update_rank(i, counts)
+                u1.record()
+                comp[i].append((u0, u1))
         torch.cuda.synchronize(dev)
-        counts = ready_counts_all(plan, used_by_rank)
         idx = plan.index()
         ready_bytes = grad_bytes = 0
+        comm_model = 0.0
         for key in sorted(modules):
             group = plan.groups.get(key, [])
-            if len(group) < 2:
+            g = len(group)
+            if g < 2:
                 continue
-            ready_bytes += READY_ENTRY_BYTES * len(group)
+            spans = len({node_of[i] for i in group}) > 1
+            alpha = topo.alpha_inter if spans else topo.alpha_intra
+            beta = topo.beta_inter if spans else topo.beta_intra
+            ready_bytes += READY_ENTRY_BYTES * g
+            comm_model += ring_allreduce_time(READY_ENTRY_BYTES, g, alpha, beta)
             if counts[idx[key]] >= 1:
-                grad_bytes += GRAD_BYTES_PER_PARAM * modules[key].n_params
-        ledger.records.append(StepRecord(
-            step=step, ready_bytes=ready_bytes, grad_bytes=grad_bytes,
-            comm_time=c0.elapsed_time(c1) * 1e-3,
-            compute_time=max(a.elapsed_time(b) for a, b in comp.values()) * 1e-3 if comp else 0.0,
-            tokens=step_tokens))
+                payload = GRAD_BYTES_PER_PARAM * modules[key].n_params
+                grad_bytes += payload
+                comm_model += ring_allreduce_time(payload, g, alpha, beta)
+        if timing == "modeled":
+            comm_t = comm_model
+            comp_t = max(modeled.values()) if modeled else 0.0
+        else:
+            comm_t = c0.elapsed_time(c1) * 1e-3
+            comp_t = max(sum(a.elapsed_time(b) for a, b in v) for v in comp.values()) * 1e-3 if comp else 0.0
+        ledger.records.append(StepRecord(step=step, ready_bytes=ready_bytes, grad_bytes=grad_bytes,
+                                         comm_time=comm_t, compute_time=comp_t, tokens=step_tokens))
     summary = {
         "steps": steps, "devices": len(ranks), "tasks": len(tasks), "modules": len(modules),
         "total_tokens": ledger.total_tokens, "total_time_sec": ledger.total_time,
@@ -342,3 +441,22 @@ def run_benchmark(tasks: Sequence[TaskSpec], topo: ClusterTopology, steps: int, 
     }
     return ledger, summary
 
+
+
+def scaling_experiment(arch_kind: str, gpu_counts: Sequence[int], n_gpus_per_node: int = 4,
+                       steps: int = 5, seed: int = 0, **benchmark_kwargs) -> dict:
+    """E(k) = throughput(k) / (k * throughput(1)) of the uniform workload
+    (one task per GPU, ``synthetic_uniform_tasks``), syncsim.py:461-483, over
+    this package's run_benchmark (the real engine; pass timing="modeled"
+    for the reference's cost model, timing="measured" for CUDA-event
+    times of the emulated ranks)."""
+
+    def throughput(k: int) -> float:
+        n_nodes = max(1, -(-k // n_gpus_per_node))
+        topo = ClusterTopology(n_nodes=n_nodes, n_gpus_per_node=n_gpus_per_node, n_slots_per_gpu=1)
+        tasks = synthetic_uniform_tasks(arch_kind, k, topo)
+        ledger, _ = run_benchmark(tasks, topo, steps=steps, seed=seed, **benchmark_kwargs)
+        return ledger.tokens_per_sec
+
+    base = throughput(1)
+    return {k: throughput(k) / (k * base) for k in gpu_counts}

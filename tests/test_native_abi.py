@@ -37,8 +37,19 @@ def test_header_version_matches_binding():
 
 
 def test_struct_layouts():
+    # the ctypes mirrors have the sizes the C side was compiled with
+    from paper_2403_07544_b200 import ops
+    mirrors = {"mm_sync_module": _native.SyncModule, "mm_adam_module": _native.AdamModule,
+               "mm_adam_hyper": _native.AdamHyper, "mm_reduce_item": _native.ReduceItem,
+               "mm_peer_shard": _native.PeerShard, "mm_peer_signal": _native.PeerSignal,
+               "mm_gemm_args": ops.GemmArgs, "mm_attn_args": ops.AttnArgs,
+               "mm_layer_offsets": _native.LayerOffsets, "mm_stack": _native.Stack,
+               "mm_embed": _native.Embed, "mm_task": _native.Task, "mm_batch": _native.BatchDesc}
+    for name, cls in mirrors.items():
+        assert _native.lib().mm_abi_sizeof(name.encode()) == ctypes.sizeof(cls), name
+    assert _native.lib().mm_abi_sizeof(b"nope") == -1
     # offsets the C side relies on (include/mmb200.h)
-    assert ctypes.sizeof(_native.SyncModule) == 8 * 8 + 8 + 8 + 4 + 4
+    assert ctypes.sizeof(_native.SyncModule) == 32 * 8 + 8 + 8 + 4 + 4
     assert ctypes.sizeof(_native.AdamModule) == 5 * 8 + 8 + 4 + 4 + 4 + 4
     assert ctypes.sizeof(_native.AdamHyper) == 7 * 4 + 4 + 4  # + zero_grad
     assert ctypes.sizeof(_native.ReduceItem) == 8 + 8 + 8 + 4 + 4

@@ -21,34 +21,112 @@ def golden():
 
 
 def _devices(meta, arrays, s, cuda):
+    """The scenario's devices with CUDA buffers (cuda) or the reference's own
+    numpy buffers (cuda=None)."""
     from paper_2403_07544_b200.syncsim import DeviceState
     devs = []
     for j, d in enumerate(meta["devices"]):
         hosted = frozenset(ModuleKey.parse(k) for k in d["hosted"])
-        bufs = {k: torch.from_numpy(arrays[f"s{s}_in_{j}_{k}"]).to(cuda) for k in d["hosted"]}
-        bufs = {ModuleKey.parse(k): v for k, v in bufs.items()}
+        bufs = {ModuleKey.parse(k): arrays[f"s{s}_in_{j}_{k}"].copy() for k in d["hosted"]}
+        if cuda is not None:
+            bufs = {k: torch.from_numpy(v).to(cuda) for k, v in bufs.items()}
         devs.append(DeviceState(d["index"], hosted, 1, bufs, {ModuleKey.parse(k) for k in d["used"]}))
     return devs
 
 
-def test_sync_step_bit_exact_vs_reference(golden, cuda):
+def _as_np(x):
+    return x.cpu().numpy() if isinstance(x, torch.Tensor) else x
+
+
+@pytest.mark.parametrize("where", ["cuda", "host"])
+def test_sync_step_bit_exact_vs_reference(golden, cuda, where):
+    """All 40 golden scenarios -- fp32 AND fp64 buffers (the reference's
+    default dtype) -- through sync_step: synced values and every device's
+    buffers afterwards equal the reference's own outputs bit for bit, with
+    CUDA buffers and with the reference's numpy buffers (staged through the
+    GPU kernels, written back as the reference does)."""
     from paper_2403_07544_b200.syncsim import sync_step
     arrays = np.load(os.path.join(GOLD, "sync_scenarios.npz"))
-    n_checked = 0
+    n_checked = {"float32": 0, "float64": 0}
     for meta in golden["scenarios"]:
-        if meta["dtype"] != "float32":
-            continue
         s = meta["seed"]
-        devs = _devices(meta, arrays, s, cuda)
+        devs = _devices(meta, arrays, s, cuda if where == "cuda" else None)
         synced = sync_step(devs)
         for key, val in synced.items():
             ref = arrays[f"s{s}_synced_{key}"]
-            assert np.array_equal(val.cpu().numpy(), ref), (s, str(key))
+            got = _as_np(val)
+            assert got.dtype == ref.dtype and np.array_equal(got, ref), (s, str(key))
+            if where == "host":
+                assert isinstance(val, np.ndarray)
         for j, d in enumerate(sorted(devs, key=lambda d: d.index)):
             for key, buf in d.buffers.items():
-                assert np.array_equal(buf.cpu().numpy(), arrays[f"s{s}_after_{j}_{key}"]), (s, j)
-        n_checked += 1
-    assert n_checked >= 15
+                assert np.array_equal(_as_np(buf), arrays[f"s{s}_after_{j}_{key}"]), (s, j)
+        n_checked[meta["dtype"]] += 1
+    assert n_checked["float32"] >= 15 and n_checked["float64"] >= 15
+
+
+def test_reference_device_state_semantics(cuda):
+    """The reference's DeviceState API unchanged (syncsim.py:90-153): float64
+    numpy buffers by default, numpy gradients accumulated, buffers written
+    in place by the user, results returned as numpy arrays -- every add and
+    divide done by the CUDA kernels."""
+    from paper_2403_07544_b200.domain import Side
+    from paper_2403_07544_b200.plan import SimulationError
+    from paper_2403_07544_b200.syncsim import DeviceState, sync_step
+    key = ModuleKey(Side.ENCODER, 0, "full")
+    d1, d2 = DeviceState(0, frozenset({key}), 1), DeviceState(1, frozenset({key}), 1)
+    assert d1.buffers[key].dtype == np.float64 and d1.buffers[key].shape == (1, 1)
+    d1.buffers[key][:] = 2.0
+    d2.buffers[key][:] = 4.0
+    d1.used.add(key)
+    d2.used.add(key)
+    synced = sync_step([d1, d2])
+    assert synced[key][0, 0] == 3.0 and d1.buffers[key][0, 0] == 3.0 and d2.buffers[key][0, 0] == 3.0
+    # renormalised by users, not hosts
+    d1, d2 = DeviceState(0, frozenset({key}), 1), DeviceState(1, frozenset({key}), 1)
+    d1.buffers[key][:] = 4.0
+    d1.used.add(key)
+    synced = sync_step([d1, d2])
+    assert synced[key][0, 0] == 4.0 and d2.buffers[key][0, 0] == 4.0
+    # unused module stays zero
+    d1, d2 = DeviceState(0, frozenset({key}), 2), DeviceState(1, frozenset({key}), 2)
+    assert np.all(sync_step([d1, d2])[key] == 0.0)
+    # device mean, not task mean: ((1 + 3) + 2) / 2
+    d1, d2 = DeviceState(0, frozenset({key}), 1), DeviceState(1, frozenset({key}), 1)
+    d1.accumulate({key: np.array([[1.0]])})
+    d1.accumulate({key: np.array([[3.0]])})
+    d2.accumulate({key: np.array([[2.0]])})
+    assert sync_step([d1, d2])[key][0, 0] == 3.0
+    # unhosted gradient and duplicate index rejected
+    other = ModuleKey(Side.DECODER, 0, "x")
+    with pytest.raises(SimulationError):
+        d1.accumulate({other: np.zeros((1, 1))})
+    with pytest.raises(SimulationError):
+        sync_step([DeviceState(0, frozenset({key}), 1), DeviceState(0, frozenset({key}), 1)])
+    # reset clears buffers and the used set
+    d1.reset()
+    assert d1.buffers[key][0, 0] == 0.0 and not d1.used
+
+
+def test_toy_chain_vs_oracle_reference_fp64(cuda):
+    """The reference's randomized scenario (toy chain, syncsim.py:34-87)
+    through DeviceState.accumulate + sync_step in float64 on the GPU against
+    the oracle's oracle_reference: rtol 1e-9 as the reference asserts
+    (tests/test_syncsim.py:186-191)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(__file__)))
+    from oracle import algorithm1 as A
+    from paper_2403_07544_b200.syncsim import DeviceState, sync_step
+    for seed in range(6):
+        w, y, runs, hosted = A.random_toy_scenario(seed, accum_count=1 + seed % 2)
+        devices = {d: DeviceState(d, hosted[d], 3) for d in sorted(hosted)}
+        for d, chain, x in runs:
+            devices[d].accumulate(A.toy_neg_grads(w, y, chain, A.toy_forward(w, chain, x)))
+        synced = sync_step(list(devices.values()))
+        oracle = A.device_mean_oracle(runs, hosted, w, y, 3)
+        for key in oracle:
+            scale = max(1.0, np.abs(oracle[key]).max())
+            assert np.allclose(synced[key], oracle[key], rtol=1e-9, atol=1e-12 * scale), (seed, str(key))
 
 
 @pytest.mark.parametrize("only_ready", [False, True])

@@ -74,7 +74,11 @@ for name, m, n, k, ak, bk, epi in cases:
         if var != "auto":
             cg, bn = var.split(":")
             os.environ["MM_GEMM_CG"], os.environ["MM_GEMM_BN"] = cg, bn
-        us = timeit(run)
+        try:
+            us = timeit(run)
+        except Exception as e:  # shapes the kernel rejects (e.g. ld % 8)
+            line += f" {var} rejected ({str(e)[-40:]}) |"
+            continue
         D.zero_()
         ops.gemm(A, B, D, a_kmajor=ak, b_kmajor=bk, epilogue=epi, bias=bias)
         torch.cuda.synchronize()
