@@ -18,9 +18,17 @@ stopped) and the trainer's step index.
 
 Files are written to a temporary name and renamed, so a reader never sees a
 partial file.  Every rank calls ``save`` / ``load``; ranks write disjoint files.
+Saving a module in one layout removes that module's files of the other layout
+(a directory reused after switching the exchange never mixes them), and each
+rank's json is written LAST and lists the module files that rank wrote with
+the save's step index: the loader accepts a module file only if some rank's
+manifest lists it for the step being resumed, so an interrupted save (module
+files newer than their manifest, or missing) fails loudly instead of resuming
+a mix of steps.
 """
 from __future__ import annotations
 
+import glob
 import json
 import os
 from typing import Optional
@@ -50,7 +58,48 @@ def write_module(root: str, key, state: dict, step: int, n_elems: int,
     meta = np.array([step, n_elems] + (list(shard) if shard else [0, 1, 0, n_elems]), np.int64)
     path = module_path(root, key, None if shard is None else shard[:2])
     _atomic_savez(path, meta=meta, **arrays)
+    # drop this module's files of the other layout (or of another group size)
+    stale = glob.glob(glob.escape(module_path(root, key))[:-4] + ".s*of*.npz")
+    if shard is not None:  # keep the shards of this group size, drop the whole file
+        stale = [f for f in stale if not f.endswith(f"of{shard[1]}.npz")] + [module_path(root, key)]
+    for f in stale:
+        try:
+            os.remove(f)
+        except FileNotFoundError:
+            pass
     return path
+
+
+def manifest(root: str) -> dict:
+    """{module file (relative to root): step index} over every rank's json."""
+    out = {}
+    for path in glob.glob(os.path.join(glob.escape(root), "rank*.json")):
+        with open(path) as f:
+            st = json.load(f)
+        for rel in st.get("files", ()):
+            out[rel] = st.get("step_idx")
+    return out
+
+
+def check_manifest(root: str, files, step_idx) -> None:
+    """Every module file read must be listed by some rank's manifest for
+    ``step_idx`` (the resumed save)."""
+    listed = manifest(root)
+    for path in files:
+        rel = os.path.relpath(path, root)
+        if rel not in listed:
+            raise ValueError(f"{rel}: not in any rank's manifest (interrupted or stale save)")
+        if listed[rel] != step_idx:
+            raise ValueError(f"{rel}: written by the save of step {listed[rel]}, resuming {step_idx}")
+
+
+def module_files(root: str, key) -> list[str]:
+    """The files holding a module: its whole file, or all its shards."""
+    whole = module_path(root, key)
+    if os.path.exists(whole):
+        return [whole]
+    g = _shard_count(root, key)
+    return [module_path(root, key, (j, g)) for j in range(g)]
 
 
 def read_module(root: str, key, n_elems: int) -> tuple[dict, int]:

@@ -185,11 +185,9 @@ __device__ __forceinline__ bool has_bias(const Prob& p) {
                       ep == MM_EPI_F32_RESID || ep == MM_EPI_F32_RESID_LN);
 }
 
-// bv: this lane's bias value for column col0 + lane (preloaded per tile).
-// coalesced = true: the residual add / ReLU-backward mask are left to the
-// staged fix-up (epi_fixup_*), which reads those operands row-coalesced.
+// bv: this lane's bias value for column col0 + lane (preloaded per tile)
 __device__ __forceinline__ void epilogue_math(const Prob& p, int64_t row, int64_t col0,
-                                              float (&acc)[32], float bv, bool coalesced) {
+                                              float (&acc)[32], float bv) {
     const int ep = p.epilogue;
     if (has_bias(p)) {
 #pragma unroll
@@ -199,7 +197,7 @@ __device__ __forceinline__ void epilogue_math(const Prob& p, int64_t row, int64_
 #pragma unroll
         for (int j = 0; j < 32; ++j) acc[j] = fmaxf(acc[j], 0.f);
     }
-    if (coalesced || row >= p.m) return;
+    if (row >= p.m) return;
     const bool full = col0 + 32 <= p.n;
     if (ep == MM_EPI_BF16_DRELU) {
         const uint16_t* aux = reinterpret_cast<const uint16_t*>(p.aux) + row * p.ldd + col0;
@@ -261,59 +259,6 @@ __device__ __forceinline__ void stage_row(uint8_t* buf, int r, const float (&acc
             *reinterpret_cast<float4*>(buf + r * 128 + phys * 16) =
                 make_float4(acc[q * 4], acc[q * 4 + 1], acc[q * 4 + 2], acc[q * 4 + 3]);
         }
-    }
-}
-
-// Row-coalesced epilogue operands.  A lane-per-row read of a 32 x 32 tile
-// (lane r reads its row's 128 B) touches 32 cache lines per instruction and
-// is L1-wavefront bound (~3 us per 4096 x 512 fp32 residual); here lane j
-// reads column j of every row (one 128 B line per instruction for fp32, 64 B
-// for bf16 pairs), and the operand is
-// applied to the staged box in place -- same arithmetic, same order
-// (acc + bias, then + resid; bf16 rounding, then the ReLU-backward mask).
-// 32 independent coalesced loads per lane and chunk: one L2 round trip.
-__device__ __forceinline__ void resid_load(const Prob& p, int64_t row0, int64_t col0, int lane,
-                                               float (&r)[32]) {
-    const int64_t col = col0 + lane;
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-        r[i] = (row0 + i < p.m && col < p.n) ? __ldg(p.resid + (row0 + i) * p.ldd + col) : 0.f;
-}
-// fp32 box (SWIZZLE_128B, 128 B rows): element (i, lane)
-__device__ __forceinline__ void resid_fixup(uint8_t* buf, int lane, const float (&r)[32]) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        float* e = reinterpret_cast<float*>(buf + i * 128 + (((lane >> 2) ^ (i & 7)) << 4)) + (lane & 3);
-        *e += r[i];
-    }
-}
-// bf16 aux pairs: lane covers rows 2i + (lane >> 4), columns 2 (lane & 15) + {0, 1}
-__device__ __forceinline__ void aux_load(const Prob& p, int64_t row0, int64_t col0, int lane,
-                                             uint32_t (&a)[16]) {
-    const int64_t col = col0 + 2 * (lane & 15);
-    const uint16_t* aux = reinterpret_cast<const uint16_t*>(p.aux);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        const int64_t row = row0 + 2 * i + (lane >> 4);
-        uint32_t w = 0;
-        if (row < p.m) {
-            if (col + 1 < p.n) w = __ldg(reinterpret_cast<const uint32_t*>(aux + row * p.ldd + col));
-            else if (col < p.n) w = __ldg(aux + row * p.ldd + col);
-        }
-        a[i] = w;
-    }
-}
-// bf16 box (SWIZZLE_64B, 64 B rows): zero where the saved activation is <= 0
-__device__ __forceinline__ void drelu_fixup(uint8_t* buf, int lane, const uint32_t (&a)[16]) {
-    const int c2 = lane & 15;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        const int r = 2 * i + (lane >> 4);
-        uint32_t* e = reinterpret_cast<uint32_t*>(buf + r * 64 + (((c2 >> 2) ^ ((r >> 1) & 3)) << 4)) + (c2 & 3);
-        uint32_t v = *e;
-        if (bf16_to_f(a[i] & 0xffff) <= 0.f) v &= 0xffff0000u;
-        if (bf16_to_f(a[i] >> 16) <= 0.f) v &= 0x0000ffffu;
-        *e = v;
     }
 }
 
@@ -644,8 +589,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) + acc * BN +
                                    half * (BN / kSlices);
             float xs[CN > 1 ? kChunks : 1][32];  // LayerNorm input kept in registers
-            const bool co_resid = CN == 1 && P.epilogue == MM_EPI_F32_RESID;
-            const bool co_drelu = P.epilogue == MM_EPI_BF16_DRELU;
 #pragma unroll
             for (int c = 0; c < kChunks; ++c) {
                 const int col0 = cbase + c * 32;
@@ -656,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float f[32];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-                    epilogue_math(P, row, col0, f, bv[c], co_resid || co_drelu);
+                    epilogue_math(P, row, col0, f, bv[c]);
                     if constexpr (CN > 1) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) xs[c][j] = f[j];
@@ -665,19 +608,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (lane == 0) tc::bulk_wait_read<kEpiBufs - 1>();  // the store that last read `buf` is done
                     __syncwarp();
                     stage_row(buf, lane, f, out_bf16);
-                    // (operands loaded after staging: the accumulator registers
-                    // are dead by then, so the 32 loads in flight cost no spills)
-                    if (co_resid) {
-                        float rres[32];
-                        resid_load(P, row0, col0, lane, rres);
-                        __syncwarp();
-                        resid_fixup(buf, lane, rres);
-                    } else if (co_drelu) {
-                        uint32_t raux[16];
-                        aux_load(P, row0, col0, lane, raux);
-                        __syncwarp();
-                        drelu_fixup(buf, lane, raux);
-                    }
                     tc::fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0 && !(MM_GEMM_DEBUG & 2)) {

@@ -170,20 +170,34 @@ class CorpusStream:
         self.tokenize = tokenize
         self.max_len = max_len
         self.epoch = 0
+        self.line = 0  # lines of the current epoch already consumed
+        self._it = self._pairs()
+
+    def state(self) -> dict:
+        return {"epoch": self.epoch, "line": self.line}
+
+    def load_state(self, st: dict) -> None:
+        """Resume at (epoch, line): the next pair is the first usable one
+        after the consumed lines of that epoch."""
+        self.epoch, self.line = int(st["epoch"]), int(st["line"])
         self._it = self._pairs()
 
     def _pairs(self) -> Iterator[tuple[list[int], list[int]]]:
         while True:
-            n = 0
+            n, skip = 0, self.line
             with open(self.src_path) as fs, open(self.tgt_path) as ft:
-                for ls, lt in zip(fs, ft):
+                for idx, (ls, lt) in enumerate(zip(fs, ft)):
+                    if idx < skip:
+                        continue
+                    self.line = idx + 1
                     s, t = self.tokenize(ls)[:self.max_len], self.tokenize(lt)[:self.max_len - 1]
                     if s and t:
                         n += 1
                         yield s, t
-            if n == 0:
+            if n == 0 and skip == 0:
                 raise ValueError(f"corpus {self.src_path} / {self.tgt_path} has no usable pair")
             self.epoch += 1
+            self.line = 0
 
     def take(self, n: int) -> list[tuple[list[int], list[int]]]:
         return [next(self._it) for _ in range(n)]
@@ -268,3 +282,16 @@ class DataPipeline:
 
     def batch_for(self, task: TaskSpec) -> Batch:
         return self.batchers[task.id].next_batch()
+
+    def state(self) -> dict:
+        """Per task: reservoir draws and the corpus position (checkpointed
+        with the trainer, so a resumed run continues the same data)."""
+        return {tid: {"draws": b.draws, **b.stream.state()} for tid, b in self.batchers.items()}
+
+    def load_state(self, state: dict) -> None:
+        if set(state) != set(self.batchers):
+            raise ValueError("pipeline state is for a different task set")
+        for tid, st in state.items():
+            b = self.batchers[tid]
+            b.draws = int(st["draws"])
+            b.stream.load_state(st)

@@ -719,8 +719,11 @@ class Engine:
                                               st.step, n, (j, g, b, e)))
             elif self.rank == members[0]:
                 written.append(C.write_module(root, k, host, st.step, n))
+        # the rank's json goes last: it is the manifest of the files above
+        extra = dict(extra or {})
         C.write_rank_state(root, self.rank, {"mux_rng": C.rng_to_json(self.mux.rng),
-                                             **(extra or {})})
+                                             "files": [os.path.relpath(f, root) for f in written],
+                                             **extra})
         return written
 
     def load_checkpoint(self, root: str) -> dict:
@@ -729,6 +732,9 @@ class Engine:
         this rank's extra host state."""
         from . import checkpoint as C
         self.sync_updates()
+        state = C.read_rank_state(root, self.rank)
+        C.check_manifest(root, [f for k in self.states for f in C.module_files(root, k)],
+                         state.get("step_idx"))
         for k, st in self.states.items():
             arrays, step = C.read_module(root, k, st.master.numel())
             for f in C.FIELDS:
@@ -737,7 +743,7 @@ class Engine:
             ops.cast_bf16(st.master, st.weights)
             ops.memset(st.grad, 0)
             self._dirty.discard(k)
-        state = C.read_rank_state(root, self.rank)
+        state.pop("files", None)
         C.rng_from_json(self.mux.rng, state.pop("mux_rng"))
         torch.cuda.synchronize(self.device)
         return state
@@ -774,6 +780,10 @@ class Trainer:
         self.device = self.engine.device
         self._pinned = [torch.empty(pinned_elems, dtype=torch.int32, pin_memory=True)
                         for _ in range(4)]
+        # per pinned buffer: event recorded after its H2D copy was queued; the
+        # host waits on it before writing the buffer again (the copy is
+        # asynchronous, and a step may stage more micro-batches than buffers)
+        self._pin_events: list = [None] * len(self._pinned)
         self._loss_host = torch.empty(1, dtype=torch.float32, pin_memory=True)
         self._pin_next = 0  # rotating pinned staging buffer (reused >= 2 steps later)
         self.step_idx = 0
@@ -783,9 +793,14 @@ class Trainer:
     def stage(self, batches) -> list:
         out = []
         for b in batches:
-            pin = self._pinned[self._pin_next % len(self._pinned)]
+            slot = self._pin_next % len(self._pinned)
             self._pin_next += 1
-            out.append(DeviceBatch(b, self.device, pinned=pin))
+            if self._pin_events[slot] is not None:
+                self._pin_events[slot].synchronize()  # its previous H2D copy has read it
+            out.append(DeviceBatch(b, self.device, pinned=self._pinned[slot]))
+            ev = torch.cuda.Event()
+            ev.record()
+            self._pin_events[slot] = ev
         self.h2d_bytes = sum(d.h2d_bytes for d in out)
         return out
 
@@ -827,12 +842,21 @@ class Trainer:
         torch.cuda.current_stream().synchronize()  # also retires the pinned staging
         return float(self._loss_host[0])
 
-    def save_checkpoint(self, root: str) -> list[str]:
-        """Every rank calls this after the same step (f4)."""
-        return self.engine.save_checkpoint(root, {"step_idx": self.step_idx})
+    def save_checkpoint(self, root: str, pipeline=None) -> list[str]:
+        """Every rank calls this after the same step (f4); ``pipeline`` (a
+        ``datapath.DataPipeline``) adds its corpus positions and draws."""
+        extra = {"step_idx": self.step_idx}
+        if pipeline is not None:
+            extra["pipeline"] = pipeline.state()
+        return self.engine.save_checkpoint(root, extra)
 
-    def load_checkpoint(self, root: str) -> None:
-        self.step_idx = int(self.engine.load_checkpoint(root)["step_idx"])
+    def load_checkpoint(self, root: str, pipeline=None) -> None:
+        state = self.engine.load_checkpoint(root)
+        self.step_idx = int(state["step_idx"])
+        if pipeline is not None:
+            if "pipeline" not in state:
+                raise ValueError("checkpoint holds no data-pipeline state")
+            pipeline.load_state(state["pipeline"])
 
     def close(self) -> None:
         self.engine.close()

@@ -1,6 +1,7 @@
 """Per-module checkpoint files (f4) on the CPU: whole-module and sharded
 layouts round-trip bit-exactly, shards written by different members
 assemble into the module, and broken checkpoints fail loudly."""
+import os
 import random
 
 import numpy as np
@@ -63,3 +64,38 @@ def test_rank_state_and_rng(tmp_path):
     other = random.Random(0)
     C.rng_from_json(other, st["mux_rng"])
     assert [other.random() for _ in range(4)] == want and st["step_idx"] == 5
+
+
+def test_layout_switch_drops_the_other_layout(tmp_path):
+    """Saving a module whole after a sharded save (exchange switched from
+    peer to nccl) removes its shards, and vice versa: a reused directory never
+    resolves a module from a stale layout."""
+    root, n, g = str(tmp_path), 1000, 4
+    old = _state(n, 5)
+    for j in range(g):
+        b, e = shard_begin(n, g, j), shard_begin(n, g, j + 1)
+        C.write_module(root, KEY, {f: v[b:e] for f, v in old.items()}, 3, n, (j, g, b, e))
+    new = _state(n, 6)
+    C.write_module(root, KEY, new, 4, n)
+    assert C.module_files(root, KEY) == [C.module_path(root, KEY)]
+    got, step = C.read_module(root, KEY, n)
+    assert step == 4 and np.array_equal(got["master"], new["master"])
+    b, e = shard_begin(n, g, 0), shard_begin(n, g, 1)
+    C.write_module(root, KEY, {f: v[b:e] for f, v in old.items()}, 5, n, (0, g, b, e))
+    assert not (tmp_path / "modules" / f"{KEY}.npz").exists()
+
+
+def test_manifest_rejects_interrupted_save(tmp_path):
+    """Each rank's json, written last, lists its module files with the step:
+    files of a later, interrupted save (no updated manifest) or files no
+    manifest lists are rejected."""
+    root, n = str(tmp_path), 64
+    f1 = C.write_module(root, KEY, _state(n, 1), 2, n)
+    C.write_rank_state(root, 0, {"step_idx": 2, "files": [os.path.relpath(f1, root)]})
+    C.check_manifest(root, C.module_files(root, KEY), 2)
+    with pytest.raises(ValueError):
+        C.check_manifest(root, C.module_files(root, KEY), 3)  # resuming another step
+    other = ModuleKey(Side.DECODER, 0, "x")
+    C.write_module(root, other, _state(n, 2), 3, n)  # written, manifest never updated
+    with pytest.raises(ValueError):
+        C.check_manifest(root, C.module_files(root, other), 2)

@@ -153,3 +153,29 @@ def test_pack_pairs_order_is_a_permutation(tmp_path):
     b1 = pack_pairs(pairs, tokens=10_000, order=True)
     assert b0.n_src == b1.n_src and b0.n_tgt == b1.n_tgt
     assert sorted(np.diff(b0.cu_src).tolist()) == sorted(np.diff(b1.cu_src).tolist())
+
+
+def test_pipeline_state_resumes_the_same_data(tmp_path):
+    """DataPipeline.state / load_state (checkpointed by Trainer): a fresh
+    pipeline restored from the state after k batches yields the same next
+    batches as the original, across an epoch boundary."""
+    cfg = load_full_config(os.path.join(GOLD, "fullconfig_config1.yaml"))
+    for t in cfg.task_list():
+        os.makedirs(tmp_path / os.path.dirname(t.src_path), exist_ok=True)
+        sp, tp = _corpus(tmp_path, seed=len(t.id) + ord(t.id[-1]))
+        os.replace(sp, tmp_path / t.src_path)
+        os.replace(tp, tmp_path / t.tgt_path)
+    mk = lambda: DataPipeline(cfg.task_list(), tokens=96, root=str(tmp_path), seed=1, capacity=8,
+                              pool=20)
+    tasks = cfg.task_list()
+    a = mk()
+    for i in range(5):
+        a.batch_for(tasks[i % len(tasks)])
+    state = json.loads(json.dumps(a.state()))  # as stored in the rank json
+    b = mk()
+    b.load_state(state)
+    for i in range(6):  # the 20-pair pools cross the corpus' epoch boundary
+        t = tasks[(i * 2) % len(tasks)]
+        x, y = a.batch_for(t), b.batch_for(t)
+        assert all(np.array_equal(getattr(x, f), getattr(y, f)) for f in x.host_arrays())
+    assert any(st["epoch"] > 0 for st in a.state().values())
