@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 19
+#define MMB200_ABI_VERSION 20
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 /* emulated devices of one sync (mm_sync_emulated): the reference's multi-node
  * scaling harness reaches 20 devices per group (syncsim.py:461-483) */
@@ -136,16 +136,23 @@ int mm_ready_count(void* ctx, const int32_t* flags_dev, int32_t* n_dev, int n_mo
 
 typedef struct {
     void* group;     /* from mm_group_create; NULL items are skipped */
-    void* buf;       /* in-place sum */
-    int64_t n_elems;
+    void* buf;       /* in place */
+    int64_t n_elems; /* mode 0: elements; modes 1 / 2: g * shard (the padded bucket) */
     int32_t dtype;   /* 0 = fp32, 1 = bf16 */
-    int32_t root;    /* -1: sum-allreduce; >= 0: only that group rank used the module
-                        (n = 1), so its buffer already is the sum: broadcast from it */
+    int32_t root;    /* mode 0: -1 sum-allreduce; >= 0: only that group rank used the
+                        module (n = 1), so its buffer already is the sum: broadcast */
+    int32_t mode;    /* 0 = allreduce / broadcast; 1 = reduce-scatter (group rank j
+                        receives the sum of shard j at buf + j * shard); 2 = all-gather
+                        (group rank j contributes buf + j * shard) */
+    int32_t pad_;
+    int64_t shard;   /* modes 1 / 2: elements per group rank */
 } mm_reduce_item;
 
-/* Sum-allreduce (or, for n = 1, broadcast from the one ready member) of every
- * item on its group communicator, issued in array order (callers pass sorted
- * ModuleKey order) inside one ncclGroupStart/End. */
+/* Every item on its group communicator, issued in array order (callers pass
+ * sorted ModuleKey order) inside one ncclGroupStart/End: mode 0 sum-allreduce
+ * (or, for n = 1, broadcast from the one ready member); modes 1 / 2 the
+ * partitioned exchange (reduce-scatter of the gradient bucket, owner-shard
+ * K3, all-gather of the bf16 weights), SURVEY §8(e). */
 int mm_reduce_modules(void* ctx, const mm_reduce_item* items, int n, void* stream);
 
 /* ---------------------------------------------------------------------------

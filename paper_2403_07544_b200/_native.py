@@ -19,7 +19,7 @@ if os.environ.get("MM_LIB_VARIANT"):  # diagnostics: a tuning build from tools/b
                             "libmmb200.so")
 
 #: must match MMB200_ABI_VERSION in include/mmb200.h
-ABI_VERSION = 19
+ABI_VERSION = 20
 MAX_GROUP = 8
 MAX_SYNC_GROUP = 32
 
@@ -33,10 +33,49 @@ class MMError(RuntimeError):
 
 
 _lib = None
+_call_lock = None  # set while emulated ranks call the library from several threads
+
+
+class _Serialized:
+    """The library handle with every entry point behind one process-wide
+    lock (the C library keeps host-side staging state and is not re-entrant;
+    emucomm.EmulatedWorld drives several ranks from host threads)."""
+
+    def __init__(self, handle, lock):
+        self._h, self._lock = handle, lock
+
+    def __getattr__(self, name):
+        fn = getattr(self._h, name)
+        if not callable(fn):
+            return fn
+        lock = self._lock
+
+        def call(*args):
+            with lock:
+                return fn(*args)
+        return call
+
+
+class serialized_calls:
+    """Context manager: library calls from any thread take one lock."""
+
+    def __enter__(self):
+        global _call_lock
+        import threading
+        self._prev = _call_lock
+        _call_lock = _call_lock or threading.RLock()
+        return self
+
+    def __exit__(self, *exc):
+        global _call_lock
+        _call_lock = self._prev
+        return False
 
 
 def lib() -> ctypes.CDLL:
     global _lib
+    if _lib is not None and _call_lock is not None:
+        return _Serialized(_lib, _call_lock)
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise NativeLibraryError(
@@ -112,6 +151,9 @@ class ReduceItem(ctypes.Structure):
         ("n_elems", c_int64),
         ("dtype", c_int32),
         ("root", c_int32),  # -1: allreduce; >= 0: broadcast from this group rank (n = 1)
+        ("mode", c_int32),  # 0 allreduce / broadcast, 1 reduce-scatter, 2 all-gather
+        ("pad_", c_int32),
+        ("shard", c_int64),  # modes 1 / 2: elements per group rank
     ]
 
 

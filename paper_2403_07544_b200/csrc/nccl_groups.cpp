@@ -132,6 +132,31 @@ extern "C" int mm_reduce_modules(void* ctx, const mm_reduce_item* items, int n, 
             mm::set_error("reduce item root %d outside a group of %d", it.root, g->size);
             return mm::kArg;
         }
+        if (it.mode == 1 || it.mode == 2) {
+            // partitioned: in-place reduce-scatter / all-gather over the padded
+            // bucket of g * shard elements; group rank j owns [j*shard, (j+1)*shard)
+            if (it.shard <= 0 || it.n_elems != int64_t(g->size) * it.shard) {
+                ncclGroupEnd();
+                mm::set_error("partitioned item: n_elems %lld != group %d x shard %lld",
+                              (long long)it.n_elems, g->size, (long long)it.shard);
+                return mm::kArg;
+            }
+            int me = 0;
+            ncclCommUserRank(g->comm, &me);
+            const size_t esz = it.dtype == 1 ? 2 : 4;
+            char* base = static_cast<char*>(it.buf);
+            char* mine = base + size_t(me) * size_t(it.shard) * esz;
+            ncclResult_t r = it.mode == 1
+                                 ? ncclReduceScatter(base, mine, (size_t)it.shard, dt, ncclSum, g->comm,
+                                                     mm::as_stream(stream))
+                                 : ncclAllGather(mine, base, (size_t)it.shard, dt, g->comm,
+                                                 mm::as_stream(stream));
+            if (r != ncclSuccess) {
+                ncclGroupEnd();
+                return nccl_status(r, it.mode == 1 ? "ncclReduceScatter" : "ncclAllGather");
+            }
+            continue;
+        }
         // n = 1: the single ready member's buffer is the Algorithm-1 sum (the
         // others hold zeros), so a broadcast moves (g-1)/g of the allreduce's
         // 2(g-1)/g bytes and gives bit-identical results

@@ -189,7 +189,7 @@ class Engine:
     def __init__(self, tasks: Sequence[TaskSpec], topo: ClusterTopology, shape: ModelShape,
                  rank: int = 0, world: int = 1, device=None, seed: int = 0,
                  adam: AdamConfig = AdamConfig(), store=None, masters=None,
-                 exchange: Optional[str] = None):
+                 exchange: Optional[str] = None, comm=None):
         if shape.head_dim != 64:
             raise ValueError("the attention kernel is specialised for head_dim 64")
         self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
@@ -199,21 +199,32 @@ class Engine:
         self.layouts = module_layouts(self.plan, shape)
         self.index = self.plan.index()
         self.hosted = sorted(self.plan.hosted.get(rank, frozenset()))
+        # K2 transport for world > 1: "nccl" (group all-reduce / broadcast, then
+        # the replicated K3), "partitioned" (reduce-scatter, K3 on the owned
+        # shard, bf16 all-gather of the weights) or "peer" (option B: one
+        # fused peer-memory kernel per exchange, paper_2403_07544_b200/peer.py)
+        self.exchange = exchange or os.environ.get("MM_EXCHANGE", "nccl")
+        if self.exchange not in ("nccl", "peer", "partitioned"):
+            raise ValueError(f"unknown exchange {self.exchange!r}")
+        self.partitioned = world > 1 and self.exchange == "partitioned"
         self.states: dict[ModuleKey, ModuleState] = {}
         for k in self.hosted:
             m = None if masters is None else masters.get(k)
-            st = ModuleState(self.layouts[k], shape, self.device, seed, master=m)
+            cap = 0
+            g = len(self.plan.groups[k])
+            if self.partitioned and g >= 2:  # buckets padded to g equal shards
+                cap = g * self.shard_elems(self.layouts[k].numel, g)
+            st = ModuleState(self.layouts[k], shape, self.device, seed, master=m, capacity=cap)
             self.states[k] = st
         self.mux = Multiplexer(self.plan, rank, seed)
         self.adam = adam
-        self.comm = CommGroups(self.plan, rank, world, self.device.index or 0, store) \
-            if world > 1 else None
-        # K2 transport for world > 1: "nccl" (group all-reduce / broadcast, then
-        # the replicated K3) or "peer" (option B: one fused peer-memory kernel
-        # per exchange, paper_2403_07544_b200/peer.py)
-        self.exchange = exchange or os.environ.get("MM_EXCHANGE", "nccl")
-        if self.exchange not in ("nccl", "peer"):
-            raise ValueError(f"unknown exchange {self.exchange!r}")
+        # K1 / K2 communicators: NCCL (CommGroups), or an injected stand-in
+        # with the same interface (emucomm.EmuCommGroups: emulated ranks)
+        if comm is not None:
+            self.comm = comm
+        else:
+            self.comm = CommGroups(self.plan, rank, world, self.device.index or 0, store) \
+                if world > 1 else None
         self.peer = None
         if world > 1 and self.exchange == "peer":
             from .peer import PeerExchange
@@ -643,10 +654,20 @@ class Engine:
             self._pending_event = None
         self._pending_mods = set()
 
+    @staticmethod
+    def shard_elems(n_elems: int, g: int) -> int:
+        """Elements per member of the partitioned exchange: ceil(n / g) rounded
+        up to 4 (plan.shard_begin's partition; shard j = [j S, (j+1) S))."""
+        s = -(-n_elems // g)
+        return (s + 3) & ~3
+
     def exchange_and_update(self, counts: Sequence[int], used=frozenset(), only=None,
                             max_ctas: int = 0) -> None:
         """K2 for the modules of ``exchange_order`` then K3 for every hosted
         module with n >= 1; ``only`` restricts both to a subset of keys."""
+        if self.partitioned:
+            self._partitioned_exchange(counts, used, only, max_ctas)
+            return
         if self.peer is not None:
             # option B: shared modules in one fused peer-memory kernel, then
             # the local K3 for singletons
@@ -672,7 +693,38 @@ class Engine:
             self.comm.reduce(items)
         self.fused_update(counts, only, max_ctas)
 
-    def fused_update(self, counts: Sequence[int], only=None, max_ctas: int = 0) -> None:
+    def _partitioned_exchange(self, counts, used, only, max_ctas) -> None:
+        """per shared module (sorted ModuleKey order, n >= 1) a
+        reduce-scatter of the fp32 gradient bucket (member j receives the group
+        sum of shard j), K3 on the owned shard only (the sum / n rescale, Adam
+        and the bf16 cast of that shard), then an all-gather of the bf16
+        weight shards.  Wire bytes per element: (g-1)/g * (4 + 2) instead of
+        the all-reduce's 2 (g-1)/g * 4, and each member runs 1/g of the
+        optimizer.  Member j's fp32 master and moments are authoritative on
+        shard j (the checkpoint writes them per shard)."""
+        plan_items, ag_items, mods = [], [], []
+        for k, members, _root in exchange_plan(self.plan, self.rank, self._bits, only):
+            st = self.states[k]
+            g, j = len(members), members.index(self.rank)
+            s = self.shard_elems(st.layout.numel, g)
+            if k not in used and k in self._dirty:  # the zero contribution of Algorithm 1
+                ops.memset(st.grad, 0)
+            self._dirty.add(k)
+            grp = self.comm.by_set.get(tuple(members))
+            plan_items.append(_native.ReduceItem(group=grp, buf=st.grad.data_ptr(), n_elems=g * s,
+                                                 dtype=0, root=-1, mode=1, shard=s))
+            ag_items.append(_native.ReduceItem(group=grp, buf=st.weights.data_ptr(), n_elems=g * s,
+                                               dtype=1, root=-1, mode=2, shard=s))
+            mods.append((k, j * s, s))
+        self.comm.reduce(plan_items)
+        shards = {k: (off, n) for k, off, n in mods}
+        singles = {k for k in self.states if len(self.plan.groups[k]) < 2
+                   and (only is None or k in only)}
+        self.fused_update(counts, singles | set(shards), max_ctas, shards=shards)
+        self.comm.reduce(ag_items)
+
+    def fused_update(self, counts: Sequence[int], only=None, max_ctas: int = 0,
+                     shards: Optional[dict] = None) -> None:
         a = self.adam
         mods = []
         for k, st in self.states.items():
@@ -684,12 +736,14 @@ class Engine:
             st.step += 1
             bc1 = 1.0 - a.beta1 ** st.step
             bc2 = 1.0 - a.beta2 ** st.step
-            if self.zero_in_update:
+            if self.zero_in_update and not (shards and k in shards):
                 self._dirty.discard(k)  # the update leaves the bucket at zero
+            off, cnt = (shards[k] if shards and k in shards else (0, st.master.numel()))
             mods.append(_native.AdamModule(
-                grad=st.grad.data_ptr(), master=st.master.data_ptr(), exp_avg=st.exp_avg.data_ptr(),
-                exp_avg_sq=st.exp_avg_sq.data_ptr(), param_bf16=st.weights.data_ptr(),
-                n_elems=st.master.numel(), n_ready=n, ready_index=-1, step_size=a.lr / bc1,
+                grad=st.grad.data_ptr() + 4 * off, master=st.master.data_ptr() + 4 * off,
+                exp_avg=st.exp_avg.data_ptr() + 4 * off, exp_avg_sq=st.exp_avg_sq.data_ptr() + 4 * off,
+                param_bf16=st.weights.data_ptr() + 2 * off,
+                n_elems=cnt, n_ready=n, ready_index=-1, step_size=a.lr / bc1,
                 inv_sqrt_bc2=1.0 / math.sqrt(bc2)))
         if mods:
             ops.fused_update(mods, _native.AdamHyper.make(beta1=a.beta1, beta2=a.beta2, eps=a.eps,
@@ -710,9 +764,9 @@ class Engine:
         written = []
         for k, st in self.states.items():
             members = self.plan.groups[k]
-            n = st.master.numel()
-            host = {f: getattr(st, f).cpu().numpy() for f in C.FIELDS}
-            if self.peer is not None and len(members) >= 2:
+            n = st.layout.numel  # partitioned buckets carry zero padding past it
+            host = {f: getattr(st, f)[:n].cpu().numpy() for f in C.FIELDS}
+            if (self.peer is not None or self.partitioned) and len(members) >= 2:
                 j, g = members.index(self.rank), len(members)
                 b, e = shard_begin(n, g, j), shard_begin(n, g, j + 1)
                 written.append(C.write_module(root, k, {f: v[b:e] for f, v in host.items()},
@@ -736,9 +790,10 @@ class Engine:
         C.check_manifest(root, [f for k in self.states for f in C.module_files(root, k)],
                          state.get("step_idx"))
         for k, st in self.states.items():
-            arrays, step = C.read_module(root, k, st.master.numel())
+            n = st.layout.numel
+            arrays, step = C.read_module(root, k, n)
             for f in C.FIELDS:
-                getattr(st, f).copy_(torch.from_numpy(arrays[f]))
+                getattr(st, f)[:n].copy_(torch.from_numpy(arrays[f]))
             st.step = step
             ops.cast_bf16(st.master, st.weights)
             ops.memset(st.grad, 0)

@@ -152,11 +152,15 @@ class ModuleState:
     """Device buckets of one module (fp32 master / m / v / grad, bf16 weights)."""
 
     def __init__(self, layout: ModuleLayout, shape: ModelShape, device, seed: int = 0,
-                 master: Optional[np.ndarray] = None):
+                 master: Optional[np.ndarray] = None, capacity: int = 0):
+        """capacity > layout.numel pads every bucket with zeros (the
+        partitioned exchange's g * shard elements)."""
         import torch
         self.layout = layout
         self.key = layout.key
         host = init_module(layout, shape, seed) if master is None else master
+        if capacity > host.size:
+            host = np.concatenate([host, np.zeros(capacity - host.size, np.float32)])
         self.master = torch.from_numpy(host).to(device)
         self.exp_avg = torch.zeros_like(self.master)
         self.exp_avg_sq = torch.zeros_like(self.master)

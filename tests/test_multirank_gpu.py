@@ -1,0 +1,100 @@
+"""Engine.step with world > 1, on one B200: every rank's unmodified step
+(K1 ready-bitmask all-reduce, decode to counts and broadcast roots, zero
+contribution of hosted-but-unused members, K2 sum or n = 1 broadcast in
+sorted ModuleKey order, the decoder-side exchange + update on the side
+stream while the encoder backward runs, K3 with the ready count) runs in its
+own host thread against an in-process stand-in for the NCCL communicators
+(paper_2403_07544_b200/emucomm.py).
+
+Checked over three steps that cover n = 0 (config-3 structure), 1 and >= 2
+on shared modules:
+* ready counts bit-exact with the group map / multiplexer of the reference
+  (syncsim.py:313-363, through plan.ready_counts_all);
+* every rank's master, Adam moments, step count and bf16 weights
+  bit-identical to EmulatedCluster (the literal Algorithm-1 exchange,
+  syncsim.py:121-153, as one mm_sync_emulated launch + per-rank K3) applied to
+  the same per-rank gradients -- the gradients the threaded ranks posted to
+  the communicator (recorded before the reduction), since two backward runs
+  differ in the last bits (fp32 atomics).
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2403_07544_b200 import configs
+from paper_2403_07544_b200.data import make_batch
+
+pytestmark = pytest.mark.gpu
+FIELDS = ("master", "exp_avg", "exp_avg_sq", "weights")
+
+
+def _world_case(name):
+    shape = configs.SHAPE_CFG1_GPU
+    if name == "config1_w2":
+        w = configs.config1(shape)
+        return w.tasks, w.topo, shape, 2, w.data
+    w = configs.config3(4)  # config-3 structure (56 directions, groups of 4) at a small shape
+    return w.tasks, w.topo, shape, 4, configs.config1().data
+
+
+@pytest.mark.parametrize("case,exchange", [("config1_w2", "nccl"), ("config3_w4", "nccl"),
+                                           ("config1_w2", "partitioned"),
+                                           ("config3_w4", "partitioned")])
+def test_threaded_ranks_match_emulated_cluster(cuda, case, exchange):
+    """exchange="nccl": all-reduce (n = 1: broadcast) + replicated K3;
+    "partitioned": reduce-scatter, K3 on the owned shard, bf16 all-gather --
+    there masters and moments are compared on each member's own shard, the
+    bf16 weights everywhere."""
+    from paper_2403_07544_b200.cluster import EmulatedCluster
+    from paper_2403_07544_b200.emucomm import EmulatedWorld
+    from paper_2403_07544_b200.engine import DeviceBatch
+    from paper_2403_07544_b200.plan import ready_counts_all, shard_begin, task_modules
+    tasks, topo, shape, world, spec = _world_case(case)
+    emu = EmulatedWorld(tasks, topo, shape, world, device=cuda, seed=0, record=True,
+                        exchange=exchange)
+    ref = EmulatedCluster(tasks, topo, shape, world=world, device=cuda, seed=0)
+    plan = emu.plan
+    idx = plan.index()
+    by_id = {t.id: t for t in tasks}
+    seen_n = set()
+    for step in range(3):
+        rngs = [np.random.default_rng([step, r]) for r in range(world)]
+        batches = [[DeviceBatch(make_batch(rngs[r], spec, shape.vocab, sentences=12), cuda)]
+                   for r in range(world)]
+        infos = emu.step(step, batches)
+        used = {r: set(task_modules(by_id[infos[r]["tasks"][0]])) for r in range(world)}
+        counts = ready_counts_all(plan, used)
+        for r in range(world):
+            assert [infos[r]["ready"][k] for k in plan.keys] == counts
+            assert infos[r]["tasks"] == [ref.ranks[r].mux.pick(step).id]  # same multiplexer draws
+        # replay: the literal Algorithm-1 exchange on the gradients the ranks posted
+        for r, eng in enumerate(emu.engines):
+            for k, st in eng.states.items():
+                shared = len(plan.groups[k]) >= 2
+                n_el = st.layout.numel
+                if shared and counts[idx[k]] >= 1:
+                    g = emu.hub.recorded[(k, r)][-1]
+                else:
+                    g = st.grad  # singleton (K2 skipped) or n = 0 (no exchange, no update)
+                ref.ranks[r].states[k].grad.copy_(g[:n_el])
+                if shared:
+                    seen_n.add(min(counts[idx[k]], 2))
+        ref.exchange_and_update(used)
+        torch.cuda.synchronize()
+        for r in range(world):
+            for k, st in emu.engines[r].states.items():
+                want = ref.ranks[r].states[k]
+                assert st.step == want.step, (step, r, str(k))
+                members = plan.groups[k]
+                n_el = st.layout.numel
+                b, e = 0, n_el
+                if exchange == "partitioned" and len(members) >= 2:
+                    j = members.index(r)
+                    b, e = shard_begin(n_el, len(members), j), shard_begin(n_el, len(members), j + 1)
+                for f in FIELDS:
+                    lo, hi = (0, n_el) if f == "weights" else (b, e)
+                    assert torch.equal(getattr(st, f)[lo:hi], getattr(want, f)[lo:hi]), \
+                        (step, r, str(k), f)
+    # config 1: rank 1 always runs a->c, so its shared modules never see n = 0
+    assert seen_n == ({1, 2} if case == "config1_w2" else {0, 1, 2}), seen_n
+    emu.close()

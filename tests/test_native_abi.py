@@ -52,7 +52,7 @@ def test_struct_layouts():
     assert ctypes.sizeof(_native.SyncModule) == 32 * 8 + 8 + 8 + 4 + 4
     assert ctypes.sizeof(_native.AdamModule) == 5 * 8 + 8 + 4 + 4 + 4 + 4
     assert ctypes.sizeof(_native.AdamHyper) == 7 * 4 + 4 + 4  # + zero_grad
-    assert ctypes.sizeof(_native.ReduceItem) == 8 + 8 + 8 + 4 + 4
+    assert ctypes.sizeof(_native.ReduceItem) == 8 + 8 + 8 + 4 + 4 + 4 + 4 + 8
     assert ctypes.sizeof(_native.PeerShard) == 3 * 8 * 8 + 3 * 8 + 2 * 8 + 4 * 4
     assert ctypes.sizeof(_native.PeerSignal) == 8 + 32 * 8 + 32 * 4 + 4 * 4
     from paper_2403_07544_b200 import ops
