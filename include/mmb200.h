@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 20
+#define MMB200_ABI_VERSION 21
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 /* emulated devices of one sync (mm_sync_emulated): the reference's multi-node
  * scaling harness reaches 20 devices per group (syncsim.py:461-483) */
@@ -333,6 +333,16 @@ int mm_embed_fwd(const int32_t* ids, const int32_t* pos, const uint16_t* table, 
                  int64_t rows, int cols, float scale, void* stream);
 int mm_embed_bwd(const int32_t* ids, const float* dout, float* dtable, int64_t rows, int cols,
                  float scale, void* stream);
+/* Deterministic scatter-add of the same sum (no atomics, fixed order):
+ * `table` = mm_embed_segments' output for the batch's ids (device copy),
+ * scratch >= (chunks of multi-chunk ids) * cols floats. */
+int mm_embed_bwd_sorted(const int32_t* table, int64_t rows, int n_chunks, int n_multi,
+                        const float* dout, float* dtable, int cols, float scale, float* scratch,
+                        void* stream);
+/* Host: the sort / chunk tables of mm_embed_bwd_sorted for `rows` token ids
+ * (out: 7 * rows int32; see abi_host.cpp). */
+int mm_embed_segments(const int32_t* ids, int rows, int chunk_rows, int32_t* out, int* n_chunks,
+                      int* n_multi);
 
 /* K5: packed varlen multi-head attention (bf16 in/out, fp32 softmax).
  * Work is split into CTA groups of consecutive sequences: groups[2g] = first
@@ -426,6 +436,9 @@ typedef struct {
     int32_t ng_src, cap_src, ng_tgt, cap_tgt, ng_cross, cap_cross;
     const int32_t *tcg_src, *tcg_tgt, *tcg_cross; /* unpadded groups (align 1), may be NULL */
     int32_t ntc_src, ntc_tgt, ntc_cross, pad0;
+    /* mm_embed_segments tables of src / tgt_in (device), NULL: atomic scatter-add */
+    const int32_t *emb_src, *emb_tgt;
+    int32_t nch_src, nmul_src, nch_tgt, nmul_tgt;
 } mm_batch;
 
 /* dec_done (cudaEvent_t, may be NULL) is recorded on `stream` as soon as the

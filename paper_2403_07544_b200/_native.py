@@ -19,7 +19,7 @@ if os.environ.get("MM_LIB_VARIANT"):  # diagnostics: a tuning build from tools/b
                             "libmmb200.so")
 
 #: must match MMB200_ABI_VERSION in include/mmb200.h
-ABI_VERSION = 20
+ABI_VERSION = 21
 MAX_GROUP = 8
 MAX_SYNC_GROUP = 32
 
@@ -222,7 +222,9 @@ class BatchDesc(ctypes.Structure):
                                        "ng_src", "cap_src", "ng_tgt", "cap_tgt", "ng_cross",
                                        "cap_cross")] + \
                [(n, c_void_p) for n in ("tcg_src", "tcg_tgt", "tcg_cross")] + \
-               [(n, c_int32) for n in ("ntc_src", "ntc_tgt", "ntc_cross", "pad0")]
+               [(n, c_int32) for n in ("ntc_src", "ntc_tgt", "ntc_cross", "pad0")] + \
+               [(n, c_void_p) for n in ("emb_src", "emb_tgt")] + \
+               [(n, c_int32) for n in ("nch_src", "nmul_src", "nch_tgt", "nmul_tgt")]
 
 
 def _declare(h: ctypes.CDLL) -> None:
@@ -293,6 +295,9 @@ def _declare(h: ctypes.CDLL) -> None:
     sig("mm_cast_f32_bf16", c_int, c_void_p, c_void_p, c_int64, c_void_p)
     sig("mm_flush_l2", c_int, c_void_p, c_size_t, c_void_p)
     sig("mm_memset", c_int, c_void_p, c_int, c_size_t, c_void_p)
+    sig("mm_embed_bwd_sorted", c_int, c_void_p, c_int64, c_int, c_int, c_void_p, c_void_p, c_int, c_float,
+        c_void_p, c_void_p)
+    sig("mm_embed_segments", c_int, c_void_p, c_int, c_int, c_void_p, POINTER(c_int), POINTER(c_int))
     sig("mm_axpy_f32", c_int, c_void_p, c_void_p, c_float, c_int64, c_void_p)
     sig("mm_axpy_f64", c_int, c_void_p, c_void_p, c_double, c_int64, c_void_p)
     sig("mm_task_fwd_bwd", c_int, c_void_p, c_void_p, c_void_p, POINTER(c_size_t), c_void_p,

@@ -221,6 +221,50 @@ extern "C" int mm_attention_tables(const int32_t* cu_src, const int32_t* cu_tgt,
     return 0;
 }
 
+// Deterministic embedding backward (K8): the rows of a batch sorted by token
+// id (stable: ascending row within an id) and cut into chunks of at most
+// `chunk_rows` rows of one id.  out = [perm: rows][chunks: 3 per chunk]
+// [multi: 3 per id with > 1 chunk]; a chunk is (perm begin, perm end,
+// target): target >= 0 is the id itself (its only chunk adds straight into
+// the table row), target < 0 is -(scratch slot + 1) (one partial per chunk);
+// a multi entry is (id, first slot, slots): the partials are summed in chunk
+// order.  Capacity of out: 7 * rows int32.
+extern "C" int mm_embed_segments(const int32_t* ids, int rows, int chunk_rows, int32_t* out,
+                                 int* n_chunks, int* n_multi) {
+    MM_CHECK_ARG(rows >= 0 && chunk_rows >= 1 && out && n_chunks && n_multi && (rows == 0 || ids),
+                 "bad arguments");
+    std::vector<uint64_t> key(rows);
+    for (int r = 0; r < rows; ++r) {
+        MM_CHECK_ARG(ids[r] >= 0, "negative token id at row %d", r);
+        key[r] = (uint64_t(uint32_t(ids[r])) << 32) | uint32_t(r);
+    }
+    std::sort(key.begin(), key.end());
+    int32_t* perm = out;
+    for (int r = 0; r < rows; ++r) perm[r] = int32_t(key[r] & 0xffffffffu);
+    int32_t* chunks = out + rows;
+    std::vector<int32_t> multi;
+    int nc = 0, slots = 0;
+    for (int a = 0; a < rows;) {
+        const int32_t id = int32_t(key[a] >> 32);
+        int b = a;
+        while (b < rows && int32_t(key[b] >> 32) == id) ++b;
+        const int pieces = (b - a + chunk_rows - 1) / chunk_rows;
+        if (pieces > 1) multi.insert(multi.end(), {id, slots, pieces});
+        for (int c = 0; c < pieces; ++c) {
+            chunks[3 * nc] = a + c * chunk_rows;
+            chunks[3 * nc + 1] = std::min(b, a + (c + 1) * chunk_rows);
+            chunks[3 * nc + 2] = pieces > 1 ? -(slots + c + 1) : id;
+            ++nc;
+        }
+        if (pieces > 1) slots += pieces;
+        a = b;
+    }
+    std::copy(multi.begin(), multi.end(), chunks + 3 * nc);
+    *n_chunks = nc;
+    *n_multi = int(multi.size() / 3);
+    return 0;
+}
+
 // Order of a batch's sentence pairs for the attention work groups: first-fit
 // decreasing 2-D bin packing (capacity `cap` rows on both the source and the
 // target side), bins emitted in creation order, pairs longer than `cap` on

@@ -278,6 +278,137 @@ __global__ void __launch_bounds__(256, MINB) ln_bwd_row_kernel(const float* __re
 }
 
 // ----------------------------------------------------------------------------
+// LayerNorm v2 (default): one row per warp, 4-warp CTAs, every row of the
+// problem in flight in one wave (4096 rows = 1024 CTAs, ~7 per SM: balanced,
+// where 256 CTAs of 8 warps left half the SMs with one CTA and half with two).
+// Forward: 2 KB (d = 512) of fp32 row per warp loaded at once, two-pass mean /
+// variance from registers, bf16 out.
+template <int COLS>
+__global__ void __launch_bounds__(128) ln_fwd_v2_kernel(const float* __restrict__ x,
+                                                        const float* __restrict__ gamma,
+                                                        const float* __restrict__ beta,
+                                                        uint16_t* __restrict__ y, float* mean_out,
+                                                        float* rstd_out, int64_t rows, float eps) {
+    constexpr int V = COLS / 128;
+    const int lane = threadIdx.x & 31;
+    const int64_t row = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
+    pdl_wait_release();
+    if (row >= rows) return;
+    const float4* xr = reinterpret_cast<const float4*>(x + row * COLS);
+    float4 v[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) v[i] = __ldcs(xr + lane + 32 * i);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    const float mu = warp_sum(s) * (1.f / COLS);
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        const float a = v[i].x - mu, b = v[i].y - mu, c = v[i].z - mu, d = v[i].w - mu;
+        q += (a * a + b * b) + (c * c + d * d);
+    }
+    const float rs = rsqrtf(warp_sum(q) * (1.f / COLS) + eps);
+    uint2* yr = reinterpret_cast<uint2*>(y + row * COLS);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        const int c = 4 * lane + 128 * i;
+        const float4 g = __ldg(reinterpret_cast<const float4*>(gamma + c));
+        const float4 bb = __ldg(reinterpret_cast<const float4*>(beta + c));
+        uint2 o;
+        o.x = pack2((v[i].x - mu) * rs * g.x + bb.x, (v[i].y - mu) * rs * g.y + bb.y);
+        o.y = pack2((v[i].z - mu) * rs * g.z + bb.z, (v[i].w - mu) * rs * g.w + bb.w);
+        yr[lane + 32 * i] = o;
+    }
+    if (lane == 0) {
+        mean_out[row] = mu;
+        rstd_out[row] = rs;
+    }
+}
+
+// Backward v2: one row per warp, 8-warp CTAs at up to four per SM (<= 64
+// registers: the whole config-3 problem, 4096 rows, resident in one wave).
+// dy and x are loaded at once; the residual-gradient row dx is only PREFETCHED
+// into L2 then (no registers held across the reductions) and read after them.
+// dgamma / dbeta: per-CTA column partials in shared memory (a lane owns its
+// columns, no conflicts), one float4 atomic per 4 columns per CTA.
+template <int COLS>
+__global__ void __launch_bounds__(256, 4) ln_bwd_v2_kernel(const float* __restrict__ dy,
+                                                           const float* __restrict__ x,
+                                                           const float* __restrict__ gamma,
+                                                           const float* __restrict__ mean,
+                                                           const float* __restrict__ rstd, float* dx,
+                                                           uint16_t* dx_bf16, float* dgamma,
+                                                           float* dbeta, int64_t rows) {
+    constexpr int V = COLS / 128;
+    __shared__ float4 red[2][8][COLS / 4];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t row = int64_t(blockIdx.x) * 8 + warp;
+    pdl_wait_release();
+    const bool live = row < rows;
+    float4 d[V], xv[V];
+    if (live) {
+        const float4* dyr = reinterpret_cast<const float4*>(dy + row * COLS);
+        const float4* xr = reinterpret_cast<const float4*>(x + row * COLS);
+        const char* dxr = reinterpret_cast<const char*>(dx + row * COLS);
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            d[i] = __ldcs(dyr + lane + 32 * i);
+            xv[i] = __ldcs(xr + lane + 32 * i);
+        }
+        if (lane < COLS * 4 / 128)  // one 128-byte line per lane
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(dxr + lane * 128));
+    } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) d[i] = xv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float mu = live ? mean[row] : 0.f, rs = live ? rstd[row] : 0.f;
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        float4& xh = xv[i];
+        xh = make_float4((xh.x - mu) * rs, (xh.y - mu) * rs, (xh.z - mu) * rs, (xh.w - mu) * rs);
+        red[0][warp][lane + 32 * i] = make_float4(d[i].x * xh.x, d[i].y * xh.y, d[i].z * xh.z, d[i].w * xh.w);
+        red[1][warp][lane + 32 * i] = d[i];
+        const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma + 4 * lane + 128 * i));
+        d[i] = make_float4(d[i].x * gm.x, d[i].y * gm.y, d[i].z * gm.z, d[i].w * gm.w);  // dxhat
+        s1 += d[i].x + d[i].y + d[i].z + d[i].w;
+        s2 += d[i].x * xh.x + d[i].y * xh.y + d[i].z * xh.z + d[i].w * xh.w;
+    }
+    const float m1 = warp_sum(s1) * (1.f / COLS), m2 = warp_sum(s2) * (1.f / COLS);
+    if (live) {
+        float4* dxr = reinterpret_cast<float4*>(dx + row * COLS);
+        uint2* dbr = reinterpret_cast<uint2*>(dx_bf16 + row * COLS);
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            float4 w = dxr[lane + 32 * i];
+            w.x += rs * (d[i].x - m1 - xv[i].x * m2);
+            w.y += rs * (d[i].y - m1 - xv[i].y * m2);
+            w.z += rs * (d[i].z - m1 - xv[i].z * m2);
+            w.w += rs * (d[i].w - m1 - xv[i].w * m2);
+            dxr[lane + 32 * i] = w;
+            if (dx_bf16) {
+                uint2 b;
+                b.x = pack2(w.x, w.y);
+                b.y = pack2(w.z, w.w);
+                dbr[lane + 32 * i] = b;
+            }
+        }
+    }
+    __syncthreads();
+    for (int c4 = threadIdx.x; c4 < 2 * (COLS / 4); c4 += 256) {
+        const int which = c4 / (COLS / 4), c = c4 - which * (COLS / 4);
+        float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            const float4 v = red[which][w][c];
+            sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+        }
+        atomicAdd(reinterpret_cast<float4*>(which ? dbeta : dgamma) + c, sum);
+    }
+}
+
+// ----------------------------------------------------------------------------
 // Embedding: out[r,:] = table[id[r],:] * scale + PE(pos[r]) (sinusoidal,
 // sin on even / cos on odd columns, OpenNMT layout).  One warp per row.
 __global__ void __launch_bounds__(256) embed_fwd_kernel(const int32_t* __restrict__ ids,
@@ -326,6 +457,79 @@ __global__ void __launch_bounds__(256) embed_bwd_kernel(const int32_t* __restric
         float4 g = d[v];
         g.x *= scale; g.y *= scale; g.z *= scale; g.w *= scale;
         atomicAdd(t + v, g);
+    }
+}
+
+// Deterministic scatter-add (mm_embed_segments tables): a warp per chunk sums
+// its rows (ascending row order within the token id) and adds the sum into the
+// table row when the id has one chunk, else writes the chunk's partial; a warp
+// per multi-chunk id then adds the partials in chunk order.  Every table row
+// has one writer per launch and a fixed summation order: no atomics, bitwise
+// reproducible, and a Zipf-hot id costs one partial per 32 rows instead of
+// hundreds of serialised atomics on one row.
+constexpr int kEmbMaxV = 8;  // float4 per lane: cols <= 1024
+
+__global__ void __launch_bounds__(256) embed_bwd_chunk_kernel(const int32_t* __restrict__ perm,
+                                                              const int32_t* __restrict__ chunks,
+                                                              int n_chunks, const float* __restrict__ dout,
+                                                              float* dtable, float* scratch, int cols,
+                                                              float scale) {
+    pdl_wait_release();
+    const int lane = threadIdx.x & 31;
+    const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (c >= n_chunks) return;
+    const int b = chunks[3 * c], e = chunks[3 * c + 1], tgt = chunks[3 * c + 2];
+    const int nv = cols / 4;
+    float4 acc[kEmbMaxV];
+#pragma unroll
+    for (int i = 0; i < kEmbMaxV; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int p = b; p < e; ++p) {
+        const float4* d = reinterpret_cast<const float4*>(dout + int64_t(perm[p]) * cols);
+#pragma unroll
+        for (int i = 0; i < kEmbMaxV; ++i) {
+            const int v = lane + 32 * i;
+            if (v < nv) {
+                const float4 g = d[v];
+                acc[i].x = fmaf(g.x, scale, acc[i].x); acc[i].y = fmaf(g.y, scale, acc[i].y);
+                acc[i].z = fmaf(g.z, scale, acc[i].z); acc[i].w = fmaf(g.w, scale, acc[i].w);
+            }
+        }
+    }
+    float4* dst = tgt >= 0 ? reinterpret_cast<float4*>(dtable + int64_t(tgt) * cols)
+                           : reinterpret_cast<float4*>(scratch + int64_t(-tgt - 1) * cols);
+#pragma unroll
+    for (int i = 0; i < kEmbMaxV; ++i) {
+        const int v = lane + 32 * i;
+        if (v >= nv) continue;
+        if (tgt >= 0) {
+            float4 t = dst[v];
+            t.x += acc[i].x; t.y += acc[i].y; t.z += acc[i].z; t.w += acc[i].w;
+            dst[v] = t;
+        } else {
+            dst[v] = acc[i];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) embed_bwd_multi_kernel(const int32_t* __restrict__ multi, int n_multi,
+                                                              const float* __restrict__ scratch,
+                                                              float* dtable, int cols) {
+    pdl_wait_release();
+    const int lane = threadIdx.x & 31;
+    const int m = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (m >= n_multi) return;
+    const int id = multi[3 * m], s0 = multi[3 * m + 1], ns = multi[3 * m + 2];
+    const int nv = cols / 4;
+    float4* dst = reinterpret_cast<float4*>(dtable + int64_t(id) * cols);
+    for (int v = lane; v < nv; v += 32) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = 0; k < ns; ++k) {
+            const float4 x = reinterpret_cast<const float4*>(scratch + int64_t(s0 + k) * cols)[v];
+            a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+        }
+        float4 t = dst[v];
+        t.x += a.x; t.y += a.y; t.z += a.z; t.w += a.w;
+        dst[v] = t;
     }
 }
 
@@ -614,6 +818,16 @@ extern "C" int mm_layernorm_fwd(const float* x, const float* gamma, const float*
     if (rows == 0) return 0;
     const unsigned grid = static_cast<unsigned>((rows + 8 * kLnRows - 1) / (8 * kLnRows));
     auto s = mm::as_stream(stream);
+    static const bool v1 = std::getenv("MM_LN_V1") != nullptr;  // A/B: the previous kernels
+    if (!v1 && (cols == 512 || cols == 1024)) {
+        const unsigned g2 = static_cast<unsigned>((rows + 3) / 4);
+        if (cols == 512)
+            MM_CUDA_TRY(mm::launch_pdl(ln_fwd_v2_kernel<512>, dim3(g2), dim3(128), 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
+        else
+            MM_CUDA_TRY(mm::launch_pdl(ln_fwd_v2_kernel<1024>, dim3(g2), dim3(128), 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
+        MM_LAUNCH_CHECK("ln_fwd_v2_kernel");
+        return 0;
+    }
     if (cols == 512)
         MM_CUDA_TRY(mm::launch_pdl(ln_fwd_kernel<512>, dim3(grid), dim3(256), 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
     else if (cols == 1024)
@@ -637,6 +851,13 @@ extern "C" int mm_layernorm_bwd(const float* dy, const float* x, const float* ga
     if (rows == 0) return 0;
     auto s = mm::as_stream(stream);
     static const bool old_kernel = std::getenv("MM_LN_BWD_BATCHED") != nullptr;  // A/B diagnostics
+    static const bool v1 = std::getenv("MM_LN_V1") != nullptr;
+    if (!v1 && !old_kernel && cols == 512) {  // (d = 1024 spills at 64 registers: batched kernel)
+        const unsigned g2 = static_cast<unsigned>((rows + 7) / 8);
+        MM_CUDA_TRY(mm::launch_pdl(ln_bwd_v2_kernel<512>, dim3(g2), dim3(256), 0, s, dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows));
+        MM_LAUNCH_CHECK("ln_bwd_v2_kernel");
+        return 0;
+    }
     if (cols == 512 && !old_kernel) {
         // one row per warp, 2 CTAs/SM (3 CTAs/SM = 85 registers spills: 9.3 us;
         // this 5.9 us vs 6.7 us for the batched kernel, graph back to back)
@@ -690,6 +911,27 @@ extern "C" int mm_embed_bwd(const int32_t* ids, const float* dout, float* dtable
     if (rows == 0) return 0;
     MM_CUDA_TRY(mm::launch_pdl(embed_bwd_kernel, dim3(static_cast<unsigned>((rows + 7) / 8)), dim3(256), 0, mm::as_stream(stream), ids, dout, dtable, rows, cols, scale));
     MM_LAUNCH_CHECK("embed_bwd_kernel");
+    return 0;
+}
+
+extern "C" int mm_embed_bwd_sorted(const int32_t* table, int64_t rows, int n_chunks, int n_multi,
+                                   const float* dout, float* dtable, int cols, float scale,
+                                   float* scratch, void* stream) {
+    MM_CHECK_ARG(table && dout && dtable && (n_multi == 0 || scratch), "NULL argument");
+    MM_CHECK_ARG(cols % 4 == 0 && cols <= 4 * 32 * kEmbMaxV, "cols %d: multiple of 4, <= 1024", cols);
+    if (rows == 0 || n_chunks == 0) return 0;
+    const int32_t* perm = table;
+    const int32_t* chunks = table + rows;
+    const int32_t* multi = chunks + int64_t(3) * n_chunks;
+    auto s = mm::as_stream(stream);
+    MM_CUDA_TRY(mm::launch_pdl(embed_bwd_chunk_kernel, dim3((n_chunks + 7) / 8), dim3(256), 0, s, perm, chunks,
+                               n_chunks, dout, dtable, scratch, cols, scale));
+    MM_LAUNCH_CHECK("embed_bwd_chunk_kernel");
+    if (n_multi > 0) {
+        MM_CUDA_TRY(mm::launch_pdl(embed_bwd_multi_kernel, dim3((n_multi + 7) / 8), dim3(256), 0, s, multi,
+                                   n_multi, (const float*)scratch, dtable, cols));
+        MM_LAUNCH_CHECK("embed_bwd_multi_kernel");
+    }
     return 0;
 }
 

@@ -390,6 +390,20 @@ struct Driver {
         return 0;
     }
 
+    // K8 scatter-add: deterministic sorted kernels when the batch carries
+    // their tables (mm_embed_segments), else the atomic kernel
+    int embed_bwd(const int32_t* table, int nch, int nmul, const int32_t* ids, const float* dout,
+                  float* dtable, int64_t rows) {
+        const float scale = std::sqrt(float(d));
+        if (!table) {
+            TIMED(5, mm_embed_bwd(ids, dout, dtable, rows, d, scale, s));
+            return 0;
+        }
+        float* scratch = nmul ? ar.get<float>(size_t(nch) * d) : nullptr;
+        TIMED(5, mm_embed_bwd_sorted(table, rows, nch, nmul, dout, dtable, d, scale, scratch, s));
+        return 0;
+    }
+
     cudaEvent_t dec_done = nullptr;
 
     int run(float* loss_sum) {
@@ -474,7 +488,8 @@ struct Driver {
             if (int e = self_bwd(dec_l[l], dy, dy_bf, Tt, b.cu_tgt, b.max_tgt, true, b.groups_tgt, b.ng_tgt, b.cap_tgt,
                                  b.tcg_tgt, b.ntc_tgt)) return e;
         }
-        TIMED(5, mm_embed_bwd(b.tgt_in, dy, t.dec_emb.grad + t.dec_emb.emb, Tt, d, scale, s));
+        if (int e = embed_bwd(b.emb_tgt, b.nch_tgt, b.nmul_tgt, b.tgt_in, dy,
+                              t.dec_emb.grad + t.dec_emb.emb, Tt)) return e;
         if (int e = flush_wgrads()) return e;  // decoder side + generator
         if (dec_done && !sizing) MM_CUDA_TRY(cudaEventRecord(dec_done, s));
         // ---- encoder backward
@@ -488,7 +503,8 @@ struct Driver {
             if (int e = self_bwd(enc_l[l], dx, dx_bf, Ts, b.cu_src, b.max_src, false, b.groups_src, b.ng_src, b.cap_src,
                                  b.tcg_src, b.ntc_src)) return e;
         }
-        TIMED(5, mm_embed_bwd(b.src, dx, t.enc_emb.grad + t.enc_emb.emb, Ts, d, scale, s));
+        if (int e = embed_bwd(b.emb_src, b.nch_src, b.nmul_src, b.src, dx,
+                              t.enc_emb.grad + t.enc_emb.emb, Ts)) return e;
         if (int e = flush_wgrads()) return e;  // encoder side
         return 0;
     }

@@ -85,7 +85,12 @@ class DeviceBatch:
         for t, name in enumerate(("attn_src", "attn_tgt", "attn_cross", "tc_src", "tc_tgt", "tc_cross")):
             arrs[name] = tab[2 * n * t:2 * n * t + 2 * int(ng[t])]
             groups[name] = (int(ng[t]), int(foot[t])) if t < 3 else (int(ng[t]),)
-        names = list(self.FIELDS) + list(groups)
+        # deterministic embedding backward: rows sorted by token id, chunked
+        self.emb_counts = {}
+        for name, ids in (("emb_src", b.src), ("emb_tgt", b.tgt_in)):
+            arrs[name], nc, nm = ops.embed_segments(ids)
+            self.emb_counts[name] = (nc, nm)
+        names = list(self.FIELDS) + list(groups) + ["emb_src", "emb_tgt"]
         sizes = [len(arrs[f]) for f in names]
         total = sum(sizes)
         host = pinned if pinned is not None and pinned.numel() >= total else \
@@ -121,7 +126,10 @@ class DeviceBatch:
             groups_src=gs[0].data_ptr(), groups_tgt=gt[0].data_ptr(), groups_cross=gc[0].data_ptr(),
             n_seq=self.n_seq, n_src=self.n_src, n_tgt=self.n_tgt, max_src=self.max_src,
             max_tgt=self.max_tgt, ng_src=gs[1], cap_src=gs[2], ng_tgt=gt[1], cap_tgt=gt[2],
-            ng_cross=gc[1], cap_cross=gc[2])
+            ng_cross=gc[1], cap_cross=gc[2],
+            emb_src=self.emb_src.data_ptr(), emb_tgt=self.emb_tgt.data_ptr(),
+            nch_src=self.emb_counts["emb_src"][0], nmul_src=self.emb_counts["emb_src"][1],
+            nch_tgt=self.emb_counts["emb_tgt"][0], nmul_tgt=self.emb_counts["emb_tgt"][1])
 
 
 class CommGroups:
@@ -550,7 +558,7 @@ class Engine:
             self._self_bwd(st, p, sv[0], dy, dy_bf, db.cu_tgt, db.n_seq, db.max_tgt, True)
         self._tr("dy_bottom", dy)
         self._tr("dmem", dmem)
-        ops.embed_bwd(db.tgt_in, dy, emb_d.g("emb"), self.scale)
+        self._embed_bwd(db, "emb_tgt", db.tgt_in, dy, emb_d.g("emb"))
         # ---- encoder backward
         dx = self._zeros(Ts, d)
         dx_bf = torch.empty(Ts, d, device=dev, dtype=torch.bfloat16)
@@ -559,7 +567,18 @@ class Engine:
             self._ffn_bwd(st, p, sv[1], dx, dx_bf)
             self._self_bwd(st, p, sv[0], dx, dx_bf, db.cu_src, db.n_seq, db.max_src, False)
         self._tr("dx_bottom", dx)
-        ops.embed_bwd(db.src, dx, emb_e.g("emb"), self.scale)
+        self._embed_bwd(db, "emb_src", db.src, dx, emb_e.g("emb"))
+
+    def _embed_bwd(self, db, name, ids, dout, dtable) -> None:
+        """K8 scatter-add: the deterministic sorted kernels when the batch
+        carries their tables (DeviceBatch always does), else atomics."""
+        counts = getattr(db, "emb_counts", {}).get(name)
+        if counts is None:
+            ops.embed_bwd(ids, dout, dtable, self.scale)
+            return
+        nc, nm = counts
+        scratch = torch.empty(max(nc, 1), dout.shape[1], device=self.device) if nm else None
+        ops.embed_bwd_sorted(getattr(db, name), dout.shape[0], nc, nm, dout, dtable, self.scale, scratch)
 
     # ------------------------------------------------------------------ step
     def zero_grads(self, keys=None) -> None:

@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes
 import math
 
+import numpy as np
 import torch
 
 from . import _native
@@ -165,6 +166,30 @@ def embed_fwd(ids, pos, table_bf16, out, scale) -> None:
     LAUNCHES[0] += 1
     check(lib().mm_embed_fwd(ids.data_ptr(), pos.data_ptr(), table_bf16.data_ptr(), out.data_ptr(),
                              rows, cols, scale, stream_ptr()), "mm_embed_fwd")
+
+
+EMB_CHUNK_ROWS = 32  # rows per partial of the deterministic embedding backward
+
+
+def embed_segments(ids: np.ndarray) -> tuple[np.ndarray, int, int]:
+    """Host tables of the deterministic embedding backward (mm_embed_segments):
+    (int32 table, chunks, multi-chunk ids)."""
+    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    out = np.empty(7 * max(len(ids), 1), dtype=np.int32)
+    nc, nm = ctypes.c_int(), ctypes.c_int()
+    check(lib().mm_embed_segments(ids.ctypes.data, len(ids), EMB_CHUNK_ROWS, out.ctypes.data,
+                                  ctypes.byref(nc), ctypes.byref(nm)), "mm_embed_segments")
+    return out[:len(ids) + 3 * nc.value + 3 * nm.value], nc.value, nm.value
+
+
+def embed_bwd_sorted(table_dev, rows, n_chunks, n_multi, dout, dtable, scale, scratch) -> None:
+    _need(dout, torch.float32, "dout")
+    _need(dtable, torch.float32, "dtable")
+    LAUNCHES[0] += 1 + (n_multi > 0)
+    check(lib().mm_embed_bwd_sorted(table_dev.data_ptr(), rows, n_chunks, n_multi, dout.data_ptr(),
+                                    dtable.data_ptr(), dout.shape[1], scale,
+                                    scratch.data_ptr() if scratch is not None else None, stream_ptr()),
+          "mm_embed_bwd_sorted")
 
 
 def embed_bwd(ids, dout, dtable, scale) -> None:

@@ -251,6 +251,57 @@ def test_embedding(cuda):
     assert rel_err(dtable.cpu(), ref_d) < 1e-5
 
 
+@pytest.mark.parametrize("rows,d", [(4096, 512), (3000, 1024), (1, 128), (65, 64)])
+def test_embedding_backward_sorted_deterministic(cuda, rows, d):
+    """K8's sorted scatter-add (mm_embed_segments + mm_embed_bwd_sorted) on
+    Zipf(1.1) ids: bit-exact against a numpy restatement of its summation
+    order (scale 1: the kernel's fmaf(g, 1, acc) is an exact add), bitwise
+    identical over repeated launches, and accumulating into a non-zero table;
+    with scale sqrt(d) within 1e-6 of the fp64 index_add."""
+    from paper_2403_07544_b200 import ops
+    from paper_2403_07544_b200.data import ZipfIds
+    rng = np.random.default_rng(rows)
+    vocab = 32000
+    ids = ZipfIds(vocab, 1.1).draw(rng, rows)
+    tab, nc, nm = ops.embed_segments(ids)
+    tab_d = torch.from_numpy(tab).to(cuda)
+    dout = torch.from_numpy(rng.standard_normal((rows, d), dtype=np.float32)).to(cuda)
+    base = torch.from_numpy(rng.standard_normal((vocab, d), dtype=np.float32)).to(cuda)
+    scratch = torch.empty(max(nc, 1), d, device=cuda)
+    outs = []
+    for _ in range(3):
+        t = base.clone()
+        ops.embed_bwd_sorted(tab_d, rows, nc, nm, dout, t, 1.0, scratch)
+        outs.append(t)
+    torch.cuda.synchronize()
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+    # numpy restatement: chunk partials in ascending row order, partials in chunk order
+    g = dout.cpu().numpy()
+    want = base.cpu().numpy().copy()
+    perm = tab[:rows]
+    chunks = tab[rows:rows + 3 * nc].reshape(-1, 3)
+    partial = {}
+    for b, e, tgt in chunks:
+        acc = np.zeros(d, np.float32)
+        for p in perm[b:e]:
+            acc = acc + g[p]
+        if tgt >= 0:
+            want[tgt] = want[tgt] + acc
+        else:
+            partial[-tgt - 1] = acc
+    for idv, s0, ns in tab[rows + 3 * nc:].reshape(-1, 3):
+        acc = np.zeros(d, np.float32)
+        for k in range(ns):
+            acc = acc + partial[s0 + k]
+        want[idv] = want[idv] + acc
+    assert np.array_equal(outs[0].cpu().numpy(), want)
+    t = torch.zeros(vocab, d, device=cuda)
+    ops.embed_bwd_sorted(tab_d, rows, nc, nm, dout, t, math.sqrt(d), scratch)
+    ref = np.zeros((vocab, d))
+    np.add.at(ref, ids.astype(np.int64), g.astype(np.float64) * math.sqrt(d))
+    assert np.abs(t.cpu().numpy() - ref).max() <= 1e-6 * np.abs(ref).max()
+
+
 @pytest.mark.parametrize("rows,vocab", [(777, 32000), (300, 1000), (150, 40000), (2, 8)])
 def test_cross_entropy(cuda, rows, vocab):
     """Both kernels: the streamed one-CTA-per-SM kernel (vocab <= 32768) and

@@ -195,3 +195,42 @@ def test_attention_tables_one_call_matches_six():
                                            (cs, cs, 1), (ct, ct, 1), (ct, cs, 1)]):
             g, f = native_attention_groups(q, k, 128, align)
             assert np.array_equal(tab[2 * n * t:2 * n * t + 2 * ng[t]], g) and foot[t] == f, (trial, t)
+
+
+def _segments_ref(ids, chunk):
+    """numpy restatement of mm_embed_segments (stable sort by id, chunks of
+    <= chunk rows, partial slots numbered in chunk order)."""
+    perm = np.argsort(ids, kind="stable")
+    chunks, multi, slots = [], [], 0
+    i = 0
+    while i < len(perm):
+        j = i
+        while j < len(perm) and ids[perm[j]] == ids[perm[i]]:
+            j += 1
+        pieces = -(-(j - i) // chunk)
+        if pieces > 1:
+            multi.append((int(ids[perm[i]]), slots, pieces))
+        for c in range(pieces):
+            chunks.append((i + c * chunk, min(j, i + (c + 1) * chunk),
+                           -(slots + c + 1) if pieces > 1 else int(ids[perm[i]])))
+        slots += pieces if pieces > 1 else 0
+        i = j
+    return perm, chunks, multi
+
+
+@pytest.mark.parametrize("rows,vocab", [(0, 10), (1, 10), (4096, 32000), (777, 50)])
+def test_embed_segments_match_restatement(rows, vocab):
+    """K8's deterministic scatter-add tables (host C++) vs numpy: Zipf-hot
+    ids (one id over many chunks), all ids distinct, a single row, empty."""
+    from paper_2403_07544_b200 import ops
+    from paper_2403_07544_b200.data import ZipfIds
+    rng = np.random.default_rng(rows)
+    ids = ZipfIds(vocab, 1.1).draw(rng, rows) if rows else np.zeros(0, np.int32)
+    tab, nc, nm = ops.embed_segments(ids)
+    perm, chunks, multi = _segments_ref(ids, ops.EMB_CHUNK_ROWS)
+    assert np.array_equal(tab[:rows], perm)
+    assert nc == len(chunks) and nm == len(multi)
+    assert [tuple(x) for x in tab[rows:rows + 3 * nc].reshape(-1, 3)] == chunks
+    assert [tuple(x) for x in tab[rows + 3 * nc:].reshape(-1, 3)] == multi
+    if rows == 4096:
+        assert nm >= 1 and max(m[2] for m in multi) >= 10  # the hottest id spans many chunks
