@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "mm_common.h"
@@ -1032,6 +1033,428 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_tc_kernel(const __gri
     }
 }
 
+// ---------------------------------------------------------------------------
+// Groups with a sequence longer than 128 rows (config 5's length tail, up to
+// 256 per side): the unpadded table gives such a sequence a group of its own.
+//
+// Forward: one CTA per (head, group, 128-query block); S = Q K^T over all of
+// the group's keys in ONE MMA chain (N = 256 when nk > 128: K as two stacked
+// 128-row SW128 boxes is one 256-row K-major operand), sixteen warps (four
+// per TMEM lane quarter, 64 keys each) form P = softmax(S) as bf16 hi + lo in
+// four 64-key regions, O = P V (K = 256) into TMEM, then O and lse out.
+// 208 KB of shared memory, 512 TMEM columns (S 256 + O 64): one CTA per SM.
+constexpr int kLongW = 16;
+constexpr int kLongThreads = (kEpiW0 + kLongW) * 32;
+constexpr int kLongFwdSmem = kTile /*Q*/ + 2 * kTile /*K*/ + 2 * kTile /*V*/ + 8 * kTile /*P hi+lo*/ + 4096 + 1024;
+
+__device__ __forceinline__ bool long_group(int nq, int nk) { return nq > kRows || nk > kRows; }
+
+__global__ void __launch_bounds__(kLongThreads, 1) attn_fwd_long_kernel(const __grid_constant__ FwdParams p) {
+    extern __shared__ uint8_t smraw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    uint8_t* Qs = sm;
+    uint8_t* Ks = Qs + kTile;        // keys 0-127, 128-255
+    uint8_t* Vs = Ks + 2 * kTile;
+    uint8_t* Ph = Vs + 2 * kTile;    // 4 regions of 64 keys
+    uint8_t* Pl = Ph + 4 * kTile;
+    float* red = reinterpret_cast<float*>(Pl + 4 * kTile);  // [4][128] row partials
+    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 4 * kRows);
+    uint64_t* tma_bar = bars;
+    uint64_t* s_bar = bars + 1;
+    uint64_t* p_bar = bars + 2;
+    uint64_t* o_bar = bars + 3;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+
+    const int h = blockIdx.x, grp = blockIdx.y, qb = blockIdx.z;
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+    const int lane = threadIdx.x & 31;
+    const int first = p.groups[2 * grp], nseq = p.groups[2 * grp + 1];
+    const int q_lo = p.cu_q[first], nq = p.cu_q[first + nseq] - q_lo;
+    const int k_lo = p.cu_k[first], nk = p.cu_k[first + nseq] - k_lo;
+    if (!long_group(nq, nk) || qb * kRows >= nq) return;  // the short kernel's group / no rows
+    const int q0 = qb * kRows;
+    const int nkb = nk > kRows ? 2 : 1;
+    if (warp == 1 && lane == 0) {
+        tc::mbar_init(tma_bar, 1);
+        tc::mbar_init(s_bar, 1);
+        tc::mbar_init(p_bar, kLongW);
+        tc::mbar_init(o_bar, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            pdl_wait();
+            tc::mbar_expect_tx(tma_bar, (1 + 2 * nkb) * kTile);
+            tc::tma_load_2d(Qs, &p.mq, tma_bar, h * 64, q_lo + q0);
+            for (int b = 0; b < nkb; ++b) {
+                tc::tma_load_2d(Ks + b * kTile, &p.mk, tma_bar, h * 64, k_lo + b * kRows);
+                tc::tma_load_2d(Vs + b * kTile, &p.mv, tma_bar, h * 64, k_lo + b * kRows);
+            }
+        }
+    } else if (warp == 1) {
+        tc::mbar_wait(tma_bar, 0);
+        tc::tc_fence_after();
+        constexpr uint32_t id_s1 = tc::idesc_bf16_f32(128, 128, 0, 0);
+        constexpr uint32_t id_s2 = tc::idesc_bf16_f32(128, 256, 0, 0);
+        const uint32_t id_s = nkb == 2 ? id_s2 : id_s1;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+            tc::mma_bf16_elect<1>(tmem, desc(Qs + kk * 32, 16), desc(Ks + kk * 32, 16), id_s, kk > 0);
+        tc::mma_commit_elect<1>(s_bar);
+        tc::mbar_wait(p_bar, 0);
+        tc::tc_fence_after();
+        constexpr uint32_t id_o = tc::idesc_bf16_f32(128, 64, 0, 1);  // P K-major, V MN-major
+        for (int part = 0; part < 2; ++part) {
+            const uint8_t* P = part ? Pl : Ph;
+            for (int kk = 0; kk < 8 * nkb; ++kk)  // K = 16 keys per step
+                tc::mma_bf16_elect<1>(tmem + 256, desc(P + (kk >> 2) * kTile + (kk & 3) * 32, 16),
+                                      desc(Vs + kk * 2048, 2 * kTile), id_o, (part > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit_elect<1>(o_bar);
+    } else {
+        const int quarter = warp & 3, kc = (warp - kEpiW0) >> 2;  // keys kc*64 .. +64
+        const int i = q0 + quarter * 32 + lane;                    // query row within the group
+        const bool vrow = i < nq;
+        int klo = 0, khi = 0;
+        if (vrow) {
+            for (int s2 = 0; s2 < nseq; ++s2) {
+                const int a = p.cu_q[first + s2] - q_lo, b = p.cu_q[first + s2 + 1] - q_lo;
+                if (i >= a && i < b) {
+                    klo = p.cu_k[first + s2] - k_lo;
+                    khi = p.causal ? klo + (i - a) + 1 : p.cu_k[first + s2 + 1] - k_lo;
+                }
+            }
+        }
+        const int rl = quarter * 32 + lane;  // TMEM lane
+        const float c = p.scale * kLog2e;
+        tc::mbar_wait(s_bar, 0);
+        tc::tc_fence_after();
+        const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+        float pv[64];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+            const int key0 = kc * 64 + ch * 32;
+            if (key0 < nkb * kRows && __any_sync(0xffffffffu, klo < key0 + 32 && khi > key0)) {
+                uint32_t sv[32];
+                tc::tmem_ld_32x32(trow + key0, sv);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int key = key0 + j;
+                    const float v = (key >= klo && key < khi) ? __uint_as_float(sv[j]) * c : -INFINITY;
+                    pv[ch * 32 + j] = v;
+                    mx = fmaxf(mx, v);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) pv[ch * 32 + j] = -INFINITY;
+            }
+        }
+        red[kc * kRows + rl] = mx;
+        tc::named_barrier_sync(1, kLongW * 32);
+        const float m = fmaxf(fmaxf(red[rl], red[kRows + rl]), fmaxf(red[2 * kRows + rl], red[3 * kRows + rl]));
+        const float mref = m == -INFINITY ? 0.f : m;
+        float sum = 0.f;
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+            pv[j] = ex2(pv[j] - mref);
+            sum += pv[j];
+        }
+        tc::named_barrier_sync(1, kLongW * 32);
+        red[kc * kRows + rl] = sum;
+        tc::named_barrier_sync(1, kLongW * 32);
+        const float l = (red[rl] + red[kRows + rl]) + (red[2 * kRows + rl] + red[3 * kRows + rl]);
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+        for (int j = 0; j < 64; ++j) pv[j] *= inv;
+        store_row_hilo(Ph + kc * kTile, Pl + kc * kTile, rl, 0, pv);
+        store_row_hilo(Ph + kc * kTile, Pl + kc * kTile, rl, 4, pv + 32);
+        tc::fence_proxy_async_smem();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(p_bar);
+        if (vrow && kc == 0) p.lse[int64_t(h) * p.total_q + q_lo + i] = (mref + log2f(l)) * kLn2;
+        tc::mbar_wait(o_bar, 0);
+        tc::tc_fence_after();
+        uint32_t v[16];
+        tc::tmem_ld_32x16(trow + 256 + kc * 16, v);
+        tc::tmem_ld_wait();
+        if (vrow) {
+            uint4* dst = reinterpret_cast<uint4*>(p.o + int64_t(q_lo + i) * p.ldo + h * 64 + kc * 16);
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                dst[q] = make_uint4(pack_bf16(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1])),
+                                    pack_bf16(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3])),
+                                    pack_bf16(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5])),
+                                    pack_bf16(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7])));
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc(tmem, 512);
+    }
+}
+
+// Backward of a long group: one CTA per (head, group); the group's keys in
+// <= 2 blocks j of 128, its queries in <= 2 blocks i.  D_i = sum_k P dP needs
+// every key block of row i, so pass 1 computes S_ij / dP_ij for all j and
+// accumulates D_i (fixed j order); pass 2 loops j outer, i inner: S_ij, dP_ij
+// again, P_ij (bf16 hi + lo) and dS_ij = P (dP - D_i) (bf16) into shared
+// memory, then dV_j += P^T dO_i, dK_j += dS^T Q_i (accumulated over i in
+// TMEM, emitted after the i loop) and dQ_i += dS K_j (both dQ blocks live in
+// TMEM until the end).  TMEM: S 128 + dP 128 + dV_j 64 + dK_j 64 + dQ 2 x 64.
+// One control thread issues the TMA loads and MMAs strictly in order; these
+// groups are rare, so the phases are not overlapped.
+constexpr int kLongBwdSmem = 2 * kTile /*K*/ + 2 * kTile /*V*/ + kTile /*Q_i*/ + kTile /*dO_i*/ +
+                             2 * kPTile /*P hi+lo*/ + kPTile /*dS*/ + 4096 + 1024;
+
+__global__ void __launch_bounds__(kLongThreads, 1) attn_bwd_long_kernel(const __grid_constant__ BwdParams p) {
+    extern __shared__ uint8_t smraw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    uint8_t* Ks = sm;
+    uint8_t* Vs = Ks + 2 * kTile;
+    uint8_t* Qs = Vs + 2 * kTile;
+    uint8_t* dOs = Qs + kTile;
+    uint8_t* Ph = dOs + kTile;
+    uint8_t* Pl = Ph + kPTile;
+    uint8_t* Sh = Pl + kPTile;
+    float* dpart = reinterpret_cast<float*>(Sh + kPTile);  // [4][128]
+    float* Dv = dpart + 4 * kRows;                           // [2][128]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Dv + 2 * kRows);
+    uint64_t* tma_bar = bars;
+    uint64_t* s_bar = bars + 1;  // S / dP in TMEM
+    uint64_t* e_bar = bars + 2;  // warps done with S / dP (pass 1) or with dV / dK (emit)
+    uint64_t* p_bar = bars + 3;  // P / dS in shared memory
+    uint64_t* g_bar = bars + 4;  // gradient MMAs of an (i, j) tile done
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
+
+    const int h = blockIdx.x, grp = blockIdx.y;
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+    const int lane = threadIdx.x & 31;
+    const int first = p.groups[2 * grp], nseq = p.groups[2 * grp + 1];
+    const int q_lo = p.cu_q[first], nq = p.cu_q[first + nseq] - q_lo;
+    const int k_lo = p.cu_k[first], nk = p.cu_k[first + nseq] - k_lo;
+    if (!long_group(nq, nk)) return;
+    const int nqb = nq > kRows ? 2 : 1, nkb = nk > kRows ? 2 : 1;
+    if (warp == 1 && lane == 0) {
+        tc::mbar_init(tma_bar, 1);
+        tc::mbar_init(s_bar, 1);
+        tc::mbar_init(e_bar, kLongW);
+        tc::mbar_init(p_bar, kLongW);
+        tc::mbar_init(g_bar, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    constexpr uint32_t T_S = 0, T_DP = 128, T_DV = 256, T_DK = 320, T_DQ = 384;
+
+    if (warp == 1) {
+        // ------------------------------------------------ control: TMA + MMA, in order
+        pdl_wait();
+        uint32_t n_tma = 0, n_s = 0, n_e = 0, n_p = 0, n_g = 0;
+        auto load_qi = [&](int i, bool kv) {
+            if (lane == 0) {
+                tc::mbar_expect_tx(tma_bar, (2 + (kv ? 2 * nkb : 0)) * kTile);
+                tc::tma_load_2d(Qs, &p.mq, tma_bar, h * 64, q_lo + i * kRows);
+                tc::tma_load_2d(dOs, &p.mdo, tma_bar, h * 64, q_lo + i * kRows);
+                if (kv)
+                    for (int b = 0; b < nkb; ++b) {
+                        tc::tma_load_2d(Ks + b * kTile, &p.mk, tma_bar, h * 64, k_lo + b * kRows);
+                        tc::tma_load_2d(Vs + b * kTile, &p.mv, tma_bar, h * 64, k_lo + b * kRows);
+                    }
+            }
+            __syncwarp();
+            tc::mbar_wait(tma_bar, (n_tma++) & 1);
+            tc::tc_fence_after();
+        };
+        constexpr uint32_t id_s = tc::idesc_bf16_f32(128, 128, 0, 0);
+        auto s_dp = [&](int j) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                tc::mma_bf16_elect<1>(tmem + T_S, desc(Qs + kk * 32, 16), desc(Ks + j * kTile + kk * 32, 16), id_s, kk > 0);
+                tc::mma_bf16_elect<1>(tmem + T_DP, desc(dOs + kk * 32, 16), desc(Vs + j * kTile + kk * 32, 16), id_s, kk > 0);
+            }
+            tc::mma_commit_elect<1>(s_bar);
+            ++n_s;
+        };
+        // pass 1: D_i over every key block
+        for (int i = 0; i < nqb; ++i) {
+            load_qi(i, i == 0);
+            for (int j = 0; j < nkb; ++j) {
+                s_dp(j);
+                tc::mbar_wait(e_bar, (n_e++) & 1);  // warps read S / dP
+                tc::tc_fence_after();
+            }
+        }
+        // pass 2
+        constexpr uint32_t id_mn = tc::idesc_bf16_f32(128, 64, 1, 1);
+        constexpr uint32_t id_km = tc::idesc_bf16_f32(128, 64, 0, 1);
+        int loaded = nqb == 1 ? 0 : -1;  // block of Q / dO in shared memory
+        for (int j = 0; j < nkb; ++j) {
+            for (int i = 0; i < nqb; ++i) {
+                if (loaded != i) {
+                    load_qi(i, false);
+                    loaded = i;
+                }
+                s_dp(j);
+                tc::mbar_wait(p_bar, (n_p++) & 1);  // P / dS staged
+                tc::tc_fence_after();
+                for (int part = 0; part < 2; ++part) {
+                    const uint8_t* P = part ? Pl : Ph;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {  // K = 128 query rows
+                        const uint32_t acc_v = (i > 0 || part > 0 || kk > 0) ? 1u : 0u;
+                        tc::mma_bf16_elect<1>(tmem + T_DV, desc(P + kk * 2048, kTile), desc(dOs + kk * 2048, kTile), id_mn, acc_v);
+                        if (part == 0)
+                            tc::mma_bf16_elect<1>(tmem + T_DK, desc(Sh + kk * 2048, kTile), desc(Qs + kk * 2048, kTile), id_mn,
+                                                  (i > 0 || kk > 0) ? 1u : 0u);
+                    }
+                }
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)  // K = 128 keys
+                    tc::mma_bf16_elect<1>(tmem + T_DQ + i * 64, desc(Sh + (kk >> 2) * kTile + (kk & 3) * 32, 16),
+                                          desc(Ks + j * kTile + kk * 2048, 2 * kTile), id_km, (j > 0 || kk > 0) ? 1u : 0u);
+                tc::mma_commit_elect<1>(g_bar);
+                tc::mbar_wait(g_bar, (n_g++) & 1);  // smem P / dS and Q / dO free again
+                tc::tc_fence_after();
+            }
+            tc::mbar_wait(e_bar, (n_e++) & 1);  // dV_j / dK_j emitted
+            tc::tc_fence_after();
+        }
+    } else if (warp >= kEpiW0) {
+        const int quarter = warp & 3, kc = (warp - kEpiW0) >> 2;  // keys kc*32 .. +32 of a block
+        const int rl = quarter * 32 + lane;
+        const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+        const float c = p.scale * kLog2e;
+        uint32_t n_s = 0, n_g = 0;
+        // this row's key range (group coordinates) for query block i
+        auto range = [&](int i, int& klo, int& khi, float& l2) {
+            const int qi = i * kRows + rl;
+            klo = khi = 0;
+            l2 = 0.f;
+            if (qi >= nq) return false;
+            for (int s2 = 0; s2 < nseq; ++s2) {
+                const int a = p.cu_q[first + s2] - q_lo, b = p.cu_q[first + s2 + 1] - q_lo;
+                if (qi >= a && qi < b) {
+                    klo = p.cu_k[first + s2] - k_lo;
+                    khi = p.causal ? klo + (qi - a) + 1 : p.cu_k[first + s2 + 1] - k_lo;
+                }
+            }
+            l2 = p.lse[int64_t(h) * p.total_q + q_lo + qi] * kLog2e;
+            return true;
+        };
+        // P (this warp's 32 keys of block j) and dP out of TMEM
+        auto load_p = [&](int j, int klo, int khi, float l2, float (&pv)[32], float (&dpv)[32]) {
+            const int key0 = j * kRows + kc * 32;
+            if (__any_sync(0xffffffffu, klo < key0 + 32 && khi > key0)) {
+                uint32_t sv[32], dv[32];
+                tc::tmem_ld_32x32(trow + T_S + kc * 32, sv);
+                tc::tmem_ld_32x32(trow + T_DP + kc * 32, dv);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) {
+                    const int key = key0 + jj;
+                    pv[jj] = (key >= klo && key < khi) ? ex2(fmaf(__uint_as_float(sv[jj]), c, -l2)) : 0.f;
+                    dpv[jj] = __uint_as_float(dv[jj]);
+                }
+            } else {
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) pv[jj] = dpv[jj] = 0.f;
+            }
+        };
+        // pass 1: D_i = sum over key blocks (j order) of sum_k P dP
+        for (int i = 0; i < nqb; ++i) {
+            int klo, khi;
+            float l2;
+            range(i, klo, khi, l2);
+            for (int j = 0; j < nkb; ++j) {
+                tc::mbar_wait(s_bar, (n_s++) & 1);
+                tc::tc_fence_after();
+                float pv[32], dpv[32];
+                load_p(j, klo, khi, l2, pv, dpv);
+                float dsum = 0.f;
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) dsum = fmaf(pv[jj], dpv[jj], dsum);
+                dpart[kc * kRows + rl] = dsum;
+                tc::tc_fence_before();
+                tc::named_barrier_sync(1, kLongW * 32);
+                if (kc == 0) {
+                    const float t = (dpart[rl] + dpart[kRows + rl]) + (dpart[2 * kRows + rl] + dpart[3 * kRows + rl]);
+                    Dv[i * kRows + rl] = j == 0 ? t : Dv[i * kRows + rl] + t;
+                }
+                tc::named_barrier_sync(1, kLongW * 32);
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(e_bar);
+            }
+        }
+        // pass 2
+        auto emit = [&](uint32_t col, uint16_t* base, int64_t ld, int row, bool vr, float sc) {
+            uint32_t v[16];
+            tc::tmem_ld_32x16(trow + col + kc * 16, v);
+            tc::tmem_ld_wait();
+            if (!vr) return;
+            uint4* dst = reinterpret_cast<uint4*>(base + int64_t(row) * ld + h * 64 + kc * 16);
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                dst[q] = make_uint4(pack_bf16(__uint_as_float(v[8 * q + 0]) * sc, __uint_as_float(v[8 * q + 1]) * sc),
+                                    pack_bf16(__uint_as_float(v[8 * q + 2]) * sc, __uint_as_float(v[8 * q + 3]) * sc),
+                                    pack_bf16(__uint_as_float(v[8 * q + 4]) * sc, __uint_as_float(v[8 * q + 5]) * sc),
+                                    pack_bf16(__uint_as_float(v[8 * q + 6]) * sc, __uint_as_float(v[8 * q + 7]) * sc));
+        };
+        for (int j = 0; j < nkb; ++j) {
+            for (int i = 0; i < nqb; ++i) {
+                int klo, khi;
+                float l2;
+                range(i, klo, khi, l2);
+                tc::mbar_wait(s_bar, (n_s++) & 1);
+                tc::tc_fence_after();
+                float pv[32], dpv[32];
+                load_p(j, klo, khi, l2, pv, dpv);
+                const float D = Dv[i * kRows + rl];
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) dpv[jj] = pv[jj] * (dpv[jj] - D);  // dS
+                store_row_hilo(Ph + (kc >> 1) * kTile, Pl + (kc >> 1) * kTile, rl, (kc & 1) * 4, pv);
+                store_row_hi(Sh + (kc >> 1) * kTile, rl, (kc & 1) * 4, dpv);
+                tc::fence_proxy_async_smem();
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(p_bar);
+                tc::mbar_wait(g_bar, (n_g++) & 1);  // this tile's gradient MMAs done
+                tc::tc_fence_after();
+            }
+            // dV_j, dK_j: TMEM lane = key row of block j
+            const int key = j * kRows + rl;
+            emit(T_DV, p.dv, p.ld_dv, k_lo + key, key < nk, 1.f);
+            emit(T_DK, p.dk, p.ld_dk, k_lo + key, key < nk, p.scale);
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(e_bar);
+        }
+        for (int i = 0; i < nqb; ++i) {
+            const int qi = i * kRows + rl;
+            emit(T_DQ + i * 64, p.dq, p.ld_dq, q_lo + qi, qi < nq, p.scale);
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc(tmem, 512);
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -1104,10 +1527,14 @@ extern "C" int mm_attention_fwd(const mm_attn_args* a, void* stream) {
     // attention: 8.3 vs 10.0 us); beyond that (config-3 cross attention: 40+
     // groups x 8 heads) the mma.sync kernel's four CTAs per SM win (9.5 vs
     // 11.7 us).  MM_ATTN_TC_FWD=1 / 0 forces either kernel (tests, A/B).
+    // Every group runs on tcgen05 by default now (groups past 128 rows in
+    // attn_fwd_long_kernel); MM_ATTN_TC_FWD=0 restores the mma.sync kernel for
+    // all groups, MM_ATTN_TC_FWD=auto the previous one-wave rule (A/B).
     const char* tcf = std::getenv("MM_ATTN_TC_FWD");
     const bool have_tcg = a->tc_groups != nullptr && a->n_tc_groups > 0;
-    const bool use_tc = tcf ? tcf[0] == '1'
-                            : have_tcg && int64_t(a->n_tc_groups) * a->heads <= 2 * int64_t(mm::num_sms());
+    const bool auto_rule = tcf && std::strcmp(tcf, "auto") == 0;
+    const bool use_tc = (tcf && !auto_rule) ? tcf[0] == '1'
+                        : have_tcg && (!auto_rule || int64_t(a->n_tc_groups) * a->heads <= 2 * int64_t(mm::num_sms()));
     mm_attn_args b = *a;
     if (use_tc && a->total_k > 0) {
         tca::FwdParams fp{};
@@ -1130,6 +1557,19 @@ extern "C" int mm_attention_fwd(const mm_attn_args* a, void* stream) {
                                    tca::kFwdSmemBytes, mm::as_stream(stream), fp));
         MM_LAUNCH_CHECK("attn_fwd_tc_kernel");
         if (a->cap <= tca::kRows) return 0;
+        if (tcg && !std::getenv("MM_ATTN_LONG_MMA_SYNC")) {
+            // groups with a sequence past 128 rows: tcgen05, one CTA per 128-query block
+            static bool attr_l = false;
+            if (!attr_l) {
+                MM_CUDA_TRY(cudaFuncSetAttribute(tca::attn_fwd_long_kernel,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, tca::kLongFwdSmem));
+                attr_l = true;
+            }
+            MM_CUDA_TRY(mm::launch_pdl(tca::attn_fwd_long_kernel, dim3(a->heads, a->n_tc_groups, 2),
+                                       dim3(tca::kLongThreads), tca::kLongFwdSmem, mm::as_stream(stream), fp));
+            MM_LAUNCH_CHECK("attn_fwd_long_kernel");
+            return 0;
+        }
         b.flags = 1;  // the mma.sync kernel takes only groups with a longer sequence
     }
     a = &b;
@@ -1174,6 +1614,18 @@ extern "C" int mm_attention_bwd(const mm_attn_args* a, void* stream) {
                                    dim3(tca::kThreads), tca::kSmemBytes, mm::as_stream(stream), bp));
         MM_LAUNCH_CHECK("attn_bwd_tc_kernel");
         if (a->cap <= tca::kRows) return 0;
+        if (tcg && !std::getenv("MM_ATTN_LONG_MMA_SYNC")) {
+            static bool attr_l = false;
+            if (!attr_l) {
+                MM_CUDA_TRY(cudaFuncSetAttribute(tca::attn_bwd_long_kernel,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, tca::kLongBwdSmem));
+                attr_l = true;
+            }
+            MM_CUDA_TRY(mm::launch_pdl(tca::attn_bwd_long_kernel, dim3(a->heads, bp.n_groups),
+                                       dim3(tca::kLongThreads), tca::kLongBwdSmem, mm::as_stream(stream), bp));
+            MM_LAUNCH_CHECK("attn_bwd_long_kernel");
+            return 0;
+        }
     }
     // groups with a sequence longer than 128 rows (or the diagnostics path):
     // the mma.sync kernel, skipping groups the tcgen05 kernel took

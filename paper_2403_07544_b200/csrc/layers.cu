@@ -852,7 +852,10 @@ extern "C" int mm_layernorm_bwd(const float* dy, const float* x, const float* ga
     auto s = mm::as_stream(stream);
     static const bool old_kernel = std::getenv("MM_LN_BWD_BATCHED") != nullptr;  // A/B diagnostics
     static const bool v1 = std::getenv("MM_LN_V1") != nullptr;
-    if (!v1 && !old_kernel && cols == 512) {  // (d = 1024 spills at 64 registers: batched kernel)
+    // v2 (row per warp, one wave): 8.5 vs 5.9 us back to back at 4096 x 512 --
+    // the persistent row kernel below wins; kept for A/B (MM_LN_BWD_V2=1)
+    static const bool bwd_v2 = std::getenv("MM_LN_BWD_V2") != nullptr;
+    if (bwd_v2 && !v1 && !old_kernel && cols == 512) {  // (d = 1024 spills at 64 registers)
         const unsigned g2 = static_cast<unsigned>((rows + 7) / 8);
         MM_CUDA_TRY(mm::launch_pdl(ln_bwd_v2_kernel<512>, dim3(g2), dim3(256), 0, s, dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows));
         MM_LAUNCH_CHECK("ln_bwd_v2_kernel");

@@ -354,17 +354,32 @@ def poison_smem(cuda):
 
 
 @pytest.mark.parametrize("tc_fwd", [False, True], ids=["fwd_mma_sync", "fwd_tcgen05"])
-@pytest.mark.parametrize("causal,maxlen", [(True, 128), (False, 128), (True, 256)])
-def test_attention(cuda, causal, maxlen, tc_fwd, monkeypatch):
-    """Forward (mma.sync, or the opt-in tcgen05 kernel) and backward (tcgen05
-    for groups within 128 rows, mma.sync for longer sequences) vs an fp32
-    PyTorch reference."""
+@pytest.mark.parametrize("causal,maxlen,maxk", [(True, 128, 128), (False, 128, 128), (True, 256, 256),
+                                                (False, 256, 256), (False, 256, 100), (False, 90, 256)])
+@pytest.mark.parametrize("long_path", ["tcgen05", "mma_sync"])
+def test_attention(cuda, causal, maxlen, maxk, tc_fwd, long_path, monkeypatch):
+    """Forward (tcgen05 by default, or the mma.sync kernel) and backward
+    (tcgen05) vs an fp32 PyTorch reference; sequences past 128 rows (query
+    side, key side or both) take the long-group tcgen05 kernels, or with
+    long_path=mma_sync the previous mma.sync kernels."""
+    if long_path == "mma_sync" and maxlen <= 128 and maxk <= 128:
+        pytest.skip("no long groups")
     monkeypatch.setenv("MM_ATTN_TC_FWD", "1" if tc_fwd else "0")
+    if long_path == "mma_sync":
+        monkeypatch.setenv("MM_ATTN_LONG_MMA_SYNC", "1")
+    else:
+        monkeypatch.delenv("MM_ATTN_LONG_MMA_SYNC", raising=False)
     from paper_2403_07544_b200 import ops
-    rng = np.random.default_rng(maxlen + causal)
+    rng = np.random.default_rng(maxlen + causal + maxk)
     heads, d = 8, 512
     lq = rng.integers(1, maxlen + 1, size=13)
-    lk = lq.copy() if causal else rng.integers(1, maxlen + 1, size=13)
+    lk = lq.copy() if causal else rng.integers(1, maxk + 1, size=13)
+    if maxlen > 128:
+        lq[3] = maxlen  # the clip's edge
+    if maxk > 128:
+        lk[7] = maxk
+    if causal:
+        lk = lq.copy()
     cu_q = np.concatenate([[0], np.cumsum(lq)]).astype(np.int32)
     cu_k = np.concatenate([[0], np.cumsum(lk)]).astype(np.int32)
     tq, tk = int(cu_q[-1]), int(cu_k[-1])
