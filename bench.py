@@ -53,7 +53,9 @@ def gemm_traffic(config: str):
     committed ncu capture (profiles/r01d_gemm_traffic.json, tools/gemm_traffic.py;
     cold-cache, serialised launches) next to the algorithmic FLOPs of the same
     step; None for other workloads (not captured)."""
-    path = os.path.join(ROOT, "profiles", "r01d_gemm_traffic.json")
+    path = os.path.join(ROOT, "profiles", "r02_gemm_traffic.json")
+    if not os.path.exists(path):
+        path = os.path.join(ROOT, "profiles", "r01d_gemm_traffic.json")
     if config != "config3" or not os.path.exists(path):
         return None
     with open(path) as f:
@@ -61,7 +63,8 @@ def gemm_traffic(config: str):
     return {"dram_bytes_per_step": t["dram_bytes_per_step"], "launches": t["gemm_launches"],
             "dram_bytes_per_launch": t["dram_bytes_per_launch"],
             "algorithmic_flops_per_step": t["algorithmic_flops_per_step"],
-            "flops_per_dram_byte": t["flops_per_dram_byte"], "source": "profiles/r01d_gemm_traffic.json"}
+            "flops_per_dram_byte": t["flops_per_dram_byte"],
+            "source": os.path.relpath(path, ROOT)}
 
 
 class ClockSampler:

@@ -340,7 +340,7 @@ int mm_embed_bwd_sorted(const int32_t* table, int64_t rows, int n_chunks, int n_
                         const float* dout, float* dtable, int cols, float scale, float* scratch,
                         void* stream);
 /* Host: the sort / chunk tables of mm_embed_bwd_sorted for `rows` token ids
- * (out: 7 * rows int32; see abi_host.cpp). */
+ * (chunk_rows in [1, 32]; out: 7 * rows int32; see abi_host.cpp). */
 int mm_embed_segments(const int32_t* ids, int rows, int chunk_rows, int32_t* out, int* n_chunks,
                       int* n_multi);
 

@@ -231,8 +231,9 @@ extern "C" int mm_attention_tables(const int32_t* cu_src, const int32_t* cu_tgt,
 // order.  Capacity of out: 7 * rows int32.
 extern "C" int mm_embed_segments(const int32_t* ids, int rows, int chunk_rows, int32_t* out,
                                  int* n_chunks, int* n_multi) {
-    MM_CHECK_ARG(rows >= 0 && chunk_rows >= 1 && out && n_chunks && n_multi && (rows == 0 || ids),
-                 "bad arguments");
+    MM_CHECK_ARG(rows >= 0 && chunk_rows >= 1 && chunk_rows <= 32 && out && n_chunks && n_multi &&
+                     (rows == 0 || ids),
+                 "bad arguments (chunk_rows must be in [1, 32])");
     std::vector<uint64_t> key(rows);
     for (int r = 0; r < rows; ++r) {
         MM_CHECK_ARG(ids[r] >= 0, "negative token id at row %d", r);

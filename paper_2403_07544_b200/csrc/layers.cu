@@ -469,38 +469,49 @@ __global__ void __launch_bounds__(256) embed_bwd_kernel(const int32_t* __restric
 // hundreds of serialised atomics on one row.
 constexpr int kEmbMaxV = 8;  // float4 per lane: cols <= 1024
 
+// V = cols / 128 float4 per lane; R rows loaded per batch (independent loads
+// in flight, summed in row order): the chunk's row indices come in with one
+// coalesced load and are broadcast by shuffles, so no load waits on another
+template <int V, int R>
 __global__ void __launch_bounds__(256) embed_bwd_chunk_kernel(const int32_t* __restrict__ perm,
                                                               const int32_t* __restrict__ chunks,
                                                               int n_chunks, const float* __restrict__ dout,
-                                                              float* dtable, float* scratch, int cols,
-                                                              float scale) {
+                                                              float* dtable, float* scratch, float scale) {
+    constexpr int cols = V * 128;
     pdl_wait_release();
     const int lane = threadIdx.x & 31;
     const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (c >= n_chunks) return;
     const int b = chunks[3 * c], e = chunks[3 * c + 1], tgt = chunks[3 * c + 2];
-    const int nv = cols / 4;
-    float4 acc[kEmbMaxV];
+    const int n = e - b;  // <= 32 (EMB_CHUNK_ROWS)
+    const int my_row = lane < n ? perm[b + lane] : 0;
+    float4 acc[V];
 #pragma unroll
-    for (int i = 0; i < kEmbMaxV; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int p = b; p < e; ++p) {
-        const float4* d = reinterpret_cast<const float4*>(dout + int64_t(perm[p]) * cols);
+    for (int i = 0; i < V; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r0 = 0; r0 < n; r0 += R) {
+        float4 g[R][V];
 #pragma unroll
-        for (int i = 0; i < kEmbMaxV; ++i) {
-            const int v = lane + 32 * i;
-            if (v < nv) {
-                const float4 g = d[v];
-                acc[i].x = fmaf(g.x, scale, acc[i].x); acc[i].y = fmaf(g.y, scale, acc[i].y);
-                acc[i].z = fmaf(g.z, scale, acc[i].z); acc[i].w = fmaf(g.w, scale, acc[i].w);
+        for (int u = 0; u < R; ++u) {
+            const int row = __shfl_sync(0xffffffffu, my_row, (r0 + u) & 31);
+            const float4* d = reinterpret_cast<const float4*>(dout + int64_t(row) * cols);
+#pragma unroll
+            for (int i = 0; i < V; ++i) g[u][i] = r0 + u < n ? d[lane + 32 * i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            if (r0 + u >= n) break;
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                acc[i].x = fmaf(g[u][i].x, scale, acc[i].x); acc[i].y = fmaf(g[u][i].y, scale, acc[i].y);
+                acc[i].z = fmaf(g[u][i].z, scale, acc[i].z); acc[i].w = fmaf(g[u][i].w, scale, acc[i].w);
             }
         }
     }
     float4* dst = tgt >= 0 ? reinterpret_cast<float4*>(dtable + int64_t(tgt) * cols)
                            : reinterpret_cast<float4*>(scratch + int64_t(-tgt - 1) * cols);
 #pragma unroll
-    for (int i = 0; i < kEmbMaxV; ++i) {
+    for (int i = 0; i < V; ++i) {
         const int v = lane + 32 * i;
-        if (v >= nv) continue;
         if (tgt >= 0) {
             float4 t = dst[v];
             t.x += acc[i].x; t.y += acc[i].y; t.z += acc[i].z; t.w += acc[i].w;
@@ -511,26 +522,61 @@ __global__ void __launch_bounds__(256) embed_bwd_chunk_kernel(const int32_t* __r
     }
 }
 
+// one warp per multi-chunk id: its partials (R per batch, independent loads)
+// added in chunk order, then into the table row
+template <int V, int R>
 __global__ void __launch_bounds__(256) embed_bwd_multi_kernel(const int32_t* __restrict__ multi, int n_multi,
                                                               const float* __restrict__ scratch,
-                                                              float* dtable, int cols) {
+                                                              float* dtable) {
+    constexpr int cols = V * 128;
     pdl_wait_release();
     const int lane = threadIdx.x & 31;
     const int m = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (m >= n_multi) return;
     const int id = multi[3 * m], s0 = multi[3 * m + 1], ns = multi[3 * m + 2];
-    const int nv = cols / 4;
-    float4* dst = reinterpret_cast<float4*>(dtable + int64_t(id) * cols);
-    for (int v = lane; v < nv; v += 32) {
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int k = 0; k < ns; ++k) {
-            const float4 x = reinterpret_cast<const float4*>(scratch + int64_t(s0 + k) * cols)[v];
-            a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+    float4 a[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k0 = 0; k0 < ns; k0 += R) {
+        float4 x[R][V];
+#pragma unroll
+        for (int u = 0; u < R; ++u)
+#pragma unroll
+            for (int i = 0; i < V; ++i)
+                x[u][i] = k0 + u < ns ? reinterpret_cast<const float4*>(scratch + int64_t(s0 + k0 + u) * cols)[lane + 32 * i]
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            if (k0 + u >= ns) break;
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                a[i].x += x[u][i].x; a[i].y += x[u][i].y; a[i].z += x[u][i].z; a[i].w += x[u][i].w;
+            }
         }
-        float4 t = dst[v];
-        t.x += a.x; t.y += a.y; t.z += a.z; t.w += a.w;
-        dst[v] = t;
     }
+    float4* dst = reinterpret_cast<float4*>(dtable + int64_t(id) * cols);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        float4 t = dst[lane + 32 * i];
+        t.x += a[i].x; t.y += a[i].y; t.z += a[i].z; t.w += a[i].w;
+        dst[lane + 32 * i] = t;
+    }
+}
+
+template <int V>
+int embed_sorted_launch(const int32_t* perm, const int32_t* chunks, int n_chunks, const int32_t* multi,
+                        int n_multi, const float* dout, float* dtable, float scale, float* scratch,
+                        cudaStream_t s) {
+    constexpr int R = V >= 8 ? 2 : (V >= 4 ? 4 : 8);
+    MM_CUDA_TRY(mm::launch_pdl(embed_bwd_chunk_kernel<V, R>, dim3((n_chunks + 7) / 8), dim3(256), 0, s, perm,
+                               chunks, n_chunks, dout, dtable, scratch, scale));
+    MM_LAUNCH_CHECK("embed_bwd_chunk_kernel");
+    if (n_multi > 0) {
+        MM_CUDA_TRY(mm::launch_pdl(embed_bwd_multi_kernel<V, R>, dim3((n_multi + 7) / 8), dim3(256), 0, s,
+                                   multi, n_multi, (const float*)scratch, dtable));
+        MM_LAUNCH_CHECK("embed_bwd_multi_kernel");
+    }
+    return 0;
 }
 
 // ----------------------------------------------------------------------------
@@ -921,21 +967,19 @@ extern "C" int mm_embed_bwd_sorted(const int32_t* table, int64_t rows, int n_chu
                                    const float* dout, float* dtable, int cols, float scale,
                                    float* scratch, void* stream) {
     MM_CHECK_ARG(table && dout && dtable && (n_multi == 0 || scratch), "NULL argument");
-    MM_CHECK_ARG(cols % 4 == 0 && cols <= 4 * 32 * kEmbMaxV, "cols %d: multiple of 4, <= 1024", cols);
+    MM_CHECK_ARG(cols == 128 || cols == 256 || cols == 512 || cols == 1024,
+                 "cols %d: 128, 256, 512 or 1024", cols);
     if (rows == 0 || n_chunks == 0) return 0;
     const int32_t* perm = table;
     const int32_t* chunks = table + rows;
     const int32_t* multi = chunks + int64_t(3) * n_chunks;
     auto s = mm::as_stream(stream);
-    MM_CUDA_TRY(mm::launch_pdl(embed_bwd_chunk_kernel, dim3((n_chunks + 7) / 8), dim3(256), 0, s, perm, chunks,
-                               n_chunks, dout, dtable, scratch, cols, scale));
-    MM_LAUNCH_CHECK("embed_bwd_chunk_kernel");
-    if (n_multi > 0) {
-        MM_CUDA_TRY(mm::launch_pdl(embed_bwd_multi_kernel, dim3((n_multi + 7) / 8), dim3(256), 0, s, multi,
-                                   n_multi, (const float*)scratch, dtable, cols));
-        MM_LAUNCH_CHECK("embed_bwd_multi_kernel");
+    switch (cols) {
+        case 128: return embed_sorted_launch<1>(perm, chunks, n_chunks, multi, n_multi, dout, dtable, scale, scratch, s);
+        case 256: return embed_sorted_launch<2>(perm, chunks, n_chunks, multi, n_multi, dout, dtable, scale, scratch, s);
+        case 512: return embed_sorted_launch<4>(perm, chunks, n_chunks, multi, n_multi, dout, dtable, scale, scratch, s);
+        default: return embed_sorted_launch<8>(perm, chunks, n_chunks, multi, n_multi, dout, dtable, scale, scratch, s);
     }
-    return 0;
 }
 
 extern "C" int mm_xent_fwd_bwd(const uint16_t* logits, const int32_t* labels, uint16_t* dlogits,
