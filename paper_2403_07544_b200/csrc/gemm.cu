@@ -86,7 +86,11 @@ struct Cfg {
     static constexpr int kLnBytes = CN > 1 ? 4 * BM * 8 : 0;  // float2 [2][BM] x 2
     static constexpr int kStagesFit = (kSmemLimit - kEpiSmem - 1024 - kBarBytes - kLnBytes) / kStageBytes;
     static constexpr int kStages = kStagesFit > MM_GEMM_MAX_STAGES ? MM_GEMM_MAX_STAGES : kStagesFit;
-    static constexpr int kTmemCols = BN == 128 ? 256 : 512;  // 2 accumulators, power of 2
+    // 2 accumulators (power of 2); a single-CTA 128-wide tile also parks the
+    // tile's fp32 residual in columns 256..383 (loaded while the MMAs run)
+    static constexpr bool kResidTmem = BN == 128 && CG == 1 && CN == 1;
+    static constexpr int kTmemCols = 512;
+    static constexpr uint32_t kResidCol = 2 * BN;
     static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 + kBarBytes + kLnBytes;
     static_assert(kSmem <= kSmemLimit, "smem budget");
     static_assert(CG == 1 || kBRows % 64 == 0, "pair tiles need 64-aligned B halves");
@@ -185,9 +189,10 @@ __device__ __forceinline__ bool has_bias(const Prob& p) {
                       ep == MM_EPI_F32_RESID || ep == MM_EPI_F32_RESID_LN);
 }
 
-// bv: this lane's bias value for column col0 + lane (preloaded per tile)
+// bv: this lane's bias value for column col0 + lane (preloaded per tile);
+// resid_done: the residual is added by the caller (parked in TMEM)
 __device__ __forceinline__ void epilogue_math(const Prob& p, int64_t row, int64_t col0,
-                                              float (&acc)[32], float bv) {
+                                              float (&acc)[32], float bv, bool resid_done = false) {
     const int ep = p.epilogue;
     if (has_bias(p)) {
 #pragma unroll
@@ -220,7 +225,7 @@ __device__ __forceinline__ void epilogue_math(const Prob& p, int64_t row, int64_
                 if (col0 + j < p.n && bf16_to_f(aux[j]) <= 0.f) acc[j] = 0.f;
         }
     }
-    if (ep == MM_EPI_F32_RESID || ep == MM_EPI_F32_RESID_LN) {
+    if ((ep == MM_EPI_F32_RESID && !resid_done) || ep == MM_EPI_F32_RESID_LN) {
         const float* res = p.resid + row * p.ldd + col0;
         if (full) {
 #pragma unroll
@@ -571,6 +576,39 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             const int cbase = tn * BN + half * (BN / kSlices);
+            // residual tile of this warp's rows / columns into TMEM while the
+            // MMAs of the unit run (lane = row: 128 B per lane per chunk; the
+            // LSU is idle during the mainloop), read back next to the
+            // accumulator in the epilogue -- the add order stays
+            // (acc + bias) + resid
+            const bool resid_tm = C::kResidTmem && P.epilogue == MM_EPI_F32_RESID;
+            if constexpr (C::kResidTmem) {
+                if (resid_tm) {
+                    const int64_t rrow = int64_t(tm) * BM + lane_grp * 32 + lane;
+                    const uint32_t t_res = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) +
+                                           C::kResidCol + half * (BN / kSlices);
+#pragma unroll 1
+                    for (int c = 0; c < kChunks; ++c) {
+                        const int col0 = cbase + c * 32;
+                        uint32_t r[32];
+                        if (rrow < P.m && col0 + 32 <= P.n) {
+                            const float4* res = reinterpret_cast<const float4*>(P.resid + rrow * P.ldd + col0);
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const float4 x = res[q];
+                                r[4 * q] = __float_as_uint(x.x); r[4 * q + 1] = __float_as_uint(x.y);
+                                r[4 * q + 2] = __float_as_uint(x.z); r[4 * q + 3] = __float_as_uint(x.w);
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                r[j] = (rrow < P.m && col0 + j < P.n) ? __float_as_uint(P.resid[rrow * P.ldd + col0 + j]) : 0u;
+                        }
+                        tc::tmem_st_32x32(t_res + c * 32, r);
+                    }
+                    tc::tmem_st_wait();
+                }
+            }
             // bias for this warp's columns, fetched before waiting on the MMAs
             float bv[kChunks];
 #pragma unroll
@@ -599,7 +637,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float f[32];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-                    epilogue_math(P, row, col0, f, bv[c]);
+                    epilogue_math(P, row, col0, f, bv[c], resid_tm);
+                    if constexpr (C::kResidTmem) {
+                        if (resid_tm) {
+                            const uint32_t t_res = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) +
+                                                   C::kResidCol + half * (BN / kSlices) + c * 32;
+                            tc::tmem_ld_32x32(t_res, v);
+                            tc::tmem_ld_wait();
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) f[j] += __uint_as_float(v[j]);
+                        }
+                    }
                     if constexpr (CN > 1) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) xs[c][j] = f[j];
