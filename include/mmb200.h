@@ -452,6 +452,8 @@ int mm_task_fwd_bwd(const mm_task* task, const mm_batch* batch, void* workspace,
 /* out[c] += sum over rows of x[r, c] (bf16 in, fp32 accumulate) */
 int mm_colsum_bf16(const uint16_t* x, float* out, int64_t rows, int cols, void* stream);
 int mm_cast_f32_bf16(const float* x, uint16_t* y, int64_t n, void* stream);
+/* y = (float) x, bf16 -> fp32 (n % 4 == 0): the bf16 gradient wire's way back */
+int mm_cast_bf16_f32(const uint16_t* x, float* y, int64_t n, void* stream);
 int mm_flush_l2(void* scratch, size_t bytes, void* stream);
 /* y += alpha * x (fp32): DeviceState.accumulate (syncsim.py:113-118) */
 int mm_axpy_f32(float* y, const float* x, float alpha, int64_t n, void* stream);

@@ -298,6 +298,7 @@ def _declare(h: ctypes.CDLL) -> None:
     sig("mm_embed_bwd_sorted", c_int, c_void_p, c_int64, c_int, c_int, c_void_p, c_void_p, c_int, c_float,
         c_void_p, c_void_p)
     sig("mm_embed_segments", c_int, c_void_p, c_int, c_int, c_void_p, POINTER(c_int), POINTER(c_int))
+    sig("mm_cast_bf16_f32", c_int, c_void_p, c_void_p, c_int64, c_void_p)
     sig("mm_axpy_f32", c_int, c_void_p, c_void_p, c_float, c_int64, c_void_p)
     sig("mm_axpy_f64", c_int, c_void_p, c_void_p, c_double, c_int64, c_void_p)
     sig("mm_task_fwd_bwd", c_int, c_void_p, c_void_p, c_void_p, POINTER(c_size_t), c_void_p,

@@ -57,7 +57,11 @@ constexpr int kEpiWarp0 = 2;
 // two slices each take half of the tile's columns
 constexpr int kEpiWarps = MM_GEMM_EPI_WARPS;
 constexpr int kSlices = kEpiWarps / 4;
-constexpr int kEpiBufs = MM_GEMM_EPI_BUFS;  // staging boxes per epilogue warp
+#ifndef MM_GEMM_EPI_BUFS128
+// single-CTA 128-wide tiles (the small, multi-tile forward / dgrad GEMMs,
+// whose epilogue warps bound the kernel): staging boxes per epilogue warp
+#define MM_GEMM_EPI_BUFS128 MM_GEMM_EPI_BUFS
+#endif
 constexpr int kBiasWarp = kEpiWarp0 + kEpiWarps;  // first of the bias-gradient warps
 // bias-gradient warps: second consumer of every smem stage; each sums 16 of
 // the stage's 64 K-rows (one warp summing all 64 was slower than a 256-wide
@@ -67,7 +71,7 @@ constexpr int kThreads = (kBiasWarp + kBiasWarps) * 32;
 constexpr int kMaxProbs = 48;  // problems per grouped launch (kernel parameter space: ~21 KB of 32 KB)
 
 constexpr int kEpiBufBytes = 32 * 128;                    // 32 rows x 128 B box
-constexpr int kEpiSmem = kEpiWarps * kEpiBufs * kEpiBufBytes;
+
 constexpr int kSmemLimit = 232448;
 
 // CG = CTAs per MMA: 1, or 2 for a CTA pair (cta_group::2) computing a
@@ -75,6 +79,8 @@ constexpr int kSmemLimit = 232448;
 // per-SM shared-memory traffic per MMA drops by a quarter (BN=128) to a half.
 template <int BN, int CG, int CN = 1>
 struct Cfg {
+    static constexpr int kEpiBufs = (BN == 128 && CG == 1 && CN == 1) ? MM_GEMM_EPI_BUFS128 : MM_GEMM_EPI_BUFS;
+    static constexpr int kEpiSmem = kEpiWarps * kEpiBufs * kEpiBufBytes;
     static constexpr int kBRows = BN / CG;             // B rows (N) staged by one CTA
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = kBRows * BK * 2;
@@ -192,7 +198,8 @@ __device__ __forceinline__ bool has_bias(const Prob& p) {
 // bv: this lane's bias value for column col0 + lane (preloaded per tile);
 // resid_done: the residual is added by the caller (parked in TMEM)
 __device__ __forceinline__ void epilogue_math(const Prob& p, int64_t row, int64_t col0,
-                                              float (&acc)[32], float bv, bool resid_done = false) {
+                                              float (&acc)[32], float bv, bool resid_done = false,
+                                              const uint32_t* aux_pre = nullptr) {
     const int ep = p.epilogue;
     if (has_bias(p)) {
 #pragma unroll
@@ -206,7 +213,13 @@ __device__ __forceinline__ void epilogue_math(const Prob& p, int64_t row, int64_
     const bool full = col0 + 32 <= p.n;
     if (ep == MM_EPI_BF16_DRELU) {
         const uint16_t* aux = reinterpret_cast<const uint16_t*>(p.aux) + row * p.ldd + col0;
-        if (full) {
+        if (aux_pre != nullptr) {  // this row's 32 mask values, loaded before the accumulator wait
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                if (bf16_to_f(aux_pre[e] & 0xffff) <= 0.f) acc[2 * e] = 0.f;
+                if (bf16_to_f(aux_pre[e] >> 16) <= 0.f) acc[2 * e + 1] = 0.f;
+            }
+        } else if (full) {
             const uint4* a4 = reinterpret_cast<const uint4*>(aux);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -315,14 +328,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem_a = smem;
     uint8_t* smem_b = smem + C::kStages * C::kABytes;
     uint8_t* smem_epi = smem + C::kStages * C::kStageBytes;  // 1024-aligned
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_epi + kEpiSmem);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem_epi + C::kEpiSmem);
     uint64_t* empty_bar = full_bar + C::kStages;
     uint64_t* bias_bar = empty_bar + C::kStages;  // pair: "stage consumed by the MMA" for the bias warp
     uint64_t* tfull_bar = bias_bar + C::kStages;
     uint64_t* tempty_bar = tfull_bar + 2;
     uint64_t* xch_bar = tempty_bar + 2;  // CN > 1: row-sum exchange, one per parity
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xch_bar + 2);
-    float* ln_part = reinterpret_cast<float*>(smem_epi + kEpiSmem + C::kBarBytes);  // [2][BM]
+    float* ln_part = reinterpret_cast<float*>(smem_epi + C::kEpiSmem + C::kBarBytes);  // [2][BM]
     float* ln_xch = ln_part + 4 * BM;                                                // float2 [2][BM]
 
     // warp index through a shuffle: ptxas then knows it is warp-uniform, so
@@ -561,7 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int lane_grp = warp & 3;                   // TMEM lanes this warp may access
         const int half = (warp - kEpiWarp0) >> 2;        // which column slice of the tile
         constexpr int kChunks = BN / 32 / kSlices;       // 32-column chunks per warp
-        uint8_t* bufs = smem_epi + (warp - kEpiWarp0) * kEpiBufs * kEpiBufBytes;
+        uint8_t* bufs = smem_epi + (warp - kEpiWarp0) * C::kEpiBufs * kEpiBufBytes;
         int nbuf = 0;
         int local = 0;
         int ln_round = 0;  // CN > 1: row-sum exchanges so far (two per tile)
@@ -609,6 +622,38 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc::tmem_st_wait();
                 }
             }
+            // ReLU-backward mask of this warp's rows / columns, fetched before
+            // waiting on the MMAs (the wait then hides the load; 128-wide tiles)
+            constexpr bool kAuxPre = kChunks <= 2;
+            uint32_t auxr[kAuxPre ? kChunks : 1][16];
+            const bool aux_pre = kAuxPre && P.epilogue == MM_EPI_BF16_DRELU;
+            if constexpr (kAuxPre) {
+                if (aux_pre) {
+                    const int64_t arow = int64_t(tm) * (BM * CG) + rank * BM + lane_grp * 32 + lane;
+#pragma unroll
+                    for (int c = 0; c < kChunks; ++c) {
+                        const int col0 = cbase + c * 32;
+                        if (arow < P.m && col0 + 32 <= P.n) {
+                            const uint4* a4 = reinterpret_cast<const uint4*>(
+                                reinterpret_cast<const uint16_t*>(P.aux) + arow * P.ldd + col0);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const uint4 w = __ldg(a4 + q);
+                                auxr[c][4 * q] = w.x; auxr[c][4 * q + 1] = w.y;
+                                auxr[c][4 * q + 2] = w.z; auxr[c][4 * q + 3] = w.w;
+                            }
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) {
+                                const uint16_t* a = reinterpret_cast<const uint16_t*>(P.aux) + arow * P.ldd + col0 + 2 * e;
+                                const uint32_t lo = (arow < P.m && col0 + 2 * e < P.n) ? a[0] : 0u;
+                                const uint32_t hi = (arow < P.m && col0 + 2 * e + 1 < P.n) ? a[1] : 0u;
+                                auxr[c][e] = lo | (hi << 16);
+                            }
+                        }
+                    }
+                }
+            }
             // bias for this warp's columns, fetched before waiting on the MMAs
             float bv[kChunks];
 #pragma unroll
@@ -637,7 +682,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float f[32];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-                    epilogue_math(P, row, col0, f, bv[c], resid_tm);
+                    const uint32_t* ap = nullptr;
+                    if constexpr (kAuxPre) ap = aux_pre ? auxr[c] : nullptr;
+                    epilogue_math(P, row, col0, f, bv[c], resid_tm, ap);
                     if constexpr (C::kResidTmem) {
                         if (resid_tm) {
                             const uint32_t t_res = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) +
@@ -653,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int j = 0; j < 32; ++j) xs[c][j] = f[j];
                     }
                     uint8_t* buf = bufs + nbuf * kEpiBufBytes;
-                    if (lane == 0) tc::bulk_wait_read<kEpiBufs - 1>();  // the store that last read `buf` is done
+                    if (lane == 0) tc::bulk_wait_read<C::kEpiBufs - 1>();  // the store that last read `buf` is done
                     __syncwarp();
                     stage_row(buf, lane, f, out_bf16);
                     tc::fence_proxy_async_smem();
@@ -663,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         else tc::tma_store_2d(&P.td, buf, col0, row0);
                         tc::bulk_commit();
                     }
-                    if (++nbuf == kEpiBufs) nbuf = 0;
+                    if (++nbuf == C::kEpiBufs) nbuf = 0;
                 }
             }
             // accumulator drained: one arrive per warp on the MMA CTA's barrier
@@ -739,7 +786,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         hv[4 * q + 3] = (xs[c][4 * q + 3] - mu) * rs * gg.w + bb.w;
                     }
                     uint8_t* buf = bufs + nbuf * kEpiBufBytes;
-                    if (lane == 0) tc::bulk_wait_read<kEpiBufs - 1>();
+                    if (lane == 0) tc::bulk_wait_read<C::kEpiBufs - 1>();
                     __syncwarp();
                     stage_row(buf, lane, hv, true);
                     tc::fence_proxy_async_smem();
@@ -748,7 +795,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tc::tma_store_2d(&g.ln.th, buf, col0, row0);
                         tc::bulk_commit();
                     }
-                    if (++nbuf == kEpiBufs) nbuf = 0;
+                    if (++nbuf == C::kEpiBufs) nbuf = 0;
                 }
                 if (crank == 0 && half == 0 && row < P.m) {
                     g.ln.mean[row] = mu;

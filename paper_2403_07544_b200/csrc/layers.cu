@@ -855,6 +855,16 @@ __global__ void cast_kernel(const float* __restrict__ x, uint16_t* __restrict__ 
     }
 }
 
+__global__ void widen_kernel(const uint16_t* __restrict__ x, float* __restrict__ y, int64_t n4) {
+    pdl_wait_release();
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const uint2 w = reinterpret_cast<const uint2*>(x)[i];
+        reinterpret_cast<float4*>(y)[i] = make_float4(bf2f(w.x & 0xffff), bf2f(w.x >> 16),
+                                                      bf2f(w.y & 0xffff), bf2f(w.y >> 16));
+    }
+}
+
 }  // namespace
 
 extern "C" int mm_layernorm_fwd(const float* x, const float* gamma, const float* beta, uint16_t* y,
@@ -1015,6 +1025,16 @@ extern "C" int mm_colsum_bf16(const uint16_t* x, float* out, int64_t rows, int c
     dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(slabs));
     MM_CUDA_TRY(mm::launch_pdl(colsum_kernel, dim3(grid), dim3(256), 0, mm::as_stream(stream), x, out, rows, cols, slab));
     MM_LAUNCH_CHECK("colsum_kernel");
+    return 0;
+}
+
+extern "C" int mm_cast_bf16_f32(const uint16_t* x, float* y, int64_t n, void* stream) {
+    MM_CHECK_ARG(x && y && n % 4 == 0, "n must be a multiple of 4");
+    if (n == 0) return 0;
+    const int64_t n4 = n / 4;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n4 + 255) / 256, 8 * mm::num_sms()));
+    MM_CUDA_TRY(mm::launch_pdl(widen_kernel, dim3(grid), dim3(256), 0, mm::as_stream(stream), x, y, n4));
+    MM_LAUNCH_CHECK("widen_kernel");
     return 0;
 }
 

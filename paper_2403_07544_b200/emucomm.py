@@ -21,7 +21,9 @@ GPU, with ``EmuCommGroups`` in place of ``CommGroups``:
   ncclBroadcast up to the ring's summation order;
 * the partitioned transport's reduce-scatter / all-gather (mode 1 / 2 items)
   are the same sum restricted to the owner's use, and a copy of each owner's
-  bf16 weight shard into every member.
+  bf16 weight shard into every member;
+* bf16 gradient items (the bf16 wire) are summed in fp32 in rank order and
+  rounded once (NCCL's ring rounds its partial sums: same order of error).
 
 The C library is not re-entrant, so ``_native.serialized_calls`` makes every
 ctypes call take one process-wide lock while the threads run.
@@ -159,8 +161,19 @@ class EmuCommGroups:
                             dst[j * shard:(j + 1) * shard].copy_(src[j * shard:(j + 1) * shard])
                 torch.cuda.synchronize()
                 return
-            if dtype != 0:
-                raise RuntimeError("the emulated communicator sums fp32 buckets only")
+            if dtype == 1:  # bf16 wire: fp32 sum in rank order, one rounding
+                views = [hub.buckets[reqs[r][0]][2] for r in members]
+                if mode == 0 and root >= 0:
+                    tot = views[root].clone()
+                else:
+                    acc = torch.zeros(n_elems, dtype=torch.float32, device=views[0].device)
+                    for v in views:
+                        acc += v.float()
+                    tot = acc.bfloat16()
+                for v in views:
+                    v.copy_(tot)
+                torch.cuda.synchronize()
+                return
             if hub.record:
                 for r in members:
                     _, key, t = hub.buckets[reqs[r][0]]
@@ -205,6 +218,8 @@ class EmulatedWorld:
             for k, st in e.states.items():
                 self.hub.buckets[st.grad.data_ptr()] = (r, k, st.grad)
                 self.hub.buckets[st.weights.data_ptr()] = (r, k, st.weights)
+                if getattr(st, "wire", None) is not None:
+                    self.hub.buckets[st.wire.data_ptr()] = (r, k, st.wire)
         self.plan = self.engines[0].plan
 
     def step(self, step_idx: int, batches) -> list:

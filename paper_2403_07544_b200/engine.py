@@ -197,7 +197,7 @@ class Engine:
     def __init__(self, tasks: Sequence[TaskSpec], topo: ClusterTopology, shape: ModelShape,
                  rank: int = 0, world: int = 1, device=None, seed: int = 0,
                  adam: AdamConfig = AdamConfig(), store=None, masters=None,
-                 exchange: Optional[str] = None, comm=None):
+                 exchange: Optional[str] = None, comm=None, grad_wire: Optional[str] = None):
         if shape.head_dim != 64:
             raise ValueError("the attention kernel is specialised for head_dim 64")
         self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
@@ -215,6 +215,12 @@ class Engine:
         if self.exchange not in ("nccl", "peer", "partitioned"):
             raise ValueError(f"unknown exchange {self.exchange!r}")
         self.partitioned = world > 1 and self.exchange == "partitioned"
+        # K2's gradient wire format: "fp32", or "bf16" (the bucket is cast to a
+        # bf16 copy before the all-reduce / reduce-scatter and widened back:
+        # half the NVLink bytes for a 2^-9 relative rounding of the sum)
+        self.grad_wire = grad_wire or os.environ.get("MM_GRAD_WIRE", "fp32")
+        if self.grad_wire not in ("fp32", "bf16"):
+            raise ValueError(f"unknown grad_wire {self.grad_wire!r}")
         self.states: dict[ModuleKey, ModuleState] = {}
         for k in self.hosted:
             m = None if masters is None else masters.get(k)
@@ -223,6 +229,9 @@ class Engine:
             if self.partitioned and g >= 2:  # buckets padded to g equal shards
                 cap = g * self.shard_elems(self.layouts[k].numel, g)
             st = ModuleState(self.layouts[k], shape, self.device, seed, master=m, capacity=cap)
+            st.wire = None
+            if world > 1 and g >= 2 and self.grad_wire == "bf16" and self.exchange != "peer":
+                st.wire = torch.empty(st.grad.numel(), dtype=torch.bfloat16, device=self.device)
             self.states[k] = st
         self.mux = Multiplexer(self.plan, rank, seed)
         self.adam = adam
@@ -707,9 +716,18 @@ class Engine:
                 if root < 0 and k not in used and k in self._dirty:  # contribute the zero of Algorithm 1
                     ops.memset(st.grad, 0)
                 self._dirty.add(k)  # receives the group's sum
-                items.append(_native.ReduceItem(group=grp, buf=st.grad.data_ptr(),
-                                                n_elems=st.grad.numel(), dtype=0, root=root))
+                if st.wire is not None:  # bf16 wire: cast, reduce the copy, widen back below
+                    ops.cast_bf16(st.grad, st.wire)
+                    items.append(_native.ReduceItem(group=grp, buf=st.wire.data_ptr(),
+                                                    n_elems=st.wire.numel(), dtype=1, root=root))
+                else:
+                    items.append(_native.ReduceItem(group=grp, buf=st.grad.data_ptr(),
+                                                    n_elems=st.grad.numel(), dtype=0, root=root))
             self.comm.reduce(items)
+            for k, _members, _root in exchange_plan(self.plan, self.rank, self._bits, only):
+                st = self.states[k]
+                if st.wire is not None:
+                    ops.widen_bf16(st.wire, st.grad)
         self.fused_update(counts, only, max_ctas)
 
     def _partitioned_exchange(self, counts, used, only, max_ctas) -> None:
@@ -730,12 +748,21 @@ class Engine:
                 ops.memset(st.grad, 0)
             self._dirty.add(k)
             grp = self.comm.by_set.get(tuple(members))
-            plan_items.append(_native.ReduceItem(group=grp, buf=st.grad.data_ptr(), n_elems=g * s,
-                                                 dtype=0, root=-1, mode=1, shard=s))
+            if st.wire is not None:  # bf16 wire: reduce-scatter the bf16 copy
+                ops.cast_bf16(st.grad, st.wire)
+                plan_items.append(_native.ReduceItem(group=grp, buf=st.wire.data_ptr(), n_elems=g * s,
+                                                     dtype=1, root=-1, mode=1, shard=s))
+            else:
+                plan_items.append(_native.ReduceItem(group=grp, buf=st.grad.data_ptr(), n_elems=g * s,
+                                                     dtype=0, root=-1, mode=1, shard=s))
             ag_items.append(_native.ReduceItem(group=grp, buf=st.weights.data_ptr(), n_elems=g * s,
                                                dtype=1, root=-1, mode=2, shard=s))
             mods.append((k, j * s, s))
         self.comm.reduce(plan_items)
+        for k, off, cnt in mods:  # widen the owned shard of a bf16 reduce-scatter
+            st = self.states[k]
+            if st.wire is not None:
+                ops.widen_bf16(st.wire[off:off + cnt], st.grad[off:off + cnt])
         shards = {k: (off, n) for k, off, n in mods}
         singles = {k for k in self.states if len(self.plan.groups[k]) < 2
                    and (only is None or k in only)}

@@ -220,6 +220,13 @@ def cast_bf16(x, y) -> None:
           "mm_cast_f32_bf16")
 
 
+def widen_bf16(x, y) -> None:
+    """y (fp32) = x (bf16), elementwise."""
+    LAUNCHES[0] += 1
+    check(lib().mm_cast_bf16_f32(x.data_ptr(), y.data_ptr(), x.numel(), stream_ptr()),
+          "mm_cast_bf16_f32")
+
+
 def attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, heads, max_q, max_k, causal,
                    d_o=None, dq=None, dk=None, dv=None, groups=None, tc_groups=None) -> AttnArgs:
     """groups: (device int32 tensor [2*n_groups], n_groups, cap) from
