@@ -58,8 +58,9 @@ constexpr int kEpiWarp0 = 2;
 constexpr int kEpiWarps = MM_GEMM_EPI_WARPS;
 constexpr int kSlices = kEpiWarps / 4;
 #ifndef MM_GEMM_EPI_BUFS128
-// single-CTA 128-wide tiles (the small, multi-tile forward / dgrad GEMMs,
-// whose epilogue warps bound the kernel): staging boxes per epilogue warp
+// single-CTA 128-wide tiles (the small forward / dgrad GEMMs): staging boxes
+// per epilogue warp.  2 measured slower in the step (3.579 vs 3.525 ms: one
+// mainloop stage fewer), so it follows MM_GEMM_EPI_BUFS
 #define MM_GEMM_EPI_BUFS128 MM_GEMM_EPI_BUFS
 #endif
 constexpr int kBiasWarp = kEpiWarp0 + kEpiWarps;  // first of the bias-gradient warps
@@ -198,8 +199,7 @@ __device__ __forceinline__ bool has_bias(const Prob& p) {
 // bv: this lane's bias value for column col0 + lane (preloaded per tile);
 // resid_done: the residual is added by the caller (parked in TMEM)
 __device__ __forceinline__ void epilogue_math(const Prob& p, int64_t row, int64_t col0,
-                                              float (&acc)[32], float bv, bool resid_done = false,
-                                              const uint32_t* aux_pre = nullptr) {
+                                              float (&acc)[32], float bv, bool resid_done = false) {
     const int ep = p.epilogue;
     if (has_bias(p)) {
 #pragma unroll
@@ -213,13 +213,7 @@ __device__ __forceinline__ void epilogue_math(const Prob& p, int64_t row, int64_
     const bool full = col0 + 32 <= p.n;
     if (ep == MM_EPI_BF16_DRELU) {
         const uint16_t* aux = reinterpret_cast<const uint16_t*>(p.aux) + row * p.ldd + col0;
-        if (aux_pre != nullptr) {  // this row's 32 mask values, loaded before the accumulator wait
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                if (bf16_to_f(aux_pre[e] & 0xffff) <= 0.f) acc[2 * e] = 0.f;
-                if (bf16_to_f(aux_pre[e] >> 16) <= 0.f) acc[2 * e + 1] = 0.f;
-            }
-        } else if (full) {
+        if (full) {
             const uint4* a4 = reinterpret_cast<const uint4*>(aux);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -622,38 +616,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc::tmem_st_wait();
                 }
             }
-            // ReLU-backward mask of this warp's rows / columns, fetched before
-            // waiting on the MMAs (the wait then hides the load; 128-wide tiles)
-            constexpr bool kAuxPre = kChunks <= 2;
-            uint32_t auxr[kAuxPre ? kChunks : 1][16];
-            const bool aux_pre = kAuxPre && P.epilogue == MM_EPI_BF16_DRELU;
-            if constexpr (kAuxPre) {
-                if (aux_pre) {
-                    const int64_t arow = int64_t(tm) * (BM * CG) + rank * BM + lane_grp * 32 + lane;
-#pragma unroll
-                    for (int c = 0; c < kChunks; ++c) {
-                        const int col0 = cbase + c * 32;
-                        if (arow < P.m && col0 + 32 <= P.n) {
-                            const uint4* a4 = reinterpret_cast<const uint4*>(
-                                reinterpret_cast<const uint16_t*>(P.aux) + arow * P.ldd + col0);
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                const uint4 w = __ldg(a4 + q);
-                                auxr[c][4 * q] = w.x; auxr[c][4 * q + 1] = w.y;
-                                auxr[c][4 * q + 2] = w.z; auxr[c][4 * q + 3] = w.w;
-                            }
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < 16; ++e) {
-                                const uint16_t* a = reinterpret_cast<const uint16_t*>(P.aux) + arow * P.ldd + col0 + 2 * e;
-                                const uint32_t lo = (arow < P.m && col0 + 2 * e < P.n) ? a[0] : 0u;
-                                const uint32_t hi = (arow < P.m && col0 + 2 * e + 1 < P.n) ? a[1] : 0u;
-                                auxr[c][e] = lo | (hi << 16);
-                            }
-                        }
-                    }
-                }
-            }
             // bias for this warp's columns, fetched before waiting on the MMAs
             float bv[kChunks];
 #pragma unroll
@@ -682,9 +644,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float f[32];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-                    const uint32_t* ap = nullptr;
-                    if constexpr (kAuxPre) ap = aux_pre ? auxr[c] : nullptr;
-                    epilogue_math(P, row, col0, f, bv[c], resid_tm, ap);
+                    epilogue_math(P, row, col0, f, bv[c], resid_tm);
                     if constexpr (C::kResidTmem) {
                         if (resid_tm) {
                             const uint32_t t_res = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) +
