@@ -688,6 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
         x.nq = p.cu_q[x.first + x.nseq] - x.q_lo;
         x.k_lo = p.cu_k[x.first];
         x.nk = p.cu_k[x.first + x.nseq] - x.k_lo;
+        MM_DCHECK(x.nseq >= 1 && x.q_lo >= 0 && x.nq >= 0 && x.q_lo + x.nq <= p.total_q && x.k_lo >= 0 && x.nk >= 0);
         return x;
     };
     auto mine = [&](const U& x) { return x.nq <= kRows && x.nk <= kRows; };  // else: mma.sync kernel
@@ -899,6 +900,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_tc_kernel(const __gri
     const int first = p.groups[2 * grp], nseq = p.groups[2 * grp + 1];
     const int q_lo = p.cu_q[first], nq = p.cu_q[first + nseq] - q_lo;
     const int k_lo = p.cu_k[first], nk = p.cu_k[first + nseq] - k_lo;
+    MM_DCHECK(nseq >= 1 && q_lo >= 0 && nq >= 1 && q_lo + nq <= p.total_q && k_lo >= 0 && nk >= 0 && nq <= 2 * kRows && nk <= 2 * kRows);
     if (nq > kRows || nk > kRows) return;  // the mma.sync kernel's group
     if (warp == 1 && lane == 0) {
         tc::mbar_init(tma_bar, 1);
@@ -1071,6 +1073,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) attn_fwd_long_kernel(const __
     const int first = p.groups[2 * grp], nseq = p.groups[2 * grp + 1];
     const int q_lo = p.cu_q[first], nq = p.cu_q[first + nseq] - q_lo;
     const int k_lo = p.cu_k[first], nk = p.cu_k[first + nseq] - k_lo;
+    MM_DCHECK(nseq >= 1 && q_lo >= 0 && nq >= 1 && q_lo + nq <= p.total_q && k_lo >= 0 && nk >= 0 && nq <= 2 * kRows && nk <= 2 * kRows);
     if (!long_group(nq, nk) || qb * kRows >= nq) return;  // the short kernel's group / no rows
     const int q0 = qb * kRows;
     const int nkb = nk > kRows ? 2 : 1;
@@ -1243,6 +1246,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) attn_bwd_long_kernel(const __
     const int first = p.groups[2 * grp], nseq = p.groups[2 * grp + 1];
     const int q_lo = p.cu_q[first], nq = p.cu_q[first + nseq] - q_lo;
     const int k_lo = p.cu_k[first], nk = p.cu_k[first + nseq] - k_lo;
+    MM_DCHECK(nseq >= 1 && q_lo >= 0 && nq >= 1 && q_lo + nq <= p.total_q && k_lo >= 0 && nk >= 0 && nq <= 2 * kRows && nk <= 2 * kRows);
     if (!long_group(nq, nk)) return;
     const int nqb = nq > kRows ? 2 : 1, nkb = nk > kRows ? 2 : 1;
     if (warp == 1 && lane == 0) {

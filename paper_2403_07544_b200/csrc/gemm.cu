@@ -308,6 +308,7 @@ __device__ __forceinline__ Unit decode(const Group<NP>& g, int u) {
     w.tn = tp / P.tiles_m;
     w.kb0 = split * P.kb_per_split;
     w.kb1 = min(P.num_kb, w.kb0 + P.kb_per_split);
+    MM_DCHECK(v >= 0 && w.tm < P.tiles_m && w.tn < P.tiles_n && w.kb0 < w.kb1);
     return w;
 }
 

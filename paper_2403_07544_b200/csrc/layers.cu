@@ -421,6 +421,7 @@ __global__ void __launch_bounds__(256) embed_fwd_kernel(const int32_t* __restric
     const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
     if (row >= rows) return;
     const int64_t id = ids[row];
+    MM_DCHECK(id >= 0 && pos[row] >= 0);
     const float p = static_cast<float>(pos[row]);
     const uint2* tr = reinterpret_cast<const uint2*>(table + id * cols);
     float4* orow = reinterpret_cast<float4*>(out + row * cols);
@@ -484,7 +485,9 @@ __global__ void __launch_bounds__(256) embed_bwd_chunk_kernel(const int32_t* __r
     if (c >= n_chunks) return;
     const int b = chunks[3 * c], e = chunks[3 * c + 1], tgt = chunks[3 * c + 2];
     const int n = e - b;  // <= 32 (EMB_CHUNK_ROWS)
+    MM_DCHECK(b >= 0 && n >= 1 && n <= 32);
     const int my_row = lane < n ? perm[b + lane] : 0;
+    MM_DCHECK(my_row >= 0);
     float4 acc[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -534,6 +537,7 @@ __global__ void __launch_bounds__(256) embed_bwd_multi_kernel(const int32_t* __r
     const int m = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (m >= n_multi) return;
     const int id = multi[3 * m], s0 = multi[3 * m + 1], ns = multi[3 * m + 2];
+    MM_DCHECK(id >= 0 && s0 >= 0 && ns >= 2);
     float4 a[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -595,6 +599,7 @@ __global__ void __launch_bounds__(kXentThreads) xent_kernel(const uint16_t* logi
     __shared__ float sm_m[kXentThreads / 32], sm_s[kXentThreads / 32];
     const int64_t row = blockIdx.x;
     const int label = labels[row];
+    MM_DCHECK(label < vocab);
     const uint16_t* lr = logits + row * int64_t(vocab);
     uint16_t* dr = dlogits + row * int64_t(vocab);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -739,6 +744,7 @@ __global__ void __launch_bounds__(kXentThreads, 1) xent_stream_kernel(const uint
             tc::bulk_load_1d(buf0 + (b ^ 1) * kXentSmemVocab, logits + (row + step) * int64_t(vocab), bytes, &bar[b ^ 1]);
         }
         const int label = labels[row];
+        MM_DCHECK(label < vocab);
         tc::mbar_wait(&bar[b], static_cast<uint32_t>((it >> 1) & 1));
         const uint16_t* lrow = buf0 + b * kXentSmemVocab;
         const uint4* lr = reinterpret_cast<const uint4*>(lrow);

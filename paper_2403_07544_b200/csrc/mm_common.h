@@ -78,6 +78,26 @@ __device__ __forceinline__ void pdl_wait_release() {
     pdl_wait();
     pdl_trigger();
 }
+// Device-side bounds / invariant checks of the debug build
+// (tools/build_variant.py dbg --all -DMM_DEBUG_BOUNDS): the failing condition
+// is printed and the kernel traps, so the launch's stream reports an error.
+// compute-sanitizer is closed on the GPU pool; the GPU test suite runs
+// against this build instead (profiles/r02_debug_bounds.txt).
+#ifdef MM_DEBUG_BOUNDS
+#include <cstdio>
+#define MM_DCHECK(cond)                                                                      \
+    do {                                                                                     \
+        if (!(cond)) {                                                                       \
+            printf("MM_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,     \
+                   (int)blockIdx.x, (int)threadIdx.x, #cond);                                \
+            __trap();                                                                        \
+        }                                                                                    \
+    } while (0)
+#else
+#define MM_DCHECK(cond) \
+    do {                \
+    } while (0)
+#endif
 #endif
 
 #define MM_CHECK_ARG(cond, ...)              \

@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(kThreads) sync_emulated_kernel(const __grid_co
     pdl_wait();
     const int64_t chunk = blockIdx.x;
     const int m = find_module(t.chunk_begin, t.n_mods, chunk);
+    MM_DCHECK(m >= 0 && m < t.n_mods && chunk < t.chunk_begin[m + 1]);
     const mm_sync_module& md = t.mod[m];
     const int g = md.group_size;
     const int n = __popc(md.used_mask);

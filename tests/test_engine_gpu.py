@@ -36,7 +36,11 @@ from paper_2403_07544_b200.plan import embedding_keys  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 TOL_BF16 = 2e-2      # loss, block-level
-TOL_MODEL = 3e-2     # whole-model gradients, L2 norm, vs the bf16-faithful oracle
+# whole-model gradients at the small test shape (d128, ~320 tokens), L2 norm,
+# vs the bf16-faithful oracle: any bf16 implementation sits at 2-6 % max-rel
+# there (tools/diag_parity.py); the 2e-2 max-relative contract is asserted at
+# the BASELINE shapes in test_parity_shapes_gpu.py
+TOL_MODEL = 3e-2
 
 
 def effective_weights(layout, master):
@@ -113,7 +117,10 @@ def test_single_rank_step_vs_oracle(cuda, accum):
 @pytest.mark.parametrize("accum", [1, 2])
 def test_config1_two_ranks_emulated(cuda, accum):
     """Config 1 (world 2) on one B200: ready counts bit-exact with the
-    reference, Algorithm-1 synced gradients within 2e-2 of the oracle."""
+    reference, Algorithm-1 synced gradients within TOL_MODEL (3e-2, relative
+    L2) of the bf16-faithful oracle at this 16-sentence shape; the 2e-2
+    max-relative contract is asserted at the BASELINE shapes
+    (test_parity_shapes_gpu.py)."""
     from paper_2403_07544_b200.cluster import EmulatedCluster
     from paper_2403_07544_b200.engine import DeviceBatch
     with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
