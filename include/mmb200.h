@@ -366,7 +366,12 @@ typedef struct {
     int32_t n_groups;
     int32_t cap;
     int32_t total_k;       /* key rows (the K / V tensors' extent, for TMA maps) */
-    int32_t flags;         /* internal: 0 */
+    int32_t flags;         /* bit 1 (2): q / k / v / lse were complete before the
+                              previous kernel on the stream started (backward:
+                              the forward pass's tensors), so the tcgen05
+                              backward may load them before griddepcontrol.wait;
+                              bit 2 (4): the same for k / v of a forward call
+                              (cross attention); bit 0 is internal */
     /* optional: the same sequences packed WITHOUT the 32-row padding
      * (mm_attention_groups with align = 1) for the tcgen05 backward, whose
      * units load one contiguous 128-row box per side; NULL = use `groups`.

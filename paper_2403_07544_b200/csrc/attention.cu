@@ -560,6 +560,7 @@ struct alignas(64) BwdParams {
     int total_q, causal;
     float scale;
     int n_groups, heads;
+    int early_qkv;  // Q / K / V may be loaded before griddepcontrol.wait (mm_attn_args.flags & 2)
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -695,7 +696,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
 
     if (warp == 0) {
         if (lane == 0) {
-            pdl_wait();
+            // the forward pass's Q / K / V can be in flight before the previous
+            // kernel (which produced dO) has finished
+            bool waited = !p.early_qkv;
+            if (waited) pdl_wait();
             int n = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
                 const U x = unit(u);
@@ -705,9 +709,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
                 tc::tma_load_2d(Qs, &p.mq, tma_bar, x.h * 64, x.q_lo);
                 tc::tma_load_2d(Ks, &p.mk, tma_bar, x.h * 64, x.k_lo);
                 tc::tma_load_2d(Vs, &p.mv, tma_bar, x.h * 64, x.k_lo);
+                if (!waited) {
+                    pdl_wait();
+                    waited = true;
+                }
                 tc::tma_load_2d(dOs, &p.mdo, tma_bar, x.h * 64, x.q_lo);
                 ++n;
             }
+            if (!waited) pdl_wait();
         }
     } else if (warp == 1) {
         int n = 0;
@@ -876,6 +885,7 @@ struct alignas(64) FwdParams {
     int64_t ldo;
     int total_q, causal;
     float scale;
+    int early_kv;  // K / V may be loaded before griddepcontrol.wait (mm_attn_args.flags & 4)
 };
 
 __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_tc_kernel(const __grid_constant__ FwdParams p) {
@@ -917,11 +927,12 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_tc_kernel(const __gri
 
     if (warp == 0) {
         if (lane == 0) {
-            pdl_wait();
+            if (!p.early_kv) pdl_wait();
             tc::mbar_expect_tx(tma_bar, 3 * kTile);
-            tc::tma_load_2d(Qs, &p.mq, tma_bar, h * 64, q_lo);
             tc::tma_load_2d(Ks, &p.mk, tma_bar, h * 64, k_lo);
             tc::tma_load_2d(Vs, &p.mv, tma_bar, h * 64, k_lo);
+            if (p.early_kv) pdl_wait();  // (cross attention: only Q is the previous kernel's)
+            tc::tma_load_2d(Qs, &p.mq, tma_bar, h * 64, q_lo);
         }
     } else if (warp == 1) {
         tc::mbar_wait(tma_bar, 0);
@@ -1550,6 +1561,7 @@ extern "C" int mm_attention_fwd(const mm_attn_args* a, void* stream) {
         fp.cu_q = a->cu_q; fp.cu_k = a->cu_k; fp.groups = tcg ? a->tc_groups : a->groups; fp.lse = a->lse;
         fp.o = a->o; fp.ldo = a->ldo;
         fp.total_q = a->total_q; fp.causal = a->causal; fp.scale = a->scale;
+        fp.early_kv = (a->flags & 4) != 0;
         static bool attr = false;
         if (!attr) {
             MM_CUDA_TRY(cudaFuncSetAttribute(tca::attn_fwd_tc_kernel,
@@ -1607,6 +1619,7 @@ extern "C" int mm_attention_bwd(const mm_attn_args* a, void* stream) {
         bp.ld_dq = a->ld_dq; bp.ld_dk = a->ld_dk; bp.ld_dv = a->ld_dv;
         bp.total_q = a->total_q; bp.causal = a->causal; bp.scale = a->scale;
         bp.n_groups = tcg ? a->n_tc_groups : a->n_groups; bp.heads = a->heads;
+        bp.early_qkv = (a->flags & 2) != 0;
         static bool attr = false;
         if (!attr) {
             MM_CUDA_TRY(cudaFuncSetAttribute(tca::attn_bwd_tc_kernel,

@@ -285,6 +285,7 @@ struct Driver {
         mm_attn_args a = attn(sv.q, sv.kv, sv.kv + d, d, 2 * d, sv.a, sv.lse, b.cu_tgt, b.cu_src,
                               b.max_tgt, b.max_src, false, int(T), b.groups_cross, b.ng_cross,
                               b.cap_cross, b.tcg_cross, b.ntc_cross);
+        a.flags |= 4;  // K / V: the grouped projection of the encoder memory, launched before
         TIMED(2, mm_attention_fwd(&a, s));
         out = ar.get<float>(T * d);
         if (int e = residual(sv.a, wb(st, o->cout_w), out, T, d, wf(st, o->cout_b), x, next, ln_out)) return e;
@@ -340,6 +341,7 @@ struct Driver {
                               maxlen, maxlen, causal, int(T), groups, ng, cap, tcg, ntc);
         a.d_o = da; a.dq = dqkv; a.dk = dqkv + d; a.dv = dqkv + 2 * d;
         a.ld_dq = a.ld_dk = a.ld_dv = 3 * d;
+        a.flags |= 2;  // Q / K / V / lse come from the forward pass
         TIMED(3, mm_attention_bwd(&a, s));
         TRY(wgrad(dqkv, sv.h, g(st, o->qkv_w), T, d, 3 * d, g(st, o->qkv_b)));
         float* dh = ar.get<float>(T * d);
@@ -368,6 +370,7 @@ struct Driver {
                               b.cap_cross, b.tcg_cross, b.ntc_cross);
         a.d_o = da; a.dq = dq; a.dk = dkv; a.dv = dkv + d;
         a.ld_dq = d; a.ld_dk = a.ld_dv = 2 * d;
+        a.flags |= 2;  // Q / K / V / lse come from the forward pass
         TIMED(3, mm_attention_bwd(&a, s));
         TRY(wgrad(dkv, mem, g(st, o->ckv_w), S, d, 2 * d, g(st, o->ckv_b)));
         TRY(wgrad(dq, sv.h, g(st, o->cq_w), T, d, d, g(st, o->cq_b)));
