@@ -57,6 +57,12 @@ constexpr int kEpiWarp0 = 2;
 // two slices each take half of the tile's columns
 constexpr int kEpiWarps = MM_GEMM_EPI_WARPS;
 constexpr int kSlices = kEpiWarps / 4;
+#ifndef MM_GEMM_BN64
+// 64-wide single-CTA tiles (diagnostics build: MM_GEMM_OVERRIDE "...=1:64"):
+// twice the tiles of a narrow GEMM, so a CTA's first epilogue overlaps its
+// second tile's mainloop
+#define MM_GEMM_BN64 0
+#endif
 #ifndef MM_GEMM_EPI_BUFS128
 // single-CTA 128-wide tiles (the small forward / dgrad GEMMs): staging boxes
 // per epilogue warp.  2 measured slower in the step (3.579 vs 3.525 ms: one
@@ -95,7 +101,7 @@ struct Cfg {
     static constexpr int kStages = kStagesFit > MM_GEMM_MAX_STAGES ? MM_GEMM_MAX_STAGES : kStagesFit;
     // 2 accumulators (power of 2); a single-CTA 128-wide tile also parks the
     // tile's fp32 residual in columns 256..383 (loaded while the MMAs run)
-    static constexpr bool kResidTmem = BN == 128 && CG == 1 && CN == 1;
+    static constexpr bool kResidTmem = BN <= 128 && CG == 1 && CN == 1;
     static constexpr int kTmemCols = 512;
     static constexpr uint32_t kResidCol = 2 * BN;
     static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 + kBarBytes + kLnBytes;
@@ -979,7 +985,8 @@ TileChoice choose_tile(const mm_gemm_args* const* probs, int n, int sms) {
             long on = 0, ok = 0, ob = 0, ocg = 0, obn = 0;
             if (std::sscanf(q, "%ld,%ld,%ld=%ld:%ld", &on, &ok, &ob, &ocg, &obn) == 5 &&
                 on == probs[0]->n && ok == probs[0]->k && ob == (probs[0]->b_kmajor ? 0 : 1) &&
-                (ocg == 1 || ocg == 2) && (obn == 128 || obn == 192 || obn == 256)) {
+                (ocg == 1 || ocg == 2) && (obn == 128 || obn == 192 || obn == 256 ||
+                                           (MM_GEMM_BN64 && obn == 64 && ocg == 1))) {
                 best = {static_cast<int>(obn), static_cast<int>(ocg)};
                 break;
             }
@@ -1121,6 +1128,9 @@ int run_group(const mm_gemm_args* const* probs, int n, cudaStream_t s) {
     } else {
         if (bn == 256) rc = dispatch<256, NP, 1>(a_mn, b_mn, g, s);
         else if (bn == 192) rc = dispatch<192, NP, 1>(a_mn, b_mn, g, s);
+#if MM_GEMM_BN64
+        else if (bn == 64 && NP == 1) rc = dispatch<64, NP, 1>(a_mn, b_mn, g, s);
+#endif
         else rc = dispatch<128, NP, 1>(a_mn, b_mn, g, s);
     }
     return rc;
