@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 21
+#define MMB200_ABI_VERSION 22
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 /* emulated devices of one sync (mm_sync_emulated): the reference's multi-node
  * scaling harness reaches 20 devices per group (syncsim.py:461-483) */
@@ -271,6 +271,11 @@ typedef struct {
     float* ln_mean;     /* [M] */
     float* ln_rstd;     /* [M] */
     float ln_eps;
+    /* optional 1-bit ReLU mask, [M, ceil(N / 32)] uint32 words, bit j of word
+     * (r, c) = column 32c + j: written by MM_EPI_BF16_RELU (bit = the bf16
+     * output is non-zero), read by MM_EPI_BF16_DRELU instead of `aux` (16x
+     * fewer bytes than the bf16 activation) */
+    uint32_t* relu_mask;
 } mm_gemm_args;
 
 int mm_gemm(const mm_gemm_args* args, void* stream);

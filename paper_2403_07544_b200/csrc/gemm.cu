@@ -120,6 +120,8 @@ struct alignas(64) Prob {
     const float* bias;
     const float* resid;
     const __nv_bfloat16* aux;
+    uint32_t* relu_mask;  // [m, mask_ld] 1-bit ReLU mask (written by RELU, read by DRELU)
+    int64_t mask_ld;
     float* dbias;
     int epilogue;
     int tiles_m, tiles_n, splits, kb_per_split, num_kb;
@@ -219,7 +221,12 @@ __device__ __forceinline__ void epilogue_math(const Prob& p, int64_t row, int64_
     const bool full = col0 + 32 <= p.n;
     if (ep == MM_EPI_BF16_DRELU) {
         const uint16_t* aux = reinterpret_cast<const uint16_t*>(p.aux) + row * p.ldd + col0;
-        if (full) {
+        if (p.relu_mask) {  // one word per row and 32 columns
+            const uint32_t bits = p.relu_mask[row * p.mask_ld + (col0 >> 5)];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (!((bits >> j) & 1u)) acc[j] = 0.f;
+        } else if (full) {
             const uint4* a4 = reinterpret_cast<const uint4*>(aux);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -652,6 +659,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
                     epilogue_math(P, row, col0, f, bv[c], resid_tm);
+                    if (P.epilogue == MM_EPI_BF16_RELU && P.relu_mask && row < P.m) {
+                        uint32_t bits = 0;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const __nv_bfloat16 h = __float2bfloat16_rn(f[j]);
+                            if (col0 + j < P.n && *reinterpret_cast<const uint16_t*>(&h) != 0) bits |= 1u << j;
+                        }
+                        P.relu_mask[row * P.mask_ld + (col0 >> 5)] = bits;
+                    }
                     if constexpr (C::kResidTmem) {
                         if (resid_tm) {
                             const uint32_t t_res = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) +
@@ -908,7 +924,9 @@ int check_args(const mm_gemm_args* a) {
                  "D must be 16-byte aligned with 16-byte row stride");
     MM_CHECK_ARG((a->epilogue != MM_EPI_F32_RESID && a->epilogue != MM_EPI_F32_RESID_LN) || a->resid,
                  "RESID epilogue needs resid");
-    MM_CHECK_ARG(a->epilogue != MM_EPI_BF16_DRELU || a->aux, "DRELU epilogue needs aux");
+    MM_CHECK_ARG(a->epilogue != MM_EPI_BF16_DRELU || a->aux || a->relu_mask, "DRELU epilogue needs aux or relu_mask");
+    MM_CHECK_ARG(!a->relu_mask || a->epilogue == MM_EPI_BF16_RELU || a->epilogue == MM_EPI_BF16_DRELU,
+                 "relu_mask is for the RELU / DRELU epilogues");
     MM_CHECK_ARG(a->dbias == nullptr || !a->a_kmajor, "dbias needs an MN-major A operand");
     MM_CHECK_ARG(a->m < (int64_t(1) << 31) && a->n < (int64_t(1) << 31) && a->k < (int64_t(1) << 31),
                  "GEMM dimension >= 2^31");
@@ -1035,6 +1053,8 @@ int setup_prob(Prob& P, const mm_gemm_args* a, int bn, int cg, int splits_cap) {
     P.m = a->m; P.n = a->n; P.k = a->k; P.ldd = a->ldd;
     P.d = a->d; P.bias = a->bias; P.resid = a->resid;
     P.aux = reinterpret_cast<const __nv_bfloat16*>(a->aux);
+    P.relu_mask = a->relu_mask;
+    P.mask_ld = (a->n + 31) / 32;
     P.dbias = a->dbias;
     P.epilogue = a->epilogue;
     P.tiles_m = static_cast<int>(tiles_m);

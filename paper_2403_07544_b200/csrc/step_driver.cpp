@@ -89,7 +89,16 @@ struct Arena {
 
 struct SelfSave { const float* x_in; uint16_t* h; float* mean; float* rstd; uint16_t* qkv; uint16_t* a; float* lse; };
 struct CrossSave { const float* x_in; uint16_t* h; float* mean; float* rstd; uint16_t* q; uint16_t* kv; uint16_t* a; float* lse; };
-struct FfnSave { const float* x_in; uint16_t* h; float* mean; float* rstd; uint16_t* f; };
+// MM_RELU_MASK=0: the ReLU-backward epilogue reads the bf16 activation (A/B)
+static bool use_relu_mask() {
+    static const bool on = [] {
+        const char* e = std::getenv("MM_RELU_MASK");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+struct FfnSave { const float* x_in; uint16_t* h; float* mean; float* rstd; uint16_t* f; uint32_t* mask; };
 
 // A LayerNorm's outputs (bf16 normalised rows + per-row statistics), and the
 // parameters of the LayerNorm that follows a residual GEMM
@@ -300,7 +309,13 @@ struct Driver {
         sv.x_in = x;
         if (int e = ln_in(st, o->ln2_g, o->ln2_b, x, T, pre, sv.h, sv.mean, sv.rstd)) return e;
         sv.f = ar.get<uint16_t>(T * F);
-        TRY(linear(sv.h, wb(st, o->ff1_w), sv.f, T, d, F, MM_EPI_BF16_RELU, wf(st, o->ff1_b)));
+        sv.mask = ar.get<uint32_t>(T * ((F + 31) / 32));  // 1-bit ReLU mask for the backward
+        {
+            mm_gemm_args a = make_args(sv.h, true, wb(st, o->ff1_w), true, sv.f, T, F, d, d, d, F,
+                                       MM_EPI_BF16_RELU, wf(st, o->ff1_b));
+            a.relu_mask = use_relu_mask() ? sv.mask : nullptr;
+            TRY(mm_gemm(&a, s));
+        }
         out = ar.get<float>(T * d);
         if (int e = residual(sv.f, wb(st, o->ff2_w), out, T, F, wf(st, o->ff2_b), x, next, ln_out)) return e;
         return 0;
@@ -315,7 +330,12 @@ struct Driver {
         const size_t mark = ar.off;
         TRY(wgrad(dx_bf, sv.f, g(st, o->ff2_w), T, F, d, g(st, o->ff2_b)));
         uint16_t* df = ar.get<uint16_t>(T * F);
-        TRY(dgrad(dx_bf, wb(st, o->ff2_w), df, T, F, d, MM_EPI_BF16_DRELU, sv.f));
+        {
+            mm_gemm_args a = make_args(dx_bf, true, wb(st, o->ff2_w), false, df, T, F, d, d, F, F,
+                                       MM_EPI_BF16_DRELU, nullptr, nullptr, sv.f);
+            a.relu_mask = use_relu_mask() ? sv.mask : nullptr;  // 1 bit per element instead of the bf16 activation
+            TRY(mm_gemm(&a, s));
+        }
         TRY(wgrad(df, sv.h, g(st, o->ff1_w), T, d, F, g(st, o->ff1_b)));
         float* dh = ar.get<float>(T * d);
         TRY(dgrad(df, wb(st, o->ff1_w), dh, T, d, F, MM_EPI_F32));

@@ -30,6 +30,7 @@ class GemmArgs(ctypes.Structure):
         ("dbias", ctypes.c_void_p),
         ("ln_gamma", ctypes.c_void_p), ("ln_beta", ctypes.c_void_p), ("ln_out", ctypes.c_void_p),
         ("ln_mean", ctypes.c_void_p), ("ln_rstd", ctypes.c_void_p), ("ln_eps", ctypes.c_float),
+        ("relu_mask", ctypes.c_void_p),
     ]
 
 
@@ -80,7 +81,7 @@ def _rowstride(t: torch.Tensor, name: str) -> int:
 
 def gemm_args(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bool = True,
               b_kmajor: bool = True, epilogue: int = EPI_BF16, bias=None, resid=None, aux=None,
-              dbias=None, ln=None) -> GemmArgs:
+              dbias=None, ln=None, relu_mask=None) -> GemmArgs:
     """Validated mm_gemm_args for d[M,N] (epilogue)= op(a) @ op(b)^T."""
     _need(a, torch.bfloat16, "a")
     _need(b, torch.bfloat16, "b")
@@ -109,19 +110,26 @@ def gemm_args(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bo
         raise ValueError("resid must share d's row stride")
     if aux is not None and _rowstride(aux, "aux") != args.ldd:
         raise ValueError("aux must share d's row stride")
+    if relu_mask is not None:
+        _need(relu_mask, torch.int32, "relu_mask")
+        if relu_mask.numel() < m * ((n + 31) // 32) or not relu_mask.is_contiguous():
+            raise ValueError("relu_mask must be a contiguous [M, ceil(N/32)] int32 tensor")
+        args.relu_mask = relu_mask.data_ptr()
     args.b_prefetch = 0
     return args
 
 
 def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bool = True,
          b_kmajor: bool = True, epilogue: int = EPI_BF16, bias=None, resid=None, aux=None,
-         dbias=None, ln=None) -> None:
+         dbias=None, ln=None, relu_mask=None) -> None:
     """d[M,N] (epilogue)= op(a) @ op(b)^T on tcgen05.
 
     a: [M,K] if a_kmajor else [K,M]; b: [N,K] if b_kmajor else [K,N] (bf16).
+    relu_mask (int32 [M, ceil(N/32)]): written by EPI_BF16_RELU, read by
+    EPI_BF16_DRELU in place of aux.
     """
     args = gemm_args(a, b, d, a_kmajor=a_kmajor, b_kmajor=b_kmajor, epilogue=epilogue,
-                     bias=bias, resid=resid, aux=aux, dbias=dbias, ln=ln)
+                     bias=bias, resid=resid, aux=aux, dbias=dbias, ln=ln, relu_mask=relu_mask)
     m, n, k = args.m, args.n, args.k
     LAUNCHES[0] += 1
     if GEMM_PROFILE is not None:

@@ -75,6 +75,36 @@ def test_gemm_epilogues(cuda, tile, shape):
     assert rel_err(d, (ref - bias) * (aux.float() > 0)) < 1e-2
 
 
+@pytest.mark.parametrize("shape", [(4096, 2048, 512), (333, 1536, 512), (300, 200, 136)])
+def test_gemm_relu_bitmask(cuda, tile, shape):
+    """The 1-bit ReLU mask: EPI_BF16_RELU writes bit j of word (r, c) = the
+    bf16 output (r, 32c + j) is non-zero; EPI_BF16_DRELU reading the mask is
+    bit-identical to reading the bf16 activation (aux)."""
+    from paper_2403_07544_b200 import ops
+    m, n, k = shape
+    g = torch.Generator(device="cuda").manual_seed(n + k)
+    A = torch.randn(m, k, device=cuda, generator=g).bfloat16()
+    B = (torch.randn(n, k, device=cuda, generator=g) / math.sqrt(k)).bfloat16()
+    bias = torch.randn(n, device=cuda, generator=g)
+    f = torch.empty(m, n, device=cuda, dtype=torch.bfloat16)
+    words = (n + 31) // 32
+    mask = torch.full((m, words), -1, device=cuda, dtype=torch.int32)
+    ops.gemm(A, B, f, epilogue=ops.EPI_BF16_RELU, bias=bias, relu_mask=mask)
+    nz = torch.zeros(m, words * 32, dtype=torch.int64)
+    nz[:, :n] = (f.cpu().view(torch.int16) != 0).long()
+    want = (nz.view(m, words, 32) << torch.arange(32)).sum(-1)
+    got = mask.cpu().long() & 0xFFFFFFFF
+    assert torch.equal(got, want)
+    dY = torch.randn(m, k, device=cuda, generator=g).bfloat16()
+    W = torch.randn(k, n, device=cuda, generator=g).bfloat16()  # dX = dY W, B MN-major
+    d1 = torch.empty(m, n, device=cuda, dtype=torch.bfloat16)
+    d2 = torch.empty_like(d1)
+    ops.gemm(dY, W, d1, b_kmajor=False, epilogue=ops.EPI_BF16_DRELU, aux=f)
+    ops.gemm(dY, W, d2, b_kmajor=False, epilogue=ops.EPI_BF16_DRELU, relu_mask=mask)
+    assert torch.equal(d1, d2)
+    assert rel_err(d1, (dY.float() @ W.float()) * (f.float() > 0)) < 1e-2
+
+
 @pytest.mark.parametrize("shape", [(4096, 512, 512), (333, 512, 2048), (4100, 1024, 1024), (128, 512, 64)])
 def test_gemm_fused_layernorm(cuda, shape):
     """MM_EPI_F32_RESID_LN: x = resid + A B^T + bias (fp32) and the following
