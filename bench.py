@@ -67,11 +67,32 @@ def gemm_traffic(config: str):
             "source": os.path.relpath(path, ROOT)}
 
 
+def _nvml_poll(index: int, conn, period: float) -> None:
+    """Child process of ClockSampler: (time, SM MHz, max MHz, reason mask)
+    every `period` s until told to stop (no GIL shared with the benchmark)."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+    except Exception:  # noqa: BLE001  (no NVML here: the parent falls back)
+        conn.send("fail")
+        return
+    rows = []
+    conn.send("ready")
+    while not conn.poll(period):
+        rows.append((time.time(), pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), mx,
+                     pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+    conn.recv()
+    conn.send(rows)
+
+
 class ClockSampler:
-    """SM clocks and clock-event (throttle) reasons sampled during the timed
-    region: NVML polled every 5 ms from a host thread (the timed region of a
-    default run is ~0.1 s, shorter than nvidia-smi's start-up), with
-    `nvidia-smi -lms 100` as the fallback when NVML is unavailable."""
+    """SM clocks and clock-event (throttle) reasons during the timed region:
+    an NVML polling process (every 5 ms, started before the warm-up so it is
+    sampling when the timed region begins; `mark()` brackets the region and
+    only samples inside it count), with `nvidia-smi -lms 100` as the
+    fallback when NVML is unavailable."""
 
     REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
                ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
@@ -83,62 +104,86 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.thread = None
+        self.proc = self.child = None
         self.rows = []  # (sm_mhz, max_mhz, reasons)
+        self.window = None
+        self.source = None
+        self.started = False
 
-    def __enter__(self):
+    def start(self):
+        self.started = True
         try:
-            import threading
-            import pynvml
-            pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-            masks = [(name, getattr(pynvml, attr)) for name, attr in self.REASONS]
-            self.stop = threading.Event()
-
-            def poll():
-                while True:
-                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    self.rows.append((float(sm), float(mx), [n for n, m in masks if r & m]))
-                    if self.stop.wait(0.005):
-                        break
-
-            self.thread = threading.Thread(target=poll, daemon=True)
-            self.thread.start()
-            return self
-        except Exception:  # noqa: BLE001  (no NVML: nvidia-smi)
-            self.thread = None
+            import multiprocessing as mp
+            import pynvml  # noqa: F401
+            ctx = mp.get_context("spawn")
+            self.conn, child_conn = ctx.Pipe()
+            self.child = ctx.Process(target=_nvml_poll, args=(self.index, child_conn, 0.005), daemon=True)
+            self.child.start()
+            deadline = time.time() + 60
+            while self.child.is_alive() and time.time() < deadline:
+                if self.conn.poll(0.05):
+                    if self.conn.recv() == "ready":
+                        self.source = "nvml"
+                        return self
+                    break
+            self.child.terminate()
+        except Exception:  # noqa: BLE001
+            pass
+        self.child = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.source = "nvidia-smi"
         except OSError:
             self.proc = None
         return self
 
+    def mark(self, begin: bool) -> None:
+        if begin:
+            self.window = [time.time(), None]
+        elif self.window:
+            self.window[1] = time.time()
+
+    def __enter__(self):
+        if not self.started:
+            self.start()
+        self.mark(True)
+        return self
+
     def __exit__(self, *exc):
-        if self.thread is not None:
-            self.stop.set()
-            self.thread.join(2)
-            return False
+        self.mark(False)
+        self.stop()
+        return False
+
+    def stop(self) -> None:
+        if self.child is not None:
+            self.conn.send("stop")
+            raw = self.conn.recv() if self.conn.poll(10) else []
+            self.child.join(5)
+            self.child = None
+            import pynvml
+            masks = [(name, getattr(pynvml, attr)) for name, attr in self.REASONS]
+            lo, hi = self.window or (0, float("inf"))
+            self.rows = [(float(sm), float(mx), [n for n, m in masks if r & m])
+                         for t, sm, mx, r in raw if lo <= t <= (hi or float("inf"))]
+            return
         if self.proc is None:
-            return False
+            return
         self.proc.terminate()
         try:
             out, _ = self.proc.communicate(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
             out, _ = self.proc.communicate()
+        self.proc = None
         names = [n for n, _ in self.REASONS]
         for line in out.strip().splitlines():
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 8 and parts[1].replace(".", "").isdigit():
                 self.rows.append((float(parts[1]), float(parts[2]),
                                   [names[i] for i in range(4) if parts[4 + i] == "Active"]))
-        return False
 
     def summary(self):
         if not self.rows:
@@ -146,7 +191,7 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(r[0] for r in self.rows),
                 "sm_max_mhz": max(r[1] for r in self.rows),
                 "reasons": sorted({n for r in self.rows for n in r[2]}), "samples": len(self.rows),
-                "source": "nvml" if self.thread is not None else "nvidia-smi"}
+                "source": self.source}
 
 
 def dist_env():
@@ -507,12 +552,13 @@ def run_train(args, pk):
         torch.cuda.synchronize()
 
     # ---- device-resident inputs (value)
+    clk = ClockSampler(local).start()  # sampling before the timed region begins
     for s in range(args.warmup):
         eng.step(s, [dbs[s]])
     barrier()
     launches0 = _native.lib().mm_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with clk:
         e0.record()
         for s in range(args.warmup, n_total):
             eng.step(s, [dbs[s]])

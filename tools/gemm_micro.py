@@ -1,4 +1,8 @@
-"""Back-to-back GEMM timing per shape (CUDA events), for kernel tuning."""
+"""Back-to-back GEMM timing per shape (CUDA graph of 20 launches, CUDA
+events), ours vs cuBLAS (torch.mm, bf16 in / bf16 out).  Our epilogue is the
+one the step uses for that shape: bf16 out (EPI_BF16*), fp32 out (EPI_F32:
+twice cuBLAS's output bytes) or an fp32 TMA reduce-add (EPI_F32_ACCUM: read +
+write of an fp32 output) -- the "out" column says which."""
 import os, sys
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -67,7 +71,8 @@ for name, m, n, k, ak, bk, epi in cases:
         return e0.elapsed_time(e1) * 1e3 / (5 * n_it)
     uc = timeit(runc)
     ref = (At.float() @ Bt.float())
-    line = f"{name:10s} {m:6d}x{n:6d}x{k:6d} cublas {uc:7.2f}us {2*m*n*k/uc/1e6:7.1f}TF |"
+    outk = {ops.EPI_F32: "f32", ops.EPI_F32_ACCUM: "f32+=", ops.EPI_F32_RESID: "f32+res"}.get(epi, "bf16")
+    line = f"{name:10s} {m:6d}x{n:6d}x{k:6d} out {outk:6s} cublas {uc:7.2f}us {2*m*n*k/uc/1e6:7.1f}TF |"
     for var in VARIANTS:
         for key in ("MM_GEMM_CG", "MM_GEMM_BN"):
             os.environ.pop(key, None)
