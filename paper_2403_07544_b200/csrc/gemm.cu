@@ -63,6 +63,10 @@ constexpr int kSlices = kEpiWarps / 4;
 // second tile's mainloop
 #define MM_GEMM_BN64 0
 #endif
+#ifndef MM_GEMM_EPI_BUFS256P
+// CTA-pair 256-wide tiles (generator, grouped weight gradients)
+#define MM_GEMM_EPI_BUFS256P MM_GEMM_EPI_BUFS
+#endif
 #ifndef MM_GEMM_EPI_BUFS128
 // single-CTA 128-wide tiles (the small forward / dgrad GEMMs): staging boxes
 // per epilogue warp.  2 measured slower in the step (3.579 vs 3.525 ms: one
@@ -86,7 +90,9 @@ constexpr int kSmemLimit = 232448;
 // per-SM shared-memory traffic per MMA drops by a quarter (BN=128) to a half.
 template <int BN, int CG, int CN = 1>
 struct Cfg {
-    static constexpr int kEpiBufs = (BN == 128 && CG == 1 && CN == 1) ? MM_GEMM_EPI_BUFS128 : MM_GEMM_EPI_BUFS;
+    static constexpr int kEpiBufs = (BN == 128 && CG == 1 && CN == 1) ? MM_GEMM_EPI_BUFS128
+                                    : (BN == 256 && CG == 2) ? MM_GEMM_EPI_BUFS256P
+                                                             : MM_GEMM_EPI_BUFS;
     static constexpr int kEpiSmem = kEpiWarps * kEpiBufs * kEpiBufBytes;
     static constexpr int kBRows = BN / CG;             // B rows (N) staged by one CTA
     static constexpr int kABytes = BM * BK * 2;
