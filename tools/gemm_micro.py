@@ -25,6 +25,16 @@ cases = [  # name, m, n, k, a_k, b_k, epi
     ("wgrad ff1", 2048, 512, T, False, False, ops.EPI_F32_ACCUM),
     ("wgrad ff2", 512, 2048, T, False, False, ops.EPI_F32_ACCUM),
     ("wgrad gen", 32000, 512, T, False, False, ops.EPI_F32_ACCUM),
+    # config 5 (d 1024, ffn 4096, 16384 tokens)
+    ("c5 fwd qkv", 16384, 3072, 1024, True, True, ops.EPI_BF16),
+    ("c5 fwd ff1", 16384, 4096, 1024, True, True, ops.EPI_BF16_RELU),
+    ("c5 fwd ff2", 16384, 1024, 4096, True, True, ops.EPI_F32),
+    ("c5 fwd out", 16384, 1024, 1024, True, True, ops.EPI_F32),
+    ("c5 dgrad ff1", 16384, 1024, 4096, True, False, ops.EPI_F32),
+    ("c5 dgrad ff2", 16384, 4096, 1024, True, False, ops.EPI_BF16),
+    ("c5 wgrad ff1", 4096, 1024, 16384, False, False, ops.EPI_F32_ACCUM),
+    ("c5 wgrad qkv", 3072, 1024, 16384, False, False, ops.EPI_F32_ACCUM),
+    ("c5 fwd gen", 16384, 32000, 1024, True, True, ops.EPI_BF16),
     ("tiny", 128, 128, 64, True, True, ops.EPI_F32),
     ("big", 8192, 8192, 8192, True, True, ops.EPI_BF16),
     ("maj kk", 2048, 512, 4096, True, True, ops.EPI_F32),
