@@ -131,6 +131,7 @@ struct alignas(64) Prob {
     float* dbias;
     int epilogue;
     int tiles_m, tiles_n, splits, kb_per_split, num_kb;
+    int group_m;  // unit order: M-tiles walked in groups of group_m (L2 reuse of A)
     int unit_begin;
 };
 
@@ -323,8 +324,18 @@ __device__ __forceinline__ Unit decode(const Group<NP>& g, int u) {
     const int tp = v / P.splits, split = v - tp * P.splits;
     Unit w;
     w.pi = pi;
-    w.tm = tp % P.tiles_m;
-    w.tn = tp / P.tiles_m;
+    if (P.group_m >= P.tiles_m) {  // A fits the L2 budget: M fastest over every M-tile
+        w.tm = tp % P.tiles_m;
+        w.tn = tp / P.tiles_m;
+    } else {  // groups of group_m M-tiles, N-tiles within a group, M fastest inside
+        const int per = P.group_m * P.tiles_n;
+        const int grp = tp / per;
+        const int first = grp * P.group_m;
+        const int gm = min(P.group_m, P.tiles_m - first);
+        const int r = tp - grp * per;
+        w.tm = first + r % gm;
+        w.tn = r / gm;
+    }
     w.kb0 = split * P.kb_per_split;
     w.kb1 = min(P.num_kb, w.kb0 + P.kb_per_split);
     MM_DCHECK(v >= 0 && w.tm < P.tiles_m && w.tn < P.tiles_n && w.kb0 < w.kb1);
@@ -1068,6 +1079,16 @@ int setup_prob(Prob& P, const mm_gemm_args* a, int bn, int cg, int splits_cap) {
     P.splits = splits;
     P.kb_per_split = kb_per;
     P.num_kb = num_kb;
+    // Consecutive units run at the same time on the persistent CTAs.  Walking
+    // M first over every M-tile re-streams A from HBM for each N-tile once A
+    // outgrows the L2 (8192^3: 2.3x cuBLAS's DRAM traffic, lower clocks under
+    // the power cap); group the M-tiles so one group's A slices stay resident.
+    const char* env_budget = std::getenv("MM_GEMM_L2_GROUP_MB");  // diagnostics / tests (0: off)
+    const double budget = (env_budget ? std::atof(env_budget) : 48.0) * 1e6;
+    const double a_slice = double(BM * cg) * double(a->k) * 2.0;  // bytes of A per M-tile
+    P.group_m = static_cast<int>(tiles_m);
+    if (budget > 0 && a_slice * double(tiles_m) > budget)
+        P.group_m = std::max(1, static_cast<int>(budget / a_slice));
     return 0;
 }
 

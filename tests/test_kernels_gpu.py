@@ -48,6 +48,27 @@ def test_gemm_majors_f32(cuda, tile, shape, a_k, b_k):
     assert rel_err(d, ref) < 2e-3
 
 
+@pytest.mark.parametrize("budget_mb", ["0.25", "1", "0"])
+@pytest.mark.parametrize("shape", [(1000, 2048, 512), (4096, 1536, 1024), (512, 512, 4096)])
+def test_gemm_grouped_unit_order(cuda, tile, shape, budget_mb, monkeypatch):
+    """The L2-grouped unit order (M-tiles walked in groups when A outgrows
+    the budget; small budgets force it at test sizes, including a partial
+    last group) computes the same product as the plain M-first order."""
+    from paper_2403_07544_b200 import ops
+    m, n, k = shape
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    A = torch.randn(m, k, device=cuda, generator=g).bfloat16()
+    B = torch.randn(n, k, device=cuda, generator=g).bfloat16()
+    d = torch.empty(m, n, device=cuda, dtype=torch.float32)
+    monkeypatch.setenv("MM_GEMM_L2_GROUP_MB", budget_mb)
+    ops.gemm(A, B, d, epilogue=ops.EPI_F32)
+    monkeypatch.setenv("MM_GEMM_L2_GROUP_MB", "0")
+    d0 = torch.empty_like(d)
+    ops.gemm(A, B, d0, epilogue=ops.EPI_F32)
+    assert torch.equal(d, d0)
+    assert rel_err(d, A.float() @ B.float().t()) < 2e-3
+
+
 @pytest.mark.parametrize("shape", [(4096, 512, 512), (333, 1536, 512), (4096, 2048, 512)])
 def test_gemm_epilogues(cuda, tile, shape):
     from paper_2403_07544_b200 import ops
