@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 22
+#define MMB200_ABI_VERSION 23
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 /* emulated devices of one sync (mm_sync_emulated): the reference's multi-node
  * scaling harness reaches 20 devices per group (syncsim.py:461-483) */
@@ -422,6 +422,11 @@ typedef struct {
     int32_t n_layers;
     int32_t decoder;
     int64_t lnf_g, lnf_b;   /* final LayerNorm, -1 if absent */
+    int32_t store_wgrad;    /* 1: the weight-matrix gradients are STORED (this
+                               micro-batch is the module's first of the step;
+                               the caller zeroed only the rest of the bucket),
+                               0: reduce-added onto the bucket */
+    int32_t pad_;
 } mm_stack;
 
 typedef struct {
@@ -429,6 +434,8 @@ typedef struct {
     const float* w_f32;
     float* grad;
     int64_t emb, gen_w, gen_b; /* gen_* only for the decoder-side module */
+    int32_t store_gen_w;       /* as mm_stack.store_wgrad, for the generator matrix */
+    int32_t pad_;
 } mm_embed;
 
 typedef struct {

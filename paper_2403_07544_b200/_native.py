@@ -19,7 +19,7 @@ if os.environ.get("MM_LIB_VARIANT"):  # diagnostics: a tuning build from tools/b
                             "libmmb200.so")
 
 #: must match MMB200_ABI_VERSION in include/mmb200.h
-ABI_VERSION = 22
+ABI_VERSION = 23
 MAX_GROUP = 8
 MAX_SYNC_GROUP = 32
 
@@ -201,12 +201,13 @@ class LayerOffsets(ctypes.Structure):
 class Stack(ctypes.Structure):
     _fields_ = [("w_bf16", c_void_p), ("w_f32", c_void_p), ("grad", c_void_p),
                 ("layers", POINTER(LayerOffsets)), ("n_layers", c_int32), ("decoder", c_int32),
-                ("lnf_g", c_int64), ("lnf_b", c_int64)]
+                ("lnf_g", c_int64), ("lnf_b", c_int64), ("store_wgrad", c_int32), ("pad_", c_int32)]
 
 
 class Embed(ctypes.Structure):
     _fields_ = [("w_bf16", c_void_p), ("w_f32", c_void_p), ("grad", c_void_p),
-                ("emb", c_int64), ("gen_w", c_int64), ("gen_b", c_int64)]
+                ("emb", c_int64), ("gen_w", c_int64), ("gen_b", c_int64), ("store_gen_w", c_int32),
+                ("pad_", c_int32)]
 
 
 class Task(ctypes.Structure):

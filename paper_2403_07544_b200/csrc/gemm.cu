@@ -974,6 +974,13 @@ constexpr double kAccumWaveUs = 0.9;  // extra per wave of fp32 reduce-add (spli
 
 int split_cap(const mm_gemm_args* const* probs, int n, int bn, int cg, int sms);
 
+// an fp32 weight-gradient problem: reduce-add (MM_EPI_F32_ACCUM) or the store
+// of a module's first micro-batch (MM_EPI_F32 with both operands MN-major)
+bool f32_wgrad(const mm_gemm_args* a) {
+    return a->epilogue == MM_EPI_F32_ACCUM ||
+           (a->epilogue == MM_EPI_F32 && !a->a_kmajor && !a->b_kmajor);
+}
+
 TileChoice choose_tile(const mm_gemm_args* const* probs, int n, int sms) {
     TileChoice best{128, 1};
     double best_cost = 1e300;
@@ -983,7 +990,9 @@ TileChoice choose_tile(const mm_gemm_args* const* probs, int n, int sms) {
             bool fits = true, accum = true;
             for (int i = 0; i < n; ++i) {
                 if (cand > 128 && probs[i]->n <= cand - 64) fits = false;
-                accum = accum && probs[i]->epilogue == MM_EPI_F32_ACCUM;
+                // fp32 weight-gradient launches (reduce-add, or the store of a
+                // module's first micro-batch) share one cost model
+                accum = accum && f32_wgrad(probs[i]);
             }
             if (!fits) continue;
             const int cap = split_cap(probs, n, cand, cg, sms);
@@ -1102,7 +1111,7 @@ int split_cap(const mm_gemm_args* const* probs, int n, int bn, int cg, int sms) 
     for (int i = 0; i < n; ++i) {
         tiles += ((probs[i]->m + BM * cg - 1) / (BM * cg)) * ((probs[i]->n + bn - 1) / bn);
         min_kb = std::min<int>(min_kb, static_cast<int>((probs[i]->k + BK - 1) / BK));
-        all_accum = all_accum && probs[i]->epilogue == MM_EPI_F32_ACCUM;
+        all_accum = all_accum && f32_wgrad(probs[i]);
     }
     int splits = 1;
     if (all_accum)
@@ -1111,12 +1120,30 @@ int split_cap(const mm_gemm_args* const* probs, int n, int bn, int cg, int sms) 
 }
 
 template <int NP>
-int run_group(const mm_gemm_args* const* probs, int n, cudaStream_t s) {
+int run_group(const mm_gemm_args* const* probs_in, int n, cudaStream_t s) {
     const int sms = mm::num_sms();
-    const bool ln = probs[0]->epilogue == MM_EPI_F32_RESID_LN;
-    const TileChoice tc = ln ? TileChoice{128, 1} : choose_tile(probs, n, sms);
+    const bool ln = probs_in[0]->epilogue == MM_EPI_F32_RESID_LN;
+    const TileChoice tc = ln ? TileChoice{128, 1} : choose_tile(probs_in, n, sms);
     const int bn = tc.bn, cg = tc.cg;
-    const int cap = ln ? 1 : split_cap(probs, n, bn, cg, sms);
+    const int cap = ln ? 1 : split_cap(probs_in, n, bn, cg, sms);
+    // a launch that splits K: store-mode weight gradients become zero + the
+    // split reduce-add, so the result never depends on which micro-batch
+    // stored (bit-identical to memset + MM_EPI_F32_ACCUM)
+    static mm_gemm_args conv[kMaxProbs];
+    static const mm_gemm_args* conv_ptr[kMaxProbs];
+    const mm_gemm_args* const* probs = probs_in;
+    if (cap > 1) {
+        for (int i = 0; i < n; ++i) {
+            conv[i] = *probs_in[i];
+            if (conv[i].epilogue == MM_EPI_F32 && f32_wgrad(&conv[i])) {
+                MM_CUDA_TRY(cudaMemset2DAsync(conv[i].d, size_t(conv[i].ldd) * 4, 0, size_t(conv[i].n) * 4,
+                                              size_t(conv[i].m), s));
+                conv[i].epilogue = MM_EPI_F32_ACCUM;
+            }
+            conv_ptr[i] = &conv[i];
+        }
+        probs = conv_ptr;
+    }
     static Group<NP> g;  // host staging of the kernel parameter (large: tensor maps)
     std::memset(&g, 0, sizeof(g));
     int64_t units = 0;

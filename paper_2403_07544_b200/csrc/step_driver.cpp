@@ -198,13 +198,14 @@ struct Driver {
               int epi, const void* aux = nullptr) {
         return gemm(dY, true, W, false, dX, T, in, out, out, in, in, epi, nullptr, nullptr, aux);
     }
-    // dW[out,in] += dY[T,out]^T X[T,in];  db[out] += sum_t dY[t,out] (fused)
+    // dW[out,in] += dY[T,out]^T X[T,in] (store: dW = ..., the module's first
+    // micro-batch of the step);  db[out] += sum_t dY[t,out] (fused)
     int wgrad(const uint16_t* dY, const uint16_t* X, float* dW, int64_t T, int64_t in, int64_t out,
-              float* db) {
+              float* db, bool store) {
         mm_gemm_args a{};
         a.a = dY; a.b = X; a.d = dW; a.dbias = db;
         a.m = out; a.n = in; a.k = T; a.lda = out; a.ldb = in; a.ldd = in;
-        a.a_kmajor = 0; a.b_kmajor = 0; a.epilogue = MM_EPI_F32_ACCUM;
+        a.a_kmajor = 0; a.b_kmajor = 0; a.epilogue = store ? MM_EPI_F32 : MM_EPI_F32_ACCUM;
         a.b_prefetch = 1;
         if (defer) {
             pending.push_back(a);
@@ -328,7 +329,7 @@ struct Driver {
         const mm_layer_offsets* o = L.o;
         FfnSave& sv = L.ffn;
         const size_t mark = ar.off;
-        TRY(wgrad(dx_bf, sv.f, g(st, o->ff2_w), T, F, d, g(st, o->ff2_b)));
+        TRY(wgrad(dx_bf, sv.f, g(st, o->ff2_w), T, F, d, g(st, o->ff2_b), st->store_wgrad != 0));
         uint16_t* df = ar.get<uint16_t>(T * F);
         {
             mm_gemm_args a = make_args(dx_bf, true, wb(st, o->ff2_w), false, df, T, F, d, d, F, F,
@@ -336,7 +337,7 @@ struct Driver {
             a.relu_mask = use_relu_mask() ? sv.mask : nullptr;  // 1 bit per element instead of the bf16 activation
             TRY(mm_gemm(&a, s));
         }
-        TRY(wgrad(df, sv.h, g(st, o->ff1_w), T, d, F, g(st, o->ff1_b)));
+        TRY(wgrad(df, sv.h, g(st, o->ff1_w), T, d, F, g(st, o->ff1_b), st->store_wgrad != 0));
         float* dh = ar.get<float>(T * d);
         TRY(dgrad(df, wb(st, o->ff1_w), dh, T, d, F, MM_EPI_F32));
         uint16_t* nbf = next_bf(dx_bf, T);
@@ -353,7 +354,7 @@ struct Driver {
         const mm_layer_offsets* o = L.o;
         SelfSave& sv = L.self;
         const size_t mark = ar.off;
-        TRY(wgrad(dx_bf, sv.a, g(st, o->out_w), T, d, d, g(st, o->out_b)));
+        TRY(wgrad(dx_bf, sv.a, g(st, o->out_w), T, d, d, g(st, o->out_b), st->store_wgrad != 0));
         uint16_t* da = ar.get<uint16_t>(T * d);
         TRY(dgrad(dx_bf, wb(st, o->out_w), da, T, d, d, MM_EPI_BF16));
         uint16_t* dqkv = ar.get<uint16_t>(T * 3 * d);
@@ -363,7 +364,7 @@ struct Driver {
         a.ld_dq = a.ld_dk = a.ld_dv = 3 * d;
         a.flags |= 2;  // Q / K / V / lse come from the forward pass
         TIMED(3, mm_attention_bwd(&a, s));
-        TRY(wgrad(dqkv, sv.h, g(st, o->qkv_w), T, d, 3 * d, g(st, o->qkv_b)));
+        TRY(wgrad(dqkv, sv.h, g(st, o->qkv_w), T, d, 3 * d, g(st, o->qkv_b), st->store_wgrad != 0));
         float* dh = ar.get<float>(T * d);
         TRY(dgrad(dqkv, wb(st, o->qkv_w), dh, T, d, 3 * d, MM_EPI_F32));
         uint16_t* nbf = next_bf(dx_bf, T);
@@ -380,7 +381,7 @@ struct Driver {
         CrossSave& sv = L.cross;
         const int64_t T = b.n_tgt, S = b.n_src;
         const size_t mark = ar.off;
-        TRY(wgrad(dx_bf, sv.a, g(st, o->cout_w), T, d, d, g(st, o->cout_b)));
+        TRY(wgrad(dx_bf, sv.a, g(st, o->cout_w), T, d, d, g(st, o->cout_b), st->store_wgrad != 0));
         uint16_t* da = ar.get<uint16_t>(T * d);
         TRY(dgrad(dx_bf, wb(st, o->cout_w), da, T, d, d, MM_EPI_BF16));
         uint16_t* dq = ar.get<uint16_t>(T * d);
@@ -392,8 +393,8 @@ struct Driver {
         a.ld_dq = d; a.ld_dk = a.ld_dv = 2 * d;
         a.flags |= 2;  // Q / K / V / lse come from the forward pass
         TIMED(3, mm_attention_bwd(&a, s));
-        TRY(wgrad(dkv, mem, g(st, o->ckv_w), S, d, 2 * d, g(st, o->ckv_b)));
-        TRY(wgrad(dq, sv.h, g(st, o->cq_w), T, d, d, g(st, o->cq_b)));
+        TRY(wgrad(dkv, mem, g(st, o->ckv_w), S, d, 2 * d, g(st, o->ckv_b), st->store_wgrad != 0));
+        TRY(wgrad(dq, sv.h, g(st, o->cq_w), T, d, d, g(st, o->cq_b), st->store_wgrad != 0));
         float* dh = ar.get<float>(T * d);
         // the two independent dgrads of the block (memory side, query side)
         // share one grouped launch
@@ -495,7 +496,7 @@ struct Driver {
         float* row_loss = ar.get<float>(Tt);
         TIMED(4, mm_xent_fwd_bwd(logits, b.labels, logits, row_loss, loss_sum, Tt, V, 1.f / float(Tt), s));
         // ---- generator backward (dlogits in place of the logits)
-        TRY(wgrad(logits, hdec, E.grad + E.gen_w, Tt, d, V, E.grad + E.gen_b));
+        TRY(wgrad(logits, hdec, E.grad + E.gen_w, Tt, d, V, E.grad + E.gen_b, E.store_gen_w != 0));
         float* dh = ar.get<float>(Tt * d);
         TRY(dgrad(logits, E.w_bf16 + E.gen_w, dh, Tt, d, V, MM_EPI_F32));
         float* dy = ar.get<float>(Tt * d);

@@ -273,6 +273,10 @@ class Engine:
         # reduced gradients stay readable after a step, as the parity tests
         # and the reference's DeviceState.buffers expect).
         self.zero_in_update = False
+        # first micro-batch of a module per step: weight-matrix gradients are
+        # stored (no memset of [0, dense_end), no reduce-add read);
+        # MM_STORE_WGRAD=0 restores memset + reduce-add (bit-identical results)
+        self.store_first_wgrad = os.environ.get("MM_STORE_WGRAD", "1") != "0"
         self._dirty: set = set(self.states)   # buckets that may hold a gradient
         self._counts_host = torch.zeros(len(self.plan.keys), dtype=torch.int32, pin_memory=True)
         self._side_stream = torch.cuda.Stream(device=self.device)
@@ -469,11 +473,15 @@ class Engine:
         return self._task_desc[task.id][0]
 
     def forward_backward(self, task: TaskSpec, db: DeviceBatch, loss_sum: torch.Tensor,
-                         dec_done=None) -> None:
+                         dec_done=None, store=frozenset()) -> None:
         """One micro-batch of one task; gradients accumulate into the buckets.
         ``dec_done`` (torch.cuda.Event) is recorded once the decoder-side
-        gradients are final (native path only)."""
+        gradients are final (native path only).  Modules in ``store`` (native
+        path) get their weight-matrix gradients [0, layout.dense_end) STORED
+        rather than reduce-added: the caller zeroed only the rest of their
+        buckets (``zero_grads(tail_only=True)``)."""
         if not self.native or self.trace is not None:
+            assert not store, "store mode is for the native step driver"
             self.forward_backward_py(task, db, loss_sum)
             if dec_done is not None:
                 dec_done.record()
@@ -481,6 +489,11 @@ class Engine:
         import ctypes
         L = _native.lib()
         t = self.task_desc(task)
+        _t, enc_arr, dec_arr, _keep = self._task_desc[task.id]
+        for arr, keys in ((enc_arr, task.enc_modules), (dec_arr, task.dec_modules)):
+            for i, k in enumerate(keys):
+                arr[i].store_wgrad = int(k in store)
+        t.dec_emb.store_gen_w = int(embedding_keys(task)[1] in store)
         if dec_done is not None and not dec_done.cuda_event:
             raise RuntimeError("dec_done event has no CUDA handle yet")
         need = ctypes.c_size_t(0)
@@ -590,12 +603,15 @@ class Engine:
         ops.embed_bwd_sorted(getattr(db, name), dout.shape[0], nc, nm, dout, dtable, self.scale, scratch)
 
     # ------------------------------------------------------------------ step
-    def zero_grads(self, keys=None) -> None:
+    def zero_grads(self, keys=None, tail_only: bool = False) -> None:
         """DeviceState.reset (syncsim.py:108-111).  Only buckets that will be
         written this step need zeroing: K3 never reads a module with n = 0,
-        and a module's bucket is zeroed before its first use in a step."""
+        and a module's bucket is zeroed before its first use in a step.
+        ``tail_only``: zero [layout.dense_end, end) only -- the weight matrices
+        in front are stored whole by the native driver's store-mode wgrads."""
         for k in (self.states if keys is None else keys):
-            ops.memset(self.states[k].grad, 0)
+            st = self.states[k]
+            ops.memset(st.grad[st.layout.dense_end:] if tail_only else st.grad, 0)
             self._dirty.discard(k)
 
     def step(self, step_idx: int, batches: Sequence[DeviceBatch], tasks=None) -> dict:
@@ -627,13 +643,17 @@ class Engine:
         zeroed: set[ModuleKey] = set()
         overlap = self.overlap and self.native
         dec_done = self._dec_done if overlap else None
+        store_mode = self.native and self.trace is None and self.store_first_wgrad
         for i, (task, db) in enumerate(zip(tasks, batches)):
             fresh = [k for k in task_modules(task) if k not in zeroed]
-            self.zero_grads([k for k in fresh if k in self._dirty])
+            # a module's first micro-batch of the step: its weight-gradient
+            # GEMMs store, so only the bucket's tail needs the memset
+            self.zero_grads([k for k in fresh if k in self._dirty], tail_only=store_mode)
             zeroed.update(fresh)
             self._dirty.update(fresh)
             self.forward_backward(task, db, self.loss_sum,
-                                  dec_done if i == len(tasks) - 1 else None)
+                                  dec_done if i == len(tasks) - 1 else None,
+                                  store=frozenset(fresh) if store_mode else frozenset())
         if counts_ready is not None:
             counts_ready.synchronize()  # waits for K1 only, not for the compute behind it
             self._bits = self._counts_host.tolist()

@@ -67,6 +67,13 @@ class ModuleLayout:
     final_ln: bool
     params: dict[str, Param]
     numel: int           # padded bucket length
+    # [0, dense_end): the weight matrices whose gradients the weight-gradient
+    # GEMMs write whole (stacks: every projection / FFN matrix; the decoder
+    # embedding module: the generator).  A module's first micro-batch of a
+    # step stores them instead of reduce-adding onto zeros, so only
+    # [dense_end, numel) -- biases, LayerNorm, embedding tables -- needs the
+    # reset memset.
+    dense_end: int = 0
 
     def p(self, name: str) -> Param:
         return self.params[name]
@@ -87,13 +94,19 @@ def layout_for(key: ModuleKey, shape: ModelShape, n_layers: int, final_ln: bool)
             spec += _layer_params(f"l{i}.", shape, dec)
         if final_ln:
             spec += [("lnf.g", (shape.d_model,), "ones"), ("lnf.b", (shape.d_model,), "zeros")]
-    params: dict[str, Param] = {}
-    off = 0
-    for name, shp, init in spec:
-        params[name] = Param(name, shp, init, off)
-        n = int(np.prod(shp))
-        off += (n + ALIGN - 1) // ALIGN * ALIGN
-    return ModuleLayout(key, kind, n_layers, final_ln, params, off)
+    # offsets: GEMM-written matrices first (dense_end), then everything else,
+    # each in spec order; params keeps spec order, so init_module draws the
+    # same random stream whatever the placement
+    offsets: dict[str, int] = {}
+    off = dense_end = 0
+    dense = [x for x in spec if x[2] == "xavier"]
+    for i, (name, shp, _init) in enumerate(dense + [x for x in spec if x[2] != "xavier"]):
+        offsets[name] = off
+        off += (int(np.prod(shp)) + ALIGN - 1) // ALIGN * ALIGN
+        if i == len(dense) - 1:
+            dense_end = off
+    params = {name: Param(name, shp, init, offsets[name]) for name, shp, init in spec}
+    return ModuleLayout(key, kind, n_layers, final_ln, params, off, dense_end)
 
 
 def true_param_count(layout: ModuleLayout) -> int:

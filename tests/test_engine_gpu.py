@@ -351,6 +351,49 @@ def test_lazy_grad_zeroing_matches_memset(cuda):
         assert rel(masters[1][k], masters[0][k]) < 1e-5, str(k)
 
 
+def test_store_first_wgrad_matches_reduce_add(cuda):
+    """A module's first micro-batch of a step STORES its weight-matrix
+    gradients (memset of the bucket tail only); later micro-batches
+    reduce-add.  Three steps of two micro-batches of different tasks (modules
+    fresh in the first or in the second micro-batch, shared ones
+    accumulating; dirty buckets from the previous step) against memset +
+    reduce-add everywhere (MM_STORE_WGRAD=0), both engines restarted from the
+    same state every step: gradients and optimizer states agree up to fp32
+    summation order (at this shape the weight-gradient launches split K, and
+    the split partials, like the fused bias-gradient atomics, reduce-add in
+    whatever order the CTAs finish).  A store that missed its zeroing or a
+    double count would be O(1)."""
+    from paper_2403_07544_b200.engine import DeviceBatch, Engine
+    shape = configs.SHAPE_CFG1_GPU
+    w = configs.config1(shape)
+    tasks = [t.with_device(DeviceId(0, 0)) for t in w.tasks]
+    hb = batches_for(1, 6, shape, seed=11)[0]
+    engs = []
+    for store in (True, False):
+        eng = Engine(tasks, ClusterTopology(1, 1, 3), shape, device=cuda, seed=0)
+        eng.store_first_wgrad = store
+        eng.defer_update = False
+        engs.append(eng)
+    assert any(st.layout.dense_end > 0 for st in engs[0].states.values())
+    fields = ("grad", "master", "exp_avg", "exp_avg_sq", "weights")
+    for s in range(3):
+        for k, st in engs[0].states.items():  # same starting state, dirty gradients included
+            sb = engs[1].states[k]
+            for f in fields:
+                getattr(sb, f).copy_(getattr(st, f))
+            sb.step = st.step
+        engs[1]._dirty = set(engs[0]._dirty)
+        pick = [tasks[(s + j) % len(tasks)] for j in range(2)]
+        for eng in engs:
+            eng.step(s, [DeviceBatch(hb[2 * s + j], cuda) for j in range(2)], tasks=pick)
+        torch.cuda.synchronize()
+        for k, st in engs[0].states.items():
+            sb = engs[1].states[k]
+            for f in fields[:4]:
+                assert rel(getattr(st, f).cpu().numpy(), getattr(sb, f).cpu().numpy()) < 1e-5, \
+                    (s, str(k), f)
+
+
 def test_config1_peer_exchange_bit_exact_vs_sync(cuda):
     """Option B (one mm_peer_update launch over both emulated ranks' shards)
     vs the sync + per-rank K3 path on the SAME gradients (the backward's
