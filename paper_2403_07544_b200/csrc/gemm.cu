@@ -982,6 +982,12 @@ bool f32_wgrad(const mm_gemm_args* a) {
 }
 
 TileChoice choose_tile(const mm_gemm_args* const* probs, int n, int sms) {
+    // MM_GEMM_RULES=0 (diagnostics): the bare fitted model, without the two
+    // measured corrections for CTA pairs below
+    static const bool rules = [] {
+        const char* e = std::getenv("MM_GEMM_RULES");
+        return !(e && e[0] == '0');
+    }();
     TileChoice best{128, 1};
     double best_cost = 1e300;
     for (int cg : {1, 2}) {
@@ -1010,8 +1016,22 @@ TileChoice choose_tile(const mm_gemm_args* const* probs, int n, int sms) {
             const int slots = sms / cg;
             const double waves = double((units + slots - 1) / slots);
             const TileCost tc = tile_cost(cand, cg);
-            double cost =
-                tc.c0_us + waves * ((kb_sum / double(units)) * tc.x_us + (accum ? kAccumWaveUs : 0.0));
+            const double kb_unit = kb_sum / double(units);
+            double x_us = tc.x_us;
+            double wave_us = accum ? kAccumWaveUs : 0.0;
+            if (cg == 2 && rules) {
+                // measured in the config-3 step (MM_GEMM_OVERRIDE A/B, r02ai):
+                // a pair's per-unit handshakes (cluster-scope accumulator
+                // barriers, multicast commits) do not amortise over 8 k-blocks
+                // -- the generator forward (4096 x 32000 x 512) runs 12 us
+                // faster on single-CTA 256-wide tiles -- while over hundreds of
+                // k-blocks the pair's halved B traffic per SM wins -- the
+                // generator dgrad (4096 x 512 x 32000) runs 7 us faster on
+                // 256 x 128 pair tiles
+                if (kb_unit <= 8.0) wave_us += 0.35;
+                if (cand == 128 && kb_unit >= 256.0) x_us *= 0.9;
+            }
+            double cost = tc.c0_us + waves * (kb_unit * x_us + wave_us);
             // a launch that keeps every SM busy is L2->SM bandwidth bound
             // (~32 KB per k-block per CTA at every shape): only the pair's
             // 128 x 256 per-SM tile does enough MMA work per byte (measured on
