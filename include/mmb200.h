@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define MMB200_ABI_VERSION 23
+#define MMB200_ABI_VERSION 24
 #define MM_MAX_GROUP 8 /* one 8-GPU box: a module group has at most 8 ranks */
 /* emulated devices of one sync (mm_sync_emulated): the reference's multi-node
  * scaling harness reaches 20 devices per group (syncsim.py:461-483) */
@@ -276,6 +276,13 @@ typedef struct {
      * output is non-zero), read by MM_EPI_BF16_DRELU instead of `aux` (16x
      * fewer bytes than the bf16 activation) */
     uint32_t* relu_mask;
+    /* 1: `resid` was not written by the immediately preceding kernel on the
+     * stream (with programmatic dependent launch every kernel of the library
+     * signals its dependents only after its own griddepcontrol.wait, so data
+     * of the kernel before that is complete), so a CTA's first residual tile
+     * may be fetched before griddepcontrol.wait */
+    int32_t resid_early;
+    int32_t pad_;
 } mm_gemm_args;
 
 int mm_gemm(const mm_gemm_args* args, void* stream);

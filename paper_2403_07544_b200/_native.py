@@ -19,7 +19,7 @@ if os.environ.get("MM_LIB_VARIANT"):  # diagnostics: a tuning build from tools/b
                             "libmmb200.so")
 
 #: must match MMB200_ABI_VERSION in include/mmb200.h
-ABI_VERSION = 23
+ABI_VERSION = 24
 MAX_GROUP = 8
 MAX_SYNC_GROUP = 32
 

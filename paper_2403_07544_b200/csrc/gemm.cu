@@ -57,6 +57,10 @@ constexpr int kEpiWarp0 = 2;
 // two slices each take half of the tile's columns
 constexpr int kEpiWarps = MM_GEMM_EPI_WARPS;
 constexpr int kSlices = kEpiWarps / 4;
+#ifndef MM_GEMM_RESID_TMEM
+// residual tile of single-CTA 128-wide tiles parked in TMEM columns 256..383
+#define MM_GEMM_RESID_TMEM 1
+#endif
 #ifndef MM_GEMM_BN64
 // 64-wide single-CTA tiles (diagnostics build: MM_GEMM_OVERRIDE "...=1:64"):
 // twice the tiles of a narrow GEMM, so a CTA's first epilogue overlaps its
@@ -88,7 +92,7 @@ constexpr int kSmemLimit = 232448;
 // CG = CTAs per MMA: 1, or 2 for a CTA pair (cta_group::2) computing a
 // (2*BM) x BN tile -- each CTA holds its BM rows of A and BN/2 rows of B, so
 // per-SM shared-memory traffic per MMA drops by a quarter (BN=128) to a half.
-template <int BN, int CG, int CN = 1>
+template <int BN, int CG, int CN = 1, int RT = 0>
 struct Cfg {
     static constexpr int kEpiBufs = (BN == 128 && CG == 1 && CN == 1) ? MM_GEMM_EPI_BUFS128
                                     : (BN == 256 && CG == 2) ? MM_GEMM_EPI_BUFS256P
@@ -107,8 +111,13 @@ struct Cfg {
     static constexpr int kStages = kStagesFit > MM_GEMM_MAX_STAGES ? MM_GEMM_MAX_STAGES : kStagesFit;
     // 2 accumulators (power of 2); a single-CTA 128-wide tile also parks the
     // tile's fp32 residual in columns 256..383 (loaded while the MMAs run)
-    static constexpr bool kResidTmem = BN <= 128 && CG == 1 && CN == 1;
-    static constexpr int kTmemCols = 512;
+    // RT = 1: the residual-epilogue instantiation (single-CTA 128-wide tiles
+    // of one MM_EPI_F32_RESID problem) parks the tile's fp32 residual in TMEM
+    // columns 256..383; every other launch allocates only the 256 columns of
+    // its two accumulators (a 512-column allocation made the FFN-up / QKV
+    // launches 0.5-2 us slower in the config-3 step, r02al)
+    static constexpr bool kResidTmem = MM_GEMM_RESID_TMEM && RT && BN <= 128 && CG == 1 && CN == 1;
+    static constexpr int kTmemCols = kResidTmem || 2 * BN > 256 ? 512 : 256;
     static constexpr uint32_t kResidCol = 2 * BN;
     static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 + kBarBytes + kLnBytes;
     static_assert(kSmem <= kSmemLimit, "smem budget");
@@ -132,6 +141,7 @@ struct alignas(64) Prob {
     int epilogue;
     int tiles_m, tiles_n, splits, kb_per_split, num_kb;
     int group_m;  // unit order: M-tiles walked in groups of group_m (L2 reuse of A)
+    int resid_early;  // residual not written by the preceding kernel (see mm_gemm_args)
     int unit_begin;
 };
 
@@ -342,10 +352,10 @@ __device__ __forceinline__ Unit decode(const Group<NP>& g, int u) {
     return w;
 }
 
-template <int BN, int A_MN, int B_MN, int NP, int CG, int CN = 1>
+template <int BN, int A_MN, int B_MN, int NP, int CG, int CN = 1, int RT = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ Group<NP> g) {
-    using C = Cfg<BN, CG, CN>;
+    using C = Cfg<BN, CG, CN, RT>;
     static_assert(CN == 1 || (CG == 1 && NP == 1), "LayerNorm clusters: single CTAs, one problem");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -595,10 +605,54 @@ __global__ void __launch_bounds__(kThreads, 1)
     done:;
     } else {
         // ------------------------------------------------------------ epilogue
-        pdl_wait();
         const int lane_grp = warp & 3;                   // TMEM lanes this warp may access
         const int half = (warp - kEpiWarp0) >> 2;        // which column slice of the tile
         constexpr int kChunks = BN / 32 / kSlices;       // 32-column chunks per warp
+        // residual tile of this warp's rows / columns into TMEM while the
+        // MMAs of the unit run (lane = row: 128 B per lane per chunk; the
+        // LSU is idle during the mainloop), read back next to the
+        // accumulator in the epilogue -- the add order stays
+        // (acc + bias) + resid
+        auto resid_to_tmem = [&](const Prob& P, int tm, int cbase) {
+            const int64_t rrow = int64_t(tm) * BM + lane_grp * 32 + lane;
+            const uint32_t t_res = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) +
+                                   C::kResidCol + half * (BN / kSlices);
+#pragma unroll 1
+            for (int c = 0; c < kChunks; ++c) {
+                const int col0 = cbase + c * 32;
+                uint32_t r[32];
+                if (rrow < P.m && col0 + 32 <= P.n) {
+                    const float4* res = reinterpret_cast<const float4*>(P.resid + rrow * P.ldd + col0);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 x = res[q];
+                        r[4 * q] = __float_as_uint(x.x); r[4 * q + 1] = __float_as_uint(x.y);
+                        r[4 * q + 2] = __float_as_uint(x.z); r[4 * q + 3] = __float_as_uint(x.w);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        r[j] = (rrow < P.m && col0 + j < P.n) ? __float_as_uint(P.resid[rrow * P.ldd + col0 + j]) : 0u;
+                }
+                tc::tmem_st_32x32(t_res + c * 32, r);
+            }
+            tc::tmem_st_wait();
+        };
+        // the first unit's residual before griddepcontrol.wait when the
+        // caller says the previous kernel did not write it: its fetch then
+        // overlaps that kernel's tail instead of this launch's mainloop
+        bool resid_pre = false;
+        if constexpr (C::kResidTmem) {
+            if (cid < g.units) {
+                const Unit w0 = unit_at(cid);
+                const Prob& P0 = g.prob[w0.pi];
+                if (P0.epilogue == MM_EPI_F32_RESID && P0.resid_early) {
+                    resid_to_tmem(P0, w0.tm, w0.tn * BN + half * (BN / kSlices));
+                    resid_pre = true;
+                }
+            }
+        }
+        pdl_wait();
         uint8_t* bufs = smem_epi + (warp - kEpiWarp0) * C::kEpiBufs * kEpiBufBytes;
         int nbuf = 0;
         int local = 0;
@@ -614,38 +668,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             const int cbase = tn * BN + half * (BN / kSlices);
-            // residual tile of this warp's rows / columns into TMEM while the
-            // MMAs of the unit run (lane = row: 128 B per lane per chunk; the
-            // LSU is idle during the mainloop), read back next to the
-            // accumulator in the epilogue -- the add order stays
-            // (acc + bias) + resid
             const bool resid_tm = C::kResidTmem && P.epilogue == MM_EPI_F32_RESID;
             if constexpr (C::kResidTmem) {
-                if (resid_tm) {
-                    const int64_t rrow = int64_t(tm) * BM + lane_grp * 32 + lane;
-                    const uint32_t t_res = tmem_base + (static_cast<uint32_t>(lane_grp * 32) << 16) +
-                                           C::kResidCol + half * (BN / kSlices);
-#pragma unroll 1
-                    for (int c = 0; c < kChunks; ++c) {
-                        const int col0 = cbase + c * 32;
-                        uint32_t r[32];
-                        if (rrow < P.m && col0 + 32 <= P.n) {
-                            const float4* res = reinterpret_cast<const float4*>(P.resid + rrow * P.ldd + col0);
-#pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                const float4 x = res[q];
-                                r[4 * q] = __float_as_uint(x.x); r[4 * q + 1] = __float_as_uint(x.y);
-                                r[4 * q + 2] = __float_as_uint(x.z); r[4 * q + 3] = __float_as_uint(x.w);
-                            }
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j)
-                                r[j] = (rrow < P.m && col0 + j < P.n) ? __float_as_uint(P.resid[rrow * P.ldd + col0 + j]) : 0u;
-                        }
-                        tc::tmem_st_32x32(t_res + c * 32, r);
-                    }
-                    tc::tmem_st_wait();
-                }
+                if (resid_tm && !(local == 0 && resid_pre)) resid_to_tmem(P, tm, cbase);
             }
             // bias for this warp's columns, fetched before waiting on the MMAs
             float bv[kChunks];
@@ -869,19 +894,20 @@ int make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, i
     return 0;
 }
 
-template <int BN, int A_MN, int B_MN, int NP, int CG, int CN = 1>
+template <int BN, int A_MN, int B_MN, int NP, int CG, int CN = 1, int RT = 0>
 int launch(const Group<NP>& g, cudaStream_t s) {
-    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, NP, CG, CN>;
+    using C = Cfg<BN, CG, CN, RT>;
+    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, NP, CG, CN, RT>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg<BN, CG, CN>::kSmem));
+                                         C::kSmem));
         attr_set = true;
     }
     // persistent: one CTA (pair / LayerNorm cluster) per SM (pair / CN SMs)
     const int per = CG * CN;
     const int ctas = std::min(g.units, mm::num_sms() / per) * per;
-    MM_CUDA_TRY(mm::launch_pdl_cluster(kern, dim3(ctas), dim3(kThreads), Cfg<BN, CG, CN>::kSmem, s,
+    MM_CUDA_TRY(mm::launch_pdl_cluster(kern, dim3(ctas), dim3(kThreads), C::kSmem, s,
                                        static_cast<unsigned>(per), g));
     MM_LAUNCH_CHECK("gemm_tcgen05_kernel");
     return 0;
@@ -1105,6 +1131,7 @@ int setup_prob(Prob& P, const mm_gemm_args* a, int bn, int cg, int splits_cap) {
     P.epilogue = a->epilogue;
     P.tiles_m = static_cast<int>(tiles_m);
     P.tiles_n = static_cast<int>(tiles_n);
+    P.resid_early = a->resid_early != 0;
     P.splits = splits;
     P.kb_per_split = kb_per;
     P.num_kb = num_kb;
@@ -1219,6 +1246,8 @@ int run_group(const mm_gemm_args* const* probs_in, int n, cudaStream_t s) {
     } else if (cg == 2) {
         if (bn == 256) rc = dispatch<256, NP, 2>(a_mn, b_mn, g, s);
         else rc = dispatch<128, NP, 2>(a_mn, b_mn, g, s);
+    } else if (NP == 1 && bn == 128 && !a_mn && !b_mn && probs[0]->epilogue == MM_EPI_F32_RESID) {
+        rc = launch<128, 0, 0, NP, 1, 1, 1>(g, s);  // residual parked in TMEM
     } else {
         if (bn == 256) rc = dispatch<256, NP, 1>(a_mn, b_mn, g, s);
         else if (bn == 192) rc = dispatch<192, NP, 1>(a_mn, b_mn, g, s);

@@ -191,8 +191,16 @@ struct Driver {
     // Y[T,out] (epi)= X[T,in] W[out,in]^T
     int linear(const uint16_t* X, const uint16_t* W, void* Y, int64_t T, int64_t in, int64_t out,
                int epi, const float* bias = nullptr, const float* resid = nullptr) {
-        return gemm(X, true, W, true, Y, T, out, in, in, in, out, epi, bias, resid);
+        mm_gemm_args a = make_args(X, true, W, true, Y, T, out, in, in, in, out, epi, bias, resid);
+        // every residual GEMM of the step reads a residual stream written at
+        // least two kernels earlier (out-proj: the block input, then LN,
+        // QKV, attention; cross out-proj: the self-attention output, then
+        // LN, Q, cross attention; FFN-down: the attention output, then LN,
+        // FFN-up), so its first residual tile is fetched before the wait
+        a.resid_early = resid != nullptr && resid_early;
+        return mm_gemm(&a, s);
     }
+    bool resid_early = true;
     // dX[T,in] (epi)= dY[T,out] W[out,in]
     int dgrad(const uint16_t* dY, const uint16_t* W, void* dX, int64_t T, int64_t in, int64_t out,
               int epi, const void* aux = nullptr) {
@@ -588,6 +596,11 @@ extern "C" int mm_task_fwd_bwd(const mm_task* task, const mm_batch* batch, void*
         const char* e = std::getenv("MM_FUSE_LN");
         return e && e[0] == '1';
     }();
+    // MM_RESID_EARLY=0 (A/B): residual tiles only after griddepcontrol.wait
+    const bool resid_early = [] {
+        const char* e = std::getenv("MM_RESID_EARLY");
+        return !(e && e[0] == '0');
+    }();
     Arena ar;
     ar.base = static_cast<uint8_t*>(workspace);
     ar.sizing = workspace == nullptr;
@@ -607,6 +620,7 @@ extern "C" int mm_task_fwd_bwd(const mm_task* task, const mm_batch* batch, void*
     drv.dec_done = static_cast<cudaEvent_t>(dec_done);
     drv.defer = defer;
     drv.fuse_ln = fuse_ln;
+    drv.resid_early = resid_early;
     const int st = drv.run(loss_sum);
     if (ar.sizing) *ws_bytes = ar.peak;
     return st;

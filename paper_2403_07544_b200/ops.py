@@ -30,7 +30,7 @@ class GemmArgs(ctypes.Structure):
         ("dbias", ctypes.c_void_p),
         ("ln_gamma", ctypes.c_void_p), ("ln_beta", ctypes.c_void_p), ("ln_out", ctypes.c_void_p),
         ("ln_mean", ctypes.c_void_p), ("ln_rstd", ctypes.c_void_p), ("ln_eps", ctypes.c_float),
-        ("relu_mask", ctypes.c_void_p),
+        ("relu_mask", ctypes.c_void_p), ("resid_early", ctypes.c_int32), ("pad_", ctypes.c_int32),
     ]
 
 
@@ -121,15 +121,17 @@ def gemm_args(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bo
 
 def gemm(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, *, a_kmajor: bool = True,
          b_kmajor: bool = True, epilogue: int = EPI_BF16, bias=None, resid=None, aux=None,
-         dbias=None, ln=None, relu_mask=None) -> None:
+         dbias=None, ln=None, relu_mask=None, resid_early: bool = False) -> None:
     """d[M,N] (epilogue)= op(a) @ op(b)^T on tcgen05.
 
     a: [M,K] if a_kmajor else [K,M]; b: [N,K] if b_kmajor else [K,N] (bf16).
     relu_mask (int32 [M, ceil(N/32)]): written by EPI_BF16_RELU, read by
-    EPI_BF16_DRELU in place of aux.
+    EPI_BF16_DRELU in place of aux.  resid_early: the caller guarantees the
+    previous kernel on the stream did not write ``resid`` (mm_gemm_args).
     """
     args = gemm_args(a, b, d, a_kmajor=a_kmajor, b_kmajor=b_kmajor, epilogue=epilogue,
                      bias=bias, resid=resid, aux=aux, dbias=dbias, ln=ln, relu_mask=relu_mask)
+    args.resid_early = int(resid_early)
     m, n, k = args.m, args.n, args.k
     LAUNCHES[0] += 1
     if GEMM_PROFILE is not None:

@@ -90,6 +90,11 @@ def test_gemm_epilogues(cuda, tile, shape):
     out = resid.clone()
     ops.gemm(A, B, out, epilogue=ops.EPI_F32_RESID, bias=bias, resid=out)
     assert rel_err(out, resid + ref) < 2e-3
+    # the same with the first residual tiles fetched before griddepcontrol.wait
+    # (the clone below is a torch kernel, which never releases its dependents early)
+    out2 = resid.clone()
+    ops.gemm(A, B, out2, epilogue=ops.EPI_F32_RESID, bias=bias, resid=out2, resid_early=True)
+    assert torch.equal(out2, out)
     # relu-backward mask
     aux = torch.randn(m, n, device=cuda, generator=g).bfloat16()
     ops.gemm(A, B, d, epilogue=ops.EPI_BF16_DRELU, aux=aux)
