@@ -115,10 +115,10 @@ __global__ void __launch_bounds__(kThreads, 4) peer_update_kernel(const __grid_c
                         if (r < g && ((mask >> r) & 1u)) add4(acc, x[r][u]);
                     // total / n * inv_loss_scale: the rounding sequence of
                     // sync_emulated + fused_update(n_ready = 1) (x / 1 is exact)
-                    adam_elem(__fdiv_rn(acc.x, fn) * unscale, p[u].x, m[u].x, s[u].x, ss, isb, t.hp);
-                    adam_elem(__fdiv_rn(acc.y, fn) * unscale, p[u].y, m[u].y, s[u].y, ss, isb, t.hp);
-                    adam_elem(__fdiv_rn(acc.z, fn) * unscale, p[u].z, m[u].z, s[u].z, ss, isb, t.hp);
-                    adam_elem(__fdiv_rn(acc.w, fn) * unscale, p[u].w, m[u].w, s[u].w, ss, isb, t.hp);
+                    adam_elem(adam_grad(acc.x, fn, unscale), p[u].x, m[u].x, s[u].x, ss, isb, t.hp);
+                    adam_elem(adam_grad(acc.y, fn, unscale), p[u].y, m[u].y, s[u].y, ss, isb, t.hp);
+                    adam_elem(adam_grad(acc.z, fn, unscale), p[u].z, m[u].z, s[u].z, ss, isb, t.hp);
+                    adam_elem(adam_grad(acc.w, fn, unscale), p[u].w, m[u].w, s[u].w, ss, isb, t.hp);
                     __stcs(P + vi, p[u]); __stcs(M + vi, m[u]); __stcs(V + vi, s[u]);
                     uint2 b;
                     b.x = pack_bf16x2(p[u].x, p[u].y);
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, 4) peer_update_kernel(const __grid_c
                     if (zero_grad) sh.grad[r][i] = 0.f;
                 }
                 float p = sh.master[i], m = sh.exp_avg[i], s = sh.exp_avg_sq[i];
-                adam_elem(__fdiv_rn(acc, fn) * unscale, p, m, s, ss, isb, t.hp);
+                adam_elem(adam_grad(acc, fn, unscale), p, m, s, ss, isb, t.hp);
                 sh.master[i] = p; sh.exp_avg[i] = m; sh.exp_avg_sq[i] = s;
                 __nv_bfloat16 h = __float2bfloat16_rn(p);
                 const uint16_t hb = *reinterpret_cast<uint16_t*>(&h);

@@ -198,10 +198,10 @@ __global__ void __launch_bounds__(kThreads) fused_update_kernel(const __grid_con
             for (int u = 0; u < 2; ++u) {
                 const int64_t vi = v + int64_t(u) * kThreads;
                 if (vi >= v1) continue;
-                adam_elem(__fdiv_rn(g[u].x, fn) * unscale, p[u].x, m[u].x, s[u].x, ss, isb, t.hp);
-                adam_elem(__fdiv_rn(g[u].y, fn) * unscale, p[u].y, m[u].y, s[u].y, ss, isb, t.hp);
-                adam_elem(__fdiv_rn(g[u].z, fn) * unscale, p[u].z, m[u].z, s[u].z, ss, isb, t.hp);
-                adam_elem(__fdiv_rn(g[u].w, fn) * unscale, p[u].w, m[u].w, s[u].w, ss, isb, t.hp);
+                adam_elem(adam_grad(g[u].x, fn, unscale), p[u].x, m[u].x, s[u].x, ss, isb, t.hp);
+                adam_elem(adam_grad(g[u].y, fn, unscale), p[u].y, m[u].y, s[u].y, ss, isb, t.hp);
+                adam_elem(adam_grad(g[u].z, fn, unscale), p[u].z, m[u].z, s[u].z, ss, isb, t.hp);
+                adam_elem(adam_grad(g[u].w, fn, unscale), p[u].w, m[u].w, s[u].w, ss, isb, t.hp);
                 __stcs(P + vi, p[u]); __stcs(M + vi, m[u]); __stcs(V + vi, s[u]);
                 if (zero_grad) __stcs(G0 + vi, make_float4(0.f, 0.f, 0.f, 0.f));  // lazy zeroing
                 if (B) {
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kThreads) fused_update_kernel(const __grid_con
             float p = md.master[i], m = md.exp_avg[i], s = md.exp_avg_sq[i];
             const float gi = md.grad[i];
             if (zero_grad) md.grad[i] = 0.f;
-            adam_elem(__fdiv_rn(gi, fn) * unscale, p, m, s, ss, isb, t.hp);
+            adam_elem(adam_grad(gi, fn, unscale), p, m, s, ss, isb, t.hp);
             md.master[i] = p; md.exp_avg[i] = m; md.exp_avg_sq[i] = s;
             if (md.param_bf16) {
                 __nv_bfloat16 h = __float2bfloat16_rn(p);
