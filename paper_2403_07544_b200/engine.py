@@ -906,6 +906,7 @@ class Trainer:
         # asynchronous, and a step may stage more micro-batches than buffers)
         self._pin_events: list = [None] * len(self._pinned)
         self._loss_host = torch.empty(1, dtype=torch.float32, pin_memory=True)
+        self._loss_ring = torch.empty(2, dtype=torch.float32, pin_memory=True)  # train_steps
         self._pin_next = 0  # rotating pinned staging buffer (reused >= 2 steps later)
         self.step_idx = 0
         self.h2d_bytes = 0
@@ -927,24 +928,34 @@ class Trainer:
 
     def train_steps(self, step_batches, n_steps: int) -> list:
         """``n_steps`` training steps over an iterable of per-step micro-batch
-        lists, with one step of lookahead: the host builds and stages step
-        k+1's batches (one H2D copy each, queued behind step k) while the GPU
-        runs step k; every step still reads its loss back.  Returns the losses."""
+        lists, with lookahead: the host builds and stages step k+1's batches
+        (one H2D copy each, queued behind step k) and issues step k+1 before
+        it waits for step k's loss, so the GPU never idles between steps;
+        every step's loss is copied back (a two-slot pinned ring, the copy
+        queued before the next step resets the device sum) and read on the
+        host one step later.  Returns the losses."""
         it = iter(step_batches)
         losses = []
         staged = self.stage(next(it)) if n_steps > 0 else None
         h2d = [self.h2d_bytes]
+        pending = None  # (event, ring slot) of the previous step's loss copy
         for k in range(n_steps):
             self.engine.step(self.step_idx, staged)
             self.step_idx += 1
-            self._loss_host.copy_(self.engine.loss_sum, non_blocking=True)
+            slot = k & 1
+            self._loss_ring[slot:slot + 1].copy_(self.engine.loss_sum, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record()
             if k + 1 < n_steps:  # host work for step k+1 overlaps step k on the GPU
                 staged = self.stage(next(it))
                 h2d.append(self.h2d_bytes)
-            ev.synchronize()
-            losses.append(float(self._loss_host[0]))
+            if pending is not None:
+                pending[0].synchronize()
+                losses.append(float(self._loss_ring[pending[1]]))
+            pending = (ev, slot)
+        if pending is not None:
+            pending[0].synchronize()
+            losses.append(float(self._loss_ring[pending[1]]))
         self.h2d_bytes = sum(h2d) // max(1, len(h2d))
         return losses
 
