@@ -685,7 +685,11 @@ __global__ void __launch_bounds__(kXentThreads) xent_kernel(const uint16_t* logi
 // kept to one MUFU exp per logit (the exps stay in registers between the sum
 // and the write pass -- two exps per logit are SFU-bound at ~60 us for a
 // 4096 x 32000 batch on B200's 16 MUFU/clk/SM) and a packed bf16x2 max.
-constexpr int kXentSmemVocab = kXentThreads * 8 * 8;
+constexpr int kXentSmemVocab = 32768;
+#ifndef MM_XENT_STREAM_THREADS
+#define MM_XENT_STREAM_THREADS 512
+#endif
+constexpr int kXsThreads = MM_XENT_STREAM_THREADS;
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -693,6 +697,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+template <int NT>
 __device__ __forceinline__ float xent_block_reduce(float v, float* sm, bool is_max) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     v = is_max ? warp_max(v) : warp_sum(v);
@@ -701,20 +706,20 @@ __device__ __forceinline__ float xent_block_reduce(float v, float* sm, bool is_m
     __syncthreads();
     float r = is_max ? -INFINITY : 0.f;
 #pragma unroll
-    for (int j = 0; j < kXentThreads / 32; ++j) r = is_max ? fmaxf(r, sm[j]) : r + sm[j];
+    for (int j = 0; j < NT / 32; ++j) r = is_max ? fmaxf(r, sm[j]) : r + sm[j];
     return r;
 }
 
-__global__ void __launch_bounds__(kXentThreads, 1) xent_stream_kernel(const uint16_t* logits,
+__global__ void __launch_bounds__(kXsThreads, 1) xent_stream_kernel(const uint16_t* logits,
                                                                       const int32_t* __restrict__ labels,
                                                                       uint16_t* dlogits, float* row_loss,
                                                                       float* loss_sum, int64_t rows,
                                                                       int vocab, float grad_scale) {
-    constexpr int VPT = kXentSmemVocab / kXentThreads / 8;  // 8-logit vectors per thread
+    constexpr int VPT = kXentSmemVocab / kXsThreads / 8;  // 8-logit vectors per thread
     constexpr float kL2e = 1.4426950408889634f;
     extern __shared__ __align__(128) uint8_t xsm[];
     __shared__ uint64_t bar[2];
-    __shared__ float red[kXentThreads / 32];
+    __shared__ float red[kXsThreads / 32];
     uint16_t* const buf0 = reinterpret_cast<uint16_t*>(xsm);
     const uint32_t bytes = static_cast<uint32_t>(vocab) * 2u;
     const int nv = vocab / 8;
@@ -725,7 +730,7 @@ __global__ void __launch_bounds__(kXentThreads, 1) xent_stream_kernel(const uint
     }
     // each buffer is kXentSmemVocab wide; the tail past the vocab holds bf16
     // -inf (exp -> 0), so every thread's VPT vectors are unconditional
-    for (int c = vocab + threadIdx.x; c < kXentSmemVocab; c += kXentThreads)
+    for (int c = vocab + threadIdx.x; c < kXentSmemVocab; c += kXsThreads)
         buf0[c] = buf0[kXentSmemVocab + c] = 0xff80u;
     __syncthreads();
     pdl_wait_release();
@@ -750,7 +755,7 @@ __global__ void __launch_bounds__(kXentThreads, 1) xent_stream_kernel(const uint
         const uint4* lr = reinterpret_cast<const uint4*>(lrow);
         uint4* dr = reinterpret_cast<uint4*>(dlogits + row * int64_t(vocab));
         if (label < 0) {
-            for (int v = threadIdx.x; v < nv; v += kXentThreads) dr[v] = make_uint4(0, 0, 0, 0);
+            for (int v = threadIdx.x; v < nv; v += kXsThreads) dr[v] = make_uint4(0, 0, 0, 0);
             if (threadIdx.x == 0) row_loss[row] = 0.f;
             __syncthreads();
             continue;
@@ -759,20 +764,20 @@ __global__ void __launch_bounds__(kXentThreads, 1) xent_stream_kernel(const uint
         __nv_bfloat162 m2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
 #pragma unroll
         for (int i = 0; i < VPT; ++i) {
-            const uint4 w = lr[threadIdx.x + i * kXentThreads];
+            const uint4 w = lr[threadIdx.x + i * kXsThreads];
             m2 = __hmax2(m2, __hmax2(__hmax2(*reinterpret_cast<const __nv_bfloat162*>(&w.x),
                                              *reinterpret_cast<const __nv_bfloat162*>(&w.y)),
                                      __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&w.z),
                                              *reinterpret_cast<const __nv_bfloat162*>(&w.w))));
         }
-        const float gm = xent_block_reduce(fmaxf(__low2float(m2), __high2float(m2)), red, true);
+        const float gm = xent_block_reduce<kXsThreads>(fmaxf(__low2float(m2), __high2float(m2)), red, true);
         const float gm2 = gm * kL2e;
         // pass 2: one exp per logit, kept in registers
         float p[VPT][8];
         float sacc = 0.f;
 #pragma unroll
         for (int i = 0; i < VPT; ++i) {
-            const uint4 w = lr[threadIdx.x + i * kXentThreads];
+            const uint4 w = lr[threadIdx.x + i * kXsThreads];
             const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -781,7 +786,7 @@ __global__ void __launch_bounds__(kXentThreads, 1) xent_stream_kernel(const uint
                 sacc += p[i][2 * e] + p[i][2 * e + 1];
             }
         }
-        const float gs = xent_block_reduce(sacc, red, false);
+        const float gs = xent_block_reduce<kXsThreads>(sacc, red, false);
         const float sc = grad_scale / gs;
         if (threadIdx.x == 0) {
             const float l = gm + __logf(gs) - bf2f(lrow[label]);
@@ -797,10 +802,10 @@ __global__ void __launch_bounds__(kXentThreads, 1) xent_stream_kernel(const uint
                 __nv_bfloat162 h = __floats2bfloat162_rn(p[i][2 * e] * sc, p[i][2 * e + 1] * sc);
                 o[e] = *reinterpret_cast<uint32_t*>(&h);
             }
-            const int v = threadIdx.x + i * kXentThreads;
+            const int v = threadIdx.x + i * kXsThreads;
             if (v < nv) dr[v] = make_uint4(o[0], o[1], o[2], o[3]);
         }
-        if (threadIdx.x == (label >> 3) % kXentThreads) {  // the thread that stored the label's vector
+        if (threadIdx.x == (label >> 3) % kXsThreads) {  // the thread that stored the label's vector
             const float pl = ex2_approx(fmaf(bf2f(lrow[label]), kL2e, -gm2));  // == its p, recomputed
             reinterpret_cast<uint16_t*>(dr)[label] = f2bf(pl * sc - grad_scale);
         }
@@ -1010,7 +1015,7 @@ extern "C" int mm_xent_fwd_bwd(const uint16_t* logits, const int32_t* labels, ui
         MM_CUDA_TRY(cudaFuncSetAttribute(xent_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
         const unsigned grid = static_cast<unsigned>(std::min<int64_t>(rows, mm::num_sms()));
-        MM_CUDA_TRY(mm::launch_pdl(xent_stream_kernel, dim3(grid), dim3(kXentThreads), smem,
+        MM_CUDA_TRY(mm::launch_pdl(xent_stream_kernel, dim3(grid), dim3(kXsThreads), smem,
                                    mm::as_stream(stream), logits, labels, dlogits, row_loss, loss_sum,
                                    rows, vocab, grad_scale));
     } else {
