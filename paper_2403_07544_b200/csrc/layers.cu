@@ -1,6 +1,9 @@
 // K6 LayerNorm, K8 embedding gather / scatter-add, K7 softmax cross-entropy,
 // and the bias-gradient column sums.  All HBM-bound: warp-per-row mappings
 // with 128-bit vector accesses and warp-shuffle reductions.
+#ifndef MM_LN_BWD_PREFETCH
+#define MM_LN_BWD_PREFETCH 1
+#endif
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -217,6 +220,17 @@ __global__ void __launch_bounds__(256, MINB) ln_bwd_row_kernel(const float* __re
     float4* rb = red4 + (8 + warp) * (COLS / 4);
 #pragma unroll
     for (int i = 0; i < V; ++i) rg[lane + 32 * i] = rb[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#if MM_LN_BWD_PREFETCH
+    // before griddepcontrol.wait: pull this warp's rows of the forward input x
+    // and of the residual gradient dx (both written several kernels earlier;
+    // an L2 prefetch is coherent whatever the previous kernel writes) into L2,
+    // so their HBM fetch overlaps the producer of dy instead of following it
+    for (int64_t row = int64_t(blockIdx.x) * 8 + warp; row < rows; row += int64_t(gridDim.x) * 8) {
+        const float* base = (lane < 16 ? x : dx) + row * COLS;
+        for (int c = (lane & 15) * 32; c < COLS; c += 16 * 32)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(base + c));
+    }
+#endif
     pdl_wait_release();
     for (int64_t row = int64_t(blockIdx.x) * 8 + warp; row < rows; row += int64_t(gridDim.x) * 8) {
         const float4* dyr = reinterpret_cast<const float4*>(dy + row * COLS);
