@@ -974,10 +974,12 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_tc_kernel(const __gri
         const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
         float pv[64];
         float mx = -INFINITY;
+        bool live[2];  // warp-uniform: some row of this warp attends to the 32-key chunk
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
             const int key0 = kh * 64 + ch * 32;
-            if (__any_sync(0xffffffffu, klo < key0 + 32 && khi > key0)) {
+            live[ch] = __any_sync(0xffffffffu, klo < key0 + 32 && khi > key0);
+            if (live[ch]) {
                 uint32_t sv[32];
                 tc::tmem_ld_32x32(trow + key0, sv);
                 tc::tmem_ld_wait();
@@ -999,9 +1001,17 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_tc_kernel(const __gri
         const float mref = m == -INFINITY ? 0.f : m;
         float sum = 0.f;
 #pragma unroll
-        for (int j = 0; j < 64; ++j) {
-            pv[j] = ex2(pv[j] - mref);  // -inf -> 0
-            sum += pv[j];
+        for (int ch = 0; ch < 2; ++ch) {
+            if (live[ch]) {  // dead chunks stay 0 without spending the SFU
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    pv[ch * 32 + j] = ex2(pv[ch * 32 + j] - mref);  // -inf -> 0
+                    sum += pv[ch * 32 + j];
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) pv[ch * 32 + j] = 0.f;
+            }
         }
         tc::named_barrier_sync(1, kFwdEpiW * 32);  // every max read before the slots are reused
         red[kh * kRows + i] = sum;
