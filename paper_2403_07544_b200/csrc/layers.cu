@@ -1,6 +1,10 @@
 // K6 LayerNorm, K8 embedding gather / scatter-add, K7 softmax cross-entropy,
 // and the bias-gradient column sums.  All HBM-bound: warp-per-row mappings
 // with 128-bit vector accesses and warp-shuffle reductions.
+#ifndef MM_LN_FWD_WARPS
+// rows (warps) per CTA of the row-per-warp LayerNorm forward
+#define MM_LN_FWD_WARPS 4
+#endif
 #ifndef MM_LN_BWD_PREFETCH
 #define MM_LN_BWD_PREFETCH 1
 #endif
@@ -298,14 +302,14 @@ __global__ void __launch_bounds__(256, MINB) ln_bwd_row_kernel(const float* __re
 // Forward: 2 KB (d = 512) of fp32 row per warp loaded at once, two-pass mean /
 // variance from registers, bf16 out.
 template <int COLS>
-__global__ void __launch_bounds__(128) ln_fwd_v2_kernel(const float* __restrict__ x,
+__global__ void __launch_bounds__(32 * MM_LN_FWD_WARPS) ln_fwd_v2_kernel(const float* __restrict__ x,
                                                         const float* __restrict__ gamma,
                                                         const float* __restrict__ beta,
                                                         uint16_t* __restrict__ y, float* mean_out,
                                                         float* rstd_out, int64_t rows, float eps) {
     constexpr int V = COLS / 128;
     const int lane = threadIdx.x & 31;
-    const int64_t row = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
+    const int64_t row = int64_t(blockIdx.x) * MM_LN_FWD_WARPS + (threadIdx.x >> 5);
     pdl_wait_release();
     if (row >= rows) return;
     const float4* xr = reinterpret_cast<const float4*>(x + row * COLS);
@@ -901,11 +905,12 @@ extern "C" int mm_layernorm_fwd(const float* x, const float* gamma, const float*
     auto s = mm::as_stream(stream);
     static const bool v1 = std::getenv("MM_LN_V1") != nullptr;  // A/B: the previous kernels
     if (!v1 && (cols == 512 || cols == 1024)) {
-        const unsigned g2 = static_cast<unsigned>((rows + 3) / 4);
+        const unsigned g2 = static_cast<unsigned>((rows + MM_LN_FWD_WARPS - 1) / MM_LN_FWD_WARPS);
+        const dim3 blk(32 * MM_LN_FWD_WARPS);
         if (cols == 512)
-            MM_CUDA_TRY(mm::launch_pdl(ln_fwd_v2_kernel<512>, dim3(g2), dim3(128), 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
+            MM_CUDA_TRY(mm::launch_pdl(ln_fwd_v2_kernel<512>, dim3(g2), blk, 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
         else
-            MM_CUDA_TRY(mm::launch_pdl(ln_fwd_v2_kernel<1024>, dim3(g2), dim3(128), 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
+            MM_CUDA_TRY(mm::launch_pdl(ln_fwd_v2_kernel<1024>, dim3(g2), blk, 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
         MM_LAUNCH_CHECK("ln_fwd_v2_kernel");
         return 0;
     }
