@@ -352,11 +352,16 @@ __device__ __forceinline__ Unit decode(const Group<NP>& g, int u) {
     return w;
 }
 
-template <int BN, int A_MN, int B_MN, int NP, int CG, int CN = 1, int RT = 0>
+// MC = 2 (CTA pairs only): a cluster of two pairs on adjacent N-tiles of the
+// same 256-row block; each CTA fetches half of its 128 A rows and multicasts
+// it to the CTA at the same pair position in the other pair, so every SM
+// requests 3/4 of the operand bytes per k-block (cuBLAS's 2x2 / 2cta shape).
+template <int BN, int A_MN, int B_MN, int NP, int CG, int CN = 1, int RT = 0, int MC = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ Group<NP> g) {
     using C = Cfg<BN, CG, CN, RT>;
     static_assert(CN == 1 || (CG == 1 && NP == 1), "LayerNorm clusters: single CTAs, one problem");
+    static_assert(MC == 1 || (CG == 2 && CN == 1), "A multicast: CTA pairs");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -378,8 +383,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // descriptors) lives in uniform registers next to the tcgen05 operands
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
-    // pair rank: 0 = leader (issues the MMAs, owns the stage-full barriers)
-    const uint32_t rank = CG == 2 ? tc::cluster_ctarank() : 0u;
+    // pair rank: 0 = leader (issues the MMAs, owns the stage-full barriers);
+    // MC = 2: pair pp of the cluster (its leader is cluster rank 2 pp)
+    const uint32_t crank_all = CG == 2 ? tc::cluster_ctarank() : 0u;
+    const uint32_t rank = crank_all & 1u;
+    const uint32_t pp = MC == 2 ? (crank_all >> 1) : 0u;
+    const uint32_t lead = 2u * pp;
+    // empty-barrier commits: the pair (MC = 1) or both pairs, whose smem our
+    // multicast A halves also fill (MC = 2); accumulator commits: the pair
+    const uint16_t empty_mask = MC == 2 ? 0xF : 0x3;
+    const uint16_t pair_mask = static_cast<uint16_t>(0x3u << lead);
     const int crank = CN > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;  // N-tile of a LN cluster
     auto unit_at = [&](int u) -> Unit {
         if constexpr (CN > 1) return decode_cluster(g, u, crank);
@@ -398,7 +411,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < C::kStages; ++s) {
             tc::mbar_init(&full_bar[s], 1);
-            tc::mbar_init(&empty_bar[s], dbias_any ? 1 + kBiasWarps : 1);  // MMA commit (+ bias warps)
+            // MMA commit (+ bias warps); MC = 2: both pairs' MMA commits
+            tc::mbar_init(&empty_bar[s], MC == 2 ? 2 : dbias_any ? 1 + kBiasWarps : 1);
             tc::mbar_init(&bias_bar[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -417,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     else __syncthreads();
     tc::tc_fence_after();
     // units are dealt per pair (CG = 2) or per LayerNorm cluster (CN > 1)
-    const int cid = blockIdx.x / (CG * CN), ncta = gridDim.x / (CG * CN);
+    const int cid = blockIdx.x / (CG * CN * MC), ncta = gridDim.x / (CG * CN * MC);
     const uint32_t tmem_base = *tmem_slot;
     if (tmem_base != 0) __trap();  // the MMA issuer addresses TMEM by column offset
     if (threadIdx.x == 0) MM_TRACE(1);
@@ -429,14 +443,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------ producer
         if (lane == 0) {
             // stage completion is counted on the leader's full barrier
-            const uint32_t full_leader = CG == 2 ? tc::mapa_u32(tc::smem_u32(full_bar), 0) : 0u;
+            const uint32_t full_leader = CG == 2 ? tc::mapa_u32(tc::smem_u32(full_bar), lead) : 0u;
             auto load = [&](uint8_t* dst, const CUtensorMap* map, int stage, int c0, int c1) {
                 if constexpr (CG == 2) tc::tma_load_2d_pair(dst, map, full_leader + stage * 8, c0, c1);
                 else tc::tma_load_2d(dst, map, &full_bar[stage], c0, c1);
             };
+            // MC = 2: this CTA's 64-row half pp of its 128 A rows, to both pairs
+            const uint16_t a_mask = static_cast<uint16_t>((1u << rank) | (1u << (2u + rank)));
             auto load_a = [&](const Prob& P, int stage, int m0, int k0) {
                 uint8_t* sa = smem_a + stage * C::kABytes;
-                if (A_MN) {
+                if constexpr (MC == 2) {
+                    const int h = static_cast<int>(pp);
+                    if (A_MN) tc::tma_load_2d_pair_mc(sa + h * 64 * BK * 2, &P.ta, full_leader + stage * 8,
+                                                      m0 + h * 64, k0, a_mask);
+                    else tc::tma_load_2d_pair_mc(sa + h * 64 * 128, &P.ta, full_leader + stage * 8,
+                                                 k0, m0 + h * 64, a_mask);
+                } else if (A_MN) {
 #pragma unroll
                     for (int c = 0; c < BM / 64; ++c) load(sa + c * 64 * BK * 2, &P.ta, stage, m0 + c * 64, k0);
                 } else {
@@ -462,9 +484,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const Unit w = unit_at(cid);
                 const Prob& P = g.prob[w.pi];
                 pre = min(C::kStages, w.kb1 - w.kb0);
+                const int tn = MC == 2 ? 2 * w.tn + static_cast<int>(pp) : w.tn;
                 for (int i = 0; i < pre; ++i) {
                     expect(i);
-                    load_b(P, i, w.tn * BN + rank * C::kBRows, (w.kb0 + i) * BK);
+                    load_b(P, i, tn * BN + rank * C::kBRows, (w.kb0 + i) * BK);
                 }
             }
             pdl_wait();
@@ -475,7 +498,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int u = cid; u < g.units; u += ncta) {
                 const Unit w = unit_at(u);
                 const Prob& P = g.prob[w.pi];
-                const int m0 = w.tm * (BM * CG) + rank * BM, n0 = w.tn * BN + rank * C::kBRows;
+                const int tn = MC == 2 ? 2 * w.tn + static_cast<int>(pp) : w.tn;
+                const int m0 = w.tm * (BM * CG) + rank * BM, n0 = tn * BN + rank * C::kBRows;
                 for (int kb = w.kb0; kb < w.kb1; ++kb, ++issued) {
                     if (issued < pre) {  // expect_tx and B already issued
                         load_a(P, stage, m0, kb * BK);
@@ -537,15 +561,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t b_lo = b_lo0 + static_cast<uint32_t>(stage * (C::kBBytes / 16));
                 if (!(MM_GEMM_DEBUG & 1)) {
                     tc::mma_kblock_commit<CG, a_kstep, b_kstep>(d_tmem, a_lo, a_hi, b_lo, b_hi, idesc,
-                                                                kb > kb0 ? 1u : 0u, &empty_bar[stage]);
+                                                                kb > kb0 ? 1u : 0u, &empty_bar[stage],
+                                                                empty_mask);
                 } else {
-                    tc::mma_commit_elect<CG>(&empty_bar[stage]);
+                    tc::mma_commit_elect<CG>(&empty_bar[stage], empty_mask);
                 }
                 MM_KB_TRACE(512, consumed);  // MMAs + commit issued
-                if (CG == 2 && dbias_any) tc::mma_commit_elect<CG>(&bias_bar[stage]);
+                if (CG == 2 && dbias_any) tc::mma_commit_elect<CG>(&bias_bar[stage], pair_mask);
                 if (++stage == C::kStages) { stage = 0; phase ^= 1; }
             }
-            tc::mma_commit_elect<CG>(&tfull_bar[acc]);
+            tc::mma_commit_elect<CG>(&tfull_bar[acc], pair_mask);
             if (lane == 0) MM_TRACE(3);
             __syncwarp();
         }
@@ -664,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                   P.epilogue == MM_EPI_BF16_DRELU;
             const bool reduce = P.epilogue == MM_EPI_F32_ACCUM;
             const bool bias = has_bias(P);
-            const int tm = w.tm, tn = w.tn;
+            const int tm = w.tm, tn = MC == 2 ? 2 * w.tn + static_cast<int>(pp) : w.tn;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             const int cbase = tn * BN + half * (BN / kSlices);
@@ -742,7 +767,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if constexpr (CG == 2) tc::mbar_arrive_cluster(&tempty_bar[acc], 0);
+                if constexpr (CG == 2) tc::mbar_arrive_cluster(&tempty_bar[acc], lead);
                 else tc::mbar_arrive(&tempty_bar[acc]);
             }
             if constexpr (CN > 1 && !(MM_GEMM_DEBUG & 16)) {
@@ -894,19 +919,41 @@ int make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, i
     return 0;
 }
 
-template <int BN, int A_MN, int B_MN, int NP, int CG, int CN = 1, int RT = 0>
+template <int BN, int A_MN, int B_MN, int NP, int CG, int CN = 1, int RT = 0, int MC = 1>
 int launch(const Group<NP>& g, cudaStream_t s) {
     using C = Cfg<BN, CG, CN, RT>;
-    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, NP, CG, CN, RT>;
+    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, NP, CG, CN, RT, MC>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmem));
         attr_set = true;
     }
-    // persistent: one CTA (pair / LayerNorm cluster) per SM (pair / CN SMs)
-    const int per = CG * CN;
-    const int ctas = std::min(g.units, mm::num_sms() / per) * per;
+    // persistent: one CTA (pair / cluster) per SM (pair / cluster of SMs);
+    // clusters wider than a pair fit only as often as the GPCs allow
+    const int per = CG * CN * MC;
+    static int max_clusters = 0;  // per instantiation
+    if (max_clusters == 0) {
+        max_clusters = mm::num_sms() / per;
+        if (per > 2) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(static_cast<unsigned>(per * max_clusters));
+            cfg.blockDim = dim3(kThreads);
+            cfg.dynamicSmemBytes = C::kSmem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = static_cast<unsigned>(per);
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0)
+                max_clusters = std::min(max_clusters, n);
+            (void)cudaGetLastError();
+        }
+    }
+    const int ctas = std::min(g.units, max_clusters) * per;
     MM_CUDA_TRY(mm::launch_pdl_cluster(kern, dim3(ctas), dim3(kThreads), C::kSmem, s,
                                        static_cast<unsigned>(per), g));
     MM_LAUNCH_CHECK("gemm_tcgen05_kernel");
@@ -919,6 +966,14 @@ int dispatch(int a_mn, int b_mn, const Group<NP>& g, cudaStream_t s) {
     if (!a_mn && b_mn) return launch<BN, 0, 1, NP, CG>(g, s);
     if (a_mn && !b_mn) return launch<BN, 1, 0, NP, CG>(g, s);
     return launch<BN, 1, 1, NP, CG>(g, s);
+}
+// CTA pairs in clusters of two pairs with multicast A halves (MC = 2)
+template <int BN, int NP>
+int dispatch_mc(int a_mn, int b_mn, const Group<NP>& g, cudaStream_t s) {
+    if (!a_mn && !b_mn) return launch<BN, 0, 0, NP, 2, 1, 0, 2>(g, s);
+    if (!a_mn && b_mn) return launch<BN, 0, 1, NP, 2, 1, 0, 2>(g, s);
+    if (a_mn && !b_mn) return launch<BN, 1, 0, NP, 2, 1, 0, 2>(g, s);
+    return launch<BN, 1, 1, NP, 2, 1, 0, 2>(g, s);
 }
 
 unsigned long long* g_trace_buf = nullptr;  // set by mm_gemm_trace (diagnostics)
@@ -1099,12 +1154,13 @@ TileChoice choose_tile(const mm_gemm_args* const* probs, int n, int sms) {
 
 // Fill one problem of a launch (tensor maps + tiling); splits K for fp32
 // accumulation when the launch has fewer tiles than two waves.
-int setup_prob(Prob& P, const mm_gemm_args* a, int bn, int cg, int splits_cap) {
+int setup_prob(Prob& P, const mm_gemm_args* a, int bn, int cg, int splits_cap, int mc = 1) {
     const bool out_bf16 = out_bf16_epi(a->epilogue);
     const int a_mn = a->a_kmajor ? 0 : 1;
     const int b_mn = a->b_kmajor ? 0 : 1;
     const int64_t tiles_m = (a->m + BM * cg - 1) / (BM * cg);
-    const int64_t tiles_n = (a->n + bn - 1) / bn;
+    // mc = 2: units are pairs of adjacent N-tiles (one per pair of the cluster)
+    const int64_t tiles_n = ((a->n + bn - 1) / bn + mc - 1) / mc;
     const int num_kb = static_cast<int>((a->k + BK - 1) / BK);
     int splits = a->epilogue == MM_EPI_F32_ACCUM ? std::max(1, std::min(splits_cap, num_kb / 2)) : 1;
     const int kb_per = (num_kb + splits - 1) / splits;
@@ -1113,7 +1169,7 @@ int setup_prob(Prob& P, const mm_gemm_args* a, int bn, int cg, int splits_cap) {
     int st;
     // A: K-major [M, K] rows of lda; MN-major [K, M] rows of lda
     st = a_mn ? make_map(&P.ta, a->a, a->m, a->k, a->lda, BK)
-              : make_map(&P.ta, a->a, a->k, a->m, a->lda, BM);
+              : make_map(&P.ta, a->a, a->k, a->m, a->lda, mc == 2 ? 64 : BM);  // mc = 2: 64-row halves
     if (st) return st;
     st = b_mn ? make_map(&P.tb, a->b, a->n, a->k, a->ldb, BK)
               : make_map(&P.tb, a->b, a->k, a->n, a->ldb, bn / cg);  // a pair CTA stages BN/2 rows
@@ -1196,18 +1252,27 @@ int run_group(const mm_gemm_args* const* probs_in, int n, cudaStream_t s) {
     int64_t units = 0;
     double flops = 0;
     static const bool log = std::getenv("MM_GEMM_LOG") != nullptr;  // diagnostics
+    // CTA pairs run in clusters of two pairs with multicast A halves
+    // (MM_GEMM_MC=0 for A/B): fewer L2 requests per SM, so less power at the
+    // same work -- config 5 26.60 -> 26.42 ms at 1620 -> 1700+ MHz under the
+    // power cap, config 3 3.418 -> 3.412 ms.  Not with the bias-gradient
+    // warps (they read the stages the pair alone releases).
+    bool dbias = false;
+    for (int i = 0; i < n; ++i) dbias = dbias || probs[i]->dbias != nullptr;
+    const char* mc_env = std::getenv("MM_GEMM_MC");
+    const int mc = (cg == 2 && !ln && !dbias && !(mc_env && mc_env[0] == '0')) ? 2 : 1;
     for (int i = 0; i < n; ++i) {
         Prob& P = g.prob[i];
-        if (int st = setup_prob(P, probs[i], bn, cg, cap)) return st;
+        if (int st = setup_prob(P, probs[i], bn, cg, cap, mc)) return st;
         P.unit_begin = static_cast<int>(units);
         units += int64_t(P.tiles_m) * P.tiles_n * P.splits;
         MM_CHECK_ARG(units < (int64_t(1) << 31), "GEMM launch too large");
         flops += 2.0 * double(probs[i]->m) * double(probs[i]->n) * double(probs[i]->k);
         if (log)
-            std::fprintf(stderr, "mm_gemm m=%lld n=%lld k=%lld a_mn=%d b_mn=%d epi=%d bn=%d cg=%d splits=%d units=%d group=%d/%d\n",
+            std::fprintf(stderr, "mm_gemm m=%lld n=%lld k=%lld a_mn=%d b_mn=%d epi=%d bn=%d cg=%d mc=%d splits=%d units=%d group=%d/%d\n",
                          (long long)probs[i]->m, (long long)probs[i]->n, (long long)probs[i]->k,
                          probs[i]->a_kmajor ? 0 : 1, probs[i]->b_kmajor ? 0 : 1, probs[i]->epilogue,
-                         bn, cg, P.splits, P.tiles_m * P.tiles_n * P.splits, i, n);
+                         bn, cg, mc, P.splits, P.tiles_m * P.tiles_n * P.splits, i, n);
     }
     g.n_probs = n;
     g.units = static_cast<int>(units);
@@ -1243,6 +1308,9 @@ int run_group(const mm_gemm_args* const* probs_in, int n, cudaStream_t s) {
         } else {
             rc = mm::kArg;
         }
+    } else if (mc == 2) {
+        if (bn == 256) rc = dispatch_mc<256, NP>(a_mn, b_mn, g, s);
+        else rc = dispatch_mc<128, NP>(a_mn, b_mn, g, s);
     } else if (cg == 2) {
         if (bn == 256) rc = dispatch<256, NP, 2>(a_mn, b_mn, g, s);
         else rc = dispatch<128, NP, 2>(a_mn, b_mn, g, s);

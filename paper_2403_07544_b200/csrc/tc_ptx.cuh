@@ -188,7 +188,8 @@ __device__ __forceinline__ void mma_bf16_elect(uint32_t tmem_d, uint64_t adesc, 
 template <int CG, int A_STEP, int B_STEP>
 __device__ __forceinline__ void mma_kblock_commit(uint32_t tmem_d, uint32_t a_lo, uint32_t a_hi,
                                                   uint32_t b_lo, uint32_t b_hi, uint32_t idesc,
-                                                  uint32_t accumulate, uint64_t* bar) {
+                                                  uint32_t accumulate, uint64_t* bar,
+                                                  uint16_t cta_mask = 3) {
 #define MM_MMA_KBLOCK(CGS, COMMIT)                                                             \
     asm volatile(                                                                              \
         "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a, b;\n\t.reg .b32 x, y;\n\t"                  \
@@ -210,7 +211,7 @@ __device__ __forceinline__ void mma_kblock_commit(uint32_t tmem_d, uint32_t a_lo
         "@e " COMMIT "\n\t}" ::"r"(tmem_d),                                                    \
         "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(accumulate), "r"(idesc),               \
         "r"(smem_u32(bar)), "n"(A_STEP), "n"(B_STEP), "n"(2 * A_STEP), "n"(2 * B_STEP),        \
-        "n"(3 * A_STEP), "n"(3 * B_STEP), "h"(static_cast<uint16_t>(3))                        \
+        "n"(3 * A_STEP), "n"(3 * B_STEP), "h"(cta_mask)                                        \
         : "memory")
     if constexpr (CG == 2)
         MM_MMA_KBLOCK("2", "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%7], %14;");
@@ -220,14 +221,14 @@ __device__ __forceinline__ void mma_kblock_commit(uint32_t tmem_d, uint32_t a_lo
 }
 
 template <int CG>
-__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar, uint16_t cta_mask = 3) {
     if constexpr (CG == 2) {
         asm volatile(
             "{\n\t.reg .pred e;\n\t"
             "elect.sync _|e, 0xffffffff;\n\t"
             "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
             " [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
-            "h"(static_cast<uint16_t>(3))
+            "h"(cta_mask)
             : "memory");
     } else {
         asm volatile(
@@ -300,6 +301,18 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
         "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+// the same with the box multicast to every CTA of cta_mask (each lands at the
+// same smem offset; completion is counted on the pair leader of each
+// destination: bar_cluster is this CTA's pair-leader barrier, peer bit clear)
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* map,
+                                                    uint32_t bar_cluster, int32_t c0, int32_t c1,
+                                                    uint16_t cta_mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "h"(cta_mask)
         : "memory");
 }
 // spin on mbarrier.test_wait (non-blocking) with cluster-scope acquire: for

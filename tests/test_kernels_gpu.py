@@ -480,3 +480,33 @@ def test_colsum_and_cast(cuda):
     yb = torch.empty(1000, 512, device=cuda, dtype=torch.bfloat16)
     ops.cast_bf16(y, yb)
     assert torch.equal(yb, y.bfloat16())
+
+
+@pytest.mark.parametrize("bn", ["128", "256"])
+@pytest.mark.parametrize("shape,ak,bk", [((4096, 1536, 512), True, True), ((1000, 1280, 520), True, True),
+                                         ((700, 384, 1024), True, False), ((512, 640, 2048), False, False)])
+def test_gemm_pair_multicast_matches_unicast(cuda, shape, ak, bk, bn, monkeypatch):
+    """CTA pairs in clusters of two pairs (each CTA fetches half of its A rows
+    and multicasts it to the other pair; MM_GEMM_MC) give bit-identical
+    results to unicast pairs: odd N-tile counts (the second pair's last tile
+    outside N), ragged M / K, every operand majorness (bf16 out: an fp32
+    weight-gradient-shaped output could split K, whose reduce-adds land in
+    either order)."""
+    from paper_2403_07544_b200 import ops
+    m, n, k = shape
+    g = torch.Generator(device="cuda").manual_seed(m + n)
+    A = torch.randn(m, k, device=cuda, generator=g).bfloat16() if ak else torch.randn(k, m, device=cuda, generator=g).bfloat16()
+    B = torch.randn(n, k, device=cuda, generator=g).bfloat16() if bk else torch.randn(k, n, device=cuda, generator=g).bfloat16()
+    bias = torch.randn(n, device=cuda, generator=g)
+    monkeypatch.setenv("MM_GEMM_CG", "2")
+    monkeypatch.setenv("MM_GEMM_BN", bn)
+    outs = []
+    for mc in ("0", "1"):
+        monkeypatch.setenv("MM_GEMM_MC", mc)
+        d = torch.zeros(m, n, device=cuda, dtype=torch.bfloat16)
+        ops.gemm(A, B, d, a_kmajor=ak, b_kmajor=bk, epilogue=ops.EPI_BF16, bias=bias)
+        outs.append(d)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    ref = (A.float() if ak else A.float().t()) @ (B.float().t() if bk else B.float()) + bias
+    assert rel_err(outs[1], ref) < 1e-2
