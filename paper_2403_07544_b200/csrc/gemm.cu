@@ -215,18 +215,18 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 }
 
 // Epilogue math for one row (this thread) x 32 columns held in registers.
-__device__ __forceinline__ bool has_bias(const Prob& p) {
-    const int ep = p.epilogue;
+// ep: the problem's epilogue -- a compile-time constant in the specialised
+// instantiations (EK >= 0), so only its path is compiled
+__device__ __forceinline__ bool has_bias(const Prob& p, int ep) {
     return p.bias && (ep == MM_EPI_BF16 || ep == MM_EPI_BF16_RELU || ep == MM_EPI_F32 ||
                       ep == MM_EPI_F32_RESID || ep == MM_EPI_F32_RESID_LN);
 }
 
 // bv: this lane's bias value for column col0 + lane (preloaded per tile);
 // resid_done: the residual is added by the caller (parked in TMEM)
-__device__ __forceinline__ void epilogue_math(const Prob& p, int64_t row, int64_t col0,
+__device__ __forceinline__ void epilogue_math(const Prob& p, int ep, int64_t row, int64_t col0,
                                               float (&acc)[32], float bv, bool resid_done = false) {
-    const int ep = p.epilogue;
-    if (has_bias(p)) {
+    if (has_bias(p, ep)) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) acc[j] += __shfl_sync(0xffffffffu, bv, j);
     }
@@ -356,7 +356,10 @@ __device__ __forceinline__ Unit decode(const Group<NP>& g, int u) {
 // same 256-row block; each CTA fetches half of its 128 A rows and multicasts
 // it to the CTA at the same pair position in the other pair, so every SM
 // requests 3/4 of the operand bytes per k-block (cuBLAS's 2x2 / 2cta shape).
-template <int BN, int A_MN, int B_MN, int NP, int CG, int CN = 1, int RT = 0, int MC = 1>
+// EK >= 0: an instantiation for one epilogue (the single-problem launches of
+// the step), whose code is a fraction of the generic kernel's -- a launch
+// after another GEMM instantiation pays less instruction-fetch warm-up
+template <int BN, int A_MN, int B_MN, int NP, int CG, int CN = 1, int RT = 0, int MC = 1, int EK = -1>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ Group<NP> g) {
     using C = Cfg<BN, CG, CN, RT>;
@@ -685,15 +688,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int u = cid; u < g.units; u += ncta, ++local) {
             const Unit w = unit_at(u);
             const Prob& P = g.prob[w.pi];
-            const bool out_bf16 = P.epilogue == MM_EPI_BF16 || P.epilogue == MM_EPI_BF16_RELU ||
-                                  P.epilogue == MM_EPI_BF16_DRELU;
-            const bool reduce = P.epilogue == MM_EPI_F32_ACCUM;
-            const bool bias = has_bias(P);
+            const int epi = EK >= 0 ? EK : P.epilogue;
+            const bool out_bf16 = epi == MM_EPI_BF16 || epi == MM_EPI_BF16_RELU || epi == MM_EPI_BF16_DRELU;
+            const bool reduce = epi == MM_EPI_F32_ACCUM;
+            const bool bias = has_bias(P, epi);
             const int tm = w.tm, tn = MC == 2 ? 2 * w.tn + static_cast<int>(pp) : w.tn;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             const int cbase = tn * BN + half * (BN / kSlices);
-            const bool resid_tm = C::kResidTmem && P.epilogue == MM_EPI_F32_RESID;
+            const bool resid_tm = C::kResidTmem && epi == MM_EPI_F32_RESID;
             if constexpr (C::kResidTmem) {
                 if (resid_tm && !(local == 0 && resid_pre)) resid_to_tmem(P, tm, cbase);
             }
@@ -725,8 +728,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float f[32];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-                    epilogue_math(P, row, col0, f, bv[c], resid_tm);
-                    if (P.epilogue == MM_EPI_BF16_RELU && P.relu_mask && row < P.m) {
+                    epilogue_math(P, epi, row, col0, f, bv[c], resid_tm);
+                    if (epi == MM_EPI_BF16_RELU && P.relu_mask && row < P.m) {
                         uint32_t bits = 0;
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
@@ -919,10 +922,10 @@ int make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, i
     return 0;
 }
 
-template <int BN, int A_MN, int B_MN, int NP, int CG, int CN = 1, int RT = 0, int MC = 1>
+template <int BN, int A_MN, int B_MN, int NP, int CG, int CN = 1, int RT = 0, int MC = 1, int EK = -1>
 int launch(const Group<NP>& g, cudaStream_t s) {
     using C = Cfg<BN, CG, CN, RT>;
-    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, NP, CG, CN, RT, MC>;
+    auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, NP, CG, CN, RT, MC, EK>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -966,6 +969,26 @@ int dispatch(int a_mn, int b_mn, const Group<NP>& g, cudaStream_t s) {
     if (!a_mn && b_mn) return launch<BN, 0, 1, NP, CG>(g, s);
     if (a_mn && !b_mn) return launch<BN, 1, 0, NP, CG>(g, s);
     return launch<BN, 1, 1, NP, CG>(g, s);
+}
+// single-problem 128-wide single-CTA launches, one instantiation per
+// epilogue of the step's hot shapes (forward: K-major A and B; dgrad:
+// MN-major B); kNotSpecialised: use the generic instantiation
+constexpr int kNotSpecialised = 1;  // (library status codes are <= 0)
+template <int NP>
+int dispatch_epi(int a_mn, int b_mn, int epi, const Group<NP>& g, cudaStream_t s) {
+    if constexpr (NP == 1) {
+        if (!a_mn && !b_mn) {
+            if (epi == MM_EPI_BF16) return launch<128, 0, 0, 1, 1, 1, 0, 1, MM_EPI_BF16>(g, s);
+            if (epi == MM_EPI_BF16_RELU) return launch<128, 0, 0, 1, 1, 1, 0, 1, MM_EPI_BF16_RELU>(g, s);
+            if (epi == MM_EPI_F32) return launch<128, 0, 0, 1, 1, 1, 0, 1, MM_EPI_F32>(g, s);
+        } else if (!a_mn && b_mn) {
+            if (epi == MM_EPI_BF16) return launch<128, 0, 1, 1, 1, 1, 0, 1, MM_EPI_BF16>(g, s);
+            if (epi == MM_EPI_BF16_DRELU) return launch<128, 0, 1, 1, 1, 1, 0, 1, MM_EPI_BF16_DRELU>(g, s);
+            if (epi == MM_EPI_F32) return launch<128, 0, 1, 1, 1, 1, 0, 1, MM_EPI_F32>(g, s);
+            if (epi == MM_EPI_F32_ACCUM) return launch<128, 0, 1, 1, 1, 1, 0, 1, MM_EPI_F32_ACCUM>(g, s);
+        }
+    }
+    return kNotSpecialised;
 }
 // CTA pairs in clusters of two pairs with multicast A halves (MC = 2)
 template <int BN, int NP>
@@ -1293,6 +1316,10 @@ int run_group(const mm_gemm_args* const* probs_in, int n, cudaStream_t s) {
     }
     const int a_mn = probs[0]->a_kmajor ? 0 : 1;
     const int b_mn = probs[0]->b_kmajor ? 0 : 1;
+    static const bool specialize = [] {
+        const char* e = std::getenv("MM_GEMM_SPECIALIZE");
+        return !(e && e[0] == '0');
+    }();
     int rc;
     if (ln) {
         // units are 128-row blocks; a cluster of N / 128 CTAs shares each one
@@ -1316,6 +1343,9 @@ int run_group(const mm_gemm_args* const* probs_in, int n, cudaStream_t s) {
         else rc = dispatch<128, NP, 2>(a_mn, b_mn, g, s);
     } else if (NP == 1 && bn == 128 && !a_mn && !b_mn && probs[0]->epilogue == MM_EPI_F32_RESID) {
         rc = launch<128, 0, 0, NP, 1, 1, 1>(g, s);  // residual parked in TMEM
+    } else if (NP == 1 && bn == 128 && specialize &&
+               (rc = dispatch_epi<NP>(a_mn, b_mn, probs[0]->epilogue, g, s)) != kNotSpecialised) {
+        // one epilogue's instantiation (MM_GEMM_SPECIALIZE=0 for A/B)
     } else {
         if (bn == 256) rc = dispatch<256, NP, 1>(a_mn, b_mn, g, s);
         else if (bn == 192) rc = dispatch<192, NP, 1>(a_mn, b_mn, g, s);
