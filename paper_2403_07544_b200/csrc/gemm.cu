@@ -401,7 +401,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (CN > 1) return decode_cluster(g, u, crank);
         else return decode(g, u);
     };
-    const bool dbias_any = g.any_dbias != 0;
+    // bias gradients need an MN-major A (check_args): compiled out otherwise
+    const bool dbias_any = A_MN && g.any_dbias != 0;
     if (threadIdx.x == 0) MM_TRACE(0);
 
     if (warp == 0 && lane == 0) {
@@ -1336,16 +1337,22 @@ int run_group(const mm_gemm_args* const* probs_in, int n, cudaStream_t s) {
             rc = mm::kArg;
         }
     } else if (mc == 2) {
-        if (bn == 256) rc = dispatch_mc<256, NP>(a_mn, b_mn, g, s);
+        if (NP == 1 && specialize && bn == 128 && !a_mn && b_mn && probs[0]->epilogue == MM_EPI_F32)
+            rc = launch<128, 0, 1, NP, 2, 1, 0, 2, MM_EPI_F32>(g, s);  // the generator dgrad
+        else if (bn == 256) rc = dispatch_mc<256, NP>(a_mn, b_mn, g, s);
         else rc = dispatch_mc<128, NP>(a_mn, b_mn, g, s);
     } else if (cg == 2) {
         if (bn == 256) rc = dispatch<256, NP, 2>(a_mn, b_mn, g, s);
         else rc = dispatch<128, NP, 2>(a_mn, b_mn, g, s);
     } else if (NP == 1 && bn == 128 && !a_mn && !b_mn && probs[0]->epilogue == MM_EPI_F32_RESID) {
-        rc = launch<128, 0, 0, NP, 1, 1, 1>(g, s);  // residual parked in TMEM
+        // residual parked in TMEM; the RESID epilogue alone
+        if (specialize) rc = launch<128, 0, 0, NP, 1, 1, 1, 1, MM_EPI_F32_RESID>(g, s);
+        else rc = launch<128, 0, 0, NP, 1, 1, 1>(g, s);
     } else if (NP == 1 && bn == 128 && specialize &&
                (rc = dispatch_epi<NP>(a_mn, b_mn, probs[0]->epilogue, g, s)) != kNotSpecialised) {
         // one epilogue's instantiation (MM_GEMM_SPECIALIZE=0 for A/B)
+    } else if (NP == 1 && bn == 256 && specialize && !a_mn && !b_mn && probs[0]->epilogue == MM_EPI_BF16) {
+        rc = launch<256, 0, 0, NP, 1, 1, 0, 1, MM_EPI_BF16>(g, s);  // the generator forward
     } else {
         if (bn == 256) rc = dispatch<256, NP, 1>(a_mn, b_mn, g, s);
         else if (bn == 192) rc = dispatch<192, NP, 1>(a_mn, b_mn, g, s);
