@@ -991,6 +991,23 @@ int dispatch_epi(int a_mn, int b_mn, int epi, const Group<NP>& g, cudaStream_t s
     }
     return kNotSpecialised;
 }
+// the same for 256-wide tiles: single CTAs (MC = 1) and clustered CTA pairs
+// (MC = 2) -- the config-5 shapes and the generator
+template <int NP, int CG, int MC>
+int dispatch_epi256(int a_mn, int b_mn, int epi, const Group<NP>& g, cudaStream_t s) {
+    if constexpr (NP == 1) {
+        if (!a_mn && !b_mn) {
+            if (epi == MM_EPI_BF16) return launch<256, 0, 0, 1, CG, 1, 0, MC, MM_EPI_BF16>(g, s);
+            if (epi == MM_EPI_BF16_RELU) return launch<256, 0, 0, 1, CG, 1, 0, MC, MM_EPI_BF16_RELU>(g, s);
+            if (epi == MM_EPI_F32_RESID) return launch<256, 0, 0, 1, CG, 1, 0, MC, MM_EPI_F32_RESID>(g, s);
+        } else if (!a_mn && b_mn) {
+            if (epi == MM_EPI_BF16) return launch<256, 0, 1, 1, CG, 1, 0, MC, MM_EPI_BF16>(g, s);
+            if (epi == MM_EPI_BF16_DRELU) return launch<256, 0, 1, 1, CG, 1, 0, MC, MM_EPI_BF16_DRELU>(g, s);
+            if (epi == MM_EPI_F32) return launch<256, 0, 1, 1, CG, 1, 0, MC, MM_EPI_F32>(g, s);
+        }
+    }
+    return kNotSpecialised;
+}
 // CTA pairs in clusters of two pairs with multicast A halves (MC = 2)
 template <int BN, int NP>
 int dispatch_mc(int a_mn, int b_mn, const Group<NP>& g, cudaStream_t s) {
@@ -1339,7 +1356,9 @@ int run_group(const mm_gemm_args* const* probs_in, int n, cudaStream_t s) {
     } else if (mc == 2) {
         if (NP == 1 && specialize && bn == 128 && !a_mn && b_mn && probs[0]->epilogue == MM_EPI_F32)
             rc = launch<128, 0, 1, NP, 2, 1, 0, 2, MM_EPI_F32>(g, s);  // the generator dgrad
-        else if (bn == 256) rc = dispatch_mc<256, NP>(a_mn, b_mn, g, s);
+        else if (NP == 1 && specialize && bn == 256 &&
+                 (rc = dispatch_epi256<NP, 2, 2>(a_mn, b_mn, probs[0]->epilogue, g, s)) != kNotSpecialised) {
+        } else if (bn == 256) rc = dispatch_mc<256, NP>(a_mn, b_mn, g, s);
         else rc = dispatch_mc<128, NP>(a_mn, b_mn, g, s);
     } else if (cg == 2) {
         if (bn == 256) rc = dispatch<256, NP, 2>(a_mn, b_mn, g, s);
@@ -1351,8 +1370,9 @@ int run_group(const mm_gemm_args* const* probs_in, int n, cudaStream_t s) {
     } else if (NP == 1 && bn == 128 && specialize &&
                (rc = dispatch_epi<NP>(a_mn, b_mn, probs[0]->epilogue, g, s)) != kNotSpecialised) {
         // one epilogue's instantiation (MM_GEMM_SPECIALIZE=0 for A/B)
-    } else if (NP == 1 && bn == 256 && specialize && !a_mn && !b_mn && probs[0]->epilogue == MM_EPI_BF16) {
-        rc = launch<256, 0, 0, NP, 1, 1, 0, 1, MM_EPI_BF16>(g, s);  // the generator forward
+    } else if (NP == 1 && bn == 256 && cg == 1 && specialize &&
+               (rc = dispatch_epi256<NP, 1, 1>(a_mn, b_mn, probs[0]->epilogue, g, s)) != kNotSpecialised) {
+        // the generator forward, config 5's 256-wide single-CTA launches
     } else {
         if (bn == 256) rc = dispatch<256, NP, 1>(a_mn, b_mn, g, s);
         else if (bn == 192) rc = dispatch<192, NP, 1>(a_mn, b_mn, g, s);
