@@ -1,7 +1,7 @@
 # round-2 final evidence (second pass, final build): tests, smoke, bench lines,
 # GEMM spans, ncu launch lists + GEMM DRAM traffic, cuBLAS tables, and
 # ncu --set full captures of the step's top kernels
-D=gpurun_out/r02final3
+D=gpurun_out/r02final4
 mkdir -p $D
 timeout 2400 python -m pytest tests -q -m gpu -p no:cacheprovider > $D/gpu_all.log 2>&1
 tail -n 1 $D/gpu_all.log
