@@ -1,7 +1,7 @@
 # round-2 final evidence (second pass, final build): tests, smoke, bench lines,
 # GEMM spans, ncu launch lists + GEMM DRAM traffic, cuBLAS tables, and
 # ncu --set full captures of the step's top kernels
-D=gpurun_out/r02final4
+D=gpurun_out/r02final5
 mkdir -p $D
 timeout 2400 python -m pytest tests -q -m gpu -p no:cacheprovider > $D/gpu_all.log 2>&1
 tail -n 1 $D/gpu_all.log
@@ -25,6 +25,7 @@ full() {  # name, ncu selection args...
   local name=$1; shift
   timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on "$@" -o $D/$name python tools/profile_step.py > $D/ncu_$name.out 2>&1
   ncu -i $D/$name.ncu-rep --page details --csv > $D/ncu_${name}_details.csv 2>/dev/null
+  rm -f $D/$name.ncu-rep  # the merged gpurun_out/ must stay under 64 MiB
 }
 full gemm_ff1 -k regex:gemm_tcgen05 -s 2 -c 1
 full gemm_wgrad_dec -k regex:gemm_tcgen05 -s 99 -c 1
