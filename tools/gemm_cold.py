@@ -22,6 +22,8 @@ gam, bet = torch.ones(d, device=dev), torch.zeros(d, device=dev)
 y = torch.empty(T, d, device=dev, dtype=torch.bfloat16)
 mu, rs = torch.empty(T, device=dev), torch.empty(T, device=dev)
 ff1 = lambda: ops.gemm(h, W1, f, epilogue=ops.EPI_BF16_RELU, bias=b1)
+mask = torch.empty((T, F // 32), device=dev, dtype=torch.int32)
+ff1m = lambda: ops.gemm(h, W1, f, epilogue=ops.EPI_BF16_RELU, bias=b1, relu_mask=mask)
 other = lambda: ops.gemm(h, W, dx, b_kmajor=False, epilogue=ops.EPI_F32)
 ln = lambda: ops.layernorm_fwd(x, gam, bet, y, mu, rs)
 
@@ -47,6 +49,8 @@ def spans(seq, reps=20):
 L.mm_gemm_spans.argtypes = [ctypes.c_int] + [ctypes.c_void_p] * 5
 for name, seq in (("A ff1 only", [ff1]), ("B ff1 + LN", [ff1, ln]),
                   ("C ff1 + LN + other GEMM", [ff1, ln, other]),
-                  ("E ff1 + other GEMM", [ff1, other])):
+                  ("E ff1 + other GEMM", [ff1, other]),
+                  ("F ff1 (ReLU mask) + LN + other", [ff1m, ln, other]),
+                  ("G ff1 (ReLU mask) only", [ff1m])):
     med, mean = spans(seq)
     print(f"{name:28s} ff1 span median {med:6.2f} us  mean {mean:6.2f} us", flush=True)

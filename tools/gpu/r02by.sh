@@ -1,0 +1,8 @@
+D=gpurun_out/r02by
+mkdir -p $D
+timeout 600 python -m pytest tests/test_kernels_gpu.py -q -x -k "relu or gemm" > $D/t.log 2>&1; tail -n 1 $D/t.log
+timeout 300 python tools/gemm_cold.py 2>&1 | tail -3
+for rep in 1 2; do
+  timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline > $D/c3_$rep.json 2> $D/c3_$rep.err
+  echo "c3 $(python -c "import json; d=json.loads(open('$D/c3_$rep.json').read().strip().splitlines()[-1]); print(d['ms_per_step'], d['roofline']['frac'], d['clocks']['sm_mhz'])")"
+done
