@@ -711,6 +711,10 @@ constexpr int kXentSmemVocab = 32768;
 #define MM_XENT_STREAM_THREADS 512
 #endif
 constexpr int kXsThreads = MM_XENT_STREAM_THREADS;
+#ifndef MM_XENT_BUFS
+#define MM_XENT_BUFS 3
+#endif
+constexpr int kXentBufs = MM_XENT_BUFS;  // logit rows in flight + the one being reduced
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -739,39 +743,43 @@ __global__ void __launch_bounds__(kXsThreads, 1) xent_stream_kernel(const uint16
     constexpr int VPT = kXentSmemVocab / kXsThreads / 8;  // 8-logit vectors per thread
     constexpr float kL2e = 1.4426950408889634f;
     extern __shared__ __align__(128) uint8_t xsm[];
-    __shared__ uint64_t bar[2];
+    __shared__ uint64_t bar[kXentBufs];
     __shared__ float red[kXsThreads / 32];
     uint16_t* const buf0 = reinterpret_cast<uint16_t*>(xsm);
     const uint32_t bytes = static_cast<uint32_t>(vocab) * 2u;
     const int nv = vocab / 8;
     if (threadIdx.x == 0) {
-        tc::mbar_init(&bar[0], 1);
-        tc::mbar_init(&bar[1], 1);
+        for (int i = 0; i < kXentBufs; ++i) tc::mbar_init(&bar[i], 1);
         tc::fence_barrier_init();
     }
     // each buffer is kXentSmemVocab wide; the tail past the vocab holds bf16
     // -inf (exp -> 0), so every thread's VPT vectors are unconditional
     for (int c = vocab + threadIdx.x; c < kXentSmemVocab; c += kXsThreads)
-        buf0[c] = buf0[kXentSmemVocab + c] = 0xff80u;
+        for (int i = 0; i < kXentBufs; ++i) buf0[i * kXentSmemVocab + c] = 0xff80u;
     __syncthreads();
     pdl_wait_release();
     const int64_t first = blockIdx.x, step = gridDim.x;
-    if (threadIdx.x == 0 && first < rows) {
-        tc::mbar_expect_tx(&bar[0], bytes);
-        tc::bulk_load_1d(buf0, logits + first * int64_t(vocab), bytes, &bar[0]);
+    if (threadIdx.x == 0) {  // the first kXentBufs - 1 rows in flight
+        for (int i = 0; i < kXentBufs - 1 && first + i * step < rows; ++i) {
+            tc::mbar_expect_tx(&bar[i], bytes);
+            tc::bulk_load_1d(buf0 + i * kXentSmemVocab, logits + (first + i * step) * int64_t(vocab), bytes, &bar[i]);
+        }
     }
     int it = 0;
     for (int64_t row = first; row < rows; row += step, ++it) {
-        const int b = it & 1;
-        // prefetch the next row into the other buffer (its previous row was
-        // fully consumed before the trailing __syncthreads of the last iteration)
-        if (threadIdx.x == 0 && row + step < rows) {
-            tc::mbar_expect_tx(&bar[b ^ 1], bytes);
-            tc::bulk_load_1d(buf0 + (b ^ 1) * kXentSmemVocab, logits + (row + step) * int64_t(vocab), bytes, &bar[b ^ 1]);
+        const int b = it % kXentBufs;
+        // prefetch kXentBufs - 1 rows ahead into the buffer the previous row
+        // used (fully consumed before the trailing __syncthreads of the last
+        // iteration)
+        const int64_t ahead = row + int64_t(kXentBufs - 1) * step;
+        if (threadIdx.x == 0 && ahead < rows) {
+            const int nb = (it + kXentBufs - 1) % kXentBufs;
+            tc::mbar_expect_tx(&bar[nb], bytes);
+            tc::bulk_load_1d(buf0 + nb * kXentSmemVocab, logits + ahead * int64_t(vocab), bytes, &bar[nb]);
         }
         const int label = labels[row];
         MM_DCHECK(label < vocab);
-        tc::mbar_wait(&bar[b], static_cast<uint32_t>((it >> 1) & 1));
+        tc::mbar_wait(&bar[b], static_cast<uint32_t>((it / kXentBufs) & 1));
         const uint16_t* lrow = buf0 + b * kXentSmemVocab;
         const uint4* lr = reinterpret_cast<const uint4*>(lrow);
         uint4* dr = reinterpret_cast<uint4*>(dlogits + row * int64_t(vocab));
@@ -1033,7 +1041,7 @@ extern "C" int mm_xent_fwd_bwd(const uint16_t* logits, const int32_t* labels, ui
     if (rows == 0) return 0;
     static const bool force_rowwise = std::getenv("MM_XENT_ROWWISE") != nullptr;  // diagnostics
     if (vocab <= kXentSmemVocab && !force_rowwise) {
-        const size_t smem = size_t(2) * kXentSmemVocab * 2;
+        const size_t smem = size_t(kXentBufs) * kXentSmemVocab * 2;
         MM_CUDA_TRY(cudaFuncSetAttribute(xent_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
         const unsigned grid = static_cast<unsigned>(std::min<int64_t>(rows, mm::num_sms()));
