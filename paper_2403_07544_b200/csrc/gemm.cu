@@ -1339,10 +1339,8 @@ int run_group(const mm_gemm_args* const* probs_in, int n, cudaStream_t s) {
     }
     const int a_mn = probs[0]->a_kmajor ? 0 : 1;
     const int b_mn = probs[0]->b_kmajor ? 0 : 1;
-    static const bool specialize = [] {
-        const char* e = std::getenv("MM_GEMM_SPECIALIZE");
-        return !(e && e[0] == '0');
-    }();
+    const char* spec_env = std::getenv("MM_GEMM_SPECIALIZE");  // read per call: tests toggle it
+    const bool specialize = !(spec_env && spec_env[0] == '0');
     int rc;
     if (ln) {
         // units are 128-row blocks; a cluster of N / 128 CTAs shares each one

@@ -510,3 +510,50 @@ def test_gemm_pair_multicast_matches_unicast(cuda, shape, ak, bk, bn, monkeypatc
     assert torch.equal(outs[0], outs[1])
     ref = (A.float() if ak else A.float().t()) @ (B.float().t() if bk else B.float()) + bias
     assert rel_err(outs[1], ref) < 1e-2
+
+
+@pytest.mark.parametrize("case", [
+    # (a_kmajor, b_kmajor, epilogue, bn, cg): every specialised instantiation
+    (True, True, "BF16", 128, 1), (True, True, "BF16_RELU", 128, 1), (True, True, "F32", 128, 1),
+    (True, True, "F32_RESID", 128, 1), (True, False, "BF16", 128, 1), (True, False, "BF16_DRELU", 128, 1),
+    (True, False, "F32", 128, 1), (True, False, "F32_ACCUM", 128, 1), (True, True, "BF16", 256, 1),
+    (True, True, "BF16_RELU", 256, 1), (True, True, "F32_RESID", 256, 1), (True, False, "F32", 256, 1),
+    (True, False, "BF16_DRELU", 256, 1), (True, True, "BF16", 256, 2), (True, False, "F32", 256, 2),
+    (True, False, "F32", 128, 2)])
+def test_gemm_specialised_matches_generic(cuda, case, monkeypatch):
+    """The per-epilogue instantiations (MM_GEMM_SPECIALIZE) are bit-identical
+    to the generic kernel on ragged shapes, with bias / residual / ReLU-mask
+    operands as the epilogue takes them."""
+    from paper_2403_07544_b200 import ops
+    ak, bk, epi_name, bn, cg = case
+    epi = getattr(ops, "EPI_" + epi_name)
+    # (an fp32 accumulation with more k-blocks could split K, whose partial
+    # sums reduce-add in either order)
+    m, n, k = 1000, 520 if bn == 128 else 776, 136 if epi_name == "F32_ACCUM" else 392
+    g = torch.Generator(device="cuda").manual_seed(bn + cg + epi)
+    A = torch.randn(m, k, device=cuda, generator=g).bfloat16()
+    B = (torch.randn(n, k, device=cuda, generator=g) if bk else torch.randn(k, n, device=cuda, generator=g)).bfloat16()
+    bias = torch.randn(n, device=cuda, generator=g)
+    resid = torch.randn(m, n, device=cuda, generator=g)
+    mask = torch.randint(-2 ** 31, 2 ** 31 - 1, (m, (n + 31) // 32), device=cuda, dtype=torch.int32, generator=g)
+    start = torch.randn(m, n, device=cuda, generator=g)
+    monkeypatch.setenv("MM_GEMM_CG", str(cg))
+    monkeypatch.setenv("MM_GEMM_BN", str(bn))
+    outs = []
+    for spec in ("0", "1"):
+        monkeypatch.setenv("MM_GEMM_SPECIALIZE", spec)
+        bf = epi in (ops.EPI_BF16, ops.EPI_BF16_RELU, ops.EPI_BF16_DRELU)
+        d = torch.zeros(m, n, device=cuda, dtype=torch.bfloat16) if bf else start.clone()
+        kw = {}
+        if epi in (ops.EPI_BF16, ops.EPI_BF16_RELU, ops.EPI_F32, ops.EPI_F32_RESID):
+            kw["bias"] = bias
+        if epi == ops.EPI_F32_RESID:
+            kw["resid"] = resid
+        if epi in (ops.EPI_BF16_RELU, ops.EPI_BF16_DRELU):
+            kw["relu_mask"] = mask if epi == ops.EPI_BF16_DRELU else torch.zeros_like(mask)
+        ops.gemm(A, B, d, a_kmajor=ak, b_kmajor=bk, epilogue=epi, **kw)
+        outs.append((d, kw.get("relu_mask")))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0])
+    if epi == ops.EPI_BF16_RELU:
+        assert torch.equal(outs[0][1], outs[1][1])
