@@ -255,7 +255,9 @@ class Engine:
         self.native = True  # C++ step driver (mm_task_fwd_bwd); False -> per-op Python path
         self._task_desc: dict = {}
         self._ws = None
-        self.overlap = True  # decoder-side exchange + update overlap the encoder backward
+        # decoder-side exchange + update overlap the encoder backward
+        # (MM_OVERLAP=0 for A/B: every exchange + update after the backward)
+        self.overlap = os.environ.get("MM_OVERLAP", "1") != "0"
         # 0 = full grid.  A capped background update (MM_OVERLAP_CTAS=64) breaks
         # even at N=1 (r01 sweep: 8/16/32/64 CTAs -> 266K/413K/587K/740K vs
         # 756K tok/s): the update is HBM-bound and latency-bound per CTA.
