@@ -57,6 +57,9 @@ constexpr int kEpiWarp0 = 2;
 // two slices each take half of the tile's columns
 constexpr int kEpiWarps = MM_GEMM_EPI_WARPS;
 constexpr int kSlices = kEpiWarps / 4;
+#ifndef MM_GEMM_WIDE_LAST
+#define MM_GEMM_WIDE_LAST 1
+#endif
 #ifndef MM_GEMM_RESID_TMEM
 // residual tile of single-CTA 128-wide tiles parked in TMEM columns 256..383
 #define MM_GEMM_RESID_TMEM 1
@@ -698,6 +701,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t acc_phase = (local >> 1) & 1;
             const int cbase = tn * BN + half * (BN / kSlices);
             const bool resid_tm = C::kResidTmem && epi == MM_EPI_F32_RESID;
+            // this CTA's last tile: once its accumulator is final every
+            // mainloop stage is idle (no further loads; the MMAs that read
+            // them have completed), so each warp stages each chunk in its own
+            // box there instead of waiting for the previous box's store to be
+            // read (single CTAs without bias-gradient warps)
+            const bool wide = MM_GEMM_WIDE_LAST && CG == 1 && CN == 1 && !dbias_any && u + ncta >= g.units;
             if constexpr (C::kResidTmem) {
                 if (resid_tm && !(local == 0 && resid_pre)) resid_to_tmem(P, tm, cbase);
             }
@@ -758,9 +767,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int j = 0; j < 32; ++j) xs[c][j] = f[j];
                     }
-                    uint8_t* buf = bufs + nbuf * kEpiBufBytes;
-                    if (lane == 0) tc::bulk_wait_read<C::kEpiBufs - 1>();  // the store that last read `buf` is done
-                    __syncwarp();
+                    uint8_t* buf;
+                    if (wide) {
+                        buf = smem_a + ((warp - kEpiWarp0) * kChunks + c) * kEpiBufBytes;
+                    } else {
+                        buf = bufs + nbuf * kEpiBufBytes;
+                        if (lane == 0) tc::bulk_wait_read<C::kEpiBufs - 1>();  // the store that last read `buf` is done
+                        __syncwarp();
+                    }
                     stage_row(buf, lane, f, out_bf16);
                     tc::fence_proxy_async_smem();
                     __syncwarp();
@@ -769,7 +783,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         else tc::tma_store_2d(&P.td, buf, col0, row0);
                         tc::bulk_commit();
                     }
-                    if (++nbuf == C::kEpiBufs) nbuf = 0;
+                    if (!wide && ++nbuf == C::kEpiBufs) nbuf = 0;
                 }
             }
             // accumulator drained: one arrive per warp on the MMA CTA's barrier
