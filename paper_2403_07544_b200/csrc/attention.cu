@@ -772,25 +772,44 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
         const int i = quarter * 32 + lane;  // query row within the group
         const float c = p.scale * kLog2e;
         pdl_wait();
-        int n = 0;
-        for (int u = blockIdx.x; u < units; u += gridDim.x) {
-            const U x = unit(u);
-            if (!mine(x)) continue;
-            const uint32_t trow = tmem0 + (n & 1) * 256 + (static_cast<uint32_t>(quarter * 32) << 16);
-            const bool vrow = i < x.nq;
-            // this row's keys: one contiguous range of the group's key rows (its
+        // this row's metadata of a unit -- group -> sequence offsets -> the
+        // row's key range and lse, a chain of dependent global loads -- is
+        // fetched for the next unit while the current unit's gradient MMAs
+        // run, off the per-unit critical path
+        struct RowMeta {
+            U x;
+            int u, klo, khi;
+            float lse;
+        };
+        auto fetch = [&](int u, RowMeta& m) {  // m.u = units: no unit left
+            for (; u < units; u += gridDim.x) {
+                m.x = unit(u);
+                if (mine(m.x)) break;
+            }
+            m.u = u;
+            m.klo = m.khi = 0;
+            m.lse = 0.f;
+            if (u >= units || i >= m.x.nq) return;
+            // the row's keys: one contiguous range of the group's key rows (its
             // own sequence; causal: up to its position)
-            int klo = 0, khi = 0;
-            if (vrow) {
-                for (int s2 = 0; s2 < x.nseq; ++s2) {
-                    const int a = p.cu_q[x.first + s2] - x.q_lo, b = p.cu_q[x.first + s2 + 1] - x.q_lo;
-                    if (i >= a && i < b) {
-                        klo = p.cu_k[x.first + s2] - x.k_lo;
-                        khi = p.causal ? klo + (i - a) + 1 : p.cu_k[x.first + s2 + 1] - x.k_lo;
-                    }
+            for (int s2 = 0; s2 < m.x.nseq; ++s2) {
+                const int a = p.cu_q[m.x.first + s2] - m.x.q_lo, b = p.cu_q[m.x.first + s2 + 1] - m.x.q_lo;
+                if (i >= a && i < b) {
+                    m.klo = p.cu_k[m.x.first + s2] - m.x.k_lo;
+                    m.khi = p.causal ? m.klo + (i - a) + 1 : p.cu_k[m.x.first + s2 + 1] - m.x.k_lo;
                 }
             }
-            const float l2 = vrow ? p.lse[int64_t(x.h) * p.total_q + x.q_lo + i] * kLog2e : 0.f;
+            m.lse = p.lse[int64_t(m.x.h) * p.total_q + m.x.q_lo + i];
+        };
+        RowMeta cur;
+        fetch(blockIdx.x, cur);
+        int n = 0;
+        while (cur.u < units) {
+            const U x = cur.x;
+            const uint32_t trow = tmem0 + (n & 1) * 256 + (static_cast<uint32_t>(quarter * 32) << 16);
+            const bool vrow = i < x.nq;
+            const int klo = cur.klo, khi = cur.khi;
+            const float l2 = cur.lse * kLog2e;
             WP_BEGIN(w2_);
             tc::mbar_wait(s_bar, n & 1);
             if (warp == kEpiW0) WP_ADD(2, w2_);
@@ -832,15 +851,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(p_bar);
             if (warp == kEpiW0) ATTN_STAMP_LANE0(2);
-            // ---- gradients out of TMEM: this warp's 16 of each output's 64 columns
+            RowMeta nxt;
+            fetch(cur.u + gridDim.x, nxt);
+            // ---- gradients out of TMEM: this warp's 16 of each output's 64 columns,
+            // all three loaded before one wait (the stores' source registers are
+            // not reused by a following TMEM load)
             WP_BEGIN(w3_);
             tc::mbar_wait(g_bar, n & 1);
             if (warp == kEpiW0) WP_ADD(3, w3_);
             tc::tc_fence_after();
-            auto emit = [&](uint32_t col, uint16_t* base, int64_t ld, int row_lo, bool vr, float sc) {
-                uint32_t v[16];
-                tc::tmem_ld_32x16(trow + col + kc * 16, v);
-                tc::tmem_ld_wait();
+            uint32_t gv[3][16];
+            tc::tmem_ld_32x16(trow + 0 + kc * 16, gv[0]);    // dV: TMEM lane = key row
+            tc::tmem_ld_32x16(trow + 64 + kc * 16, gv[1]);   // dK
+            tc::tmem_ld_32x16(trow + 128 + kc * 16, gv[2]);  // dQ: TMEM lane = query row
+            tc::tmem_ld_wait();
+            auto emit = [&](const uint32_t (&v)[16], uint16_t* base, int64_t ld, int row_lo, bool vr, float sc) {
                 if (!vr) return;
                 uint4* dst = reinterpret_cast<uint4*>(base + int64_t(row_lo + i) * ld + x.h * 64 + kc * 16);
 #pragma unroll
@@ -850,11 +875,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_tc_kernel(const __grid_c
                                         pack_bf16(__uint_as_float(v[8 * q + 4]) * sc, __uint_as_float(v[8 * q + 5]) * sc),
                                         pack_bf16(__uint_as_float(v[8 * q + 6]) * sc, __uint_as_float(v[8 * q + 7]) * sc));
             };
-            emit(0, p.dv, p.ld_dv, x.k_lo, i < x.nk, 1.f);        // TMEM lane = key row
-            emit(64, p.dk, p.ld_dk, x.k_lo, i < x.nk, p.scale);
-            emit(128, p.dq, p.ld_dq, x.q_lo, vrow, p.scale);      // TMEM lane = query row
+            emit(gv[0], p.dv, p.ld_dv, x.k_lo, i < x.nk, 1.f);
+            emit(gv[1], p.dk, p.ld_dk, x.k_lo, i < x.nk, p.scale);
+            emit(gv[2], p.dq, p.ld_dq, x.q_lo, vrow, p.scale);
             if (warp == kEpiW0) ATTN_STAMP_LANE0(3);
             tc::tc_fence_before();
+            cur = nxt;
             ++n;
         }
     }
