@@ -561,6 +561,7 @@ struct alignas(64) BwdParams {
     float scale;
     int n_groups, heads;
     int early_qkv;  // Q / K / V may be loaded before griddepcontrol.wait (mm_attn_args.flags & 2)
+    int long_skip;  // long kernel: long groups before this one belong to an earlier launch
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -912,6 +913,7 @@ struct alignas(64) FwdParams {
     int total_q, causal;
     float scale;
     int early_kv;  // K / V may be loaded before griddepcontrol.wait (mm_attn_args.flags & 4)
+    int n_groups, heads, long_skip;  // long kernel: the table to scan (see collect_long)
 };
 
 __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_tc_kernel(const __grid_constant__ FwdParams p) {
@@ -1094,9 +1096,55 @@ __global__ void __launch_bounds__(kFwdThreads, 2) attn_fwd_tc_kernel(const __gri
 // 208 KB of shared memory, 512 TMEM columns (S 256 + O 64): one CTA per SM.
 constexpr int kLongW = 16;
 constexpr int kLongThreads = (kEpiW0 + kLongW) * 32;
-constexpr int kLongFwdSmem = kTile /*Q*/ + 2 * kTile /*K*/ + 2 * kTile /*V*/ + 8 * kTile /*P hi+lo*/ + 4096 + 1024;
+constexpr int kLongList = (1024 + 32) * 4;  // list of long groups (kMaxLong) + chunk counts
+constexpr int kLongFwdSmem = kTile /*Q*/ + 2 * kTile /*K*/ + 2 * kTile /*V*/ + 8 * kTile /*P hi+lo*/ + 4096 + kLongList + 1024;
 
 __device__ __forceinline__ bool long_group(int nq, int nk) { return nq > kRows || nk > kRows; }
+
+// Long groups are rare (config 5: a few per table of ~150), so the long
+// kernels run one wave of persistent CTAs instead of one CTA per (head, group
+// [, query block]) -- that grid was ~4800 CTAs of 208 KB shared memory, one
+// per SM at a time, nearly all exiting at once: ~40 us of CTA turnover per
+// launch.  Every CTA lists the table's long groups in table order (one
+// parallel pass over the table, a ballot prefix per chunk), from the
+// skip-th on and at most kMaxLong of them (the launcher covers the rest with
+// further launches), and walks its units of that list.
+constexpr int kMaxLong = 1024;
+// upper bound on a table's long groups: each holds a sequence of > 128 rows
+inline int long_bound(int n_groups, int total_q, int total_k) {
+    return static_cast<int>(std::min<int64_t>(n_groups, int64_t(total_q) / (kRows + 1) + int64_t(total_k) / (kRows + 1)));
+}
+
+template <int NT>
+__device__ int collect_long(const int32_t* groups, const int32_t* cu_q, const int32_t* cu_k, int n_groups,
+                            int skip, int* list, int* wsum) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int base = 0;  // long groups in earlier chunks
+    for (int g0 = 0; g0 < n_groups; g0 += NT) {
+        const int g = g0 + static_cast<int>(threadIdx.x);
+        bool lg = false;
+        if (g < n_groups) {
+            const int first = groups[2 * g], nseq = groups[2 * g + 1];
+            lg = long_group(cu_q[first + nseq] - cu_q[first], cu_k[first + nseq] - cu_k[first]);
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, lg);
+        if (lane == 0) wsum[warp] = __popc(b);
+        __syncthreads();
+        int before = base, total = 0;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) {
+            before += w < warp ? wsum[w] : 0;
+            total += wsum[w];
+        }
+        if (lg) {
+            const int idx = before + __popc(b & ((1u << lane) - 1u)) - skip;
+            if (idx >= 0 && idx < kMaxLong) list[idx] = g;
+        }
+        base += total;
+        __syncthreads();  // wsum reused by the next chunk; list complete after the last
+    }
+    return min(max(base - skip, 0), kMaxLong);
+}
 
 __global__ void __launch_bounds__(kLongThreads, 1) attn_fwd_long_kernel(const __grid_constant__ FwdParams p) {
     extern __shared__ uint8_t smraw[];
@@ -1113,17 +1161,14 @@ __global__ void __launch_bounds__(kLongThreads, 1) attn_fwd_long_kernel(const __
     uint64_t* p_bar = bars + 2;
     uint64_t* o_bar = bars + 3;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+    int* list = reinterpret_cast<int*>(sm + 13 * kTile + 4096);  // [kMaxLong] + [32] chunk counts
 
-    const int h = blockIdx.x, grp = blockIdx.y, qb = blockIdx.z;
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
-    const int first = p.groups[2 * grp], nseq = p.groups[2 * grp + 1];
-    const int q_lo = p.cu_q[first], nq = p.cu_q[first + nseq] - q_lo;
-    const int k_lo = p.cu_k[first], nk = p.cu_k[first + nseq] - k_lo;
-    MM_DCHECK(nseq >= 1 && q_lo >= 0 && nq >= 1 && q_lo + nq <= p.total_q && k_lo >= 0 && nk >= 0 && nq <= 2 * kRows && nk <= 2 * kRows);
-    if (!long_group(nq, nk) || qb * kRows >= nq) return;  // the short kernel's group / no rows
-    const int q0 = qb * kRows;
-    const int nkb = nk > kRows ? 2 : 1;
+    const int n_long = collect_long<kLongThreads>(p.groups, p.cu_q, p.cu_k, p.n_groups, p.long_skip, list,
+                                                  list + kMaxLong);
+    const int per = p.heads * 2;  // units of a long group: (head, 128-query block)
+    if (static_cast<int>(blockIdx.x) >= n_long * per) return;
     if (warp == 1 && lane == 0) {
         tc::mbar_init(tma_bar, 1);
         tc::mbar_init(s_bar, 1);
@@ -1137,9 +1182,19 @@ __global__ void __launch_bounds__(kLongThreads, 1) attn_fwd_long_kernel(const __
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    uint32_t n = 0;  // units done: barrier parity
+    for (int u = blockIdx.x; u < n_long * per; u += gridDim.x) {
+    const int grp = list[u / per], h = (u % per) >> 1, qb = u & 1;
+    const int first = p.groups[2 * grp], nseq = p.groups[2 * grp + 1];
+    const int q_lo = p.cu_q[first], nq = p.cu_q[first + nseq] - q_lo;
+    const int k_lo = p.cu_k[first], nk = p.cu_k[first + nseq] - k_lo;
+    MM_DCHECK(nseq >= 1 && q_lo >= 0 && nq >= 1 && q_lo + nq <= p.total_q && k_lo >= 0 && nk >= 0 && nq <= 2 * kRows && nk <= 2 * kRows);
+    if (qb * kRows >= nq) continue;  // no second query block (uniform over the CTA)
+    const int q0 = qb * kRows;
+    const int nkb = nk > kRows ? 2 : 1;
     if (warp == 0) {
         if (lane == 0) {
-            pdl_wait();
+            if (n == 0) pdl_wait();
             tc::mbar_expect_tx(tma_bar, (1 + 2 * nkb) * kTile);
             tc::tma_load_2d(Qs, &p.mq, tma_bar, h * 64, q_lo + q0);
             for (int b = 0; b < nkb; ++b) {
@@ -1148,7 +1203,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) attn_fwd_long_kernel(const __
             }
         }
     } else if (warp == 1) {
-        tc::mbar_wait(tma_bar, 0);
+        tc::mbar_wait(tma_bar, n & 1);
         tc::tc_fence_after();
         constexpr uint32_t id_s1 = tc::idesc_bf16_f32(128, 128, 0, 0);
         constexpr uint32_t id_s2 = tc::idesc_bf16_f32(128, 256, 0, 0);
@@ -1157,7 +1212,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) attn_fwd_long_kernel(const __
         for (int kk = 0; kk < 4; ++kk)
             tc::mma_bf16_elect<1>(tmem, desc(Qs + kk * 32, 16), desc(Ks + kk * 32, 16), id_s, kk > 0);
         tc::mma_commit_elect<1>(s_bar);
-        tc::mbar_wait(p_bar, 0);
+        tc::mbar_wait(p_bar, n & 1);
         tc::tc_fence_after();
         constexpr uint32_t id_o = tc::idesc_bf16_f32(128, 64, 0, 1);  // P K-major, V MN-major
         for (int part = 0; part < 2; ++part) {
@@ -1183,7 +1238,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) attn_fwd_long_kernel(const __
         }
         const int rl = quarter * 32 + lane;  // TMEM lane
         const float c = p.scale * kLog2e;
-        tc::mbar_wait(s_bar, 0);
+        tc::mbar_wait(s_bar, n & 1);
         tc::tc_fence_after();
         const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
         float pv[64];
@@ -1231,7 +1286,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) attn_fwd_long_kernel(const __
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(p_bar);
         if (vrow && kc == 0) p.lse[int64_t(h) * p.total_q + q_lo + i] = (mref + log2f(l)) * kLn2;
-        tc::mbar_wait(o_bar, 0);
+        tc::mbar_wait(o_bar, n & 1);
         tc::tc_fence_after();
         uint32_t v[16];
         tc::tmem_ld_32x16(trow + 256 + kc * 16, v);
@@ -1245,6 +1300,13 @@ __global__ void __launch_bounds__(kLongThreads, 1) attn_fwd_long_kernel(const __
                                     pack_bf16(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5])),
                                     pack_bf16(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7])));
         }
+    }
+    // unit done: its TMEM reads and MMAs are complete before the next unit's
+    // loads and MMAs reuse shared memory and TMEM
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    ++n;
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -1265,7 +1327,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) attn_fwd_long_kernel(const __
 // One control thread issues the TMA loads and MMAs strictly in order; these
 // groups are rare, so the phases are not overlapped.
 constexpr int kLongBwdSmem = 2 * kTile /*K*/ + 2 * kTile /*V*/ + kTile /*Q_i*/ + kTile /*dO_i*/ +
-                             2 * kPTile /*P hi+lo*/ + kPTile /*dS*/ + 4096 + 1024;
+                             2 * kPTile /*P hi+lo*/ + kPTile /*dS*/ + 4096 + kLongList + 1024;
 
 __global__ void __launch_bounds__(kLongThreads, 1) attn_bwd_long_kernel(const __grid_constant__ BwdParams p) {
     extern __shared__ uint8_t smraw[];
@@ -1286,16 +1348,13 @@ __global__ void __launch_bounds__(kLongThreads, 1) attn_bwd_long_kernel(const __
     uint64_t* p_bar = bars + 3;  // P / dS in shared memory
     uint64_t* g_bar = bars + 4;  // gradient MMAs of an (i, j) tile done
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
+    int* list = reinterpret_cast<int*>(Sh + kPTile + 4096);  // [kMaxLong] + [32] chunk counts
 
-    const int h = blockIdx.x, grp = blockIdx.y;
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
-    const int first = p.groups[2 * grp], nseq = p.groups[2 * grp + 1];
-    const int q_lo = p.cu_q[first], nq = p.cu_q[first + nseq] - q_lo;
-    const int k_lo = p.cu_k[first], nk = p.cu_k[first + nseq] - k_lo;
-    MM_DCHECK(nseq >= 1 && q_lo >= 0 && nq >= 1 && q_lo + nq <= p.total_q && k_lo >= 0 && nk >= 0 && nq <= 2 * kRows && nk <= 2 * kRows);
-    if (!long_group(nq, nk)) return;
-    const int nqb = nq > kRows ? 2 : 1, nkb = nk > kRows ? 2 : 1;
+    const int n_long = collect_long<kLongThreads>(p.groups, p.cu_q, p.cu_k, p.n_groups, p.long_skip, list,
+                                                  list + kMaxLong);
+    if (static_cast<int>(blockIdx.x) >= n_long * p.heads) return;
     if (warp == 1 && lane == 0) {
         tc::mbar_init(tma_bar, 1);
         tc::mbar_init(s_bar, 1);
@@ -1310,11 +1369,18 @@ __global__ void __launch_bounds__(kLongThreads, 1) attn_bwd_long_kernel(const __
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t T_S = 0, T_DP = 128, T_DV = 256, T_DK = 320, T_DQ = 384;
-
+    // barrier phase counts, running over this CTA's units
+    uint32_t n_tma = 0, n_s = 0, n_e = 0, n_p = 0, n_g = 0;
+    for (int u = blockIdx.x; u < n_long * p.heads; u += gridDim.x) {
+    const int grp = list[u / p.heads], h = u % p.heads;
+    const int first = p.groups[2 * grp], nseq = p.groups[2 * grp + 1];
+    const int q_lo = p.cu_q[first], nq = p.cu_q[first + nseq] - q_lo;
+    const int k_lo = p.cu_k[first], nk = p.cu_k[first + nseq] - k_lo;
+    MM_DCHECK(nseq >= 1 && q_lo >= 0 && nq >= 1 && q_lo + nq <= p.total_q && k_lo >= 0 && nk >= 0 && nq <= 2 * kRows && nk <= 2 * kRows);
+    const int nqb = nq > kRows ? 2 : 1, nkb = nk > kRows ? 2 : 1;
     if (warp == 1) {
         // ------------------------------------------------ control: TMA + MMA, in order
-        pdl_wait();
-        uint32_t n_tma = 0, n_s = 0, n_e = 0, n_p = 0, n_g = 0;
+        if (n_tma == 0) pdl_wait();
         auto load_qi = [&](int i, bool kv) {
             if (lane == 0) {
                 tc::mbar_expect_tx(tma_bar, (2 + (kv ? 2 * nkb : 0)) * kTile);
@@ -1389,7 +1455,6 @@ __global__ void __launch_bounds__(kLongThreads, 1) attn_bwd_long_kernel(const __
         const int rl = quarter * 32 + lane;
         const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
         const float c = p.scale * kLog2e;
-        uint32_t n_s = 0, n_g = 0;
         // this row's key range (group coordinates) for query block i
         auto range = [&](int i, int& klo, int& khi, float& l2) {
             const int qi = i * kRows + rl;
@@ -1497,6 +1562,12 @@ __global__ void __launch_bounds__(kLongThreads, 1) attn_bwd_long_kernel(const __
             const int qi = i * kRows + rl;
             emit(T_DQ + i * 64, p.dq, p.ld_dq, q_lo + qi, qi < nq, p.scale);
         }
+    }
+    // unit done (every role's phase counts advanced alike): TMEM reads and
+    // MMAs complete before the next unit reuses shared memory and TMEM
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -1617,9 +1688,16 @@ extern "C" int mm_attention_fwd(const mm_attn_args* a, void* stream) {
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, tca::kLongFwdSmem));
                 attr_l = true;
             }
-            MM_CUDA_TRY(mm::launch_pdl(tca::attn_fwd_long_kernel, dim3(a->heads, a->n_tc_groups, 2),
-                                       dim3(tca::kLongThreads), tca::kLongFwdSmem, mm::as_stream(stream), fp));
-            MM_LAUNCH_CHECK("attn_fwd_long_kernel");
+            fp.n_groups = a->n_tc_groups;
+            fp.heads = a->heads;
+            const int bound = tca::long_bound(a->n_tc_groups, a->total_q, a->total_k);
+            for (int skip = 0; skip < bound; skip += tca::kMaxLong) {  // one launch unless > kMaxLong
+                fp.long_skip = skip;
+                const int64_t units = int64_t(std::min(bound - skip, tca::kMaxLong)) * a->heads * 2;
+                MM_CUDA_TRY(mm::launch_pdl(tca::attn_fwd_long_kernel, dim3(int(std::min<int64_t>(units, mm::num_sms()))),
+                                           dim3(tca::kLongThreads), tca::kLongFwdSmem, mm::as_stream(stream), fp));
+                MM_LAUNCH_CHECK("attn_fwd_long_kernel");
+            }
             return 0;
         }
         b.flags = 1;  // the mma.sync kernel takes only groups with a longer sequence
@@ -1674,9 +1752,14 @@ extern "C" int mm_attention_bwd(const mm_attn_args* a, void* stream) {
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, tca::kLongBwdSmem));
                 attr_l = true;
             }
-            MM_CUDA_TRY(mm::launch_pdl(tca::attn_bwd_long_kernel, dim3(a->heads, bp.n_groups),
-                                       dim3(tca::kLongThreads), tca::kLongBwdSmem, mm::as_stream(stream), bp));
-            MM_LAUNCH_CHECK("attn_bwd_long_kernel");
+            const int bound = tca::long_bound(bp.n_groups, a->total_q, a->total_k);
+            for (int skip = 0; skip < bound; skip += tca::kMaxLong) {
+                bp.long_skip = skip;
+                const int64_t units = int64_t(std::min(bound - skip, tca::kMaxLong)) * a->heads;
+                MM_CUDA_TRY(mm::launch_pdl(tca::attn_bwd_long_kernel, dim3(int(std::min<int64_t>(units, mm::num_sms()))),
+                                           dim3(tca::kLongThreads), tca::kLongBwdSmem, mm::as_stream(stream), bp));
+                MM_LAUNCH_CHECK("attn_bwd_long_kernel");
+            }
             return 0;
         }
     }

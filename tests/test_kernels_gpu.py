@@ -470,6 +470,47 @@ def test_attention(cuda, causal, maxlen, maxk, tc_fwd, long_path, monkeypatch):
     assert rel_err(dv.cpu(), vr.grad) < 2e-2
 
 
+@pytest.mark.parametrize("causal", [False, True])
+def test_attention_many_long_groups(cuda, causal, monkeypatch):
+    """Many sequences past 128 rows: the long-group kernels run one wave of
+    persistent CTAs over the list of long groups (attention.cu collect_long),
+    so each CTA takes several (head, group[, query block]) units in turn --
+    40 long sequences x 8 heads = 640 forward / 320 backward units on 148
+    CTAs, short sequences between them -- vs the fp32 reference."""
+    monkeypatch.delenv("MM_ATTN_LONG_MMA_SYNC", raising=False)
+    monkeypatch.setenv("MM_ATTN_TC_FWD", "1")
+    from paper_2403_07544_b200 import ops
+    rng = np.random.default_rng(11 + causal)
+    heads, d, n = 8, 512, 60
+    lq = rng.integers(129, 257, size=n)
+    lq[rng.permutation(n)[:20]] = rng.integers(1, 129, size=20)  # 20 short ones between
+    lk = lq.copy() if causal else np.where(lq > 128, rng.integers(1, 257, size=n), rng.integers(129, 257, size=n))
+    cu_q = np.concatenate([[0], np.cumsum(lq)]).astype(np.int32)
+    cu_k = np.concatenate([[0], np.cumsum(lk)]).astype(np.int32)
+    tq, tk = int(cu_q[-1]), int(cu_k[-1])
+    g = torch.Generator().manual_seed(1)
+    q = torch.randn(tq, d, generator=g).bfloat16().float()
+    k = torch.randn(tk, d, generator=g).bfloat16().float()
+    v = torch.randn(tk, d, generator=g).bfloat16().float()
+    qr, kr, vr = (t.clone().requires_grad_(True) for t in (q, k, v))
+    ref = ref_attention(qr, kr, vr, cu_q, cu_k, heads, causal)
+    do = torch.randn(tq, d, generator=g).bfloat16().float()
+    ref.backward(do)
+    qd, kd, vd = (t.bfloat16().cuda() for t in (q, k, v))
+    o = torch.empty(tq, d, device=cuda, dtype=torch.bfloat16)
+    lse = torch.empty(heads, tq, device=cuda)
+    cq, ck = torch.from_numpy(cu_q).cuda(), torch.from_numpy(cu_k).cuda()
+    dq, dk, dv = torch.empty_like(qd), torch.empty_like(kd), torch.empty_like(vd)
+    args = ops.attention_args(qd, kd, vd, o, lse, cq, ck, n, heads, int(lq.max()), int(lk.max()),
+                              causal, d_o=do.bfloat16().cuda(), dq=dq, dk=dk, dv=dv)
+    ops.attention_fwd(args)
+    assert rel_err(o.cpu(), ref.detach()) < 1e-2
+    ops.attention_bwd(args)
+    assert rel_err(dq.cpu(), qr.grad) < 2e-2
+    assert rel_err(dk.cpu(), kr.grad) < 2e-2
+    assert rel_err(dv.cpu(), vr.grad) < 2e-2
+
+
 def test_colsum_and_cast(cuda):
     from paper_2403_07544_b200 import ops
     x = torch.randn(4097, 1536, device=cuda).bfloat16()
