@@ -1,5 +1,5 @@
 # final check of the final commit: GPU suite, smoke, bench lines, spans
-D=gpurun_out/r02cc3
+D=gpurun_out/r02cc4
 mkdir -p $D
 timeout 2400 python -m pytest tests -q -m gpu -p no:cacheprovider > $D/gpu_all.log 2>&1
 tail -n 1 $D/gpu_all.log
