@@ -1,5 +1,5 @@
 # attention backward: warm timing + ncu source-level capture (config 5 shapes)
-D=gpurun_out/r02_attnsrc
+D=gpurun_out/r02_attnsrc2
 mkdir -p $D
 REPS=20 timeout 300 python tools/attn_waitprof.py > $D/c3_warm.log 2>&1
 C5=1 REPS=20 timeout 300 python tools/attn_waitprof.py > $D/c5_warm.log 2>&1
