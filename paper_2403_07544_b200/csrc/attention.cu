@@ -1618,7 +1618,8 @@ size_t bwd_smem(const mm_attn_args& a) { return size_t(4) * a.cap * kP * 2 + siz
 
 int check(const mm_attn_args* a, bool bwd) {
     MM_CHECK_ARG(a != nullptr, "args is NULL");
-    MM_CHECK_ARG(a->head_dim == kHd, "head_dim must be 64 (got %d)", a->head_dim);
+    MM_CHECK_ARG(a->head_dim == kHd || a->head_dim == 16 || a->head_dim == 32,
+                 "head_dim must be 16, 32 or 64 (got %d)", a->head_dim);
     MM_CHECK_ARG(a->q && a->k && a->v && a->o && a->lse && a->cu_q && a->cu_k, "NULL tensor");
     MM_CHECK_ARG(a->n_seq >= 0 && a->heads > 0 && a->max_q > 0 && a->max_k > 0, "bad sizes");
     MM_CHECK_ARG(a->max_q <= 256 && a->max_k <= 256, "sequence longer than 256");
@@ -1631,6 +1632,9 @@ int check(const mm_attn_args* a, bool bwd) {
 
 }  // namespace
 
+// head_dim 16 / 32 (config 1's true shape): CUDA-core kernels, attn_small.cu
+int mm_attention_small(const mm_attn_args* a, void* stream, bool bwd);
+
 #ifdef MM_ATTN_TRACE
 extern "C" int mm_attn_trace_read(unsigned long long* host, int n) {
     MM_CUDA_TRY(cudaMemcpyFromSymbol(host, g_attn_trace, sizeof(unsigned long long) * n));
@@ -1641,6 +1645,7 @@ extern "C" int mm_attn_trace_read(unsigned long long* host, int n) {
 extern "C" int mm_attention_fwd(const mm_attn_args* a, void* stream) {
     if (int st = check(a, false)) return st;
     if (a->n_seq == 0) return 0;
+    if (a->head_dim != kHd) return mm_attention_small(a, stream, false);
     // On the padded (32-row aligned) groups the tcgen05 forward lost to the
     // mma.sync kernel (13.1 vs 10.0 us: 83 KB of smem and 256 TMEM columns
     // allow two CTAs per SM against four).
@@ -1715,6 +1720,7 @@ extern "C" int mm_attention_fwd(const mm_attn_args* a, void* stream) {
 extern "C" int mm_attention_bwd(const mm_attn_args* a, void* stream) {
     if (int st = check(a, true)) return st;
     if (a->n_seq == 0) return 0;
+    if (a->head_dim != kHd) return mm_attention_small(a, stream, true);
     static const bool mma_sync_only = std::getenv("MM_ATTN_MMA_SYNC") != nullptr;  // diagnostics
     if (!mma_sync_only && a->total_k > 0) {
         // tcgen05 kernel for every group that fits one 128-row block per side

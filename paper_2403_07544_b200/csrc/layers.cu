@@ -53,8 +53,11 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x
                                                      uint16_t* __restrict__ y, float* mean_out,
                                                      float* rstd_out, int64_t rows, float eps) {
     pdl_wait_release();
-    constexpr int V = COLS / 128;
+    // COLS = 64 (config 1): one float4 per lane on half the warp, the other
+    // lanes hold zeros and stay out of the variance and the stores
+    constexpr int V = (COLS + 127) / 128;
     const int lane = threadIdx.x & 31;
+    auto live = [&](int i) { return COLS % 128 == 0 || lane + 32 * i < COLS / 4; };
     const int64_t row0 = (int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5)) * kLnRows;
     float4 v[kLnRows][V];
 #pragma unroll
@@ -62,7 +65,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x
         const int64_t row = min(row0 + r, rows - 1);
         const float4* xr = reinterpret_cast<const float4*>(x + row * COLS);
 #pragma unroll
-        for (int i = 0; i < V; ++i) v[r][i] = xr[lane + 32 * i];
+        for (int i = 0; i < V; ++i) v[r][i] = live(i) ? xr[lane + 32 * i] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int r = 0; r < kLnRows; ++r) {
@@ -74,6 +77,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x
         float q = 0.f;
 #pragma unroll
         for (int i = 0; i < V; ++i) {
+            if (!live(i)) continue;
             const float a = v[r][i].x - mu, b = v[r][i].y - mu, c = v[r][i].z - mu, d = v[r][i].w - mu;
             q += a * a + b * b + c * c + d * d;
         }
@@ -82,6 +86,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x
         uint2* yr = reinterpret_cast<uint2*>(y + row * COLS);
 #pragma unroll
         for (int i = 0; i < V; ++i) {
+            if (!live(i)) continue;
             const int c = 4 * lane + 128 * i;
             const float4 g = __ldg(reinterpret_cast<const float4*>(gamma + c));
             const float4 bb = __ldg(reinterpret_cast<const float4*>(beta + c));
@@ -110,10 +115,12 @@ __global__ void __launch_bounds__(256, (COLS <= 512 ? 2 : 1)) ln_bwd_kernel(cons
                                                      uint16_t* dx_bf16, float* dgamma,
                                                      float* dbeta, int64_t rows) {
     pdl_wait_release();
-    constexpr int V = COLS / 128;
+    constexpr int V = (COLS + 127) / 128;  // COLS = 64: half the lanes live (see ln_fwd_kernel)
     constexpr int R = COLS <= 512 ? kLnRows : 1;  // rows per warp batch (register budget)
     __shared__ float red_g[8][COLS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto lane_on = [&](int i) { return COLS % 128 == 0 || lane + 32 * i < COLS / 4; };
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     float4 ag[V], ab[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) ag[i] = ab[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -133,13 +140,13 @@ __global__ void __launch_bounds__(256, (COLS <= 512 ? 2 : 1)) ln_bwd_kernel(cons
             const float4* xr = reinterpret_cast<const float4*>(x + row * COLS);
 #pragma unroll
             for (int i = 0; i < V; ++i) {
-                d[r][i] = dyr[lane + 32 * i];
-                xv[r][i] = xr[lane + 32 * i];
+                d[r][i] = lane_on(i) ? dyr[lane + 32 * i] : z4;
+                xv[r][i] = lane_on(i) ? xr[lane + 32 * i] : z4;
             }
             if constexpr (kPreDx) {
                 const float4* dxr = reinterpret_cast<const float4*>(dx + row * COLS);
 #pragma unroll
-                for (int i = 0; i < V; ++i) opre[i] = dxr[lane + 32 * i];
+                for (int i = 0; i < V; ++i) opre[i] = lane_on(i) ? dxr[lane + 32 * i] : z4;
             }
         }
 #pragma unroll
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(256, (COLS <= 512 ? 2 : 1)) ln_bwd_kernel(cons
                 float4& xh = xv[r][i];
                 xh = make_float4((xh.x - mu[r]) * rs[r], (xh.y - mu[r]) * rs[r],
                                  (xh.z - mu[r]) * rs[r], (xh.w - mu[r]) * rs[r]);
-                const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma + 4 * lane + 128 * i));
+                const float4 gm = lane_on(i) ? __ldg(reinterpret_cast<const float4*>(gamma + 4 * lane + 128 * i)) : z4;
                 const float4 g = make_float4(d[r][i].x * gm.x, d[r][i].y * gm.y,
                                              d[r][i].z * gm.z, d[r][i].w * gm.w);
                 s1 += g.x + g.y + g.z + g.w;
@@ -170,9 +177,10 @@ __global__ void __launch_bounds__(256, (COLS <= 512 ? 2 : 1)) ln_bwd_kernel(cons
             uint2* dbr = reinterpret_cast<uint2*>(dx_bf16 + row * COLS);
             float4 o[V];
 #pragma unroll
-            for (int i = 0; i < V; ++i) o[i] = kPreDx ? opre[kPreDx ? i : 0] : dxr[lane + 32 * i];
+            for (int i = 0; i < V; ++i) o[i] = kPreDx ? opre[kPreDx ? i : 0] : (lane_on(i) ? dxr[lane + 32 * i] : z4);
 #pragma unroll
             for (int i = 0; i < V; ++i) {
+                if (!lane_on(i)) continue;
                 float4 w = o[i];
                 w.x += rs[r] * (d[r][i].x - m1 - xv[r][i].x * m2);
                 w.y += rs[r] * (d[r][i].y - m1 - xv[r][i].y * m2);
@@ -193,7 +201,7 @@ __global__ void __launch_bounds__(256, (COLS <= 512 ? 2 : 1)) ln_bwd_kernel(cons
 #pragma unroll
         for (int i = 0; i < V; ++i) {
             const float4 a = pass == 0 ? ag[i] : ab[i];
-            *reinterpret_cast<float4*>(&red_g[warp][4 * lane + 128 * i]) = a;
+            if (lane_on(i)) *reinterpret_cast<float4*>(&red_g[warp][4 * lane + 128 * i]) = a;
         }
         __syncthreads();
         float* dst = pass == 0 ? dgamma : dbeta;
@@ -494,12 +502,12 @@ constexpr int kEmbMaxV = 8;  // float4 per lane: cols <= 1024
 // V = cols / 128 float4 per lane; R rows loaded per batch (independent loads
 // in flight, summed in row order): the chunk's row indices come in with one
 // coalesced load and are broadcast by shuffles, so no load waits on another
-template <int V, int R>
+template <int V, int R, int C4 = 32 * V>  // C4 float4 per row (16: cols = 64)
 __global__ void __launch_bounds__(256) embed_bwd_chunk_kernel(const int32_t* __restrict__ perm,
                                                               const int32_t* __restrict__ chunks,
                                                               int n_chunks, const float* __restrict__ dout,
                                                               float* dtable, float* scratch, float scale) {
-    constexpr int cols = V * 128;
+    constexpr int cols = C4 * 4;
     pdl_wait_release();
     const int lane = threadIdx.x & 31;
     const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -519,7 +527,7 @@ __global__ void __launch_bounds__(256) embed_bwd_chunk_kernel(const int32_t* __r
             const int row = __shfl_sync(0xffffffffu, my_row, (r0 + u) & 31);
             const float4* d = reinterpret_cast<const float4*>(dout + int64_t(row) * cols);
 #pragma unroll
-            for (int i = 0; i < V; ++i) g[u][i] = r0 + u < n ? d[lane + 32 * i] : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int i = 0; i < V; ++i) g[u][i] = r0 + u < n && (C4 == 32 * V || lane + 32 * i < C4) ? d[lane + 32 * i] : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int u = 0; u < R; ++u) {
@@ -536,6 +544,7 @@ __global__ void __launch_bounds__(256) embed_bwd_chunk_kernel(const int32_t* __r
 #pragma unroll
     for (int i = 0; i < V; ++i) {
         const int v = lane + 32 * i;
+        if (C4 != 32 * V && v >= C4) continue;
         if (tgt >= 0) {
             float4 t = dst[v];
             t.x += acc[i].x; t.y += acc[i].y; t.z += acc[i].z; t.w += acc[i].w;
@@ -548,11 +557,11 @@ __global__ void __launch_bounds__(256) embed_bwd_chunk_kernel(const int32_t* __r
 
 // one warp per multi-chunk id: its partials (R per batch, independent loads)
 // added in chunk order, then into the table row
-template <int V, int R>
+template <int V, int R, int C4 = 32 * V>  // C4 float4 per row (16: cols = 64)
 __global__ void __launch_bounds__(256) embed_bwd_multi_kernel(const int32_t* __restrict__ multi, int n_multi,
                                                               const float* __restrict__ scratch,
                                                               float* dtable) {
-    constexpr int cols = V * 128;
+    constexpr int cols = C4 * 4;
     pdl_wait_release();
     const int lane = threadIdx.x & 31;
     const int m = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -568,7 +577,7 @@ __global__ void __launch_bounds__(256) embed_bwd_multi_kernel(const int32_t* __r
         for (int u = 0; u < R; ++u)
 #pragma unroll
             for (int i = 0; i < V; ++i)
-                x[u][i] = k0 + u < ns ? reinterpret_cast<const float4*>(scratch + int64_t(s0 + k0 + u) * cols)[lane + 32 * i]
+                x[u][i] = k0 + u < ns && (C4 == 32 * V || lane + 32 * i < C4) ? reinterpret_cast<const float4*>(scratch + int64_t(s0 + k0 + u) * cols)[lane + 32 * i]
                                       : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int u = 0; u < R; ++u) {
@@ -582,22 +591,23 @@ __global__ void __launch_bounds__(256) embed_bwd_multi_kernel(const int32_t* __r
     float4* dst = reinterpret_cast<float4*>(dtable + int64_t(id) * cols);
 #pragma unroll
     for (int i = 0; i < V; ++i) {
+        if (C4 != 32 * V && lane + 32 * i >= C4) continue;
         float4 t = dst[lane + 32 * i];
         t.x += a[i].x; t.y += a[i].y; t.z += a[i].z; t.w += a[i].w;
         dst[lane + 32 * i] = t;
     }
 }
 
-template <int V>
+template <int V, int C4 = 32 * V>
 int embed_sorted_launch(const int32_t* perm, const int32_t* chunks, int n_chunks, const int32_t* multi,
                         int n_multi, const float* dout, float* dtable, float scale, float* scratch,
                         cudaStream_t s) {
     constexpr int R = V >= 8 ? 2 : (V >= 4 ? 4 : 8);
-    MM_CUDA_TRY(mm::launch_pdl(embed_bwd_chunk_kernel<V, R>, dim3((n_chunks + 7) / 8), dim3(256), 0, s, perm,
+    MM_CUDA_TRY(mm::launch_pdl(embed_bwd_chunk_kernel<V, R, C4>, dim3((n_chunks + 7) / 8), dim3(256), 0, s, perm,
                                chunks, n_chunks, dout, dtable, scratch, scale));
     MM_LAUNCH_CHECK("embed_bwd_chunk_kernel");
     if (n_multi > 0) {
-        MM_CUDA_TRY(mm::launch_pdl(embed_bwd_multi_kernel<V, R>, dim3((n_multi + 7) / 8), dim3(256), 0, s,
+        MM_CUDA_TRY(mm::launch_pdl(embed_bwd_multi_kernel<V, R, C4>, dim3((n_multi + 7) / 8), dim3(256), 0, s,
                                    multi, n_multi, (const float*)scratch, dtable));
         MM_LAUNCH_CHECK("embed_bwd_multi_kernel");
     }
@@ -929,12 +939,14 @@ extern "C" int mm_layernorm_fwd(const float* x, const float* gamma, const float*
         MM_CUDA_TRY(mm::launch_pdl(ln_fwd_kernel<512>, dim3(grid), dim3(256), 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
     else if (cols == 1024)
         MM_CUDA_TRY(mm::launch_pdl(ln_fwd_kernel<1024>, dim3(grid), dim3(256), 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
+    else if (cols == 64)
+        MM_CUDA_TRY(mm::launch_pdl(ln_fwd_kernel<64>, dim3(grid), dim3(256), 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
     else if (cols == 128)
         MM_CUDA_TRY(mm::launch_pdl(ln_fwd_kernel<128>, dim3(grid), dim3(256), 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
     else if (cols == 256)
         MM_CUDA_TRY(mm::launch_pdl(ln_fwd_kernel<256>, dim3(grid), dim3(256), 0, s, x, gamma, beta, y, mean, rstd, rows, eps));
     else {
-        mm::set_error("layernorm: cols=%d unsupported (128/256/512/1024)", cols);
+        mm::set_error("layernorm: cols=%d unsupported (64/128/256/512/1024)", cols);
         return mm::kUnsupported;
     }
     MM_LAUNCH_CHECK("ln_fwd_kernel");
@@ -982,12 +994,14 @@ extern "C" int mm_layernorm_bwd(const float* dy, const float* x, const float* ga
         MM_CUDA_TRY(mm::launch_pdl(ln_bwd_kernel<512>, dim3(grid), dim3(256), 0, s, dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows));
     else if (cols == 1024)
         MM_CUDA_TRY(mm::launch_pdl(ln_bwd_kernel<1024>, dim3(grid), dim3(256), 0, s, dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows));
+    else if (cols == 64)
+        MM_CUDA_TRY(mm::launch_pdl(ln_bwd_kernel<64>, dim3(grid), dim3(256), 0, s, dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows));
     else if (cols == 128)
         MM_CUDA_TRY(mm::launch_pdl(ln_bwd_kernel<128>, dim3(grid), dim3(256), 0, s, dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows));
     else if (cols == 256)
         MM_CUDA_TRY(mm::launch_pdl(ln_bwd_kernel<256>, dim3(grid), dim3(256), 0, s, dy, x, gamma, mean, rstd, dx, dx_bf16, dgamma, dbeta, rows));
     else {
-        mm::set_error("layernorm: cols=%d unsupported (128/256/512/1024)", cols);
+        mm::set_error("layernorm: cols=%d unsupported (64/128/256/512/1024)", cols);
         return mm::kUnsupported;
     }
     MM_LAUNCH_CHECK("ln_bwd_kernel");
@@ -1018,14 +1032,15 @@ extern "C" int mm_embed_bwd_sorted(const int32_t* table, int64_t rows, int n_chu
                                    const float* dout, float* dtable, int cols, float scale,
                                    float* scratch, void* stream) {
     MM_CHECK_ARG(table && dout && dtable && (n_multi == 0 || scratch), "NULL argument");
-    MM_CHECK_ARG(cols == 128 || cols == 256 || cols == 512 || cols == 1024,
-                 "cols %d: 128, 256, 512 or 1024", cols);
+    MM_CHECK_ARG(cols == 64 || cols == 128 || cols == 256 || cols == 512 || cols == 1024,
+                 "cols %d: 64, 128, 256, 512 or 1024", cols);
     if (rows == 0 || n_chunks == 0) return 0;
     const int32_t* perm = table;
     const int32_t* chunks = table + rows;
     const int32_t* multi = chunks + int64_t(3) * n_chunks;
     auto s = mm::as_stream(stream);
     switch (cols) {
+        case 64: return embed_sorted_launch<1, 16>(perm, chunks, n_chunks, multi, n_multi, dout, dtable, scale, scratch, s);
         case 128: return embed_sorted_launch<1>(perm, chunks, n_chunks, multi, n_multi, dout, dtable, scale, scratch, s);
         case 256: return embed_sorted_launch<2>(perm, chunks, n_chunks, multi, n_multi, dout, dtable, scale, scratch, s);
         case 512: return embed_sorted_launch<4>(perm, chunks, n_chunks, multi, n_multi, dout, dtable, scale, scratch, s);

@@ -257,8 +257,8 @@ struct Driver {
         a.q = q; a.k = k; a.v = v; a.o = o; a.lse = lse;
         a.cu_q = cu_q; a.cu_k = cu_k;
         a.ldq = ldq; a.ldk = ldkv; a.ldv = ldkv; a.ldo = d;
-        a.n_seq = b.n_seq; a.heads = H; a.head_dim = 64; a.causal = causal;
-        a.max_q = max_q; a.max_k = max_k; a.scale = 0.125f; a.total_q = total_q;
+        a.n_seq = b.n_seq; a.heads = H; a.head_dim = d / H; a.causal = causal;
+        a.max_q = max_q; a.max_k = max_k; a.scale = 1.f / std::sqrt(float(d / H)); a.total_q = total_q;
         a.groups = groups; a.n_groups = ng; a.cap = cap;
         a.total_k = cu_k == cu_q ? total_q : int(b.n_src);
         return a;
@@ -572,8 +572,10 @@ extern "C" int mm_task_fwd_bwd(const mm_task* task, const mm_batch* batch, void*
                                size_t* ws_bytes, float* loss_sum, void* stream, void* dec_done) {
     MM_CHECK_ARG(task && batch && ws_bytes, "NULL argument");
     MM_CHECK_ARG(task->n_enc >= 1 && task->n_dec >= 1 && task->enc && task->dec, "empty task");
-    MM_CHECK_ARG(task->d_model % 64 == 0 && task->heads * 64 == task->d_model,
-                 "head_dim must be 64 (d_model %d, heads %d)", task->d_model, task->heads);
+    MM_CHECK_ARG(task->heads > 0 && task->d_model % task->heads == 0 &&
+                     (task->d_model / task->heads == 64 || task->d_model / task->heads == 32 ||
+                      task->d_model / task->heads == 16),
+                 "head_dim must be 16, 32 or 64 (d_model %d, heads %d)", task->d_model, task->heads);
     int nl = 0;
     for (int i = 0; i < task->n_enc; ++i) nl += task->enc[i].n_layers;
     MM_CHECK_ARG(nl <= 64, "more than 64 encoder layers");

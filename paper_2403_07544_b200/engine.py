@@ -198,8 +198,8 @@ class Engine:
                  rank: int = 0, world: int = 1, device=None, seed: int = 0,
                  adam: AdamConfig = AdamConfig(), store=None, masters=None,
                  exchange: Optional[str] = None, comm=None, grad_wire: Optional[str] = None):
-        if shape.head_dim != 64:
-            raise ValueError("the attention kernel is specialised for head_dim 64")
+        if shape.head_dim not in (16, 32, 64) or shape.d_model % shape.heads:
+            raise ValueError(f"head_dim {shape.d_model}/{shape.heads}: the attention kernels take 16, 32 or 64")
         self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
         self.shape = shape
         self.rank, self.world = rank, world
@@ -315,7 +315,7 @@ class Engine:
             if kw["tc_groups"] is None and kw.get("groups") is not None:
                 kw["tc_groups"] = False  # staged padded table without a twin
         return ops.attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, self.shape.heads, max_q,
-                                  max_k, causal, **kw)
+                                  max_k, causal, head_dim=self.shape.head_dim, **kw)
 
     def _self_block_fwd(self, st, p, x, cu, n_seq, max_len, causal, sv, groups=None):
         d = self.shape.d_model

@@ -238,12 +238,15 @@ def widen_bf16(x, y) -> None:
 
 
 def attention_args(q, k, v, o, lse, cu_q, cu_k, n_seq, heads, max_q, max_k, causal,
-                   d_o=None, dq=None, dk=None, dv=None, groups=None, tc_groups=None) -> AttnArgs:
+                   d_o=None, dq=None, dk=None, dv=None, groups=None, tc_groups=None,
+                   head_dim: int = 64) -> AttnArgs:
     """groups: (device int32 tensor [2*n_groups], n_groups, cap) from
     data.attention_groups (32-row aligned); tc_groups: the unpadded packing
     (align = 1) for the tcgen05 backward.  Both are built here from cu_q /
-    cu_k when omitted; tc_groups=False keeps the backward on `groups`."""
-    hd = 64
+    cu_k when omitted; tc_groups=False keeps the backward on `groups`.
+    head_dim 64 runs the tcgen05 kernels, 16 / 32 (config 1's true shape)
+    the CUDA-core kernels of attn_small.cu."""
+    hd = int(head_dim)
     import numpy as _np
     from .data import attention_groups
     if groups is None:

@@ -250,7 +250,7 @@ def test_gemm_grouped_rejects_mixed_majors(cuda):
 
 def test_layernorm(cuda):
     from paper_2403_07544_b200 import ops
-    for cols in (512, 1024):
+    for cols in (64, 128, 512, 1024):  # 64: config 1's d_model (half-warp rows)
         rows = 1031
         g = torch.Generator(device="cuda").manual_seed(cols)
         x = torch.randn(rows, cols, device=cuda, generator=g) * 3 + 1
@@ -307,7 +307,7 @@ def test_embedding(cuda):
     assert rel_err(dtable.cpu(), ref_d) < 1e-5
 
 
-@pytest.mark.parametrize("rows,d", [(4096, 512), (3000, 1024), (1, 128), (65, 256)])
+@pytest.mark.parametrize("rows,d", [(4096, 512), (3000, 1024), (1, 128), (65, 256), (777, 64)])
 def test_embedding_backward_sorted_deterministic(cuda, rows, d):
     """K8's sorted scatter-add (mm_embed_segments + mm_embed_bwd_sorted) on
     Zipf(1.1) ids: bit-exact against a numpy restatement of its summation
