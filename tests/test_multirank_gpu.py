@@ -30,6 +30,9 @@ FIELDS = ("master", "exp_avg", "exp_avg_sq", "weights")
 
 def _world_case(name):
     shape = configs.SHAPE_CFG1_GPU
+    if name == "config1true_w2":  # config 1 at its own shape (d64, head_dim 16)
+        w = configs.config1()
+        return w.tasks, w.topo, w.shape, 2, w.data
     if name == "config1_w2":
         w = configs.config1(shape)
         return w.tasks, w.topo, shape, 2, w.data
@@ -38,6 +41,7 @@ def _world_case(name):
 
 
 @pytest.mark.parametrize("case,exchange", [("config1_w2", "nccl"), ("config3_w4", "nccl"),
+                                           ("config1true_w2", "nccl"), ("config1true_w2", "partitioned"),
                                            ("config1_w2", "partitioned"),
                                            ("config3_w4", "partitioned")])
 def test_threaded_ranks_match_emulated_cluster(cuda, case, exchange):
@@ -96,7 +100,7 @@ def test_threaded_ranks_match_emulated_cluster(cuda, case, exchange):
                     assert torch.equal(getattr(st, f)[lo:hi], getattr(want, f)[lo:hi]), \
                         (step, r, str(k), f)
     # config 1: rank 1 always runs a->c, so its shared modules never see n = 0
-    assert seen_n == ({1, 2} if case == "config1_w2" else {0, 1, 2}), seen_n
+    assert seen_n == ({1, 2} if case.startswith("config1") else {0, 1, 2}), seen_n
     emu.close()
 
 
