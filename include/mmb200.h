@@ -357,6 +357,8 @@ int mm_embed_segments(const int32_t* ids, int rows, int chunk_rows, int32_t* out
                       int* n_multi);
 
 /* K5: packed varlen multi-head attention (bf16 in/out, fp32 softmax).
+ * head_dim 64: tcgen05 kernels; head_dim 16 / 32 (config 1's d64 / 4 heads):
+ * CUDA-core kernels (attn_small.cu) on the same arguments.
  * Work is split into CTA groups of consecutive sequences: groups[2g] = first
  * sequence, groups[2g+1] = count; every sequence occupies ceil(len/32)*32
  * rows of the group's shared-memory tile and the per-group footprint is at
