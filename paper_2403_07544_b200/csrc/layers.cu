@@ -302,7 +302,9 @@ __global__ void __launch_bounds__(256, MINB) ln_bwd_row_kernel(const float* __re
             const float4 v = red4[(which * 8 + w) * (COLS / 4) + c];
             sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
         }
+#ifndef MM_LN_DIAG_NO_COLSUM  // diagnostics only (timing A/B): drops dgamma / dbeta
         atomicAdd(reinterpret_cast<float4*>(which ? dbeta : dgamma) + c, sum);
+#endif
     }
 }
 
