@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(kWarps * 32) attn_small_fwd_kernel(const mm_at
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int q0 = a.cu_q[s], lq = a.cu_q[s + 1] - q0;
     const int k0 = a.cu_k[s], lk = a.cu_k[s + 1] - k0;
+    MM_DCHECK(q0 >= 0 && lq >= 0 && q0 + lq <= a.total_q && k0 >= 0 && lk >= 0 && k0 + lk <= a.total_k);
     const float sl2 = a.scale * kLog2e;
     for (int i = warp; i < lq; i += kWarps) {
         float q[HD];
@@ -126,7 +127,8 @@ __global__ void __launch_bounds__(kWarps * 32) attn_small_bwd_kernel(const mm_at
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int q0 = a.cu_q[s], lq = a.cu_q[s + 1] - q0;
     const int k0 = a.cu_k[s], lk = a.cu_k[s + 1] - k0;
-    MM_DCHECK(lq <= 256 && lk <= 256);
+    MM_DCHECK(lq <= 256 && lk <= 256 && q0 >= 0 && lq >= 0 && q0 + lq <= a.total_q && k0 >= 0 &&
+              lk >= 0 && k0 + lk <= a.total_k);
     const float sl2 = a.scale * kLog2e;
     const int hl = lane < HD ? lane : 0;
     for (int i = warp; i < lq; i += kWarps) {
