@@ -63,6 +63,15 @@ __device__ __forceinline__ void load_row(const uint16_t* p, float (&r)[HD]) {
     }
 }
 
+// the sequence's rows of one head into shared memory (n rows of HD bf16)
+template <int HD>
+__device__ __forceinline__ void stage_rows(uint16_t* dst, const uint16_t* src, int64_t ld, int n) {
+    for (int t = threadIdx.x; t < n * (HD / 8); t += blockDim.x) {
+        const int r = t / (HD / 8), c = t - r * (HD / 8);
+        reinterpret_cast<uint4*>(dst + r * HD)[c] = reinterpret_cast<const uint4*>(src + int64_t(r) * ld)[c];
+    }
+}
+
 template <int HD>
 __device__ __forceinline__ float dot(const float (&a)[HD], const float (&b)[HD]) {
     float t = 0.f;
@@ -76,12 +85,19 @@ __device__ __forceinline__ float dot(const float (&a)[HD], const float (&b)[HD])
 // chunk's keys in key order
 template <int HD>
 __global__ void __launch_bounds__(kWarps * 32) attn_small_fwd_kernel(const mm_attn_args a) {
+    extern __shared__ uint4 smem_fwd[];  // K then V rows of this (sequence, head)
     pdl_wait_release();
     const int s = blockIdx.x, h = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int q0 = a.cu_q[s], lq = a.cu_q[s + 1] - q0;
     const int k0 = a.cu_k[s], lk = a.cu_k[s + 1] - k0;
     MM_DCHECK(q0 >= 0 && lq >= 0 && q0 + lq <= a.total_q && k0 >= 0 && lk >= 0 && k0 + lk <= a.total_k);
+    MM_DCHECK(lk <= a.max_k);
+    uint16_t* sk = reinterpret_cast<uint16_t*>(smem_fwd);
+    uint16_t* sv = sk + a.max_k * HD;
+    stage_rows<HD>(sk, a.k + int64_t(k0) * a.ldk + h * HD, a.ldk, lk);
+    stage_rows<HD>(sv, a.v + int64_t(k0) * a.ldv + h * HD, a.ldv, lk);
+    __syncthreads();
     const float sl2 = a.scale * kLog2e;
     for (int i = warp; i < lq; i += kWarps) {
         float q[HD];
@@ -93,7 +109,7 @@ __global__ void __launch_bounds__(kWarps * 32) attn_small_fwd_kernel(const mm_at
             float sc = -INFINITY;
             if (j < nk) {
                 float k[HD];
-                load_row<HD>(a.k + int64_t(k0 + j) * a.ldk + h * HD, k);
+                load_row<HD>(sk + j * HD, k);
                 sc = dot<HD>(q, k) * sl2;
             }
             const float mn = fmaxf(m, wmax(sc));  // finite: key c is live
@@ -102,10 +118,10 @@ __global__ void __launch_bounds__(kWarps * 32) attn_small_fwd_kernel(const mm_at
             l = l * corr + wsum(p);
             acc *= corr;
             const int cnt = min(32, nk - c);
-            const uint16_t* vb = a.v + int64_t(k0 + c) * a.ldv + h * HD + (lane < HD ? lane : 0);
+            const uint16_t* vb = sv + c * HD + (lane < HD ? lane : 0);
             for (int u = 0; u < cnt; ++u) {
                 const float pu = __shfl_sync(kFull, p, u);
-                acc = fmaf(pu, bf(vb[int64_t(u) * a.ldv]), acc);
+                acc = fmaf(pu, bf(vb[u * HD]), acc);
             }
             m = mn;
         }
@@ -122,19 +138,29 @@ __global__ void __launch_bounds__(kWarps * 32) attn_small_fwd_kernel(const mm_at
 template <int HD>
 __global__ void __launch_bounds__(kWarps * 32) attn_small_bwd_kernel(const mm_attn_args a) {
     __shared__ float d_s[256], lse_s[256];
+    extern __shared__ uint4 smem_bwd[];  // K, V, Q, dO rows of this (sequence, head)
     pdl_wait_release();
     const int s = blockIdx.x, h = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int q0 = a.cu_q[s], lq = a.cu_q[s + 1] - q0;
     const int k0 = a.cu_k[s], lk = a.cu_k[s + 1] - k0;
     MM_DCHECK(lq <= 256 && lk <= 256 && q0 >= 0 && lq >= 0 && q0 + lq <= a.total_q && k0 >= 0 &&
-              lk >= 0 && k0 + lk <= a.total_k);
+              lk >= 0 && k0 + lk <= a.total_k && lq <= a.max_q && lk <= a.max_k);
+    uint16_t* sk = reinterpret_cast<uint16_t*>(smem_bwd);
+    uint16_t* sv = sk + a.max_k * HD;
+    uint16_t* sq = sv + a.max_k * HD;
+    uint16_t* sg = sq + a.max_q * HD;
+    stage_rows<HD>(sk, a.k + int64_t(k0) * a.ldk + h * HD, a.ldk, lk);
+    stage_rows<HD>(sv, a.v + int64_t(k0) * a.ldv + h * HD, a.ldv, lk);
+    stage_rows<HD>(sq, a.q + int64_t(q0) * a.ldq + h * HD, a.ldq, lq);
+    stage_rows<HD>(sg, a.d_o + int64_t(q0) * a.ldo + h * HD, a.ldo, lq);
+    __syncthreads();
     const float sl2 = a.scale * kLog2e;
     const int hl = lane < HD ? lane : 0;
     for (int i = warp; i < lq; i += kWarps) {
         float q[HD], g[HD];
-        load_row<HD>(a.q + int64_t(q0 + i) * a.ldq + h * HD, q);
-        load_row<HD>(a.d_o + int64_t(q0 + i) * a.ldo + h * HD, g);
+        load_row<HD>(sq + i * HD, q);
+        load_row<HD>(sg + i * HD, g);
         const float lse2 = a.lse[int64_t(h) * a.total_q + q0 + i] * kLog2e;
         const int nk = a.causal ? min(lk, i + 1) : lk;
         float dsum = 0.f;
@@ -142,8 +168,8 @@ __global__ void __launch_bounds__(kWarps * 32) attn_small_bwd_kernel(const mm_at
             const int j = c + lane;
             if (j < nk) {
                 float k[HD], v[HD];
-                load_row<HD>(a.k + int64_t(k0 + j) * a.ldk + h * HD, k);
-                load_row<HD>(a.v + int64_t(k0 + j) * a.ldv + h * HD, v);
+                load_row<HD>(sk + j * HD, k);
+                load_row<HD>(sv + j * HD, v);
                 dsum += exp2f(dot<HD>(q, k) * sl2 - lse2) * dot<HD>(g, v);
             }
         }
@@ -154,14 +180,14 @@ __global__ void __launch_bounds__(kWarps * 32) attn_small_bwd_kernel(const mm_at
             float ds = 0.f;
             if (j < nk) {
                 float k[HD], v[HD];
-                load_row<HD>(a.k + int64_t(k0 + j) * a.ldk + h * HD, k);
-                load_row<HD>(a.v + int64_t(k0 + j) * a.ldv + h * HD, v);
+                load_row<HD>(sk + j * HD, k);
+                load_row<HD>(sv + j * HD, v);
                 const float p = exp2f(dot<HD>(q, k) * sl2 - lse2);
                 ds = p * (dot<HD>(g, v) - D);
             }
             const int cnt = min(32, nk - c);
-            const uint16_t* kb = a.k + int64_t(k0 + c) * a.ldk + h * HD + hl;
-            for (int u = 0; u < cnt; ++u) dq = fmaf(__shfl_sync(kFull, ds, u), bf(kb[int64_t(u) * a.ldk]), dq);
+            const uint16_t* kb = sk + c * HD + hl;
+            for (int u = 0; u < cnt; ++u) dq = fmaf(__shfl_sync(kFull, ds, u), bf(kb[u * HD]), dq);
         }
         if (lane < HD) a.dq[int64_t(q0 + i) * a.ld_dq + h * HD + lane] = to_bf(dq * a.scale);
         if (lane == 0) {
@@ -172,8 +198,8 @@ __global__ void __launch_bounds__(kWarps * 32) attn_small_bwd_kernel(const mm_at
     __syncthreads();
     for (int j = warp; j < lk; j += kWarps) {
         float k[HD], v[HD];
-        load_row<HD>(a.k + int64_t(k0 + j) * a.ldk + h * HD, k);
-        load_row<HD>(a.v + int64_t(k0 + j) * a.ldv + h * HD, v);
+        load_row<HD>(sk + j * HD, k);
+        load_row<HD>(sv + j * HD, v);
         const int i0 = a.causal ? j : 0;  // queries that see key j
         float dv = 0.f, dk = 0.f;
         for (int c = i0; c < lq; c += 32) {
@@ -181,17 +207,17 @@ __global__ void __launch_bounds__(kWarps * 32) attn_small_bwd_kernel(const mm_at
             float p = 0.f, ds = 0.f;
             if (i < lq) {
                 float q[HD], g[HD];
-                load_row<HD>(a.q + int64_t(q0 + i) * a.ldq + h * HD, q);
-                load_row<HD>(a.d_o + int64_t(q0 + i) * a.ldo + h * HD, g);
+                load_row<HD>(sq + i * HD, q);
+                load_row<HD>(sg + i * HD, g);
                 p = exp2f(dot<HD>(q, k) * sl2 - lse_s[i]);
                 ds = p * (dot<HD>(g, v) - d_s[i]);
             }
             const int cnt = min(32, lq - c);
-            const uint16_t* qb = a.q + int64_t(q0 + c) * a.ldq + h * HD + hl;
-            const uint16_t* gb = a.d_o + int64_t(q0 + c) * a.ldo + h * HD + hl;
+            const uint16_t* qb = sq + c * HD + hl;
+            const uint16_t* gb = sg + c * HD + hl;
             for (int u = 0; u < cnt; ++u) {
-                dv = fmaf(__shfl_sync(kFull, p, u), bf(gb[int64_t(u) * a.ldo]), dv);
-                dk = fmaf(__shfl_sync(kFull, ds, u), bf(qb[int64_t(u) * a.ldq]), dk);
+                dv = fmaf(__shfl_sync(kFull, p, u), bf(gb[u * HD]), dv);
+                dk = fmaf(__shfl_sync(kFull, ds, u), bf(qb[u * HD]), dk);
             }
         }
         if (lane < HD) {
@@ -205,11 +231,16 @@ template <int HD>
 int launch(const mm_attn_args* a, cudaStream_t s, bool bwd) {
     if (a->n_seq == 0) return 0;
     const dim3 grid(a->n_seq, a->heads), blk(kWarps * 32);
+    const size_t row = HD * sizeof(uint16_t);
     if (bwd) {
-        MM_CUDA_TRY(mm::launch_pdl(attn_small_bwd_kernel<HD>, grid, blk, 0, s, *a));
+        const size_t smem = (2 * size_t(a->max_k) + 2 * size_t(a->max_q)) * row;  // <= 64 KB
+        MM_CUDA_TRY(cudaFuncSetAttribute(attn_small_bwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+        MM_CUDA_TRY(mm::launch_pdl(attn_small_bwd_kernel<HD>, grid, blk, smem, s, *a));
         MM_LAUNCH_CHECK("attn_small_bwd_kernel");
     } else {
-        MM_CUDA_TRY(mm::launch_pdl(attn_small_fwd_kernel<HD>, grid, blk, 0, s, *a));
+        const size_t smem = 2 * size_t(a->max_k) * row;
+        MM_CUDA_TRY(mm::launch_pdl(attn_small_fwd_kernel<HD>, grid, blk, smem, s, *a));
         MM_LAUNCH_CHECK("attn_small_fwd_kernel");
     }
     return 0;

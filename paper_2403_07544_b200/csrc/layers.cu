@@ -622,6 +622,7 @@ int embed_sorted_launch(const int32_t* perm, const int32_t* chunks, int n_chunks
 // L1/L2-resident): dlogits = (softmax - onehot(label)) * grad_scale in bf16.
 // label < 0 marks padding: zero loss, zero gradient.
 constexpr int kXentThreads = 512;
+constexpr int kXentStreamMinVocab = 4096;  // below: the row-per-CTA kernel
 
 __global__ void __launch_bounds__(kXentThreads) xent_kernel(const uint16_t* logits,
                                                             const int32_t* __restrict__ labels,
@@ -1057,7 +1058,10 @@ extern "C" int mm_xent_fwd_bwd(const uint16_t* logits, const int32_t* labels, ui
     MM_CHECK_ARG(vocab % 8 == 0, "vocab must be a multiple of 8");
     if (rows == 0) return 0;
     static const bool force_rowwise = std::getenv("MM_XENT_ROWWISE") != nullptr;  // diagnostics
-    if (vocab <= kXentSmemVocab && !force_rowwise) {
+    // short rows (config 1's V1000): one CTA per row -- the streamed kernel's
+    // per-row TMA round trip dominates there (365 us for 16K rows x 1000 in
+    // one config-1 step, profiles/r02_launch_summary_c1.txt)
+    if (vocab >= kXentStreamMinVocab && vocab <= kXentSmemVocab && !force_rowwise) {
         const size_t smem = size_t(kXentBufs) * kXentSmemVocab * 2;
         MM_CUDA_TRY(cudaFuncSetAttribute(xent_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));

@@ -358,7 +358,7 @@ def test_embedding_backward_sorted_deterministic(cuda, rows, d):
     assert np.abs(t.cpu().numpy() - ref).max() <= 1e-6 * np.abs(ref).max()
 
 
-@pytest.mark.parametrize("rows,vocab", [(777, 32000), (300, 1000), (150, 40000), (2, 8)])
+@pytest.mark.parametrize("rows,vocab", [(777, 32000), (300, 1000), (150, 40000), (2, 8), (513, 4096)])
 def test_cross_entropy(cuda, rows, vocab):
     """Both kernels: the streamed one-CTA-per-SM kernel (vocab <= 32768) and
     the one-row-per-CTA fallback (larger vocabularies)."""
